@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark of the batched LF-LTS MLMC hot path (BASELINE.json config 1).
+
+One step = the whole fixed-N MLMC estimator of config 1: coupled pairs on
+levels 0..4 (h_l = 1/16..1/256, p_l = 32..2, N_l = 65536, 16384, 4096, 1024,
+256), both solves of every pair, FP64, plus the per-level moment sums and
+(N > 1) one NCCL allreduce of them.  Metric: DOF-updates/s with
+U = n + (p-1)|R| per global step per solve.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Under torchrun every rank evaluates the index range [r N_l / G, (r+1) N_l / G)
+of every level (weak in samples per GPU? no: total work is fixed -> "strong").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+METRIC = "DOF-updates/s (FP64, LTS substeps incl.)"
+UNIT = "DOF-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="fraction of N_l (1.0 = BASELINE config 1)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        exe = shutil.which("nvidia-smi")
+        if not exe:
+            return
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run([exe, "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (the reference compiled from its own sources, else our port)
+
+def ref_sample_counts(threads: int):
+    """Bounded sample of config 1 for the CPU: per level a few samples per
+    thread, sized for ~10-30 s of wall time."""
+    t = max(1, threads)
+    return [4 * t, 2 * t, t, max(1, t // 2), max(1, t // 4)]
+
+
+def run_reference_cpu(defs, threads: int):
+    """Config 1 sample through the unmodified reference library (oracle/_ref),
+    its own run_jobs-style pool of `threads` workers.  Returns dict."""
+    import oracle_py
+    from paper_2106_11117_b200 import configs
+    counts = ref_sample_counts(threads)
+    tmp = tempfile.mkdtemp(prefix="wmc_bench_")
+    specs = []
+    for l, d in enumerate(defs):
+        p = os.path.join(tmp, f"l{l}.mesh")
+        configs.build_mesh(d).dump(p)
+        specs.append((p, d.dt, d.substeps))
+    drv = oracle_py.RefDriver()
+    res = drv.mlmc(specs, counts, threads=threads)
+    shutil.rmtree(tmp, ignore_errors=True)
+    return {"value": res["dof_updates"] / res["seconds"], "seconds": res["seconds"],
+            "dof_updates": res["dof_updates"], "counts": counts, "kind": "reference", "cores": res["threads"]}
+
+
+def run_port_cpu(defs, threads: int):
+    """Fallback when oracle/_ref is absent: our C restatement, `threads` workers."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle_py
+    from paper_2106_11117_b200 import configs
+    oracle_py.build()
+    orc = oracle_py.COracle()
+    counts = ref_sample_counts(threads)
+    from paper_2106_11117_b200 import wavemc
+    meshes = [oracle_py.MeshArrays(*configs.build_mesh(d).arrays()) for d in defs]
+    probs = [oracle_py.problem(d.dt, d.substeps) for d in defs]
+    upd = [wavemc.level_plan(configs.build_mesh(d), configs.level_spec(d))["dof_updates_per_solve"] for d in defs]
+    jobs = [(l, i) for l in range(len(defs)) for i in range(counts[l])]
+
+    def one(job):
+        l, i = job
+        rc, _, _, _, _ = orc.eval_pairs(meshes[l], probs[l], meshes[l - 1] if l else None,
+                                        probs[l - 1] if l else None, 0, l, i, 1)
+        return upd[l] + (upd[l - 1] if l else 0.0)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        total = sum(ex.map(one, jobs))
+    dt = time.perf_counter() - t0
+    return {"value": total / dt, "seconds": dt, "dof_updates": total, "counts": counts, "kind": "port",
+            "cores": threads}
+
+
+def cpu_baseline(defs, threads: int):
+    import oracle_py
+    if os.path.exists(oracle_py.REF_DRIVER):
+        return run_reference_cpu(defs, threads)
+    return run_port_cpu(defs, threads)
+
+
+# ---------------------------------------------------------------------------
+
+def reference_arm(args, world, rank):
+    from paper_2106_11117_b200 import configs
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    defs = configs.config1()
+    try:
+        runs = [cpu_baseline(defs, threads) for _ in range(args.warmup + args.steps)]
+    except Exception as exc:  # the oracle always exists; report loudly
+        print(json.dumps({"impl": "reference", "unavailable": f"reference CPU run failed: {exc}"}))
+        return 0
+    timed = runs[args.warmup:]
+    value = sum(r["dof_updates"] for r in timed) / sum(r["seconds"] for r in timed)
+    r0 = timed[0]
+    sample = (f"config 1 bounded sample N_l={r0['counts']} (of {configs.CONFIG1_COUNTS}) per step, "
+              f"{r0['cores']} threads, {r0['kind']}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(r["seconds"] for r in timed) / len(timed),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (counter-based RNG draws, seed 0)",
+            "config": {"workload": "BASELINE config 1 (MLMC LF-LTS, 5 levels), bounded CPU sample",
+                       "parallelism": f"{r0['cores']} CPU threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": r0["cores"], "kind": r0["kind"],
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def b200_arm(args, world, rank, local):
+    import torch
+
+    from paper_2106_11117_b200 import configs, wavemc
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    defs = configs.config1()
+    counts_total = [max(1, int(round(n * args.scale))) for n in configs.CONFIG1_COUNTS]
+    levels = [configs.build_level(d, device=local) for d in defs]
+    first = [r * 0 for r in counts_total]
+    counts = []
+    for l, n in enumerate(counts_total):
+        a, b = rank * n // world, (rank + 1) * n // world
+        first[l] = a
+        counts.append(b - a)
+    upd = [lv.info["dof_updates_per_solve"] for lv in levels]
+    per_pair = [upd[l] + (upd[l - 1] if l else 0.0) for l in range(len(levels))]
+    total_updates = sum(n * per_pair[l] for l, n in enumerate(counts_total))
+
+    dev = torch.device("cuda", local)
+    d_dq = [torch.empty(max(c, 1), dtype=torch.float64, device=dev) for c in counts]
+    d_qf = [torch.empty(max(c, 1), dtype=torch.float64, device=dev) for c in counts]
+    d_mom = torch.zeros(4 * len(levels), dtype=torch.float64, device=dev)
+    streams = [torch.cuda.ExternalStream(lv.stream, device=dev) for lv in levels]
+    main = torch.cuda.current_stream(dev)
+
+    def step_device():
+        d_mom.zero_()
+        ev0 = torch.cuda.Event()
+        ev0.record(main)
+        for l, lv in enumerate(levels):
+            if counts[l] == 0:
+                continue
+            streams[l].wait_event(ev0)
+            wavemc.eval_pairs_device(lv, levels[l - 1] if l else None, 0, l, first[l], counts[l],
+                                     d_dq[l].data_ptr(), d_qf[l].data_ptr())
+            wavemc.moments_device(lv, d_dq[l].data_ptr(), d_qf[l].data_ptr(), counts[l],
+                                  d_mom.data_ptr() + 8 * 4 * l)
+        for l in range(len(levels)):
+            e = torch.cuda.Event()
+            e.record(streams[l])
+            main.wait_event(e)
+        if dist is not None:
+            dist.all_reduce(d_mom)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+
+    # warm-up, then K timed steps bracketed by barrier + synchronize
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    launches0 = wavemc.launch_count()
+    with ClockSampler(local) as clocks:
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(main)
+        for _ in range(args.steps):
+            step_device()
+        end.record(main)
+        barrier()
+    launches = wavemc.launch_count() - launches0
+    ms = start.elapsed_time(end) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = total_updates / (ms * 1e-3)
+    mom = d_mom.cpu().tolist()
+
+    # e2e: the public host API (per-sample results D2H + host fold in index
+    # order) per step, plus the allreduce of the per-level sums
+    def step_e2e():
+        stats = wavemc.run_mlmc_fixed(levels, counts, 0, first)
+        if dist is not None:
+            t = torch.tensor([[s["sum_dq"], s["sum_dq2"], s["sum_q"], s["sum_q2"], s["n_samples"]] for s in stats],
+                             dtype=torch.float64, device=dev)
+            dist.all_reduce(t)
+            t.cpu()
+        return stats
+
+    step_e2e()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 2))
+    t0.record(main)
+    for _ in range(e2e_steps):
+        stats = step_e2e()
+    t1.record(main)
+    barrier()
+    e2e_ms = t0.elapsed_time(t1) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    d2h = sum(16 * c + 4 * c * (2 if l else 1) for l, c in enumerate(counts))
+
+    # kernel-level profile pass (not timed above): per-kernel device time
+    roofline, kernels = None, None
+    if not args.no_profile:
+        for lv in levels:
+            wavemc.profile_enable(lv, True)
+        step_device()
+        torch.cuda.synchronize(dev)
+        prof = []
+        for lv in levels:
+            prof.append(wavemc.profile_read(lv))
+            wavemc.profile_enable(lv, False)
+        roofline, kernels = roofline_from_profile(levels, counts, prof, ms)
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    if roofline is not None:
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roofline["peak"] = peak
+        roofline["frac"] = roofline["achieved"] / peak
+        roofline["peak_source"] = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback"
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based RNG draws, seed 0)",
+            "config": {"workload": "BASELINE config 1: fixed-N MLMC, LF-LTS, 5 levels h=1/16..1/256, p=32..2",
+                       "N_l": counts_total, "levels": [{"n": lv.info["n"], "n_r": lv.info["n_r"], "p": lv.info["p"],
+                                                        "n_steps": lv.info["n_steps"]} for lv in levels],
+                       "dof_updates_per_step": total_updates, "parallelism": f"samples sharded over {world} GPU(s)",
+                       "l2": "inputs (state 2 x n x batch x 8 B per level) exceed L2 at levels 2-4; no flush"},
+            "e2e": {"value": total_updates / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": launches, "clocks": clocks.summary(),
+            "moments": [{"level": l, "sum_dq": mom[4 * l], "sum_dq2": mom[4 * l + 1], "sum_q": mom[4 * l + 2],
+                         "sum_q2": mom[4 * l + 3]} for l in range(len(levels))],
+            "variance": [s["variance"] for s in stats] if world == 1 else None}
+    if roofline is not None:
+        line["roofline"] = roofline
+        line["kernels"] = kernels
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        try:
+            cb = cpu_baseline(defs, threads)
+            line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
+                                    "sample": f"config 1 bounded sample N_l={cb['counts']}, {cb['seconds']:.1f} s"}
+        except Exception as exc:
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                                    "sample": f"failed: {exc}"}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline_from_profile(levels, counts, prof, step_ms):
+    """Dominant-kernel roofline from the profiled pass.  Sweep kernel
+    algorithmic bytes per launch: 8 B x S x (n reads of z_n + (n - |R|) reads
+    of z_{n-1} + n writes of z_{n+1} or g); substep kernel: 8 B x S x 4 |R|
+    (g, z_n, z_{n-1} in, z_{n+1} out) plus its on-chip FP64 work."""
+    sweep_ms = sum(p["sweep_ms"] for p in prof)
+    sub_ms = sum(p["sub_ms"] for p in prof)
+    sweep_bytes = 0.0
+    sub_bytes = 0.0
+    sub_flops = 0.0
+    sub_updates = 0.0
+    for l, lv in enumerate(levels):
+        for lvl in ([l] + ([l - 1] if l else [])):
+            info = levels[lvl].info
+            n, nr, steps, p = info["n"], info["n_r"], info["n_steps"], info["p"]
+            c = counts[l]
+            sweep_bytes += 8.0 * c * (steps - 1) * (2 * n + (n - nr))
+            sub_bytes += 8.0 * c * (steps - 1) * 4 * nr
+            sub_flops += c * (steps - 1) * (p - 1) * (2.0 * info["ap_nnz"] + 7.0 * nr)
+            sub_updates += c * (steps - 1) * (p - 1) * nr
+    kernels = {"sweep": {"ms": sweep_ms, "launches": sum(p["sweep_launches"] for p in prof),
+                         "share_of_step": sweep_ms / step_ms if step_ms else None,
+                         "achieved_GBps": sweep_bytes / (sweep_ms * 1e-3) / 1e9 if sweep_ms else None},
+               "substep": {"ms": sub_ms, "launches": sum(p["sub_launches"] for p in prof),
+                           "share_of_step": sub_ms / step_ms if step_ms else None,
+                           "fp64_TFLOPs": sub_flops / (sub_ms * 1e-3) / 1e12 if sub_ms else None,
+                           "substep_dof_updates_per_s": sub_updates / (sub_ms * 1e-3) if sub_ms else None,
+                           "hbm_GBps": sub_bytes / (sub_ms * 1e-3) / 1e9 if sub_ms else None}}
+    roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",
+            "traffic": None,
+            "note": ("HBM roofline of the sweep kernel (algorithmic bytes); the substep kernel is on-chip "
+                     "(shared memory / FP64 issue) bound, see kernels.substep")}
+    return roof, kernels
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+    return b200_arm(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,211 @@
+/* wavemc-b200: C ABI of the B200-native batched LF / LF-LTS sample evaluator.
+ *
+ * This is the drop-in boundary for the reference's sample-parallel hot path.
+ * The reference plugs a per-sample solver into its MLMC driver through
+ *
+ *   struct MlmcProblem { grid; max_levels_available; model_cost; draw; solve; }
+ *                                          reference include/wavemc/mlmc.hpp:41-47
+ *
+ * and evaluates job lists (level, index) in run_jobs (src/mlmc.cpp:107-149),
+ * one sample_delta_q (src/mlmc.cpp:21-37) per job.  Here one call evaluates a
+ * contiguous index range of coupled (fine, coarse) pairs on a B200:
+ *
+ *   wmc_level_create   replaces the per-level context build of make_problem /
+ *                      build_state_2d (src/experiments.cpp:132-148, :194-237):
+ *                      mesh -> operator tables, selector P, R = rows(A P),
+ *                      initial data, QoI weights, resident in HBM.
+ *   wmc_eval_pairs     replaces run_jobs' loop over sample_delta_q for one
+ *                      level: draw (RngStream(seed, level, index), src/rng.cpp:14-32)
+ *                      -> solve fine and coarse (assemble + run_wave + QoI,
+ *                      src/experiments.cpp:150-172) -> dQ, Q_fine per index.
+ *   wmc_run_mlmc_fixed / wmc_run_mlmc
+ *                      the fixed-N sweep and the adaptive Giles driver
+ *                      (run_mlmc, src/mlmc.cpp:165-233) over batched pairs,
+ *                      folding results in (level, index) order like
+ *                      src/mlmc.cpp:145-147.
+ *
+ * Conventions:
+ *   - status codes, no exceptions: 0 ok, 2 config error (reference
+ *     ConfigError), 3 numerical error (NumericalError / InstabilityError with
+ *     err->sample and err->step), 4 device/runtime error;
+ *   - host buffers are caller-owned, device memory is handle-owned;
+ *   - calls are synchronous; one host thread per device.
+ * The message of the last failure on the calling thread: wmc_last_error().
+ */
+#ifndef WAVEMC_B200_H
+#define WAVEMC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WMC_OK 0
+#define WMC_CONFIG_ERROR 2
+#define WMC_NUMERICAL_ERROR 3
+#define WMC_DEVICE_ERROR 4
+
+#define WMC_LEAPFROG 0
+#define WMC_LOCAL_TIME_STEPPING 1
+
+typedef struct wmc_mesh wmc_mesh;
+typedef struct wmc_level wmc_level;
+
+/* Unit square, structured right triangles, refined square at h/ratio with
+ * 2:1 balanced transitions (no reference counterpart: SURVEY.md Appendix A
+ * item 4; transition cells follow src/mesh2d.cpp:96-130, fine flags
+ * src/mesh2d.cpp:285-301). */
+typedef struct {
+    int n_coarse;        /* cells per side, h = 1/n_coarse */
+    int ratio;           /* h / h_min, power of two */
+    double fine_lo, fine_hi;  /* refined square [lo, hi]^2 */
+    double snap;         /* snap grid for the square (0 -> coarse grid) */
+    double small_factor; /* small triangle: longest edge < small_factor*sqrt(2)*h */
+} wmc_square_mesh_spec;
+
+int wmc_mesh_build_square(const wmc_square_mesh_spec* spec, wmc_mesh** out);
+/* A mesh from arrays, e.g. a reference TriMesh (include/wavemc/mesh.hpp:48-74). */
+int wmc_mesh_create(int n_vertices, int n_triangles, const double* xy, const int* tri, const unsigned char* fine,
+                    const unsigned char* boundary, double coarse_h, double fine_h, wmc_mesh** out);
+int wmc_mesh_info(const wmc_mesh* mesh, int* n_vertices, int* n_triangles, double* coarse_h, double* fine_h);
+int wmc_mesh_export(const wmc_mesh* mesh, double* xy, int* tri, unsigned char* fine, unsigned char* boundary);
+/* Reference fixture text format (src/mesh_io.cpp:1-9). */
+int wmc_mesh_dump(const wmc_mesh* mesh, const char* path);
+void wmc_mesh_destroy(wmc_mesh* mesh);
+
+typedef struct {
+    int cells_x, cells_y;        /* piecewise-constant coefficient grid on [0,1]^2 */
+    double coef_lo, coef_hi;     /* c_k = next_uniform(lo, hi), row-major cell order */
+    double final_time;           /* T */
+    double dt;                   /* requested coarse step (snapped, integrators.cpp:188-189) */
+    int substeps;                /* p */
+    double nu;                   /* stabilisation, reference default 0.01 */
+    int integrator;              /* WMC_LEAPFROG or WMC_LOCAL_TIME_STEPPING */
+    double ic_x, ic_y, ic_width2;  /* u0 = exp(-((x-ic_x)^2 + (y-ic_y)^2) / ic_width2), v0 = 0 */
+    double qoi_box[4];           /* x0, x1, y0, y1: Q = lumped integral of u(T) over the box */
+    int device;                  /* CUDA device ordinal */
+    int batch;                   /* samples per device batch, 0 = automatic */
+} wmc_level_desc;
+
+void wmc_level_desc_default(wmc_level_desc* desc);
+
+typedef struct {
+    int n;                    /* interior DOFs */
+    int n_r;                  /* |R|, rows of A P with a nonzero */
+    int n_p;                  /* |P| */
+    int p;                    /* substeps */
+    long n_steps;
+    double dt;
+    long nnz;                 /* stored operator entries (exact zeros dropped) */
+    long ap_nnz;              /* A P entries on R */
+    long n_recipes;
+    int batch;                /* samples per device batch */
+    double dof_updates_per_solve;  /* n + (n_steps-1)(n + (p-1)|R|) for LTS, n_steps*n for LF */
+} wmc_level_info;
+
+int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);
+/* Host-only: build the level tables and report their sizes, no device work. */
+int wmc_level_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level_info* info);
+int wmc_level_get_info(const wmc_level* level, wmc_level_info* info);
+void wmc_level_destroy(wmc_level* level);
+
+typedef struct {
+    long matvec_full, matvec_fine, matvec_coarse;  /* reference CostRecord, mlmc.hpp:25-32 */
+    long weighted_work;
+    double dof_updates;
+} wmc_cost;
+
+typedef struct {
+    long sample;  /* global index of the first failing sample, -1 if none */
+    long step;    /* reference InstabilityError::step */
+    int level;
+} wmc_error;
+
+/* Coupled pairs for indices first .. first+count-1 of MLMC level `level`:
+ * c drawn once from RngStream(seed, level, index) and shared by the fine
+ * solve (on `fine`) and the coarse solve (on `coarse`; NULL on level 0).
+ * dq[i] = Q_fine - Q_coarse (Q_fine on level 0), q_fine[i] = Q_fine.
+ * cost and err may be NULL. */
+int wmc_eval_pairs(wmc_level* fine, wmc_level* coarse, uint64_t seed, uint32_t level, uint64_t first, uint64_t count,
+                   double* dq, double* q_fine, wmc_cost* cost, wmc_error* err);
+
+/* Same work with the per-sample results left in device memory (d_dq, d_q_fine:
+ * device pointers, or NULL to keep them in the handle) and no host
+ * synchronisation: the device-resident leg used for kernel-level timing. */
+int wmc_eval_pairs_device(wmc_level* fine, wmc_level* coarse, uint64_t seed, uint32_t level, uint64_t first,
+                          uint64_t count, double* d_dq, double* d_q_fine);
+
+/* The handle's CUDA stream (cudaStream_t) for event timing; all work of a
+ * level pair is issued on the fine level's stream. */
+void* wmc_level_stream(wmc_level* level);
+int wmc_synchronize(wmc_level* level, wmc_error* err);
+
+/* Per-sample coefficients exactly as the device draws them (RNG parity). */
+int wmc_draw_cells(uint64_t seed, uint32_t level, uint64_t first, uint64_t count, int n_cells, double lo, double hi,
+                   int device, double* out);
+
+typedef struct {
+    int level;
+    long n_samples;
+    double sum_dq, sum_dq2, sum_q, sum_q2;  /* LevelAccumulator, mlmc.hpp:53-66 */
+    double variance;     /* estimate_variance, mlmc.cpp:61-66 */
+    double mc_variance;  /* estimate_mc_variance, mlmc.cpp:68-73 */
+    double mean_dq;
+    double model_cost;
+    wmc_cost cost;
+} wmc_level_stats;
+
+/* Fixed sample counts on levels 0..n_levels-1 (BASELINE config 1): indices
+ * first[l] .. first[l]+counts[l]-1 of level l (first may be NULL = 0), i.e.
+ * one rank's shard; stats hold the shard's LevelAccumulator sums. */
+int wmc_run_mlmc_fixed(wmc_level** levels, int n_levels, const long* first, const long* counts, uint64_t seed,
+                       wmc_level_stats* stats, wmc_error* err);
+
+typedef struct {
+    double eps;             /* root-MSE target */
+    double alpha;           /* bias decay exponent */
+    int initial_samples;    /* 16 */
+    int initial_levels;     /* 2 */
+    int max_level;
+    uint64_t master_seed;
+    int bias_window;        /* 1 */
+} wmc_mlmc_config;
+
+void wmc_mlmc_config_default(wmc_mlmc_config* cfg);
+
+typedef struct {
+    double estimate;
+    int converged;
+    int levels_used;
+    double total_variance;
+    double bias;
+    double total_model_cost;
+    double rmse;            /* sqrt(total_variance + bias) */
+} wmc_mlmc_result;
+
+/* Adaptive Giles driver (reference run_mlmc, src/mlmc.cpp:165-233) with
+ * model_cost[l] per level; stats must hold n_levels entries. */
+int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
+                 wmc_mlmc_result* result, wmc_level_stats* stats, wmc_error* err);
+
+/* Device-side per-level fold: d_out[0..3] += {sum dq, sum dq^2, sum q, sum q^2}
+ * over count device values, one fixed-order block (deterministic). */
+int wmc_moments_device(wmc_level* level, const double* d_dq, const double* d_q, uint64_t count, double* d_out);
+
+/* Kernel-level timing: with profiling on, every sweep and substep launch of
+ * the level is bracketed by CUDA events on its stream; read returns the summed
+ * device time and launch counts and resets. */
+int wmc_profile_enable(wmc_level* level, int on);
+int wmc_profile_read(wmc_level* level, double* sweep_ms, long* sweep_launches, double* sub_ms, long* sub_launches);
+
+/* Number of kernels this library has launched in the process. */
+long wmc_launch_count(void);
+
+const char* wmc_last_error(void);
+int wmc_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

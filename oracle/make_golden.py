@@ -1,0 +1,103 @@
+"""Generate tests/golden/*.json from the UNMODIFIED reference library
+(oracle/_ref/wavemc_ref_driver) -- run in the build container, where
+/root/reference exists:  python oracle/make_golden.py
+
+The meshes come from the shared problem definition (the product's host mesh
+builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
+read back by the reference's load_trimesh, so geometry is never a parity
+variable.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+from oracle_py import RefDriver, build  # noqa: E402
+
+from paper_2106_11117_b200 import configs  # noqa: E402
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def dump(name, obj):
+    os.makedirs(GOLDEN, exist_ok=True)
+    with open(os.path.join(GOLDEN, name), "w") as f:
+        json.dump(obj, f, indent=1)
+        f.write("\n")
+
+
+def main():
+    build()
+    ref = RefDriver()
+    tmp = tempfile.mkdtemp(prefix="wmc_golden_")
+
+    # RNG words and uniform draws (rng.hpp:14-19, rng.cpp:14-32)
+    streams = [(0, 0, 0), (0, 1, 7), (12345, 3, 987654321), (2**63 + 5, 4, 2**40 + 3)]
+    dump("rng.json", {
+        "words": [{"seed": s, "level": l, "index": i, "words": [hex(w) for w in ref.rng(s, l, i, 6)]}
+                  for s, l, i in streams],
+        "uniform": [{"seed": s, "level": l, "index": i, "lo": 0.5, "hi": 1.5,
+                     "values": ref.rng(s, l, i, 16, uniform=True)} for s, l, i in streams],
+    })
+
+    # Chebyshev constants (integrators.cpp:34-66)
+    cases = [(1, 0.0), (2, 0.0), (2, 0.01), (4, 0.01), (8, 0.01), (16, 0.01), (32, 0.01), (32, 0.0), (5, 0.5)]
+    dump("chebyshev.json", [{"p": p, "nu": nu, **dict(zip(["delta", "omega", "beta_int", "beta_half"],
+                                                            ref.consts(p, nu)))} for p, nu in cases])
+
+    # meshes: reference check_mesh report (mesh2d.cpp:415-452)
+    defs = {"config0": configs.config0()}
+    for l, d in enumerate(configs.config1()):
+        defs[f"config1_l{l}"] = d
+    paths = {}
+    meshes = {}
+    for name, d in defs.items():
+        m = configs.build_mesh(d)
+        p = os.path.join(tmp, name + ".mesh")
+        m.dump(p)
+        paths[name] = p
+        meshes[name] = {"n_coarse": d.n_coarse, "ratio": d.ratio, **ref.meshcheck(p)}
+    dump("meshes.json", meshes)
+
+    # config 0 level data: z0, lumped mass, QoI weights (interior vertex order)
+    d0 = configs.config0()
+    vid, z0, mass, w = ref.level(paths["config0"], d0.dt, d0.substeps)
+    dump("config0_level.json", {"interior_vertex": vid.tolist(), "z0": z0.tolist(), "mass": mass.tolist(),
+                                "qoi_w": w.tolist()})
+
+    # config 0 per-sample QoI, LF-LTS and global leap-frog
+    hdr, q = ref.solve(paths["config0"], d0.dt, d0.substeps, "lts", 0, 0, 32)
+    lf = configs.config0_leapfrog()
+    hdr_lf, q_lf = ref.solve(paths["config0"], lf.dt, 1, "lf", 0, 0, 8)
+    # nu = 0 and a non-zero first index / stream level
+    hdr_nu0, q_nu0 = ref.solve(paths["config0"], d0.dt, d0.substeps, "lts", 2, 1000, 8, nu=0.0)
+    dump("config0_samples.json", {
+        "lts": {"dt": d0.dt, "p": d0.substeps, "nu": 0.01, "stream_level": 0, "first": 0, "header": hdr,
+                "q": q.tolist()},
+        "lf": {"dt": lf.dt, "p": 1, "stream_level": 0, "first": 0, "header": hdr_lf, "q": q_lf.tolist()},
+        "lts_nu0": {"dt": d0.dt, "p": d0.substeps, "nu": 0.0, "stream_level": 2, "first": 1000, "header": hdr_nu0,
+                    "q": q_nu0.tolist()},
+    })
+
+    # config 0 MLMC moments over 256 samples (single level)
+    mo = ref.mlmc([(paths["config0"], d0.dt, d0.substeps)], [256], per_sample=True)
+    dump("config0_moments.json", mo)
+
+    # config 1 coupled pairs on every level, per-sample dQ and Q_fine
+    c1 = configs.config1()
+    specs = [(paths[f"config1_l{l}"], d.dt, d.substeps) for l, d in enumerate(c1)]
+    pairs = ref.mlmc(specs, [6, 6, 4, 3, 2], per_sample=True)
+    dump("config1_pairs.json", pairs)
+    print("golden fixtures written to", GOLDEN)
+
+
+if __name__ == "__main__":
+    main()

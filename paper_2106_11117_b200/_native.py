@@ -1,0 +1,152 @@
+"""ctypes binding of the C ABI in include/wavemc_b200.h.
+
+The product path has no fallback: if libwavemc_b200.so is missing or fails to
+load, every call raises.  Build it with ``python -c 'import __graft_entry__ as
+g; g.build()'`` (or ``make -C paper_2106_11117_b200/csrc``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwavemc_b200.so")
+
+WMC_OK = 0
+WMC_CONFIG_ERROR = 2
+WMC_NUMERICAL_ERROR = 3
+WMC_DEVICE_ERROR = 4
+WMC_LEAPFROG = 0
+WMC_LOCAL_TIME_STEPPING = 1
+
+
+class SquareMeshSpec(C.Structure):
+    _fields_ = [("n_coarse", C.c_int), ("ratio", C.c_int), ("fine_lo", C.c_double), ("fine_hi", C.c_double),
+                ("snap", C.c_double), ("small_factor", C.c_double)]
+
+
+class LevelDesc(C.Structure):
+    _fields_ = [("cells_x", C.c_int), ("cells_y", C.c_int), ("coef_lo", C.c_double), ("coef_hi", C.c_double),
+                ("final_time", C.c_double), ("dt", C.c_double), ("substeps", C.c_int), ("nu", C.c_double),
+                ("integrator", C.c_int), ("ic_x", C.c_double), ("ic_y", C.c_double), ("ic_width2", C.c_double),
+                ("qoi_box", C.c_double * 4), ("device", C.c_int), ("batch", C.c_int)]
+
+
+class LevelInfo(C.Structure):
+    _fields_ = [("n", C.c_int), ("n_r", C.c_int), ("n_p", C.c_int), ("p", C.c_int), ("n_steps", C.c_long),
+                ("dt", C.c_double), ("nnz", C.c_long), ("ap_nnz", C.c_long), ("n_recipes", C.c_long),
+                ("batch", C.c_int), ("dof_updates_per_solve", C.c_double)]
+
+
+class Cost(C.Structure):
+    _fields_ = [("matvec_full", C.c_long), ("matvec_fine", C.c_long), ("matvec_coarse", C.c_long),
+                ("weighted_work", C.c_long), ("dof_updates", C.c_double)]
+
+
+class Error(C.Structure):
+    _fields_ = [("sample", C.c_long), ("step", C.c_long), ("level", C.c_int)]
+
+
+class LevelStats(C.Structure):
+    _fields_ = [("level", C.c_int), ("n_samples", C.c_long), ("sum_dq", C.c_double), ("sum_dq2", C.c_double),
+                ("sum_q", C.c_double), ("sum_q2", C.c_double), ("variance", C.c_double),
+                ("mc_variance", C.c_double), ("mean_dq", C.c_double), ("model_cost", C.c_double), ("cost", Cost)]
+
+
+class MlmcConfig(C.Structure):
+    _fields_ = [("eps", C.c_double), ("alpha", C.c_double), ("initial_samples", C.c_int),
+                ("initial_levels", C.c_int), ("max_level", C.c_int), ("master_seed", C.c_uint64),
+                ("bias_window", C.c_int)]
+
+
+class MlmcResult(C.Structure):
+    _fields_ = [("estimate", C.c_double), ("converged", C.c_int), ("levels_used", C.c_int),
+                ("total_variance", C.c_double), ("bias", C.c_double), ("total_model_cost", C.c_double),
+                ("rmse", C.c_double)]
+
+
+P = C.POINTER
+_VP = C.c_void_p
+_DP = P(C.c_double)
+
+# (name, restype, argtypes) for every symbol include/wavemc_b200.h declares
+SIGNATURES = [
+    ("wmc_mesh_build_square", C.c_int, [P(SquareMeshSpec), P(_VP)]),
+    ("wmc_mesh_create", C.c_int, [C.c_int, C.c_int, _DP, P(C.c_int), P(C.c_ubyte), P(C.c_ubyte), C.c_double,
+                                  C.c_double, P(_VP)]),
+    ("wmc_mesh_info", C.c_int, [_VP, P(C.c_int), P(C.c_int), _DP, _DP]),
+    ("wmc_mesh_export", C.c_int, [_VP, _DP, P(C.c_int), P(C.c_ubyte), P(C.c_ubyte)]),
+    ("wmc_mesh_dump", C.c_int, [_VP, C.c_char_p]),
+    ("wmc_mesh_destroy", None, [_VP]),
+    ("wmc_level_desc_default", None, [P(LevelDesc)]),
+    ("wmc_level_create", C.c_int, [_VP, P(LevelDesc), P(_VP)]),
+    ("wmc_level_plan", C.c_int, [_VP, P(LevelDesc), P(LevelInfo)]),
+    ("wmc_level_get_info", C.c_int, [_VP, P(LevelInfo)]),
+    ("wmc_level_destroy", None, [_VP]),
+    ("wmc_eval_pairs", C.c_int, [_VP, _VP, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, _DP, _DP, P(Cost),
+                                 P(Error)]),
+    ("wmc_eval_pairs_device", C.c_int, [_VP, _VP, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, _VP, _VP]),
+    ("wmc_level_stream", _VP, [_VP]),
+    ("wmc_synchronize", C.c_int, [_VP, P(Error)]),
+    ("wmc_draw_cells", C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, C.c_double, C.c_double,
+                                 C.c_int, _DP]),
+    ("wmc_run_mlmc_fixed", C.c_int, [P(_VP), C.c_int, P(C.c_long), P(C.c_long), C.c_uint64, P(LevelStats),
+                                     P(Error)]),
+    ("wmc_mlmc_config_default", None, [P(MlmcConfig)]),
+    ("wmc_run_mlmc", C.c_int, [P(_VP), C.c_int, _DP, P(MlmcConfig), P(MlmcResult), P(LevelStats), P(Error)]),
+    ("wmc_moments_device", C.c_int, [_VP, _VP, _VP, C.c_uint64, _VP]),
+    ("wmc_profile_enable", C.c_int, [_VP, C.c_int]),
+    ("wmc_profile_read", C.c_int, [_VP, _DP, P(C.c_long), _DP, P(C.c_long)]),
+    ("wmc_launch_count", C.c_long, []),
+    ("wmc_last_error", C.c_char_p, []),
+    ("wmc_device_count", C.c_int, []),
+]
+
+_lib = None
+
+
+def lib():
+    """Load libwavemc_b200.so (raises if it is missing: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"wavemc-b200: native library {LIB_PATH} is not built "
+                               "(run __graft_entry__.build()); there is no CPU fallback")
+        handle = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+class WavemcError(RuntimeError):
+    def __init__(self, code: int, message: str, sample: int = -1, step: int = 0, level: int = -1):
+        super().__init__(message)
+        self.code = code
+        self.sample = sample
+        self.step = step
+        self.level = level
+
+
+class ConfigError(WavemcError):
+    pass
+
+
+class NumericalError(WavemcError):
+    pass
+
+
+class DeviceError(WavemcError):
+    pass
+
+
+def check(code: int, err: Error | None = None) -> None:
+    if code == WMC_OK:
+        return
+    msg = (lib().wmc_last_error() or b"").decode()
+    cls = {WMC_CONFIG_ERROR: ConfigError, WMC_NUMERICAL_ERROR: NumericalError}.get(code, DeviceError)
+    if err is not None:
+        raise cls(code, msg, err.sample, err.step, err.level)
+    raise cls(code, msg)

@@ -1,0 +1,78 @@
+"""BASELINE.json configurations as mesh + level specifications.
+
+The choices the BASELINE text leaves open are fixed here once and shared by
+the GPU path and the oracles:
+  * the refined square [0.45, 0.55]^2 is snapped outward to the level-0 grid
+    (h = 1/16): [0.4375, 0.5625]^2 on every level;
+  * c is U[0.5, 1.5) per cell of a 4x4 grid, drawn in row-major cell order
+    k = iy*4 + ix from RngStream(seed=0, level, index) ("Philox" in the
+    BASELINE text names the counter-based role; the reference generator is
+    SplitMix64-keyed, rng.cpp:14-32);
+  * fixed dt = 0.2 h_l for LF-LTS and 0.2 h_min for global leap-frog;
+  * config 1 uses L = 4, i.e. five levels h_l = 1/16 .. 1/256 with
+    p_l = 32, 16, 8, 4, 2, matching the five N_l values;
+  * QoI: lumped quadrature of u(T) over the triangles whose centroid lies in
+    [0.7, 0.9] x [0.4, 0.6].
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from ._native import WMC_LEAPFROG, WMC_LOCAL_TIME_STEPPING
+
+FINE_LO, FINE_HI, SNAP = 0.45, 0.55, 1.0 / 16
+H_MIN = 1.0 / 512
+
+CONFIG1_COUNTS = [65536, 16384, 4096, 1024, 256]
+
+
+@dataclass(frozen=True)
+class LevelDef:
+    n_coarse: int       # 1/h
+    ratio: int          # h / h_min of this mesh (= p for LTS)
+    dt: float
+    substeps: int
+    integrator: int
+    final_time: float = 1.0
+
+    @property
+    def h(self) -> float:
+        return 1.0 / self.n_coarse
+
+
+def config0() -> LevelDef:
+    """Single-level MC: h = 1/32 refined by 4, p = 4, dt = 0.2 h, T = 1."""
+    return LevelDef(32, 4, 0.2 / 32, 4, WMC_LOCAL_TIME_STEPPING)
+
+
+def config0_leapfrog() -> LevelDef:
+    return LevelDef(32, 4, 0.2 / 128, 1, WMC_LEAPFROG)
+
+
+def config1(kind: str = "lts", n_levels: int = 5) -> list[LevelDef]:
+    """MLMC, h_l = 1/16 * 2^-l, fixed h_min = 1/512, p_l = h_l / h_min."""
+    out = []
+    for l in range(n_levels):
+        n_coarse = 16 << l
+        ratio = 512 // n_coarse
+        if kind == "lts":
+            out.append(LevelDef(n_coarse, ratio, 0.2 / n_coarse, ratio, WMC_LOCAL_TIME_STEPPING))
+        else:
+            out.append(LevelDef(n_coarse, ratio, 0.2 * H_MIN, 1, WMC_LEAPFROG))
+    return out
+
+
+def build_mesh(d: LevelDef):
+    from .wavemc import Mesh
+    return Mesh.build_square(d.n_coarse, d.ratio, FINE_LO, FINE_HI, SNAP)
+
+
+def level_spec(d: LevelDef, device: int = 0, batch: int = 0):
+    from .wavemc import LevelSpec
+    return LevelSpec(dt=d.dt, substeps=d.substeps, integrator=d.integrator, final_time=d.final_time, device=device,
+                     batch=batch)
+
+
+def build_level(d: LevelDef, device: int = 0, batch: int = 0):
+    from .wavemc import Level
+    return Level(build_mesh(d), level_spec(d, device, batch))

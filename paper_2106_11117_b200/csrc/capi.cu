@@ -1,0 +1,833 @@
+// C ABI of the batched evaluator (include/wavemc_b200.h): per-level device
+// contexts, the pair evaluator that replaces the reference's run_jobs loop
+// over sample_delta_q, and the host MLMC drivers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/wavemc_b200.h"
+#include "host/level.hpp"
+#include "host/mesh.hpp"
+#include "kernels.cuh"
+
+struct wmc_mesh {
+    wmc::TriMesh mesh;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<long> g_launches{0};  // kernels launched by this library (all devices)
+
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct DeviceError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return WMC_OK;
+    } catch (const ConfigError& e) {
+        g_last_error = e.what();
+        return WMC_CONFIG_ERROR;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return WMC_CONFIG_ERROR;
+    } catch (const NumericalError& e) {
+        g_last_error = e.what();
+        return WMC_NUMERICAL_ERROR;
+    } catch (const DeviceError& e) {
+        g_last_error = e.what();
+        return WMC_DEVICE_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return WMC_DEVICE_ERROR;
+    }
+}
+
+template <class T>
+T* upload(const std::vector<T>& v) {
+    T* d = nullptr;
+    const std::size_t bytes = sizeof(T) * std::max<std::size_t>(v.size(), 1);
+    check(cudaMalloc(&d, bytes), "cudaMalloc");
+    if (!v.empty()) check(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "upload");
+    return d;
+}
+
+}  // namespace
+
+struct wmc_level {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    wmc::LevelSpec spec;
+    wmc::LevelTables tab;
+    int batch = 0;  // capacity in samples (multiple of 64)
+
+    // sweep operator
+    int* d_row_ptr = nullptr;
+    int* d_ent = nullptr;
+    double* d_a0 = nullptr;
+    double* d_z0 = nullptr;
+    // substep operator (SELL A P on R) and recipes
+    std::uint32_t* d_sub_ent = nullptr;
+    int* d_slice_off = nullptr;
+    int n_sub_ent = 0;
+    int* d_rc_ptr = nullptr;
+    int* d_rc_cell = nullptr;
+    double* d_rc_a0 = nullptr;
+    int n_wid = 0;
+    double* d_beta = nullptr;
+    double* d_cm = nullptr;
+    int sub_smem = 0;
+    int sub_grid = 0;
+    // QoI
+    int* d_qdof = nullptr;
+    double* d_qw = nullptr;
+    double* d_qsm = nullptr;
+    // batch state
+    double* d_za = nullptr;
+    double* d_zb = nullptr;
+    double* d_g = nullptr;
+    double* d_cells = nullptr;
+    int* d_fail = nullptr;
+    double* d_q = nullptr;
+    double* d_dq = nullptr;
+    // optional per-kernel event timing (profiling pass only)
+    bool profile = false;
+    std::vector<cudaEvent_t> ev_sweep, ev_sub;  // start/stop pairs
+
+    ~wmc_level() {
+        cudaSetDevice(device);
+        for (void* p : {(void*)d_row_ptr, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
+                        (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
+                        (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_za, (void*)d_zb,
+                        (void*)d_g, (void*)d_cells, (void*)d_fail, (void*)d_q, (void*)d_dq})
+            if (p) cudaFree(p);
+        for (auto e : ev_sweep) cudaEventDestroy(e);
+        for (auto e : ev_sub) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+int round64(long v) { return static_cast<int>((v + 63) / 64 * 64); }
+
+void build_device_level(wmc_level& L) {
+    const wmc::LevelTables& t = L.tab;
+    check(cudaSetDevice(L.device), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+
+    if (t.n >= (1 << 24)) throw ConfigError("level: more than 2^24 DOFs");
+    std::vector<int> ent(t.col.size());
+    for (std::size_t k = 0; k < ent.size(); ++k) ent[k] = t.col[k] | (t.cell[k] << 24);
+    L.d_row_ptr = upload(t.row_ptr);
+    L.d_ent = upload(ent);
+    L.d_a0 = upload(t.a0);
+    L.d_z0 = upload(t.z0);
+
+    // SELL-32 of A P on R
+    const bool lts = t.kind == wmc::Integrator::LocalTimeStepping && t.n_r > 0;
+    L.n_wid = static_cast<int>(t.rc_ptr.size()) - 1;
+    if (lts) {
+        if (t.n_r > wmc::kSubThreads * wmc::kSubMaxRpt || t.n_r >= 65536)
+            throw ConfigError("level: |R| = " + std::to_string(t.n_r) + " exceeds the on-chip substep kernel (" +
+                              std::to_string(wmc::kSubThreads * wmc::kSubMaxRpt) + ")");
+        if (L.n_wid >= 65535) throw ConfigError("level: too many weight recipes");
+        const int n_slices = (t.n_r + 31) / 32;
+        std::vector<int> soff(n_slices + 1, 0);
+        std::vector<std::uint32_t> sent;
+        const std::uint32_t pad = static_cast<std::uint32_t>(L.n_wid) << 16;
+        for (int sl = 0; sl < n_slices; ++sl) {
+            int width = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int r = sl * 32 + l;
+                if (r < t.n_r) width = std::max(width, t.ap_row_ptr[r + 1] - t.ap_row_ptr[r]);
+            }
+            const std::size_t base = sent.size();
+            sent.resize(base + static_cast<std::size_t>(width) * 32, pad);
+            for (int l = 0; l < 32; ++l) {
+                const int r = sl * 32 + l;
+                if (r >= t.n_r) continue;
+                for (int e = t.ap_row_ptr[r]; e < t.ap_row_ptr[r + 1]; ++e) {
+                    const int slot = e - t.ap_row_ptr[r];
+                    sent[base + slot * 32 + l] =
+                        static_cast<std::uint32_t>(t.ap_col[e]) | (static_cast<std::uint32_t>(t.ap_wid[e]) << 16);
+                }
+            }
+            soff[sl + 1] = static_cast<int>(sent.size());
+        }
+        L.n_sub_ent = static_cast<int>(sent.size());
+        L.d_sub_ent = upload(sent);
+        L.d_slice_off = upload(soff);
+        L.d_rc_ptr = upload(t.rc_ptr);
+        L.d_rc_cell = upload(t.rc_cell);
+        L.d_rc_a0 = upload(t.rc_a0);
+        L.d_beta = upload(t.beta);
+        L.d_cm = upload(t.cm);
+        wmc::SubArgs probe{};
+        probe.n_r = t.n_r;
+        probe.p = t.p;
+        probe.n_wid = L.n_wid;
+        probe.n_cells = t.n_cells;
+        probe.n_ent = L.n_sub_ent;
+        L.sub_smem = wmc::substep_smem_bytes(probe);
+        L.sub_grid = wmc::substep_max_grid(L.device, L.sub_smem);
+        if (L.sub_grid <= 0)
+            throw ConfigError("level: substep working set " + std::to_string(L.sub_smem) +
+                              " B exceeds shared memory");
+    }
+    L.d_qdof = upload(t.qoi_dof);
+    L.d_qw = upload(t.qoi_w);
+    L.d_qsm = upload(t.sqrt_mass_qoi);
+
+    const std::size_t S = static_cast<std::size_t>(L.batch);
+    auto alloc = [&](auto** p, std::size_t elems) {
+        check(cudaMalloc(p, sizeof(**p) * std::max<std::size_t>(elems, 1)), "cudaMalloc batch");
+    };
+    alloc(&L.d_za, S * t.n);
+    alloc(&L.d_zb, S * t.n);
+    alloc(&L.d_g, S * std::max(t.n_r, 1));
+    alloc(&L.d_cells, S * t.n_cells);
+    alloc(&L.d_fail, S);
+    alloc(&L.d_q, S);
+    alloc(&L.d_dq, S);
+}
+
+// one batch of solves on level L with coefficients `cells` (stride S), result
+// Q per sample in L.d_q; asynchronous on `stream`
+cudaEvent_t mark(wmc_level& L, std::vector<cudaEvent_t>& v, cudaStream_t st) {
+    cudaEvent_t e;
+    check(cudaEventCreate(&e), "cudaEventCreate");
+    check(cudaEventRecord(e, st), "cudaEventRecord");
+    v.push_back(e);
+    (void)L;
+    return e;
+}
+
+void solve_batch(wmc_level& L, const double* cells, int S, int count, cudaStream_t stream) {
+    const wmc::LevelTables& t = L.tab;
+    const bool lts = t.kind == wmc::Integrator::LocalTimeStepping && t.n_r > 0;
+    wmc::launch_fill_int(L.d_fail, INT_MAX, S, stream);
+
+    wmc::SweepArgs sw{};
+    sw.n = t.n;
+    sw.S = S;
+    sw.count = count;
+    sw.row_ptr = L.d_row_ptr;
+    sw.ent = L.d_ent;
+    sw.a0 = L.d_a0;
+    sw.cells = cells;
+    sw.z0 = L.d_z0;
+    sw.zp = L.d_zb;
+    sw.zc_out = L.d_za;
+    sw.factor = t.init_factor;
+    sw.step = 1;
+    sw.fail = L.d_fail;
+    wmc::launch_sweep_init(sw, stream);
+    g_launches += 2;
+
+    double* cur = L.d_za;
+    double* prev = L.d_zb;
+    wmc::SubArgs sb{};
+    if (lts) {
+        sb.n_r = t.n_r;
+        sb.S = S;
+        sb.count = count;
+        sb.p = t.p;
+        sb.n_wid = L.n_wid;
+        sb.n_cells = t.n_cells;
+        sb.n_ent = L.n_sub_ent;
+        sb.ent = L.d_sub_ent;
+        sb.slice_off = L.d_slice_off;
+        sb.rc_ptr = L.d_rc_ptr;
+        sb.rc_cell = L.d_rc_cell;
+        sb.rc_a0 = L.d_rc_a0;
+        sb.cells = cells;
+        sb.g = L.d_g;
+        sb.beta = L.d_beta;
+        sb.cm = L.d_cm;
+        sb.c0 = t.c0;
+        sb.fail = L.d_fail;
+    }
+    const int sub_grid = std::min(L.sub_grid, count);
+    for (long s = 1; s < t.n_steps; ++s) {
+        sw.zc = cur;
+        sw.zp = prev;
+        sw.zc_out = nullptr;
+        sw.g = L.d_g;
+        sw.split = lts ? t.n_r : 0;
+        sw.factor = t.coarse_factor;
+        sw.step = static_cast<int>(s + 1);
+        if (L.profile) mark(L, L.ev_sweep, stream);
+        wmc::launch_sweep_step(sw, stream);
+        if (L.profile) mark(L, L.ev_sweep, stream);
+        ++g_launches;
+        if (lts) {
+            sb.zc = cur;
+            sb.zp = prev;
+            sb.step = static_cast<int>(s + 1);
+            if (L.profile) mark(L, L.ev_sub, stream);
+            const int e = wmc::launch_substeps(sb, sub_grid, stream);
+            if (e != 0) check(static_cast<cudaError_t>(e), "substep launch");
+            if (L.profile) mark(L, L.ev_sub, stream);
+            ++g_launches;
+        }
+        std::swap(cur, prev);
+    }
+    wmc::QoIArgs qa{};
+    qa.nq = static_cast<int>(t.qoi_dof.size());
+    qa.S = S;
+    qa.count = count;
+    qa.dof = L.d_qdof;
+    qa.w = L.d_qw;
+    qa.sqrt_mass = L.d_qsm;
+    qa.z = cur;
+    qa.fail = L.d_fail;
+    qa.q = L.d_q;
+    wmc::launch_qoi(qa, stream);
+    ++g_launches;
+    check(cudaGetLastError(), "kernel launch");
+}
+
+void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
+    if (!fine) throw ConfigError("eval_pairs: fine level is NULL");
+    if (!coarse) return;
+    if (fine->device != coarse->device) throw ConfigError("eval_pairs: levels on different devices");
+    if (fine->tab.n_cells != coarse->tab.n_cells || fine->spec.coef_lo != coarse->spec.coef_lo ||
+        fine->spec.coef_hi != coarse->spec.coef_hi)
+        throw ConfigError("eval_pairs: coefficient grids of the pair differ");
+}
+
+void solve_counts(const wmc::LevelTables& t, wmc_cost& c, long solves) {
+    const bool lts = t.kind == wmc::Integrator::LocalTimeStepping;
+    if (lts) {
+        c.matvec_full += solves;
+        c.matvec_coarse += solves * (t.n_steps - 1);
+        c.matvec_fine += solves * (t.n_steps - 1) * t.p;
+        c.weighted_work += solves * (static_cast<long>(t.col.size()) +
+                                     (t.n_steps - 1) * (static_cast<long>(t.col.size()) +
+                                                        t.p * static_cast<long>(t.ap_col.size())));
+    } else {
+        c.matvec_full += solves * t.n_steps;
+        c.weighted_work += solves * t.n_steps * static_cast<long>(t.col.size());
+    }
+    c.dof_updates += static_cast<double>(solves) * wmc::dof_updates_per_solve(t);
+}
+
+// evaluates pairs; host_dq/host_qf may be NULL (device-resident mode: the
+// results for index first+i are written to dev_dq/dev_qf + i when given)
+void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::uint32_t level, std::uint64_t first,
+                     std::uint64_t count, double* host_dq, double* host_qf, double* dev_dq, double* dev_qf,
+                     wmc_cost* cost, wmc_error* err) {
+    check_pair_compat(fine, coarse);
+    check(cudaSetDevice(fine->device), "cudaSetDevice");
+    if (err) {
+        err->sample = -1;
+        err->step = 0;
+        err->level = static_cast<int>(level);
+    }
+    const int cap = coarse ? std::min(fine->batch, coarse->batch) : fine->batch;
+    cudaStream_t st = fine->stream;
+    std::vector<int> ff, fc;
+    for (std::uint64_t off = 0; off < count; off += cap) {
+        const int c = static_cast<int>(std::min<std::uint64_t>(cap, count - off));
+        const int S = round64(c);
+        wmc::launch_draw_cells(seed, level, first + off, c, S, fine->tab.n_cells, fine->spec.coef_lo,
+                               fine->spec.coef_hi, fine->d_cells, st);
+        g_launches += 2;  // draw + pair difference
+        solve_batch(*fine, fine->d_cells, S, c, st);
+        if (coarse) solve_batch(*coarse, fine->d_cells, S, c, st);
+        double* dq_dst = dev_dq ? dev_dq + off : fine->d_dq;
+        wmc::launch_pair_diff(fine->d_q, coarse ? coarse->d_q : nullptr, dq_dst, c, st);
+        if (dev_qf) check(cudaMemcpyAsync(dev_qf + off, fine->d_q, sizeof(double) * c, cudaMemcpyDeviceToDevice, st),
+                          "copy q");
+        if (host_dq || host_qf || err) {
+            ff.resize(c);
+            check(cudaMemcpyAsync(ff.data(), fine->d_fail, sizeof(int) * c, cudaMemcpyDeviceToHost, st), "fail");
+            if (coarse) {
+                fc.resize(c);
+                check(cudaMemcpyAsync(fc.data(), coarse->d_fail, sizeof(int) * c, cudaMemcpyDeviceToHost, st),
+                      "fail");
+            }
+            if (host_dq)
+                check(cudaMemcpyAsync(host_dq + off, dq_dst, sizeof(double) * c, cudaMemcpyDeviceToHost, st), "dq");
+            if (host_qf)
+                check(cudaMemcpyAsync(host_qf + off, fine->d_q, sizeof(double) * c, cudaMemcpyDeviceToHost, st),
+                      "q");
+            check(cudaStreamSynchronize(st), "synchronize");
+            for (int i = 0; i < c; ++i) {
+                const bool bad_f = ff[i] != INT_MAX, bad_c = coarse && fc[i] != INT_MAX;
+                if (bad_f || bad_c) {
+                    if (err) {
+                        err->sample = static_cast<long>(first + off + i);
+                        err->step = bad_f ? ff[i] : fc[i];
+                        err->level = bad_f ? static_cast<int>(level) : static_cast<int>(level) - 1;
+                    }
+                    g_last_error = "level " + std::to_string(level) + ", sample " +
+                                   std::to_string(first + off + i) + ": time integration unstable";
+                    throw NumericalError(g_last_error);
+                }
+            }
+        }
+    }
+    if (cost) {
+        std::memset(cost, 0, sizeof(*cost));
+        solve_counts(fine->tab, *cost, static_cast<long>(count));
+        if (coarse) solve_counts(coarse->tab, *cost, static_cast<long>(count));
+    }
+}
+
+struct Acc {
+    long n = 0;
+    double s_dq = 0.0, s_dq2 = 0.0, s_q = 0.0, s_q2 = 0.0;
+    wmc_cost cost{};
+    // LevelAccumulator::add (reference src/mlmc.cpp:44-53) on the scalar
+    // QoI; QoIVector::norm() of the 2-point encoding is sqrt(1*v*v)
+    void add(double dq, double q) {
+        ++n;
+        const double a = std::sqrt(dq * dq), b = std::sqrt(q * q);
+        s_dq2 += a * a;
+        s_q2 += b * b;
+        s_dq += dq;
+        s_q += q;
+    }
+    // estimate_variance / estimate_mc_variance (src/mlmc.cpp:61-73)
+    double variance() const {
+        if (n < 2) throw NumericalError("estimate_variance: need at least two samples");
+        const double nn = static_cast<double>(n), sn = std::sqrt(s_dq * s_dq);
+        return std::max(0.0, (s_dq2 - sn * sn / nn) / (nn - 1.0));
+    }
+    double mc_variance() const {
+        if (n < 2) throw NumericalError("estimate_mc_variance: need at least two samples");
+        const double nn = static_cast<double>(n), sn = std::sqrt(s_q * s_q);
+        return std::max(0.0, (s_q2 - sn * sn / nn) / nn);
+    }
+    double mean_dq() const { return n > 0 ? s_dq * (1.0 / static_cast<double>(n)) : 0.0; }
+};
+
+void fill_stats(int level, const Acc& a, double model_cost, wmc_level_stats& s) {
+    s.level = level;
+    s.n_samples = a.n;
+    s.sum_dq = a.s_dq;
+    s.sum_dq2 = a.s_dq2;
+    s.sum_q = a.s_q;
+    s.sum_q2 = a.s_q2;
+    s.variance = a.n >= 2 ? a.variance() : 0.0;
+    s.mc_variance = a.n >= 2 ? a.mc_variance() : 0.0;
+    s.mean_dq = a.mean_dq();
+    s.model_cost = model_cost;
+    s.cost = a.cost;
+}
+
+void run_level(wmc_level** levels, int l, std::uint64_t seed, long first, long count, Acc& acc, wmc_error* err) {
+    std::vector<double> dq(count), q(count);
+    wmc_cost c{};
+    eval_pairs_impl(levels[l], l > 0 ? levels[l - 1] : nullptr, seed, static_cast<std::uint32_t>(l),
+                    static_cast<std::uint64_t>(first), static_cast<std::uint64_t>(count), dq.data(), q.data(),
+                    nullptr, nullptr, &c, err);
+    for (long i = 0; i < count; ++i) acc.add(dq[i], q[i]);  // fold in index order (mlmc.cpp:145-147)
+    acc.cost.matvec_full += c.matvec_full;
+    acc.cost.matvec_fine += c.matvec_fine;
+    acc.cost.matvec_coarse += c.matvec_coarse;
+    acc.cost.weighted_work += c.weighted_work;
+    acc.cost.dof_updates += c.dof_updates;
+}
+
+}  // namespace
+
+namespace {
+wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
+    if (desc->integrator != WMC_LEAPFROG && desc->integrator != WMC_LOCAL_TIME_STEPPING)
+        throw ConfigError("wmc_level_create: unknown integrator");
+    if (!(desc->coef_lo > 0.0) || !(desc->coef_hi >= desc->coef_lo))
+        throw ConfigError("wmc_level_create: coefficient range must be positive");
+    if (desc->nu < 0.0 || desc->nu > 1.0) throw ConfigError("wmc_level_create: nu in [0,1]");
+    wmc::LevelSpec s;
+    s.cells_x = desc->cells_x;
+    s.cells_y = desc->cells_y;
+    s.coef_lo = desc->coef_lo;
+    s.coef_hi = desc->coef_hi;
+    s.final_time = desc->final_time;
+    s.dt = desc->dt;
+    s.substeps = desc->substeps;
+    s.nu = desc->nu;
+    s.kind = desc->integrator == WMC_LEAPFROG ? wmc::Integrator::Leapfrog : wmc::Integrator::LocalTimeStepping;
+    s.ic.x0 = desc->ic_x;
+    s.ic.y0 = desc->ic_y;
+    s.ic.width2 = desc->ic_width2;
+    s.qoi.x0 = desc->qoi_box[0];
+    s.qoi.x1 = desc->qoi_box[1];
+    s.qoi.y0 = desc->qoi_box[2];
+    s.qoi.y1 = desc->qoi_box[3];
+    return s;
+}
+
+void fill_info(const wmc::LevelTables& t, int batch, wmc_level_info* info) {
+    info->n = t.n;
+    info->n_r = t.n_r;
+    info->n_p = t.n_p;
+    info->p = t.p;
+    info->n_steps = t.n_steps;
+    info->dt = t.dt;
+    info->nnz = static_cast<long>(t.col.size());
+    info->ap_nnz = static_cast<long>(t.ap_col.size());
+    info->n_recipes = static_cast<long>(t.rc_ptr.size()) - 1;
+    info->batch = batch;
+    info->dof_updates_per_solve = wmc::dof_updates_per_solve(t);
+}
+}  // namespace
+
+extern "C" {
+
+const char* wmc_last_error(void) { return g_last_error.c_str(); }
+
+int wmc_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int wmc_mesh_build_square(const wmc_square_mesh_spec* spec, wmc_mesh** out) {
+    return guarded([&] {
+        if (!spec || !out) throw ConfigError("wmc_mesh_build_square: NULL argument");
+        wmc::SquareMeshSpec s;
+        s.n_coarse = spec->n_coarse;
+        s.ratio = spec->ratio;
+        s.fine_lo = spec->fine_lo;
+        s.fine_hi = spec->fine_hi;
+        s.snap = spec->snap;
+        s.small_factor = spec->small_factor > 0.0 ? spec->small_factor : 0.7;
+        auto m = std::make_unique<wmc_mesh>();
+        m->mesh = wmc::build_refined_square(s);
+        *out = m.release();
+    });
+}
+
+int wmc_mesh_create(int n_vertices, int n_triangles, const double* xy, const int* tri, const unsigned char* fine,
+                    const unsigned char* boundary, double coarse_h, double fine_h, wmc_mesh** out) {
+    return guarded([&] {
+        if (n_vertices <= 0 || n_triangles <= 0 || !xy || !tri || !out) throw ConfigError("wmc_mesh_create: bad arguments");
+        auto m = std::make_unique<wmc_mesh>();
+        auto& M = m->mesh;
+        M.coarse_h = coarse_h;
+        M.fine_h = fine_h;
+        M.vertices.resize(n_vertices);
+        M.boundary_vertex.assign(n_vertices, 0);
+        for (int v = 0; v < n_vertices; ++v) {
+            M.vertices[v] = {xy[2 * v], xy[2 * v + 1]};
+            if (boundary) M.boundary_vertex[v] = boundary[v] ? 1 : 0;
+        }
+        M.triangles.resize(n_triangles);
+        M.fine_flags.assign(n_triangles, 0);
+        for (int t = 0; t < n_triangles; ++t) {
+            for (int k = 0; k < 3; ++k) {
+                const int v = tri[3 * t + k];
+                if (v < 0 || v >= n_vertices) throw ConfigError("wmc_mesh_create: vertex index out of range");
+                M.triangles[t][k] = v;
+            }
+            if (fine) M.fine_flags[t] = fine[t] ? 1 : 0;
+        }
+        *out = m.release();
+    });
+}
+
+int wmc_mesh_info(const wmc_mesh* mesh, int* nv, int* nt, double* coarse_h, double* fine_h) {
+    return guarded([&] {
+        if (!mesh) throw ConfigError("wmc_mesh_info: NULL mesh");
+        if (nv) *nv = mesh->mesh.n_vertices();
+        if (nt) *nt = mesh->mesh.n_triangles();
+        if (coarse_h) *coarse_h = mesh->mesh.coarse_h;
+        if (fine_h) *fine_h = mesh->mesh.fine_h;
+    });
+}
+
+int wmc_mesh_export(const wmc_mesh* mesh, double* xy, int* tri, unsigned char* fine, unsigned char* boundary) {
+    return guarded([&] {
+        if (!mesh) throw ConfigError("wmc_mesh_export: NULL mesh");
+        const auto& M = mesh->mesh;
+        for (int v = 0; v < M.n_vertices(); ++v) {
+            if (xy) {
+                xy[2 * v] = M.vertices[v][0];
+                xy[2 * v + 1] = M.vertices[v][1];
+            }
+            if (boundary) boundary[v] = M.boundary_vertex[v];
+        }
+        for (int t = 0; t < M.n_triangles(); ++t) {
+            if (tri)
+                for (int k = 0; k < 3; ++k) tri[3 * t + k] = M.triangles[t][k];
+            if (fine) fine[t] = M.fine_flags[t];
+        }
+    });
+}
+
+int wmc_mesh_dump(const wmc_mesh* mesh, const char* path) {
+    return guarded([&] {
+        if (!mesh || !path) throw ConfigError("wmc_mesh_dump: NULL argument");
+        wmc::dump_mesh_text(mesh->mesh, path);
+    });
+}
+
+void wmc_mesh_destroy(wmc_mesh* mesh) { delete mesh; }
+
+void wmc_level_desc_default(wmc_level_desc* d) {
+    if (!d) return;
+    std::memset(d, 0, sizeof(*d));
+    d->cells_x = 4;
+    d->cells_y = 4;
+    d->coef_lo = 0.5;
+    d->coef_hi = 1.5;
+    d->final_time = 1.0;
+    d->dt = 0.2 / 32.0;
+    d->substeps = 4;
+    d->nu = 0.01;
+    d->integrator = WMC_LOCAL_TIME_STEPPING;
+    d->ic_x = 0.3;
+    d->ic_y = 0.5;
+    d->ic_width2 = 0.01;
+    d->qoi_box[0] = 0.7;
+    d->qoi_box[1] = 0.9;
+    d->qoi_box[2] = 0.4;
+    d->qoi_box[3] = 0.6;
+    d->device = 0;
+    d->batch = 0;
+}
+
+int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out) {
+    return guarded([&] {
+        if (!mesh || !desc || !out) throw ConfigError("wmc_level_create: NULL argument");
+        auto L = std::make_unique<wmc_level>();
+        L->device = desc->device;
+        L->spec = spec_from_desc(desc);
+        L->tab = wmc::build_level_tables(mesh->mesh, L->spec);
+        if (L->tab.n_steps >= INT_MAX) throw ConfigError("wmc_level_create: too many steps");
+        L->batch = round64(desc->batch > 0 ? desc->batch : 4096);
+        int ndev = 0;
+        check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (L->device < 0 || L->device >= ndev) throw ConfigError("wmc_level_create: no such device");
+        build_device_level(*L);
+        *out = L.release();
+    });
+}
+
+
+int wmc_level_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level_info* info) {
+    return guarded([&] {
+        if (!mesh || !desc || !info) throw ConfigError("wmc_level_plan: NULL argument");
+        const wmc::LevelTables t = wmc::build_level_tables(mesh->mesh, spec_from_desc(desc));
+        fill_info(t, 0, info);
+    });
+}
+
+int wmc_level_get_info(const wmc_level* L, wmc_level_info* info) {
+    return guarded([&] {
+        if (!L || !info) throw ConfigError("wmc_level_get_info: NULL argument");
+        fill_info(L->tab, L->batch, info);
+    });
+}
+
+void wmc_level_destroy(wmc_level* L) { delete L; }
+
+void* wmc_level_stream(wmc_level* L) { return L ? static_cast<void*>(L->stream) : nullptr; }
+
+int wmc_synchronize(wmc_level* L, wmc_error* err) {
+    (void)err;
+    return guarded([&] {
+        if (!L) throw ConfigError("wmc_synchronize: NULL level");
+        check(cudaSetDevice(L->device), "cudaSetDevice");
+        check(cudaStreamSynchronize(L->stream), "synchronize");
+    });
+}
+
+int wmc_eval_pairs(wmc_level* fine, wmc_level* coarse, uint64_t seed, uint32_t level, uint64_t first, uint64_t count,
+                   double* dq, double* q_fine, wmc_cost* cost, wmc_error* err) {
+    return guarded([&] { eval_pairs_impl(fine, coarse, seed, level, first, count, dq, q_fine, nullptr, nullptr, cost, err); });
+}
+
+int wmc_eval_pairs_device(wmc_level* fine, wmc_level* coarse, uint64_t seed, uint32_t level, uint64_t first,
+                          uint64_t count, double* d_dq, double* d_q_fine) {
+    return guarded([&] {
+        if (fine && count > static_cast<std::uint64_t>(coarse ? std::min(fine->batch, coarse->batch) : fine->batch) &&
+            !(d_dq && d_q_fine))
+            throw ConfigError("wmc_eval_pairs_device: results of more than one batch need device buffers");
+        eval_pairs_impl(fine, coarse, seed, level, first, count, nullptr, nullptr, d_dq, d_q_fine, nullptr, nullptr);
+    });
+}
+
+int wmc_draw_cells(uint64_t seed, uint32_t level, uint64_t first, uint64_t count, int n_cells, double lo, double hi,
+                   int device, double* out) {
+    return guarded([&] {
+        if (!out || n_cells <= 0) throw ConfigError("wmc_draw_cells: bad arguments");
+        check(cudaSetDevice(device), "cudaSetDevice");
+        const int S = round64(static_cast<long>(count));
+        double* d = nullptr;
+        check(cudaMalloc(&d, sizeof(double) * S * n_cells), "cudaMalloc");
+        wmc::launch_draw_cells(seed, level, first, static_cast<int>(count), S, n_cells, lo, hi, d, nullptr);
+        std::vector<double> h(static_cast<std::size_t>(S) * n_cells);
+        const cudaError_t e = cudaMemcpy(h.data(), d, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        check(e, "draw_cells copy");
+        for (std::uint64_t i = 0; i < count; ++i)
+            for (int k = 0; k < n_cells; ++k) out[i * n_cells + k] = h[static_cast<std::size_t>(k) * S + i];
+    });
+}
+
+int wmc_run_mlmc_fixed(wmc_level** levels, int n_levels, const long* first, const long* counts, uint64_t seed,
+                       wmc_level_stats* stats, wmc_error* err) {
+    return guarded([&] {
+        if (!levels || n_levels < 1 || !counts || !stats) throw ConfigError("wmc_run_mlmc_fixed: bad arguments");
+        for (int l = 0; l < n_levels; ++l) {
+            Acc acc;
+            if (counts[l] > 0) run_level(levels, l, seed, first ? first[l] : 0, counts[l], acc, err);
+            fill_stats(l, acc, 0.0, stats[l]);
+        }
+    });
+}
+
+void wmc_mlmc_config_default(wmc_mlmc_config* c) {
+    if (!c) return;
+    c->eps = 1e-3;
+    c->alpha = 2.0;
+    c->initial_samples = 16;
+    c->initial_levels = 2;
+    c->max_level = 6;
+    c->master_seed = 0;
+    c->bias_window = 1;
+}
+
+// Adaptive driver restating reference run_mlmc (src/mlmc.cpp:165-233) with
+// optimal_samples (:75-92), bias_proxy_sq (:94-98) and bias_over_window
+// (:151-161); jobs of one level run as one batched index range.
+int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
+                 wmc_mlmc_result* result, wmc_level_stats* stats, wmc_error* err) {
+    return guarded([&] {
+        if (!levels || n_levels < 1 || !model_cost || !cfg || !result || !stats)
+            throw ConfigError("wmc_run_mlmc: bad arguments");
+        if (!(cfg->eps > 0.0)) throw ConfigError("run_mlmc: eps must be positive");
+        if (cfg->alpha < 1.0) throw ConfigError("run_mlmc: alpha >= 1 required");
+        const int cap = std::min(cfg->max_level, n_levels - 1);
+        int top = std::min(cfg->initial_levels, cap);
+        std::vector<Acc> acc(top + 1);
+        std::vector<long> targets(top + 1, cfg->initial_samples);
+        auto bias_proxy = [&](double mean) {
+            const double denom = std::pow(2.0, cfg->alpha) - 1.0;
+            const double norm = std::sqrt(mean * mean) / denom;
+            return norm * norm;
+        };
+        auto bias_window = [&]() {
+            double worst = 0.0;
+            for (int j = 0; j < cfg->bias_window && top - j >= 1; ++j) {
+                const int l = top - j;
+                worst = std::max(worst, bias_proxy(acc[l].mean_dq()) * std::pow(2.0, -2.0 * cfg->alpha * (top - l)));
+            }
+            return worst;
+        };
+        bool converged = false;
+        {
+            while (true) {
+                for (int l = 0; l <= top; ++l)
+                    if (acc[l].n < targets[l]) run_level(levels, l, cfg->master_seed, acc[l].n, targets[l] - acc[l].n, acc[l], err);
+                std::vector<double> v(top + 1);
+                double total = 0.0;
+                for (int l = 0; l <= top; ++l) {
+                    v[l] = acc[l].variance();
+                    if (!(model_cost[l] > 0.0)) throw ConfigError("optimal_samples: costs must be positive");
+                    total += std::sqrt(v[l] * model_cost[l]);
+                }
+                bool increased = false;
+                for (int l = 0; l <= top; ++l) {
+                    const double nl = 2.0 / (cfg->eps * cfg->eps) * std::sqrt(v[l] / model_cost[l]) * total;
+                    const long want = std::max(2L, static_cast<long>(std::ceil(nl - 1e-9)));
+                    if (want > targets[l]) {
+                        targets[l] = want;
+                        increased = true;
+                    }
+                }
+                if (increased) continue;
+                if (top >= 1 && bias_window() < 0.5 * cfg->eps * cfg->eps) {
+                    converged = true;
+                    break;
+                }
+                if (top >= cap) break;
+                ++top;
+                acc.emplace_back();
+                targets.push_back(cfg->initial_samples);
+            }
+        }
+        std::memset(result, 0, sizeof(*result));
+        result->converged = converged ? 1 : 0;
+        result->levels_used = top;
+        for (int l = 0; l <= top; ++l) {
+            fill_stats(l, acc[l], model_cost[l], stats[l]);
+            result->estimate += acc[l].mean_dq();
+            result->total_variance += stats[l].variance / static_cast<double>(stats[l].n_samples);
+            result->total_model_cost += model_cost[l] * static_cast<double>(stats[l].n_samples);
+        }
+        result->bias = bias_window();
+        result->rmse = std::sqrt(result->total_variance + result->bias);
+    });
+}
+
+long wmc_launch_count(void) { return g_launches.load(); }
+
+int wmc_moments_device(wmc_level* level, const double* d_dq, const double* d_q, uint64_t count, double* d_out) {
+    return guarded([&] {
+        if (!level || !d_dq || !d_q || !d_out) throw ConfigError("wmc_moments_device: NULL argument");
+        if (count > static_cast<std::uint64_t>(INT_MAX)) throw ConfigError("wmc_moments_device: count too large");
+        check(cudaSetDevice(level->device), "cudaSetDevice");
+        wmc::launch_moments(d_dq, d_q, static_cast<int>(count), d_out, level->stream);
+        ++g_launches;
+        check(cudaGetLastError(), "moments launch");
+    });
+}
+
+int wmc_profile_enable(wmc_level* level, int on) {
+    return guarded([&] {
+        if (!level) throw ConfigError("wmc_profile_enable: NULL level");
+        level->profile = on != 0;
+    });
+}
+
+int wmc_profile_read(wmc_level* level, double* sweep_ms, long* sweep_launches, double* sub_ms, long* sub_launches) {
+    return guarded([&] {
+        if (!level) throw ConfigError("wmc_profile_read: NULL level");
+        check(cudaSetDevice(level->device), "cudaSetDevice");
+        check(cudaStreamSynchronize(level->stream), "synchronize");
+        auto total = [](std::vector<cudaEvent_t>& v, double* ms, long* n) {
+            double acc = 0.0;
+            for (std::size_t i = 0; i + 1 < v.size(); i += 2) {
+                float f = 0.0f;
+                check(cudaEventElapsedTime(&f, v[i], v[i + 1]), "cudaEventElapsedTime");
+                acc += f;
+            }
+            if (ms) *ms = acc;
+            if (n) *n = static_cast<long>(v.size() / 2);
+            for (auto e : v) cudaEventDestroy(e);
+            v.clear();
+        };
+        total(level->ev_sweep, sweep_ms, sweep_launches);
+        total(level->ev_sub, sub_ms, sub_launches);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// Per-level operator tables: the sample-independent geometry of one MLMC
+// level, laid out for the device kernels.
+//
+// Reference semantics restated here (all file:line into /root/reference/proj):
+//   * element stiffness K_e = c(centroid) * area * grad(phi_i).grad(phi_j) and
+//     lumped mass M_ii += area/3                          src/fem.cpp:91-126
+//   * A = M^{-1/2} K M^{-1/2}, selector P = vertices of fine-flagged
+//     triangles, A P / A (I-P) column masks               src/fem.cpp:42-63
+//   * lumped L2 projection of u0 (edge-midpoint rule), z0 = sqrt(M) coef
+//                                                          src/fem.cpp:223-269
+//   * n_steps = ceil(T/dt - 1e-12), dt = T/n_steps         src/integrators.cpp:188-189
+//   * Chebyshev constants and the LTS substep constants   src/integrators.cpp:34-66, :126-141
+//
+// The per-sample coefficient c is piecewise constant on an nx x ny cell grid
+// and enters A linearly, so A(omega)_ij = sum_k c_k(omega) * a0_ijk with the
+// geometric a0_ijk shared by all samples (the "parts" representation).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "mesh.hpp"
+
+namespace wmc {
+
+enum class Integrator : int { Leapfrog = 0, LocalTimeStepping = 1 };
+
+struct GaussianIC {
+    double x0 = 0.3, y0 = 0.5, width2 = 0.01;  // u0 = exp(-((x-x0)^2+(y-y0)^2)/width2)
+};
+
+struct QoIBox {
+    double x0 = 0.7, x1 = 0.9, y0 = 0.4, y1 = 0.6;
+};
+
+struct LevelSpec {
+    int cells_x = 4, cells_y = 4;  // coefficient grid on [0,1]^2, cell k = iy*cells_x + ix
+    double coef_lo = 0.5, coef_hi = 1.5;  // c_k ~ U[coef_lo, coef_hi)
+    double final_time = 1.0;
+    double dt = 0.0;  // requested coarse step (snapped so n_steps*dt == T)
+    int substeps = 1;
+    double nu = 0.01;
+    Integrator kind = Integrator::LocalTimeStepping;
+    GaussianIC ic;
+    QoIBox qoi;
+};
+
+struct ChebyshevConstants {
+    int p = 1;
+    double nu = 0.0, delta = 1.0, omega = 2.0;
+    std::vector<double> beta_int, beta_half;
+};
+
+ChebyshevConstants chebyshev_constants(int p, double nu);
+
+struct LevelTables {
+    int n = 0;       // interior DOFs (Dirichlet boundary eliminated)
+    int n_r = 0;     // DOFs [0, n_r) are R = rows of A P with a nonzero
+    int n_p = 0;     // |P|
+    int n_cells = 0;
+    std::vector<int> dof_vertex;        // dof -> mesh vertex
+    std::vector<std::uint8_t> in_p;     // per dof
+
+    // full operator, row-wise "parts": A_ij(omega) = sum over the row's
+    // entries e with col[e] == j of c[cell[e]] * a0[e]; exact zeros dropped
+    std::vector<int> row_ptr;
+    std::vector<int> col;
+    std::vector<int> cell;
+    std::vector<double> a0;
+
+    // A P restricted to R rows, as recipes: entry (row r, col j in P, wid);
+    // recipe wid = sum_t c[rc_cell[t]] * rc_a0[t] for t in [rc_ptr[wid], rc_ptr[wid+1])
+    std::vector<int> ap_row_ptr;
+    std::vector<int> ap_col;
+    std::vector<int> ap_wid;
+    std::vector<int> rc_ptr;
+    std::vector<int> rc_cell;
+    std::vector<double> rc_a0;
+
+    std::vector<double> mass;       // lumped mass per dof
+    std::vector<double> z0;         // sqrt(M) * projected u0, per dof
+    std::vector<int> qoi_dof;       // dofs with a nonzero QoI weight
+    std::vector<double> qoi_w;      // Q = sum w_i * (z_i / sqrt(M_i))
+    std::vector<double> sqrt_mass_qoi;  // sqrt(M_i) for qoi_dof
+
+    std::vector<int> elem_cell;     // per triangle (diagnostics)
+
+    // time stepping
+    long n_steps = 0;
+    double dt = 0.0;
+    int p = 1;
+    Integrator kind = Integrator::LocalTimeStepping;
+    double c0 = 0.0;                 // d_1 = -c0 (A z_n)
+    std::vector<double> beta;        // beta_int[m-1], m = 1..p-1
+    std::vector<double> cm;          // c_m, m = 1..p-1
+    double coarse_factor = 0.0;      // rows outside R: z+ = 2z - z- - coarse_factor * (A z)
+    double init_factor = 0.0;        // start-up: z1 = z0 - init_factor * (A z0)
+};
+
+LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec);
+
+/// DOF-updates per solve: steps * (n + (p-1)|R|) for LTS, steps * n for LF
+/// (SURVEY.md section 8(d)); the start-up step counts as one sweep.
+double dof_updates_per_solve(const LevelTables& t);
+
+}  // namespace wmc

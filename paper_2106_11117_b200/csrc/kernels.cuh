@@ -1,0 +1,81 @@
+// Device kernels of the batched LF / LF-LTS sample evaluator (sm_100a, FP64).
+//
+// Layout in HBM (per level, per batch of S samples, S a multiple of 64):
+//   z[i * S + s]      nodal state, node-major with samples interleaved, so a
+//                     warp reads one row for 64 samples as 32 x 16 B
+//   g[r * S + s]      A z_n on the R rows (r < n_r), stashed by the sweep
+//   cells[k * S + s]  per-sample coefficient of cell k
+// The geometric operator tables are shared by all samples.
+#pragma once
+
+#include <cstdint>
+
+namespace wmc {
+
+constexpr int kSweepChunk = 64;  // samples per warp in the sweep (2 per lane)
+constexpr int kSweepWarps = 8;   // rows per sweep block
+constexpr int kSubThreads = 1024;
+constexpr int kSubMaxRpt = 8;    // rows per thread in the substep kernel
+
+struct SweepArgs {
+    int n;           // rows
+    int split;       // rows < split stash g (LTS); 0 for leapfrog
+    int S;           // batch stride
+    int count;       // live samples
+    const int* row_ptr;
+    const int* ent;      // col | cell << 24
+    const double* a0;
+    const double* cells;
+    const double* z0;    // init only
+    const double* zc;    // z_n
+    double* zp;          // z_{n-1} in, z_{n+1} out; init: z0 out
+    double* zc_out;      // init only: z_1 out
+    double* g;
+    double factor;       // init_factor or coarse_factor
+    int step;
+    int* fail;
+};
+
+struct SubArgs {
+    int n_r, S, count, p;
+    int n_wid, n_cells, n_ent;
+    const std::uint32_t* ent;   // SELL: [slice][width][32], col | wid << 16
+    const int* slice_off;       // per slice: entry offset; width = (off[s+1]-off[s]) / 32
+    const int* rc_ptr;
+    const int* rc_cell;
+    const double* rc_a0;
+    const double* cells;
+    const double* g;
+    const double* zc;
+    double* zp;
+    const double* beta;   // p-1
+    const double* cm;     // p-1
+    double c0;
+    int step;
+    int* fail;
+};
+
+struct QoIArgs {
+    int nq, S, count;
+    const int* dof;
+    const double* w;
+    const double* sqrt_mass;
+    const double* z;
+    const int* fail;
+    double* q;
+};
+
+void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
+                       double lo, double hi, double* cells, void* stream);
+void launch_sweep_init(const SweepArgs& a, void* stream);
+void launch_sweep_step(const SweepArgs& a, void* stream);
+int substep_smem_bytes(const SubArgs& a);
+int launch_substeps(const SubArgs& a, int grid, void* stream);  // returns cudaError_t
+void launch_qoi(const QoIArgs& a, void* stream);
+void launch_fill_int(int* p, int value, int n, void* stream);
+void launch_pair_diff(const double* qf, const double* qc, double* dq, int count, void* stream);
+int substep_max_grid(int device, int smem_bytes);
+// deterministic single-block fold of (dq, q) into out[0..3] += {sum dq, sum dq^2, sum q, sum q^2}
+void launch_moments(const double* dq, const double* q, int count, double* out, void* stream);
+
+}  // namespace wmc

@@ -1,0 +1,260 @@
+"""Host-side mirror of the reference sampler API over the B200 C ABI.
+
+Reference interface this mirrors (paths in /root/reference/proj):
+  * MlmcProblem / sample_delta_q / run_jobs  include/wavemc/mlmc.hpp:41-51,
+    src/mlmc.cpp:21-37, :107-149  ->  Level + eval_pairs (batched pairs)
+  * LevelAccumulator / estimate_variance     include/wavemc/mlmc.hpp:53-73
+    ->  LevelStats fields (sum_dq, sum_dq2, sum_q, sum_q2, variance, ...)
+  * run_mlmc / MlmcConfig / MlmcResult       include/wavemc/mlmc.hpp:14-112
+    ->  run_mlmc, run_mlmc_fixed
+  * RngStream(seed, level, index)            include/wavemc/rng.hpp:27-46
+    ->  draw_cells (device draws, bit-identical)
+  * errors: ConfigError (exit 2), NumericalError / InstabilityError{step}
+    (exit 3)                                 include/wavemc/errors.hpp:9-26
+All compute runs in libwavemc_b200.so on the GPU; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._native import ConfigError, DeviceError, NumericalError, WavemcError  # noqa: F401
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Mesh:
+    """A triangulation of the unit square (TriMesh, reference mesh.hpp:48-74)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    @classmethod
+    def build_square(cls, n_coarse: int, ratio: int, fine_lo: float = 0.45, fine_hi: float = 0.55,
+                     snap: float = 1.0 / 16, small_factor: float = 0.7) -> "Mesh":
+        spec = N.SquareMeshSpec(n_coarse, ratio, fine_lo, fine_hi, snap, small_factor)
+        h = C.c_void_p()
+        N.check(N.lib().wmc_mesh_build_square(C.byref(spec), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_arrays(cls, xy, tri, fine, boundary, coarse_h=0.0, fine_h=0.0) -> "Mesh":
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        tri = np.ascontiguousarray(tri, dtype=np.int32)
+        fine = np.ascontiguousarray(fine, dtype=np.uint8)
+        boundary = np.ascontiguousarray(boundary, dtype=np.uint8)
+        h = C.c_void_p()
+        N.check(N.lib().wmc_mesh_create(len(xy), len(tri), _dptr(xy), tri.ctypes.data_as(C.POINTER(C.c_int)),
+                                        fine.ctypes.data_as(C.POINTER(C.c_ubyte)),
+                                        boundary.ctypes.data_as(C.POINTER(C.c_ubyte)), coarse_h, fine_h,
+                                        C.byref(h)))
+        return cls(h.value)
+
+    def info(self):
+        nv, nt = C.c_int(), C.c_int()
+        ch, fh = C.c_double(), C.c_double()
+        N.check(N.lib().wmc_mesh_info(self._h, C.byref(nv), C.byref(nt), C.byref(ch), C.byref(fh)))
+        return nv.value, nt.value, ch.value, fh.value
+
+    def arrays(self):
+        nv, nt, _, _ = self.info()
+        xy = np.zeros((nv, 2), np.float64)
+        tri = np.zeros((nt, 3), np.int32)
+        fine = np.zeros(nt, np.uint8)
+        boundary = np.zeros(nv, np.uint8)
+        N.check(N.lib().wmc_mesh_export(self._h, _dptr(xy), tri.ctypes.data_as(C.POINTER(C.c_int)),
+                                        fine.ctypes.data_as(C.POINTER(C.c_ubyte)),
+                                        boundary.ctypes.data_as(C.POINTER(C.c_ubyte))))
+        return xy, tri, fine, boundary
+
+    def dump(self, path: str) -> None:
+        N.check(N.lib().wmc_mesh_dump(self._h, str(path).encode()))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            N.lib().wmc_mesh_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+@dataclass
+class LevelSpec:
+    """Per-level problem definition (wmc_level_desc)."""
+    dt: float
+    substeps: int = 1
+    integrator: int = N.WMC_LOCAL_TIME_STEPPING
+    final_time: float = 1.0
+    nu: float = 0.01
+    cells_x: int = 4
+    cells_y: int = 4
+    coef_lo: float = 0.5
+    coef_hi: float = 1.5
+    ic: tuple = (0.3, 0.5, 0.01)
+    qoi_box: tuple = (0.7, 0.9, 0.4, 0.6)
+    device: int = 0
+    batch: int = 0
+
+    def desc(self) -> N.LevelDesc:
+        d = N.LevelDesc()
+        N.lib().wmc_level_desc_default(C.byref(d))
+        d.cells_x, d.cells_y = self.cells_x, self.cells_y
+        d.coef_lo, d.coef_hi = self.coef_lo, self.coef_hi
+        d.final_time, d.dt, d.substeps, d.nu = self.final_time, self.dt, self.substeps, self.nu
+        d.integrator = self.integrator
+        d.ic_x, d.ic_y, d.ic_width2 = self.ic
+        for i, v in enumerate(self.qoi_box):
+            d.qoi_box[i] = v
+        d.device, d.batch = self.device, self.batch
+        return d
+
+
+def level_plan(mesh: Mesh, spec: LevelSpec) -> dict:
+    """Host-only level tables: sizes and DOF-update counts (no device)."""
+    d = spec.desc()
+    info = N.LevelInfo()
+    N.check(N.lib().wmc_level_plan(mesh._h, C.byref(d), C.byref(info)))
+    return {k: getattr(info, k) for k, _ in N.LevelInfo._fields_}
+
+
+class Level:
+    """One MLMC level resident on a device (wmc_level)."""
+
+    def __init__(self, mesh: Mesh, spec: LevelSpec):
+        self.mesh = mesh
+        self.spec = spec
+        d = spec.desc()
+        h = C.c_void_p()
+        N.check(N.lib().wmc_level_create(mesh._h, C.byref(d), C.byref(h)))
+        self._h = h
+        info = N.LevelInfo()
+        N.check(N.lib().wmc_level_get_info(self._h, C.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in N.LevelInfo._fields_}
+
+    @property
+    def stream(self) -> int:
+        return N.lib().wmc_level_stream(self._h) or 0
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            N.lib().wmc_level_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+def eval_pairs(fine: Level, coarse: Level | None, seed: int, level: int, first: int, count: int):
+    """Batched sample_delta_q (reference src/mlmc.cpp:21-37) over indices
+    first..first+count-1: returns (dq, q_fine, cost dict)."""
+    dq = np.empty(count, np.float64)
+    qf = np.empty(count, np.float64)
+    cost = N.Cost()
+    err = N.Error()
+    rc = N.lib().wmc_eval_pairs(fine._h, coarse._h if coarse is not None else None, seed, level, first, count,
+                                _dptr(dq), _dptr(qf), C.byref(cost), C.byref(err))
+    N.check(rc, err)
+    return dq, qf, {k: getattr(cost, k) for k, _ in N.Cost._fields_}
+
+
+def eval_pairs_device(fine: Level, coarse: Level | None, seed: int, level: int, first: int, count: int,
+                      d_dq: int = 0, d_qf: int = 0) -> None:
+    """Same work, results left in device memory, no host synchronisation."""
+    N.check(N.lib().wmc_eval_pairs_device(fine._h, coarse._h if coarse is not None else None, seed, level, first,
+                                          count, d_dq or None, d_qf or None))
+
+
+def synchronize(level: Level) -> None:
+    err = N.Error()
+    N.check(N.lib().wmc_synchronize(level._h, C.byref(err)), err)
+
+
+def draw_cells(seed: int, level: int, first: int, count: int, n_cells: int = 16, lo: float = 0.5,
+               hi: float = 1.5, device: int = 0) -> np.ndarray:
+    out = np.empty((count, n_cells), np.float64)
+    N.check(N.lib().wmc_draw_cells(seed, level, first, count, n_cells, lo, hi, device, _dptr(out)))
+    return out
+
+
+def _stats(s: N.LevelStats) -> dict:
+    d = {k: getattr(s, k) for k, _ in N.LevelStats._fields_ if k != "cost"}
+    d["cost"] = {k: getattr(s.cost, k) for k, _ in N.Cost._fields_}
+    return d
+
+
+def run_mlmc_fixed(levels: list[Level], counts: list[int], seed: int = 0, first: list[int] | None = None) -> list[dict]:
+    """Fixed N_l over levels 0..L (BASELINE config 1): per-level LevelAccumulator
+    sums and estimators, folded in index order.  With ``first`` the call covers
+    indices first[l] .. first[l]+counts[l]-1 (one rank's shard)."""
+    n = len(levels)
+    arr = (C.c_void_p * n)(*[lv._h.value for lv in levels])
+    cnt = (C.c_long * n)(*counts)
+    fst = (C.c_long * n)(*(first or [0] * n))
+    stats = (N.LevelStats * n)()
+    err = N.Error()
+    N.check(N.lib().wmc_run_mlmc_fixed(arr, n, fst, cnt, seed, stats, C.byref(err)), err)
+    return [_stats(stats[i]) for i in range(n)]
+
+
+@dataclass
+class MlmcConfig:
+    """Reference MlmcConfig (include/wavemc/mlmc.hpp:14-23)."""
+    eps: float = 1e-3
+    alpha: float = 2.0
+    initial_samples: int = 16
+    initial_levels: int = 2
+    max_level: int = 6
+    master_seed: int = 0
+    bias_window: int = 1
+
+
+@dataclass
+class MlmcResult:
+    estimate: float
+    converged: bool
+    levels_used: int
+    total_variance: float
+    bias: float
+    total_model_cost: float
+    rmse: float
+    levels: list = field(default_factory=list)
+
+
+def run_mlmc(levels: list[Level], model_cost: list[float], config: MlmcConfig | None = None) -> MlmcResult:
+    """Adaptive Giles driver (reference run_mlmc, src/mlmc.cpp:165-233)."""
+    config = config or MlmcConfig()
+    n = len(levels)
+    arr = (C.c_void_p * n)(*[lv._h.value for lv in levels])
+    cost = (C.c_double * n)(*model_cost)
+    cfg = N.MlmcConfig(config.eps, config.alpha, config.initial_samples, config.initial_levels, config.max_level,
+                       config.master_seed, config.bias_window)
+    res = N.MlmcResult()
+    stats = (N.LevelStats * n)()
+    err = N.Error()
+    N.check(N.lib().wmc_run_mlmc(arr, n, cost, C.byref(cfg), C.byref(res), stats, C.byref(err)), err)
+    return MlmcResult(res.estimate, bool(res.converged), res.levels_used, res.total_variance, res.bias,
+                      res.total_model_cost, res.rmse, [_stats(stats[i]) for i in range(res.levels_used + 1)])
+
+
+def moments_device(level: Level, d_dq: int, d_q: int, count: int, d_out: int) -> None:
+    """d_out[0..3] += {sum dq, sum dq^2, sum q, sum q^2} on the device."""
+    N.check(N.lib().wmc_moments_device(level._h, d_dq, d_q, count, d_out))
+
+
+def profile_enable(level: Level, on: bool = True) -> None:
+    N.check(N.lib().wmc_profile_enable(level._h, int(on)))
+
+
+def profile_read(level: Level) -> dict:
+    sm, su = C.c_double(), C.c_double()
+    ns, nu = C.c_long(), C.c_long()
+    N.check(N.lib().wmc_profile_read(level._h, C.byref(sm), C.byref(ns), C.byref(su), C.byref(nu)))
+    return {"sweep_ms": sm.value, "sweep_launches": ns.value, "sub_ms": su.value, "sub_launches": nu.value}
+
+
+def launch_count() -> int:
+    return N.lib().wmc_launch_count()
+
+
+def device_count() -> int:
+    return N.lib().wmc_device_count()

@@ -1,0 +1,186 @@
+"""Parity of the CUDA path (through the C ABI) with the reference: golden
+vectors from the unmodified reference library and the C restatement as the
+checker.  Tolerances (BASELINE north_star): per-sample QoI within 1e-10
+relative, per-level means and variances within 1e-9 relative."""
+import numpy as np
+import pytest
+
+from oracle_py import MeshArrays, problem
+from paper_2106_11117_b200 import configs, wavemc
+from paper_2106_11117_b200._native import WMC_LEAPFROG, WMC_LOCAL_TIME_STEPPING
+
+pytestmark = pytest.mark.gpu
+
+QOI_RTOL = 1e-10
+MOMENT_RTOL = 1e-9
+
+
+def rel_err(got, ref, scale=None):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    scale = np.max(np.abs(ref)) if scale is None else scale
+    return float(np.max(np.abs(got - ref)) / scale)
+
+
+def per_sample_rel(got, ref):
+    got, ref = np.asarray(got), np.asarray(ref)
+    return float(np.max(np.abs(got - ref) / np.abs(ref)))
+
+
+@pytest.fixture(scope="module")
+def level0():
+    return configs.build_level(configs.config0())
+
+
+@pytest.fixture(scope="module")
+def mesh0_arrays():
+    return MeshArrays(*configs.build_mesh(configs.config0()).arrays())
+
+
+def test_draw_cells_bit_identical_to_reference(golden):
+    for case in golden("rng.json")["uniform"]:
+        got = wavemc.draw_cells(case["seed"], case["level"], case["index"], 1, len(case["values"]), case["lo"],
+                                case["hi"])
+        assert got[0].tolist() == case["values"]
+
+
+def test_draw_cells_match_c_oracle_many(coracle):
+    got = wavemc.draw_cells(7, 3, 10**6, 300)
+    for i in (0, 1, 63, 64, 299):
+        assert got[i].tolist() == coracle.draw_cells(7, 3, 10**6 + i).tolist()
+
+
+def test_level_info_matches_reference_counts(golden, level0):
+    hdr = golden("config0_samples.json")["lts"]["header"]
+    assert level0.info["n"] == int(hdr["n"])
+    assert level0.info["n_r"] == int(hdr["n_r"])
+    assert level0.info["n_steps"] == int(hdr["n_steps"])
+    assert level0.info["dof_updates_per_solve"] == pytest.approx(float(hdr["dof_updates_per_solve"]))
+
+
+def test_config0_lts_matches_reference(golden, level0):
+    g = golden("config0_samples.json")["lts"]
+    dq, qf, cost = wavemc.eval_pairs(level0, None, 0, 0, 0, len(g["q"]))
+    assert per_sample_rel(qf, g["q"]) < QOI_RTOL
+    assert np.array_equal(dq, qf)
+    assert cost["matvec_fine"] == len(g["q"]) * (level0.info["n_steps"] - 1) * 4
+
+
+def test_config0_lts_nu0_offset_stream_matches_reference(golden):
+    g = golden("config0_samples.json")["lts_nu0"]
+    d = configs.config0()
+    lv = wavemc.Level(configs.build_mesh(d), wavemc.LevelSpec(dt=d.dt, substeps=d.substeps, nu=0.0))
+    _, qf, _ = wavemc.eval_pairs(lv, None, 0, g["stream_level"], g["first"], len(g["q"]))
+    assert per_sample_rel(qf, g["q"]) < QOI_RTOL
+
+
+def test_config0_leapfrog_matches_reference(golden):
+    g = golden("config0_samples.json")["lf"]
+    lv = configs.build_level(configs.config0_leapfrog())
+    _, qf, cost = wavemc.eval_pairs(lv, None, 0, 0, 0, len(g["q"]))
+    assert per_sample_rel(qf, g["q"]) < QOI_RTOL
+    assert cost["matvec_full"] == len(g["q"]) * lv.info["n_steps"]
+
+
+def test_config0_matches_c_oracle(coracle, level0, mesh0_arrays):
+    d = configs.config0()
+    n = 48
+    _, qf, _ = wavemc.eval_pairs(level0, None, 0, 0, 500, n)
+    rc, _, ref, _, _ = coracle.eval_pairs(mesh0_arrays, problem(d.dt, d.substeps), None, None, 0, 0, 500, n)
+    assert rc == 0
+    assert per_sample_rel(qf, ref) < QOI_RTOL
+
+
+def test_config1_pairs_every_level_match_reference(golden):
+    levels = [configs.build_level(d) for d in configs.config1()]
+    for lv in golden("config1_pairs.json")["levels"]:
+        l, n = lv["level"], lv["N"]
+        dq, qf, _ = wavemc.eval_pairs(levels[l], levels[l - 1] if l else None, 0, l, 0, n)
+        assert per_sample_rel(qf, lv["q"]) < QOI_RTOL, l
+        # dQ is a difference of O(|Q|) numbers: hold it to the QoI budget of Q
+        assert np.max(np.abs(dq - lv["dq"]) / np.abs(lv["q"])) < 2 * QOI_RTOL, l
+
+
+def test_fixed_mlmc_moments_match_reference(golden, level0):
+    lv = golden("config0_moments.json")["levels"][0]
+    st = wavemc.run_mlmc_fixed([level0], [lv["N"]], seed=0)[0]
+    assert st["n_samples"] == lv["N"]
+    for k in ("sum_dq", "sum_q", "variance", "mc_variance", "mean_dq", "sum_dq2", "sum_q2"):
+        assert st[k] == pytest.approx(lv[k], rel=MOMENT_RTOL), k
+
+
+def test_batching_and_offsets_are_bitwise_invariant():
+    d = configs.config0()
+    small = configs.build_level(d, batch=64)
+    big = configs.build_level(d, batch=1024)
+    _, a, _ = wavemc.eval_pairs(small, None, 0, 0, 0, 200)
+    _, b, _ = wavemc.eval_pairs(big, None, 0, 0, 0, 200)
+    _, c, _ = wavemc.eval_pairs(big, None, 0, 0, 37, 100)
+    assert np.array_equal(a, b)
+    assert np.array_equal(a[37:137], c)
+
+
+def test_repeat_runs_are_bitwise_identical(level0):
+    _, a, _ = wavemc.eval_pairs(level0, None, 3, 1, 0, 300)
+    _, b, _ = wavemc.eval_pairs(level0, None, 3, 1, 0, 300)
+    assert np.array_equal(a, b)
+
+
+def test_lts_p1_nu0_equals_leapfrog():
+    """reference tests/test_integrators.cpp:217-236 on the P1 mesh."""
+    d = configs.config0()
+    dt = 0.2 / 128
+    lts = wavemc.Level(configs.build_mesh(d), wavemc.LevelSpec(dt=dt, substeps=1, nu=0.0))
+    lf = wavemc.Level(configs.build_mesh(d), wavemc.LevelSpec(dt=dt, integrator=WMC_LEAPFROG))
+    _, a, _ = wavemc.eval_pairs(lts, None, 0, 0, 0, 64)
+    _, b, _ = wavemc.eval_pairs(lf, None, 0, 0, 0, 64)
+    assert rel_err(a, b) < 1e-12
+
+
+def test_empty_selector_equals_leapfrog():
+    """reference tests/test_integrators.cpp:238-265: P empty -> LTS == LF."""
+    mesh = wavemc.Mesh.build_square(32, 4, small_factor=0.0)
+    _, _, fine, _ = mesh.arrays()
+    assert fine.sum() == 0
+    dt = 0.2 / 128
+    lts = wavemc.Level(mesh, wavemc.LevelSpec(dt=dt, substeps=16, nu=0.01))
+    assert lts.info["n_r"] == 0
+    lf = wavemc.Level(mesh, wavemc.LevelSpec(dt=dt, integrator=WMC_LEAPFROG))
+    _, a, ca = wavemc.eval_pairs(lts, None, 0, 0, 0, 64)
+    _, b, _ = wavemc.eval_pairs(lf, None, 0, 0, 0, 64)
+    assert rel_err(a, b) < 1e-11
+    assert ca["matvec_fine"] == 64 * (lts.info["n_steps"] - 1) * 16
+
+
+def test_instability_raises_numerical_error_with_step(coracle, mesh0_arrays):
+    lv = wavemc.Level(configs.build_mesh(configs.config0()),
+                      wavemc.LevelSpec(dt=0.2, final_time=20.0, integrator=WMC_LEAPFROG))
+    with pytest.raises(wavemc.NumericalError) as ei:
+        wavemc.eval_pairs(lv, None, 0, 0, 5, 3)
+    assert ei.value.sample == 5
+    rc, _, step, _ = coracle.solve(mesh0_arrays, problem(0.2, 1, 0, final_time=20.0),
+                                   coracle.draw_cells(0, 0, 5))
+    assert rc == 3 and ei.value.step == step
+
+
+def test_config_errors_are_reported():
+    with pytest.raises(wavemc.ConfigError):
+        wavemc.Level(configs.build_mesh(configs.config0()), wavemc.LevelSpec(dt=0.01, nu=2.0))
+    with pytest.raises(wavemc.ConfigError):
+        wavemc.Level(configs.build_mesh(configs.config0()), wavemc.LevelSpec(dt=-1.0))
+
+
+def test_config1_level0_full_batch_spot_checks(coracle):
+    """Full-size run (65536 samples of config 1 level 0): spot indices against
+    the C oracle, and the batch result is independent of the index range."""
+    d = configs.config1()[0]
+    lv = configs.build_level(d)
+    n = 65536
+    _, qf, _ = wavemc.eval_pairs(lv, None, 0, 0, 0, n)
+    assert np.all(np.isfinite(qf))
+    mesh = MeshArrays(*configs.build_mesh(d).arrays())
+    for i in (0, 4095, 4096, 40000, n - 1):
+        rc, _, ref, _, _ = coracle.eval_pairs(mesh, problem(d.dt, d.substeps), None, None, 0, 0, i, 1)
+        assert rc == 0
+        assert abs(qf[i] - ref[0]) / abs(ref[0]) < QOI_RTOL, i
+    _, tail, _ = wavemc.eval_pairs(lv, None, 0, 0, n - 100, 100)
+    assert np.array_equal(tail, qf[-100:])
