@@ -61,7 +61,7 @@ typedef struct {
     int ratio;           /* h / h_min, power of two */
     double fine_lo, fine_hi;  /* refined square [lo, hi]^2 */
     double snap;         /* snap grid for the square (0 -> coarse grid) */
-    double small_factor; /* small triangle: longest edge < small_factor*sqrt(2)*h */
+    double small_factor; /* small triangle: longest edge < small_factor*sqrt(2)*h (0: none) */
 } wmc_square_mesh_spec;
 
 int wmc_mesh_build_square(const wmc_square_mesh_spec* spec, wmc_mesh** out);
@@ -102,6 +102,7 @@ typedef struct {
     long n_recipes;
     int batch;                /* samples per device batch */
     double dof_updates_per_solve;  /* n + (n_steps-1)(n + (p-1)|R|) for LTS, n_steps*n for LF */
+    int lattice;              /* 1: substeps use the structured refined-square kernel */
 } wmc_level_info;
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);

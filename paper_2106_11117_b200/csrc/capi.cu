@@ -76,6 +76,17 @@ T* upload(const std::vector<T>& v) {
 
 }  // namespace
 
+// per-role batch state: a level is solved as the fine level of its own pair
+// and as the coarse level of the next one, possibly concurrently on two
+// streams, so each role owns its buffers
+struct Workspace {
+    double* za = nullptr;
+    double* zb = nullptr;
+    double* g = nullptr;
+    double* q = nullptr;
+    int* fail = nullptr;
+};
+
 struct wmc_level {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -104,13 +115,25 @@ struct wmc_level {
     int* d_qdof = nullptr;
     double* d_qw = nullptr;
     double* d_qsm = nullptr;
-    // batch state
-    double* d_za = nullptr;
-    double* d_zb = nullptr;
-    double* d_g = nullptr;
+    // structured substep path
+    bool lattice = false;
+    int* d_strip_j0 = nullptr;
+    int* d_strip_len = nullptr;
+    int* d_cellx = nullptr;
+    int* d_celly = nullptr;
+    int* d_gen_rows = nullptr;
+    double* d_gen_rs = nullptr;
+    int* d_gen_soff = nullptr;
+    std::uint16_t* d_gen_col = nullptr;
+    int* d_slot_rc = nullptr;
+    int* d_grc_cell = nullptr;
+    double* d_grc_a0 = nullptr;
+    int n_slots = 0;
+    int lat_smem = 0;
+    int lat_grid = 0;
+    // batch state: ws[0] as the fine level of a pair, ws[1] as the coarse one
+    Workspace ws[2];
     double* d_cells = nullptr;
-    int* d_fail = nullptr;
-    double* d_q = nullptr;
     double* d_dq = nullptr;
     // optional per-kernel event timing (profiling pass only)
     bool profile = false;
@@ -120,9 +143,14 @@ struct wmc_level {
         cudaSetDevice(device);
         for (void* p : {(void*)d_row_ptr, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
                         (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
-                        (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_za, (void*)d_zb,
-                        (void*)d_g, (void*)d_cells, (void*)d_fail, (void*)d_q, (void*)d_dq})
+                        (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
+                        (void*)d_strip_j0, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
+                        (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_grc_cell,
+                        (void*)d_grc_a0})
             if (p) cudaFree(p);
+        for (auto& w : ws)
+            for (void* p : {(void*)w.za, (void*)w.zb, (void*)w.g, (void*)w.q, (void*)w.fail})
+                if (p) cudaFree(p);
         for (auto e : ev_sweep) cudaEventDestroy(e);
         for (auto e : ev_sub) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
@@ -201,17 +229,81 @@ void build_device_level(wmc_level& L) {
     L.d_qw = upload(t.qoi_w);
     L.d_qsm = upload(t.sqrt_mass_qoi);
 
-    const std::size_t S = static_cast<std::size_t>(L.batch);
-    auto alloc = [&](auto** p, std::size_t elems) {
-        check(cudaMalloc(p, sizeof(**p) * std::max<std::size_t>(elems, 1)), "cudaMalloc batch");
-    };
-    alloc(&L.d_za, S * t.n);
-    alloc(&L.d_zb, S * t.n);
-    alloc(&L.d_g, S * std::max(t.n_r, 1));
-    alloc(&L.d_cells, S * t.n_cells);
-    alloc(&L.d_fail, S);
-    alloc(&L.d_q, S);
-    alloc(&L.d_dq, S);
+    if (lts && t.lattice && static_cast<int>(t.gen_rows.size()) <= wmc::kLatThreads * wmc::kLatGen) {
+        // SELL-32 over the generic rows, per slot: column and recipe range
+        const int n_gen = static_cast<int>(t.gen_rows.size());
+        const int n_slices = (n_gen + 31) / 32;
+        std::vector<int> soff(n_slices + 1, 0), slot_rc{0}, rc_cell;
+        std::vector<std::uint16_t> gcol;
+        std::vector<double> rc_a0;
+        for (int sl = 0; sl < n_slices; ++sl) {
+            int width = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int q = sl * 32 + l;
+                if (q < n_gen) width = std::max(width, t.gen_ptr[q + 1] - t.gen_ptr[q]);
+            }
+            for (int e = 0; e < width; ++e)
+                for (int l = 0; l < 32; ++l) {
+                    const int q = sl * 32 + l;
+                    std::uint16_t c = 0;
+                    if (q < n_gen && e < t.gen_ptr[q + 1] - t.gen_ptr[q]) {
+                        const int ent = t.gen_ptr[q] + e;
+                        c = static_cast<std::uint16_t>(t.gen_col[ent]);
+                        for (int k = t.gen_rc_ptr[ent]; k < t.gen_rc_ptr[ent + 1]; ++k) {
+                            rc_cell.push_back(t.gen_rc_cell[k]);
+                            rc_a0.push_back(t.gen_rc_a0[k]);
+                        }
+                    }
+                    gcol.push_back(c);
+                    slot_rc.push_back(static_cast<int>(rc_cell.size()));
+                }
+            soff[sl + 1] = static_cast<int>(gcol.size());
+        }
+        L.n_slots = static_cast<int>(gcol.size());
+        L.d_strip_j0 = upload(t.strip_j0);
+        L.d_strip_len = upload(t.strip_len);
+        L.d_cellx = upload(t.lat_cellx);
+        L.d_celly = upload(t.lat_celly);
+        L.d_gen_rows = upload(t.gen_rows);
+        L.d_gen_rs = upload(t.gen_rs);
+        L.d_gen_soff = upload(soff);
+        L.d_gen_col = upload(gcol);
+        L.d_slot_rc = upload(slot_rc);
+        L.d_grc_cell = upload(rc_cell);
+        L.d_grc_a0 = upload(rc_a0);
+        wmc::LatArgs probe{};
+        probe.n_r = t.n_r;
+        probe.p = t.p;
+        probe.n_cells = t.n_cells;
+        probe.m = t.lat_m;
+        probe.n_strips = static_cast<int>(t.strip_j0.size());
+        probe.n_gen = n_gen;
+        probe.n_slots = L.n_slots;
+        L.lat_smem = wmc::lattice_smem_bytes(probe);
+        L.lat_grid = wmc::substep_max_grid(L.device, L.lat_smem);
+        L.lattice = L.lat_grid > 0;
+    }
+    L.d_cells = nullptr;
+    check(cudaMalloc(&L.d_cells, sizeof(double) * std::max<std::size_t>(static_cast<std::size_t>(L.batch) * t.n_cells, 1)),
+          "cudaMalloc batch");
+    check(cudaMalloc(&L.d_dq, sizeof(double) * std::max(L.batch, 1)), "cudaMalloc batch");
+}
+
+Workspace& workspace(wmc_level& L, int role) {
+    Workspace& w = L.ws[role];
+    if (!w.za) {
+        const std::size_t S = static_cast<std::size_t>(L.batch);
+        const wmc::LevelTables& t = L.tab;
+        auto alloc = [&](auto** p, std::size_t elems) {
+            check(cudaMalloc(p, sizeof(**p) * std::max<std::size_t>(elems, 1)), "cudaMalloc batch");
+        };
+        alloc(&w.za, S * t.n);
+        alloc(&w.zb, S * t.n);
+        alloc(&w.g, S * std::max(t.n_r, 1));
+        alloc(&w.fail, S);
+        alloc(&w.q, S);
+    }
+    return w;
 }
 
 // one batch of solves on level L with coefficients `cells` (stride S), result
@@ -225,10 +317,10 @@ cudaEvent_t mark(wmc_level& L, std::vector<cudaEvent_t>& v, cudaStream_t st) {
     return e;
 }
 
-void solve_batch(wmc_level& L, const double* cells, int S, int count, cudaStream_t stream) {
+void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
     const wmc::LevelTables& t = L.tab;
     const bool lts = t.kind == wmc::Integrator::LocalTimeStepping && t.n_r > 0;
-    wmc::launch_fill_int(L.d_fail, INT_MAX, S, stream);
+    wmc::launch_fill_int(ws.fail, INT_MAX, S, stream);
 
     wmc::SweepArgs sw{};
     sw.n = t.n;
@@ -239,16 +331,48 @@ void solve_batch(wmc_level& L, const double* cells, int S, int count, cudaStream
     sw.a0 = L.d_a0;
     sw.cells = cells;
     sw.z0 = L.d_z0;
-    sw.zp = L.d_zb;
-    sw.zc_out = L.d_za;
+    sw.zp = ws.zb;
+    sw.zc_out = ws.za;
     sw.factor = t.init_factor;
     sw.step = 1;
-    sw.fail = L.d_fail;
+    sw.fail = ws.fail;
     wmc::launch_sweep_init(sw, stream);
     g_launches += 2;
 
-    double* cur = L.d_za;
-    double* prev = L.d_zb;
+    double* cur = ws.za;
+    double* prev = ws.zb;
+    wmc::LatArgs la{};
+    if (lts && L.lattice) {
+        la.n_r = t.n_r;
+        la.S = S;
+        la.count = count;
+        la.p = t.p;
+        la.n_cells = t.n_cells;
+        la.cells_x = L.spec.cells_x;
+        la.m = t.lat_m;
+        la.cw = t.lat_cw;
+        la.n_strips = static_cast<int>(t.strip_j0.size());
+        la.n_gen = static_cast<int>(t.gen_rows.size());
+        la.n_slots = L.n_slots;
+        la.inv_h = t.lat_inv_h;
+        la.c0 = t.c0;
+        la.strip_j0 = L.d_strip_j0;
+        la.strip_len = L.d_strip_len;
+        la.cellx = L.d_cellx;
+        la.celly = L.d_celly;
+        la.gen_rows = L.d_gen_rows;
+        la.gen_rs = L.d_gen_rs;
+        la.gen_soff = L.d_gen_soff;
+        la.gen_col = L.d_gen_col;
+        la.slot_rc = L.d_slot_rc;
+        la.rc_cell = L.d_grc_cell;
+        la.rc_a0 = L.d_grc_a0;
+        la.cells = cells;
+        la.g = ws.g;
+        la.beta = L.d_beta;
+        la.cm = L.d_cm;
+        la.fail = ws.fail;
+    }
     wmc::SubArgs sb{};
     if (lts) {
         sb.n_r = t.n_r;
@@ -264,18 +388,18 @@ void solve_batch(wmc_level& L, const double* cells, int S, int count, cudaStream
         sb.rc_cell = L.d_rc_cell;
         sb.rc_a0 = L.d_rc_a0;
         sb.cells = cells;
-        sb.g = L.d_g;
+        sb.g = ws.g;
         sb.beta = L.d_beta;
         sb.cm = L.d_cm;
         sb.c0 = t.c0;
-        sb.fail = L.d_fail;
+        sb.fail = ws.fail;
     }
-    const int sub_grid = std::min(L.sub_grid, count);
+    const int sub_grid = std::min(L.lattice ? L.lat_grid : L.sub_grid, count);
     for (long s = 1; s < t.n_steps; ++s) {
         sw.zc = cur;
         sw.zp = prev;
         sw.zc_out = nullptr;
-        sw.g = L.d_g;
+        sw.g = ws.g;
         sw.split = lts ? t.n_r : 0;
         sw.factor = t.coarse_factor;
         sw.step = static_cast<int>(s + 1);
@@ -287,8 +411,12 @@ void solve_batch(wmc_level& L, const double* cells, int S, int count, cudaStream
             sb.zc = cur;
             sb.zp = prev;
             sb.step = static_cast<int>(s + 1);
+            la.zc = cur;
+            la.zp = prev;
+            la.step = static_cast<int>(s + 1);
             if (L.profile) mark(L, L.ev_sub, stream);
-            const int e = wmc::launch_substeps(sb, sub_grid, stream);
+            const int e = L.lattice ? wmc::launch_lattice_substeps(la, sub_grid, stream)
+                                    : wmc::launch_substeps(sb, sub_grid, stream);
             if (e != 0) check(static_cast<cudaError_t>(e), "substep launch");
             if (L.profile) mark(L, L.ev_sub, stream);
             ++g_launches;
@@ -303,8 +431,8 @@ void solve_batch(wmc_level& L, const double* cells, int S, int count, cudaStream
     qa.w = L.d_qw;
     qa.sqrt_mass = L.d_qsm;
     qa.z = cur;
-    qa.fail = L.d_fail;
-    qa.q = L.d_q;
+    qa.fail = ws.fail;
+    qa.q = ws.q;
     wmc::launch_qoi(qa, stream);
     ++g_launches;
     check(cudaGetLastError(), "kernel launch");
@@ -356,25 +484,28 @@ void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std
         wmc::launch_draw_cells(seed, level, first + off, c, S, fine->tab.n_cells, fine->spec.coef_lo,
                                fine->spec.coef_hi, fine->d_cells, st);
         g_launches += 2;  // draw + pair difference
-        solve_batch(*fine, fine->d_cells, S, c, st);
-        if (coarse) solve_batch(*coarse, fine->d_cells, S, c, st);
+        Workspace& wf = workspace(*fine, 0);
+        solve_batch(*fine, wf, fine->d_cells, S, c, st);
+        Workspace* wc = nullptr;
+        if (coarse) {
+            wc = &workspace(*coarse, 1);
+            solve_batch(*coarse, *wc, fine->d_cells, S, c, st);
+        }
         double* dq_dst = dev_dq ? dev_dq + off : fine->d_dq;
-        wmc::launch_pair_diff(fine->d_q, coarse ? coarse->d_q : nullptr, dq_dst, c, st);
-        if (dev_qf) check(cudaMemcpyAsync(dev_qf + off, fine->d_q, sizeof(double) * c, cudaMemcpyDeviceToDevice, st),
+        wmc::launch_pair_diff(wf.q, wc ? wc->q : nullptr, dq_dst, c, st);
+        if (dev_qf) check(cudaMemcpyAsync(dev_qf + off, wf.q, sizeof(double) * c, cudaMemcpyDeviceToDevice, st),
                           "copy q");
         if (host_dq || host_qf || err) {
             ff.resize(c);
-            check(cudaMemcpyAsync(ff.data(), fine->d_fail, sizeof(int) * c, cudaMemcpyDeviceToHost, st), "fail");
-            if (coarse) {
+            check(cudaMemcpyAsync(ff.data(), wf.fail, sizeof(int) * c, cudaMemcpyDeviceToHost, st), "fail");
+            if (wc) {
                 fc.resize(c);
-                check(cudaMemcpyAsync(fc.data(), coarse->d_fail, sizeof(int) * c, cudaMemcpyDeviceToHost, st),
-                      "fail");
+                check(cudaMemcpyAsync(fc.data(), wc->fail, sizeof(int) * c, cudaMemcpyDeviceToHost, st), "fail");
             }
             if (host_dq)
                 check(cudaMemcpyAsync(host_dq + off, dq_dst, sizeof(double) * c, cudaMemcpyDeviceToHost, st), "dq");
             if (host_qf)
-                check(cudaMemcpyAsync(host_qf + off, fine->d_q, sizeof(double) * c, cudaMemcpyDeviceToHost, st),
-                      "q");
+                check(cudaMemcpyAsync(host_qf + off, wf.q, sizeof(double) * c, cudaMemcpyDeviceToHost, st), "q");
             check(cudaStreamSynchronize(st), "synchronize");
             for (int i = 0; i < c; ++i) {
                 const bool bad_f = ff[i] != INT_MAX, bad_c = coarse && fc[i] != INT_MAX;
@@ -483,7 +614,8 @@ wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     return s;
 }
 
-void fill_info(const wmc::LevelTables& t, int batch, wmc_level_info* info) {
+void fill_info(const wmc::LevelTables& t, int batch, bool lattice, wmc_level_info* info) {
+    info->lattice = lattice ? 1 : 0;
     info->n = t.n;
     info->n_r = t.n_r;
     info->n_p = t.n_p;
@@ -517,7 +649,7 @@ int wmc_mesh_build_square(const wmc_square_mesh_spec* spec, wmc_mesh** out) {
         s.fine_lo = spec->fine_lo;
         s.fine_hi = spec->fine_hi;
         s.snap = spec->snap;
-        s.small_factor = spec->small_factor > 0.0 ? spec->small_factor : 0.7;
+        s.small_factor = spec->small_factor;
         auto m = std::make_unique<wmc_mesh>();
         m->mesh = wmc::build_refined_square(s);
         *out = m.release();
@@ -635,14 +767,14 @@ int wmc_level_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level_i
     return guarded([&] {
         if (!mesh || !desc || !info) throw ConfigError("wmc_level_plan: NULL argument");
         const wmc::LevelTables t = wmc::build_level_tables(mesh->mesh, spec_from_desc(desc));
-        fill_info(t, 0, info);
+        fill_info(t, 0, t.lattice, info);
     });
 }
 
 int wmc_level_get_info(const wmc_level* L, wmc_level_info* info) {
     return guarded([&] {
         if (!L || !info) throw ConfigError("wmc_level_get_info: NULL argument");
-        fill_info(L->tab, L->batch, info);
+        fill_info(L->tab, L->batch, L->lattice, info);
     });
 }
 

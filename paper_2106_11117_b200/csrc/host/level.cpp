@@ -51,6 +51,111 @@ int cell_of(double x, double y, int nx, int ny) {
     return iy * nx + ix;
 }
 
+constexpr int kLatticeThreads = 512;  // threads of the lattice substep kernel
+constexpr int kLatticeStrip = 8;      // max rows per thread
+
+using StiffMap = std::map<std::tuple<int, int, int>, double>;
+
+// Finds the structured block of the refined square and checks, numerically
+// against the assembled element stiffness, that every node of L = [1, m-1]^2
+// has the 5-point lattice stencil with edge conductances (c_a + c_b) / 2 and
+// lumped mass h^2.  Fills the lattice fields of L and returns the box
+// vertices in (j, i) order, or an empty vector (with lattice_reason) when the
+// fast path does not apply.
+std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const std::vector<double>& mass,
+                               const StiffMap& stiff, const std::vector<std::uint8_t>& in_r, LevelTables& L) {
+    auto fail = [&](const std::string& why) {
+        L.lattice = false;
+        L.lattice_reason = why;
+        return std::vector<int>{};
+    };
+    if (mesh.fine_box_lo < 0 || mesh.lattice.size() != mesh.vertices.size()) return fail("no refined box");
+    const int qa = mesh.fine_box_lo, m = mesh.fine_box_hi - mesh.fine_box_lo;
+    if (m < 4) return fail("refined box too small");
+    const double h = mesh.fine_h;
+    std::map<std::pair<int, int>, int> at;
+    for (int v = 0; v < mesh.n_vertices(); ++v) at[{mesh.lattice[v][0], mesh.lattice[v][1]}] = v;
+    std::vector<int> box;
+    box.reserve(static_cast<std::size_t>(m + 1) * (m + 1));
+    for (int j = 0; j <= m; ++j)
+        for (int i = 0; i <= m; ++i) {
+            const auto it = at.find({qa + i, qa + j});
+            if (it == at.end()) return fail("box node missing");
+            if (mesh.boundary_vertex[it->second] || !in_r[it->second]) return fail("box node not in R");
+            box.push_back(it->second);
+        }
+    std::vector<int> cx(m), cy(m);
+    for (int i = 0; i < m; ++i) {
+        const double x = (qa + i + 0.5) * h;
+        cx[i] = cell_of(x, 0.5, spec.cells_x, 1);
+        cy[i] = cell_of(0.5, x, 1, spec.cells_y);
+    }
+    // distinct test coefficients per cell
+    const int nc = spec.cells_x * spec.cells_y;
+    std::vector<double> ct(nc);
+    for (int k = 0; k < nc; ++k) ct[k] = 1.0 + 0.371 * k + 0.013 * k * k;
+    auto csq = [&](int i, int j) { return ct[cy[j] * spec.cells_x + cx[i]]; };
+    for (int j = 1; j <= m - 1; ++j)
+        for (int i = 1; i <= m - 1; ++i) {
+            const int v = box[j * (m + 1) + i];
+            if (std::abs(mass[v] - h * h) > 1e-12 * h * h) return fail("lumped mass != h^2 in L");
+            const int nb[4] = {box[j * (m + 1) + i + 1], box[j * (m + 1) + i - 1], box[(j + 1) * (m + 1) + i],
+                               box[(j - 1) * (m + 1) + i]};
+            const double kap[4] = {0.5 * (csq(i, j) + csq(i, j - 1)), 0.5 * (csq(i - 1, j) + csq(i - 1, j - 1)),
+                                   0.5 * (csq(i - 1, j) + csq(i, j)), 0.5 * (csq(i - 1, j - 1) + csq(i, j - 1))};
+            double want_diag = 0.0, got_diag = 0.0;
+            double got[4] = {0.0, 0.0, 0.0, 0.0};
+            int others = 0;
+            for (auto it = stiff.lower_bound({v, -1, -1}); it != stiff.end() && std::get<0>(it->first) == v; ++it) {
+                const int u = std::get<1>(it->first);
+                const double val = it->second * ct[std::get<2>(it->first)];
+                if (it->second == 0.0) continue;
+                if (u == v) {
+                    got_diag += val;
+                    continue;
+                }
+                int d = 0;
+                while (d < 4 && nb[d] != u) ++d;
+                if (d == 4) {
+                    ++others;
+                    continue;
+                }
+                got[d] += val;
+            }
+            if (others) return fail("non 5-point stencil in L");
+            for (int d = 0; d < 4; ++d) {
+                want_diag += kap[d];
+                if (std::abs(got[d] + kap[d]) > 1e-12 * kap[d]) return fail("edge conductance mismatch in L");
+            }
+            if (std::abs(got_diag - want_diag) > 1e-12 * want_diag) return fail("diagonal mismatch in L");
+        }
+    // row strips: every coefficient line (celly changes between squares j-1
+    // and j) starts a strip, so the rows after a strip's first share one
+    // coefficient row
+    std::vector<int> j0s, lens;
+    int start = 1;
+    for (int j = 2; j <= m; ++j) {
+        if (j == m || cy[j] != cy[j - 1]) {
+            for (int a = start; a < j; a += kLatticeStrip) {
+                j0s.push_back(a);
+                lens.push_back(std::min(kLatticeStrip, j - a));
+            }
+            start = j;
+        }
+    }
+    const int cw = (m - 1 + 31) / 32 * 32;
+    if (static_cast<int>(j0s.size()) * cw > kLatticeThreads) return fail("too many strips for the CTA");
+    L.lattice = true;
+    L.lat_m = m;
+    L.lat_inv_h = 1.0 / h;
+    L.lat_cellx = cx;
+    L.lat_celly = cy;
+    L.strip_j0 = j0s;
+    L.strip_len = lens;
+    L.lat_cw = cw;
+    return box;
+}
+
 }  // namespace
 
 LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
@@ -66,7 +171,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
 
     // lumped mass and element stiffness by cell (fem.cpp:91-116)
     std::vector<double> mass(nv, 0.0);
-    std::map<std::tuple<int, int, int>, double> stiff;  // (vi, vj, cell) -> sum area*grad.grad
+    StiffMap stiff;  // (vi, vj, cell) -> sum area*grad.grad
     L.elem_cell.resize(nt);
     for (int t = 0; t < nt; ++t) {
         const auto& tri = mesh.triangles[t];
@@ -107,11 +212,22 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         if (s != 0.0 && sel[vj]) in_r[vi] = 1;
     }
 
-    // dof order: R rows first, then the rest, each in mesh vertex order
+    // structured lattice block (substep fast path), decided in vertex space
+    std::vector<int> box_vertex;  // (m+1)^2 box nodes in (j, i) order, or empty
+    if (spec.kind == Integrator::LocalTimeStepping)
+        box_vertex = lattice_block(mesh, spec, mass, stiff, in_r, L);
+
+    // dof order: the lattice box (row-major), the other R rows, then the
+    // rest, each in mesh vertex order
     std::vector<int> vdof(nv, -1);
+    for (int v : box_vertex) {
+        vdof[v] = static_cast<int>(L.dof_vertex.size());
+        L.dof_vertex.push_back(v);
+        ++L.n_r;
+    }
     for (int pass = 0; pass < 2; ++pass)
         for (int v = 0; v < nv; ++v) {
-            if (mesh.boundary_vertex[v]) continue;
+            if (mesh.boundary_vertex[v] || vdof[v] >= 0) continue;
             if ((pass == 0) != (in_r[v] != 0)) continue;
             vdof[v] = static_cast<int>(L.dof_vertex.size());
             L.dof_vertex.push_back(v);
@@ -174,6 +290,32 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
             L.ap_wid.push_back(wid);
         }
         L.ap_row_ptr[i + 1] = static_cast<int>(L.ap_col.size());
+    }
+    if (L.lattice) {
+        const int W = L.lat_m + 1;
+        L.gen_ptr.push_back(0);
+        L.gen_rc_ptr.push_back(0);
+        for (int i = 0; i < L.n_r; ++i) {
+            const int bi = i % W, bj = i / W;
+            if (i < W * W && bi >= 1 && bi <= L.lat_m - 1 && bj >= 1 && bj <= L.lat_m - 1) continue;  // in L
+            L.gen_rows.push_back(i);
+            L.gen_rs.push_back(1.0 / std::sqrt(L.mass[i]));
+            const auto& r = rows[i];
+            for (std::size_t e = 0; e < r.size();) {
+                const int j = std::get<0>(r[e]);
+                const std::size_t e0 = e;
+                while (e < r.size() && std::get<0>(r[e]) == j) ++e;
+                if (!L.in_p[j]) continue;
+                L.gen_col.push_back(j);
+                const double sq = std::sqrt(L.mass[j]);
+                for (std::size_t t = e0; t < e; ++t) {
+                    L.gen_rc_cell.push_back(std::get<1>(r[t]));
+                    L.gen_rc_a0.push_back(std::get<2>(r[t]) * sq);
+                }
+                L.gen_rc_ptr.push_back(static_cast<int>(L.gen_rc_cell.size()));
+            }
+            L.gen_ptr.push_back(static_cast<int>(L.gen_col.size()));
+        }
     }
     L.rc_ptr.assign(recipes.size() + 1, 0);
     for (std::size_t w = 0; w < recipes.size(); ++w) {

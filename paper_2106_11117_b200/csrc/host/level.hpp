@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "mesh.hpp"
@@ -84,6 +85,25 @@ struct LevelTables {
     std::vector<double> sqrt_mass_qoi;  // sqrt(M_i) for qoi_dof
 
     std::vector<int> elem_cell;     // per triangle (diagnostics)
+
+    // Structured block of the refined square for the substep fast path.  The
+    // box has (m+1)^2 lattice nodes with dof = j*(m+1) + i (Q-local i, j);
+    // L = [1, m-1]^2 are nodes whose six triangles are h_min lattice
+    // triangles, so (A d)_i = (1/h) sum_dir kappa_dir (v_i - v_dir) with
+    // v = d / sqrt(M) and kappa = mean coefficient of the two triangles on an
+    // edge; every other R row ("generic") keeps explicit per-entry recipes.
+    bool lattice = false;
+    int lat_m = 0;
+    double lat_inv_h = 0.0;
+    std::vector<int> lat_cellx, lat_celly;  // coefficient column / row of square column i / row j
+    std::vector<int> strip_j0, strip_len;   // row strips of L (coefficient lines start a strip)
+    int lat_cw = 0;                         // threads per strip row (columns, rounded up to 32)
+    std::string lattice_reason;             // why the fast path is off (diagnostics)
+    std::vector<int> gen_rows;              // generic R rows (dofs)
+    std::vector<double> gen_rs;             // 1/sqrt(M) of each generic row
+    std::vector<int> gen_ptr, gen_col;      // CSR over gen_rows, columns in P
+    std::vector<int> gen_rc_ptr, gen_rc_cell;  // per entry: terms of w = sum c_k a0_k sqrt(M_j)
+    std::vector<double> gen_rc_a0;
 
     // time stepping
     long n_steps = 0;

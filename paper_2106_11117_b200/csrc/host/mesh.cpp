@@ -227,6 +227,10 @@ TriMesh build_refined_square(const SquareMeshSpec& spec) {
     TriMesh mesh;
     mesh.coarse_h = 1.0 / static_cast<double>(n);
     mesh.fine_h = mesh.coarse_h / static_cast<double>(R);
+    if (R > 1 && qb > qa) {
+        mesh.fine_box_lo = static_cast<int>(qa);
+        mesh.fine_box_hi = static_cast<int>(qb);
+    }
     const double unit = mesh.fine_h;
     mesh.vertices.resize(lat.size());
     mesh.lattice.resize(lat.size());

@@ -24,6 +24,7 @@ struct TriMesh {
     std::vector<std::uint8_t> fine_flags;       // per triangle
     std::vector<std::uint8_t> boundary_vertex;  // per vertex (Dirichlet)
     std::vector<std::array<int, 2>> lattice;    // integer lattice coordinates (units of fine_h)
+    int fine_box_lo = -1, fine_box_hi = -1;     // refined square [lo, hi]^2 in lattice units (-1: none)
     double coarse_h = 0.0;
     double fine_h = 0.0;
 

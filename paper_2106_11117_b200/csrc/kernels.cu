@@ -249,6 +249,234 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
     (void)n_slices;
 }
 
+
+// ---------------------------------------------------------------------------
+// K2 (structured): the p LTS substeps on R with the refined-square lattice
+// as a register-blocked 5-point stencil.  Thread t owns column i = 1 + t % cw
+// of strip t / cw (<= kLatStrip consecutive rows of L = [1, m-1]^2), keeping
+// d_m, d_{m-1}, g and v = d / h of its nodes in registers; N/S neighbours
+// inside the strip come from registers, E/W and the strip ends from the
+// shared-memory copy of v (double-buffered, one barrier per substep).
+// Edge conductances kappa = (c_a + c_b)/2 come from the sample's cell
+// coefficients; a coefficient line always starts a strip, so a thread needs
+// one set of constants for its first row and one for the rest.
+// Generic rows (box ring + transition belt) use a SELL of per-sample
+// weights w_ij = A_ij(omega) sqrt(M_j) acting on v.
+
+struct LatSmem {
+    double* v0;
+    double* v1;
+    double* gw;
+    double* cl;
+    double* beta;
+    double* cm;
+    std::uint16_t* gcol;
+    int* gsoff;
+    int* sj0;
+    int* slen;
+    int* cx;
+    int* cy;
+};
+
+__host__ __device__ inline std::size_t lat_layout(const LatArgs& a, char* base, LatSmem* s) {
+    const int n_slices = (a.n_gen + 31) / 32;
+    std::size_t off = 0;
+    auto take = [&](std::size_t bytes) {
+        const std::size_t o = off;
+        off = align16(off + bytes);
+        return o;
+    };
+    const std::size_t o0 = take(sizeof(double) * a.n_r);
+    const std::size_t o1 = take(sizeof(double) * a.n_r);
+    const std::size_t ow = take(sizeof(double) * (a.n_slots > 0 ? a.n_slots : 1));
+    const std::size_t ol = take(sizeof(double) * a.n_cells);
+    const std::size_t ob = take(sizeof(double) * (a.p > 1 ? a.p - 1 : 1));
+    const std::size_t oc = take(sizeof(double) * (a.p > 1 ? a.p - 1 : 1));
+    const std::size_t og = take(sizeof(std::uint16_t) * (a.n_slots > 0 ? a.n_slots : 1));
+    const std::size_t os = take(sizeof(int) * (n_slices + 1));
+    const std::size_t oj = take(sizeof(int) * a.n_strips);
+    const std::size_t olen = take(sizeof(int) * a.n_strips);
+    const std::size_t ox = take(sizeof(int) * a.m);
+    const std::size_t oy = take(sizeof(int) * a.m);
+    if (s) {
+        s->v0 = reinterpret_cast<double*>(base + o0);
+        s->v1 = reinterpret_cast<double*>(base + o1);
+        s->gw = reinterpret_cast<double*>(base + ow);
+        s->cl = reinterpret_cast<double*>(base + ol);
+        s->beta = reinterpret_cast<double*>(base + ob);
+        s->cm = reinterpret_cast<double*>(base + oc);
+        s->gcol = reinterpret_cast<std::uint16_t*>(base + og);
+        s->gsoff = reinterpret_cast<int*>(base + os);
+        s->sj0 = reinterpret_cast<int*>(base + oj);
+        s->slen = reinterpret_cast<int*>(base + olen);
+        s->cx = reinterpret_cast<int*>(base + ox);
+        s->cy = reinterpret_cast<int*>(base + oy);
+    }
+    return off;
+}
+
+__global__ void __launch_bounds__(kLatThreads, 1) lattice_substep_kernel(LatArgs a) {
+    extern __shared__ __align__(16) char smem[];
+    LatSmem sm;
+    lat_layout(a, smem, &sm);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int n_slices = (a.n_gen + 31) / 32;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const int W = a.m + 1;
+
+    for (int i = tid; i < a.n_slots; i += kLatThreads) sm.gcol[i] = __ldg(a.gen_col + i);
+    for (int i = tid; i <= n_slices; i += kLatThreads) sm.gsoff[i] = __ldg(a.gen_soff + i);
+    for (int i = tid; i < a.n_strips; i += kLatThreads) {
+        sm.sj0[i] = __ldg(a.strip_j0 + i);
+        sm.slen[i] = __ldg(a.strip_len + i);
+    }
+    for (int i = tid; i < a.m; i += kLatThreads) {
+        sm.cx[i] = __ldg(a.cellx + i);
+        sm.cy[i] = __ldg(a.celly + i);
+    }
+    for (int i = tid; i < a.p - 1; i += kLatThreads) {
+        sm.beta[i] = __ldg(a.beta + i);
+        sm.cm[i] = __ldg(a.cm + i);
+    }
+
+    // structured role
+    const int col = tid % a.cw, strip = tid / a.cw;
+    const int ci = 1 + col;
+    const bool lat_on = ci <= a.m - 1 && strip < a.n_strips;
+    // generic role
+    int gq[kLatGen];
+#pragma unroll
+    for (int u = 0; u < kLatGen; ++u) gq[u] = tid + u * kLatThreads;
+
+    for (int s = blockIdx.x; s < a.count; s += gridDim.x) {
+        __syncthreads();
+        for (int k = tid; k < a.n_cells; k += kLatThreads) sm.cl[k] = __ldg(a.cells + k * S + s);
+        __syncthreads();
+        for (int e = tid; e < a.n_slots; e += kLatThreads) {
+            double acc = 0.0;
+            for (int t = __ldg(a.slot_rc + e); t < __ldg(a.slot_rc + e + 1); ++t)
+                acc += sm.cl[__ldg(a.rc_cell + t)] * __ldg(a.rc_a0 + t);
+            sm.gw[e] = acc;
+        }
+
+        // lattice constants of this thread (scaled by 1/h: v = d/h)
+        int j0 = 1, len = 0;
+        double kE0 = 0, kW0 = 0, kN0 = 0, kS0 = 0, dg0 = 0, kE = 0, kW = 0, kNS = 0, dg = 0;
+        double d[kLatStrip], dp[kLatStrip], gg[kLatStrip];
+        if (lat_on) {
+            j0 = sm.sj0[strip];
+            len = sm.slen[strip];
+            const int rowu = sm.cy[j0] * a.cells_x, rowd = sm.cy[j0 - 1] * a.cells_x;
+            const double cRu = sm.cl[rowu + sm.cx[ci]], cRd = sm.cl[rowd + sm.cx[ci]];
+            const double cLu = sm.cl[rowu + sm.cx[ci - 1]], cLd = sm.cl[rowd + sm.cx[ci - 1]];
+            const double f = 0.5 * a.inv_h;
+            kE0 = (cRu + cRd) * f;
+            kW0 = (cLu + cLd) * f;
+            kN0 = (cLu + cRu) * f;
+            kS0 = (cLd + cRd) * f;
+            dg0 = kE0 + kW0 + kN0 + kS0;
+            kE = cRu * a.inv_h;
+            kW = cLu * a.inv_h;
+            kNS = (cLu + cRu) * f;
+            dg = kE + kW + 2.0 * kNS;
+        }
+#pragma unroll
+        for (int k = 0; k < kLatStrip; ++k) {
+            d[k] = 0.0;
+            dp[k] = 0.0;
+            gg[k] = 0.0;
+            if (k < len) {
+                const int dof = (j0 + k) * W + ci;
+                gg[k] = __ldg(a.g + dof * S + s);
+                d[k] = -a.c0 * gg[k];
+                sm.v0[dof] = d[k] * a.inv_h;
+            }
+        }
+        double gd[kLatGen], gdp[kLatGen], ggg[kLatGen], grs[kLatGen];
+        int grow[kLatGen];
+#pragma unroll
+        for (int u = 0; u < kLatGen; ++u) {
+            gd[u] = gdp[u] = ggg[u] = grs[u] = 0.0;
+            grow[u] = -1;
+            if (gq[u] < a.n_gen) {
+                grow[u] = __ldg(a.gen_rows + gq[u]);
+                grs[u] = __ldg(a.gen_rs + gq[u]);
+                ggg[u] = __ldg(a.g + grow[u] * S + s);
+                gd[u] = -a.c0 * ggg[u];
+                sm.v0[grow[u]] = gd[u] * grs[u];
+            }
+        }
+        __syncthreads();
+
+        for (int m = 1; m <= a.p - 1; ++m) {
+            const double* cur = (m & 1) ? sm.v0 : sm.v1;
+            double* nxt = (m & 1) ? sm.v1 : sm.v0;
+            const double beta = sm.beta[m - 1];
+            const double cmm = sm.cm[m - 1];
+            const double onepb = 1.0 + beta;
+            if (len > 0) {
+                const int base = j0 * W + ci;
+                double vs = cur[base - W];  // south neighbour of the first row (old)
+                double vk = d[0] * a.inv_h;  // old v of the current node
+#pragma unroll
+                for (int k = 0; k < kLatStrip; ++k) {
+                    if (k < len) {
+                        const int dof = base + k * W;
+                        const double vn = (k + 1 < len) ? d[k + 1] * a.inv_h : cur[dof + W];
+                        const double ve = cur[dof + 1], vw = cur[dof - 1];
+                        double aq;
+                        if (k == 0)
+                            aq = dg0 * vk - kE0 * ve - kW0 * vw - kN0 * vn - kS0 * vs;
+                        else
+                            aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
+                        const double next = onepb * d[k] - beta * dp[k] - cmm * (gg[k] + aq);
+                        dp[k] = d[k];
+                        d[k] = next;
+                        nxt[dof] = next * a.inv_h;
+                        vs = vk;
+                        vk = vn;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kLatGen; ++u) {
+                if (grow[u] >= 0) {
+                    const int slice = gq[u] >> 5;
+                    const int b = sm.gsoff[slice], e = sm.gsoff[slice + 1];
+                    double aq = 0.0;
+                    for (int q = b + lane; q < e; q += 32) aq += sm.gw[q] * cur[sm.gcol[q]];
+                    const double next = onepb * gd[u] - beta * gdp[u] - cmm * (ggg[u] + aq);
+                    gdp[u] = gd[u];
+                    gd[u] = next;
+                    nxt[grow[u]] = next * grs[u];
+                }
+            }
+            __syncthreads();
+        }
+
+        // z_{n+1} = 2 z_n - z_{n-1} + 2 d_p
+#pragma unroll
+        for (int k = 0; k < kLatStrip; ++k) {
+            if (k < len) {
+                const std::size_t idx = static_cast<std::size_t>((j0 + k) * W + ci) * S + s;
+                const double out = 2.0 * a.zc[idx] - a.zp[idx] + 2.0 * d[k];
+                a.zp[idx] = out;
+                if (!(fabs(out) <= 1e100)) atomicMin(a.fail + s, a.step);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kLatGen; ++u) {
+            if (grow[u] >= 0) {
+                const std::size_t idx = static_cast<std::size_t>(grow[u]) * S + s;
+                const double out = 2.0 * a.zc[idx] - a.zp[idx] + 2.0 * gd[u];
+                a.zp[idx] = out;
+                if (!(fabs(out) <= 1e100)) atomicMin(a.fail + s, a.step);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: QoI per sample, Q = sum_t w_t (z_t / sqrt(M_t)) over the box nodes in a
 // fixed order (deterministic); failed samples report NaN.
@@ -374,6 +602,18 @@ int launch_substeps(const SubArgs& a, int grid, void* stream) {
         case 8: return launch_sub_rpt<8>(a, grid, smem, st);
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
+}
+
+int lattice_smem_bytes(const LatArgs& a) { return static_cast<int>(lat_layout(a, nullptr, nullptr)); }
+
+int launch_lattice_substeps(const LatArgs& a, int grid, void* stream) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(lattice_substep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        configured = true;
+    }
+    lattice_substep_kernel<<<grid, kLatThreads, lattice_smem_bytes(a), static_cast<cudaStream_t>(stream)>>>(a);
+    return static_cast<int>(cudaGetLastError());
 }
 
 int substep_max_grid(int device, int smem_bytes) {

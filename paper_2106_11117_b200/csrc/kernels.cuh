@@ -55,6 +55,39 @@ struct SubArgs {
     int* fail;
 };
 
+constexpr int kLatThreads = 512;  // lattice substep kernel
+constexpr int kLatStrip = 8;      // rows per thread (max)
+constexpr int kLatGen = 2;        // generic rows per thread (max)
+
+// Substep kernel with the structured fast path: the refined-square lattice
+// L = [1, m-1]^2 (5-point stencil from cell coefficients, state v = d / h)
+// plus generic rows from a per-sample weighted SELL; see kernels.cu.
+struct LatArgs {
+    int n_r, S, count, p, n_cells, cells_x;
+    int m, cw, n_strips;
+    int n_gen, n_slots;
+    double inv_h, c0;
+    const int* strip_j0;
+    const int* strip_len;
+    const int* cellx;            // m entries
+    const int* celly;            // m entries
+    const int* gen_rows;         // n_gen dofs
+    const double* gen_rs;        // 1/sqrt(M)
+    const int* gen_soff;         // slice offsets (slots), ceil(n_gen/32)+1
+    const std::uint16_t* gen_col;  // per slot
+    const int* slot_rc;          // per slot: term range [slot_rc[e], slot_rc[e+1])
+    const int* rc_cell;
+    const double* rc_a0;
+    const double* cells;
+    const double* g;
+    const double* zc;
+    double* zp;
+    const double* beta;
+    const double* cm;
+    int step;
+    int* fail;
+};
+
 struct QoIArgs {
     int nq, S, count;
     const int* dof;
@@ -75,6 +108,8 @@ void launch_qoi(const QoIArgs& a, void* stream);
 void launch_fill_int(int* p, int value, int n, void* stream);
 void launch_pair_diff(const double* qf, const double* qc, double* dq, int count, void* stream);
 int substep_max_grid(int device, int smem_bytes);
+int lattice_smem_bytes(const LatArgs& a);
+int launch_lattice_substeps(const LatArgs& a, int grid, void* stream);  // returns cudaError_t
 // deterministic single-block fold of (dq, q) into out[0..3] += {sum dq, sum dq^2, sum q, sum q^2}
 void launch_moments(const double* dq, const double* q, int count, double* out, void* stream);
 

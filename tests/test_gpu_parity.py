@@ -169,6 +169,38 @@ def test_config_errors_are_reported():
         wavemc.Level(configs.build_mesh(configs.config0()), wavemc.LevelSpec(dt=-1.0))
 
 
+def test_lattice_and_generic_substep_kernels_agree():
+    """The structured refined-square kernel against the generic SELL kernel on
+    the same mesh (a mesh passed as arrays carries no lattice block)."""
+    for d in (configs.config0(), configs.config1()[0], configs.config1()[2]):
+        m = configs.build_mesh(d)
+        lat = wavemc.Level(m, configs.level_spec(d))
+        gen = wavemc.Level(wavemc.Mesh.from_arrays(*m.arrays()), configs.level_spec(d))
+        assert lat.info["lattice"] == 1 and gen.info["lattice"] == 0
+        _, a, _ = wavemc.eval_pairs(lat, None, 0, 1, 0, 40)
+        _, b, _ = wavemc.eval_pairs(gen, None, 0, 1, 0, 40)
+        assert per_sample_rel(a, b) < QOI_RTOL
+
+
+def test_concurrent_levels_use_separate_workspaces():
+    """Pairs of adjacent levels issued back to back on their own streams share
+    the middle level (fine of one pair, coarse of the next)."""
+    import torch
+    levels = [configs.build_level(d, batch=256) for d in configs.config1()[:3]]
+    n = 300
+    ref = [wavemc.eval_pairs(levels[l], levels[l - 1] if l else None, 0, l, 0, n) for l in range(3)]
+    d_dq = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(3)]
+    d_qf = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(3)]
+    for l in range(3):
+        wavemc.eval_pairs_device(levels[l], levels[l - 1] if l else None, 0, l, 0, n, d_dq[l].data_ptr(),
+                                 d_qf[l].data_ptr())
+    for lv in levels:
+        wavemc.synchronize(lv)
+    for l in range(3):
+        assert np.array_equal(d_dq[l].cpu().numpy(), ref[l][0]), l
+        assert np.array_equal(d_qf[l].cpu().numpy(), ref[l][1]), l
+
+
 def test_config1_level0_full_batch_spot_checks(coracle):
     """Full-size run (65536 samples of config 1 level 0): spot indices against
     the C oracle, and the batch result is independent of the index range."""

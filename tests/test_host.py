@@ -115,4 +115,5 @@ def test_mesh_round_trip_through_arrays():
     assert np.array_equal(fine, fine2) and np.array_equal(boundary, b2)
     a = wavemc.level_plan(m, configs.level_spec(configs.config0()))
     b = wavemc.level_plan(m2, configs.level_spec(configs.config0()))
+    assert a.pop("lattice") == 1 and b.pop("lattice") == 0  # arrays carry no refined-box metadata
     assert a == b
