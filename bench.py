@@ -227,7 +227,7 @@ def b200_arm(args, world, rank, local):
     streams = [torch.cuda.ExternalStream(lv.stream, device=dev) for lv in levels]
     main = torch.cuda.current_stream(dev)
 
-    def step_device():
+    def step_device(sequential=False):
         d_mom.zero_()
         ev0 = torch.cuda.Event()
         ev0.record(main)
@@ -239,6 +239,8 @@ def b200_arm(args, world, rank, local):
                                      d_dq[l].data_ptr(), d_qf[l].data_ptr())
             wavemc.moments_device(lv, d_dq[l].data_ptr(), d_qf[l].data_ptr(), counts[l],
                                   d_mom.data_ptr() + 8 * 4 * l)
+            if sequential:  # profiling: kernels of one level at a time
+                wavemc.synchronize(lv)
         for l in range(len(levels)):
             e = torch.cuda.Event()
             e.record(streams[l])
@@ -306,7 +308,7 @@ def b200_arm(args, world, rank, local):
     if not args.no_profile:
         for lv in levels:
             wavemc.profile_enable(lv, True)
-        step_device()
+        step_device(sequential=True)
         torch.cuda.synchronize(dev)
         prof = []
         for lv in levels:
@@ -366,6 +368,7 @@ def roofline_from_profile(levels, counts, prof, step_ms):
     (g, z_n, z_{n-1} in, z_{n+1} out) plus its on-chip FP64 work."""
     sweep_ms = sum(p["sweep_ms"] for p in prof)
     sub_ms = sum(p["sub_ms"] for p in prof)
+    upd_ms = sum(p["upd_ms"] for p in prof)
     sweep_bytes = 0.0
     sub_bytes = 0.0
     sub_flops = 0.0
@@ -386,7 +389,9 @@ def roofline_from_profile(levels, counts, prof, step_ms):
                            "share_of_step": sub_ms / step_ms if step_ms else None,
                            "fp64_TFLOPs": sub_flops / (sub_ms * 1e-3) / 1e12 if sub_ms else None,
                            "substep_dof_updates_per_s": sub_updates / (sub_ms * 1e-3) if sub_ms else None,
-                           "hbm_GBps": sub_bytes / (sub_ms * 1e-3) / 1e9 if sub_ms else None}}
+                           "hbm_GBps": sub_bytes / (sub_ms * 1e-3) / 1e9 if sub_ms else None},
+               "r_update": {"ms": upd_ms, "launches": sum(p["upd_launches"] for p in prof),
+                            "share_of_step": upd_ms / step_ms if step_ms else None}}
     roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",
             "traffic": None,
             "note": ("HBM roofline of the sweep kernel (algorithmic bytes); the substep kernel is on-chip "

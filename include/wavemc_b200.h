@@ -194,11 +194,12 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
  * over count device values, one fixed-order block (deterministic). */
 int wmc_moments_device(wmc_level* level, const double* d_dq, const double* d_q, uint64_t count, double* d_out);
 
-/* Kernel-level timing: with profiling on, every sweep and substep launch of
- * the level is bracketed by CUDA events on its stream; read returns the summed
- * device time and launch counts and resets. */
+/* Kernel-level timing: with profiling on, every sweep, substep and R-update
+ * launch of the level is bracketed by CUDA events on its stream; read
+ * returns the summed device time and launch counts and resets. */
 int wmc_profile_enable(wmc_level* level, int on);
-int wmc_profile_read(wmc_level* level, double* sweep_ms, long* sweep_launches, double* sub_ms, long* sub_launches);
+int wmc_profile_read(wmc_level* level, double* sweep_ms, long* sweep_launches, double* sub_ms, long* sub_launches,
+                     double* upd_ms, long* upd_launches);
 
 /* Number of kernels this library has launched in the process. */
 long wmc_launch_count(void);

@@ -96,7 +96,7 @@ SIGNATURES = [
     ("wmc_run_mlmc", C.c_int, [P(_VP), C.c_int, _DP, P(MlmcConfig), P(MlmcResult), P(LevelStats), P(Error)]),
     ("wmc_moments_device", C.c_int, [_VP, _VP, _VP, C.c_uint64, _VP]),
     ("wmc_profile_enable", C.c_int, [_VP, C.c_int]),
-    ("wmc_profile_read", C.c_int, [_VP, _DP, P(C.c_long), _DP, P(C.c_long)]),
+    ("wmc_profile_read", C.c_int, [_VP, _DP, P(C.c_long), _DP, P(C.c_long), _DP, P(C.c_long)]),
     ("wmc_launch_count", C.c_long, []),
     ("wmc_last_error", C.c_char_p, []),
     ("wmc_device_count", C.c_int, []),

@@ -126,6 +126,8 @@ struct wmc_level {
     int* d_gen_soff = nullptr;
     std::uint16_t* d_gen_col = nullptr;
     int* d_slot_rc = nullptr;
+    double* d_slot_a0 = nullptr;
+    std::uint8_t* d_slot_cell = nullptr;
     int* d_grc_cell = nullptr;
     double* d_grc_a0 = nullptr;
     int n_slots = 0;
@@ -137,7 +139,7 @@ struct wmc_level {
     double* d_dq = nullptr;
     // optional per-kernel event timing (profiling pass only)
     bool profile = false;
-    std::vector<cudaEvent_t> ev_sweep, ev_sub;  // start/stop pairs
+    std::vector<cudaEvent_t> ev_sweep, ev_sub, ev_upd;  // start/stop pairs
 
     ~wmc_level() {
         cudaSetDevice(device);
@@ -145,7 +147,8 @@ struct wmc_level {
                         (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
                         (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
                         (void*)d_strip_j0, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
-                        (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_grc_cell,
+                        (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
+                        (void*)d_slot_cell, (void*)d_grc_cell,
                         (void*)d_grc_a0})
             if (p) cudaFree(p);
         for (auto& w : ws)
@@ -153,6 +156,7 @@ struct wmc_level {
                 if (p) cudaFree(p);
         for (auto e : ev_sweep) cudaEventDestroy(e);
         for (auto e : ev_sub) cudaEventDestroy(e);
+        for (auto e : ev_upd) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -229,32 +233,43 @@ void build_device_level(wmc_level& L) {
     L.d_qw = upload(t.qoi_w);
     L.d_qsm = upload(t.sqrt_mass_qoi);
 
-    if (lts && t.lattice && static_cast<int>(t.gen_rows.size()) <= wmc::kLatThreads * wmc::kLatGen) {
+    int max_gen_width = 0;
+    for (std::size_t q = 0; q + 1 < t.gen_ptr.size(); ++q)
+        max_gen_width = std::max(max_gen_width, t.gen_ptr[q + 1] - t.gen_ptr[q]);
+    if (lts && t.lattice && static_cast<int>(t.gen_rows.size()) <= 1024 && max_gen_width <= wmc::kLatGenWidth) {
         // SELL-32 over the generic rows, per slot: column and recipe range
         const int n_gen = static_cast<int>(t.gen_rows.size());
         const int n_slices = (n_gen + 31) / 32;
         std::vector<int> soff(n_slices + 1, 0), slot_rc{0}, rc_cell;
         std::vector<std::uint16_t> gcol;
-        std::vector<double> rc_a0;
+        std::vector<double> rc_a0, slot_a0;
+        std::vector<std::uint8_t> slot_cell;
         for (int sl = 0; sl < n_slices; ++sl) {
-            int width = 0;
-            for (int l = 0; l < 32; ++l) {
-                const int q = sl * 32 + l;
-                if (q < n_gen) width = std::max(width, t.gen_ptr[q + 1] - t.gen_ptr[q]);
-            }
+            const int width = wmc::kLatGenWidth;  // every slice padded to the fixed width
             for (int e = 0; e < width; ++e)
                 for (int l = 0; l < 32; ++l) {
                     const int q = sl * 32 + l;
                     std::uint16_t c = 0;
+                    double a1 = 0.0;
+                    std::uint8_t k1 = 0;
                     if (q < n_gen && e < t.gen_ptr[q + 1] - t.gen_ptr[q]) {
                         const int ent = t.gen_ptr[q] + e;
                         c = static_cast<std::uint16_t>(t.gen_col[ent]);
-                        for (int k = t.gen_rc_ptr[ent]; k < t.gen_rc_ptr[ent + 1]; ++k) {
-                            rc_cell.push_back(t.gen_rc_cell[k]);
-                            rc_a0.push_back(t.gen_rc_a0[k]);
+                        const int nt = t.gen_rc_ptr[ent + 1] - t.gen_rc_ptr[ent];
+                        if (nt == 1) {
+                            a1 = t.gen_rc_a0[t.gen_rc_ptr[ent]];
+                            k1 = static_cast<std::uint8_t>(t.gen_rc_cell[t.gen_rc_ptr[ent]]);
+                        } else {
+                            k1 = 0xff;
+                            for (int k = t.gen_rc_ptr[ent]; k < t.gen_rc_ptr[ent + 1]; ++k) {
+                                rc_cell.push_back(t.gen_rc_cell[k]);
+                                rc_a0.push_back(t.gen_rc_a0[k]);
+                            }
                         }
                     }
                     gcol.push_back(c);
+                    slot_a0.push_back(a1);
+                    slot_cell.push_back(k1);
                     slot_rc.push_back(static_cast<int>(rc_cell.size()));
                 }
             soff[sl + 1] = static_cast<int>(gcol.size());
@@ -266,12 +281,15 @@ void build_device_level(wmc_level& L) {
         L.d_celly = upload(t.lat_celly);
         L.d_gen_rows = upload(t.gen_rows);
         L.d_gen_rs = upload(t.gen_rs);
-        L.d_gen_soff = upload(soff);
         L.d_gen_col = upload(gcol);
         L.d_slot_rc = upload(slot_rc);
+        L.d_slot_a0 = upload(slot_a0);
+        L.d_slot_cell = upload(slot_cell);
         L.d_grc_cell = upload(rc_cell);
         L.d_grc_a0 = upload(rc_a0);
         wmc::LatArgs probe{};
+        probe.threads = t.lat_threads;
+        probe.strip_k = t.lat_k;
         probe.n_r = t.n_r;
         probe.p = t.p;
         probe.n_cells = t.n_cells;
@@ -289,6 +307,8 @@ void build_device_level(wmc_level& L) {
     check(cudaMalloc(&L.d_dq, sizeof(double) * std::max(L.batch, 1)), "cudaMalloc batch");
 }
 
+int g_stride(const wmc::LevelTables& t) { return std::max(8, (t.n_r + 7) / 8 * 8); }
+
 Workspace& workspace(wmc_level& L, int role) {
     Workspace& w = L.ws[role];
     if (!w.za) {
@@ -299,7 +319,7 @@ Workspace& workspace(wmc_level& L, int role) {
         };
         alloc(&w.za, S * t.n);
         alloc(&w.zb, S * t.n);
-        alloc(&w.g, S * std::max(t.n_r, 1));
+        alloc(&w.g, S * static_cast<std::size_t>(g_stride(t)));
         alloc(&w.fail, S);
         alloc(&w.q, S);
     }
@@ -343,6 +363,8 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     double* prev = ws.zb;
     wmc::LatArgs la{};
     if (lts && L.lattice) {
+        la.threads = t.lat_threads;
+        la.strip_k = t.lat_k;
         la.n_r = t.n_r;
         la.S = S;
         la.count = count;
@@ -362,16 +384,17 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         la.celly = L.d_celly;
         la.gen_rows = L.d_gen_rows;
         la.gen_rs = L.d_gen_rs;
-        la.gen_soff = L.d_gen_soff;
         la.gen_col = L.d_gen_col;
         la.slot_rc = L.d_slot_rc;
+        la.slot_a0 = L.d_slot_a0;
+        la.slot_cell = L.d_slot_cell;
         la.rc_cell = L.d_grc_cell;
         la.rc_a0 = L.d_grc_a0;
         la.cells = cells;
-        la.g = ws.g;
+        la.gd = ws.g;
+        la.g_stride = g_stride(t);
         la.beta = L.d_beta;
         la.cm = L.d_cm;
-        la.fail = ws.fail;
     }
     wmc::SubArgs sb{};
     if (lts) {
@@ -388,11 +411,11 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         sb.rc_cell = L.d_rc_cell;
         sb.rc_a0 = L.d_rc_a0;
         sb.cells = cells;
-        sb.g = ws.g;
+        sb.gd = ws.g;
+        sb.g_stride = g_stride(t);
         sb.beta = L.d_beta;
         sb.cm = L.d_cm;
         sb.c0 = t.c0;
-        sb.fail = ws.fail;
     }
     const int sub_grid = std::min(L.lattice ? L.lat_grid : L.sub_grid, count);
     for (long s = 1; s < t.n_steps; ++s) {
@@ -400,6 +423,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         sw.zp = prev;
         sw.zc_out = nullptr;
         sw.g = ws.g;
+        sw.g_stride = g_stride(t);
         sw.split = lts ? t.n_r : 0;
         sw.factor = t.coarse_factor;
         sw.step = static_cast<int>(s + 1);
@@ -408,18 +432,25 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         if (L.profile) mark(L, L.ev_sweep, stream);
         ++g_launches;
         if (lts) {
-            sb.zc = cur;
-            sb.zp = prev;
-            sb.step = static_cast<int>(s + 1);
-            la.zc = cur;
-            la.zp = prev;
-            la.step = static_cast<int>(s + 1);
             if (L.profile) mark(L, L.ev_sub, stream);
             const int e = L.lattice ? wmc::launch_lattice_substeps(la, sub_grid, stream)
                                     : wmc::launch_substeps(sb, sub_grid, stream);
             if (e != 0) check(static_cast<cudaError_t>(e), "substep launch");
             if (L.profile) mark(L, L.ev_sub, stream);
-            ++g_launches;
+            wmc::RUpdateArgs ru{};
+            ru.n_r = t.n_r;
+            ru.S = S;
+            ru.count = count;
+            ru.g_stride = g_stride(t);
+            ru.gd = ws.g;
+            ru.zc = cur;
+            ru.zp = prev;
+            ru.step = static_cast<int>(s + 1);
+            ru.fail = ws.fail;
+            if (L.profile) mark(L, L.ev_upd, stream);
+            wmc::launch_r_update(ru, stream);
+            if (L.profile) mark(L, L.ev_upd, stream);
+            g_launches += 2;
         }
         std::swap(cur, prev);
     }
@@ -940,7 +971,8 @@ int wmc_profile_enable(wmc_level* level, int on) {
     });
 }
 
-int wmc_profile_read(wmc_level* level, double* sweep_ms, long* sweep_launches, double* sub_ms, long* sub_launches) {
+int wmc_profile_read(wmc_level* level, double* sweep_ms, long* sweep_launches, double* sub_ms, long* sub_launches,
+                     double* upd_ms, long* upd_launches) {
     return guarded([&] {
         if (!level) throw ConfigError("wmc_profile_read: NULL level");
         check(cudaSetDevice(level->device), "cudaSetDevice");
@@ -959,6 +991,7 @@ int wmc_profile_read(wmc_level* level, double* sweep_ms, long* sweep_launches, d
         };
         total(level->ev_sweep, sweep_ms, sweep_launches);
         total(level->ev_sub, sub_ms, sub_launches);
+        total(level->ev_upd, upd_ms, upd_launches);
     });
 }
 

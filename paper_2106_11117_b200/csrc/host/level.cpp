@@ -1,6 +1,7 @@
 #include "level.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <stdexcept>
@@ -51,17 +52,19 @@ int cell_of(double x, double y, int nx, int ny) {
     return iy * nx + ix;
 }
 
-constexpr int kLatticeThreads = 512;  // threads of the lattice substep kernel
-constexpr int kLatticeStrip = 8;      // max rows per thread
+// lattice substep kernel variants: (threads, max rows per thread)
+constexpr int kLatticeVariants[2][2] = {{512, 8}, {1024, 4}};
 
 using StiffMap = std::map<std::tuple<int, int, int>, double>;
 
 // Finds the structured block of the refined square and checks, numerically
-// against the assembled element stiffness, that every node of L = [1, m-1]^2
-// has the 5-point lattice stencil with edge conductances (c_a + c_b) / 2 and
-// lumped mass h^2.  Fills the lattice fields of L and returns the box
-// vertices in (j, i) order, or an empty vector (with lattice_reason) when the
-// fast path does not apply.
+// against the assembled element stiffness, that every lattice node
+// (i, j) in [1, m-1]^2 has the 5-point stencil with edge conductances
+// (c_a + c_b) / 2 and lumped mass h^2.  Rows j on a horizontal coefficient
+// line (squares j-1 and j in different cells) are left to the generic path,
+// so every lattice node of a strip sees one coefficient row above and below.
+// Fills the lattice fields of L and returns the box vertices in column-major
+// order (box index i*(m+1) + j), or an empty vector (with lattice_reason).
 std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const std::vector<double>& mass,
                                const StiffMap& stiff, const std::vector<std::uint8_t>& in_r, LevelTables& L) {
     auto fail = [&](const std::string& why) {
@@ -72,18 +75,21 @@ std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const
     if (mesh.fine_box_lo < 0 || mesh.lattice.size() != mesh.vertices.size()) return fail("no refined box");
     const int qa = mesh.fine_box_lo, m = mesh.fine_box_hi - mesh.fine_box_lo;
     if (m < 4) return fail("refined box too small");
+    if ((m + 1) % 2 == 0) return fail("even box width (shared-memory bank conflicts)");
+    const int W = m + 1;
     const double h = mesh.fine_h;
     std::map<std::pair<int, int>, int> at;
     for (int v = 0; v < mesh.n_vertices(); ++v) at[{mesh.lattice[v][0], mesh.lattice[v][1]}] = v;
     std::vector<int> box;
-    box.reserve(static_cast<std::size_t>(m + 1) * (m + 1));
-    for (int j = 0; j <= m; ++j)
-        for (int i = 0; i <= m; ++i) {
+    box.reserve(static_cast<std::size_t>(W) * W);
+    for (int i = 0; i <= m; ++i)
+        for (int j = 0; j <= m; ++j) {
             const auto it = at.find({qa + i, qa + j});
             if (it == at.end()) return fail("box node missing");
             if (mesh.boundary_vertex[it->second] || !in_r[it->second]) return fail("box node not in R");
             box.push_back(it->second);
         }
+    auto node = [&](int i, int j) { return box[i * W + j]; };
     std::vector<int> cx(m), cy(m);
     for (int i = 0; i < m; ++i) {
         const double x = (qa + i + 0.5) * h;
@@ -95,12 +101,11 @@ std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const
     std::vector<double> ct(nc);
     for (int k = 0; k < nc; ++k) ct[k] = 1.0 + 0.371 * k + 0.013 * k * k;
     auto csq = [&](int i, int j) { return ct[cy[j] * spec.cells_x + cx[i]]; };
-    for (int j = 1; j <= m - 1; ++j)
-        for (int i = 1; i <= m - 1; ++i) {
-            const int v = box[j * (m + 1) + i];
+    for (int i = 1; i <= m - 1; ++i)
+        for (int j = 1; j <= m - 1; ++j) {
+            const int v = node(i, j);
             if (std::abs(mass[v] - h * h) > 1e-12 * h * h) return fail("lumped mass != h^2 in L");
-            const int nb[4] = {box[j * (m + 1) + i + 1], box[j * (m + 1) + i - 1], box[(j + 1) * (m + 1) + i],
-                               box[(j - 1) * (m + 1) + i]};
+            const int nb[4] = {node(i + 1, j), node(i - 1, j), node(i, j + 1), node(i, j - 1)};
             const double kap[4] = {0.5 * (csq(i, j) + csq(i, j - 1)), 0.5 * (csq(i - 1, j) + csq(i - 1, j - 1)),
                                    0.5 * (csq(i - 1, j) + csq(i, j)), 0.5 * (csq(i - 1, j - 1) + csq(i, j - 1))};
             double want_diag = 0.0, got_diag = 0.0;
@@ -129,27 +134,45 @@ std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const
             }
             if (std::abs(got_diag - want_diag) > 1e-12 * want_diag) return fail("diagonal mismatch in L");
         }
-    // row strips: every coefficient line (celly changes between squares j-1
-    // and j) starts a strip, so the rows after a strip's first share one
-    // coefficient row
+    // lattice rows: [1, m-1] minus rows on a horizontal coefficient line;
+    // strips of <= K consecutive lattice rows, K from the first kernel
+    // variant whose CTA holds them
+    std::vector<std::uint8_t> lat_row(m + 1, 0);
+    for (int j = 1; j <= m - 1; ++j) lat_row[j] = cy[j] == cy[j - 1];
+    const int cw = (m - 1 + 31) / 32 * 32;
     std::vector<int> j0s, lens;
-    int start = 1;
-    for (int j = 2; j <= m; ++j) {
-        if (j == m || cy[j] != cy[j - 1]) {
-            for (int a = start; a < j; a += kLatticeStrip) {
-                j0s.push_back(a);
-                lens.push_back(std::min(kLatticeStrip, j - a));
+    int threads = 0, kmax = 0;
+    const char* force = std::getenv("WMC_LATTICE_THREADS");  // tuning: force a variant
+    for (const auto& var : kLatticeVariants) {
+        if (force && std::atoi(force) != var[0]) continue;
+        j0s.clear();
+        lens.clear();
+        for (int j = 1; j <= m - 1;) {
+            if (!lat_row[j]) {
+                ++j;
+                continue;
             }
-            start = j;
+            int e = j;
+            while (e <= m - 1 && lat_row[e] && e - j < var[1]) ++e;
+            j0s.push_back(j);
+            lens.push_back(e - j);
+            j = e;
+        }
+        if (static_cast<int>(j0s.size()) * cw <= var[0]) {
+            threads = var[0];
+            kmax = var[1];
+            break;
         }
     }
-    const int cw = (m - 1 + 31) / 32 * 32;
-    if (static_cast<int>(j0s.size()) * cw > kLatticeThreads) return fail("too many strips for the CTA");
+    if (!threads) return fail("too many strips for the CTA");
+    L.lat_threads = threads;
+    L.lat_k = kmax;
     L.lattice = true;
     L.lat_m = m;
     L.lat_inv_h = 1.0 / h;
     L.lat_cellx = cx;
     L.lat_celly = cy;
+    L.lat_row = lat_row;
     L.strip_j0 = j0s;
     L.strip_len = lens;
     L.lat_cw = cw;
@@ -296,8 +319,9 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         L.gen_ptr.push_back(0);
         L.gen_rc_ptr.push_back(0);
         for (int i = 0; i < L.n_r; ++i) {
-            const int bi = i % W, bj = i / W;
-            if (i < W * W && bi >= 1 && bi <= L.lat_m - 1 && bj >= 1 && bj <= L.lat_m - 1) continue;  // in L
+            const int bi = i / W, bj = i % W;  // column-major box
+            if (i < W * W && bi >= 1 && bi <= L.lat_m - 1 && bj >= 1 && bj <= L.lat_m - 1 && L.lat_row[bj])
+                continue;  // a lattice node
             L.gen_rows.push_back(i);
             L.gen_rs.push_back(1.0 / std::sqrt(L.mass[i]));
             const auto& r = rows[i];

@@ -87,17 +87,20 @@ struct LevelTables {
     std::vector<int> elem_cell;     // per triangle (diagnostics)
 
     // Structured block of the refined square for the substep fast path.  The
-    // box has (m+1)^2 lattice nodes with dof = j*(m+1) + i (Q-local i, j);
-    // L = [1, m-1]^2 are nodes whose six triangles are h_min lattice
-    // triangles, so (A d)_i = (1/h) sum_dir kappa_dir (v_i - v_dir) with
-    // v = d / sqrt(M) and kappa = mean coefficient of the two triangles on an
-    // edge; every other R row ("generic") keeps explicit per-entry recipes.
+    // box has (m+1)^2 nodes with dof = i*(m+1) + j (Q-local i, j; column
+    // major); lattice nodes are (i, j) in [1, m-1]^2 off horizontal
+    // coefficient lines: their six triangles are h_min lattice triangles, so
+    // (A d)_i = (1/h) sum_dir kappa_dir (v_i - v_dir) with v = d / sqrt(M)
+    // and kappa = mean coefficient of the two triangles on an edge; every
+    // other R row ("generic") keeps explicit per-entry recipes.
     bool lattice = false;
     int lat_m = 0;
     double lat_inv_h = 0.0;
     std::vector<int> lat_cellx, lat_celly;  // coefficient column / row of square column i / row j
-    std::vector<int> strip_j0, strip_len;   // row strips of L (coefficient lines start a strip)
+    std::vector<std::uint8_t> lat_row;     // per box row j: 1 if its interior nodes are lattice nodes
+    std::vector<int> strip_j0, strip_len;   // row strips of lattice nodes (no coefficient line inside)
     int lat_cw = 0;                         // threads per strip row (columns, rounded up to 32)
+    int lat_threads = 0, lat_k = 0;         // kernel variant: CTA size, max rows per thread
     std::string lattice_reason;             // why the fast path is off (diagnostics)
     std::vector<int> gen_rows;              // generic R rows (dofs)
     std::vector<double> gen_rs;             // 1/sqrt(M) of each generic row

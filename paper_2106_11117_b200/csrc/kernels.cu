@@ -59,53 +59,106 @@ __device__ __forceinline__ void flag_fail(int* fail, int s, int count, int step)
 
 template <bool kInit>
 __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int row = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
-    if (row >= a.n) return;
+    __shared__ double2 tile[kSweepWarps][32];  // g of the block's R rows: [row][lane] = samples 2 lane, 2 lane + 1
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int row0 = blockIdx.x * kSweepWarps;
+    const int row = row0 + warp;
     const int s0 = blockIdx.y * kSweepChunk + 2 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
-    const int b = __ldg(a.row_ptr + row), e = __ldg(a.row_ptr + row + 1);
-    double acc0 = 0.0, acc1 = 0.0;
-    for (int k = b; k < e; ++k) {
-        const int pk = __ldg(a.ent + k);
-        const double w = __ldg(a.a0 + k);
-        const int j = pk & 0xffffff;
-        const int cell = static_cast<unsigned>(pk) >> 24;
-        const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+    if (row < a.n) {
+        const int b = __ldg(a.row_ptr + row), e = __ldg(a.row_ptr + row + 1);
+        double acc0 = 0.0, acc1 = 0.0;
+        for (int k = b; k < e; ++k) {
+            const int pk = __ldg(a.ent + k);
+            const double w = __ldg(a.a0 + k);
+            const int j = pk & 0xffffff;
+            const int cell = static_cast<unsigned>(pk) >> 24;
+            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+            if (kInit) {
+                const double zj = __ldg(a.z0 + j);
+                acc0 += (c.x * w) * zj;
+                acc1 += (c.y * w) * zj;
+            } else {
+                const double2 z = __ldg(reinterpret_cast<const double2*>(a.zc + j * S + s0));
+                acc0 += (c.x * w) * z.x;
+                acc1 += (c.y * w) * z.y;
+            }
+        }
+        const std::size_t idx = row * S + s0;
         if (kInit) {
-            const double zj = __ldg(a.z0 + j);
-            acc0 += (c.x * w) * zj;
-            acc1 += (c.y * w) * zj;
+            // z1 = z0 + dt M^{1/2} v0 + dt^2/2 (F0 - A z0), v0 = F = 0 (integrators.cpp:68-87)
+            const double z0 = __ldg(a.z0 + row);
+            double2 out;
+            out.x = z0 + a.factor * (0.0 - acc0);
+            out.y = z0 + a.factor * (0.0 - acc1);
+            *reinterpret_cast<double2*>(a.zp + idx) = make_double2(z0, z0);
+            *reinterpret_cast<double2*>(a.zc_out + idx) = out;
+            if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
+            if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+        } else if (row < a.split) {
+            tile[warp][lane] = make_double2(acc0, acc1);
         } else {
-            const double2 z = __ldg(reinterpret_cast<const double2*>(a.zc + j * S + s0));
-            acc0 += (c.x * w) * z.x;
-            acc1 += (c.y * w) * z.y;
+            const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
+            const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
+            double2 out;
+            out.x = 2.0 * zn.x - zm.x - a.factor * acc0;
+            out.y = 2.0 * zn.y - zm.y - a.factor * acc1;
+            *reinterpret_cast<double2*>(a.zp + idx) = out;
+            // check_finite (integrators.cpp:12-18): non-finite or |z| > 1e100
+            if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
+            if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
         }
     }
-    const std::size_t idx = row * S + s0;
-    if (kInit) {
-        // z1 = z0 + dt M^{1/2} v0 + dt^2/2 (F0 - A z0), v0 = F = 0 (integrators.cpp:68-87)
-        const double z0 = __ldg(a.z0 + row);
-        double2 out;
-        out.x = z0 + a.factor * (0.0 - acc0);
-        out.y = z0 + a.factor * (0.0 - acc1);
-        *reinterpret_cast<double2*>(a.zp + idx) = make_double2(z0, z0);
-        *reinterpret_cast<double2*>(a.zc_out + idx) = out;
-        if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
-        if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
-        return;
+    if (kInit || row0 >= a.split) return;  // block-uniform
+    // store the block's g rows sample-major: warp w writes samples 8w..8w+7,
+    // four lanes per sample, two rows (16 B) per lane
+    __syncthreads();
+    const int sl = 8 * warp + (lane >> 2), rr = 2 * (lane & 3);
+    const int s = blockIdx.y * kSweepChunk + sl;
+    const double2 t0 = tile[rr][sl >> 1], t1 = tile[rr + 1][sl >> 1];
+    const double g0 = (sl & 1) ? t0.y : t0.x, g1 = (sl & 1) ? t1.y : t1.x;
+    double* dst = a.g + static_cast<std::size_t>(s) * a.g_stride + row0 + rr;
+    if (row0 + rr + 1 < a.split)
+        *reinterpret_cast<double2*>(dst) = make_double2(g0, g1);
+    else if (row0 + rr < a.split)
+        dst[0] = g0;
+}
+
+// R update: z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on rows < n_r, d_p read
+// sample-major and transposed through shared memory (mirror of the sweep's
+// g store), then one warp per (row, 64 samples) as in the sweep.
+__global__ void __launch_bounds__(kSweepWarps * 32) r_update_kernel(RUpdateArgs a) {
+    __shared__ double2 tile[kSweepWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int row0 = blockIdx.x * kSweepWarps;
+    {
+        const int sl = 8 * warp + (lane >> 2), rr = 2 * (lane & 3);
+        const int s = blockIdx.y * kSweepChunk + sl;
+        const double* src = a.gd + static_cast<std::size_t>(s) * a.g_stride + row0 + rr;
+        double d0 = 0.0, d1 = 0.0;
+        if (row0 + rr + 1 < a.n_r) {
+            const double2 v = *reinterpret_cast<const double2*>(src);
+            d0 = v.x;
+            d1 = v.y;
+        } else if (row0 + rr < a.n_r) {
+            d0 = src[0];
+        }
+        double* t = reinterpret_cast<double*>(&tile[0][0]);
+        t[(rr * 32 + (sl >> 1)) * 2 + (sl & 1)] = d0;
+        t[((rr + 1) * 32 + (sl >> 1)) * 2 + (sl & 1)] = d1;
     }
-    if (row < a.split) {
-        *reinterpret_cast<double2*>(a.g + idx) = make_double2(acc0, acc1);
-        return;
-    }
+    __syncthreads();
+    const int row = row0 + warp;
+    if (row >= a.n_r) return;
+    const int s0 = blockIdx.y * kSweepChunk + 2 * lane;
+    const std::size_t idx = static_cast<std::size_t>(row) * a.S + s0;
+    const double2 d = tile[warp][lane];
     const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
     const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
     double2 out;
-    out.x = 2.0 * zn.x - zm.x - a.factor * acc0;
-    out.y = 2.0 * zn.y - zm.y - a.factor * acc1;
+    out.x = 2.0 * zn.x - zm.x + 2.0 * d.x;
+    out.y = 2.0 * zn.y - zm.y + 2.0 * d.y;
     *reinterpret_cast<double2*>(a.zp + idx) = out;
-    // check_finite (integrators.cpp:12-18): non-finite or |z| > 1e100
     if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
     if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
 }
@@ -201,7 +254,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
             dc[k] = 0.0;
             dp[k] = 0.0;
             if (r < a.n_r) {
-                g[k] = __ldg(a.g + r * S + s);
+                g[k] = a.gd[static_cast<std::size_t>(s) * a.g_stride + r];
                 dc[k] = -a.c0 * g[k];
                 sm.d0[r] = dc[k];
             }
@@ -236,14 +289,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
             const int r = tid + k * kSubThreads;
-            if (r < a.n_r) {
-                const std::size_t idx = r * S + s;
-                const double zn = a.zc[idx];
-                const double zm = a.zp[idx];
-                const double out = 2.0 * zn - zm + 2.0 * dc[k];
-                a.zp[idx] = out;
-                if (!(fabs(out) <= 1e100)) atomicMin(a.fail + s, a.step);
-            }
+            if (r < a.n_r) a.gd[static_cast<std::size_t>(s) * a.g_stride + r] = dc[k];  // d_p, coalesced
         }
     }
     (void)n_slices;
@@ -263,217 +309,221 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
 // Generic rows (box ring + transition belt) use a SELL of per-sample
 // weights w_ij = A_ij(omega) sqrt(M_j) acting on v.
 
-struct LatSmem {
-    double* v0;
-    double* v1;
-    double* gw;
-    double* cl;
-    double* beta;
-    double* cm;
-    std::uint16_t* gcol;
-    int* gsoff;
-    int* sj0;
-    int* slen;
-    int* cx;
-    int* cy;
+// Shared-memory layout of the lattice kernel, in units of doubles from the
+// dynamic shared base (integer offsets keep every access a 32-bit shared
+// address): v0 | v1 | gw | sa0 | cl | beta | cm | then 8-byte aligned int
+// and byte tables.
+struct LatOff {
+    int v0, v1, gw, sa0, cl, beta, cm, gcol, scell, sj0, slen, cx, cy, total;
 };
 
-__host__ __device__ inline std::size_t lat_layout(const LatArgs& a, char* base, LatSmem* s) {
-    const int n_slices = (a.n_gen + 31) / 32;
-    std::size_t off = 0;
-    auto take = [&](std::size_t bytes) {
-        const std::size_t o = off;
-        off = align16(off + bytes);
-        return o;
+__host__ __device__ inline LatOff lat_offsets(const LatArgs& a) {
+    LatOff o;
+    int off = 0;
+    auto take = [&](int doubles) {
+        const int r = off;
+        off += (doubles + 1) & ~1;  // keep 16-byte alignment
+        return r;
     };
-    const std::size_t o0 = take(sizeof(double) * a.n_r);
-    const std::size_t o1 = take(sizeof(double) * a.n_r);
-    const std::size_t ow = take(sizeof(double) * (a.n_slots > 0 ? a.n_slots : 1));
-    const std::size_t ol = take(sizeof(double) * a.n_cells);
-    const std::size_t ob = take(sizeof(double) * (a.p > 1 ? a.p - 1 : 1));
-    const std::size_t oc = take(sizeof(double) * (a.p > 1 ? a.p - 1 : 1));
-    const std::size_t og = take(sizeof(std::uint16_t) * (a.n_slots > 0 ? a.n_slots : 1));
-    const std::size_t os = take(sizeof(int) * (n_slices + 1));
-    const std::size_t oj = take(sizeof(int) * a.n_strips);
-    const std::size_t olen = take(sizeof(int) * a.n_strips);
-    const std::size_t ox = take(sizeof(int) * a.m);
-    const std::size_t oy = take(sizeof(int) * a.m);
-    if (s) {
-        s->v0 = reinterpret_cast<double*>(base + o0);
-        s->v1 = reinterpret_cast<double*>(base + o1);
-        s->gw = reinterpret_cast<double*>(base + ow);
-        s->cl = reinterpret_cast<double*>(base + ol);
-        s->beta = reinterpret_cast<double*>(base + ob);
-        s->cm = reinterpret_cast<double*>(base + oc);
-        s->gcol = reinterpret_cast<std::uint16_t*>(base + og);
-        s->gsoff = reinterpret_cast<int*>(base + os);
-        s->sj0 = reinterpret_cast<int*>(base + oj);
-        s->slen = reinterpret_cast<int*>(base + olen);
-        s->cx = reinterpret_cast<int*>(base + ox);
-        s->cy = reinterpret_cast<int*>(base + oy);
-    }
-    return off;
+    const int slots = a.n_slots > 0 ? a.n_slots : 1;
+    o.v0 = take(a.n_r + 16);  // rows past a short strip read (never write) up to 8 beyond
+    o.v1 = take(a.n_r + 16);
+    o.gw = take(slots);
+    o.sa0 = take(slots);
+    o.cl = take(a.n_cells);
+    o.beta = take(a.p > 1 ? a.p - 1 : 1);
+    o.cm = take(a.p > 1 ? a.p - 1 : 1);
+    o.gcol = take((slots * 2 + 7) / 8);  // uint16
+    o.scell = take((slots + 7) / 8);     // uint8
+    o.sj0 = take((a.n_strips + 1) / 2);  // int
+    o.slen = take((a.n_strips + 1) / 2);
+    o.cx = take((a.m + 1) / 2);
+    o.cy = take((a.m + 1) / 2);
+    o.total = off;
+    return o;
 }
 
-__global__ void __launch_bounds__(kLatThreads, 1) lattice_substep_kernel(LatArgs a) {
-    extern __shared__ __align__(16) char smem[];
-    LatSmem sm;
-    lat_layout(a, smem, &sm);
+// K2 (structured): the p LTS substeps on R with the refined-square lattice
+// as a register-blocked 5-point stencil.  Thread t owns column i = 1 + t % cw
+// of strip t / cw (<= K consecutive rows of L = [1, m-1]^2), keeping d_m,
+// d_{m-1} and g of its nodes in registers; N/S neighbours inside the strip
+// come from registers, E/W and the strip ends from the shared-memory copy
+// of v = d / sqrt(M) (double-buffered, one barrier per substep).  Edge
+// conductances kappa = (c_a + c_b)/2 come from the sample's cell
+// coefficients; a coefficient line always starts a strip, so a thread needs
+// one set of constants for its first row and one for the rest.  Generic rows
+// (box ring + transition belt, G per thread) use a SELL of per-sample
+// weights w_ij = A_ij(omega) sqrt(M_j) on v, padded to kLatGenWidth slots so
+// the gather is straight-line code.  Rows past a short strip compute on
+// clamped addresses and never store.
+template <int T, int K, int G>
+__global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
+    extern __shared__ __align__(16) double sd[];
+    const LatOff o = lat_offsets(a);
+    std::uint16_t* gcol = reinterpret_cast<std::uint16_t*>(sd + o.gcol);
+    std::uint8_t* scell = reinterpret_cast<std::uint8_t*>(sd + o.scell);
+    int* sj0 = reinterpret_cast<int*>(sd + o.sj0);
+    int* slen = reinterpret_cast<int*>(sd + o.slen);
+    int* cx = reinterpret_cast<int*>(sd + o.cx);
+    int* cy = reinterpret_cast<int*>(sd + o.cy);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int n_slices = (a.n_gen + 31) / 32;
     const std::size_t S = static_cast<std::size_t>(a.S);
     const int W = a.m + 1;
+    const int nr = a.n_r;
+    const double inv_h = a.inv_h;
 
-    for (int i = tid; i < a.n_slots; i += kLatThreads) sm.gcol[i] = __ldg(a.gen_col + i);
-    for (int i = tid; i <= n_slices; i += kLatThreads) sm.gsoff[i] = __ldg(a.gen_soff + i);
-    for (int i = tid; i < a.n_strips; i += kLatThreads) {
-        sm.sj0[i] = __ldg(a.strip_j0 + i);
-        sm.slen[i] = __ldg(a.strip_len + i);
+    // static tables, once per CTA
+    for (int i = tid; i < a.n_slots; i += T) {
+        gcol[i] = __ldg(a.gen_col + i);
+        scell[i] = __ldg(a.slot_cell + i);
+        sd[o.sa0 + i] = __ldg(a.slot_a0 + i);
     }
-    for (int i = tid; i < a.m; i += kLatThreads) {
-        sm.cx[i] = __ldg(a.cellx + i);
-        sm.cy[i] = __ldg(a.celly + i);
+    for (int i = tid; i < a.n_strips; i += T) {
+        sj0[i] = __ldg(a.strip_j0 + i);
+        slen[i] = __ldg(a.strip_len + i);
     }
-    for (int i = tid; i < a.p - 1; i += kLatThreads) {
-        sm.beta[i] = __ldg(a.beta + i);
-        sm.cm[i] = __ldg(a.cm + i);
+    for (int i = tid; i < a.m; i += T) {
+        cx[i] = __ldg(a.cellx + i);
+        cy[i] = __ldg(a.celly + i);
+    }
+    for (int i = tid; i < a.p - 1; i += T) {
+        sd[o.beta + i] = __ldg(a.beta + i);
+        sd[o.cm + i] = __ldg(a.cm + i);
     }
 
-    // structured role
+    // structured role: column ci of strip `strip`
     const int col = tid % a.cw, strip = tid / a.cw;
     const int ci = 1 + col;
     const bool lat_on = ci <= a.m - 1 && strip < a.n_strips;
-    // generic role
-    int gq[kLatGen];
+    // generic role: list entries tid + u*T, slots [slice][kLatGenWidth][32]
+    int grow[G], gslot[G];
+    double grs[G];
 #pragma unroll
-    for (int u = 0; u < kLatGen; ++u) gq[u] = tid + u * kLatThreads;
+    for (int u = 0; u < G; ++u) {
+        const int q = tid + u * T;
+        grow[u] = q < a.n_gen ? __ldg(a.gen_rows + q) : -1;
+        grs[u] = q < a.n_gen ? __ldg(a.gen_rs + q) : 0.0;
+        gslot[u] = (q < a.n_gen ? (q >> 5) * (32 * kLatGenWidth) : 0) + lane;  // idle lanes read slice 0
+    }
+    __syncthreads();
+    int j0 = 1, len = 0;
+    if (lat_on) {
+        j0 = sj0[strip];
+        len = slen[strip];
+    }
+    // column-major box: the strip's nodes are base .. base + len - 1; idle
+    // threads point at node (1, 1) and never store
+    const int base = lat_on ? ci * W + j0 : W + 1;
 
     for (int s = blockIdx.x; s < a.count; s += gridDim.x) {
+        // ---- per-sample set-up: g staged coalesced into v1, coefficients,
+        // generic weights
+        double* gdrow = a.gd + static_cast<std::size_t>(s) * a.g_stride;
+        for (int r = tid; r < nr; r += T) sd[o.v1 + r] = gdrow[r];
+        for (int k = tid; k < a.n_cells; k += T) sd[o.cl + k] = __ldg(a.cells + k * S + s);
         __syncthreads();
-        for (int k = tid; k < a.n_cells; k += kLatThreads) sm.cl[k] = __ldg(a.cells + k * S + s);
-        __syncthreads();
-        for (int e = tid; e < a.n_slots; e += kLatThreads) {
-            double acc = 0.0;
-            for (int t = __ldg(a.slot_rc + e); t < __ldg(a.slot_rc + e + 1); ++t)
-                acc += sm.cl[__ldg(a.rc_cell + t)] * __ldg(a.rc_a0 + t);
-            sm.gw[e] = acc;
+        double gg[K], ggg[G];
+#pragma unroll
+        for (int k = 0; k < K; ++k) gg[k] = k < len ? sd[o.v1 + base + k] : 0.0;
+#pragma unroll
+        for (int u = 0; u < G; ++u) ggg[u] = grow[u] >= 0 ? sd[o.v1 + grow[u]] : 0.0;
+        for (int e = tid; e < a.n_slots; e += T) {
+            const int c = scell[e];
+            double w;
+            if (c != 0xff) {
+                w = sd[o.cl + c] * sd[o.sa0 + e];
+            } else {  // several cells share this entry (edge on a coefficient line)
+                w = 0.0;
+                for (int t = __ldg(a.slot_rc + e); t < __ldg(a.slot_rc + e + 1); ++t)
+                    w += sd[o.cl + __ldg(a.rc_cell + t)] * __ldg(a.rc_a0 + t);
+            }
+            sd[o.gw + e] = w;
         }
-
-        // lattice constants of this thread (scaled by 1/h: v = d/h)
-        int j0 = 1, len = 0;
-        double kE0 = 0, kW0 = 0, kN0 = 0, kS0 = 0, dg0 = 0, kE = 0, kW = 0, kNS = 0, dg = 0;
-        double d[kLatStrip], dp[kLatStrip], gg[kLatStrip];
+        // edge conductances of this thread's column, scaled by 1/h (v = d/h):
+        // squares right (column ci) and left (ci - 1) of the strip, all in
+        // the strip's coefficient row
+        double kE = 0, kW = 0, kNS = 0, dg = 0;
         if (lat_on) {
-            j0 = sm.sj0[strip];
-            len = sm.slen[strip];
-            const int rowu = sm.cy[j0] * a.cells_x, rowd = sm.cy[j0 - 1] * a.cells_x;
-            const double cRu = sm.cl[rowu + sm.cx[ci]], cRd = sm.cl[rowd + sm.cx[ci]];
-            const double cLu = sm.cl[rowu + sm.cx[ci - 1]], cLd = sm.cl[rowd + sm.cx[ci - 1]];
-            const double f = 0.5 * a.inv_h;
-            kE0 = (cRu + cRd) * f;
-            kW0 = (cLu + cLd) * f;
-            kN0 = (cLu + cRu) * f;
-            kS0 = (cLd + cRd) * f;
-            dg0 = kE0 + kW0 + kN0 + kS0;
-            kE = cRu * a.inv_h;
-            kW = cLu * a.inv_h;
-            kNS = (cLu + cRu) * f;
+            const int row = o.cl + cy[j0] * a.cells_x;
+            const double cR = sd[row + cx[ci]], cL = sd[row + cx[ci - 1]];
+            kE = cR * inv_h;
+            kW = cL * inv_h;
+            kNS = (cL + cR) * (0.5 * inv_h);
             dg = kE + kW + 2.0 * kNS;
         }
+        double d[K], dp[K];
 #pragma unroll
-        for (int k = 0; k < kLatStrip; ++k) {
-            d[k] = 0.0;
+        for (int k = 0; k < K; ++k) {
             dp[k] = 0.0;
-            gg[k] = 0.0;
-            if (k < len) {
-                const int dof = (j0 + k) * W + ci;
-                gg[k] = __ldg(a.g + dof * S + s);
-                d[k] = -a.c0 * gg[k];
-                sm.v0[dof] = d[k] * a.inv_h;
-            }
+            d[k] = -a.c0 * gg[k];
+            if (k < len) sd[o.v0 + base + k] = d[k] * inv_h;
         }
-        double gd[kLatGen], gdp[kLatGen], ggg[kLatGen], grs[kLatGen];
-        int grow[kLatGen];
+        double gd[G], gdp[G];
 #pragma unroll
-        for (int u = 0; u < kLatGen; ++u) {
-            gd[u] = gdp[u] = ggg[u] = grs[u] = 0.0;
-            grow[u] = -1;
-            if (gq[u] < a.n_gen) {
-                grow[u] = __ldg(a.gen_rows + gq[u]);
-                grs[u] = __ldg(a.gen_rs + gq[u]);
-                ggg[u] = __ldg(a.g + grow[u] * S + s);
-                gd[u] = -a.c0 * ggg[u];
-                sm.v0[grow[u]] = gd[u] * grs[u];
-            }
+        for (int u = 0; u < G; ++u) {
+            gdp[u] = 0.0;
+            gd[u] = -a.c0 * ggg[u];
+            if (grow[u] >= 0) sd[o.v0 + grow[u]] = gd[u] * grs[u];
         }
         __syncthreads();
 
+        // ---- p - 1 substeps, state on chip
+        const int sS = lat_on ? base - 1 : 0, sN = lat_on ? base + len : 0;
         for (int m = 1; m <= a.p - 1; ++m) {
-            const double* cur = (m & 1) ? sm.v0 : sm.v1;
-            double* nxt = (m & 1) ? sm.v1 : sm.v0;
-            const double beta = sm.beta[m - 1];
-            const double cmm = sm.cm[m - 1];
+            const int cur = (m & 1) ? o.v0 : o.v1;
+            const int nxt = (m & 1) ? o.v1 : o.v0;
+            const double beta = sd[o.beta + m - 1];
+            const double cmm = sd[o.cm + m - 1];
             const double onepb = 1.0 + beta;
-            if (len > 0) {
-                const int base = j0 * W + ci;
-                double vs = cur[base - W];  // south neighbour of the first row (old)
-                double vk = d[0] * a.inv_h;  // old v of the current node
+            double gaq[G];
 #pragma unroll
-                for (int k = 0; k < kLatStrip; ++k) {
-                    if (k < len) {
-                        const int dof = base + k * W;
-                        const double vn = (k + 1 < len) ? d[k + 1] * a.inv_h : cur[dof + W];
-                        const double ve = cur[dof + 1], vw = cur[dof - 1];
-                        double aq;
-                        if (k == 0)
-                            aq = dg0 * vk - kE0 * ve - kW0 * vw - kN0 * vn - kS0 * vs;
-                        else
-                            aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
-                        const double next = onepb * d[k] - beta * dp[k] - cmm * (gg[k] + aq);
-                        dp[k] = d[k];
-                        d[k] = next;
-                        nxt[dof] = next * a.inv_h;
-                        vs = vk;
-                        vk = vn;
-                    }
+            for (int u = 0; u < G; ++u) {
+                double acc = 0.0;
+#pragma unroll
+                for (int e = 0; e < kLatGenWidth; ++e) {
+                    const int q = gslot[u] + 32 * e;
+                    acc += sd[o.gw + q] * sd[cur + gcol[q]];
                 }
+                gaq[u] = acc;
+            }
+            const int ce = cur + base + W, cw_ = cur + base - W;
+            const double vnl = sd[cur + sN];
+            double vs = sd[cur + sS];
+            double vk = d[0] * inv_h;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const double ve = sd[ce + k], vw = sd[cw_ + k];
+                const double vn = (k + 1 < len) ? d[k + 1] * inv_h : vnl;
+                const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
+                const double next = onepb * d[k] - beta * dp[k] - cmm * (gg[k] + aq);
+                dp[k] = d[k];
+                d[k] = next;
+                if (k < len) sd[nxt + base + k] = next * inv_h;
+                vs = vk;
+                vk = vn;
             }
 #pragma unroll
-            for (int u = 0; u < kLatGen; ++u) {
-                if (grow[u] >= 0) {
-                    const int slice = gq[u] >> 5;
-                    const int b = sm.gsoff[slice], e = sm.gsoff[slice + 1];
-                    double aq = 0.0;
-                    for (int q = b + lane; q < e; q += 32) aq += sm.gw[q] * cur[sm.gcol[q]];
-                    const double next = onepb * gd[u] - beta * gdp[u] - cmm * (ggg[u] + aq);
-                    gdp[u] = gd[u];
-                    gd[u] = next;
-                    nxt[grow[u]] = next * grs[u];
-                }
+            for (int u = 0; u < G; ++u) {
+                const double next = onepb * gd[u] - beta * gdp[u] - cmm * (ggg[u] + gaq[u]);
+                gdp[u] = gd[u];
+                gd[u] = next;
+                if (grow[u] >= 0) sd[nxt + grow[u]] = next * grs[u];
             }
             __syncthreads();
         }
 
-        // z_{n+1} = 2 z_n - z_{n-1} + 2 d_p
+        // ---- d_p out, staged through v0 for a coalesced store (the R update
+        // kernel forms z_{n+1})
 #pragma unroll
-        for (int k = 0; k < kLatStrip; ++k) {
-            if (k < len) {
-                const std::size_t idx = static_cast<std::size_t>((j0 + k) * W + ci) * S + s;
-                const double out = 2.0 * a.zc[idx] - a.zp[idx] + 2.0 * d[k];
-                a.zp[idx] = out;
-                if (!(fabs(out) <= 1e100)) atomicMin(a.fail + s, a.step);
-            }
-        }
+        for (int k = 0; k < K; ++k)
+            if (k < len) sd[o.v0 + base + k] = d[k];
 #pragma unroll
-        for (int u = 0; u < kLatGen; ++u) {
-            if (grow[u] >= 0) {
-                const std::size_t idx = static_cast<std::size_t>(grow[u]) * S + s;
-                const double out = 2.0 * a.zc[idx] - a.zp[idx] + 2.0 * gd[u];
-                a.zp[idx] = out;
-                if (!(fabs(out) <= 1e100)) atomicMin(a.fail + s, a.step);
-            }
-        }
+        for (int u = 0; u < G; ++u)
+            if (grow[u] >= 0) sd[o.v0 + grow[u]] = gd[u];
+        __syncthreads();
+        for (int r = tid; r < nr; r += T) gdrow[r] = sd[o.v0 + r];
+        __syncthreads();  // cl / gw / v buffers are rewritten for the next sample
     }
 }
 
@@ -604,16 +654,24 @@ int launch_substeps(const SubArgs& a, int grid, void* stream) {
     }
 }
 
-int lattice_smem_bytes(const LatArgs& a) { return static_cast<int>(lat_layout(a, nullptr, nullptr)); }
+int lattice_smem_bytes(const LatArgs& a) { return lat_offsets(a).total * static_cast<int>(sizeof(double)); }
 
-int launch_lattice_substeps(const LatArgs& a, int grid, void* stream) {
+template <int T, int K, int G>
+static int launch_lat(const LatArgs& a, int grid, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(lattice_substep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(lattice_substep_kernel<T, K, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         configured = true;
     }
-    lattice_substep_kernel<<<grid, kLatThreads, lattice_smem_bytes(a), static_cast<cudaStream_t>(stream)>>>(a);
+    lattice_substep_kernel<T, K, G><<<grid, T, lattice_smem_bytes(a), st>>>(a);
     return static_cast<int>(cudaGetLastError());
+}
+
+int launch_lattice_substeps(const LatArgs& a, int grid, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (a.threads == 1024 && a.strip_k == 4) return launch_lat<1024, 4, 1>(a, grid, st);
+    if (a.threads == 512 && a.strip_k == 8) return launch_lat<512, 8, 2>(a, grid, st);
+    return static_cast<int>(cudaErrorInvalidValue);
 }
 
 int substep_max_grid(int device, int smem_bytes) {
@@ -622,6 +680,11 @@ int substep_max_grid(int device, int smem_bytes) {
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (smem_bytes > optin) return 0;
     return sms;  // one 1024-thread CTA per SM
+}
+
+void launch_r_update(const RUpdateArgs& a, void* stream) {
+    dim3 grid((a.n_r + kSweepWarps - 1) / kSweepWarps, a.S / kSweepChunk);
+    r_update_kernel<<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_qoi(const QoIArgs& a, void* stream) {

@@ -3,7 +3,11 @@
 // Layout in HBM (per level, per batch of S samples, S a multiple of 64):
 //   z[i * S + s]      nodal state, node-major with samples interleaved, so a
 //                     warp reads one row for 64 samples as 32 x 16 B
-//   g[r * S + s]      A z_n on the R rows (r < n_r), stashed by the sweep
+//   gd[s * G + r]     per-sample rows of R (r < n_r, G = n_r rounded up to 8):
+//                     A z_n written by the sweep (transposed through shared
+//                     memory), read by the substep kernel, overwritten with
+//                     d_p, read by the R update -- sample-major so the
+//                     one-sample-per-CTA substep kernel moves it coalesced
 //   cells[k * S + s]  per-sample coefficient of cell k
 // The geometric operator tables are shared by all samples.
 #pragma once
@@ -30,7 +34,8 @@ struct SweepArgs {
     const double* zc;    // z_n
     double* zp;          // z_{n-1} in, z_{n+1} out; init: z0 out
     double* zc_out;      // init only: z_1 out
-    double* g;
+    double* g;           // gd buffer, rows < split
+    int g_stride;        // G
     double factor;       // init_factor or coarse_factor
     int step;
     int* fail;
@@ -45,24 +50,22 @@ struct SubArgs {
     const int* rc_cell;
     const double* rc_a0;
     const double* cells;
-    const double* g;
-    const double* zc;
-    double* zp;
+    double* gd;           // [s][g_stride]: g in, d_p out
+    int g_stride;
     const double* beta;   // p-1
     const double* cm;     // p-1
     double c0;
-    int step;
-    int* fail;
 };
 
-constexpr int kLatThreads = 512;  // lattice substep kernel
-constexpr int kLatStrip = 8;      // rows per thread (max)
-constexpr int kLatGen = 2;        // generic rows per thread (max)
+// lattice substep kernel variants (threads, rows per thread, generic rows per
+// thread): (1024, 4, 1) and (512, 8, 2); generic SELL rows hold <= 8 entries
+constexpr int kLatGenWidth = 8;
 
 // Substep kernel with the structured fast path: the refined-square lattice
 // L = [1, m-1]^2 (5-point stencil from cell coefficients, state v = d / h)
 // plus generic rows from a per-sample weighted SELL; see kernels.cu.
 struct LatArgs {
+    int threads, strip_k;        // kernel variant
     int n_r, S, count, p, n_cells, cells_x;
     int m, cw, n_strips;
     int n_gen, n_slots;
@@ -73,17 +76,26 @@ struct LatArgs {
     const int* celly;            // m entries
     const int* gen_rows;         // n_gen dofs
     const double* gen_rs;        // 1/sqrt(M)
-    const int* gen_soff;         // slice offsets (slots), ceil(n_gen/32)+1
-    const std::uint16_t* gen_col;  // per slot
-    const int* slot_rc;          // per slot: term range [slot_rc[e], slot_rc[e+1])
+    const std::uint16_t* gen_col;  // per slot: [slice][kLatGenWidth][32], padding: col 0, weight 0
+    const double* slot_a0;       // per slot: a0 of the single term
+    const std::uint8_t* slot_cell;  // per slot: its cell, 0xff when the weight has several terms
+    const int* slot_rc;          // per slot: term range [slot_rc[e], slot_rc[e+1]) (several terms)
     const int* rc_cell;
     const double* rc_a0;
     const double* cells;
-    const double* g;
-    const double* zc;
-    double* zp;
+    double* gd;                  // [s][g_stride]: g in, d_p out
+    int g_stride;
     const double* beta;
     const double* cm;
+};
+
+// z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on the R rows (reference
+// src/integrators.cpp:149-153), d_p transposed back through shared memory.
+struct RUpdateArgs {
+    int n_r, S, count, g_stride;
+    const double* gd;
+    const double* zc;
+    double* zp;
     int step;
     int* fail;
 };
@@ -105,6 +117,7 @@ void launch_sweep_step(const SweepArgs& a, void* stream);
 int substep_smem_bytes(const SubArgs& a);
 int launch_substeps(const SubArgs& a, int grid, void* stream);  // returns cudaError_t
 void launch_qoi(const QoIArgs& a, void* stream);
+void launch_r_update(const RUpdateArgs& a, void* stream);
 void launch_fill_int(int* p, int value, int n, void* stream);
 void launch_pair_diff(const double* qf, const double* qc, double* dq, int count, void* stream);
 int substep_max_grid(int device, int smem_bytes);

@@ -246,10 +246,12 @@ def profile_enable(level: Level, on: bool = True) -> None:
 
 
 def profile_read(level: Level) -> dict:
-    sm, su = C.c_double(), C.c_double()
-    ns, nu = C.c_long(), C.c_long()
-    N.check(N.lib().wmc_profile_read(level._h, C.byref(sm), C.byref(ns), C.byref(su), C.byref(nu)))
-    return {"sweep_ms": sm.value, "sweep_launches": ns.value, "sub_ms": su.value, "sub_launches": nu.value}
+    sm, su, sr = C.c_double(), C.c_double(), C.c_double()
+    ns, nu, nr = C.c_long(), C.c_long(), C.c_long()
+    N.check(N.lib().wmc_profile_read(level._h, C.byref(sm), C.byref(ns), C.byref(su), C.byref(nu), C.byref(sr),
+                                     C.byref(nr)))
+    return {"sweep_ms": sm.value, "sweep_launches": ns.value, "sub_ms": su.value, "sub_launches": nu.value,
+            "upd_ms": sr.value, "upd_launches": nr.value}
 
 
 def launch_count() -> int:

@@ -1,0 +1,35 @@
+"""Run one config-1 level (fine solves only) for a few batches: the small,
+repeatable command profiled with ncu (see profiles/README.md)."""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2106_11117_b200 import configs, wavemc  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--level", type=int, default=0)
+    ap.add_argument("--count", type=int, default=1184)
+    ap.add_argument("--generic", action="store_true", help="mesh without lattice metadata")
+    ap.add_argument("--repeat", type=int, default=2)
+    a = ap.parse_args()
+    d = configs.config1()[a.level]
+    m = configs.build_mesh(d)
+    if a.generic:
+        m = wavemc.Mesh.from_arrays(*m.arrays())
+    lv = wavemc.Level(m, configs.level_spec(d))
+    for r in range(a.repeat):
+        t0 = time.perf_counter()
+        _, q, _ = wavemc.eval_pairs(lv, None, 0, a.level, 0, a.count)
+        dt = time.perf_counter() - t0
+        upd = a.count * lv.info["dof_updates_per_solve"]
+        print(f"level {a.level} lattice={lv.info['lattice']} {a.count} solves {dt:.3f} s "
+              f"{upd / dt:.3e} DOF-updates/s q0={q[0]:.12e}")
+
+
+if __name__ == "__main__":
+    main()
