@@ -105,10 +105,12 @@ class ClockSampler:
 # CPU baselines (the reference compiled from its own sources, else our port)
 
 def ref_sample_counts(threads: int):
-    """Bounded sample of config 1 for the CPU: per level a few samples per
-    thread, sized for ~10-30 s of wall time."""
+    """Bounded sample of config 1 for the CPU, in the proportions of N_l
+    (65536 : 16384 : 4096 : 1024 : 256 ~ 256 : 64 : 16 : 4 : 1), sized for
+    ~10-30 s of wall time on `threads` cores (about 2 s of reference work per
+    thread per level-0 sample batch of 16)."""
     t = max(1, threads)
-    return [4 * t, 2 * t, t, max(1, t // 2), max(1, t // 4)]
+    return [16 * t, 4 * t, t, max(1, t // 4), max(1, t // 16)]
 
 
 def run_reference_cpu(defs, threads: int):

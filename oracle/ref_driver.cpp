@@ -358,37 +358,49 @@ int cmd_mlmc(const Args& a) {
     const std::uint64_t seed = a.u64("seed", 0);
     const int threads = default_threads(a);
     const bool per_sample = a.integer("per-sample", 0) != 0;
+    // one job list over all levels, level-major and index-ascending, run by
+    // one worker pool and folded in (level, index) order -- the reference's
+    // run_jobs (src/mlmc.cpp:107-149, :181-183)
+    struct Job {
+        int level;
+        long index;
+    };
+    std::vector<Job> jobs;
+    for (std::size_t l = 0; l < levels->size(); ++l)
+        for (long i = 0; i < counts[l]; ++i) jobs.push_back({static_cast<int>(l), i});
+    std::vector<SampleResult> results(jobs.size());
+    const double t0 = now_s();
+    parallel_for(static_cast<long>(jobs.size()), threads, [&](long k) {
+        results[k] = sample_delta_q(problem, jobs[k].level,
+                                    derive_stream(seed, static_cast<std::uint32_t>(jobs[k].level),
+                                                  static_cast<std::uint64_t>(jobs[k].index)));
+    });
+    const double total_s = now_s() - t0;
+    double total_upd = 0.0;
     std::printf("{\"threads\": %d, \"levels\": [\n", threads);
-    double total_s = 0.0, total_upd = 0.0;
+    std::size_t k0 = 0;
     for (std::size_t l = 0; l < levels->size(); ++l) {
         const long N = counts[l];
-        std::vector<SampleResult> results(N);
-        const double t0 = now_s();
-        parallel_for(N, threads, [&](long i) {
-            results[i] = sample_delta_q(problem, static_cast<int>(l),
-                                        derive_stream(seed, static_cast<std::uint32_t>(l), static_cast<std::uint64_t>(i)));
-        });
-        const double t1 = now_s();
         LevelAccumulator acc(static_cast<int>(l), kScalarGrid);
-        for (long i = 0; i < N; ++i) acc.add(results[i]);
+        for (long i = 0; i < N; ++i) acc.add(results[k0 + i]);
         const double upd = N * (dof_updates(d, (*levels)[l]) + (l > 0 ? dof_updates(d, (*levels)[l - 1]) : 0.0));
-        total_s += t1 - t0;
         total_upd += upd;
         std::printf("  {\"level\": %zu, \"N\": %ld, \"sum_dq\": %.17g, \"sum_dq2\": %.17g, \"sum_q\": %.17g, "
                     "\"sum_q2\": %.17g, \"variance\": %.17g, \"mc_variance\": %.17g, \"mean_dq\": %.17g, "
-                    "\"seconds\": %.6f, \"dof_updates\": %.17g, \"n\": %zu, \"n_r\": %ld, \"n_steps\": %ld",
+                    "\"dof_updates\": %.17g, \"n\": %zu, \"n_r\": %ld, \"n_steps\": %ld",
                     l, N, acc.sum_dq.values[0], acc.sum_norm2_dq, acc.sum_q.values[0], acc.sum_norm2_q,
                     N >= 2 ? estimate_variance(acc) : 0.0, N >= 2 ? estimate_mc_variance(acc) : 0.0,
-                    acc.mean_dq().values[0], t1 - t0, upd, (*levels)[l].interior.size(), (*levels)[l].n_r,
+                    acc.mean_dq().values[0], upd, (*levels)[l].interior.size(), (*levels)[l].n_r,
                     (*levels)[l].n_steps);
         if (per_sample) {
             std::printf(", \"dq\": [");
-            for (long i = 0; i < N; ++i) std::printf("%s%.17g", i ? ", " : "", results[i].delta_q.values[0]);
+            for (long i = 0; i < N; ++i) std::printf("%s%.17g", i ? ", " : "", results[k0 + i].delta_q.values[0]);
             std::printf("], \"q\": [");
-            for (long i = 0; i < N; ++i) std::printf("%s%.17g", i ? ", " : "", results[i].q_fine.values[0]);
+            for (long i = 0; i < N; ++i) std::printf("%s%.17g", i ? ", " : "", results[k0 + i].q_fine.values[0]);
             std::printf("]");
         }
         std::printf("}%s\n", l + 1 < levels->size() ? "," : "");
+        k0 += static_cast<std::size_t>(N);
     }
     std::printf("], \"seconds\": %.6f, \"dof_updates\": %.17g}\n", total_s, total_upd);
     return 0;

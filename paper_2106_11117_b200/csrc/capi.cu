@@ -240,20 +240,37 @@ void build_device_level(wmc_level& L) {
         // SELL-32 over the generic rows, per slot: column and recipe range
         const int n_gen = static_cast<int>(t.gen_rows.size());
         const int n_slices = (n_gen + 31) / 32;
+        // rows sorted by entry count (descending) so each 32-row slice is
+        // padded only to its own widest row
+        std::vector<int> ord(n_gen);
+        for (int q = 0; q < n_gen; ++q) ord[q] = q;
+        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+            return t.gen_ptr[x + 1] - t.gen_ptr[x] > t.gen_ptr[y + 1] - t.gen_ptr[y];
+        });
+        std::vector<int> grows(n_gen);
+        std::vector<double> grs(n_gen);
+        for (int q = 0; q < n_gen; ++q) {
+            grows[q] = t.gen_rows[ord[q]];
+            grs[q] = t.gen_rs[ord[q]];
+        }
         std::vector<int> soff(n_slices + 1, 0), slot_rc{0}, rc_cell;
         std::vector<std::uint16_t> gcol;
         std::vector<double> rc_a0, slot_a0;
         std::vector<std::uint8_t> slot_cell;
         for (int sl = 0; sl < n_slices; ++sl) {
-            const int width = wmc::kLatGenWidth;  // every slice padded to the fixed width
+            int width = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int q = sl * 32 + l;
+                if (q < n_gen) width = std::max(width, t.gen_ptr[ord[q] + 1] - t.gen_ptr[ord[q]]);
+            }
             for (int e = 0; e < width; ++e)
                 for (int l = 0; l < 32; ++l) {
                     const int q = sl * 32 + l;
                     std::uint16_t c = 0;
                     double a1 = 0.0;
                     std::uint8_t k1 = 0;
-                    if (q < n_gen && e < t.gen_ptr[q + 1] - t.gen_ptr[q]) {
-                        const int ent = t.gen_ptr[q] + e;
+                    if (q < n_gen && e < t.gen_ptr[ord[q] + 1] - t.gen_ptr[ord[q]]) {
+                        const int ent = t.gen_ptr[ord[q]] + e;
                         c = static_cast<std::uint16_t>(t.gen_col[ent]);
                         const int nt = t.gen_rc_ptr[ent + 1] - t.gen_rc_ptr[ent];
                         if (nt == 1) {
@@ -279,8 +296,9 @@ void build_device_level(wmc_level& L) {
         L.d_strip_len = upload(t.strip_len);
         L.d_cellx = upload(t.lat_cellx);
         L.d_celly = upload(t.lat_celly);
-        L.d_gen_rows = upload(t.gen_rows);
-        L.d_gen_rs = upload(t.gen_rs);
+        L.d_gen_rows = upload(grows);
+        L.d_gen_rs = upload(grs);
+        L.d_gen_soff = upload(soff);
         L.d_gen_col = upload(gcol);
         L.d_slot_rc = upload(slot_rc);
         L.d_slot_a0 = upload(slot_a0);
@@ -384,6 +402,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         la.celly = L.d_celly;
         la.gen_rows = L.d_gen_rows;
         la.gen_rs = L.d_gen_rs;
+        la.gen_soff = L.d_gen_soff;
         la.gen_col = L.d_gen_col;
         la.slot_rc = L.d_slot_rc;
         la.slot_a0 = L.d_slot_a0;

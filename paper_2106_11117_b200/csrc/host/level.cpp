@@ -274,6 +274,8 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         const int i = vdof[vi], j = vdof[vj];
         rows[i].emplace_back(j, k, s / std::sqrt(mass[vi] * mass[vj]));
     }
+    // sweep tables: each row's entries in column order (cell-split entries
+    // of one column adjacent)
     L.row_ptr.assign(L.n + 1, 0);
     for (int i = 0; i < L.n; ++i) {
         auto& r = rows[i];

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -57,7 +58,7 @@ __device__ __forceinline__ void flag_fail(int* fail, int s, int count, int step)
 // (reference src/integrators.cpp:89-115; for LTS rows outside R the
 // recursion collapses to factor = -2 d_p(g = 1), :117-157).
 
-template <bool kInit>
+template <bool kInit, bool kParts>
 __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
     __shared__ double2 tile[kSweepWarps][32];  // g of the block's R rows: [row][lane] = samples 2 lane, 2 lane + 1
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -68,20 +69,55 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
     if (row < a.n) {
         const int b = __ldg(a.row_ptr + row), e = __ldg(a.row_ptr + row + 1);
         double acc0 = 0.0, acc1 = 0.0;
-        for (int k = b; k < e; ++k) {
-            const int pk = __ldg(a.ent + k);
-            const double w = __ldg(a.a0 + k);
-            const int j = pk & 0xffffff;
-            const int cell = static_cast<unsigned>(pk) >> 24;
-            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
-            if (kInit) {
-                const double zj = __ldg(a.z0 + j);
-                acc0 += (c.x * w) * zj;
-                acc1 += (c.y * w) * zj;
-            } else {
-                const double2 z = __ldg(reinterpret_cast<const double2*>(a.zc + j * S + s0));
-                acc0 += (c.x * w) * z.x;
-                acc1 += (c.y * w) * z.y;
+        double2 zself = make_double2(0.0, 0.0);
+        if (kParts) {
+            // entries grouped by cell: sum a0 z_j within a part, then scale by
+            // the part's coefficient (one coefficient load per part)
+            double p0 = 0.0, p1 = 0.0;
+            int pcell = static_cast<unsigned>(__ldg(a.ent + b)) >> 24;
+            double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + pcell * S + s0));
+            for (int k = b; k < e; ++k) {
+                const int pk = __ldg(a.ent + k);
+                const double w = __ldg(a.a0 + k);
+                const int j = pk & 0xffffff;
+                const int cell = static_cast<unsigned>(pk) >> 24;
+                if (cell != pcell) {  // warp-uniform
+                    acc0 += c.x * p0;
+                    acc1 += c.y * p1;
+                    p0 = p1 = 0.0;
+                    pcell = cell;
+                    c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+                }
+                if (kInit) {
+                    const double zj = __ldg(a.z0 + j);
+                    p0 += w * zj;
+                    p1 += w * zj;
+                } else {
+                    const double2 z = __ldg(reinterpret_cast<const double2*>(a.zc + j * S + s0));
+                    if (j == row) zself = z;
+                    p0 += w * z.x;
+                    p1 += w * z.y;
+                }
+            }
+            acc0 += c.x * p0;
+            acc1 += c.y * p1;
+        } else {
+            for (int k = b; k < e; ++k) {
+                const int pk = __ldg(a.ent + k);
+                const double w = __ldg(a.a0 + k);
+                const int j = pk & 0xffffff;
+                const int cell = static_cast<unsigned>(pk) >> 24;
+                const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+                if (kInit) {
+                    const double zj = __ldg(a.z0 + j);
+                    acc0 += (c.x * w) * zj;
+                    acc1 += (c.y * w) * zj;
+                } else {
+                    const double2 z = __ldg(reinterpret_cast<const double2*>(a.zc + j * S + s0));
+                    if (j == row) zself = z;
+                    acc0 += (c.x * w) * z.x;
+                    acc1 += (c.y * w) * z.y;
+                }
             }
         }
         const std::size_t idx = row * S + s0;
@@ -98,7 +134,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
         } else if (row < a.split) {
             tile[warp][lane] = make_double2(acc0, acc1);
         } else {
-            const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
+            const double2 zn = zself;  // every row holds its diagonal entry
             const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
             double2 out;
             out.x = 2.0 * zn.x - zm.x - a.factor * acc0;
@@ -353,8 +389,9 @@ __host__ __device__ inline LatOff lat_offsets(const LatArgs& a) {
 // coefficients; a coefficient line always starts a strip, so a thread needs
 // one set of constants for its first row and one for the rest.  Generic rows
 // (box ring + transition belt, G per thread) use a SELL of per-sample
-// weights w_ij = A_ij(omega) sqrt(M_j) on v, padded to kLatGenWidth slots so
-// the gather is straight-line code.  Rows past a short strip compute on
+// weights w_ij = A_ij(omega) sqrt(M_j) on v; rows are sorted by length and
+// each warp-wide slice is padded to its widest row, the gather is predicated
+// straight-line code.  Rows past a short strip compute on
 // clamped addresses and never store.
 template <int T, int K, int G>
 __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
@@ -396,15 +433,17 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
     const int col = tid % a.cw, strip = tid / a.cw;
     const int ci = 1 + col;
     const bool lat_on = ci <= a.m - 1 && strip < a.n_strips;
-    // generic role: list entries tid + u*T, slots [slice][kLatGenWidth][32]
-    int grow[G], gslot[G];
+    // generic role: list entries tid + u*T, slots [slice][width][32]
+    int grow[G], gslot[G], gwid[G];
     double grs[G];
 #pragma unroll
     for (int u = 0; u < G; ++u) {
         const int q = tid + u * T;
         grow[u] = q < a.n_gen ? __ldg(a.gen_rows + q) : -1;
         grs[u] = q < a.n_gen ? __ldg(a.gen_rs + q) : 0.0;
-        gslot[u] = (q < a.n_gen ? (q >> 5) * (32 * kLatGenWidth) : 0) + lane;  // idle lanes read slice 0
+        const int sl = q < a.n_gen ? q >> 5 : 0;  // idle lanes point at slice 0, width 0
+        gslot[u] = __ldg(a.gen_soff + sl) + lane;
+        gwid[u] = q < a.n_gen ? (__ldg(a.gen_soff + sl + 1) - __ldg(a.gen_soff + sl)) >> 5 : 0;
     }
     __syncthreads();
     int j0 = 1, len = 0;
@@ -483,7 +522,10 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
 #pragma unroll
                 for (int e = 0; e < kLatGenWidth; ++e) {
                     const int q = gslot[u] + 32 * e;
-                    acc += sd[o.gw + q] * sd[cur + gcol[q]];
+                    const bool on = e < gwid[u];  // warp-uniform: predicated loads, no branch
+                    const double w = on ? sd[o.gw + q] : 0.0;
+                    const double v = on ? sd[cur + gcol[q]] : 0.0;
+                    acc += w * v;
                 }
                 gaq[u] = acc;
             }
@@ -615,12 +657,19 @@ void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t fi
 
 void launch_sweep_init(const SweepArgs& a, void* stream) {
     dim3 grid((a.n + kSweepWarps - 1) / kSweepWarps, a.S / kSweepChunk);
-    sweep_kernel<true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    sweep_kernel<true, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_sweep_step(const SweepArgs& a, void* stream) {
     dim3 grid((a.n + kSweepWarps - 1) / kSweepWarps, a.S / kSweepChunk);
-    sweep_kernel<false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    static const int parts = [] {
+        const char* v = std::getenv("WMC_SWEEP_PARTS");  // tuning knob
+        return v ? std::atoi(v) : 0;
+    }();
+    if (parts)
+        sweep_kernel<false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    else
+        sweep_kernel<false, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 int substep_smem_bytes(const SubArgs& a) { return static_cast<int>(sub_layout(a, nullptr, nullptr)); }

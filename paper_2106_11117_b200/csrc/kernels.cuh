@@ -76,7 +76,8 @@ struct LatArgs {
     const int* celly;            // m entries
     const int* gen_rows;         // n_gen dofs
     const double* gen_rs;        // 1/sqrt(M)
-    const std::uint16_t* gen_col;  // per slot: [slice][kLatGenWidth][32], padding: col 0, weight 0
+    const int* gen_soff;         // slot offset of each 32-row slice (rows sorted by length), n_slices + 1
+    const std::uint16_t* gen_col;  // per slot: [slice][width][32], padding: col 0, weight 0
     const double* slot_a0;       // per slot: a0 of the single term
     const std::uint8_t* slot_cell;  // per slot: its cell, 0xff when the weight has several terms
     const int* slot_rc;          // per slot: term range [slot_rc[e], slot_rc[e+1]) (several terms)
