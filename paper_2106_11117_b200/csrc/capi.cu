@@ -7,6 +7,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -244,9 +245,12 @@ void build_device_level(wmc_level& L) {
         // padded only to its own widest row
         std::vector<int> ord(n_gen);
         for (int q = 0; q < n_gen; ++q) ord[q] = q;
-        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
-            return t.gen_ptr[x + 1] - t.gen_ptr[x] > t.gen_ptr[y + 1] - t.gen_ptr[y];
-        });
+        const char* pad8 = std::getenv("WMC_GEN_PAD8");  // tuning: unsorted, every slice 8 wide
+        const bool fixed_width = pad8 && std::atoi(pad8);
+        if (!fixed_width)
+            std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+                return t.gen_ptr[x + 1] - t.gen_ptr[x] > t.gen_ptr[y + 1] - t.gen_ptr[y];
+            });
         std::vector<int> grows(n_gen);
         std::vector<double> grs(n_gen);
         for (int q = 0; q < n_gen; ++q) {
@@ -258,7 +262,7 @@ void build_device_level(wmc_level& L) {
         std::vector<double> rc_a0, slot_a0;
         std::vector<std::uint8_t> slot_cell;
         for (int sl = 0; sl < n_slices; ++sl) {
-            int width = 0;
+            int width = fixed_width ? wmc::kLatGenWidth : 0;
             for (int l = 0; l < 32; ++l) {
                 const int q = sl * 32 + l;
                 if (q < n_gen) width = std::max(width, t.gen_ptr[ord[q] + 1] - t.gen_ptr[ord[q]]);

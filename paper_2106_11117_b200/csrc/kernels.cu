@@ -519,14 +519,22 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 double acc = 0.0;
-#pragma unroll
-                for (int e = 0; e < kLatGenWidth; ++e) {
-                    const int q = gslot[u] + 32 * e;
-                    const bool on = e < gwid[u];  // warp-uniform: predicated loads, no branch
-                    const double w = on ? sd[o.gw + q] : 0.0;
-                    const double v = on ? sd[cur + gcol[q]] : 0.0;
-                    acc += w * v;
+                // warp-uniform jump into a straight-line gather of the
+                // slice's width (Duff's device; widths are <= kLatGenWidth)
+                const int q0 = gslot[u];
+#define WMC_GEN_SLOT(E) acc += sd[o.gw + q0 + 32 * (E)] * sd[cur + gcol[q0 + 32 * (E)]]
+                switch (gwid[u]) {
+                    case 8: WMC_GEN_SLOT(7); [[fallthrough]];
+                    case 7: WMC_GEN_SLOT(6); [[fallthrough]];
+                    case 6: WMC_GEN_SLOT(5); [[fallthrough]];
+                    case 5: WMC_GEN_SLOT(4); [[fallthrough]];
+                    case 4: WMC_GEN_SLOT(3); [[fallthrough]];
+                    case 3: WMC_GEN_SLOT(2); [[fallthrough]];
+                    case 2: WMC_GEN_SLOT(1); [[fallthrough]];
+                    case 1: WMC_GEN_SLOT(0); [[fallthrough]];
+                    default: break;
                 }
+#undef WMC_GEN_SLOT
                 gaq[u] = acc;
             }
             const int ce = cur + base + W, cw_ = cur + base - W;
