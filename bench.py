@@ -202,7 +202,7 @@ def reference_arm(args, world, rank):
 def b200_arm(args, world, rank, local):
     import torch
 
-    from paper_2106_11117_b200 import configs, wavemc
+    from paper_2106_11117_b200 import configs, shard, wavemc
 
     torch.cuda.set_device(local)
     dist = None
@@ -212,12 +212,9 @@ def b200_arm(args, world, rank, local):
     defs = configs.config1()
     counts_total = [max(1, int(round(n * args.scale))) for n in configs.CONFIG1_COUNTS]
     levels = [configs.build_level(d, device=local) for d in defs]
-    first = [r * 0 for r in counts_total]
-    counts = []
-    for l, n in enumerate(counts_total):
-        a, b = rank * n // world, (rank + 1) * n // world
-        first[l] = a
-        counts.append(b - a)
+    spans = [shard.shard_range(n, rank, world) for n in counts_total]
+    first = [f for f, _ in spans]
+    counts = [c for _, c in spans]
     upd = [lv.info["dof_updates_per_solve"] for lv in levels]
     per_pair = [upd[l] + (upd[l - 1] if l else 0.0) for l in range(len(levels))]
     total_updates = sum(n * per_pair[l] for l, n in enumerate(counts_total))
@@ -281,12 +278,7 @@ def b200_arm(args, world, rank, local):
     # order) per step, plus the allreduce of the per-level sums
     def step_e2e():
         stats = wavemc.run_mlmc_fixed(levels, counts, 0, first)
-        if dist is not None:
-            t = torch.tensor([[s["sum_dq"], s["sum_dq2"], s["sum_q"], s["sum_q2"], s["n_samples"]] for s in stats],
-                             dtype=torch.float64, device=dev)
-            dist.all_reduce(t)
-            t.cpu()
-        return stats
+        return shard.allreduce_level_sums(stats, device=dev)
 
     step_e2e()
     barrier()
@@ -343,7 +335,7 @@ def b200_arm(args, world, rank, local):
             "gpu_launches": launches, "clocks": clocks.summary(),
             "moments": [{"level": l, "sum_dq": mom[4 * l], "sum_dq2": mom[4 * l + 1], "sum_q": mom[4 * l + 2],
                          "sum_q2": mom[4 * l + 3]} for l in range(len(levels))],
-            "variance": [s["variance"] for s in stats] if world == 1 else None}
+            "variance": [s["variance"] for s in stats]}
     if roofline is not None:
         line["roofline"] = roofline
         line["kernels"] = kernels
