@@ -97,6 +97,7 @@ struct wmc_level {
 
     // sweep operator
     int* d_row_ptr = nullptr;
+    signed char* d_row_cell = nullptr;
     int* d_ent = nullptr;
     double* d_a0 = nullptr;
     double* d_z0 = nullptr;
@@ -119,6 +120,7 @@ struct wmc_level {
     // structured substep path
     bool lattice = false;
     int* d_strip_j0 = nullptr;
+    unsigned char* d_lat_smask = nullptr;
     int* d_strip_len = nullptr;
     int* d_cellx = nullptr;
     int* d_celly = nullptr;
@@ -144,10 +146,10 @@ struct wmc_level {
 
     ~wmc_level() {
         cudaSetDevice(device);
-        for (void* p : {(void*)d_row_ptr, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
+        for (void* p : {(void*)d_row_ptr, (void*)d_row_cell, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
                         (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
                         (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
-                        (void*)d_strip_j0, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
+                        (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_grc_cell,
                         (void*)d_grc_a0})
@@ -175,6 +177,16 @@ void build_device_level(wmc_level& L) {
     std::vector<int> ent(t.col.size());
     for (std::size_t k = 0; k < ent.size(); ++k) ent[k] = t.col[k] | (t.cell[k] << 24);
     L.d_row_ptr = upload(t.row_ptr);
+    {
+        std::vector<signed char> rc(t.n, -1);
+        for (int i = 0; i < t.n; ++i) {
+            int c = t.cell[t.row_ptr[i]];
+            for (int k = t.row_ptr[i]; k < t.row_ptr[i + 1]; ++k)
+                if (t.cell[k] != c) c = -1;
+            rc[i] = static_cast<signed char>(c < 128 ? c : -1);
+        }
+        L.d_row_cell = upload(rc);
+    }
     L.d_ent = upload(ent);
     L.d_a0 = upload(t.a0);
     L.d_z0 = upload(t.z0);
@@ -297,6 +309,27 @@ void build_device_level(wmc_level& L) {
         }
         L.n_slots = static_cast<int>(gcol.size());
         L.d_strip_j0 = upload(t.strip_j0);
+        {
+            // nodes read through shared memory by another thread: warp-edge
+            // lanes (E/W shuffles stop there), strip ends (N/S across
+            // strips) and every lattice node a generic row gathers
+            const int W = t.lat_m + 1;
+            std::vector<std::uint8_t> gen_read(static_cast<std::size_t>(W) * W, 0);
+            for (int c : t.gen_col)
+                if (c < W * W) gen_read[c] = 1;
+            std::vector<unsigned char> mask(t.lat_threads, 0);
+            for (int tid = 0; tid < t.lat_threads; ++tid) {
+                const int col = tid % t.lat_cw, strip = tid / t.lat_cw, ci = 1 + col;
+                if (ci > t.lat_m - 1 || strip >= static_cast<int>(t.strip_j0.size())) continue;
+                const int lane = tid & 31, j0 = t.strip_j0[strip], len = t.strip_len[strip];
+                for (int k = 0; k < len; ++k) {
+                    const bool ext = lane == 0 || lane == 31 || k == 0 || k == len - 1 ||
+                                     gen_read[static_cast<std::size_t>(ci) * W + j0 + k];
+                    if (ext) mask[tid] |= static_cast<unsigned char>(1u << k);
+                }
+            }
+            L.d_lat_smask = upload(mask);
+        }
         L.d_strip_len = upload(t.strip_len);
         L.d_cellx = upload(t.lat_cellx);
         L.d_celly = upload(t.lat_celly);
@@ -369,6 +402,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     sw.S = S;
     sw.count = count;
     sw.row_ptr = L.d_row_ptr;
+    sw.row_cell = L.d_row_cell;
     sw.ent = L.d_ent;
     sw.a0 = L.d_a0;
     sw.cells = cells;
@@ -401,6 +435,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         la.inv_h = t.lat_inv_h;
         la.c0 = t.c0;
         la.strip_j0 = L.d_strip_j0;
+        la.lat_smask = L.d_lat_smask;
         la.strip_len = L.d_strip_len;
         la.cellx = L.d_cellx;
         la.celly = L.d_celly;

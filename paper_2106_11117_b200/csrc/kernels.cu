@@ -101,7 +101,30 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             }
             acc0 += c.x * p0;
             acc1 += c.y * p1;
+        } else if (a.row_cell && __ldg(a.row_cell + row) >= 0) {
+            // the row's elements all lie in one coefficient cell: one
+            // coefficient load, A(omega)_ij = c * a0_ij
+            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + __ldg(a.row_cell + row) * S + s0));
+            double p0 = 0.0, p1 = 0.0;
+#pragma unroll 4
+            for (int k = b; k < e; ++k) {
+                const int j = __ldg(a.ent + k) & 0xffffff;
+                const double w = __ldg(a.a0 + k);
+                if (kInit) {
+                    const double zj = __ldg(a.z0 + j);
+                    p0 += w * zj;
+                    p1 += w * zj;
+                } else {
+                    const double2 z = __ldg(reinterpret_cast<const double2*>(a.zc + j * S + s0));
+                    if (j == row) zself = z;
+                    p0 += w * z.x;
+                    p1 += w * z.y;
+                }
+            }
+            acc0 = c.x * p0;
+            acc1 = c.y * p1;
         } else {
+#pragma unroll 4
             for (int k = b; k < e; ++k) {
                 const int pk = __ldg(a.ent + k);
                 const double w = __ldg(a.a0 + k);

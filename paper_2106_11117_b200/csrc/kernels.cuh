@@ -29,6 +29,7 @@ struct SweepArgs {
     const int* row_ptr;
     const int* ent;      // col | cell << 24
     const double* a0;
+    const signed char* row_cell;  // cell of a single-cell row, -1 otherwise (may be NULL)
     const double* cells;
     const double* z0;    // init only
     const double* zc;    // z_n
@@ -72,6 +73,7 @@ struct LatArgs {
     double inv_h, c0;
     const int* strip_j0;
     const int* strip_len;
+    const unsigned char* lat_smask;  // per thread: bit k set if the strip's node k is read through shared memory
     const int* cellx;            // m entries
     const int* celly;            // m entries
     const int* gen_rows;         // n_gen dofs
