@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import shutil
 import subprocess
@@ -29,6 +30,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 METRIC = "DOF-updates/s (FP64, LTS substeps incl.)"
+TTR_EPS = 1e-4  # RMSE target of the time-to-RMSE run (config-1 hierarchy)
 UNIT = "DOF-updates/s"
 
 
@@ -161,6 +163,24 @@ def run_port_cpu(defs, threads: int):
             "cores": threads}
 
 
+def reference_time_to_rmse(defs, threads: int):
+    """The reference's own run_mlmc (src/mlmc.cpp:165-233) to RMSE TTR_EPS on
+    the config-1 hierarchy, wall time measured by the driver."""
+    import oracle_py
+    from paper_2106_11117_b200 import configs
+    tmp = tempfile.mkdtemp(prefix="wmc_ttr_")
+    specs = []
+    for l, d in enumerate(defs):
+        p = os.path.join(tmp, f"l{l}.mesh")
+        configs.build_mesh(d).dump(p)
+        specs.append((p, d.dt, d.substeps))
+    res = oracle_py.RefDriver().adaptive(specs, TTR_EPS, threads=threads)
+    shutil.rmtree(tmp, ignore_errors=True)
+    return {"eps": TTR_EPS, "seconds": res["seconds"], "rmse": math.sqrt(res["total_variance"] + res["bias"]),
+            "converged": res["converged"], "estimate": res["estimate"], "N_l": [lv["N"] for lv in res["levels"]],
+            "threads": res["threads"]}
+
+
 def cpu_baseline(defs, threads: int):
     import oracle_py
     if os.path.exists(oracle_py.REF_DRIVER):
@@ -183,6 +203,11 @@ def reference_arm(args, world, rank):
         return 0
     timed = runs[args.warmup:]
     value = sum(r["dof_updates"] for r in timed) / sum(r["seconds"] for r in timed)
+    ttr = None
+    try:
+        ttr = reference_time_to_rmse(defs, threads)
+    except Exception as exc:
+        ttr = {"eps": TTR_EPS, "error": str(exc)}
     r0 = timed[0]
     sample = (f"config 1 bounded sample N_l={r0['counts']} (of {configs.CONFIG1_COUNTS}) per step, "
               f"{r0['cores']} threads, {r0['kind']}")
@@ -194,7 +219,8 @@ def reference_arm(args, world, rank):
                        "parallelism": f"{r0['cores']} CPU threads"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": r0["cores"], "kind": r0["kind"],
                              "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "time_to_rmse": ttr}
     print(json.dumps(line))
     return 0
 
@@ -297,6 +323,18 @@ def b200_arm(args, world, rank, local):
         e2e_ms = float(t.item())
     d2h = sum(16 * c + 4 * c * (2 if l else 1) for l, c in enumerate(counts))
 
+    # MLMC time-to-RMSE: the adaptive driver (reference run_mlmc, batched)
+    # from scratch to convergence at TTR_EPS, wall time around the public call
+    ttr = None
+    if world == 1:
+        costs = [lv.info["dof_updates_per_solve"] for lv in levels]
+        wavemc.run_mlmc(levels, costs, wavemc.MlmcConfig(eps=TTR_EPS * 4))  # warm-up
+        torch.cuda.synchronize(dev)
+        t_0 = time.perf_counter()
+        res = wavemc.run_mlmc(levels, costs, wavemc.MlmcConfig(eps=TTR_EPS))
+        ttr = {"eps": TTR_EPS, "seconds": time.perf_counter() - t_0, "rmse": res.rmse, "converged": res.converged,
+               "estimate": res.estimate, "N_l": [lv["n_samples"] for lv in res.levels]}
+
     # kernel-level profile pass (not timed above): per-kernel device time
     roofline, kernels = None, None
     if not args.no_profile:
@@ -336,6 +374,8 @@ def b200_arm(args, world, rank, local):
             "moments": [{"level": l, "sum_dq": mom[4 * l], "sum_dq2": mom[4 * l + 1], "sum_q": mom[4 * l + 2],
                          "sum_q2": mom[4 * l + 3]} for l in range(len(levels))],
             "variance": [s["variance"] for s in stats]}
+    if ttr is not None:
+        line["time_to_rmse"] = ttr
     if roofline is not None:
         line["roofline"] = roofline
         line["kernels"] = kernels

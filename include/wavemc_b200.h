@@ -190,6 +190,12 @@ typedef struct {
 int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
                  wmc_mlmc_result* result, wmc_level_stats* stats, wmc_error* err);
 
+/* Host-only helpers of the adaptive driver, as the reference's
+ * optimal_samples (src/mlmc.cpp:75-92) and bias_proxy_sq (:94-98). */
+int wmc_optimal_samples(const double* variances, const double* costs, int n_levels, double eps, long min_samples,
+                        long* out);
+double wmc_bias_proxy_sq(double mean_dq, double alpha);
+
 /* Device-side per-level fold: d_out[0..3] += {sum dq, sum dq^2, sum q, sum q^2}
  * over count device values, one fixed-order block (deterministic). */
 int wmc_moments_device(wmc_level* level, const double* d_dq, const double* d_q, uint64_t count, double* d_out);

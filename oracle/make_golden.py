@@ -96,6 +96,14 @@ def main():
     specs = [(paths[f"config1_l{l}"], d.dt, d.substeps) for l, d in enumerate(c1)]
     pairs = ref.mlmc(specs, [6, 6, 4, 3, 2], per_sample=True)
     dump("config1_pairs.json", pairs)
+
+    # adaptive Giles driver (reference run_mlmc) on the config-1 hierarchy;
+    # model cost = DOF-updates of one solve on the level
+    adaptive = ref.adaptive(specs, 2e-4)
+    adaptive["eps"] = 2e-4
+    adaptive["model_cost"] = [lv["n"] + (lv["n_steps"] - 1) * (lv["n"] + (d.substeps - 1) * lv["n_r"])
+                              for lv, d in zip(pairs["levels"], c1)]
+    dump("config1_adaptive.json", adaptive)
     print("golden fixtures written to", GOLDEN)
 
 

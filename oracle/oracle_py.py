@@ -183,6 +183,14 @@ class RefDriver:
             args += [f"--{k}", v]
         return json.loads(self.run(*args))
 
+    def adaptive(self, specs, eps, threads=0, seed=0, max_level=6, kind="lts"):
+        """Reference run_mlmc (src/mlmc.cpp:165-233) over the given levels."""
+        args = ["adaptive", "--kind", kind, "--eps", repr(eps), "--threads", threads, "--seed", seed,
+                "--max-level", max_level]
+        for mesh_path, dt, p in specs:
+            args += ["--level-spec", f"{mesh_path},{dt!r},{p}"]
+        return json.loads(self.run(*args))
+
     def level(self, mesh_path, dt, p, kind="lts"):
         out = self.run("level", "--level-spec", f"{mesh_path},{dt!r},{p}", "--kind", kind)
         rows = [l.split() for l in out.strip().splitlines()[1:]]

@@ -94,6 +94,8 @@ SIGNATURES = [
                                      P(Error)]),
     ("wmc_mlmc_config_default", None, [P(MlmcConfig)]),
     ("wmc_run_mlmc", C.c_int, [P(_VP), C.c_int, _DP, P(MlmcConfig), P(MlmcResult), P(LevelStats), P(Error)]),
+    ("wmc_optimal_samples", C.c_int, [_DP, _DP, C.c_int, C.c_double, C.c_long, P(C.c_long)]),
+    ("wmc_bias_proxy_sq", C.c_double, [C.c_double, C.c_double]),
     ("wmc_moments_device", C.c_int, [_VP, _VP, _VP, C.c_uint64, _VP]),
     ("wmc_profile_enable", C.c_int, [_VP, C.c_int]),
     ("wmc_profile_read", C.c_int, [_VP, _DP, P(C.c_long), _DP, P(C.c_long), _DP, P(C.c_long)]),

@@ -677,6 +677,30 @@ void run_level(wmc_level** levels, int l, std::uint64_t seed, long first, long c
 }  // namespace
 
 namespace {
+// reference optimal_samples (src/mlmc.cpp:75-92):
+// N_l = max(min, ceil((2/eps^2) sqrt(V_l/C_l) sum sqrt(V C) - 1e-9))
+std::vector<long> optimal_samples_impl(const double* v, const double* c, int n, double eps, long min_samples) {
+    double total = 0.0;
+    for (int l = 0; l < n; ++l) {
+        if (!(c[l] > 0.0)) throw ConfigError("optimal_samples: costs must be positive");
+        if (v[l] < 0.0) throw ConfigError("optimal_samples: negative variance");
+        total += std::sqrt(v[l] * c[l]);
+    }
+    std::vector<long> out(n);
+    for (int l = 0; l < n; ++l) {
+        const double nl = 2.0 / (eps * eps) * std::sqrt(v[l] / c[l]) * total;
+        out[l] = std::max(min_samples, static_cast<long>(std::ceil(nl - 1e-9)));
+    }
+    return out;
+}
+
+// reference bias_proxy_sq (src/mlmc.cpp:94-98) on the scalar QoI
+double bias_proxy_impl(double mean_dq, double alpha) {
+    const double denom = std::pow(2.0, alpha) - 1.0;
+    const double norm = std::sqrt(mean_dq * mean_dq) / denom;
+    return norm * norm;
+}
+
 wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     if (desc->integrator != WMC_LEAPFROG && desc->integrator != WMC_LOCAL_TIME_STEPPING)
         throw ConfigError("wmc_level_create: unknown integrator");
@@ -950,11 +974,7 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
         int top = std::min(cfg->initial_levels, cap);
         std::vector<Acc> acc(top + 1);
         std::vector<long> targets(top + 1, cfg->initial_samples);
-        auto bias_proxy = [&](double mean) {
-            const double denom = std::pow(2.0, cfg->alpha) - 1.0;
-            const double norm = std::sqrt(mean * mean) / denom;
-            return norm * norm;
-        };
+        auto bias_proxy = [&](double mean) { return bias_proxy_impl(mean, cfg->alpha); };
         auto bias_window = [&]() {
             double worst = 0.0;
             for (int j = 0; j < cfg->bias_window && top - j >= 1; ++j) {
@@ -969,18 +989,12 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
                 for (int l = 0; l <= top; ++l)
                     if (acc[l].n < targets[l]) run_level(levels, l, cfg->master_seed, acc[l].n, targets[l] - acc[l].n, acc[l], err);
                 std::vector<double> v(top + 1);
-                double total = 0.0;
-                for (int l = 0; l <= top; ++l) {
-                    v[l] = acc[l].variance();
-                    if (!(model_cost[l] > 0.0)) throw ConfigError("optimal_samples: costs must be positive");
-                    total += std::sqrt(v[l] * model_cost[l]);
-                }
+                for (int l = 0; l <= top; ++l) v[l] = acc[l].variance();
+                const std::vector<long> wanted = optimal_samples_impl(v.data(), model_cost, top + 1, cfg->eps, 2);
                 bool increased = false;
                 for (int l = 0; l <= top; ++l) {
-                    const double nl = 2.0 / (cfg->eps * cfg->eps) * std::sqrt(v[l] / model_cost[l]) * total;
-                    const long want = std::max(2L, static_cast<long>(std::ceil(nl - 1e-9)));
-                    if (want > targets[l]) {
-                        targets[l] = want;
+                    if (wanted[l] > targets[l]) {
+                        targets[l] = wanted[l];
                         increased = true;
                     }
                 }
@@ -1010,6 +1024,18 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
 }
 
 long wmc_launch_count(void) { return g_launches.load(); }
+
+int wmc_optimal_samples(const double* variances, const double* costs, int n_levels, double eps, long min_samples,
+                        long* out) {
+    return guarded([&] {
+        if (!variances || !costs || !out || n_levels < 1) throw ConfigError("wmc_optimal_samples: bad arguments");
+        if (!(eps > 0.0)) throw ConfigError("wmc_optimal_samples: eps must be positive");
+        const std::vector<long> r = optimal_samples_impl(variances, costs, n_levels, eps, min_samples);
+        std::copy(r.begin(), r.end(), out);
+    });
+}
+
+double wmc_bias_proxy_sq(double mean_dq, double alpha) { return bias_proxy_impl(mean_dq, alpha); }
 
 int wmc_moments_device(wmc_level* level, const double* d_dq, const double* d_q, uint64_t count, double* d_out) {
     return guarded([&] {

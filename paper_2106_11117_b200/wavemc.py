@@ -236,6 +236,21 @@ def run_mlmc(levels: list[Level], model_cost: list[float], config: MlmcConfig | 
                       res.total_model_cost, res.rmse, [_stats(stats[i]) for i in range(res.levels_used + 1)])
 
 
+def optimal_samples(variances, costs, eps: float, min_samples: int = 2) -> list[int]:
+    """Reference optimal_samples (src/mlmc.cpp:75-92)."""
+    n = len(variances)
+    v = (C.c_double * n)(*variances)
+    c = (C.c_double * n)(*costs)
+    out = (C.c_long * n)()
+    N.check(N.lib().wmc_optimal_samples(v, c, n, eps, min_samples, out))
+    return list(out)
+
+
+def bias_proxy_sq(mean_dq: float, alpha: float = 2.0) -> float:
+    """Reference bias_proxy_sq (src/mlmc.cpp:94-98) on the scalar QoI."""
+    return N.lib().wmc_bias_proxy_sq(mean_dq, alpha)
+
+
 def moments_device(level: Level, d_dq: int, d_q: int, count: int, d_out: int) -> None:
     """d_out[0..3] += {sum dq, sum dq^2, sum q, sum q^2} on the device."""
     N.check(N.lib().wmc_moments_device(level._h, d_dq, d_q, count, d_out))

@@ -216,3 +216,20 @@ def test_config1_level0_full_batch_spot_checks(coracle):
         assert abs(qf[i] - ref[0]) / abs(ref[0]) < QOI_RTOL, i
     _, tail, _ = wavemc.eval_pairs(lv, None, 0, 0, n - 100, 100)
     assert np.array_equal(tail, qf[-100:])
+
+
+def test_adaptive_mlmc_matches_reference_run_mlmc(golden):
+    """wmc_run_mlmc against the reference's own run_mlmc (src/mlmc.cpp:165-233)
+    on the config-1 hierarchy: same sample counts per level, estimates within
+    the moment tolerance."""
+    g = golden("config1_adaptive.json")
+    levels = [configs.build_level(d) for d in configs.config1()]
+    res = wavemc.run_mlmc(levels, g["model_cost"], wavemc.MlmcConfig(eps=g["eps"]))
+    assert res.converged == g["converged"]
+    assert res.levels_used + 1 == len(g["levels"])
+    for got, want in zip(res.levels, g["levels"]):
+        assert got["n_samples"] == want["N"]
+        assert got["variance"] == pytest.approx(want["variance"], rel=MOMENT_RTOL)
+    assert res.estimate == pytest.approx(g["estimate"], rel=MOMENT_RTOL)
+    assert res.total_variance == pytest.approx(g["total_variance"], rel=MOMENT_RTOL)
+    assert res.bias == pytest.approx(g["bias"], rel=MOMENT_RTOL)

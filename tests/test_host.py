@@ -117,3 +117,20 @@ def test_mesh_round_trip_through_arrays():
     b = wavemc.level_plan(m2, configs.level_spec(configs.config0()))
     assert a.pop("lattice") == 1 and b.pop("lattice") == 0  # arrays carry no refined-box metadata
     assert a == b
+
+
+def test_optimal_samples_known_answers():
+    """reference tests/test_mlmc.cpp:89-96"""
+    assert wavemc.optimal_samples([1.0, 0.25], [1.0, 4.0], 1.0) == [4, 2]
+    assert wavemc.optimal_samples([0.7], [5.0], 0.1) == [140]
+    base = wavemc.optimal_samples([1.0, 0.3, 0.02], [1.0, 8.0, 64.0], 0.05)
+    assert base == wavemc.optimal_samples([1.0, 0.3, 0.02], [100.0, 800.0, 6400.0], 0.05)
+    with pytest.raises(wavemc.ConfigError):
+        wavemc.optimal_samples([1.0], [0.0], 1.0)
+
+
+def test_bias_proxy_known_answers():
+    """reference tests/test_mlmc.cpp:137-142"""
+    assert wavemc.bias_proxy_sq(0.0, 2.0) == 0.0
+    assert wavemc.bias_proxy_sq(3e-5, 2.0) == pytest.approx(1e-10, rel=1e-12)
+    assert wavemc.bias_proxy_sq(3e-5, 1.0) == pytest.approx(9.0 * wavemc.bias_proxy_sq(3e-5, 2.0), rel=1e-12)
