@@ -103,6 +103,7 @@ typedef struct {
     int batch;                /* samples per device batch */
     double dof_updates_per_solve;  /* n + (n_steps-1)(n + (p-1)|R|) for LTS, n_steps*n for LF */
     int lattice;              /* 1: substeps use the structured refined-square kernel */
+    int substep_path;         /* 0 none (LF or p = 1), 1 lattice, 2 generic on-chip, 3 HBM-resident; -1 plan only */
 } wmc_level_info;
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);

@@ -35,7 +35,8 @@ class LevelDesc(C.Structure):
 class LevelInfo(C.Structure):
     _fields_ = [("n", C.c_int), ("n_r", C.c_int), ("n_p", C.c_int), ("p", C.c_int), ("n_steps", C.c_long),
                 ("dt", C.c_double), ("nnz", C.c_long), ("ap_nnz", C.c_long), ("n_recipes", C.c_long),
-                ("batch", C.c_int), ("dof_updates_per_solve", C.c_double), ("lattice", C.c_int)]
+                ("batch", C.c_int), ("dof_updates_per_solve", C.c_double), ("lattice", C.c_int),
+                ("substep_path", C.c_int)]
 
 
 class Cost(C.Structure):

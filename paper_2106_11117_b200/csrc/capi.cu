@@ -86,7 +86,11 @@ struct Workspace {
     double* g = nullptr;
     double* q = nullptr;
     int* fail = nullptr;
+    double* da = nullptr;  // HBM-resident substep path: d buffers [r][S]
+    double* db = nullptr;
 };
+
+enum class SubPath { None, Lattice, OnChip, Global };
 
 struct wmc_level {
     int device = 0;
@@ -113,6 +117,10 @@ struct wmc_level {
     double* d_cm = nullptr;
     int sub_smem = 0;
     int sub_grid = 0;
+    SubPath path = SubPath::None;
+    int* d_apg_ptr = nullptr;
+    int* d_apg_ent = nullptr;
+    double* d_apg_a0 = nullptr;
     // QoI
     int* d_qdof = nullptr;
     double* d_qw = nullptr;
@@ -152,10 +160,10 @@ struct wmc_level {
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_grc_cell,
-                        (void*)d_grc_a0})
+                        (void*)d_grc_a0, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
             if (p) cudaFree(p);
         for (auto& w : ws)
-            for (void* p : {(void*)w.za, (void*)w.zb, (void*)w.g, (void*)w.q, (void*)w.fail})
+            for (void* p : {(void*)w.za, (void*)w.zb, (void*)w.g, (void*)w.q, (void*)w.fail, (void*)w.da, (void*)w.db})
                 if (p) cudaFree(p);
         for (auto e : ev_sweep) cudaEventDestroy(e);
         for (auto e : ev_sub) cudaEventDestroy(e);
@@ -191,14 +199,22 @@ void build_device_level(wmc_level& L) {
     L.d_a0 = upload(t.a0);
     L.d_z0 = upload(t.z0);
 
-    // SELL-32 of A P on R
-    const bool lts = t.kind == wmc::Integrator::LocalTimeStepping && t.n_r > 0;
+    // substep path: structured lattice kernel, generic on-chip kernel, or the
+    // HBM-resident kernel when R is too large for one SM (WMC_SUBSTEP_PATH
+    // = lattice|onchip|global forces one, for tests)
+    const bool lts = t.kind == wmc::Integrator::LocalTimeStepping && t.n_r > 0 && t.p > 1;
+    const char* force_path = std::getenv("WMC_SUBSTEP_PATH");
+    const std::string fp = force_path ? force_path : "";
     L.n_wid = static_cast<int>(t.rc_ptr.size()) - 1;
-    if (lts) {
-        if (t.n_r > wmc::kSubThreads * wmc::kSubMaxRpt || t.n_r >= 65536)
-            throw ConfigError("level: |R| = " + std::to_string(t.n_r) + " exceeds the on-chip substep kernel (" +
-                              std::to_string(wmc::kSubThreads * wmc::kSubMaxRpt) + ")");
-        if (L.n_wid >= 65535) throw ConfigError("level: too many weight recipes");
+    const bool onchip_fits = t.n_r <= wmc::kSubThreads * wmc::kSubMaxRpt && t.n_r < 65536 && L.n_wid < 65535;
+    if (lts && (fp == "global" || !onchip_fits)) {
+        if (t.n >= (1 << 24)) throw ConfigError("level: more than 2^24 DOFs");
+        L.path = SubPath::Global;
+        L.d_apg_ptr = upload(t.apg_ptr);
+        L.d_apg_ent = upload(t.apg_ent);
+        L.d_apg_a0 = upload(t.apg_a0);
+    }
+    if (lts && L.path != SubPath::Global) {
         const int n_slices = (t.n_r + 31) / 32;
         std::vector<int> soff(n_slices + 1, 0);
         std::vector<std::uint32_t> sent;
@@ -238,9 +254,6 @@ void build_device_level(wmc_level& L) {
         probe.n_ent = L.n_sub_ent;
         L.sub_smem = wmc::substep_smem_bytes(probe);
         L.sub_grid = wmc::substep_max_grid(L.device, L.sub_smem);
-        if (L.sub_grid <= 0)
-            throw ConfigError("level: substep working set " + std::to_string(L.sub_smem) +
-                              " B exceeds shared memory");
     }
     L.d_qdof = upload(t.qoi_dof);
     L.d_qw = upload(t.qoi_w);
@@ -249,7 +262,8 @@ void build_device_level(wmc_level& L) {
     int max_gen_width = 0;
     for (std::size_t q = 0; q + 1 < t.gen_ptr.size(); ++q)
         max_gen_width = std::max(max_gen_width, t.gen_ptr[q + 1] - t.gen_ptr[q]);
-    if (lts && t.lattice && static_cast<int>(t.gen_rows.size()) <= 1024 && max_gen_width <= wmc::kLatGenWidth) {
+    if (lts && L.path != SubPath::Global && t.lattice && static_cast<int>(t.gen_rows.size()) <= 1024 &&
+        max_gen_width <= wmc::kLatGenWidth) {
         // SELL-32 over the generic rows, per slot: column and recipe range
         const int n_gen = static_cast<int>(t.gen_rows.size());
         const int n_slices = (n_gen + 31) / 32;
@@ -356,6 +370,12 @@ void build_device_level(wmc_level& L) {
         L.lat_grid = wmc::substep_max_grid(L.device, L.lat_smem);
         L.lattice = L.lat_grid > 0;
     }
+    if (lts && L.path != SubPath::Global) {
+        L.path = (L.lattice && fp != "onchip") ? SubPath::Lattice : SubPath::OnChip;
+        if (L.path == SubPath::OnChip && L.sub_grid <= 0)
+            throw ConfigError("level: substep working set exceeds shared memory");
+    }
+    L.lattice = L.path == SubPath::Lattice;
     L.d_cells = nullptr;
     check(cudaMalloc(&L.d_cells, sizeof(double) * std::max<std::size_t>(static_cast<std::size_t>(L.batch) * t.n_cells, 1)),
           "cudaMalloc batch");
@@ -377,6 +397,10 @@ Workspace& workspace(wmc_level& L, int role) {
         alloc(&w.g, S * static_cast<std::size_t>(g_stride(t)));
         alloc(&w.fail, S);
         alloc(&w.q, S);
+        if (L.path == SubPath::Global) {
+            alloc(&w.da, S * t.n_r);
+            alloc(&w.db, S * t.n_r);
+        }
     }
     return w;
 }
@@ -394,7 +418,8 @@ cudaEvent_t mark(wmc_level& L, std::vector<cudaEvent_t>& v, cudaStream_t st) {
 
 void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
     const wmc::LevelTables& t = L.tab;
-    const bool lts = t.kind == wmc::Integrator::LocalTimeStepping && t.n_r > 0;
+    const bool lts = L.path != SubPath::None;
+    const bool global = L.path == SubPath::Global;
     wmc::launch_fill_int(ws.fail, INT_MAX, S, stream);
 
     wmc::SweepArgs sw{};
@@ -475,13 +500,14 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         sb.cm = L.d_cm;
         sb.c0 = t.c0;
     }
-    const int sub_grid = std::min(L.lattice ? L.lat_grid : L.sub_grid, count);
+    const int sub_grid = std::max(1, std::min(L.lattice ? L.lat_grid : L.sub_grid, count));
     for (long s = 1; s < t.n_steps; ++s) {
         sw.zc = cur;
         sw.zp = prev;
         sw.zc_out = nullptr;
         sw.g = ws.g;
         sw.g_stride = g_stride(t);
+        sw.g_node_major = global ? 1 : 0;
         sw.split = lts ? t.n_r : 0;
         sw.factor = t.coarse_factor;
         sw.step = static_cast<int>(s + 1);
@@ -489,7 +515,36 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         wmc::launch_sweep_step(sw, stream);
         if (L.profile) mark(L, L.ev_sweep, stream);
         ++g_launches;
-        if (lts) {
+        if (global) {
+            if (L.profile) mark(L, L.ev_sub, stream);
+            wmc::GSubArgs ga{};
+            ga.n_r = t.n_r;
+            ga.S = S;
+            ga.count = count;
+            ga.ptr = L.d_apg_ptr;
+            ga.ent = L.d_apg_ent;
+            ga.a0 = L.d_apg_a0;
+            ga.cells = cells;
+            ga.g = ws.g;
+            ga.c0 = t.c0;
+            ga.zc = cur;
+            ga.zp = prev;
+            ga.step = static_cast<int>(s + 1);
+            ga.fail = ws.fail;
+            for (int m = 1; m <= t.p - 1; ++m) {
+                // d_m / d_{m-1}: m = 1 -> (-c0 g, 0); m = 2 -> (A, -c0 g); then A/B alternate
+                ga.cur_mode = m == 1 ? 1 : 0;
+                ga.prev_mode = m == 1 ? 2 : (m == 2 ? 1 : 0);
+                ga.dcur = m == 1 ? nullptr : ((m % 2 == 0) ? ws.da : ws.db);
+                ga.dprev = m == 1 ? ws.da : ((m % 2 == 0) ? ws.db : ws.da);
+                ga.beta = t.beta[m - 1];
+                ga.cm = t.cm[m - 1];
+                ga.last = m == t.p - 1;
+                wmc::launch_global_substep(ga, stream);
+                ++g_launches;
+            }
+            if (L.profile) mark(L, L.ev_sub, stream);
+        } else if (lts) {
             if (L.profile) mark(L, L.ev_sub, stream);
             const int e = L.lattice ? wmc::launch_lattice_substeps(la, sub_grid, stream)
                                     : wmc::launch_substeps(sb, sub_grid, stream);
@@ -727,8 +782,9 @@ wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     return s;
 }
 
-void fill_info(const wmc::LevelTables& t, int batch, bool lattice, wmc_level_info* info) {
+void fill_info(const wmc::LevelTables& t, int batch, bool lattice, wmc_level_info* info, int path = -1) {
     info->lattice = lattice ? 1 : 0;
+    info->substep_path = path;
     info->n = t.n;
     info->n_r = t.n_r;
     info->n_p = t.n_p;
@@ -866,10 +922,23 @@ int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level
         L->spec = spec_from_desc(desc);
         L->tab = wmc::build_level_tables(mesh->mesh, L->spec);
         if (L->tab.n_steps >= INT_MAX) throw ConfigError("wmc_level_create: too many steps");
-        L->batch = round64(desc->batch > 0 ? desc->batch : 4096);
         int ndev = 0;
         check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
         if (L->device < 0 || L->device >= ndev) throw ConfigError("wmc_level_create: no such device");
+        if (desc->batch > 0) {
+            L->batch = round64(desc->batch);
+        } else {
+            // automatic batch: at most 4096 samples, both workspaces of the
+            // level within 15 % of the device memory
+            check(cudaSetDevice(L->device), "cudaSetDevice");
+            std::size_t free_b = 0, total_b = 0;
+            check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            const auto& t = L->tab;
+            const double per_sample =
+                2.0 * 8.0 * (2.0 * t.n + g_stride(t) + t.n_cells + 4.0 + 2.0 * t.n_r);
+            const long cap = static_cast<long>(0.15 * static_cast<double>(total_b) / per_sample) / 64 * 64;
+            L->batch = static_cast<int>(std::max(64L, std::min(4096L, cap)));
+        }
         build_device_level(*L);
         *out = L.release();
     });
@@ -887,7 +956,7 @@ int wmc_level_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level_i
 int wmc_level_get_info(const wmc_level* L, wmc_level_info* info) {
     return guarded([&] {
         if (!L || !info) throw ConfigError("wmc_level_get_info: NULL argument");
-        fill_info(L->tab, L->batch, L->lattice, info);
+        fill_info(L->tab, L->batch, L->lattice, info, static_cast<int>(L->path));
     });
 }
 

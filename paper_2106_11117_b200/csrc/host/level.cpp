@@ -288,6 +288,17 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         L.row_ptr[i + 1] = static_cast<int>(L.col.size());
     }
 
+    // A P on R rows, parts form (global-memory substep path)
+    L.apg_ptr.assign(L.n_r + 1, 0);
+    for (int i = 0; i < L.n_r; ++i) {
+        for (const auto& [j, k, a] : rows[i]) {
+            if (!L.in_p[j]) continue;
+            L.apg_ent.push_back(j | (k << 24));
+            L.apg_a0.push_back(a);
+        }
+        L.apg_ptr[i + 1] = static_cast<int>(L.apg_ent.size());
+    }
+
     // A P on R rows as deduplicated recipes
     std::map<std::vector<std::pair<int, double>>, int> recipe_id;
     std::vector<std::vector<std::pair<int, double>>> recipes;

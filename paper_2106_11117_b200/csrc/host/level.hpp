@@ -78,6 +78,11 @@ struct LevelTables {
     std::vector<int> rc_cell;
     std::vector<double> rc_a0;
 
+    // A P on R rows as sweep-style parts (col | cell << 24, a0): the
+    // HBM-resident substep path for sets R too large for one SM
+    std::vector<int> apg_ptr, apg_ent;
+    std::vector<double> apg_a0;
+
     std::vector<double> mass;       // lumped mass per dof
     std::vector<double> z0;         // sqrt(M) * projected u0, per dof
     std::vector<int> qoi_dof;       // dofs with a nonzero QoI weight

@@ -155,7 +155,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
             if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
         } else if (row < a.split) {
-            tile[warp][lane] = make_double2(acc0, acc1);
+            if (a.g_node_major)
+                *reinterpret_cast<double2*>(a.g + idx) = make_double2(acc0, acc1);
+            else
+                tile[warp][lane] = make_double2(acc0, acc1);
         } else {
             const double2 zn = zself;  // every row holds its diagonal entry
             const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
         }
     }
-    if (kInit || row0 >= a.split) return;  // block-uniform
+    if (kInit || row0 >= a.split || a.g_node_major) return;  // block-uniform
     // store the block's g rows sample-major: warp w writes samples 8w..8w+7,
     // four lanes per sample, two rows (16 B) per lane
     __syncthreads();
@@ -181,6 +184,65 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
         *reinterpret_cast<double2*>(dst) = make_double2(g0, g1);
     else if (row0 + rr < a.split)
         dst[0] = g0;
+}
+
+// K2 (HBM-resident): one substep over the R rows, warp per (row, 64
+// samples) as in the sweep; A(omega) P d gathered node-centrically from the
+// current d buffer, d_{m+1} written over d_{m-1} (own row only), the last
+// substep forms z_{n+1} directly (reference src/integrators.cpp:137-153).
+__global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
+    if (row >= a.n_r) return;
+    const int s0 = blockIdx.y * kSweepChunk + 2 * lane;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const double* src = a.cur_mode == 0 ? a.dcur : a.g;
+    const double scale = a.cur_mode == 0 ? 1.0 : -a.c0;
+    double acc0 = 0.0, acc1 = 0.0;
+    const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
+#pragma unroll 4
+    for (int k = b; k < e; ++k) {
+        const int pk = __ldg(a.ent + k);
+        const double w = __ldg(a.a0 + k);
+        const int j = pk & 0xffffff;
+        const int cell = static_cast<unsigned>(pk) >> 24;
+        const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+        const double2 v = *reinterpret_cast<const double2*>(src + j * S + s0);
+        acc0 += (c.x * w) * v.x;
+        acc1 += (c.y * w) * v.y;
+    }
+    acc0 *= scale;
+    acc1 *= scale;
+    const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
+    const double2 g = __ldg(reinterpret_cast<const double2*>(a.g + idx));
+    double2 dm, dmm;
+    if (a.cur_mode == 0) {
+        dm = *reinterpret_cast<const double2*>(a.dcur + idx);
+    } else {
+        dm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
+    }
+    if (a.prev_mode == 0) {
+        dmm = *reinterpret_cast<const double2*>(a.dprev + idx);
+    } else if (a.prev_mode == 1) {
+        dmm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
+    } else {
+        dmm = make_double2(0.0, 0.0);
+    }
+    double2 next;
+    next.x = (1.0 + a.beta) * dm.x - a.beta * dmm.x - a.cm * (g.x + acc0);
+    next.y = (1.0 + a.beta) * dm.y - a.beta * dmm.y - a.cm * (g.y + acc1);
+    if (!a.last) {
+        *reinterpret_cast<double2*>(a.dprev + idx) = next;
+        return;
+    }
+    const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
+    const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
+    double2 out;
+    out.x = 2.0 * zn.x - zm.x + 2.0 * next.x;
+    out.y = 2.0 * zn.y - zm.y + 2.0 * next.y;
+    *reinterpret_cast<double2*>(a.zp + idx) = out;
+    if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
+    if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
 }
 
 // R update: z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on rows < n_r, d_p read
@@ -760,6 +822,11 @@ int substep_max_grid(int device, int smem_bytes) {
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (smem_bytes > optin) return 0;
     return sms;  // one 1024-thread CTA per SM
+}
+
+void launch_global_substep(const GSubArgs& a, void* stream) {
+    dim3 grid((a.n_r + kSweepWarps - 1) / kSweepWarps, a.S / kSweepChunk);
+    global_substep_kernel<<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_r_update(const RUpdateArgs& a, void* stream) {

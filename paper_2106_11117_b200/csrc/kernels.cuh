@@ -37,6 +37,7 @@ struct SweepArgs {
     double* zc_out;      // init only: z_1 out
     double* g;           // gd buffer, rows < split
     int g_stride;        // G
+    int g_node_major;    // 1: g[r * S + s] (global substep path), 0: gd[s * G + r]
     double factor;       // init_factor or coarse_factor
     int step;
     int* fail;
@@ -103,6 +104,28 @@ struct RUpdateArgs {
     int* fail;
 };
 
+// One LTS substep of the HBM-resident path (|R| too large for one SM): warp
+// per (row, 64 samples) over the R rows, d in node-major global buffers.
+// d_m / d_{m-1} come from a buffer, from -c0 g (d_1) or are zero (d_0).
+struct GSubArgs {
+    int n_r, S, count;
+    const int* ptr;
+    const int* ent;       // col | cell << 24, columns in P
+    const double* a0;
+    const double* cells;
+    const double* g;      // [r][S]
+    const double* dcur;   // d_m (cur_mode 0)
+    double* dprev;        // d_{m-1} in (prev_mode 0), d_{m+1} out
+    int cur_mode;         // 0 buffer, 1 = -c0 g
+    int prev_mode;        // 0 buffer, 1 = -c0 g, 2 = zero
+    double c0, beta, cm;
+    int last;             // fuse z_{n+1} = 2 z_n - z_{n-1} + 2 d_p
+    const double* zc;
+    double* zp;
+    int step;
+    int* fail;
+};
+
 struct QoIArgs {
     int nq, S, count;
     const int* dof;
@@ -121,6 +144,7 @@ int substep_smem_bytes(const SubArgs& a);
 int launch_substeps(const SubArgs& a, int grid, void* stream);  // returns cudaError_t
 void launch_qoi(const QoIArgs& a, void* stream);
 void launch_r_update(const RUpdateArgs& a, void* stream);
+void launch_global_substep(const GSubArgs& a, void* stream);
 void launch_fill_int(int* p, int value, int n, void* stream);
 void launch_pair_diff(const double* qf, const double* qc, double* dq, int count, void* stream);
 int substep_max_grid(int device, int smem_bytes);

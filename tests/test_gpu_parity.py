@@ -233,3 +233,36 @@ def test_adaptive_mlmc_matches_reference_run_mlmc(golden):
     assert res.estimate == pytest.approx(g["estimate"], rel=MOMENT_RTOL)
     assert res.total_variance == pytest.approx(g["total_variance"], rel=MOMENT_RTOL)
     assert res.bias == pytest.approx(g["bias"], rel=MOMENT_RTOL)
+
+
+@pytest.mark.parametrize("path", ["global", "onchip"])
+def test_substep_paths_agree(path, monkeypatch):
+    """The HBM-resident and the generic on-chip substep kernels against the
+    lattice kernel (and, through it, the reference) on config-0 and config-1
+    level meshes."""
+    for d in (configs.config0(), configs.config1()[1]):
+        ref = configs.build_level(d)
+        monkeypatch.setenv("WMC_SUBSTEP_PATH", path)
+        alt = configs.build_level(d)
+        monkeypatch.delenv("WMC_SUBSTEP_PATH")
+        assert ref.info["substep_path"] == 1
+        assert alt.info["substep_path"] == {"global": 3, "onchip": 2}[path]
+        _, a, _ = wavemc.eval_pairs(ref, None, 0, 2, 0, 70)
+        _, b, _ = wavemc.eval_pairs(alt, None, 0, 2, 0, 70)
+        assert per_sample_rel(b, a) < QOI_RTOL
+
+
+def test_large_r_uses_the_hbm_path():
+    """A refined square of 256 x 256 fine cells (|R| > 8192) cannot live in one
+    SM: the level falls back to the HBM-resident substep kernel and still
+    matches the C oracle."""
+    m = wavemc.Mesh.build_square(32, 64)
+    lv = wavemc.Level(m, wavemc.LevelSpec(dt=0.2 / 32, substeps=64, final_time=0.05))
+    assert lv.info["n_r"] > 8192 and lv.info["substep_path"] == 3
+    _, q, _ = wavemc.eval_pairs(lv, None, 0, 0, 0, 3)
+    import oracle_py
+    orc = oracle_py.COracle()
+    rc, _, ref, _, _ = orc.eval_pairs(oracle_py.MeshArrays(*m.arrays()),
+                                     oracle_py.problem(0.2 / 32, 64, final_time=0.05), None, None, 0, 0, 0, 3)
+    assert rc == 0
+    assert per_sample_rel(q, ref) < QOI_RTOL
