@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--scale", type=float, default=1.0, help="fraction of N_l (1.0 = BASELINE config 1)")
+    ap.add_argument("--scale", type=float, default=1.0, help="fraction of N_l (1.0 = the BASELINE counts)")
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 3],
+                    help="BASELINE config: 1 (default, MLMC), 0 (single-level MC), 3 (large single level)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     return ap.parse_args()
@@ -106,6 +108,20 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baselines (the reference compiled from its own sources, else our port)
 
+def workload(config: int):
+    """(level defs, N per level, description, CPU horizon override)."""
+    from paper_2106_11117_b200 import configs
+    if config == 0:
+        return [configs.config0()], [configs.CONFIG0_COUNT], "BASELINE config 0: single-level MC, h=1/32 refined x4, p=4", None
+    if config == 3:
+        d = configs.config3()
+        # the CPU sample keeps the mesh and the per-step work but shortens the
+        # horizon to 16 global steps (per-step cost is uniform in time)
+        return [d], [configs.CONFIG3_COUNT], "BASELINE config 3: single level h=1/1024 refined x8, p=8, T=0.5", 16 * d.dt
+    return configs.config1(), list(configs.CONFIG1_COUNTS), (
+        "BASELINE config 1: fixed-N MLMC, LF-LTS, 5 levels h=1/16..1/256, p=32..2"), None
+
+
 def ref_sample_counts(threads: int):
     """Bounded sample of config 1 for the CPU, in the proportions of N_l
     (65536 : 16384 : 4096 : 1024 : 256 = 256 : 64 : 16 : 4 : 1), sized for
@@ -115,12 +131,12 @@ def ref_sample_counts(threads: int):
     return [64 * t, 16 * t, 4 * t, t, max(1, t // 4)]
 
 
-def run_reference_cpu(defs, threads: int):
-    """Config 1 sample through the unmodified reference library (oracle/_ref),
+def run_reference_cpu(defs, threads: int, final_time=None):
+    """A bounded sample through the unmodified reference library (oracle/_ref),
     its own run_jobs-style pool of `threads` workers.  Returns dict."""
     import oracle_py
     from paper_2106_11117_b200 import configs
-    counts = ref_sample_counts(threads)
+    counts = ref_sample_counts(threads) if len(defs) > 1 else [4 * threads if final_time is None else threads]
     tmp = tempfile.mkdtemp(prefix="wmc_bench_")
     specs = []
     for l, d in enumerate(defs):
@@ -128,13 +144,14 @@ def run_reference_cpu(defs, threads: int):
         configs.build_mesh(d).dump(p)
         specs.append((p, d.dt, d.substeps))
     drv = oracle_py.RefDriver()
-    res = drv.mlmc(specs, counts, threads=threads)
+    extra = {"T": repr(final_time)} if final_time is not None else {}
+    res = drv.mlmc(specs, counts, threads=threads, **extra)
     shutil.rmtree(tmp, ignore_errors=True)
     return {"value": res["dof_updates"] / res["seconds"], "seconds": res["seconds"],
             "dof_updates": res["dof_updates"], "counts": counts, "kind": "reference", "cores": res["threads"]}
 
 
-def run_port_cpu(defs, threads: int):
+def run_port_cpu(defs, threads: int, final_time=None):
     """Fallback when oracle/_ref is absent: our C restatement, `threads` workers."""
     from concurrent.futures import ThreadPoolExecutor
 
@@ -142,11 +159,16 @@ def run_port_cpu(defs, threads: int):
     from paper_2106_11117_b200 import configs
     oracle_py.build()
     orc = oracle_py.COracle()
-    counts = ref_sample_counts(threads)
+    counts = ref_sample_counts(threads) if len(defs) > 1 else [4 * threads if final_time is None else threads]
     from paper_2106_11117_b200 import wavemc
     meshes = [oracle_py.MeshArrays(*configs.build_mesh(d).arrays()) for d in defs]
-    probs = [oracle_py.problem(d.dt, d.substeps) for d in defs]
-    upd = [wavemc.level_plan(configs.build_mesh(d), configs.level_spec(d))["dof_updates_per_solve"] for d in defs]
+    T = [final_time if final_time is not None else d.final_time for d in defs]
+    probs = [oracle_py.problem(d.dt, d.substeps, final_time=t) for d, t in zip(defs, T)]
+    upd = []
+    for d, t in zip(defs, T):
+        spec = configs.level_spec(d)
+        spec.final_time = t
+        upd.append(wavemc.level_plan(configs.build_mesh(d), spec)["dof_updates_per_solve"])
     jobs = [(l, i) for l in range(len(defs)) for i in range(counts[l])]
 
     def one(job):
@@ -181,11 +203,11 @@ def reference_time_to_rmse(defs, threads: int):
             "threads": res["threads"]}
 
 
-def cpu_baseline(defs, threads: int):
+def cpu_baseline(defs, threads: int, final_time=None):
     import oracle_py
     if os.path.exists(oracle_py.REF_DRIVER):
-        return run_reference_cpu(defs, threads)
-    return run_port_cpu(defs, threads)
+        return run_reference_cpu(defs, threads, final_time)
+    return run_port_cpu(defs, threads, final_time)
 
 
 # ---------------------------------------------------------------------------
@@ -195,27 +217,29 @@ def reference_arm(args, world, rank):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    defs = configs.config1()
+    defs, counts_total, label, cpu_T = workload(args.config)
     try:
-        runs = [cpu_baseline(defs, threads) for _ in range(args.warmup + args.steps)]
+        runs = [cpu_baseline(defs, threads, cpu_T) for _ in range(args.warmup + args.steps)]
     except Exception as exc:  # the oracle always exists; report loudly
         print(json.dumps({"impl": "reference", "unavailable": f"reference CPU run failed: {exc}"}))
         return 0
     timed = runs[args.warmup:]
     value = sum(r["dof_updates"] for r in timed) / sum(r["seconds"] for r in timed)
     ttr = None
-    try:
-        ttr = reference_time_to_rmse(defs, threads)
-    except Exception as exc:
-        ttr = {"eps": TTR_EPS, "error": str(exc)}
+    if args.config == 1:
+        try:
+            ttr = reference_time_to_rmse(defs, threads)
+        except Exception as exc:
+            ttr = {"eps": TTR_EPS, "error": str(exc)}
     r0 = timed[0]
-    sample = (f"config 1 bounded sample N_l={r0['counts']} (of {configs.CONFIG1_COUNTS}) per step, "
-              f"{r0['cores']} threads, {r0['kind']}")
+    sample = (f"config {args.config} bounded sample N_l={r0['counts']} (of {counts_total}) per step"
+              + (f", horizon shortened to T={cpu_T!r}" if cpu_T is not None else "")
+              + f", {r0['cores']} threads, {r0['kind']}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(r["seconds"] for r in timed) / len(timed),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (counter-based RNG draws, seed 0)",
-            "config": {"workload": "BASELINE config 1 (MLMC LF-LTS, 5 levels), bounded CPU sample",
+            "config": {"workload": label + " (bounded CPU sample)",
                        "parallelism": f"{r0['cores']} CPU threads"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": r0["cores"], "kind": r0["kind"],
                              "sample": sample},
@@ -235,8 +259,8 @@ def b200_arm(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    defs = configs.config1()
-    counts_total = [max(1, int(round(n * args.scale))) for n in configs.CONFIG1_COUNTS]
+    defs, counts_total, label, cpu_T = workload(args.config)
+    counts_total = [max(1, int(round(n * args.scale))) for n in counts_total]
     levels = [configs.build_level(d, device=local) for d in defs]
     spans = [shard.shard_range(n, rank, world) for n in counts_total]
     first = [f for f, _ in spans]
@@ -326,7 +350,7 @@ def b200_arm(args, world, rank, local):
     # MLMC time-to-RMSE: the adaptive driver (reference run_mlmc, batched)
     # from scratch to convergence at TTR_EPS, wall time around the public call
     ttr = None
-    if world == 1:
+    if world == 1 and args.config == 1:
         costs = [lv.info["dof_updates_per_solve"] for lv in levels]
         wavemc.run_mlmc(levels, costs, wavemc.MlmcConfig(eps=TTR_EPS * 4))  # warm-up
         torch.cuda.synchronize(dev)
@@ -363,7 +387,7 @@ def b200_arm(args, world, rank, local):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based RNG draws, seed 0)",
-            "config": {"workload": "BASELINE config 1: fixed-N MLMC, LF-LTS, 5 levels h=1/16..1/256, p=32..2",
+            "config": {"workload": label,
                        "N_l": counts_total, "levels": [{"n": lv.info["n"], "n_r": lv.info["n_r"], "p": lv.info["p"],
                                                         "n_steps": lv.info["n_steps"]} for lv in levels],
                        "dof_updates_per_step": total_updates, "parallelism": f"samples sharded over {world} GPU(s)",
@@ -382,9 +406,11 @@ def b200_arm(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         try:
-            cb = cpu_baseline(defs, threads)
+            cb = cpu_baseline(defs, threads, cpu_T)
             line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
-                                    "sample": f"config 1 bounded sample N_l={cb['counts']}, {cb['seconds']:.1f} s"}
+                                    "sample": f"config {args.config} bounded sample N_l={cb['counts']}"
+                                              + (f", T={cpu_T!r}" if cpu_T is not None else "")
+                                              + f", {cb['seconds']:.1f} s"}
         except Exception as exc:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                                     "sample": f"failed: {exc}"}
@@ -396,40 +422,51 @@ def b200_arm(args, world, rank, local):
 
 
 def roofline_from_profile(levels, counts, prof, step_ms):
-    """Dominant-kernel roofline from the profiled pass.  Sweep kernel
-    algorithmic bytes per launch: 8 B x S x (n reads of z_n + (n - |R|) reads
-    of z_{n-1} + n writes of z_{n+1} or g); substep kernel: 8 B x S x 4 |R|
-    (g, z_n, z_{n-1} in, z_{n+1} out) plus its on-chip FP64 work."""
+    """Per-kernel device time from the profiled pass, and the roofline of the
+    dominant HBM-bound kernel.  Algorithmic bytes per launch (per sample):
+      sweep                  8 B x (n reads of z_n + (n - |R|) reads of z_{n-1}
+                             + n writes of z_{n+1} or g)
+      on-chip substep        8 B x 2 |R| (g in, d_p out) -- on-chip bound
+      HBM-resident substep   8 B x 4 |R| per substep (d_m, d_{m-1}, g in,
+                             d_{m+1} out) + 8 B x 2 |R| on the last (z_n, z_{n-1})
+      R update               8 B x 4 |R|"""
     sweep_ms = sum(p["sweep_ms"] for p in prof)
     sub_ms = sum(p["sub_ms"] for p in prof)
     upd_ms = sum(p["upd_ms"] for p in prof)
-    sweep_bytes = 0.0
-    sub_bytes = 0.0
-    sub_flops = 0.0
-    sub_updates = 0.0
+    sweep_bytes = sub_bytes = sub_flops = sub_updates = 0.0
+    global_path = any(lv.info["substep_path"] == 3 for lv in levels)
     for l, lv in enumerate(levels):
         for lvl in ([l] + ([l - 1] if l else [])):
             info = levels[lvl].info
             n, nr, steps, p = info["n"], info["n_r"], info["n_steps"], info["p"]
             c = counts[l]
             sweep_bytes += 8.0 * c * (steps - 1) * (2 * n + (n - nr))
-            sub_bytes += 8.0 * c * (steps - 1) * 4 * nr
+            if info["substep_path"] == 3:
+                sub_bytes += 8.0 * c * (steps - 1) * (4 * nr * (p - 1) + 2 * nr)
+            elif info["substep_path"] in (1, 2):
+                sub_bytes += 8.0 * c * (steps - 1) * 2 * nr
             sub_flops += c * (steps - 1) * (p - 1) * (2.0 * info["ap_nnz"] + 7.0 * nr)
             sub_updates += c * (steps - 1) * (p - 1) * nr
+    gbps = lambda b, ms: b / (ms * 1e-3) / 1e9 if ms else None  # noqa: E731
     kernels = {"sweep": {"ms": sweep_ms, "launches": sum(p["sweep_launches"] for p in prof),
                          "share_of_step": sweep_ms / step_ms if step_ms else None,
-                         "achieved_GBps": sweep_bytes / (sweep_ms * 1e-3) / 1e9 if sweep_ms else None},
+                         "achieved_GBps": gbps(sweep_bytes, sweep_ms)},
                "substep": {"ms": sub_ms, "launches": sum(p["sub_launches"] for p in prof),
+                           "path": "hbm-resident" if global_path else "on-chip",
                            "share_of_step": sub_ms / step_ms if step_ms else None,
                            "fp64_TFLOPs": sub_flops / (sub_ms * 1e-3) / 1e12 if sub_ms else None,
                            "substep_dof_updates_per_s": sub_updates / (sub_ms * 1e-3) if sub_ms else None,
-                           "hbm_GBps": sub_bytes / (sub_ms * 1e-3) / 1e9 if sub_ms else None},
+                           "achieved_GBps": gbps(sub_bytes, sub_ms)},
                "r_update": {"ms": upd_ms, "launches": sum(p["upd_launches"] for p in prof),
                             "share_of_step": upd_ms / step_ms if step_ms else None}}
-    roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",
-            "traffic": None,
-            "note": ("HBM roofline of the sweep kernel (algorithmic bytes); the substep kernel is on-chip "
-                     "(shared memory / FP64 issue) bound, see kernels.substep")}
+    if global_path and sub_ms >= sweep_ms:
+        roof = {"bound": "hbm", "kernel": "global_substep", "achieved": kernels["substep"]["achieved_GBps"],
+                "unit": "GB/s", "traffic": None, "note": "dominant kernel, HBM-resident substeps (algorithmic bytes)"}
+    else:
+        roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",
+                "traffic": None,
+                "note": ("HBM roofline of the sweep kernel (algorithmic bytes); the dominant substep kernel is "
+                         "on-chip (shared-memory) bound, see kernels.substep")}
     return roof, kernels
 
 

@@ -62,6 +62,15 @@ def config1(kind: str = "lts", n_levels: int = 5) -> list[LevelDef]:
     return out
 
 
+def config3() -> LevelDef:
+    """Large batch: h = 1/1024, refined square at h/8, p = 8, T = 0.5."""
+    return LevelDef(1024, 8, 0.2 / 1024, 8, WMC_LOCAL_TIME_STEPPING, final_time=0.5)
+
+
+CONFIG0_COUNT = 1024
+CONFIG3_COUNT = 8192
+
+
 def build_mesh(d: LevelDef):
     from .wavemc import Mesh
     return Mesh.build_square(d.n_coarse, d.ratio, FINE_LO, FINE_HI, SNAP)

@@ -45,6 +45,14 @@ __global__ void draw_cells_kernel(std::uint64_t seed, std::uint32_t level, std::
     }
 }
 
+// 1D grid over (row group of kSweepWarps rows, 64-sample chunk), row group
+// fastest: concurrently resident blocks cover a contiguous band of rows, so
+// the N/S neighbour rows of a gather are L2 hits (measured faster than
+// chunk-fastest order, which favours DRAM page locality)
+__device__ __forceinline__ int n_groups(int rows) { return (rows + kSweepWarps - 1) / kSweepWarps; }
+__device__ __forceinline__ int grid_chunk(int rows) { return blockIdx.x / n_groups(rows); }
+__device__ __forceinline__ int grid_rowgroup(int rows) { return blockIdx.x % n_groups(rows); }
+
 __device__ __forceinline__ void flag_fail(int* fail, int s, int count, int step) {
     if (s < count) atomicMin(fail + s, step);
 }
@@ -62,14 +70,17 @@ template <bool kInit, bool kParts>
 __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
     __shared__ double2 tile[kSweepWarps][32];  // g of the block's R rows: [row][lane] = samples 2 lane, 2 lane + 1
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int row0 = blockIdx.x * kSweepWarps;
+    const int row0 = grid_rowgroup(a.n) * kSweepWarps;
     const int row = row0 + warp;
-    const int s0 = blockIdx.y * kSweepChunk + 2 * lane;
+    const int s0 = grid_chunk(a.n) * kSweepChunk + 2 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
     if (row < a.n) {
         const int b = __ldg(a.row_ptr + row), e = __ldg(a.row_ptr + row + 1);
         double acc0 = 0.0, acc1 = 0.0;
         double2 zself = make_double2(0.0, 0.0);
+        // z_{n-1} of a leap-frog row issued before the gather (latency overlap)
+        double2 zm_early = make_double2(0.0, 0.0);
+        if (!kInit && row >= a.split) zm_early = *reinterpret_cast<const double2*>(a.zp + row * S + s0);
         if (kParts) {
             // entries grouped by cell: sum a0 z_j within a part, then scale by
             // the part's coefficient (one coefficient load per part)
@@ -161,7 +172,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
                 tile[warp][lane] = make_double2(acc0, acc1);
         } else {
             const double2 zn = zself;  // every row holds its diagonal entry
-            const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
+            const double2 zm = zm_early;
             double2 out;
             out.x = 2.0 * zn.x - zm.x - a.factor * acc0;
             out.y = 2.0 * zn.y - zm.y - a.factor * acc1;
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
     // four lanes per sample, two rows (16 B) per lane
     __syncthreads();
     const int sl = 8 * warp + (lane >> 2), rr = 2 * (lane & 3);
-    const int s = blockIdx.y * kSweepChunk + sl;
+    const int s = grid_chunk(a.n) * kSweepChunk + sl;
     const double2 t0 = tile[rr][sl >> 1], t1 = tile[rr + 1][sl >> 1];
     const double g0 = (sl & 1) ? t0.y : t0.x, g1 = (sl & 1) ? t1.y : t1.x;
     double* dst = a.g + static_cast<std::size_t>(s) * a.g_stride + row0 + rr;
@@ -192,12 +203,22 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
 // substep forms z_{n+1} directly (reference src/integrators.cpp:137-153).
 __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubArgs a) {
     const int lane = threadIdx.x & 31;
-    const int row = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
+    const int row = grid_rowgroup(a.n_r) * kSweepWarps + (threadIdx.x >> 5);
     if (row >= a.n_r) return;
-    const int s0 = blockIdx.y * kSweepChunk + 2 * lane;
+    const int s0 = grid_chunk(a.n_r) * kSweepChunk + 2 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
     const double* src = a.cur_mode == 0 ? a.dcur : a.g;
     const double scale = a.cur_mode == 0 ? 1.0 : -a.c0;
+    // the row's own values first, so their latency overlaps the gather
+    const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
+    const double2 g = __ldg(reinterpret_cast<const double2*>(a.g + idx));
+    double2 dm = make_double2(0.0, 0.0), dmm = make_double2(0.0, 0.0), zn = dm, zm = dm;
+    if (a.cur_mode == 0) dm = *reinterpret_cast<const double2*>(a.dcur + idx);
+    if (a.prev_mode == 0) dmm = *reinterpret_cast<const double2*>(a.dprev + idx);
+    if (a.last) {
+        zn = *reinterpret_cast<const double2*>(a.zc + idx);
+        zm = *reinterpret_cast<const double2*>(a.zp + idx);
+    }
     double acc0 = 0.0, acc1 = 0.0;
     const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
 #pragma unroll 4
@@ -213,21 +234,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
     }
     acc0 *= scale;
     acc1 *= scale;
-    const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
-    const double2 g = __ldg(reinterpret_cast<const double2*>(a.g + idx));
-    double2 dm, dmm;
-    if (a.cur_mode == 0) {
-        dm = *reinterpret_cast<const double2*>(a.dcur + idx);
-    } else {
-        dm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
-    }
-    if (a.prev_mode == 0) {
-        dmm = *reinterpret_cast<const double2*>(a.dprev + idx);
-    } else if (a.prev_mode == 1) {
-        dmm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
-    } else {
-        dmm = make_double2(0.0, 0.0);
-    }
+    if (a.cur_mode != 0) dm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
+    if (a.prev_mode == 1) dmm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
     double2 next;
     next.x = (1.0 + a.beta) * dm.x - a.beta * dmm.x - a.cm * (g.x + acc0);
     next.y = (1.0 + a.beta) * dm.y - a.beta * dmm.y - a.cm * (g.y + acc1);
@@ -235,8 +243,6 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
         *reinterpret_cast<double2*>(a.dprev + idx) = next;
         return;
     }
-    const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
-    const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
     double2 out;
     out.x = 2.0 * zn.x - zm.x + 2.0 * next.x;
     out.y = 2.0 * zn.y - zm.y + 2.0 * next.y;
@@ -251,10 +257,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
 __global__ void __launch_bounds__(kSweepWarps * 32) r_update_kernel(RUpdateArgs a) {
     __shared__ double2 tile[kSweepWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int row0 = blockIdx.x * kSweepWarps;
+    const int row0 = grid_rowgroup(a.n_r) * kSweepWarps;
     {
         const int sl = 8 * warp + (lane >> 2), rr = 2 * (lane & 3);
-        const int s = blockIdx.y * kSweepChunk + sl;
+        const int s = grid_chunk(a.n_r) * kSweepChunk + sl;
         const double* src = a.gd + static_cast<std::size_t>(s) * a.g_stride + row0 + rr;
         double d0 = 0.0, d1 = 0.0;
         if (row0 + rr + 1 < a.n_r) {
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) r_update_kernel(RUpdateArgs 
     __syncthreads();
     const int row = row0 + warp;
     if (row >= a.n_r) return;
-    const int s0 = blockIdx.y * kSweepChunk + 2 * lane;
+    const int s0 = grid_chunk(a.n_r) * kSweepChunk + 2 * lane;
     const std::size_t idx = static_cast<std::size_t>(row) * a.S + s0;
     const double2 d = tile[warp][lane];
     const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
@@ -749,12 +755,12 @@ void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t fi
 }
 
 void launch_sweep_init(const SweepArgs& a, void* stream) {
-    dim3 grid((a.n + kSweepWarps - 1) / kSweepWarps, a.S / kSweepChunk);
+    const unsigned grid = ((a.n + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
     sweep_kernel<true, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_sweep_step(const SweepArgs& a, void* stream) {
-    dim3 grid((a.n + kSweepWarps - 1) / kSweepWarps, a.S / kSweepChunk);
+    const unsigned grid = ((a.n + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
     static const int parts = [] {
         const char* v = std::getenv("WMC_SWEEP_PARTS");  // tuning knob
         return v ? std::atoi(v) : 0;
@@ -825,12 +831,12 @@ int substep_max_grid(int device, int smem_bytes) {
 }
 
 void launch_global_substep(const GSubArgs& a, void* stream) {
-    dim3 grid((a.n_r + kSweepWarps - 1) / kSweepWarps, a.S / kSweepChunk);
+    const unsigned grid = ((a.n_r + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
     global_substep_kernel<<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_r_update(const RUpdateArgs& a, void* stream) {
-    dim3 grid((a.n_r + kSweepWarps - 1) / kSweepWarps, a.S / kSweepChunk);
+    const unsigned grid = ((a.n_r + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
     r_update_kernel<<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 

@@ -16,8 +16,16 @@ def main():
     ap.add_argument("--count", type=int, default=1184)
     ap.add_argument("--generic", action="store_true", help="mesh without lattice metadata")
     ap.add_argument("--repeat", type=int, default=2)
+    ap.add_argument("--square", type=int, nargs=2, metavar=("N_COARSE", "RATIO"),
+                    help="custom refined-square mesh (LTS with p = RATIO, dt = 0.2 h)")
+    ap.add_argument("--steps", type=int, default=0, help="limit the horizon to this many global steps")
     a = ap.parse_args()
     d = configs.config1()[a.level]
+    if a.square:
+        nc, r = a.square
+        d = configs.LevelDef(nc, r, 0.2 / nc, r, d.integrator)
+    if a.steps:
+        d = configs.LevelDef(d.n_coarse, d.ratio, d.dt, d.substeps, d.integrator, final_time=a.steps * d.dt)
     m = configs.build_mesh(d)
     if a.generic:
         m = wavemc.Mesh.from_arrays(*m.arrays())
@@ -27,7 +35,8 @@ def main():
         _, q, _ = wavemc.eval_pairs(lv, None, 0, a.level, 0, a.count)
         dt = time.perf_counter() - t0
         upd = a.count * lv.info["dof_updates_per_solve"]
-        print(f"level {a.level} lattice={lv.info['lattice']} {a.count} solves {dt:.3f} s "
+        print(f"level {a.level} path={lv.info['substep_path']} n={lv.info['n']} n_r={lv.info['n_r']} "
+              f"{a.count} solves {dt:.3f} s "
               f"{upd / dt:.3e} DOF-updates/s q0={q[0]:.12e}")
 
 
