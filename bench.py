@@ -41,8 +41,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of N_l (1.0 = the BASELINE counts)")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 3],
-                    help="BASELINE config: 1 (default, MLMC), 0 (single-level MC), 3 (large single level)")
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 3, 4],
+                    help="BASELINE config: 1 (default, MLMC), 0 (single-level MC), 3 (large single level), "
+                         "4 (adaptive MLMC to an RMSE target, log-normal KL coefficient)")
+    ap.add_argument("--eps", type=float, default=None, help="config 4: RMSE target (default BASELINE 1e-3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     return ap.parse_args()
@@ -470,9 +472,88 @@ def roofline_from_profile(levels, counts, prof, step_ms):
     return roof, kernels
 
 
+def kl_table_file(tmp):
+    from paper_2106_11117_b200 import configs, wavemc
+    kl = configs.KL_FIELD
+    table, _ = wavemc.kl_table(kl["cells"][0], kl["cells"][1], kl["sigma"], kl["corr_len"], kl["modes"])
+    path = os.path.join(tmp, "kl.txt")
+    with open(path, "w") as f:
+        f.write(f"{table.shape[0]} {table.shape[1]}\n")
+        f.write("\n".join(repr(float(v)) for v in table.ravel()) + "\n")
+    return path, {"kl-table": path, "cells-x": kl["cells"][0], "cells-y": kl["cells"][1]}
+
+
+def adaptive_arm(args, world, rank, local):
+    """Config 4: one step = the adaptive MLMC estimator (reference run_mlmc
+    algorithm) from scratch to the RMSE target; metric DOF-updates/s of the
+    work it performed, plus the time-to-RMSE itself."""
+    from paper_2106_11117_b200 import configs
+    eps = args.eps or configs.CONFIG4_EPS
+    defs = configs.config4()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        import oracle_py
+        threads = os.cpu_count() or 1
+        tmp = tempfile.mkdtemp(prefix="wmc_c4_")
+        _, klargs = kl_table_file(tmp)
+        specs = []
+        for l, d in enumerate(defs):
+            p = os.path.join(tmp, f"l{l}.mesh")
+            configs.build_mesh(d).dump(p)
+            specs.append((p, d.dt, d.substeps))
+        runs = [oracle_py.RefDriver().adaptive(specs, eps, threads=threads, **klargs)
+                for _ in range(args.warmup + args.steps)][args.warmup:]
+        shutil.rmtree(tmp, ignore_errors=True)
+        sec = sum(r["seconds"] for r in runs) / len(runs)
+        line = {"impl": "reference", "metric": "MLMC time-to-RMSE", "value": sec, "unit": "s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (counter-based RNG, Box-Muller KL weights, seed 0)",
+                "config": {"workload": f"BASELINE config 4: adaptive MLMC to RMSE {eps}, log-normal KL", "eps": eps},
+                "cpu_baseline": {"value": sec, "unit": "s", "cores": threads, "kind": "reference",
+                                 "sample": f"full adaptive run, reference run_mlmc, {threads} threads"},
+                "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "N_l": [lv["N"] for lv in runs[0]["levels"]], "estimate": runs[0]["estimate"]}
+        print(json.dumps(line))
+        return 0
+    import torch
+    from paper_2106_11117_b200 import wavemc
+    torch.cuda.set_device(local)
+    levels = [configs.build_level(d, device=local, kl=True) for d in defs]
+    costs = [lv.info["dof_updates_per_solve"] for lv in levels]
+    for _ in range(args.warmup):
+        wavemc.run_mlmc(levels, costs, wavemc.MlmcConfig(eps=eps))
+    torch.cuda.synchronize()
+    launches0 = wavemc.launch_count()
+    times, res = [], None
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            res = wavemc.run_mlmc(levels, costs, wavemc.MlmcConfig(eps=eps))
+            times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    work = sum(lv["cost"]["dof_updates"] for lv in res.levels)
+    line = {"metric": "MLMC time-to-RMSE", "value": sec, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based RNG, Box-Muller KL weights, seed 0)",
+            "config": {"workload": f"BASELINE config 4: adaptive MLMC to RMSE {eps}, log-normal KL (sigma 0.5, "
+                                   "l 0.1, 64 modes, 16x16 cells), config-1 geometry", "eps": eps},
+            "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 16 * sum(lv["n_samples"] for lv in res.levels)},
+            "gpu_launches": (wavemc.launch_count() - launches0) // max(1, args.steps), "clocks": clocks.summary(),
+            "dof_updates_per_s": work / sec, "rmse": res.rmse, "converged": res.converged,
+            "estimate": res.estimate, "N_l": [lv["n_samples"] for lv in res.levels]}
+    if rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
+    if args.config == 4:
+        return adaptive_arm(args, world, rank, local)
     if args.impl == "reference":
         return reference_arm(args, world, rank)
     return b200_arm(args, world, rank, local)

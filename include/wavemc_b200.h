@@ -49,6 +49,9 @@ extern "C" {
 #define WMC_LEAPFROG 0
 #define WMC_LOCAL_TIME_STEPPING 1
 
+#define WMC_FIELD_UNIFORM 0        /* c_k = next_uniform(lo, hi) per cell */
+#define WMC_FIELD_LOGNORMAL_KL 1   /* c = exp(g), g a truncated KL expansion sampled at cell centres */
+
 typedef struct wmc_mesh wmc_mesh;
 typedef struct wmc_level wmc_level;
 
@@ -86,6 +89,10 @@ typedef struct {
     double qoi_box[4];           /* x0, x1, y0, y1: Q = lumped integral of u(T) over the box */
     int device;                  /* CUDA device ordinal */
     int batch;                   /* samples per device batch, 0 = automatic */
+    int field;                   /* WMC_FIELD_UNIFORM or WMC_FIELD_LOGNORMAL_KL */
+    double kl_sigma;             /* KL: standard deviation of g */
+    double kl_corr_len;          /* KL: correlation length of exp(-|dx|/l - |dy|/l) */
+    int kl_modes;                /* KL: number of terms, xi_m ~ N(0,1) by Box-Muller over next_unit pairs */
 } wmc_level_desc;
 
 void wmc_level_desc_default(wmc_level_desc* desc);
@@ -142,6 +149,15 @@ int wmc_eval_pairs_device(wmc_level* fine, wmc_level* coarse, uint64_t seed, uin
  * level pair is issued on the fine level's stream. */
 void* wmc_level_stream(wmc_level* level);
 int wmc_synchronize(wmc_level* level, wmc_error* err);
+
+/* KL table of the log-normal field: table[cell * modes + m] =
+ * sigma sqrt(lambda_m) phi_m(centre of cell), lambda[m] (unit variance). */
+int wmc_kl_table(int cells_x, int cells_y, double sigma, double corr_len, int modes, double* table, double* lambda);
+
+/* The level's per-sample cell coefficients for indices first..first+count-1,
+ * out[i * n_cells + k], exactly as the solves use them. */
+int wmc_level_draw(wmc_level* level, uint64_t seed, uint32_t level_index, uint64_t first, uint64_t count,
+                   double* out);
 
 /* Per-sample coefficients exactly as the device draws them (RNG parity). */
 int wmc_draw_cells(uint64_t seed, uint32_t level, uint64_t first, uint64_t count, int n_cells, double lo, double hi,

@@ -104,6 +104,26 @@ def main():
     adaptive["model_cost"] = [lv["n"] + (lv["n_steps"] - 1) * (lv["n"] + (d.substeps - 1) * lv["n_r"])
                               for lv, d in zip(pairs["levels"], c1)]
     dump("config1_adaptive.json", adaptive)
+
+    # config 4: log-normal KL coefficient on a 16 x 16 cell grid (new field,
+    # our shared definition), solved by the reference: coupled pairs and the
+    # reference run_mlmc at the BASELINE RMSE target
+    from paper_2106_11117_b200 import wavemc
+    kl = configs.KL_FIELD
+    table, lam = wavemc.kl_table(kl["cells"][0], kl["cells"][1], kl["sigma"], kl["corr_len"], kl["modes"])
+    tpath = os.path.join(tmp, "kl.txt")
+    with open(tpath, "w") as f:
+        f.write(f"{table.shape[0]} {table.shape[1]}\n")
+        f.write("\n".join(repr(float(v)) for v in table.ravel()))
+        f.write("\n")
+    klargs = {"kl-table": tpath, "cells-x": kl["cells"][0], "cells-y": kl["cells"][1]}
+    kl_pairs = ref.mlmc(specs[:3], [4, 3, 2], per_sample=True, **klargs)
+    kl_pairs["kl_lambda_sum"] = float(lam.sum())
+    dump("config4_pairs.json", kl_pairs)
+    kl_adaptive = ref.adaptive(specs, configs.CONFIG4_EPS, **klargs)
+    kl_adaptive["eps"] = configs.CONFIG4_EPS
+    kl_adaptive["model_cost"] = adaptive["model_cost"]
+    dump("config4_adaptive.json", kl_adaptive)
     print("golden fixtures written to", GOLDEN)
 
 

@@ -31,7 +31,7 @@ class OProblem(C.Structure):
     _fields_ = [("cells_x", C.c_int), ("cells_y", C.c_int), ("coef_lo", C.c_double), ("coef_hi", C.c_double),
                 ("final_time", C.c_double), ("dt", C.c_double), ("substeps", C.c_int), ("nu", C.c_double),
                 ("kind", C.c_int), ("ic_x", C.c_double), ("ic_y", C.c_double), ("ic_w2", C.c_double),
-                ("box", C.c_double * 4)]
+                ("box", C.c_double * 4), ("kl_table", C.POINTER(C.c_double)), ("kl_modes", C.c_int)]
 
 
 def build(force: bool = False) -> None:
@@ -58,8 +58,15 @@ class MeshArrays:
 
 
 def problem(dt, substeps=1, kind=1, final_time=1.0, nu=0.01, cells=(4, 4), coef=(0.5, 1.5),
-            ic=(0.3, 0.5, 0.01), box=(0.7, 0.9, 0.4, 0.6)) -> OProblem:
+            ic=(0.3, 0.5, 0.01), box=(0.7, 0.9, 0.4, 0.6), kl_table=None) -> OProblem:
+    """kl_table: None (uniform cells) or a contiguous float64 array [cell][mode]
+    (kept alive by the returned struct)."""
     p = OProblem()
+    if kl_table is not None:
+        kl_table = np.ascontiguousarray(kl_table, np.float64)
+        p._kl_keep = kl_table
+        p.kl_table = kl_table.ctypes.data_as(C.POINTER(C.c_double))
+        p.kl_modes = kl_table.shape[1]
     p.cells_x, p.cells_y = cells
     p.coef_lo, p.coef_hi = coef
     p.final_time, p.dt, p.substeps, p.nu, p.kind = final_time, dt, substeps, nu, kind
@@ -80,6 +87,8 @@ class COracle:
         L.wmc_oracle_stream_words.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.POINTER(C.c_uint64)]
         L.wmc_oracle_draw_cells.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_double, C.c_double,
                                             C.POINTER(C.c_double)]
+        L.wmc_oracle_draw_kl.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.POINTER(C.c_double), C.c_int,
+                                         C.c_int, C.POINTER(C.c_double)]
         L.wmc_oracle_chebyshev.argtypes = [C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                            C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.wmc_oracle_solve.argtypes = [C.POINTER(OMesh), C.POINTER(OProblem), C.POINTER(C.c_double),
@@ -101,6 +110,13 @@ class COracle:
     def draw_cells(self, seed, level, index, n_cells=16, lo=0.5, hi=1.5):
         out = np.empty(n_cells, np.float64)
         self.lib.wmc_oracle_draw_cells(seed, level, index, n_cells, lo, hi, out.ctypes.data_as(C.POINTER(C.c_double)))
+        return out
+
+    def draw_kl(self, seed, level, index, table):
+        table = np.ascontiguousarray(table, np.float64)
+        out = np.empty(table.shape[0], np.float64)
+        self.lib.wmc_oracle_draw_kl(seed, level, index, table.ctypes.data_as(C.POINTER(C.c_double)), table.shape[0],
+                                    table.shape[1], out.ctypes.data_as(C.POINTER(C.c_double)))
         return out
 
     def chebyshev(self, p, nu):
@@ -183,12 +199,14 @@ class RefDriver:
             args += [f"--{k}", v]
         return json.loads(self.run(*args))
 
-    def adaptive(self, specs, eps, threads=0, seed=0, max_level=6, kind="lts"):
+    def adaptive(self, specs, eps, threads=0, seed=0, max_level=6, kind="lts", **kw):
         """Reference run_mlmc (src/mlmc.cpp:165-233) over the given levels."""
         args = ["adaptive", "--kind", kind, "--eps", repr(eps), "--threads", threads, "--seed", seed,
                 "--max-level", max_level]
         for mesh_path, dt, p in specs:
             args += ["--level-spec", f"{mesh_path},{dt!r},{p}"]
+        for k, v in kw.items():
+            args += [f"--{k}", v]
         return json.loads(self.run(*args))
 
     def level(self, mesh_path, dt, p, kind="lts"):

@@ -88,6 +88,8 @@ struct ProblemDef {
     Integrator kind = Integrator::LocalTimeStepping;
     double ic_x = 0.3, ic_y = 0.5, ic_w2 = 0.01;
     double box_x0 = 0.7, box_x1 = 0.9, box_y0 = 0.4, box_y1 = 0.6;
+    std::vector<double> kl;  // log-normal KL table [cell * kl_modes + m] (empty: uniform cells)
+    int kl_modes = 0;
 };
 
 ProblemDef problem_from(const Args& a) {
@@ -99,6 +101,16 @@ ProblemDef problem_from(const Args& a) {
     d.final_time = a.num("T", 1.0);
     d.nu = a.num("nu", 0.01);
     d.kind = a.get("kind", "lts") == "lf" ? Integrator::Leapfrog : Integrator::LocalTimeStepping;
+    const std::string kl = a.get("kl-table");
+    if (!kl.empty()) {  // "<cells> <modes>" then cells*modes values (written by the shared problem definition)
+        std::ifstream in(kl);
+        int cells = 0;
+        in >> cells >> d.kl_modes;
+        if (!in || cells != d.cells_x * d.cells_y) throw ConfigError("kl-table: header does not match the cell grid");
+        d.kl.resize(static_cast<std::size_t>(cells) * d.kl_modes);
+        for (double& v : d.kl) in >> v;
+        if (!in) throw ConfigError("kl-table: truncated");
+    }
     return d;
 }
 
@@ -204,7 +216,25 @@ Level make_level(const ProblemDef& d, const std::string& mesh_path, double dt, i
 
 std::vector<double> draw_cells(const ProblemDef& d, RngStream& stream) {
     std::vector<double> c(d.cells_x * d.cells_y);
-    for (double& v : c) v = stream.next_uniform(d.coef_lo, d.coef_hi);
+    if (d.kl.empty()) {
+        for (double& v : c) v = stream.next_uniform(d.coef_lo, d.coef_hi);
+        return c;
+    }
+    // log-normal KL (BASELINE config 4; no reference counterpart): Box-Muller
+    // over consecutive next_unit() pairs, c_k = exp(sum_m T[k][m] xi_m)
+    std::vector<double> xi(d.kl_modes);
+    const double two_pi = 6.283185307179586;
+    for (int i = 0; 2 * i < d.kl_modes; ++i) {
+        const double u1 = stream.next_unit(), u2 = stream.next_unit();
+        const double r = std::sqrt(-2.0 * std::log(1.0 - u1)), th = two_pi * u2;
+        xi[2 * i] = r * std::cos(th);
+        if (2 * i + 1 < d.kl_modes) xi[2 * i + 1] = r * std::sin(th);
+    }
+    for (std::size_t k = 0; k < c.size(); ++k) {
+        double g = 0.0;
+        for (int m = 0; m < d.kl_modes; ++m) g += d.kl[k * d.kl_modes + m] * xi[m];
+        c[k] = std::exp(g);
+    }
     return c;
 }
 

@@ -41,6 +41,30 @@ void wmc_oracle_draw_cells(uint64_t seed, uint32_t level, uint64_t index, int n_
     }
 }
 
+/* Log-normal KL on the cell grid -- not in the reference (its only KL field is
+ * 1D with U(-1,1) weights, src/rng.cpp:42-51); the same definition as the
+ * device draw: words 2i, 2i+1 -> u1, u2 (next_unit), r = sqrt(-2 log(1-u1)),
+ * xi_2i = r cos(2 pi u2), xi_2i+1 = r sin(2 pi u2), c_k = exp(sum T[k][m] xi_m). */
+void wmc_oracle_draw_kl(uint64_t seed, uint32_t level, uint64_t index, const double* table, int n_cells, int modes,
+                        double* out) {
+    const uint64_t key = stream_key(seed, level, index);
+    double xi[128];
+    const double two_pi = 6.283185307179586;
+    for (int i = 0; 2 * i < modes && 2 * i < 128; ++i) {
+        const uint64_t w1 = wmc_oracle_mix64(key + (uint64_t)(2 * i) * 0x9e3779b97f4a7c15ULL);
+        const uint64_t w2 = wmc_oracle_mix64(key + (uint64_t)(2 * i + 1) * 0x9e3779b97f4a7c15ULL);
+        const double u1 = (double)(w1 >> 11) * 0x1.0p-53, u2 = (double)(w2 >> 11) * 0x1.0p-53;
+        const double r = sqrt(-2.0 * log(1.0 - u1)), th = two_pi * u2;
+        xi[2 * i] = r * cos(th);
+        if (2 * i + 1 < modes) xi[2 * i + 1] = r * sin(th);
+    }
+    for (int k = 0; k < n_cells; ++k) {
+        double g = 0.0;
+        for (int m = 0; m < modes; ++m) g += table[k * modes + m] * xi[m];
+        out[k] = exp(g);
+    }
+}
+
 /* ---- Chebyshev constants: src/integrators.cpp:34-66 ---- */
 
 int wmc_oracle_chebyshev(int p, double nu, double* delta, double* omega, double* beta_int, double* beta_half) {
@@ -437,7 +461,10 @@ int wmc_oracle_eval_pairs(const wmc_oracle_mesh* fine, const wmc_oracle_problem*
     double* cells = (double*)malloc(sizeof(double) * (size_t)ncell);
     int status = 0;
     for (long i = 0; i < count && status == 0; ++i) {
-        wmc_oracle_draw_cells(seed, level, first + (uint64_t)i, ncell, pf->coef_lo, pf->coef_hi, cells);
+        if (pf->kl_table)
+            wmc_oracle_draw_kl(seed, level, first + (uint64_t)i, pf->kl_table, ncell, pf->kl_modes, cells);
+        else
+            wmc_oracle_draw_cells(seed, level, first + (uint64_t)i, ncell, pf->coef_lo, pf->coef_hi, cells);
         double qf = 0.0, qc = 0.0;
         long step = 0;
         status = wmc_oracle_solve(fine, pf, cells, &qf, &step, NULL);

@@ -18,6 +18,8 @@ WMC_NUMERICAL_ERROR = 3
 WMC_DEVICE_ERROR = 4
 WMC_LEAPFROG = 0
 WMC_LOCAL_TIME_STEPPING = 1
+WMC_FIELD_UNIFORM = 0
+WMC_FIELD_LOGNORMAL_KL = 1
 
 
 class SquareMeshSpec(C.Structure):
@@ -29,7 +31,8 @@ class LevelDesc(C.Structure):
     _fields_ = [("cells_x", C.c_int), ("cells_y", C.c_int), ("coef_lo", C.c_double), ("coef_hi", C.c_double),
                 ("final_time", C.c_double), ("dt", C.c_double), ("substeps", C.c_int), ("nu", C.c_double),
                 ("integrator", C.c_int), ("ic_x", C.c_double), ("ic_y", C.c_double), ("ic_width2", C.c_double),
-                ("qoi_box", C.c_double * 4), ("device", C.c_int), ("batch", C.c_int)]
+                ("qoi_box", C.c_double * 4), ("device", C.c_int), ("batch", C.c_int), ("field", C.c_int),
+                ("kl_sigma", C.c_double), ("kl_corr_len", C.c_double), ("kl_modes", C.c_int)]
 
 
 class LevelInfo(C.Structure):
@@ -89,6 +92,8 @@ SIGNATURES = [
     ("wmc_eval_pairs_device", C.c_int, [_VP, _VP, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, _VP, _VP]),
     ("wmc_level_stream", _VP, [_VP]),
     ("wmc_synchronize", C.c_int, [_VP, P(Error)]),
+    ("wmc_kl_table", C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _DP, _DP]),
+    ("wmc_level_draw", C.c_int, [_VP, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, _DP]),
     ("wmc_draw_cells", C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, C.c_double, C.c_double,
                                  C.c_int, _DP]),
     ("wmc_run_mlmc_fixed", C.c_int, [P(_VP), C.c_int, P(C.c_long), P(C.c_long), C.c_uint64, P(LevelStats),

@@ -67,6 +67,18 @@ def config3() -> LevelDef:
     return LevelDef(1024, 8, 0.2 / 1024, 8, WMC_LOCAL_TIME_STEPPING, final_time=0.5)
 
 
+def config4() -> list[LevelDef]:
+    """Adaptive MLMC, config-1 geometry, log-normal KL coefficient (see
+    KL_FIELD); levels as config 1."""
+    return config1()
+
+
+# config 4 coefficient: c = exp(g), g = 0.5 * truncated KL (64 modes) of the
+# separable exponential covariance exp(-|dx|/0.1 - |dy|/0.1), N(0,1) weights,
+# sampled at the centres of a 16 x 16 cell grid (cell lines on mesh lines)
+KL_FIELD = {"cells": (16, 16), "sigma": 0.5, "corr_len": 0.1, "modes": 64}
+CONFIG4_EPS = 1e-3
+
 CONFIG0_COUNT = 1024
 CONFIG3_COUNT = 8192
 
@@ -76,12 +88,18 @@ def build_mesh(d: LevelDef):
     return Mesh.build_square(d.n_coarse, d.ratio, FINE_LO, FINE_HI, SNAP)
 
 
-def level_spec(d: LevelDef, device: int = 0, batch: int = 0):
+def level_spec(d: LevelDef, device: int = 0, batch: int = 0, kl: bool = False):
     from .wavemc import LevelSpec
+    if kl:
+        from ._native import WMC_FIELD_LOGNORMAL_KL
+        return LevelSpec(dt=d.dt, substeps=d.substeps, integrator=d.integrator, final_time=d.final_time,
+                         device=device, batch=batch, cells_x=KL_FIELD["cells"][0], cells_y=KL_FIELD["cells"][1],
+                         field=WMC_FIELD_LOGNORMAL_KL, kl_sigma=KL_FIELD["sigma"], kl_corr_len=KL_FIELD["corr_len"],
+                         kl_modes=KL_FIELD["modes"])
     return LevelSpec(dt=d.dt, substeps=d.substeps, integrator=d.integrator, final_time=d.final_time, device=device,
                      batch=batch)
 
 
-def build_level(d: LevelDef, device: int = 0, batch: int = 0):
+def build_level(d: LevelDef, device: int = 0, batch: int = 0, kl: bool = False):
     from .wavemc import Level
-    return Level(build_mesh(d), level_spec(d, device, batch))
+    return Level(build_mesh(d), level_spec(d, device, batch, kl))

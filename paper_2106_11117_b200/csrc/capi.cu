@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/wavemc_b200.h"
+#include "host/field.hpp"
 #include "host/level.hpp"
 #include "host/mesh.hpp"
 #include "kernels.cuh"
@@ -101,7 +102,7 @@ struct wmc_level {
 
     // sweep operator
     int* d_row_ptr = nullptr;
-    signed char* d_row_cell = nullptr;
+    short* d_row_cell = nullptr;
     int* d_ent = nullptr;
     double* d_a0 = nullptr;
     double* d_z0 = nullptr;
@@ -138,7 +139,7 @@ struct wmc_level {
     std::uint16_t* d_gen_col = nullptr;
     int* d_slot_rc = nullptr;
     double* d_slot_a0 = nullptr;
-    std::uint8_t* d_slot_cell = nullptr;
+    std::uint16_t* d_slot_cell = nullptr;
     int* d_grc_cell = nullptr;
     double* d_grc_a0 = nullptr;
     int n_slots = 0;
@@ -148,6 +149,7 @@ struct wmc_level {
     Workspace ws[2];
     double* d_cells = nullptr;
     double* d_dq = nullptr;
+    double* d_kl = nullptr;  // log-normal KL table [cell][mode]
     // optional per-kernel event timing (profiling pass only)
     bool profile = false;
     std::vector<cudaEvent_t> ev_sweep, ev_sub, ev_upd;  // start/stop pairs
@@ -160,7 +162,7 @@ struct wmc_level {
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_grc_cell,
-                        (void*)d_grc_a0, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
+                        (void*)d_grc_a0, (void*)d_kl, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
             if (p) cudaFree(p);
         for (auto& w : ws)
             for (void* p : {(void*)w.za, (void*)w.zb, (void*)w.g, (void*)w.q, (void*)w.fail, (void*)w.da, (void*)w.db})
@@ -181,17 +183,18 @@ void build_device_level(wmc_level& L) {
     check(cudaSetDevice(L.device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking), "cudaStreamCreate");
 
-    if (t.n >= (1 << 24)) throw ConfigError("level: more than 2^24 DOFs");
+    if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
+    if (t.n_cells > wmc::kMaxCells) throw ConfigError("level: more than 511 coefficient cells");
     std::vector<int> ent(t.col.size());
-    for (std::size_t k = 0; k < ent.size(); ++k) ent[k] = t.col[k] | (t.cell[k] << 24);
+    for (std::size_t k = 0; k < ent.size(); ++k) ent[k] = t.col[k] | (t.cell[k] << wmc::kColBits);
     L.d_row_ptr = upload(t.row_ptr);
     {
-        std::vector<signed char> rc(t.n, -1);
+        std::vector<short> rc(t.n, -1);
         for (int i = 0; i < t.n; ++i) {
             int c = t.cell[t.row_ptr[i]];
             for (int k = t.row_ptr[i]; k < t.row_ptr[i + 1]; ++k)
                 if (t.cell[k] != c) c = -1;
-            rc[i] = static_cast<signed char>(c < 128 ? c : -1);
+            rc[i] = static_cast<short>(c);
         }
         L.d_row_cell = upload(rc);
     }
@@ -208,7 +211,7 @@ void build_device_level(wmc_level& L) {
     L.n_wid = static_cast<int>(t.rc_ptr.size()) - 1;
     const bool onchip_fits = t.n_r <= wmc::kSubThreads * wmc::kSubMaxRpt && t.n_r < 65536 && L.n_wid < 65535;
     if (lts && (fp == "global" || !onchip_fits)) {
-        if (t.n >= (1 << 24)) throw ConfigError("level: more than 2^24 DOFs");
+        if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
         L.path = SubPath::Global;
         L.d_apg_ptr = upload(t.apg_ptr);
         L.d_apg_ent = upload(t.apg_ent);
@@ -255,6 +258,11 @@ void build_device_level(wmc_level& L) {
         L.sub_smem = wmc::substep_smem_bytes(probe);
         L.sub_grid = wmc::substep_max_grid(L.device, L.sub_smem);
     }
+    if (L.spec.field == wmc::Field::LognormalKL) {
+        const wmc::KLTable kl =
+            wmc::kl_cell_table(L.spec.cells_x, L.spec.cells_y, L.spec.kl_sigma, L.spec.kl_corr_len, L.spec.kl_modes);
+        L.d_kl = upload(kl.t);
+    }
     L.d_qdof = upload(t.qoi_dof);
     L.d_qw = upload(t.qoi_w);
     L.d_qsm = upload(t.sqrt_mass_qoi);
@@ -286,7 +294,7 @@ void build_device_level(wmc_level& L) {
         std::vector<int> soff(n_slices + 1, 0), slot_rc{0}, rc_cell;
         std::vector<std::uint16_t> gcol;
         std::vector<double> rc_a0, slot_a0;
-        std::vector<std::uint8_t> slot_cell;
+        std::vector<std::uint16_t> slot_cell;
         for (int sl = 0; sl < n_slices; ++sl) {
             int width = fixed_width ? wmc::kLatGenWidth : 0;
             for (int l = 0; l < 32; ++l) {
@@ -298,16 +306,16 @@ void build_device_level(wmc_level& L) {
                     const int q = sl * 32 + l;
                     std::uint16_t c = 0;
                     double a1 = 0.0;
-                    std::uint8_t k1 = 0;
+                    std::uint16_t k1 = 0;
                     if (q < n_gen && e < t.gen_ptr[ord[q] + 1] - t.gen_ptr[ord[q]]) {
                         const int ent = t.gen_ptr[ord[q]] + e;
                         c = static_cast<std::uint16_t>(t.gen_col[ent]);
                         const int nt = t.gen_rc_ptr[ent + 1] - t.gen_rc_ptr[ent];
                         if (nt == 1) {
                             a1 = t.gen_rc_a0[t.gen_rc_ptr[ent]];
-                            k1 = static_cast<std::uint8_t>(t.gen_rc_cell[t.gen_rc_ptr[ent]]);
+                            k1 = static_cast<std::uint16_t>(t.gen_rc_cell[t.gen_rc_ptr[ent]]);
                         } else {
-                            k1 = 0xff;
+                            k1 = wmc::kMultiCell;
                             for (int k = t.gen_rc_ptr[ent]; k < t.gen_rc_ptr[ent + 1]; ++k) {
                                 rc_cell.push_back(t.gen_rc_cell[k]);
                                 rc_a0.push_back(t.gen_rc_a0[k]);
@@ -582,13 +590,24 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     check(cudaGetLastError(), "kernel launch");
 }
 
+void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S,
+                 double* cells, cudaStream_t st) {
+    if (L.spec.field == wmc::Field::LognormalKL)
+        wmc::launch_draw_kl(seed, level, first, count, S, L.tab.n_cells, L.spec.kl_modes, L.d_kl, cells, st);
+    else
+        wmc::launch_draw_cells(seed, level, first, count, S, L.tab.n_cells, L.spec.coef_lo, L.spec.coef_hi, cells,
+                               st);
+}
+
 void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
     if (!fine) throw ConfigError("eval_pairs: fine level is NULL");
     if (!coarse) return;
     if (fine->device != coarse->device) throw ConfigError("eval_pairs: levels on different devices");
-    if (fine->tab.n_cells != coarse->tab.n_cells || fine->spec.coef_lo != coarse->spec.coef_lo ||
-        fine->spec.coef_hi != coarse->spec.coef_hi)
-        throw ConfigError("eval_pairs: coefficient grids of the pair differ");
+    const auto& a = fine->spec;
+    const auto& b = coarse->spec;
+    if (fine->tab.n_cells != coarse->tab.n_cells || a.coef_lo != b.coef_lo || a.coef_hi != b.coef_hi ||
+        a.field != b.field || a.kl_sigma != b.kl_sigma || a.kl_corr_len != b.kl_corr_len || a.kl_modes != b.kl_modes)
+        throw ConfigError("eval_pairs: coefficient fields of the pair differ");
 }
 
 void solve_counts(const wmc::LevelTables& t, wmc_cost& c, long solves) {
@@ -625,8 +644,7 @@ void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std
     for (std::uint64_t off = 0; off < count; off += cap) {
         const int c = static_cast<int>(std::min<std::uint64_t>(cap, count - off));
         const int S = round64(c);
-        wmc::launch_draw_cells(seed, level, first + off, c, S, fine->tab.n_cells, fine->spec.coef_lo,
-                               fine->spec.coef_hi, fine->d_cells, st);
+        launch_draw(*fine, seed, level, first + off, c, S, fine->d_cells, st);
         g_launches += 2;  // draw + pair difference
         Workspace& wf = workspace(*fine, 0);
         solve_batch(*fine, wf, fine->d_cells, S, c, st);
@@ -779,6 +797,15 @@ wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     s.qoi.x1 = desc->qoi_box[1];
     s.qoi.y0 = desc->qoi_box[2];
     s.qoi.y1 = desc->qoi_box[3];
+    if (desc->field != WMC_FIELD_UNIFORM && desc->field != WMC_FIELD_LOGNORMAL_KL)
+        throw ConfigError("wmc_level_create: unknown coefficient field");
+    s.field = desc->field == WMC_FIELD_LOGNORMAL_KL ? wmc::Field::LognormalKL : wmc::Field::Uniform;
+    s.kl_sigma = desc->kl_sigma;
+    s.kl_corr_len = desc->kl_corr_len;
+    s.kl_modes = desc->kl_modes;
+    if (s.field == wmc::Field::LognormalKL &&
+        (s.kl_modes < 1 || s.kl_modes > wmc::kMaxKLModes || !(s.kl_corr_len > 0.0) || !(s.kl_sigma >= 0.0)))
+        throw ConfigError("wmc_level_create: KL field needs 1..64 modes, corr_len > 0, sigma >= 0");
     return s;
 }
 
@@ -912,6 +939,10 @@ void wmc_level_desc_default(wmc_level_desc* d) {
     d->qoi_box[3] = 0.6;
     d->device = 0;
     d->batch = 0;
+    d->field = WMC_FIELD_UNIFORM;
+    d->kl_sigma = 0.5;
+    d->kl_corr_len = 0.1;
+    d->kl_modes = 64;
 }
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out) {
@@ -985,6 +1016,34 @@ int wmc_eval_pairs_device(wmc_level* fine, wmc_level* coarse, uint64_t seed, uin
             !(d_dq && d_q_fine))
             throw ConfigError("wmc_eval_pairs_device: results of more than one batch need device buffers");
         eval_pairs_impl(fine, coarse, seed, level, first, count, nullptr, nullptr, d_dq, d_q_fine, nullptr, nullptr);
+    });
+}
+
+int wmc_kl_table(int cells_x, int cells_y, double sigma, double corr_len, int modes, double* table, double* lambda) {
+    return guarded([&] {
+        if (modes > wmc::kMaxKLModes) throw ConfigError("wmc_kl_table: at most 64 modes");
+        const wmc::KLTable kl = wmc::kl_cell_table(cells_x, cells_y, sigma, corr_len, modes);
+        if (table) std::copy(kl.t.begin(), kl.t.end(), table);
+        if (lambda) std::copy(kl.lambda.begin(), kl.lambda.end(), lambda);
+    });
+}
+
+int wmc_level_draw(wmc_level* L, uint64_t seed, uint32_t level_index, uint64_t first, uint64_t count, double* out) {
+    return guarded([&] {
+        if (!L || !out) throw ConfigError("wmc_level_draw: NULL argument");
+        check(cudaSetDevice(L->device), "cudaSetDevice");
+        const int S = round64(static_cast<long>(count));
+        const int nc = L->tab.n_cells;
+        double* d = nullptr;
+        check(cudaMalloc(&d, sizeof(double) * S * nc), "cudaMalloc");
+        launch_draw(*L, seed, level_index, first, static_cast<int>(count), S, d, L->stream);
+        std::vector<double> h(static_cast<std::size_t>(S) * nc);
+        cudaError_t e = cudaMemcpyAsync(h.data(), d, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, L->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
+        cudaFree(d);
+        check(e, "draw copy");
+        for (std::uint64_t i = 0; i < count; ++i)
+            for (int k = 0; k < nc; ++k) out[i * nc + k] = h[static_cast<std::size_t>(k) * S + i];
     });
 }
 

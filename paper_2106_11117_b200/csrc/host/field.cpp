@@ -1,0 +1,87 @@
+#include "field.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+
+namespace wmc {
+
+namespace {
+
+struct Mode1D {
+    double omega, lambda;
+    bool even;
+};
+
+// 1D eigenpairs of exp(-|x - y| / l) on [-a, a], a = 1/2:
+// lambda = 2c / (omega^2 + c^2), c = 1/l, with
+//   even (cos):  c - omega tan(omega a) = 0,  omega a in (k pi, k pi + pi/2)
+//   odd  (sin):  omega + c tan(omega a) = 0,  omega a in (k pi + pi/2, (k+1) pi)
+std::vector<Mode1D> modes_1d(double corr_len, int count) {
+    const double a = 0.5, c = 1.0 / corr_len, pi = 3.14159265358979323846;
+    std::vector<Mode1D> out;
+    for (int k = 0; static_cast<int>(out.size()) < count; ++k) {
+        for (int parity = 0; parity < 2 && static_cast<int>(out.size()) < count; ++parity) {
+            const bool even = parity == 0;
+            double lo = even ? k * pi : k * pi + pi / 2, hi = even ? k * pi + pi / 2 : (k + 1) * pi;
+            lo = (lo + 1e-12) / a;
+            hi = (hi - 1e-12) / a;
+            auto f = [&](double w) { return even ? c - w * std::tan(w * a) : w + c * std::tan(w * a); };
+            double flo = f(lo);
+            for (int it = 0; it < 200; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                const double fm = f(mid);
+                if ((fm > 0) == (flo > 0)) {
+                    lo = mid;
+                    flo = fm;
+                } else {
+                    hi = mid;
+                }
+            }
+            const double w = 0.5 * (lo + hi);
+            out.push_back({w, 2.0 * c / (w * w + c * c), even});
+        }
+    }
+    std::sort(out.begin(), out.end(), [](const Mode1D& x, const Mode1D& y) { return x.lambda > y.lambda; });
+    return out;
+}
+
+double phi(const Mode1D& m, double x) {  // x in [-1/2, 1/2], L2-normalised
+    const double a = 0.5, w = m.omega;
+    if (m.even) return std::cos(w * x) / std::sqrt(a + std::sin(2.0 * w * a) / (2.0 * w));
+    return std::sin(w * x) / std::sqrt(a - std::sin(2.0 * w * a) / (2.0 * w));
+}
+
+}  // namespace
+
+KLTable kl_cell_table(int cells_x, int cells_y, double sigma, double corr_len, int modes) {
+    if (cells_x < 1 || cells_y < 1 || modes < 1 || !(sigma >= 0.0) || !(corr_len > 0.0))
+        throw std::invalid_argument("kl_cell_table: bad parameters");
+    const int n1 = modes + 8;  // enough 1D modes for the largest products
+    const std::vector<Mode1D> m1 = modes_1d(corr_len, n1);
+    struct Pair {
+        int i, j;
+        double lambda;
+    };
+    std::vector<Pair> pairs;
+    for (int i = 0; i < n1; ++i)
+        for (int j = 0; j < n1; ++j) pairs.push_back({i, j, m1[i].lambda * m1[j].lambda});
+    std::stable_sort(pairs.begin(), pairs.end(), [](const Pair& x, const Pair& y) { return x.lambda > y.lambda; });
+    pairs.resize(modes);
+    KLTable t;
+    t.cells = cells_x * cells_y;
+    t.modes = modes;
+    t.t.resize(static_cast<std::size_t>(t.cells) * modes);
+    for (const auto& p : pairs) t.lambda.push_back(p.lambda);
+    for (int iy = 0; iy < cells_y; ++iy)
+        for (int ix = 0; ix < cells_x; ++ix) {
+            const double x = (ix + 0.5) / cells_x - 0.5, y = (iy + 0.5) / cells_y - 0.5;
+            const int cell = iy * cells_x + ix;
+            for (int m = 0; m < modes; ++m)
+                t.t[static_cast<std::size_t>(cell) * modes + m] =
+                    sigma * std::sqrt(pairs[m].lambda) * phi(m1[pairs[m].i], x) * phi(m1[pairs[m].j], y);
+        }
+    return t;
+}
+
+}  // namespace wmc

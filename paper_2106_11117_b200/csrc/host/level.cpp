@@ -185,7 +185,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
     if (spec.cells_x < 1 || spec.cells_y < 1) throw std::invalid_argument("level: coefficient grid");
     if (spec.final_time <= 0.0 || spec.dt <= 0.0) throw std::invalid_argument("level: T and dt must be positive");
     if (spec.substeps < 1) throw std::invalid_argument("level: substeps >= 1");
-    if (spec.cells_x * spec.cells_y > 255) throw std::invalid_argument("level: at most 255 coefficient cells");
+    if (spec.cells_x * spec.cells_y > 511) throw std::invalid_argument("level: at most 511 coefficient cells");
 
     LevelTables L;
     const int nv = mesh.n_vertices();
@@ -293,7 +293,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
     for (int i = 0; i < L.n_r; ++i) {
         for (const auto& [j, k, a] : rows[i]) {
             if (!L.in_p[j]) continue;
-            L.apg_ent.push_back(j | (k << 24));
+            L.apg_ent.push_back(j | (k << 23));  // kColBits
             L.apg_a0.push_back(a);
         }
         L.apg_ptr[i + 1] = static_cast<int>(L.apg_ent.size());

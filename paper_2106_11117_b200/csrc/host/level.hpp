@@ -34,9 +34,14 @@ struct QoIBox {
     double x0 = 0.7, x1 = 0.9, y0 = 0.4, y1 = 0.6;
 };
 
+enum class Field : int { Uniform = 0, LognormalKL = 1 };
+
 struct LevelSpec {
     int cells_x = 4, cells_y = 4;  // coefficient grid on [0,1]^2, cell k = iy*cells_x + ix
     double coef_lo = 0.5, coef_hi = 1.5;  // c_k ~ U[coef_lo, coef_hi)
+    Field field = Field::Uniform;
+    double kl_sigma = 0.5, kl_corr_len = 0.1;  // log-normal KL (BASELINE config 4)
+    int kl_modes = 64;
     double final_time = 1.0;
     double dt = 0.0;  // requested coarse step (snapped so n_steps*dt == T)
     int substeps = 1;

@@ -53,6 +53,46 @@ __device__ __forceinline__ int n_groups(int rows) { return (rows + kSweepWarps -
 __device__ __forceinline__ int grid_chunk(int rows) { return blockIdx.x / n_groups(rows); }
 __device__ __forceinline__ int grid_rowgroup(int rows) { return blockIdx.x % n_groups(rows); }
 
+// Log-normal KL coefficients (BASELINE config 4, no reference counterpart):
+// per sample the stream's words 2i, 2i+1 give u1, u2 = next_unit(), then
+// r = sqrt(-2 log(1 - u1)), xi_2i = r cos(2 pi u2), xi_2i+1 = r sin(2 pi u2);
+// g_k = sum_m T[k][m] xi_m, c_k = exp(g_k).  One thread per sample, the
+// normals in shared memory.
+constexpr int kKLThreads = 64;
+constexpr int kKLMaxModes = 64;
+
+__global__ void __launch_bounds__(kKLThreads) draw_kl_kernel(std::uint64_t seed, std::uint32_t level,
+                                                             std::uint64_t first, int count, int S, int n_cells,
+                                                             int modes, const double* __restrict__ table,
+                                                             double* __restrict__ cells) {
+    __shared__ double xi_s[kKLMaxModes][kKLThreads];
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    if (s >= count) {
+        for (int k = 0; k < n_cells; ++k) cells[k * S + s] = 1.0;
+        return;
+    }
+    std::uint64_t key = mix64(seed);
+    key = mix64(key ^ (0xa511e9b3cc1f25d1ULL + static_cast<std::uint64_t>(level)));
+    key = mix64(key ^ (0x63d1c71ad3e29f0bULL + (first + static_cast<std::uint64_t>(s))));
+    const double two_pi = 6.283185307179586;
+    for (int i = 0; 2 * i < modes; ++i) {
+        const std::uint64_t w1 = mix64(key + static_cast<std::uint64_t>(2 * i) * 0x9e3779b97f4a7c15ULL);
+        const std::uint64_t w2 = mix64(key + static_cast<std::uint64_t>(2 * i + 1) * 0x9e3779b97f4a7c15ULL);
+        const double u1 = __dmul_rn(static_cast<double>(w1 >> 11), 0x1.0p-53);
+        const double u2 = __dmul_rn(static_cast<double>(w2 >> 11), 0x1.0p-53);
+        const double r = sqrt(-2.0 * log(1.0 - u1));
+        const double th = __dmul_rn(two_pi, u2);
+        xi_s[2 * i][threadIdx.x] = r * cos(th);
+        if (2 * i + 1 < modes) xi_s[2 * i + 1][threadIdx.x] = r * sin(th);
+    }
+    for (int k = 0; k < n_cells; ++k) {
+        double g = 0.0;
+        for (int m = 0; m < modes; ++m) g += __ldg(table + k * modes + m) * xi_s[m][threadIdx.x];
+        cells[k * S + s] = exp(g);
+    }
+}
+
 __device__ __forceinline__ void flag_fail(int* fail, int s, int count, int step) {
     if (s < count) atomicMin(fail + s, step);
 }
@@ -85,13 +125,13 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             // entries grouped by cell: sum a0 z_j within a part, then scale by
             // the part's coefficient (one coefficient load per part)
             double p0 = 0.0, p1 = 0.0;
-            int pcell = static_cast<unsigned>(__ldg(a.ent + b)) >> 24;
+            int pcell = static_cast<unsigned>(__ldg(a.ent + b)) >> kColBits;
             double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + pcell * S + s0));
             for (int k = b; k < e; ++k) {
                 const int pk = __ldg(a.ent + k);
                 const double w = __ldg(a.a0 + k);
-                const int j = pk & 0xffffff;
-                const int cell = static_cast<unsigned>(pk) >> 24;
+                const int j = pk & kColMask;
+                const int cell = static_cast<unsigned>(pk) >> kColBits;
                 if (cell != pcell) {  // warp-uniform
                     acc0 += c.x * p0;
                     acc1 += c.y * p1;
@@ -119,7 +159,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             double p0 = 0.0, p1 = 0.0;
 #pragma unroll 4
             for (int k = b; k < e; ++k) {
-                const int j = __ldg(a.ent + k) & 0xffffff;
+                const int j = __ldg(a.ent + k) & kColMask;
                 const double w = __ldg(a.a0 + k);
                 if (kInit) {
                     const double zj = __ldg(a.z0 + j);
@@ -139,8 +179,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             for (int k = b; k < e; ++k) {
                 const int pk = __ldg(a.ent + k);
                 const double w = __ldg(a.a0 + k);
-                const int j = pk & 0xffffff;
-                const int cell = static_cast<unsigned>(pk) >> 24;
+                const int j = pk & kColMask;
+                const int cell = static_cast<unsigned>(pk) >> kColBits;
                 const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
                 if (kInit) {
                     const double zj = __ldg(a.z0 + j);
@@ -225,8 +265,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
     for (int k = b; k < e; ++k) {
         const int pk = __ldg(a.ent + k);
         const double w = __ldg(a.a0 + k);
-        const int j = pk & 0xffffff;
-        const int cell = static_cast<unsigned>(pk) >> 24;
+        const int j = pk & kColMask;
+        const int cell = static_cast<unsigned>(pk) >> kColBits;
         const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
         const double2 v = *reinterpret_cast<const double2*>(src + j * S + s0);
         acc0 += (c.x * w) * v.x;
@@ -461,7 +501,7 @@ __host__ __device__ inline LatOff lat_offsets(const LatArgs& a) {
     o.beta = take(a.p > 1 ? a.p - 1 : 1);
     o.cm = take(a.p > 1 ? a.p - 1 : 1);
     o.gcol = take((slots * 2 + 7) / 8);  // uint16
-    o.scell = take((slots + 7) / 8);     // uint8
+    o.scell = take((slots * 2 + 7) / 8);  // uint16
     o.sj0 = take((a.n_strips + 1) / 2);  // int
     o.slen = take((a.n_strips + 1) / 2);
     o.cx = take((a.m + 1) / 2);
@@ -489,7 +529,7 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
     extern __shared__ __align__(16) double sd[];
     const LatOff o = lat_offsets(a);
     std::uint16_t* gcol = reinterpret_cast<std::uint16_t*>(sd + o.gcol);
-    std::uint8_t* scell = reinterpret_cast<std::uint8_t*>(sd + o.scell);
+    std::uint16_t* scell = reinterpret_cast<std::uint16_t*>(sd + o.scell);
     int* sj0 = reinterpret_cast<int*>(sd + o.sj0);
     int* slen = reinterpret_cast<int*>(sd + o.slen);
     int* cx = reinterpret_cast<int*>(sd + o.cx);
@@ -561,7 +601,7 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
         for (int e = tid; e < a.n_slots; e += T) {
             const int c = scell[e];
             double w;
-            if (c != 0xff) {
+            if (c != kMultiCell) {
                 w = sd[o.cl + c] * sd[o.sa0 + e];
             } else {  // several cells share this entry (edge on a coefficient line)
                 w = 0.0;
@@ -746,6 +786,12 @@ __global__ void __launch_bounds__(1024) moments_kernel(const double* __restrict_
 
 void launch_moments(const double* dq, const double* q, int count, double* out, void* stream) {
     moments_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(dq, q, count, out);
+}
+
+void launch_draw_kl(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
+                    int modes, const double* table, double* cells, void* stream) {
+    draw_kl_kernel<<<(S + kKLThreads - 1) / kKLThreads, kKLThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        seed, level, first, count, S, n_cells, modes, table, cells);
 }
 
 void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,

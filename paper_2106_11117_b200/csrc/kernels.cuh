@@ -16,6 +16,12 @@
 
 namespace wmc {
 
+// operator entries pack the column (23 bits) and the coefficient cell (9 bits)
+constexpr int kColBits = 23;
+constexpr int kColMask = (1 << kColBits) - 1;
+constexpr int kMaxCells = 511;
+constexpr unsigned kMultiCell = 0xffffu;  // slot weight with several cells
+
 constexpr int kSweepChunk = 64;  // samples per warp in the sweep (2 per lane)
 constexpr int kSweepWarps = 8;   // rows per sweep block
 constexpr int kSubThreads = 1024;
@@ -27,9 +33,9 @@ struct SweepArgs {
     int S;           // batch stride
     int count;       // live samples
     const int* row_ptr;
-    const int* ent;      // col | cell << 24
+    const int* ent;      // col | cell << kColBits
     const double* a0;
-    const signed char* row_cell;  // cell of a single-cell row, -1 otherwise (may be NULL)
+    const short* row_cell;  // cell of a single-cell row, -1 otherwise (may be NULL)
     const double* cells;
     const double* z0;    // init only
     const double* zc;    // z_n
@@ -82,7 +88,7 @@ struct LatArgs {
     const int* gen_soff;         // slot offset of each 32-row slice (rows sorted by length), n_slices + 1
     const std::uint16_t* gen_col;  // per slot: [slice][width][32], padding: col 0, weight 0
     const double* slot_a0;       // per slot: a0 of the single term
-    const std::uint8_t* slot_cell;  // per slot: its cell, 0xff when the weight has several terms
+    const std::uint16_t* slot_cell;  // per slot: its cell, kMultiCell when the weight has several terms
     const int* slot_rc;          // per slot: term range [slot_rc[e], slot_rc[e+1]) (several terms)
     const int* rc_cell;
     const double* rc_a0;
@@ -110,7 +116,7 @@ struct RUpdateArgs {
 struct GSubArgs {
     int n_r, S, count;
     const int* ptr;
-    const int* ent;       // col | cell << 24, columns in P
+    const int* ent;       // col | cell << kColBits, columns in P
     const double* a0;
     const double* cells;
     const double* g;      // [r][S]
@@ -136,6 +142,11 @@ struct QoIArgs {
     double* q;
 };
 
+// log-normal KL field on the cell grid: xi_m ~ N(0,1) by Box-Muller over
+// consecutive next_unit() pairs, g_k = sum_m table[k*modes+m] xi_m, c_k = exp(g_k)
+constexpr int kMaxKLModes = 64;
+void launch_draw_kl(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
+                    int modes, const double* table, double* cells, void* stream);
 void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
                        double lo, double hi, double* cells, void* stream);
 void launch_sweep_init(const SweepArgs& a, void* stream);

@@ -97,6 +97,10 @@ class LevelSpec:
     qoi_box: tuple = (0.7, 0.9, 0.4, 0.6)
     device: int = 0
     batch: int = 0
+    field: int = N.WMC_FIELD_UNIFORM
+    kl_sigma: float = 0.5
+    kl_corr_len: float = 0.1
+    kl_modes: int = 64
 
     def desc(self) -> N.LevelDesc:
         d = N.LevelDesc()
@@ -109,6 +113,7 @@ class LevelSpec:
         for i, v in enumerate(self.qoi_box):
             d.qoi_box[i] = v
         d.device, d.batch = self.device, self.batch
+        d.field, d.kl_sigma, d.kl_corr_len, d.kl_modes = self.field, self.kl_sigma, self.kl_corr_len, self.kl_modes
         return d
 
 
@@ -167,6 +172,22 @@ def eval_pairs_device(fine: Level, coarse: Level | None, seed: int, level: int, 
 def synchronize(level: Level) -> None:
     err = N.Error()
     N.check(N.lib().wmc_synchronize(level._h, C.byref(err)), err)
+
+
+def kl_table(cells_x: int, cells_y: int, sigma: float, corr_len: float, modes: int):
+    """(table[cell, mode], lambda[mode]) of the log-normal KL field."""
+    table = np.empty((cells_x * cells_y, modes), np.float64)
+    lam = np.empty(modes, np.float64)
+    N.check(N.lib().wmc_kl_table(cells_x, cells_y, sigma, corr_len, modes, _dptr(table), _dptr(lam)))
+    return table, lam
+
+
+def level_draw(level: "Level", seed: int, level_index: int, first: int, count: int) -> np.ndarray:
+    """The level's per-sample cell coefficients, shape (count, n_cells)."""
+    n_cells = level.spec.cells_x * level.spec.cells_y
+    out = np.empty((count, n_cells), np.float64)
+    N.check(N.lib().wmc_level_draw(level._h, seed, level_index, first, count, _dptr(out)))
+    return out
 
 
 def draw_cells(seed: int, level: int, first: int, count: int, n_cells: int = 16, lo: float = 0.5,

@@ -266,3 +266,36 @@ def test_large_r_uses_the_hbm_path():
                                      oracle_py.problem(0.2 / 32, 64, final_time=0.05), None, None, 0, 0, 0, 3)
     assert rc == 0
     assert per_sample_rel(q, ref) < QOI_RTOL
+
+
+def _kl_levels(n=5):
+    return [configs.build_level(d, kl=True) for d in configs.config4()[:n]]
+
+
+def test_kl_draw_matches_c_oracle(coracle):
+    kl = configs.KL_FIELD
+    table, _ = wavemc.kl_table(kl["cells"][0], kl["cells"][1], kl["sigma"], kl["corr_len"], kl["modes"])
+    lv = _kl_levels(1)[0]
+    got = wavemc.level_draw(lv, 0, 2, 777, 130)
+    for i in (0, 1, 64, 129):
+        ref = coracle.draw_kl(0, 2, 777 + i, table)
+        assert np.max(np.abs(got[i] - ref) / ref) < 1e-14
+
+
+def test_config4_pairs_match_reference(golden):
+    levels = _kl_levels(3)
+    for lv in golden("config4_pairs.json")["levels"]:
+        l, n = lv["level"], lv["N"]
+        dq, qf, _ = wavemc.eval_pairs(levels[l], levels[l - 1] if l else None, 0, l, 0, n)
+        assert per_sample_rel(qf, lv["q"]) < QOI_RTOL, l
+        assert np.max(np.abs(dq - lv["dq"]) / np.abs(lv["q"])) < 2 * QOI_RTOL, l
+
+
+def test_config4_adaptive_mlmc_matches_reference(golden):
+    g = golden("config4_adaptive.json")
+    res = wavemc.run_mlmc(_kl_levels(), g["model_cost"], wavemc.MlmcConfig(eps=g["eps"]))
+    assert res.converged == g["converged"]
+    assert [lv["n_samples"] for lv in res.levels] == [lv["N"] for lv in g["levels"]]
+    assert res.estimate == pytest.approx(g["estimate"], rel=MOMENT_RTOL)
+    for got, want in zip(res.levels, g["levels"]):
+        assert got["variance"] == pytest.approx(want["variance"], rel=MOMENT_RTOL)

@@ -109,3 +109,32 @@ def test_instability_reported_with_step(coracle, config0_mesh):
     pb = problem(0.2, 1, 0, final_time=20.0)  # leapfrog at dt = 0.2 on h_min = 1/128
     rc, q, step, _ = coracle.solve(config0_mesh, pb, np.ones(16))
     assert rc == 3 and step > 1
+
+
+def test_kl_table_is_a_truncated_expansion():
+    from paper_2106_11117_b200 import wavemc
+    kl = configs.KL_FIELD
+    table, lam = wavemc.kl_table(kl["cells"][0], kl["cells"][1], kl["sigma"], kl["corr_len"], kl["modes"])
+    assert table.shape == (256, 64)
+    assert np.all(np.diff(lam) <= 1e-15) and lam[0] < 1.0 and 0.3 < lam.sum() < 1.0
+    # per-cell variance of g = sigma^2 sum_m lambda_m phi_m(x)^2 <= sigma^2
+    var = np.sum(table ** 2, axis=1)
+    assert np.all(var > 0) and np.all(var <= kl["sigma"] ** 2)
+
+
+def test_config4_kl_pairs_match_reference(golden, coracle):
+    """Config 4 (log-normal KL coefficient): the C restatement against the
+    reference solver on the same cell coefficients."""
+    from paper_2106_11117_b200 import wavemc
+    kl = configs.KL_FIELD
+    table, _ = wavemc.kl_table(kl["cells"][0], kl["cells"][1], kl["sigma"], kl["corr_len"], kl["modes"])
+    g = golden("config4_pairs.json")["levels"]
+    c1 = configs.config1()
+    fine = MeshArrays(*configs.build_mesh(c1[1]).arrays())
+    coarse = MeshArrays(*configs.build_mesh(c1[0]).arrays())
+    pf = problem(c1[1].dt, c1[1].substeps, cells=kl["cells"], kl_table=table)
+    pc = problem(c1[0].dt, c1[0].substeps, cells=kl["cells"], kl_table=table)
+    rc, dq, qf, _, _ = coracle.eval_pairs(fine, pf, coarse, pc, 0, 1, 0, 2)
+    assert rc == 0
+    assert _rel(qf, g[1]["q"][:2]) < 1e-12
+    assert np.max(np.abs(dq - g[1]["dq"][:2])) < 1e-12 * np.max(np.abs(qf))
