@@ -150,6 +150,17 @@ struct wmc_level {
     double* d_cells = nullptr;
     double* d_dq = nullptr;
     double* d_kl = nullptr;  // log-normal KL table [cell][mode]
+    // per-call results of the pairs whose fine level this is: device and
+    // pinned host mirrors, grown on demand (so levels can run concurrently)
+    std::size_t r_cap = 0;
+    double* r_dq = nullptr;
+    double* r_qf = nullptr;
+    int* r_ff = nullptr;
+    int* r_fc = nullptr;
+    double* h_dq = nullptr;
+    double* h_qf = nullptr;
+    int* h_ff = nullptr;
+    int* h_fc = nullptr;
     // optional per-kernel event timing (profiling pass only)
     bool profile = false;
     std::vector<cudaEvent_t> ev_sweep, ev_sub, ev_upd;  // start/stop pairs
@@ -167,6 +178,10 @@ struct wmc_level {
         for (auto& w : ws)
             for (void* p : {(void*)w.za, (void*)w.zb, (void*)w.g, (void*)w.q, (void*)w.fail, (void*)w.da, (void*)w.db})
                 if (p) cudaFree(p);
+        for (void* p : {(void*)r_dq, (void*)r_qf, (void*)r_ff, (void*)r_fc})
+            if (p) cudaFree(p);
+        for (void* p : {(void*)h_dq, (void*)h_qf, (void*)h_ff, (void*)h_fc})
+            if (p) cudaFreeHost(p);
         for (auto e : ev_sweep) cudaEventDestroy(e);
         for (auto e : ev_sub) cudaEventDestroy(e);
         for (auto e : ev_upd) cudaEventDestroy(e);
@@ -628,19 +643,38 @@ void solve_counts(const wmc::LevelTables& t, wmc_cost& c, long solves) {
 
 // evaluates pairs; host_dq/host_qf may be NULL (device-resident mode: the
 // results for index first+i are written to dev_dq/dev_qf + i when given)
-void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::uint32_t level, std::uint64_t first,
-                     std::uint64_t count, double* host_dq, double* host_qf, double* dev_dq, double* dev_qf,
-                     wmc_cost* cost, wmc_error* err) {
+void ensure_results(wmc_level& L, std::size_t count) {
+    if (count <= L.r_cap) return;
+    check(cudaSetDevice(L.device), "cudaSetDevice");
+    check(cudaStreamSynchronize(L.stream), "synchronize");
+    for (void* p : {(void*)L.r_dq, (void*)L.r_qf, (void*)L.r_ff, (void*)L.r_fc})
+        if (p) cudaFree(p);
+    for (void* p : {(void*)L.h_dq, (void*)L.h_qf, (void*)L.h_ff, (void*)L.h_fc})
+        if (p) cudaFreeHost(p);
+    const std::size_t cap = std::max<std::size_t>(count, 256);
+    check(cudaMalloc(&L.r_dq, sizeof(double) * cap), "cudaMalloc results");
+    check(cudaMalloc(&L.r_qf, sizeof(double) * cap), "cudaMalloc results");
+    check(cudaMalloc(&L.r_ff, sizeof(int) * cap), "cudaMalloc results");
+    check(cudaMalloc(&L.r_fc, sizeof(int) * cap), "cudaMalloc results");
+    check(cudaMallocHost(&L.h_dq, sizeof(double) * cap), "cudaMallocHost");
+    check(cudaMallocHost(&L.h_qf, sizeof(double) * cap), "cudaMallocHost");
+    check(cudaMallocHost(&L.h_ff, sizeof(int) * cap), "cudaMallocHost");
+    check(cudaMallocHost(&L.h_fc, sizeof(int) * cap), "cudaMallocHost");
+    L.r_cap = cap;
+}
+
+// Issues the pairs of one index range asynchronously on the fine level's
+// stream.  Results land in dev_dq / dev_qf when given (device-resident
+// mode), else in the fine level's result buffers, copied to its pinned host
+// mirrors together with the fail flags (finish_pairs reads them).
+void issue_pairs(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::uint32_t level, std::uint64_t first,
+                 std::uint64_t count, double* dev_dq, double* dev_qf) {
     check_pair_compat(fine, coarse);
     check(cudaSetDevice(fine->device), "cudaSetDevice");
-    if (err) {
-        err->sample = -1;
-        err->step = 0;
-        err->level = static_cast<int>(level);
-    }
+    const bool to_host = dev_dq == nullptr;
+    if (to_host) ensure_results(*fine, count);
     const int cap = coarse ? std::min(fine->batch, coarse->batch) : fine->batch;
     cudaStream_t st = fine->stream;
-    std::vector<int> ff, fc;
     for (std::uint64_t off = 0; off < count; off += cap) {
         const int c = static_cast<int>(std::min<std::uint64_t>(cap, count - off));
         const int S = round64(c);
@@ -653,42 +687,75 @@ void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std
             wc = &workspace(*coarse, 1);
             solve_batch(*coarse, *wc, fine->d_cells, S, c, st);
         }
-        double* dq_dst = dev_dq ? dev_dq + off : fine->d_dq;
+        double* dq_dst = to_host ? fine->r_dq + off : dev_dq + off;
+        double* qf_dst = to_host ? fine->r_qf + off : dev_qf;
         wmc::launch_pair_diff(wf.q, wc ? wc->q : nullptr, dq_dst, c, st);
-        if (dev_qf) check(cudaMemcpyAsync(dev_qf + off, wf.q, sizeof(double) * c, cudaMemcpyDeviceToDevice, st),
-                          "copy q");
-        if (host_dq || host_qf || err) {
-            ff.resize(c);
-            check(cudaMemcpyAsync(ff.data(), wf.fail, sizeof(int) * c, cudaMemcpyDeviceToHost, st), "fail");
-            if (wc) {
-                fc.resize(c);
-                check(cudaMemcpyAsync(fc.data(), wc->fail, sizeof(int) * c, cudaMemcpyDeviceToHost, st), "fail");
-            }
-            if (host_dq)
-                check(cudaMemcpyAsync(host_dq + off, dq_dst, sizeof(double) * c, cudaMemcpyDeviceToHost, st), "dq");
-            if (host_qf)
-                check(cudaMemcpyAsync(host_qf + off, wf.q, sizeof(double) * c, cudaMemcpyDeviceToHost, st), "q");
-            check(cudaStreamSynchronize(st), "synchronize");
-            for (int i = 0; i < c; ++i) {
-                const bool bad_f = ff[i] != INT_MAX, bad_c = coarse && fc[i] != INT_MAX;
-                if (bad_f || bad_c) {
-                    if (err) {
-                        err->sample = static_cast<long>(first + off + i);
-                        err->step = bad_f ? ff[i] : fc[i];
-                        err->level = bad_f ? static_cast<int>(level) : static_cast<int>(level) - 1;
-                    }
-                    g_last_error = "level " + std::to_string(level) + ", sample " +
-                                   std::to_string(first + off + i) + ": time integration unstable";
-                    throw NumericalError(g_last_error);
-                }
-            }
+        if (qf_dst)
+            check(cudaMemcpyAsync(to_host ? qf_dst : qf_dst + off, wf.q, sizeof(double) * c, cudaMemcpyDeviceToDevice,
+                                  st),
+                  "copy q");
+        if (to_host) {
+            check(cudaMemcpyAsync(fine->r_ff + off, wf.fail, sizeof(int) * c, cudaMemcpyDeviceToDevice, st), "fail");
+            if (wc)
+                check(cudaMemcpyAsync(fine->r_fc + off, wc->fail, sizeof(int) * c, cudaMemcpyDeviceToDevice, st),
+                      "fail");
         }
     }
-    if (cost) {
-        std::memset(cost, 0, sizeof(*cost));
-        solve_counts(fine->tab, *cost, static_cast<long>(count));
-        if (coarse) solve_counts(coarse->tab, *cost, static_cast<long>(count));
+    if (to_host) {
+        check(cudaMemcpyAsync(fine->h_dq, fine->r_dq, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "dq");
+        check(cudaMemcpyAsync(fine->h_qf, fine->r_qf, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "q");
+        check(cudaMemcpyAsync(fine->h_ff, fine->r_ff, sizeof(int) * count, cudaMemcpyDeviceToHost, st), "fail");
+        if (coarse)
+            check(cudaMemcpyAsync(fine->h_fc, fine->r_fc, sizeof(int) * count, cudaMemcpyDeviceToHost, st), "fail");
     }
+}
+
+// Waits for issue_pairs' host results and reports the first failing sample
+// (lowest index) like sample_delta_q's wrapped error (src/mlmc.cpp:31-35).
+void finish_pairs(wmc_level* fine, bool has_coarse, std::uint32_t level, std::uint64_t first, std::uint64_t count,
+                  wmc_error* err) {
+    check(cudaSetDevice(fine->device), "cudaSetDevice");
+    check(cudaStreamSynchronize(fine->stream), "synchronize");
+    if (err) {
+        err->sample = -1;
+        err->step = 0;
+        err->level = static_cast<int>(level);
+    }
+    for (std::uint64_t i = 0; i < count; ++i) {
+        const bool bad_f = fine->h_ff[i] != INT_MAX, bad_c = has_coarse && fine->h_fc[i] != INT_MAX;
+        if (bad_f || bad_c) {
+            if (err) {
+                err->sample = static_cast<long>(first + i);
+                err->step = bad_f ? fine->h_ff[i] : fine->h_fc[i];
+                err->level = bad_f ? static_cast<int>(level) : static_cast<int>(level) - 1;
+            }
+            g_last_error = "level " + std::to_string(level) + ", sample " + std::to_string(first + i) +
+                           ": time integration unstable";
+            throw NumericalError(g_last_error);
+        }
+    }
+}
+
+void pair_cost(const wmc_level* fine, const wmc_level* coarse, std::uint64_t count, wmc_cost* cost) {
+    std::memset(cost, 0, sizeof(*cost));
+    solve_counts(fine->tab, *cost, static_cast<long>(count));
+    if (coarse) solve_counts(coarse->tab, *cost, static_cast<long>(count));
+}
+
+// evaluates pairs; host_dq/host_qf may be NULL (device-resident mode: the
+// results for index first+i are written to dev_dq/dev_qf + i when given)
+void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::uint32_t level, std::uint64_t first,
+                     std::uint64_t count, double* host_dq, double* host_qf, double* dev_dq, double* dev_qf,
+                     wmc_cost* cost, wmc_error* err) {
+    if (dev_dq) {
+        issue_pairs(fine, coarse, seed, level, first, count, dev_dq, dev_qf);
+    } else {
+        issue_pairs(fine, coarse, seed, level, first, count, nullptr, nullptr);
+        finish_pairs(fine, coarse != nullptr, level, first, count, err);
+        if (host_dq) std::memcpy(host_dq, fine->h_dq, sizeof(double) * count);
+        if (host_qf) std::memcpy(host_qf, fine->h_qf, sizeof(double) * count);
+    }
+    if (cost) pair_cost(fine, coarse, count, cost);
 }
 
 struct Acc {
@@ -733,18 +800,39 @@ void fill_stats(int level, const Acc& a, double model_cost, wmc_level_stats& s) 
     s.cost = a.cost;
 }
 
-void run_level(wmc_level** levels, int l, std::uint64_t seed, long first, long count, Acc& acc, wmc_error* err) {
-    std::vector<double> dq(count), q(count);
-    wmc_cost c{};
-    eval_pairs_impl(levels[l], l > 0 ? levels[l - 1] : nullptr, seed, static_cast<std::uint32_t>(l),
-                    static_cast<std::uint64_t>(first), static_cast<std::uint64_t>(count), dq.data(), q.data(),
-                    nullptr, nullptr, &c, err);
-    for (long i = 0; i < count; ++i) acc.add(dq[i], q[i]);  // fold in index order (mlmc.cpp:145-147)
-    acc.cost.matvec_full += c.matvec_full;
-    acc.cost.matvec_fine += c.matvec_fine;
-    acc.cost.matvec_coarse += c.matvec_coarse;
-    acc.cost.weighted_work += c.weighted_work;
-    acc.cost.dof_updates += c.dof_updates;
+// Runs the index ranges of several levels concurrently (each pair on its fine
+// level's stream; a level's workspaces per role keep neighbouring pairs
+// apart), then folds every level's results in index order
+// (src/mlmc.cpp:145-147).
+struct LevelJob {
+    int level;
+    long first, count;
+};
+
+void run_levels(wmc_level** levels, const std::vector<LevelJob>& jobs, std::uint64_t seed, std::vector<Acc>& acc,
+                wmc_error* err) {
+    for (const auto& j : jobs)
+        if (j.count > 0) ensure_results(*levels[j.level], static_cast<std::size_t>(j.count));
+    for (const auto& j : jobs)
+        if (j.count > 0)
+            issue_pairs(levels[j.level], j.level > 0 ? levels[j.level - 1] : nullptr, seed,
+                        static_cast<std::uint32_t>(j.level), static_cast<std::uint64_t>(j.first),
+                        static_cast<std::uint64_t>(j.count), nullptr, nullptr);
+    for (const auto& j : jobs) {
+        if (j.count <= 0) continue;
+        wmc_level* fine = levels[j.level];
+        finish_pairs(fine, j.level > 0, static_cast<std::uint32_t>(j.level), static_cast<std::uint64_t>(j.first),
+                     static_cast<std::uint64_t>(j.count), err);
+        Acc& a = acc[j.level];
+        for (long i = 0; i < j.count; ++i) a.add(fine->h_dq[i], fine->h_qf[i]);
+        wmc_cost c{};
+        pair_cost(fine, j.level > 0 ? levels[j.level - 1] : nullptr, static_cast<std::uint64_t>(j.count), &c);
+        a.cost.matvec_full += c.matvec_full;
+        a.cost.matvec_fine += c.matvec_fine;
+        a.cost.matvec_coarse += c.matvec_coarse;
+        a.cost.weighted_work += c.weighted_work;
+        a.cost.dof_updates += c.dof_updates;
+    }
 }
 
 }  // namespace
@@ -1069,11 +1157,11 @@ int wmc_run_mlmc_fixed(wmc_level** levels, int n_levels, const long* first, cons
                        wmc_level_stats* stats, wmc_error* err) {
     return guarded([&] {
         if (!levels || n_levels < 1 || !counts || !stats) throw ConfigError("wmc_run_mlmc_fixed: bad arguments");
-        for (int l = 0; l < n_levels; ++l) {
-            Acc acc;
-            if (counts[l] > 0) run_level(levels, l, seed, first ? first[l] : 0, counts[l], acc, err);
-            fill_stats(l, acc, 0.0, stats[l]);
-        }
+        std::vector<Acc> acc(n_levels);
+        std::vector<LevelJob> jobs;
+        for (int l = 0; l < n_levels; ++l) jobs.push_back({l, first ? first[l] : 0, counts[l]});
+        run_levels(levels, jobs, seed, acc, err);
+        for (int l = 0; l < n_levels; ++l) fill_stats(l, acc[l], 0.0, stats[l]);
     });
 }
 
@@ -1114,8 +1202,10 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
         bool converged = false;
         {
             while (true) {
+                std::vector<LevelJob> jobs;
                 for (int l = 0; l <= top; ++l)
-                    if (acc[l].n < targets[l]) run_level(levels, l, cfg->master_seed, acc[l].n, targets[l] - acc[l].n, acc[l], err);
+                    if (acc[l].n < targets[l]) jobs.push_back({l, acc[l].n, targets[l] - acc[l].n});
+                run_levels(levels, jobs, cfg->master_seed, acc, err);
                 std::vector<double> v(top + 1);
                 for (int l = 0; l <= top; ++l) v[l] = acc[l].variance();
                 const std::vector<long> wanted = optimal_samples_impl(v.data(), model_cost, top + 1, cfg->eps, 2);
