@@ -53,7 +53,7 @@ int cell_of(double x, double y, int nx, int ny) {
 }
 
 // lattice substep kernel variants: (threads, max rows per thread)
-constexpr int kLatticeVariants[2][2] = {{512, 8}, {1024, 4}};
+constexpr int kLatticeVariants[3][2] = {{512, 8}, {768, 6}, {1024, 4}};
 
 using StiffMap = std::map<std::tuple<int, int, int>, double>;
 

@@ -540,6 +540,7 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
     const int W = a.m + 1;
     const int nr = a.n_r;
     const double inv_h = a.inv_h;
+    const double hh = 1.0 / inv_h;
 
     // static tables, once per CTA
     for (int i = tid; i < a.n_slots; i += T) {
@@ -622,10 +623,12 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
             kNS = (cL + cR) * (0.5 * inv_h);
             dg = kE + kW + 2.0 * kNS;
         }
-        double d[K], dp[K];
+        // d_{m-1} of a lattice node is not kept in registers: it is the value
+        // the node published one substep ago, still in the buffer this
+        // substep overwrites (read just before the write; d_0 = 0)
+        double d[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            dp[k] = 0.0;
             d[k] = -a.c0 * gg[k];
             if (k < len) sd[o.v0 + base + k] = d[k] * inv_h;
         }
@@ -677,8 +680,8 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
                 const double ve = sd[ce + k], vw = sd[cw_ + k];
                 const double vn = (k + 1 < len) ? d[k + 1] * inv_h : vnl;
                 const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
-                const double next = onepb * d[k] - beta * dp[k] - cmm * (gg[k] + aq);
-                dp[k] = d[k];
+                const double dpk = m == 1 ? 0.0 : sd[nxt + base + k] * hh;
+                const double next = onepb * d[k] - beta * dpk - cmm * (gg[k] + aq);
                 d[k] = next;
                 if (k < len) sd[nxt + base + k] = next * inv_h;
                 vs = vk;
@@ -864,6 +867,7 @@ static int launch_lat(const LatArgs& a, int grid, cudaStream_t st) {
 int launch_lattice_substeps(const LatArgs& a, int grid, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (a.threads == 1024 && a.strip_k == 4) return launch_lat<1024, 4, 1>(a, grid, st);
+    if (a.threads == 768 && a.strip_k == 6) return launch_lat<768, 6, 2>(a, grid, st);
     if (a.threads == 512 && a.strip_k == 8) return launch_lat<512, 8, 2>(a, grid, st);
     return static_cast<int>(cudaErrorInvalidValue);
 }

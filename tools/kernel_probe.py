@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--square", type=int, nargs=2, metavar=("N_COARSE", "RATIO"),
                     help="custom refined-square mesh (LTS with p = RATIO, dt = 0.2 h)")
     ap.add_argument("--steps", type=int, default=0, help="limit the horizon to this many global steps")
+    ap.add_argument("--nocheck", action="store_true", help="device-resident results, no instability check")
+    ap.add_argument("--profile", action="store_true", help="per-kernel CUDA-event times of the last repeat")
     a = ap.parse_args()
     d = configs.config1()[a.level]
     if a.square:
@@ -30,11 +32,24 @@ def main():
     if a.generic:
         m = wavemc.Mesh.from_arrays(*m.arrays())
     lv = wavemc.Level(m, configs.level_spec(d))
+    if a.nocheck:
+        import torch
+        dq_t = torch.empty(a.count, dtype=torch.float64, device="cuda")
+        qf_t = torch.empty(a.count, dtype=torch.float64, device="cuda")
     for r in range(a.repeat):
+        if a.profile and r == a.repeat - 1:
+            wavemc.profile_enable(lv, True)
         t0 = time.perf_counter()
-        _, q, _ = wavemc.eval_pairs(lv, None, 0, a.level, 0, a.count)
+        if a.nocheck:
+            wavemc.eval_pairs_device(lv, None, 0, a.level, 0, a.count, dq_t.data_ptr(), qf_t.data_ptr())
+            wavemc.synchronize(lv)
+            q = qf_t.cpu().numpy()
+        else:
+            _, q, _ = wavemc.eval_pairs(lv, None, 0, a.level, 0, a.count)
         dt = time.perf_counter() - t0
         upd = a.count * lv.info["dof_updates_per_solve"]
+        if a.profile and r == a.repeat - 1:
+            print("profile", wavemc.profile_read(lv))
         print(f"level {a.level} path={lv.info['substep_path']} n={lv.info['n']} n_r={lv.info['n_r']} "
               f"{a.count} solves {dt:.3f} s "
               f"{upd / dt:.3e} DOF-updates/s q0={q[0]:.12e}")
