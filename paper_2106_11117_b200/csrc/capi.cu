@@ -137,7 +137,9 @@ struct wmc_level {
     double* d_gen_rs = nullptr;
     int* d_gen_soff = nullptr;
     std::uint16_t* d_gen_col = nullptr;
-    int* d_slot_rc = nullptr;
+    int* d_slot_rc = nullptr;  // lattice kernel: overflow start offsets
+    std::uint16_t* d_ovf_cell = nullptr;
+    int n_ovf = 0, n_ovf_terms = 0;
     double* d_slot_a0 = nullptr;
     std::uint16_t* d_slot_cell = nullptr;
     int* d_grc_cell = nullptr;
@@ -172,7 +174,7 @@ struct wmc_level {
                         (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
-                        (void*)d_slot_cell, (void*)d_grc_cell,
+                        (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
                         (void*)d_grc_a0, (void*)d_kl, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
             if (p) cudaFree(p);
         for (auto& w : ws)
@@ -306,9 +308,9 @@ void build_device_level(wmc_level& L) {
             grows[q] = t.gen_rows[ord[q]];
             grs[q] = t.gen_rs[ord[q]];
         }
-        std::vector<int> soff(n_slices + 1, 0), slot_rc{0}, rc_cell;
-        std::vector<std::uint16_t> gcol;
-        std::vector<double> rc_a0, slot_a0;
+        std::vector<int> soff(n_slices + 1, 0), ovf_start{0};
+        std::vector<std::uint16_t> gcol, ovf_cell;
+        std::vector<double> ovf_a0, slot_a0;
         std::vector<std::uint16_t> slot_cell;
         for (int sl = 0; sl < n_slices; ++sl) {
             int width = fixed_width ? wmc::kLatGenWidth : 0;
@@ -330,17 +332,17 @@ void build_device_level(wmc_level& L) {
                             a1 = t.gen_rc_a0[t.gen_rc_ptr[ent]];
                             k1 = static_cast<std::uint16_t>(t.gen_rc_cell[t.gen_rc_ptr[ent]]);
                         } else {
-                            k1 = wmc::kMultiCell;
+                            k1 = static_cast<std::uint16_t>(wmc::kOvfFlag | (ovf_start.size() - 1));
                             for (int k = t.gen_rc_ptr[ent]; k < t.gen_rc_ptr[ent + 1]; ++k) {
-                                rc_cell.push_back(t.gen_rc_cell[k]);
-                                rc_a0.push_back(t.gen_rc_a0[k]);
+                                ovf_cell.push_back(static_cast<std::uint16_t>(t.gen_rc_cell[k]));
+                                ovf_a0.push_back(t.gen_rc_a0[k]);
                             }
+                            ovf_start.push_back(static_cast<int>(ovf_cell.size()));
                         }
                     }
                     gcol.push_back(c);
                     slot_a0.push_back(a1);
                     slot_cell.push_back(k1);
-                    slot_rc.push_back(static_cast<int>(rc_cell.size()));
                 }
             soff[sl + 1] = static_cast<int>(gcol.size());
         }
@@ -374,11 +376,13 @@ void build_device_level(wmc_level& L) {
         L.d_gen_rs = upload(grs);
         L.d_gen_soff = upload(soff);
         L.d_gen_col = upload(gcol);
-        L.d_slot_rc = upload(slot_rc);
+        L.d_slot_rc = upload(ovf_start);
         L.d_slot_a0 = upload(slot_a0);
         L.d_slot_cell = upload(slot_cell);
-        L.d_grc_cell = upload(rc_cell);
-        L.d_grc_a0 = upload(rc_a0);
+        L.n_ovf = static_cast<int>(ovf_start.size()) - 1;
+        L.n_ovf_terms = static_cast<int>(ovf_cell.size());
+        L.d_ovf_cell = upload(ovf_cell);
+        L.d_grc_a0 = upload(ovf_a0);
         wmc::LatArgs probe{};
         probe.threads = t.lat_threads;
         probe.strip_k = t.lat_k;
@@ -389,6 +393,8 @@ void build_device_level(wmc_level& L) {
         probe.n_strips = static_cast<int>(t.strip_j0.size());
         probe.n_gen = n_gen;
         probe.n_slots = L.n_slots;
+        probe.n_ovf = L.n_ovf;
+        probe.n_ovf_terms = L.n_ovf_terms;
         L.lat_smem = wmc::lattice_smem_bytes(probe);
         L.lat_grid = wmc::substep_max_grid(L.device, L.lat_smem);
         L.lattice = L.lat_grid > 0;
@@ -491,11 +497,13 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         la.gen_rs = L.d_gen_rs;
         la.gen_soff = L.d_gen_soff;
         la.gen_col = L.d_gen_col;
-        la.slot_rc = L.d_slot_rc;
+        la.ovf_start = L.d_slot_rc;
+        la.ovf_cell = L.d_ovf_cell;
+        la.ovf_a0 = L.d_grc_a0;
+        la.n_ovf = L.n_ovf;
+        la.n_ovf_terms = L.n_ovf_terms;
         la.slot_a0 = L.d_slot_a0;
         la.slot_cell = L.d_slot_cell;
-        la.rc_cell = L.d_grc_cell;
-        la.rc_a0 = L.d_grc_a0;
         la.cells = cells;
         la.gd = ws.g;
         la.g_stride = g_stride(t);

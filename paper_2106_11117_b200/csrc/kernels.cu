@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
 // address): v0 | v1 | gw | sa0 | cl | beta | cm | then 8-byte aligned int
 // and byte tables.
 struct LatOff {
-    int v0, v1, gw, sa0, cl, beta, cm, gcol, scell, sj0, slen, cx, cy, total;
+    int v0, v1, gw, sa0, cl, beta, cm, oa0, gcol, scell, ostart, ocell, sj0, slen, cx, cy, total;
 };
 
 __host__ __device__ inline LatOff lat_offsets(const LatArgs& a) {
@@ -500,8 +500,11 @@ __host__ __device__ inline LatOff lat_offsets(const LatArgs& a) {
     o.cl = take(a.n_cells);
     o.beta = take(a.p > 1 ? a.p - 1 : 1);
     o.cm = take(a.p > 1 ? a.p - 1 : 1);
+    o.oa0 = take(a.n_ovf_terms > 0 ? a.n_ovf_terms : 1);
     o.gcol = take((slots * 2 + 7) / 8);  // uint16
     o.scell = take((slots * 2 + 7) / 8);  // uint16
+    o.ostart = take((a.n_ovf + 1 + 1) / 2);  // int
+    o.ocell = take((a.n_ovf_terms * 2 + 7) / 8);  // uint16
     o.sj0 = take((a.n_strips + 1) / 2);  // int
     o.slen = take((a.n_strips + 1) / 2);
     o.cx = take((a.m + 1) / 2);
@@ -530,6 +533,8 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
     const LatOff o = lat_offsets(a);
     std::uint16_t* gcol = reinterpret_cast<std::uint16_t*>(sd + o.gcol);
     std::uint16_t* scell = reinterpret_cast<std::uint16_t*>(sd + o.scell);
+    int* ostart = reinterpret_cast<int*>(sd + o.ostart);
+    std::uint16_t* ocell = reinterpret_cast<std::uint16_t*>(sd + o.ocell);
     int* sj0 = reinterpret_cast<int*>(sd + o.sj0);
     int* slen = reinterpret_cast<int*>(sd + o.slen);
     int* cx = reinterpret_cast<int*>(sd + o.cx);
@@ -547,6 +552,11 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
         gcol[i] = __ldg(a.gen_col + i);
         scell[i] = __ldg(a.slot_cell + i);
         sd[o.sa0 + i] = __ldg(a.slot_a0 + i);
+    }
+    for (int i = tid; i <= a.n_ovf; i += T) ostart[i] = __ldg(a.ovf_start + i);
+    for (int i = tid; i < a.n_ovf_terms; i += T) {
+        ocell[i] = __ldg(a.ovf_cell + i);
+        sd[o.oa0 + i] = __ldg(a.ovf_a0 + i);
     }
     for (int i = tid; i < a.n_strips; i += T) {
         sj0[i] = __ldg(a.strip_j0 + i);
@@ -600,14 +610,14 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
 #pragma unroll
         for (int u = 0; u < G; ++u) ggg[u] = grow[u] >= 0 ? sd[o.v1 + grow[u]] : 0.0;
         for (int e = tid; e < a.n_slots; e += T) {
-            const int c = scell[e];
+            const unsigned c = scell[e];
             double w;
-            if (c != kMultiCell) {
+            if (!(c & kOvfFlag)) {
                 w = sd[o.cl + c] * sd[o.sa0 + e];
             } else {  // several cells share this entry (edge on a coefficient line)
+                const int k = c & ~kOvfFlag;
                 w = 0.0;
-                for (int t = __ldg(a.slot_rc + e); t < __ldg(a.slot_rc + e + 1); ++t)
-                    w += sd[o.cl + __ldg(a.rc_cell + t)] * __ldg(a.rc_a0 + t);
+                for (int t = ostart[k]; t < ostart[k + 1]; ++t) w += sd[o.cl + ocell[t]] * sd[o.oa0 + t];
             }
             sd[o.gw + e] = w;
         }

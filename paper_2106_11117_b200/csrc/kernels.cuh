@@ -20,7 +20,8 @@ namespace wmc {
 constexpr int kColBits = 23;
 constexpr int kColMask = (1 << kColBits) - 1;
 constexpr int kMaxCells = 511;
-constexpr unsigned kMultiCell = 0xffffu;  // slot weight with several cells
+constexpr unsigned kMultiCell = 0xffffu;  // slot weight with several cells (on-chip generic kernel)
+constexpr unsigned kOvfFlag = 0x8000u;    // lattice kernel: slot weight in the overflow list
 
 constexpr int kSweepChunk = 64;  // samples per warp in the sweep (2 per lane)
 constexpr int kSweepWarps = 8;   // rows per sweep block
@@ -88,10 +89,11 @@ struct LatArgs {
     const int* gen_soff;         // slot offset of each 32-row slice (rows sorted by length), n_slices + 1
     const std::uint16_t* gen_col;  // per slot: [slice][width][32], padding: col 0, weight 0
     const double* slot_a0;       // per slot: a0 of the single term
-    const std::uint16_t* slot_cell;  // per slot: its cell, kMultiCell when the weight has several terms
-    const int* slot_rc;          // per slot: term range [slot_rc[e], slot_rc[e+1]) (several terms)
-    const int* rc_cell;
-    const double* rc_a0;
+    const std::uint16_t* slot_cell;  // per slot: its cell, or kOvfFlag | k: terms ovf_start[k] .. ovf_start[k+1]
+    int n_ovf, n_ovf_terms;          // slots whose weight spans several cells (edge on a coefficient line)
+    const int* ovf_start;
+    const std::uint16_t* ovf_cell;
+    const double* ovf_a0;
     const double* cells;
     double* gd;                  // [s][g_stride]: g in, d_p out
     int g_stride;

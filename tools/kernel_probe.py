@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--steps", type=int, default=0, help="limit the horizon to this many global steps")
     ap.add_argument("--nocheck", action="store_true", help="device-resident results, no instability check")
     ap.add_argument("--profile", action="store_true", help="per-kernel CUDA-event times of the last repeat")
+    ap.add_argument("--p", type=int, default=0, help="override the number of substeps (timing studies)")
     a = ap.parse_args()
     d = configs.config1()[a.level]
     if a.square:
@@ -28,6 +29,8 @@ def main():
         d = configs.LevelDef(nc, r, 0.2 / nc, r, d.integrator)
     if a.steps:
         d = configs.LevelDef(d.n_coarse, d.ratio, d.dt, d.substeps, d.integrator, final_time=a.steps * d.dt)
+    if a.p:
+        d = configs.LevelDef(d.n_coarse, d.ratio, d.dt, a.p, d.integrator, final_time=d.final_time)
     m = configs.build_mesh(d)
     if a.generic:
         m = wavemc.Mesh.from_arrays(*m.arrays())
