@@ -68,6 +68,20 @@ typedef struct {
 } wmc_square_mesh_spec;
 
 int wmc_mesh_build_square(const wmc_square_mesh_spec* spec, wmc_mesh** out);
+
+/* Graded L-shape [-1,1]^2 minus [0,1]x[-1,0] (BASELINE config 2; no
+ * reference counterpart -- the reference L-shape, src/mesh_graded.cpp:48-112,
+ * carries no fine flags): balanced quadtree at h = 1/n_per_unit, leaves split
+ * while side > h sqrt(r / grade_radius) (r = distance to the corner (0,0)),
+ * down to h / 2^tiers.  Triangle flag = refinement tier plus one adjacent
+ * layer per tier; P_k = vertices of triangles with flag >= k. */
+typedef struct {
+    int n_per_unit;      /* h = 1 / n_per_unit */
+    int tiers;           /* 0..6 */
+    double grade_radius; /* 0.25 */
+} wmc_lshape_mesh_spec;
+
+int wmc_mesh_build_lshape(const wmc_lshape_mesh_spec* spec, wmc_mesh** out);
 /* A mesh from arrays, e.g. a reference TriMesh (include/wavemc/mesh.hpp:48-74). */
 int wmc_mesh_create(int n_vertices, int n_triangles, const double* xy, const int* tri, const unsigned char* fine,
                     const unsigned char* boundary, double coarse_h, double fine_h, wmc_mesh** out);
@@ -93,6 +107,10 @@ typedef struct {
     double kl_sigma;             /* KL: standard deviation of g */
     double kl_corr_len;          /* KL: correlation length of exp(-|dx|/l - |dy|/l) */
     int kl_modes;                /* KL: number of terms, xi_m ~ N(0,1) by Box-Muller over next_unit pairs */
+    int tiers;                   /* nested LTS tiers (0 or 1: single-tier LF-LTS); tier k substeps with
+                                    p per tier on P_k = vertices of triangles with flag >= k */
+    double domain[4];            /* x0, x1, y0, y1 of the coefficient grid (all 0: unit square) */
+    int qoi_mean;                /* 1: Q = mean of u(T) over the box (weights / their sum) */
 } wmc_level_desc;
 
 void wmc_level_desc_default(wmc_level_desc* desc);
@@ -108,9 +126,12 @@ typedef struct {
     long ap_nnz;              /* A P entries on R */
     long n_recipes;
     int batch;                /* samples per device batch */
-    double dof_updates_per_solve;  /* n + (n_steps-1)(n + (p-1)|R|) for LTS, n_steps*n for LF */
+    double dof_updates_per_solve;  /* n + (n_steps-1)(n + sum_k (p^k - p^(k-1))|R_k|) for LTS, n_steps*n for LF */
     int lattice;              /* 1: substeps use the structured refined-square kernel */
-    int substep_path;         /* 0 none (LF or p = 1), 1 lattice, 2 generic on-chip, 3 HBM-resident; -1 plan only */
+    int substep_path;         /* 0 none (LF or p = 1), 1 lattice, 2 generic on-chip, 3 HBM-resident,
+                                 4 HBM-resident nested tiers; -1 plan only */
+    int tiers;                /* nested LTS tiers in use */
+    int n_r_tier[8];          /* |R_k| for tiers k = 1..tiers (n_r_tier[0] == n_r), rows [0, |R_k|) */
 } wmc_level_info;
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);

@@ -1,6 +1,6 @@
 """Generate tests/golden/*.json from the UNMODIFIED reference library
 (oracle/_ref/wavemc_ref_driver) -- run in the build container, where
-/root/reference exists:  python oracle/make_golden.py
+/root/reference exists:  python oracle/make_golden.py [--only-config2]
 
 The meshes come from the shared problem definition (the product's host mesh
 builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
@@ -34,10 +34,48 @@ def dump(name, obj):
         f.write("\n")
 
 
+def config2_reductions(ref, tmp):
+    """Config 2 (graded L-shape, nested tiers) has no reference counterpart;
+    the reference pins its geometry, boundary, coefficient grid, IC and QoI
+    through the two reductions it can run on the same mesh: single-tier LF-LTS
+    with P = P_1 and p = 2^3 (stable at the finest tier), and global
+    leap-frog at dt / 8."""
+    c = configs.CONFIG2_PROBLEM
+    args = {"cells-x": c["cells"][0], "cells-y": c["cells"][1], "ic": ",".join(map(repr, c["ic"])),
+            "box": ",".join(map(repr, c["qoi_box"])), "domain": ",".join(map(repr, c["domain"])), "qoi-mean": 1,
+            "T": 2.0}
+    out = {"problem": {k: list(v) for k, v in c.items()}, "levels": []}
+    meshes = {}
+    for l, d in enumerate(configs.config2(3)):
+        m = configs.build_mesh(d)
+        path = os.path.join(tmp, f"config2_l{l}.mesh")
+        m.dump(path)
+        meshes[f"config2_l{l}"] = {"n_per_unit": d.n_coarse, "tiers": d.tiers, **ref.meshcheck(path)}
+        if l > 0:
+            continue
+        p_fine = 2 ** d.tiers
+        hdr, q = ref.solve(path, d.dt, p_fine, "lts", 0, 0, 8, **args)
+        hdr_lf, q_lf = ref.solve(path, d.dt / p_fine, 1, "lf", 0, 0, 4, **args)
+        hdr_nu0, q_nu0 = ref.solve(path, d.dt, p_fine, "lts", 1, 77, 4, nu=0.0, **args)
+        out["levels"].append({
+            "level": l, "n_per_unit": d.n_coarse, "dt": d.dt,
+            "lts_single_tier": {"p": p_fine, "nu": 0.01, "stream_level": 0, "first": 0, "header": hdr,
+                                "q": q.tolist()},
+            "lts_single_tier_nu0": {"p": p_fine, "nu": 0.0, "stream_level": 1, "first": 77, "header": hdr_nu0,
+                                    "q": q_nu0.tolist()},
+            "lf": {"dt": d.dt / p_fine, "stream_level": 0, "first": 0, "header": hdr_lf, "q": q_lf.tolist()},
+        })
+    out["meshes"] = meshes
+    dump("config2_reductions.json", out)
+
+
 def main():
     build()
     ref = RefDriver()
     tmp = tempfile.mkdtemp(prefix="wmc_golden_")
+    if "--only-config2" in sys.argv:
+        config2_reductions(ref, tmp)
+        return
 
     # RNG words and uniform draws (rng.hpp:14-19, rng.cpp:14-32)
     streams = [(0, 0, 0), (0, 1, 7), (12345, 3, 987654321), (2**63 + 5, 4, 2**40 + 3)]
@@ -124,6 +162,7 @@ def main():
     kl_adaptive["eps"] = configs.CONFIG4_EPS
     kl_adaptive["model_cost"] = adaptive["model_cost"]
     dump("config4_adaptive.json", kl_adaptive)
+    config2_reductions(ref, tmp)
     print("golden fixtures written to", GOLDEN)
 
 

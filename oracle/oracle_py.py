@@ -31,7 +31,8 @@ class OProblem(C.Structure):
     _fields_ = [("cells_x", C.c_int), ("cells_y", C.c_int), ("coef_lo", C.c_double), ("coef_hi", C.c_double),
                 ("final_time", C.c_double), ("dt", C.c_double), ("substeps", C.c_int), ("nu", C.c_double),
                 ("kind", C.c_int), ("ic_x", C.c_double), ("ic_y", C.c_double), ("ic_w2", C.c_double),
-                ("box", C.c_double * 4), ("kl_table", C.POINTER(C.c_double)), ("kl_modes", C.c_int)]
+                ("box", C.c_double * 4), ("kl_table", C.POINTER(C.c_double)), ("kl_modes", C.c_int),
+                ("tiers", C.c_int), ("domain", C.c_double * 4), ("qoi_mean", C.c_int)]
 
 
 def build(force: bool = False) -> None:
@@ -58,7 +59,8 @@ class MeshArrays:
 
 
 def problem(dt, substeps=1, kind=1, final_time=1.0, nu=0.01, cells=(4, 4), coef=(0.5, 1.5),
-            ic=(0.3, 0.5, 0.01), box=(0.7, 0.9, 0.4, 0.6), kl_table=None) -> OProblem:
+            ic=(0.3, 0.5, 0.01), box=(0.7, 0.9, 0.4, 0.6), kl_table=None, tiers=1, domain=None,
+            qoi_mean=False) -> OProblem:
     """kl_table: None (uniform cells) or a contiguous float64 array [cell][mode]
     (kept alive by the returned struct)."""
     p = OProblem()
@@ -73,6 +75,11 @@ def problem(dt, substeps=1, kind=1, final_time=1.0, nu=0.01, cells=(4, 4), coef=
     p.ic_x, p.ic_y, p.ic_w2 = ic
     for i, v in enumerate(box):
         p.box[i] = v
+    p.tiers = tiers
+    if domain is not None:
+        for i, v in enumerate(domain):
+            p.domain[i] = v
+    p.qoi_mean = 1 if qoi_mean else 0
     return p
 
 
@@ -97,6 +104,8 @@ class COracle:
                                             C.POINTER(OProblem), C.c_uint64, C.c_uint32, C.c_uint64, C.c_long,
                                             C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_long),
                                             C.POINTER(C.c_long)]
+        L.wmc_oracle_steps.argtypes = [C.POINTER(OMesh), C.POINTER(OProblem), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_long]
         L.wmc_oracle_moments.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_long,
                                          C.POINTER(C.c_double)]
         L.wmc_oracle_level_data.argtypes = [C.POINTER(OMesh), C.POINTER(OProblem), C.POINTER(C.c_double),
@@ -136,6 +145,16 @@ class COracle:
         rc = self.lib.wmc_oracle_solve(C.byref(mesh.c), C.byref(pb), cells.ctypes.data_as(C.POINTER(C.c_double)),
                                        C.byref(q), C.byref(step), cnt)
         return rc, q.value, step.value, list(cnt)
+
+    def steps(self, mesh: MeshArrays, pb: OProblem, cells, z_prev, z_curr, n_steps):
+        """Advance a consistent pair (z_prev, z_curr) by n_steps (no start-up step)."""
+        cells = np.ascontiguousarray(cells, np.float64)
+        zp = np.array(z_prev, np.float64)
+        zc = np.array(z_curr, np.float64)
+        rc = self.lib.wmc_oracle_steps(C.byref(mesh.c), C.byref(pb), cells.ctypes.data_as(C.POINTER(C.c_double)),
+                                       zp.ctypes.data_as(C.POINTER(C.c_double)),
+                                       zc.ctypes.data_as(C.POINTER(C.c_double)), n_steps)
+        return rc, zp, zc
 
     def eval_pairs(self, fine: MeshArrays, pf: OProblem, coarse: MeshArrays | None, pc: OProblem | None, seed,
                    level, first, count):

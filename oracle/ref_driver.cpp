@@ -90,7 +90,17 @@ struct ProblemDef {
     double box_x0 = 0.7, box_x1 = 0.9, box_y0 = 0.4, box_y1 = 0.6;
     std::vector<double> kl;  // log-normal KL table [cell * kl_modes + m] (empty: uniform cells)
     int kl_modes = 0;
+    double dom_x0 = 0.0, dom_x1 = 1.0, dom_y0 = 0.0, dom_y1 = 1.0;  // coefficient grid extent
+    bool qoi_mean = false;   // Q = mean over the box
 };
+
+std::vector<double> num_list(const std::string& s) {
+    std::vector<double> out;
+    std::stringstream ss(s);
+    std::string part;
+    while (std::getline(ss, part, ',')) out.push_back(std::strtod(part.c_str(), nullptr));
+    return out;
+}
 
 ProblemDef problem_from(const Args& a) {
     ProblemDef d;
@@ -101,6 +111,22 @@ ProblemDef problem_from(const Args& a) {
     d.final_time = a.num("T", 1.0);
     d.nu = a.num("nu", 0.01);
     d.kind = a.get("kind", "lts") == "lf" ? Integrator::Leapfrog : Integrator::LocalTimeStepping;
+    if (!a.get("ic").empty()) {  // x,y,width2
+        const auto v = num_list(a.get("ic"));
+        if (v.size() != 3) throw ConfigError("--ic x,y,width2");
+        d.ic_x = v[0], d.ic_y = v[1], d.ic_w2 = v[2];
+    }
+    if (!a.get("box").empty()) {  // x0,x1,y0,y1
+        const auto v = num_list(a.get("box"));
+        if (v.size() != 4) throw ConfigError("--box x0,x1,y0,y1");
+        d.box_x0 = v[0], d.box_x1 = v[1], d.box_y0 = v[2], d.box_y1 = v[3];
+    }
+    if (!a.get("domain").empty()) {  // coefficient grid x0,x1,y0,y1
+        const auto v = num_list(a.get("domain"));
+        if (v.size() != 4) throw ConfigError("--domain x0,x1,y0,y1");
+        d.dom_x0 = v[0], d.dom_x1 = v[1], d.dom_y0 = v[2], d.dom_y1 = v[3];
+    }
+    d.qoi_mean = a.integer("qoi-mean", 0) != 0;
     const std::string kl = a.get("kl-table");
     if (!kl.empty()) {  // "<cells> <modes>" then cells*modes values (written by the shared problem definition)
         std::ifstream in(kl);
@@ -131,17 +157,23 @@ TriMesh load_mesh(const std::string& path) {
     std::ifstream in(path);
     if (!in) throw ConfigError("cannot open mesh " + path);
     TriMesh m = load_trimesh(in);
+    // Dirichlet boundary: vertices of the edges that belong to one triangle
+    // (on the unit square these are exactly the vertices with x or y in {0, 1})
+    std::map<std::pair<int, int>, int> edges;
+    for (const auto& t : m.triangles)
+        for (int e = 0; e < 3; ++e) {
+            const int a = t[e], b = t[(e + 1) % 3];
+            ++edges[{std::min(a, b), std::max(a, b)}];
+        }
     m.boundary_vertex.assign(m.n_vertices(), 0);
-    for (int v = 0; v < m.n_vertices(); ++v) {
-        const double x = m.vertices[v][0], y = m.vertices[v][1];
-        if (x == 0.0 || y == 0.0 || x == 1.0 || y == 1.0) m.boundary_vertex[v] = 1;
-    }
+    for (const auto& [e, count] : edges)
+        if (count == 1) m.boundary_vertex[e.first] = m.boundary_vertex[e.second] = 1;
     return m;
 }
 
 int cell_of(const ProblemDef& d, double x, double y) {
-    int ix = static_cast<int>(std::floor(x * d.cells_x));
-    int iy = static_cast<int>(std::floor(y * d.cells_y));
+    int ix = static_cast<int>(std::floor((x - d.dom_x0) / (d.dom_x1 - d.dom_x0) * d.cells_x));
+    int iy = static_cast<int>(std::floor((y - d.dom_y0) / (d.dom_y1 - d.dom_y0) * d.cells_y));
     ix = std::clamp(ix, 0, d.cells_x - 1);
     iy = std::clamp(iy, 0, d.cells_y - 1);
     return iy * d.cells_x + ix;
@@ -200,8 +232,10 @@ Level make_level(const ProblemDef& d, const std::string& mesh_path, double dt, i
         const double area = lv.mesh.signed_area(t);
         for (int v : lv.mesh.triangles[t]) w[v] += area / 3.0;
     }
+    double total = 0.0;
+    for (double v : w) total += v;
     lv.qoi_w.resize(n);
-    for (int i = 0; i < n; ++i) lv.qoi_w[i] = w[lv.interior[i]];
+    for (int i = 0; i < n; ++i) lv.qoi_w[i] = d.qoi_mean ? w[lv.interior[i]] / total : w[lv.interior[i]];
     const DiscreteOperator op = interior_operator(lv, full);
     // |R| = rows of A P holding a nonzero value (explicit zeros do not couple)
     for (int r = 0; r < op.a_fine.rows(); ++r)

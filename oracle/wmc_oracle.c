@@ -177,11 +177,16 @@ typedef struct {
     int* dof_vertex;
     double* mass;         /* lumped mass per dof */
     unsigned char* sel;   /* selector per dof */
+    unsigned char* vt;    /* nested tiers: largest flag (capped at tiers) of the dof's triangles */
     csr a, a_fine, a_coarse;
 } oper;
 
+/* cell k = iy * cells_x + ix, ix = floor((x - x0) / (x1 - x0) * cells_x) over the domain box */
 static int cell_of(const wmc_oracle_problem* pb, double x, double y) {
-    int ix = (int)floor(x * pb->cells_x), iy = (int)floor(y * pb->cells_y);
+    const int unit = pb->domain[0] == 0.0 && pb->domain[1] == 0.0 && pb->domain[2] == 0.0 && pb->domain[3] == 0.0;
+    const double x0 = unit ? 0.0 : pb->domain[0], x1 = unit ? 1.0 : pb->domain[1];
+    const double y0 = unit ? 0.0 : pb->domain[2], y1 = unit ? 1.0 : pb->domain[3];
+    int ix = (int)floor((x - x0) / (x1 - x0) * pb->cells_x), iy = (int)floor((y - y0) / (y1 - y0) * pb->cells_y);
     if (ix < 0) ix = 0;
     if (ix > pb->cells_x - 1) ix = pb->cells_x - 1;
     if (iy < 0) iy = 0;
@@ -247,15 +252,22 @@ static int build_operator(const wmc_oracle_mesh* m, const wmc_oracle_problem* pb
     op->dof_vertex = (int*)malloc(sizeof(int) * (size_t)(n ? n : 1));
     op->mass = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
     op->sel = (unsigned char*)calloc((size_t)(n ? n : 1), 1);
+    op->vt = (unsigned char*)calloc((size_t)(n ? n : 1), 1);
     for (int v = 0; v < nv; ++v)
         if (dof[v] >= 0) {
             op->dof_vertex[dof[v]] = v;
             op->mass[dof[v]] = vmass[v];
         }
+    const int tiers = pb->tiers > 1 ? pb->tiers : 1;
     for (int e = 0; e < nt; ++e)
         if (m->fine[e])
-            for (int i = 0; i < 3; ++i)
-                if (dof[m->tri[3 * e + i]] >= 0) op->sel[dof[m->tri[3 * e + i]]] = 1;
+            for (int i = 0; i < 3; ++i) {
+                const int d = dof[m->tri[3 * e + i]];
+                if (d < 0) continue;
+                const int f = m->fine[e] < tiers ? m->fine[e] : tiers;
+                op->sel[d] = 1;
+                if (f > op->vt[d]) op->vt[d] = (unsigned char)f;
+            }
     csr k = csr_from_triplets(n, t, ntrip);
     /* normalize: A_ij = K_ij / sqrt(M_i M_j) */
     for (int r = 0; r < n; ++r)
@@ -273,6 +285,7 @@ static void oper_free(oper* op) {
     free(op->dof_vertex);
     free(op->mass);
     free(op->sel);
+    free(op->vt);
     csr_free(&op->a);
     csr_free(&op->a_fine);
     csr_free(&op->a_coarse);
@@ -314,7 +327,9 @@ static void qoi_weights(const wmc_oracle_mesh* m, const wmc_oracle_problem* pb, 
         const double area = tri_area(m, e);
         for (int i = 0; i < 3; ++i) vw[m->tri[3 * e + i]] += area / 3.0;
     }
-    for (int i = 0; i < op->n; ++i) w[i] = vw[op->dof_vertex[i]];
+    double total = 0.0;
+    for (int v = 0; v < m->n_vertices; ++v) total += vw[v];
+    for (int i = 0; i < op->n; ++i) w[i] = pb->qoi_mean ? vw[op->dof_vertex[i]] / total : vw[op->dof_vertex[i]];
     free(vw);
 }
 
@@ -346,6 +361,159 @@ static int finite_ok(const double* z, int n) {
     return 1;
 }
 
+/* integrator state shared by the step functions */
+typedef struct {
+    const oper* op;
+    int n, kind, p, tiers;
+    double dt, delta, omega;
+    double *beta_int, *beta_half;
+    csr* a_tier;      /* nested tiers: A P_k, k = 1..tiers (column masks vt >= k) */
+    double* buf;      /* scratch */
+    long cnt[3];
+} integ;
+
+static void integ_init(integ* g, const oper* op, const wmc_oracle_problem* pb) {
+    memset(g, 0, sizeof(*g));
+    g->op = op;
+    g->n = op->n;
+    g->kind = pb->kind;
+    const long n_steps = (long)ceil(pb->final_time / pb->dt - 1e-12);
+    g->dt = pb->final_time / (double)n_steps;
+    g->p = pb->kind == 1 ? pb->substeps : 1;
+    g->tiers = pb->kind == 1 && pb->tiers > 1 ? pb->tiers : 1;
+    g->delta = 1.0;
+    g->omega = 2.0;
+    g->beta_int = (double*)malloc(sizeof(double) * (size_t)(g->p + 1));
+    g->beta_half = (double*)malloc(sizeof(double) * (size_t)(g->p + 1));
+    if (pb->kind == 1) wmc_oracle_chebyshev(g->p, pb->nu, &g->delta, &g->omega, g->beta_int, g->beta_half);
+    if (g->tiers > 1) {
+        g->a_tier = (csr*)malloc(sizeof(csr) * (size_t)g->tiers);
+        unsigned char* keep = (unsigned char*)malloc((size_t)(g->n ? g->n : 1));
+        for (int k = 1; k <= g->tiers; ++k) {
+            for (int i = 0; i < g->n; ++i) keep[i] = op->vt[i] >= k;
+            g->a_tier[k - 1] = csr_mask(&op->a, keep, 1);
+        }
+        free(keep);
+        /* per tier: rho, rt, E_prev, E_cur, E_next, product */
+        g->buf = (double*)malloc(sizeof(double) * (size_t)(g->n ? g->n : 1) * 6 * (size_t)g->tiers);
+    }
+}
+
+static void integ_free(integ* g) {
+    free(g->beta_int);
+    free(g->beta_half);
+    if (g->a_tier) {
+        for (int k = 0; k < g->tiers; ++k) csr_free(&g->a_tier[k]);
+        free(g->a_tier);
+    }
+    free(g->buf);
+}
+
+/* Nested LTS (BASELINE config 2; no reference counterpart, parity unpinned
+ * by the reference -- pinned by reduction, see tests): tier k advances the
+ * local problem e'' = -(r + A P_k e), e(0) = e'(0) = 0, over its interval
+ * dt_k = dt / p^(k-1) with the reference's stabilised recursion
+ * (src/integrators.cpp:117-157) at step dt_k / p, where the right-hand side
+ * of each stage, rho_m = r + A P_k E_m, is replaced by the effective one of
+ * tier k+1 over the stage: rt = -2 E^(k+1)_p(rho_m) / dt_(k+1)^2.  The
+ * innermost tier uses rho directly.  Returns E^k_p in out. */
+static void tier_solve(integ* g, int k, const double* r, double* out) {
+    const int n = g->n, p = g->p;
+    double* rho = g->buf + (size_t)n * 6 * (size_t)(k - 1);
+    double* rt = rho + n;
+    double* ep = rt + n;
+    double* ec = ep + n;
+    double* en = ec + n;
+    double* prod = en + n;
+    double dt_k = g->dt;
+    for (int j = 1; j < k; ++j) dt_k /= p;
+    const double tau2 = (dt_k / p) * (dt_k / p);
+    const double c0 = 0.5 * tau2 * 2.0 * p * p / (g->omega * g->delta);
+    const double dt_child = dt_k / p;
+    const double back = -2.0 / (dt_child * dt_child);
+    for (int i = 0; i < n; ++i) ep[i] = ec[i] = 0.0;
+    for (int m = 0; m < p; ++m) {
+        if (m > 0) {
+            csr_mul(&g->a_tier[k - 1], ec, prod);
+            g->cnt[1]++;
+            for (int i = 0; i < n; ++i) rho[i] = r[i] + prod[i];
+        } else {
+            for (int i = 0; i < n; ++i) rho[i] = r[i];
+        }
+        if (k < g->tiers) {
+            tier_solve(g, k + 1, rho, rt);
+            for (int i = 0; i < n; ++i) rt[i] = back * rt[i];
+        } else {
+            for (int i = 0; i < n; ++i) rt[i] = rho[i];
+        }
+        if (m == 0) {
+            for (int i = 0; i < n; ++i) en[i] = -c0 * rt[i];
+        } else {
+            const double beta = g->beta_int[m - 1];
+            const double cm = tau2 * 2.0 * p * p / g->omega * g->beta_half[m - 1];
+            for (int i = 0; i < n; ++i) en[i] = (1.0 + beta) * ec[i] - beta * ep[i] - cm * rt[i];
+        }
+        for (int i = 0; i < n; ++i) {
+            ep[i] = ec[i];
+            ec[i] = en[i];
+        }
+    }
+    for (int i = 0; i < n; ++i) out[i] = ec[i];
+}
+
+/* one global step (z_prev, z_curr) -> (z_curr, z_next), scratch of 5 n */
+static void integ_step(integ* g, double* zp, double* zc, double* s) {
+    const int n = g->n, p = g->p;
+    const oper* op = g->op;
+    double *aq = s, *w = s + n, *az = s + 2 * n, *qp = s + 3 * n, *qc = s + 4 * n;
+    if (g->kind == 0) {
+        csr_mul(&op->a, zc, aq);
+        g->cnt[0]++;
+        const double dt2 = g->dt * g->dt;
+        for (int i = 0; i < n; ++i) {
+            const double next = 2.0 * zc[i] - zp[i] - dt2 * aq[i];
+            zp[i] = zc[i];
+            zc[i] = next;
+        }
+    } else if (g->tiers > 1) {
+        csr_mul(&op->a, zc, aq);
+        g->cnt[0]++;
+        tier_solve(g, 1, aq, qc);
+        for (int i = 0; i < n; ++i) {
+            const double next = 2.0 * zc[i] - zp[i] + 2.0 * qc[i];
+            zp[i] = zc[i];
+            zc[i] = next;
+        }
+    } else {
+        const double tau2 = (g->dt / p) * (g->dt / p);
+        csr_mul(&op->a_coarse, zc, w);
+        g->cnt[2]++;
+        csr_mul(&op->a_fine, zc, az);
+        g->cnt[1]++;
+        const double c0 = 0.5 * tau2 * 2.0 * p * p / (g->omega * g->delta);
+        for (int i = 0; i < n; ++i) {
+            qp[i] = 0.0;
+            qc[i] = -c0 * (w[i] + az[i]);
+        }
+        for (int m = 1; m <= p - 1; ++m) {
+            csr_mul(&op->a_fine, qc, aq);
+            g->cnt[1]++;
+            const double beta = g->beta_int[m - 1];
+            const double cm = tau2 * 2.0 * p * p / g->omega * g->beta_half[m - 1];
+            for (int i = 0; i < n; ++i) {
+                const double next = (1.0 + beta) * qc[i] - beta * qp[i] - cm * (w[i] + az[i] + aq[i]);
+                qp[i] = qc[i];
+                qc[i] = next;
+            }
+        }
+        for (int i = 0; i < n; ++i) {
+            const double next = 2.0 * zc[i] - zp[i] + 2.0 * qc[i];
+            zp[i] = zc[i];
+            zc[i] = next;
+        }
+    }
+}
+
 int wmc_oracle_solve(const wmc_oracle_mesh* mesh, const wmc_oracle_problem* pb, const double* cells, double* q,
                      long* fail_step, long* counters) {
     oper op;
@@ -355,72 +523,27 @@ int wmc_oracle_solve(const wmc_oracle_mesh* mesh, const wmc_oracle_problem* pb, 
     double* z0 = (double*)malloc(bytes);
     double* zp = (double*)malloc(bytes);
     double* zc = (double*)malloc(bytes);
-    double* aq = (double*)malloc(bytes);
-    double* w = (double*)malloc(bytes);
-    double* az = (double*)malloc(bytes);
-    double* qp = (double*)malloc(bytes);
-    double* qc = (double*)malloc(bytes);
+    double* scratch = (double*)malloc(bytes * 5);
     double* qw = (double*)malloc(bytes);
-    long cnt[3] = {0, 0, 0};
     int status = 0;
     project_z0(mesh, pb, &op, z0);
     qoi_weights(mesh, pb, &op, qw);
-
+    integ g;
+    integ_init(&g, &op, pb);
     const long n_steps = (long)ceil(pb->final_time / pb->dt - 1e-12);
-    const double dt = pb->final_time / (double)n_steps;
-    const int p = pb->kind == 1 ? pb->substeps : 1;
-    double delta = 1.0, omega = 2.0;
-    double* beta_int = (double*)malloc(sizeof(double) * (size_t)(p + 1));
-    double* beta_half = (double*)malloc(sizeof(double) * (size_t)(p + 1));
-    if (pb->kind == 1) wmc_oracle_chebyshev(p, pb->nu, &delta, &omega, beta_int, beta_half);
+    const double dt = g.dt;
 
     /* leapfrog_init: z1 = z0 + dt M^{1/2} v0 + dt^2/2 (F0 - A z0), v0 = F = 0 */
-    csr_mul(&op.a, z0, aq);
-    cnt[0]++;
+    csr_mul(&op.a, z0, scratch);
+    g.cnt[0]++;
     for (int i = 0; i < n; ++i) {
         zp[i] = z0[i];
-        zc[i] = z0[i] + dt * 0.0 + 0.5 * dt * dt * (0.0 - aq[i]);
+        zc[i] = z0[i] + dt * 0.0 + 0.5 * dt * dt * (0.0 - scratch[i]);
     }
     long step = 1;
     if (!finite_ok(zc, n)) status = 3;
     for (long s = 1; s < n_steps && status == 0; ++s) {
-        if (pb->kind == 0) {
-            csr_mul(&op.a, zc, aq);
-            cnt[0]++;
-            const double dt2 = dt * dt;
-            for (int i = 0; i < n; ++i) {
-                const double next = 2.0 * zc[i] - zp[i] - dt2 * aq[i];
-                zp[i] = zc[i];
-                zc[i] = next;
-            }
-        } else {
-            const double tau2 = (dt / p) * (dt / p);
-            csr_mul(&op.a_coarse, zc, w);
-            cnt[2]++;
-            csr_mul(&op.a_fine, zc, az);
-            cnt[1]++;
-            const double c0 = 0.5 * tau2 * 2.0 * p * p / (omega * delta);
-            for (int i = 0; i < n; ++i) {
-                qp[i] = 0.0;
-                qc[i] = -c0 * (w[i] + az[i]);
-            }
-            for (int m = 1; m <= p - 1; ++m) {
-                csr_mul(&op.a_fine, qc, aq);
-                cnt[1]++;
-                const double beta = beta_int[m - 1];
-                const double cm = tau2 * 2.0 * p * p / omega * beta_half[m - 1];
-                for (int i = 0; i < n; ++i) {
-                    const double next = (1.0 + beta) * qc[i] - beta * qp[i] - cm * (w[i] + az[i] + aq[i]);
-                    qp[i] = qc[i];
-                    qc[i] = next;
-                }
-            }
-            for (int i = 0; i < n; ++i) {
-                const double next = 2.0 * zc[i] - zp[i] + 2.0 * qc[i];
-                zp[i] = zc[i];
-                zc[i] = next;
-            }
-        }
+        integ_step(&g, zp, zc, scratch);
         ++step;
         if (!finite_ok(zc, n)) status = 3;
     }
@@ -433,21 +556,34 @@ int wmc_oracle_solve(const wmc_oracle_mesh* mesh, const wmc_oracle_problem* pb, 
         *fail_step = step;
     }
     if (counters) {
-        counters[0] = cnt[0];
-        counters[1] = cnt[1];
-        counters[2] = cnt[2];
+        counters[0] = g.cnt[0];
+        counters[1] = g.cnt[1];
+        counters[2] = g.cnt[2];
     }
+    integ_free(&g);
     free(z0);
     free(zp);
     free(zc);
-    free(aq);
-    free(w);
-    free(az);
-    free(qp);
-    free(qc);
+    free(scratch);
     free(qw);
-    free(beta_int);
-    free(beta_half);
+    oper_free(&op);
+    return status;
+}
+
+int wmc_oracle_steps(const wmc_oracle_mesh* mesh, const wmc_oracle_problem* pb, const double* cells, double* z_prev,
+                     double* z_curr, long n_steps) {
+    oper op;
+    if (build_operator(mesh, pb, cells, &op) != 0) return 3;
+    double* scratch = (double*)malloc(sizeof(double) * (size_t)(op.n ? op.n : 1) * 5);
+    integ g;
+    integ_init(&g, &op, pb);
+    int status = 0;
+    for (long s = 0; s < n_steps && status == 0; ++s) {
+        integ_step(&g, z_prev, z_curr, scratch);
+        if (!finite_ok(z_curr, op.n)) status = 3;
+    }
+    integ_free(&g);
+    free(scratch);
     oper_free(&op);
     return status;
 }

@@ -32,14 +32,19 @@ class LevelDesc(C.Structure):
                 ("final_time", C.c_double), ("dt", C.c_double), ("substeps", C.c_int), ("nu", C.c_double),
                 ("integrator", C.c_int), ("ic_x", C.c_double), ("ic_y", C.c_double), ("ic_width2", C.c_double),
                 ("qoi_box", C.c_double * 4), ("device", C.c_int), ("batch", C.c_int), ("field", C.c_int),
-                ("kl_sigma", C.c_double), ("kl_corr_len", C.c_double), ("kl_modes", C.c_int)]
+                ("kl_sigma", C.c_double), ("kl_corr_len", C.c_double), ("kl_modes", C.c_int),
+                ("tiers", C.c_int), ("domain", C.c_double * 4), ("qoi_mean", C.c_int)]
+
+
+class LShapeMeshSpec(C.Structure):
+    _fields_ = [("n_per_unit", C.c_int), ("tiers", C.c_int), ("grade_radius", C.c_double)]
 
 
 class LevelInfo(C.Structure):
     _fields_ = [("n", C.c_int), ("n_r", C.c_int), ("n_p", C.c_int), ("p", C.c_int), ("n_steps", C.c_long),
                 ("dt", C.c_double), ("nnz", C.c_long), ("ap_nnz", C.c_long), ("n_recipes", C.c_long),
                 ("batch", C.c_int), ("dof_updates_per_solve", C.c_double), ("lattice", C.c_int),
-                ("substep_path", C.c_int)]
+                ("substep_path", C.c_int), ("tiers", C.c_int), ("n_r_tier", C.c_int * 8)]
 
 
 class Cost(C.Structure):
@@ -76,6 +81,7 @@ _DP = P(C.c_double)
 # (name, restype, argtypes) for every symbol include/wavemc_b200.h declares
 SIGNATURES = [
     ("wmc_mesh_build_square", C.c_int, [P(SquareMeshSpec), P(_VP)]),
+    ("wmc_mesh_build_lshape", C.c_int, [P(LShapeMeshSpec), P(_VP)]),
     ("wmc_mesh_create", C.c_int, [C.c_int, C.c_int, _DP, P(C.c_int), P(C.c_ubyte), P(C.c_ubyte), C.c_double,
                                   C.c_double, P(_VP)]),
     ("wmc_mesh_info", C.c_int, [_VP, P(C.c_int), P(C.c_int), _DP, _DP]),

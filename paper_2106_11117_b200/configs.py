@@ -13,6 +13,16 @@ the GPU path and the oracles:
     p_l = 32, 16, 8, 4, 2, matching the five N_l values;
   * QoI: lumped quadrature of u(T) over the triangles whose centroid lies in
     [0.7, 0.9] x [0.4, 0.6].
+Config 2 (graded L-shape, nested LTS; no reference counterpart):
+  * h_l = 1/16 * 2^-l, l = 0..4 (L = 4 -> five levels, N_l = 32768 halving);
+  * grading toward the re-entrant corner: leaf side s split while
+    s > h sqrt(r / 0.25), three tiers h/2, h/4, h/8 (r < 1/4, 1/16, 1/64),
+    each widened by one element layer; p = 2 per tier, dt = 0.2 h_l, T = 2;
+  * c ~ U[0.5, 1.5) on an 8 x 8 grid over [-1, 1]^2 (row-major, the cells of
+    the missing quadrant are drawn and unused);
+  * u0 = exp(-((x + 0.5)^2 + (y - 0.5)^2) / 0.05^2) ("Gaussian pulse, width
+    0.05", read as the initial condition as in SURVEY.md Appendix A item 8);
+  * Q = mean of u(T) over the triangles with centroid in [0.4, 0.8]^2.
 """
 from __future__ import annotations
 
@@ -34,6 +44,8 @@ class LevelDef:
     substeps: int
     integrator: int
     final_time: float = 1.0
+    shape: str = "square"  # "square" (configs 0, 1, 3, 4) or "lshape" (config 2)
+    tiers: int = 1
 
     @property
     def h(self) -> float:
@@ -62,6 +74,23 @@ def config1(kind: str = "lts", n_levels: int = 5) -> list[LevelDef]:
     return out
 
 
+CONFIG2_COUNTS = [32768, 16384, 8192, 4096, 2048]
+CONFIG2_TIERS = 3
+CONFIG2_GRADE_RADIUS = 0.25
+CONFIG2_PROBLEM = {"cells": (8, 8), "domain": (-1.0, 1.0, -1.0, 1.0), "ic": (-0.5, 0.5, 0.05 ** 2),
+                   "qoi_box": (0.4, 0.8, 0.4, 0.8)}
+
+
+def config2(n_levels: int = 5) -> list[LevelDef]:
+    """Graded L-shape MLMC with nested LTS: 3 tiers, p = 2 per tier."""
+    out = []
+    for l in range(n_levels):
+        n = 16 << l
+        out.append(LevelDef(n, 1 << CONFIG2_TIERS, 0.2 / n, 2, WMC_LOCAL_TIME_STEPPING, final_time=2.0,
+                            shape="lshape", tiers=CONFIG2_TIERS))
+    return out
+
+
 def config3() -> LevelDef:
     """Large batch: h = 1/1024, refined square at h/8, p = 8, T = 0.5."""
     return LevelDef(1024, 8, 0.2 / 1024, 8, WMC_LOCAL_TIME_STEPPING, final_time=0.5)
@@ -85,6 +114,8 @@ CONFIG3_COUNT = 8192
 
 def build_mesh(d: LevelDef):
     from .wavemc import Mesh
+    if d.shape == "lshape":
+        return Mesh.build_lshape(d.n_coarse, d.tiers, CONFIG2_GRADE_RADIUS)
     return Mesh.build_square(d.n_coarse, d.ratio, FINE_LO, FINE_HI, SNAP)
 
 
@@ -96,6 +127,11 @@ def level_spec(d: LevelDef, device: int = 0, batch: int = 0, kl: bool = False):
                          device=device, batch=batch, cells_x=KL_FIELD["cells"][0], cells_y=KL_FIELD["cells"][1],
                          field=WMC_FIELD_LOGNORMAL_KL, kl_sigma=KL_FIELD["sigma"], kl_corr_len=KL_FIELD["corr_len"],
                          kl_modes=KL_FIELD["modes"])
+    if d.shape == "lshape":
+        c = CONFIG2_PROBLEM
+        return LevelSpec(dt=d.dt, substeps=d.substeps, integrator=d.integrator, final_time=d.final_time,
+                         device=device, batch=batch, cells_x=c["cells"][0], cells_y=c["cells"][1], ic=c["ic"],
+                         qoi_box=c["qoi_box"], domain=c["domain"], qoi_mean=True, tiers=d.tiers)
     return LevelSpec(dt=d.dt, substeps=d.substeps, integrator=d.integrator, final_time=d.final_time, device=device,
                      batch=batch)
 

@@ -89,9 +89,11 @@ struct Workspace {
     int* fail = nullptr;
     double* da = nullptr;  // HBM-resident substep path: d buffers [r][S]
     double* db = nullptr;
+    std::vector<double*> tier_e;    // nested tiers: E^k buffers, 2 per tier, [row][S] over R_k
+    std::vector<double*> tier_rhs;  // r_k for k >= 2, [row][S] over R_k
 };
 
-enum class SubPath { None, Lattice, OnChip, Global };
+enum class SubPath { None, Lattice, OnChip, Global, Tiers };
 
 struct wmc_level {
     int device = 0;
@@ -122,6 +124,10 @@ struct wmc_level {
     int* d_apg_ptr = nullptr;
     int* d_apg_ent = nullptr;
     double* d_apg_a0 = nullptr;
+    // nested tiers: A P_k on R_k per tier, substep constants
+    std::vector<int*> d_tier_ptr, d_tier_ent;
+    std::vector<double*> d_tier_a0;
+    double* d_tier_cm = nullptr;
     // QoI
     int* d_qdof = nullptr;
     double* d_qw = nullptr;
@@ -177,9 +183,16 @@ struct wmc_level {
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
                         (void*)d_grc_a0, (void*)d_kl, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
             if (p) cudaFree(p);
-        for (auto& w : ws)
+        for (auto* p : d_tier_ptr) cudaFree(p);
+        for (auto* p : d_tier_ent) cudaFree(p);
+        for (auto* p : d_tier_a0) cudaFree(p);
+        if (d_tier_cm) cudaFree(d_tier_cm);
+        for (auto& w : ws) {
             for (void* p : {(void*)w.za, (void*)w.zb, (void*)w.g, (void*)w.q, (void*)w.fail, (void*)w.da, (void*)w.db})
                 if (p) cudaFree(p);
+            for (auto* p : w.tier_e) cudaFree(p);
+            for (auto* p : w.tier_rhs) cudaFree(p);
+        }
         for (void* p : {(void*)r_dq, (void*)r_qf, (void*)r_ff, (void*)r_fc})
             if (p) cudaFree(p);
         for (void* p : {(void*)h_dq, (void*)h_qf, (void*)h_ff, (void*)h_fc})
@@ -227,14 +240,27 @@ void build_device_level(wmc_level& L) {
     const std::string fp = force_path ? force_path : "";
     L.n_wid = static_cast<int>(t.rc_ptr.size()) - 1;
     const bool onchip_fits = t.n_r <= wmc::kSubThreads * wmc::kSubMaxRpt && t.n_r < 65536 && L.n_wid < 65535;
-    if (lts && (fp == "global" || !onchip_fits)) {
+    if (lts && t.tiers > 1) {
+        // nested tiers: HBM-resident stage kernels
+        if (t.tiers > wmc::kMaxTiers) throw ConfigError("level: too many tiers");
+        L.path = SubPath::Tiers;
+        for (int k = 0; k < t.tiers; ++k) {
+            L.d_tier_ptr.push_back(upload(t.tier_ptr[k]));
+            L.d_tier_ent.push_back(upload(t.tier_ent[k]));
+            L.d_tier_a0.push_back(upload(t.tier_a0[k]));
+        }
+        std::vector<double> cm;
+        for (const auto& v : t.tier_cm) cm.insert(cm.end(), v.begin(), v.end());
+        L.d_tier_cm = upload(cm);
+        L.d_beta = upload(t.beta);
+    } else if (lts && (fp == "global" || !onchip_fits)) {
         if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
         L.path = SubPath::Global;
         L.d_apg_ptr = upload(t.apg_ptr);
         L.d_apg_ent = upload(t.apg_ent);
         L.d_apg_a0 = upload(t.apg_a0);
     }
-    if (lts && L.path != SubPath::Global) {
+    if (lts && L.path != SubPath::Global && L.path != SubPath::Tiers) {
         const int n_slices = (t.n_r + 31) / 32;
         std::vector<int> soff(n_slices + 1, 0);
         std::vector<std::uint32_t> sent;
@@ -287,7 +313,7 @@ void build_device_level(wmc_level& L) {
     int max_gen_width = 0;
     for (std::size_t q = 0; q + 1 < t.gen_ptr.size(); ++q)
         max_gen_width = std::max(max_gen_width, t.gen_ptr[q + 1] - t.gen_ptr[q]);
-    if (lts && L.path != SubPath::Global && t.lattice && static_cast<int>(t.gen_rows.size()) <= 1024 &&
+    if (lts && L.path == SubPath::None && t.lattice && static_cast<int>(t.gen_rows.size()) <= 1024 &&
         max_gen_width <= wmc::kLatGenWidth) {
         // SELL-32 over the generic rows, per slot: column and recipe range
         const int n_gen = static_cast<int>(t.gen_rows.size());
@@ -399,7 +425,7 @@ void build_device_level(wmc_level& L) {
         L.lat_grid = wmc::substep_max_grid(L.device, L.lat_smem);
         L.lattice = L.lat_grid > 0;
     }
-    if (lts && L.path != SubPath::Global) {
+    if (lts && L.path == SubPath::None) {
         L.path = (L.lattice && fp != "onchip") ? SubPath::Lattice : SubPath::OnChip;
         if (L.path == SubPath::OnChip && L.sub_grid <= 0)
             throw ConfigError("level: substep working set exceeds shared memory");
@@ -430,6 +456,16 @@ Workspace& workspace(wmc_level& L, int role) {
             alloc(&w.da, S * t.n_r);
             alloc(&w.db, S * t.n_r);
         }
+        if (L.path == SubPath::Tiers) {
+            w.tier_e.assign(2 * t.tiers, nullptr);
+            w.tier_rhs.assign(t.tiers, nullptr);
+            for (int k = 0; k < t.tiers; ++k) {
+                const std::size_t rows = static_cast<std::size_t>(t.n_r_tier[k]);
+                alloc(&w.tier_e[2 * k], S * rows);
+                alloc(&w.tier_e[2 * k + 1], S * rows);
+                if (k > 0) alloc(&w.tier_rhs[k], S * rows);
+            }
+        }
     }
     return w;
 }
@@ -445,10 +481,61 @@ cudaEvent_t mark(wmc_level& L, std::vector<cudaEvent_t>& v, cudaStream_t st) {
     return e;
 }
 
+// Nested tiers, one global step after the sweep: depth-first over the
+// stage tree, tier k's stage m followed by the whole tier-(k+1) solve that
+// replaces the stage's right-hand side on R_k+1.  At stage 0 the right-hand
+// side of tier k+1 is r_k itself (no product yet), so tier k+1 reads r_k.
+void run_tiers(wmc_level& L, Workspace& ws, const double* cells, int S, int count, const double* zc, double* zp,
+               int step, cudaStream_t stream) {
+    const wmc::LevelTables& t = L.tab;
+    const int K = t.tiers, p = t.p;
+    wmc::TierArgs a{};
+    a.p = p;
+    a.S = S;
+    a.count = count;
+    a.cells = cells;
+    for (int k = 0; k < K; ++k) {
+        a.e[k][0] = ws.tier_e[2 * k];
+        a.e[k][1] = ws.tier_e[2 * k + 1];
+        a.c0[k] = t.tier_c0[k];
+        a.back[k] = t.tier_back[k];
+    }
+    a.beta = L.d_beta;
+    a.cm = L.d_tier_cm;
+    a.zc = zc;
+    a.zp = zp;
+    a.step = step;
+    a.fail = ws.fail;
+    auto run = [&](auto&& self, int k, const double* rhs) -> void {
+        const int n_rk = t.n_r_tier[k - 1];
+        const int split = k < K ? t.n_r_tier[k] : 0;
+        for (int m = 0; m < p; ++m) {
+            a.k = k;
+            a.m = m;
+            a.stage[k - 1] = m;
+            a.rhs = rhs;
+            a.rhs_next = k < K ? ws.tier_rhs[k] : nullptr;
+            a.ptr = L.d_tier_ptr[k - 1];
+            a.ent = L.d_tier_ent[k - 1];
+            a.a0 = L.d_tier_a0[k - 1];
+            a.row_begin = m == 0 ? split : 0;
+            a.row_end = n_rk;
+            a.split = split;
+            if (a.row_end > a.row_begin) {
+                wmc::launch_tier_stage(a, stream);
+                ++g_launches;
+            }
+            if (split > 0) self(self, k + 1, m == 0 ? rhs : ws.tier_rhs[k]);
+        }
+    };
+    run(run, 1, ws.g);
+}
+
 void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
     const wmc::LevelTables& t = L.tab;
     const bool lts = L.path != SubPath::None;
     const bool global = L.path == SubPath::Global;
+    const bool tiers = L.path == SubPath::Tiers;
     wmc::launch_fill_int(ws.fail, INT_MAX, S, stream);
 
     wmc::SweepArgs sw{};
@@ -538,7 +625,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         sw.zc_out = nullptr;
         sw.g = ws.g;
         sw.g_stride = g_stride(t);
-        sw.g_node_major = global ? 1 : 0;
+        sw.g_node_major = (global || tiers) ? 1 : 0;
         sw.split = lts ? t.n_r : 0;
         sw.factor = t.coarse_factor;
         sw.step = static_cast<int>(s + 1);
@@ -546,7 +633,11 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         wmc::launch_sweep_step(sw, stream);
         if (L.profile) mark(L, L.ev_sweep, stream);
         ++g_launches;
-        if (global) {
+        if (tiers) {
+            if (L.profile) mark(L, L.ev_sub, stream);
+            run_tiers(L, ws, cells, S, count, cur, prev, static_cast<int>(s + 1), stream);
+            if (L.profile) mark(L, L.ev_sub, stream);
+        } else if (global) {
             if (L.profile) mark(L, L.ev_sub, stream);
             wmc::GSubArgs ga{};
             ga.n_r = t.n_r;
@@ -635,7 +726,20 @@ void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
 
 void solve_counts(const wmc::LevelTables& t, wmc_cost& c, long solves) {
     const bool lts = t.kind == wmc::Integrator::LocalTimeStepping;
-    if (lts) {
+    if (lts && t.tiers > 1) {
+        // nested tiers: p^k stage products A P_k per step on tier k
+        long fine = 0, work = 0, pk = 1;
+        for (int k = 0; k < t.tiers; ++k) {
+            pk *= t.p;
+            fine += pk;
+            work += pk * static_cast<long>(t.tier_ent[k].size());
+        }
+        c.matvec_full += solves;
+        c.matvec_coarse += solves * (t.n_steps - 1);
+        c.matvec_fine += solves * (t.n_steps - 1) * fine;
+        c.weighted_work += solves * (static_cast<long>(t.col.size()) +
+                                     (t.n_steps - 1) * (static_cast<long>(t.col.size()) + work));
+    } else if (lts) {
         c.matvec_full += solves;
         c.matvec_coarse += solves * (t.n_steps - 1);
         c.matvec_fine += solves * (t.n_steps - 1) * t.p;
@@ -899,6 +1003,17 @@ wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     s.kl_sigma = desc->kl_sigma;
     s.kl_corr_len = desc->kl_corr_len;
     s.kl_modes = desc->kl_modes;
+    s.tiers = desc->tiers > 1 ? desc->tiers : 1;
+    if (desc->tiers < 0 || desc->tiers > wmc::kMaxTiers) throw ConfigError("wmc_level_create: tiers in [0, 8]");
+    if (desc->domain[0] != 0.0 || desc->domain[1] != 0.0 || desc->domain[2] != 0.0 || desc->domain[3] != 0.0) {
+        if (!(desc->domain[1] > desc->domain[0]) || !(desc->domain[3] > desc->domain[2]))
+            throw ConfigError("wmc_level_create: empty coefficient domain");
+        s.dom_x0 = desc->domain[0];
+        s.dom_x1 = desc->domain[1];
+        s.dom_y0 = desc->domain[2];
+        s.dom_y1 = desc->domain[3];
+    }
+    s.qoi_mean = desc->qoi_mean != 0;
     if (s.field == wmc::Field::LognormalKL &&
         (s.kl_modes < 1 || s.kl_modes > wmc::kMaxKLModes || !(s.kl_corr_len > 0.0) || !(s.kl_sigma >= 0.0)))
         throw ConfigError("wmc_level_create: KL field needs 1..64 modes, corr_len > 0, sigma >= 0");
@@ -919,6 +1034,8 @@ void fill_info(const wmc::LevelTables& t, int batch, bool lattice, wmc_level_inf
     info->n_recipes = static_cast<long>(t.rc_ptr.size()) - 1;
     info->batch = batch;
     info->dof_updates_per_solve = wmc::dof_updates_per_solve(t);
+    info->tiers = t.tiers;
+    for (int k = 0; k < 8; ++k) info->n_r_tier[k] = k < static_cast<int>(t.n_r_tier.size()) ? t.n_r_tier[k] : 0;
 }
 }  // namespace
 
@@ -948,6 +1065,19 @@ int wmc_mesh_build_square(const wmc_square_mesh_spec* spec, wmc_mesh** out) {
     });
 }
 
+int wmc_mesh_build_lshape(const wmc_lshape_mesh_spec* spec, wmc_mesh** out) {
+    return guarded([&] {
+        if (!spec || !out) throw ConfigError("wmc_mesh_build_lshape: NULL argument");
+        wmc::LShapeMeshSpec s;
+        s.n_per_unit = spec->n_per_unit;
+        s.tiers = spec->tiers;
+        s.grade_radius = spec->grade_radius;
+        auto m = std::make_unique<wmc_mesh>();
+        m->mesh = wmc::build_graded_lshape(s);
+        *out = m.release();
+    });
+}
+
 int wmc_mesh_create(int n_vertices, int n_triangles, const double* xy, const int* tri, const unsigned char* fine,
                     const unsigned char* boundary, double coarse_h, double fine_h, wmc_mesh** out) {
     return guarded([&] {
@@ -970,7 +1100,7 @@ int wmc_mesh_create(int n_vertices, int n_triangles, const double* xy, const int
                 if (v < 0 || v >= n_vertices) throw ConfigError("wmc_mesh_create: vertex index out of range");
                 M.triangles[t][k] = v;
             }
-            if (fine) M.fine_flags[t] = fine[t] ? 1 : 0;
+            if (fine) M.fine_flags[t] = fine[t];  // tier value (0 coarse, k >= 1: in P_1..P_k)
         }
         *out = m.release();
     });
@@ -1061,8 +1191,11 @@ int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level
             std::size_t free_b = 0, total_b = 0;
             check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
             const auto& t = L->tab;
+            double tier_rows = 0.0;
+            if (t.tiers > 1)
+                for (int k = 0; k < t.tiers; ++k) tier_rows += (k > 0 ? 3.0 : 2.0) * t.n_r_tier[k];
             const double per_sample =
-                2.0 * 8.0 * (2.0 * t.n + g_stride(t) + t.n_cells + 4.0 + 2.0 * t.n_r);
+                2.0 * 8.0 * (2.0 * t.n + g_stride(t) + t.n_cells + 4.0 + 2.0 * t.n_r + tier_rows);
             const long cap = static_cast<long>(0.15 * static_cast<double>(total_b) / per_sample) / 64 * 64;
             L->batch = static_cast<int>(std::max(64L, std::min(4096L, cap)));
         }

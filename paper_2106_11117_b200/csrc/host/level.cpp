@@ -42,15 +42,15 @@ ChebyshevConstants chebyshev_constants(int p, double nu) {
     return c;
 }
 
-namespace {
-
-int cell_of(double x, double y, int nx, int ny) {
-    int ix = static_cast<int>(std::floor(x * nx));
-    int iy = static_cast<int>(std::floor(y * ny));
-    ix = std::clamp(ix, 0, nx - 1);
-    iy = std::clamp(iy, 0, ny - 1);
-    return iy * nx + ix;
+int LevelSpec::cell_col(double x) const {
+    return std::clamp(static_cast<int>(std::floor((x - dom_x0) / (dom_x1 - dom_x0) * cells_x)), 0, cells_x - 1);
 }
+
+int LevelSpec::cell_row(double y) const {
+    return std::clamp(static_cast<int>(std::floor((y - dom_y0) / (dom_y1 - dom_y0) * cells_y)), 0, cells_y - 1);
+}
+
+namespace {
 
 // lattice substep kernel variants: (threads, max rows per thread)
 constexpr int kLatticeVariants[3][2] = {{512, 8}, {768, 6}, {1024, 4}};
@@ -93,8 +93,8 @@ std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const
     std::vector<int> cx(m), cy(m);
     for (int i = 0; i < m; ++i) {
         const double x = (qa + i + 0.5) * h;
-        cx[i] = cell_of(x, 0.5, spec.cells_x, 1);
-        cy[i] = cell_of(0.5, x, 1, spec.cells_y);
+        cx[i] = spec.cell_col(x);
+        cy[i] = spec.cell_row(x);
     }
     // distinct test coefficients per cell
     const int nc = spec.cells_x * spec.cells_y;
@@ -204,7 +204,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         const double area = mesh.signed_area(t);
         if (!(area > 0.0)) throw std::runtime_error("level: nonpositive triangle area");
         const auto cc = mesh.centroid(t);
-        const int k = cell_of(cc[0], cc[1], spec.cells_x, spec.cells_y);
+        const int k = spec.cell_of(cc[0], cc[1]);
         L.elem_cell[t] = k;
         const double gx[3] = {(p1[1] - p2[1]) / (2.0 * area), (p2[1] - p0[1]) / (2.0 * area),
                               (p0[1] - p1[1]) / (2.0 * area)};
@@ -220,42 +220,62 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         }
     }
 
-    // selector: interior vertices of fine-flagged triangles (fem.cpp:119-122)
-    std::vector<std::uint8_t> sel(nv, 0);
+    // selector: interior vertices of fine-flagged triangles (fem.cpp:119-122);
+    // with nested tiers, vertex tier vt = largest flag of its triangles and
+    // P_k = {vt >= k}
+    if (spec.tiers < 1 || spec.tiers > 8) throw std::invalid_argument("level: tiers in [1, 8]");
+    if (spec.tiers > 1 && (spec.kind != Integrator::LocalTimeStepping || spec.substeps < 2))
+        throw std::invalid_argument("level: nested tiers need local time stepping with p >= 2");
+    std::vector<std::uint8_t> sel(nv, 0), vt(nv, 0);
     for (int t = 0; t < nt; ++t)
         if (mesh.fine_flags[t])
             for (int v : mesh.triangles[t])
-                if (!mesh.boundary_vertex[v]) sel[v] = 1;
+                if (!mesh.boundary_vertex[v]) {
+                    sel[v] = 1;
+                    vt[v] = std::max<std::uint8_t>(vt[v], std::min<int>(mesh.fine_flags[t], spec.tiers));
+                }
 
-    // rows of A P with a nonzero: R
-    std::vector<std::uint8_t> in_r(nv, 0);
+    // rows of A P with a nonzero: R; row tier rt = deepest P_k it couples to
+    std::vector<std::uint8_t> in_r(nv, 0), rt(nv, 0);
     for (const auto& [key, s] : stiff) {
         const auto [vi, vj, k] = key;
         (void)k;
-        if (s != 0.0 && sel[vj]) in_r[vi] = 1;
+        if (s != 0.0 && sel[vj]) {
+            in_r[vi] = 1;
+            rt[vi] = std::max(rt[vi], vt[vj]);
+        }
     }
+    int tiers = 1;
+    if (spec.tiers > 1)
+        for (int v = 0; v < nv; ++v) tiers = std::max<int>(tiers, rt[v]);
+    L.tiers = tiers;
 
     // structured lattice block (substep fast path), decided in vertex space
     std::vector<int> box_vertex;  // (m+1)^2 box nodes in (j, i) order, or empty
-    if (spec.kind == Integrator::LocalTimeStepping)
+    if (spec.kind == Integrator::LocalTimeStepping && tiers == 1)
         box_vertex = lattice_block(mesh, spec, mass, stiff, in_r, L);
 
-    // dof order: the lattice box (row-major), the other R rows, then the
-    // rest, each in mesh vertex order
+    // dof order: the lattice box (row-major), the other R rows (deepest tier
+    // first), then the rest, each in mesh vertex order
     std::vector<int> vdof(nv, -1);
     for (int v : box_vertex) {
         vdof[v] = static_cast<int>(L.dof_vertex.size());
         L.dof_vertex.push_back(v);
         ++L.n_r;
     }
-    for (int pass = 0; pass < 2; ++pass)
+    for (int pass = tiers; pass >= 0; --pass)
         for (int v = 0; v < nv; ++v) {
             if (mesh.boundary_vertex[v] || vdof[v] >= 0) continue;
-            if ((pass == 0) != (in_r[v] != 0)) continue;
+            if (pass > 0 ? (!in_r[v] || (tiers > 1 && rt[v] != pass) || (tiers == 1 && pass != 1)) : in_r[v])
+                continue;
             vdof[v] = static_cast<int>(L.dof_vertex.size());
             L.dof_vertex.push_back(v);
-            if (pass == 0) ++L.n_r;
+            if (pass > 0) ++L.n_r;
         }
+    L.n_r_tier.assign(tiers, 0);
+    for (int k = 1; k <= tiers; ++k)
+        for (int v = 0; v < nv; ++v)
+            if (!mesh.boundary_vertex[v] && in_r[v] && (tiers == 1 || rt[v] >= k)) ++L.n_r_tier[k - 1];
     L.n = static_cast<int>(L.dof_vertex.size());
     if (L.n == 0) throw std::invalid_argument("level: mesh has no interior vertices");
     L.in_p.assign(L.n, 0);
@@ -297,6 +317,25 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
             L.apg_a0.push_back(a);
         }
         L.apg_ptr[i + 1] = static_cast<int>(L.apg_ent.size());
+    }
+
+    // nested tiers: A P_k on R_k rows, parts form
+    if (tiers > 1) {
+        for (int k = 1; k <= tiers; ++k) {
+            std::vector<int> ptr{0}, ent;
+            std::vector<double> a0;
+            for (int i = 0; i < L.n_r_tier[k - 1]; ++i) {
+                for (const auto& [j, c, a] : rows[i]) {
+                    if (vt[L.dof_vertex[j]] < k) continue;
+                    ent.push_back(j | (c << 23));  // kColBits
+                    a0.push_back(a);
+                }
+                ptr.push_back(static_cast<int>(ent.size()));
+            }
+            L.tier_ptr.push_back(std::move(ptr));
+            L.tier_ent.push_back(std::move(ent));
+            L.tier_a0.push_back(std::move(a0));
+        }
     }
 
     // A P on R rows as deduplicated recipes
@@ -396,6 +435,12 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         const double area = mesh.signed_area(t);
         for (int v : mesh.triangles[t]) qw[v] += area / 3.0;
     }
+    if (spec.qoi_mean) {  // mean over the box: divide by the area of its triangles
+        double total = 0.0;
+        for (int v = 0; v < nv; ++v) total += qw[v];
+        if (!(total > 0.0)) throw std::invalid_argument("level: QoI box contains no triangle");
+        for (int v = 0; v < nv; ++v) qw[v] /= total;
+    }
     for (int i = 0; i < L.n; ++i) {
         const int v = L.dof_vertex[i];
         if (qw[v] != 0.0) {
@@ -432,6 +477,18 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
             dcur = next;
         }
         L.coarse_factor = -2.0 * dcur;
+        if (tiers > 1) {
+            double dt_k = dt;  // tier k advances in steps of dt / p^k; its interval is dt_k = dt / p^(k-1)
+            for (int k = 1; k <= tiers; ++k) {
+                const double tk2 = (dt_k / p) * (dt_k / p);
+                L.tier_c0.push_back(0.5 * tk2 * 2.0 * p * p / (cc.omega * cc.delta));
+                std::vector<double> cmk(p - 1);
+                for (int m = 1; m <= p - 1; ++m) cmk[m - 1] = tk2 * 2.0 * p * p / cc.omega * cc.beta_half[m - 1];
+                L.tier_cm.push_back(cmk);
+                L.tier_back.push_back(-2.0 / (dt_k * dt_k));
+                dt_k /= p;
+            }
+        }
     }
     return L;
 }
@@ -439,6 +496,14 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
 double dof_updates_per_solve(const LevelTables& t) {
     const double n = t.n;
     if (t.kind == Integrator::Leapfrog) return static_cast<double>(t.n_steps) * n;
+    if (t.tiers > 1) {
+        double per_step = n, pk = 1.0;
+        for (int k = 1; k <= t.tiers; ++k) {
+            per_step += (pk * t.p - pk) * static_cast<double>(t.n_r_tier[k - 1]);
+            pk *= t.p;
+        }
+        return n + static_cast<double>(t.n_steps - 1) * per_step;
+    }
     return n + static_cast<double>(t.n_steps - 1) * (n + (t.p - 1) * static_cast<double>(t.n_r));
 }
 

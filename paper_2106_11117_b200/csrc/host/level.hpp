@@ -37,7 +37,7 @@ struct QoIBox {
 enum class Field : int { Uniform = 0, LognormalKL = 1 };
 
 struct LevelSpec {
-    int cells_x = 4, cells_y = 4;  // coefficient grid on [0,1]^2, cell k = iy*cells_x + ix
+    int cells_x = 4, cells_y = 4;  // coefficient grid on the domain box, cell k = iy*cells_x + ix
     double coef_lo = 0.5, coef_hi = 1.5;  // c_k ~ U[coef_lo, coef_hi)
     Field field = Field::Uniform;
     double kl_sigma = 0.5, kl_corr_len = 0.1;  // log-normal KL (BASELINE config 4)
@@ -49,6 +49,14 @@ struct LevelSpec {
     Integrator kind = Integrator::LocalTimeStepping;
     GaussianIC ic;
     QoIBox qoi;
+    bool qoi_mean = false;  // Q = mean over the box (weights normalised by their sum)
+    int tiers = 1;          // nested LTS tiers (config 2); 1 = the reference's single-tier LF-LTS
+    double dom_x0 = 0.0, dom_x1 = 1.0, dom_y0 = 0.0, dom_y1 = 1.0;  // coefficient grid extent
+
+    // cell k = iy * cells_x + ix of the coefficient grid, ix = floor((x - x0) / (x1 - x0) * cells_x)
+    int cell_col(double x) const;
+    int cell_row(double y) const;
+    int cell_of(double x, double y) const { return cell_row(y) * cells_x + cell_col(x); }
 };
 
 struct ChebyshevConstants {
@@ -118,6 +126,18 @@ struct LevelTables {
     std::vector<int> gen_rc_ptr, gen_rc_cell;  // per entry: terms of w = sum c_k a0_k sqrt(M_j)
     std::vector<double> gen_rc_a0;
 
+    // nested tiers (config 2): rows are ordered deepest tier first, so
+    // R_k = rows [0, n_r_tier[k-1]) with R_1 = [0, n_r) ⊇ R_2 ⊇ ...; per tier
+    // A P_k on R_k rows in parts form (col | cell << 23, a0) and the tier's
+    // substep constants (its "dt" is dt / p^(k-1)); back = -2 / dt_k^2 turns
+    // the tier's d_p into the effective right-hand side of tier k-1
+    int tiers = 1;
+    std::vector<int> n_r_tier;
+    std::vector<std::vector<int>> tier_ptr, tier_ent;
+    std::vector<std::vector<double>> tier_a0;
+    std::vector<double> tier_c0, tier_back;
+    std::vector<std::vector<double>> tier_cm;
+
     // time stepping
     long n_steps = 0;
     double dt = 0.0;
@@ -133,7 +153,8 @@ struct LevelTables {
 LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec);
 
 /// DOF-updates per solve: steps * (n + (p-1)|R|) for LTS, steps * n for LF
-/// (SURVEY.md section 8(d)); the start-up step counts as one sweep.
+/// (SURVEY.md section 8(d)); the start-up step counts as one sweep.  Nested
+/// tiers: a row of R_k \ R_k+1 advances p^k times per step.
 double dof_updates_per_solve(const LevelTables& t);
 
 }  // namespace wmc

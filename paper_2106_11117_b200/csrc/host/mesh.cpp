@@ -27,7 +27,12 @@ namespace {
 struct Quadtree {
     int levels = 0;  // coarse level K: coarse side = 2^K units
     long extent = 0;  // domain side in units
+    long cut = -1;    // L-shape: unit cells with px >= cut and py < cut lie outside (-1: square)
     std::unordered_set<std::uint64_t> leaves;
+
+    bool outside(long px, long py) const {
+        return px < 0 || py < 0 || px >= extent || py >= extent || (cut >= 0 && px >= cut && py < cut);
+    }
 
     static std::uint64_t key(int k, long i, long j) {
         return (std::uint64_t(k) << 56) | (std::uint64_t(i) << 28) | std::uint64_t(j);
@@ -36,7 +41,7 @@ struct Quadtree {
 
     // side of the leaf covering unit cell (px, py); 0 outside the domain
     long size_at(long px, long py) const {
-        if (px < 0 || py < 0 || px >= extent || py >= extent) return 0;
+        if (outside(px, py)) return 0;
         for (int k = 0; k <= levels; ++k)
             if (leaves.count(key(k, px >> k, py >> k))) return 1L << k;
         throw std::logic_error("quadtree: unit cell not covered");
@@ -101,6 +106,97 @@ int ilog2_exact(int v) {
     return k;
 }
 
+// triangulate the leaves: plain cells split along the SW-NE diagonal, one
+// hanging midpoint -> three triangles (the reference 2:1 cell,
+// mesh2d.cpp:96-130), two or more -> fan around the cell centre.  Vertices in
+// lattice units, tri_level = quadtree level of each triangle's leaf.
+void triangulate(const Quadtree& tree, std::vector<std::array<long, 2>>& lat, std::vector<std::array<int, 3>>& tris,
+                 std::vector<int>& tri_level) {
+    std::map<std::pair<long, long>, int> vid;
+    lat.clear();
+    tris.clear();
+    tri_level.clear();
+    auto vertex = [&](long x, long y) {
+        const auto it = vid.find({y, x});
+        if (it != vid.end()) return it->second;
+        const int id = static_cast<int>(lat.size());
+        vid.emplace(std::make_pair(y, x), id);
+        lat.push_back({x, y});
+        return id;
+    };
+    for (const auto& leaf : tree.list()) {
+        const long s = 1L << leaf.k;
+        const long x0 = leaf.x0, y0 = leaf.y0;
+        // corners CCW: SW, SE, NE, NW; side e runs from corner e to corner e+1
+        const long cx[4] = {x0, x0 + s, x0 + s, x0};
+        const long cy[4] = {y0, y0, y0 + s, y0 + s};
+        bool hang[4] = {false, false, false, false};
+        if (s >= 2) {
+            long v;
+            hang[0] = (v = tree.size_at(x0 + s / 2, y0 - 1)) && v < s;  // bottom
+            hang[1] = (v = tree.size_at(x0 + s, y0 + s / 2)) && v < s;  // right
+            hang[2] = (v = tree.size_at(x0 + s / 2, y0 + s)) && v < s;  // top
+            hang[3] = (v = tree.size_at(x0 - 1, y0 + s / 2)) && v < s;  // left
+        }
+        const int nh = hang[0] + hang[1] + hang[2] + hang[3];
+        int c[4];
+        for (int e = 0; e < 4; ++e) c[e] = vertex(cx[e], cy[e]);
+        if (nh == 0) {
+            tris.push_back({c[0], c[1], c[2]});
+            tris.push_back({c[0], c[2], c[3]});
+            tri_level.insert(tri_level.end(), 2, leaf.k);
+        } else if (nh == 1) {
+            int e = 0;
+            while (!hang[e]) ++e;
+            const int c0 = c[e], c1 = c[(e + 1) % 4], c2 = c[(e + 2) % 4], c3 = c[(e + 3) % 4];
+            const int m = vertex((cx[e] + cx[(e + 1) % 4]) / 2, (cy[e] + cy[(e + 1) % 4]) / 2);
+            tris.push_back({c0, m, c3});
+            tris.push_back({m, c2, c3});
+            tris.push_back({m, c1, c2});
+            tri_level.insert(tri_level.end(), 3, leaf.k);
+        } else {
+            const int o = vertex(x0 + s / 2, y0 + s / 2);
+            for (int e = 0; e < 4; ++e) {
+                const int a = c[e], b = c[(e + 1) % 4];
+                if (hang[e]) {
+                    const int m = vertex((cx[e] + cx[(e + 1) % 4]) / 2, (cy[e] + cy[(e + 1) % 4]) / 2);
+                    tris.push_back({o, a, m});
+                    tris.push_back({o, m, b});
+                    tri_level.insert(tri_level.end(), 2, leaf.k);
+                } else {
+                    tris.push_back({o, a, b});
+                    tri_level.push_back(leaf.k);
+                }
+            }
+        }
+    }
+}
+
+// vertex renumbering row-major (y, then x) for a deterministic order
+std::vector<int> row_major_rank(const std::vector<std::array<long, 2>>& lat) {
+    std::vector<int> order(lat.size());
+    for (std::size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        if (lat[a][1] != lat[b][1]) return lat[a][1] < lat[b][1];
+        return lat[a][0] < lat[b][0];
+    });
+    std::vector<int> rank(lat.size());
+    for (std::size_t i = 0; i < order.size(); ++i) rank[order[i]] = static_cast<int>(i);
+    return rank;
+}
+
+// 2:1 balance across edges and corners
+void balance(Quadtree& tree) {
+    for (bool changed = true; changed;) {
+        changed = false;
+        for (const auto& leaf : tree.list())
+            if (tree.has(leaf.k, leaf.x0, leaf.y0) && tree.unbalanced(leaf.k, leaf.x0, leaf.y0)) {
+                tree.split(leaf.k, leaf.x0, leaf.y0);
+                changed = true;
+            }
+    }
+}
+
 }  // namespace
 
 TriMesh build_refined_square(const SquareMeshSpec& spec) {
@@ -146,83 +242,14 @@ TriMesh build_refined_square(const SquareMeshSpec& spec) {
                     }
                 }
             }
-        // 2:1 balance across edges and corners
-        for (bool changed = true; changed;) {
-            changed = false;
-            for (const auto& leaf : tree.list())
-                if (tree.has(leaf.k, leaf.x0, leaf.y0) && tree.unbalanced(leaf.k, leaf.x0, leaf.y0)) {
-                    tree.split(leaf.k, leaf.x0, leaf.y0);
-                    changed = true;
-                }
-        }
+        balance(tree);
     }
 
-    // triangulate: plain cells split along the SW-NE diagonal, one hanging
-    // midpoint -> three triangles (the reference 2:1 cell, mesh2d.cpp:96-130),
-    // two or more -> fan around the cell centre
-    std::map<std::pair<long, long>, int> vid;
     std::vector<std::array<long, 2>> lat;
-    auto vertex = [&](long x, long y) {
-        const auto it = vid.find({y, x});
-        if (it != vid.end()) return it->second;
-        const int id = static_cast<int>(lat.size());
-        vid.emplace(std::make_pair(y, x), id);
-        lat.push_back({x, y});
-        return id;
-    };
     std::vector<std::array<int, 3>> tris;
-    for (const auto& leaf : tree.list()) {
-        const long s = 1L << leaf.k;
-        const long x0 = leaf.x0, y0 = leaf.y0;
-        // corners CCW: SW, SE, NE, NW; side e runs from corner e to corner e+1
-        const long cx[4] = {x0, x0 + s, x0 + s, x0};
-        const long cy[4] = {y0, y0, y0 + s, y0 + s};
-        bool hang[4] = {false, false, false, false};
-        if (s >= 2) {
-            long v;
-            hang[0] = (v = tree.size_at(x0 + s / 2, y0 - 1)) && v < s;  // bottom
-            hang[1] = (v = tree.size_at(x0 + s, y0 + s / 2)) && v < s;  // right
-            hang[2] = (v = tree.size_at(x0 + s / 2, y0 + s)) && v < s;  // top
-            hang[3] = (v = tree.size_at(x0 - 1, y0 + s / 2)) && v < s;  // left
-        }
-        const int nh = hang[0] + hang[1] + hang[2] + hang[3];
-        int c[4];
-        for (int e = 0; e < 4; ++e) c[e] = vertex(cx[e], cy[e]);
-        if (nh == 0) {
-            tris.push_back({c[0], c[1], c[2]});
-            tris.push_back({c[0], c[2], c[3]});
-        } else if (nh == 1) {
-            int e = 0;
-            while (!hang[e]) ++e;
-            const int c0 = c[e], c1 = c[(e + 1) % 4], c2 = c[(e + 2) % 4], c3 = c[(e + 3) % 4];
-            const int m = vertex((cx[e] + cx[(e + 1) % 4]) / 2, (cy[e] + cy[(e + 1) % 4]) / 2);
-            tris.push_back({c0, m, c3});
-            tris.push_back({m, c2, c3});
-            tris.push_back({m, c1, c2});
-        } else {
-            const int o = vertex(x0 + s / 2, y0 + s / 2);
-            for (int e = 0; e < 4; ++e) {
-                const int a = c[e], b = c[(e + 1) % 4];
-                if (hang[e]) {
-                    const int m = vertex((cx[e] + cx[(e + 1) % 4]) / 2, (cy[e] + cy[(e + 1) % 4]) / 2);
-                    tris.push_back({o, a, m});
-                    tris.push_back({o, m, b});
-                } else {
-                    tris.push_back({o, a, b});
-                }
-            }
-        }
-    }
-
-    // renumber vertices row-major (y, then x) for a deterministic order
-    std::vector<int> order(lat.size());
-    for (std::size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
-    std::sort(order.begin(), order.end(), [&](int a, int b) {
-        if (lat[a][1] != lat[b][1]) return lat[a][1] < lat[b][1];
-        return lat[a][0] < lat[b][0];
-    });
-    std::vector<int> rank(lat.size());
-    for (std::size_t i = 0; i < order.size(); ++i) rank[order[i]] = static_cast<int>(i);
+    std::vector<int> tri_level;
+    triangulate(tree, lat, tris, tri_level);
+    std::vector<int> rank = row_major_rank(lat);
 
     TriMesh mesh;
     mesh.coarse_h = 1.0 / static_cast<double>(n);
@@ -271,6 +298,94 @@ TriMesh build_refined_square(const SquareMeshSpec& spec) {
                 break;
             }
     }
+    return mesh;
+}
+
+TriMesh build_graded_lshape(const LShapeMeshSpec& spec) {
+    if (spec.n_per_unit < 1) throw std::invalid_argument("build_graded_lshape: n_per_unit >= 1");
+    if (spec.tiers < 0 || spec.tiers > 6) throw std::invalid_argument("build_graded_lshape: tiers in [0, 6]");
+    if (!(spec.grade_radius > 0.0)) throw std::invalid_argument("build_graded_lshape: grade_radius > 0");
+    const int K = spec.tiers;
+    const long n = spec.n_per_unit;  // coarse cells per unit length
+    const long R = 1L << K;
+    const long extent = 2 * n * R;   // [-1, 1] in lattice units
+    if (extent >= (1L << 27)) throw std::invalid_argument("build_graded_lshape: mesh too large");
+    const long corner = n * R;       // (0, 0) in lattice units
+    const double h = 1.0 / static_cast<double>(n);
+    const double unit = h / static_cast<double>(R);
+
+    Quadtree tree;
+    tree.levels = K;
+    tree.extent = extent;
+    tree.cut = corner;  // the quadrant x >= 0, y < 0 is not in the domain
+    for (long j = 0; j < 2 * n; ++j)
+        for (long i = 0; i < 2 * n; ++i)
+            if (!tree.outside(i * R, j * R)) tree.leaves.insert(Quadtree::key(K, i, j));
+
+    // grading toward the corner: split a leaf of side s while
+    // s > h sqrt(r / rho), i.e. r < rho (s / h)^2, r = leaf-to-corner distance
+    std::vector<Quadtree::Leaf> work = tree.list();
+    while (!work.empty()) {
+        const auto leaf = work.back();
+        work.pop_back();
+        if (leaf.k == 0) continue;
+        const long s = 1L << leaf.k;
+        const long dx = std::max({leaf.x0 - corner, 0L, corner - (leaf.x0 + s)});
+        const long dy = std::max({leaf.y0 - corner, 0L, corner - (leaf.y0 + s)});
+        const double r = std::hypot(static_cast<double>(dx), static_cast<double>(dy)) * unit;
+        const double rel = static_cast<double>(s) * unit / h;
+        if (!(r < spec.grade_radius * rel * rel)) continue;
+        tree.split(leaf.k, leaf.x0, leaf.y0);
+        const long hs = s / 2;
+        for (long cy = 0; cy < 2; ++cy)
+            for (long cx = 0; cx < 2; ++cx) work.push_back({leaf.k - 1, leaf.x0 + cx * hs, leaf.y0 + cy * hs});
+    }
+    balance(tree);
+
+    std::vector<std::array<long, 2>> lat;
+    std::vector<std::array<int, 3>> tris;
+    std::vector<int> tri_level;
+    triangulate(tree, lat, tris, tri_level);
+    const std::vector<int> rank = row_major_rank(lat);
+
+    TriMesh mesh;
+    mesh.coarse_h = h;
+    mesh.fine_h = unit;
+    mesh.vertices.resize(lat.size());
+    mesh.lattice.resize(lat.size());
+    for (std::size_t i = 0; i < lat.size(); ++i) {
+        const int r = rank[i];
+        mesh.vertices[r] = {static_cast<double>(lat[i][0] - corner) * unit,
+                            static_cast<double>(lat[i][1] - corner) * unit};
+        mesh.lattice[r] = {static_cast<int>(lat[i][0]), static_cast<int>(lat[i][1])};
+    }
+    mesh.triangles.reserve(tris.size());
+    for (const auto& t : tris) {
+        mesh.triangles.push_back({rank[t[0]], rank[t[1]], rank[t[2]]});
+        if (!(mesh.signed_area(mesh.n_triangles() - 1) > 0.0))
+            throw std::logic_error("build_graded_lshape: non-CCW triangle");
+    }
+    // Dirichlet boundary: vertices of edges that belong to one triangle
+    std::map<std::pair<int, int>, int> edges;
+    for (const auto& t : mesh.triangles)
+        for (int e = 0; e < 3; ++e) {
+            const int a = t[e], b = t[(e + 1) % 3];
+            ++edges[{std::min(a, b), std::max(a, b)}];
+        }
+    mesh.boundary_vertex.assign(mesh.vertices.size(), 0);
+    for (const auto& [e, count] : edges)
+        if (count == 1) mesh.boundary_vertex[e.first] = mesh.boundary_vertex[e.second] = 1;
+
+    // tiers: the leaf's depth below the coarse level, then one adjacent layer
+    const int nt = mesh.n_triangles();
+    std::vector<std::uint8_t> vtier(mesh.vertices.size(), 0);
+    for (int t = 0; t < nt; ++t) {
+        const auto tier = static_cast<std::uint8_t>(K - tri_level[t]);
+        for (int v : mesh.triangles[t]) vtier[v] = std::max(vtier[v], tier);
+    }
+    mesh.fine_flags.assign(nt, 0);
+    for (int t = 0; t < nt; ++t)
+        for (int v : mesh.triangles[t]) mesh.fine_flags[t] = std::max(mesh.fine_flags[t], vtier[v]);
     return mesh;
 }
 

@@ -21,7 +21,7 @@ namespace wmc {
 struct TriMesh {
     std::vector<std::array<double, 2>> vertices;
     std::vector<std::array<int, 3>> triangles;  // counter-clockwise
-    std::vector<std::uint8_t> fine_flags;       // per triangle
+    std::vector<std::uint8_t> fine_flags;       // per triangle: 0 coarse, k >= 1 tier (selector P_k = flag >= k)
     std::vector<std::uint8_t> boundary_vertex;  // per vertex (Dirichlet)
     std::vector<std::array<int, 2>> lattice;    // integer lattice coordinates (units of fine_h)
     int fine_box_lo = -1, fine_box_hi = -1;     // refined square [lo, hi]^2 in lattice units (-1: none)
@@ -58,6 +58,23 @@ struct SquareMeshSpec {
 /// at h / ratio with 2:1 balanced transitions.  Throws std::invalid_argument on
 /// bad specs.
 TriMesh build_refined_square(const SquareMeshSpec& spec);
+
+struct LShapeMeshSpec {
+    int n_per_unit = 16;        // h = 1 / n_per_unit on [-1,1]^2 minus [0,1]x[-1,0]
+    int tiers = 3;              // refinement tiers toward the re-entrant corner (0,0): h/2 .. h/2^tiers
+    double grade_radius = 0.25;  // element size target h * sqrt(r / grade_radius) near the corner
+};
+
+/// Graded L-shape (BASELINE config 2, no reference counterpart: the
+/// reference L-shape, src/mesh_graded.cpp:48-112, is a different domain with
+/// no fine flags).  Balanced quadtree as build_refined_square; a leaf of side
+/// s is split while s > h * sqrt(r / grade_radius), r = distance of the leaf
+/// to the corner, down to h / 2^tiers.  fine_flags[t] = refinement tier
+/// (0 = coarse) of the triangle, raised to the largest tier among the
+/// triangles sharing one of its vertices (the reference's "plus one adjacent
+/// layer", mesh2d.cpp:285-301, applied per tier).  Dirichlet on the whole
+/// boundary (edges of one triangle).
+TriMesh build_graded_lshape(const LShapeMeshSpec& spec);
 
 /// Reference fixture format (reference proj/src/mesh_io.cpp:1-9).
 void dump_mesh_text(const TriMesh& mesh, const std::string& path);

@@ -291,6 +291,73 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
     if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
 }
 
+// Nested-tier stage (see TierArgs): the single-tier recursion of reference
+// src/integrators.cpp:117-157 applied per tier, with the stage's right-hand
+// side on R_k+1 replaced by the tier-(k+1) solve over the stage interval.
+__global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(const __grid_constant__ TierArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int nrows = a.row_end - a.row_begin;
+    const int row = a.row_begin + grid_rowgroup(nrows) * kSweepWarps + (threadIdx.x >> 5);
+    if (row >= a.row_end) return;
+    const int s0 = grid_chunk(nrows) * kSweepChunk + 2 * lane;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
+    double2 v = __ldg(reinterpret_cast<const double2*>(a.rhs + idx));
+    if (a.m > 0) {
+        const double* src = a.e[a.k - 1][a.m & 1];
+        double acc0 = 0.0, acc1 = 0.0;
+        const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
+#pragma unroll 4
+        for (int q = b; q < e; ++q) {
+            const int pk = __ldg(a.ent + q);
+            const double w = __ldg(a.a0 + q);
+            const int j = pk & kColMask;
+            const int cell = static_cast<unsigned>(pk) >> kColBits;
+            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+            const double2 x = *reinterpret_cast<const double2*>(src + j * S + s0);
+            acc0 += (c.x * w) * x.x;
+            acc1 += (c.y * w) * x.y;
+        }
+        v.x += acc0;
+        v.y += acc1;
+    }
+    if (row < a.split) {
+        *reinterpret_cast<double2*>(a.rhs_next + idx) = v;
+        return;
+    }
+    // the tier's update, then up through the ancestors whose stage ends here
+    for (int j = a.k;; --j) {
+        const int mj = a.stage[j - 1];
+        double2 en;
+        if (mj == 0) {
+            en = make_double2(-a.c0[j - 1] * v.x, -a.c0[j - 1] * v.y);
+        } else {
+            const double beta = a.beta[mj - 1], cm = a.cm[(j - 1) * (a.p - 1) + mj - 1];
+            const double2 em = *reinterpret_cast<const double2*>(a.e[j - 1][mj & 1] + idx);
+            double2 emm = make_double2(0.0, 0.0);
+            if (mj >= 2) emm = *reinterpret_cast<const double2*>(a.e[j - 1][(mj + 1) & 1] + idx);
+            en.x = (1.0 + beta) * em.x - beta * emm.x - cm * v.x;
+            en.y = (1.0 + beta) * em.y - beta * emm.y - cm * v.y;
+        }
+        if (mj + 1 < a.p) {
+            *reinterpret_cast<double2*>(a.e[j - 1][(mj + 1) & 1] + idx) = en;
+            return;
+        }
+        if (j == 1) {
+            const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
+            const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
+            double2 out;
+            out.x = 2.0 * zn.x - zm.x + 2.0 * en.x;
+            out.y = 2.0 * zn.y - zm.y + 2.0 * en.y;
+            *reinterpret_cast<double2*>(a.zp + idx) = out;
+            if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
+            if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+            return;
+        }
+        v = make_double2(a.back[j - 1] * en.x, a.back[j - 1] * en.y);
+    }
+}
+
 // R update: z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on rows < n_r, d_p read
 // sample-major and transposed through shared memory (mirror of the sweep's
 // g store), then one warp per (row, 64 samples) as in the sweep.
@@ -893,6 +960,13 @@ int substep_max_grid(int device, int smem_bytes) {
 void launch_global_substep(const GSubArgs& a, void* stream) {
     const unsigned grid = ((a.n_r + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
     global_substep_kernel<<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+}
+
+void launch_tier_stage(const TierArgs& a, void* stream) {
+    const int rows = a.row_end - a.row_begin;
+    if (rows <= 0) return;
+    const unsigned grid = ((rows + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
+    tier_stage_kernel<<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_r_update(const RUpdateArgs& a, void* stream) {

@@ -134,6 +134,36 @@ struct GSubArgs {
     int* fail;
 };
 
+// Nested tiers (BASELINE config 2, no reference counterpart; DESIGN.md
+// section "Nested LTS"): one stage m of tier k over the rows of R_k, warp per
+// (row, 64 samples).  rho = r_k + A P_k E^k_m (the product only for m >= 1);
+// rows < split (R_k+1) hand rho to tier k+1 as its right-hand side, the
+// others apply the tier-k update and, when m is the tier's last stage, carry
+// the result up through the ancestors' updates (r~ = back_j E^j_p) down to
+// z_{n+1} = 2 z_n - z_{n-1} + 2 E^1_p.  Tier j keeps E^j_m in e[j][m & 1].
+constexpr int kMaxTiers = 8;
+
+struct TierArgs {
+    int k, m, p;                 // tier (1-based), stage, substeps per tier
+    int row_begin, row_end, split;
+    int S, count;
+    const int* ptr;              // A P_k on R_k rows: col | cell << kColBits, a0
+    const int* ent;
+    const double* a0;
+    const double* cells;
+    const double* rhs;           // r_k [row][S]
+    double* rhs_next;            // r_k+1 [row][S] (rows < split)
+    double* e[kMaxTiers][2];
+    int stage[kMaxTiers];        // current stage of tiers 1..k
+    double c0[kMaxTiers], back[kMaxTiers];
+    const double* beta;          // p - 1
+    const double* cm;            // [tier][p - 1]
+    const double* zc;
+    double* zp;
+    int step;
+    int* fail;
+};
+
 struct QoIArgs {
     int nq, S, count;
     const int* dof;
@@ -158,6 +188,7 @@ int launch_substeps(const SubArgs& a, int grid, void* stream);  // returns cudaE
 void launch_qoi(const QoIArgs& a, void* stream);
 void launch_r_update(const RUpdateArgs& a, void* stream);
 void launch_global_substep(const GSubArgs& a, void* stream);
+void launch_tier_stage(const TierArgs& a, void* stream);
 void launch_fill_int(int* p, int value, int n, void* stream);
 void launch_pair_diff(const double* qf, const double* qc, double* dq, int count, void* stream);
 int substep_max_grid(int device, int smem_bytes);

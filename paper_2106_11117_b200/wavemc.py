@@ -43,6 +43,14 @@ class Mesh:
         return cls(h.value)
 
     @classmethod
+    def build_lshape(cls, n_per_unit: int, tiers: int = 3, grade_radius: float = 0.25) -> "Mesh":
+        """Graded L-shape [-1,1]^2 minus [0,1]x[-1,0] (BASELINE config 2); flags = tiers."""
+        spec = N.LShapeMeshSpec(n_per_unit, tiers, grade_radius)
+        h = C.c_void_p()
+        N.check(N.lib().wmc_mesh_build_lshape(C.byref(spec), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
     def from_arrays(cls, xy, tri, fine, boundary, coarse_h=0.0, fine_h=0.0) -> "Mesh":
         xy = np.ascontiguousarray(xy, dtype=np.float64)
         tri = np.ascontiguousarray(tri, dtype=np.int32)
@@ -101,6 +109,9 @@ class LevelSpec:
     kl_sigma: float = 0.5
     kl_corr_len: float = 0.1
     kl_modes: int = 64
+    tiers: int = 1
+    domain: tuple = (0.0, 1.0, 0.0, 1.0)
+    qoi_mean: bool = False
 
     def desc(self) -> N.LevelDesc:
         d = N.LevelDesc()
@@ -114,7 +125,17 @@ class LevelSpec:
             d.qoi_box[i] = v
         d.device, d.batch = self.device, self.batch
         d.field, d.kl_sigma, d.kl_corr_len, d.kl_modes = self.field, self.kl_sigma, self.kl_corr_len, self.kl_modes
+        d.tiers = self.tiers
+        for i, v in enumerate(self.domain):
+            d.domain[i] = v
+        d.qoi_mean = 1 if self.qoi_mean else 0
         return d
+
+
+def _info_dict(info: N.LevelInfo) -> dict:
+    out = {k: getattr(info, k) for k, _ in N.LevelInfo._fields_}
+    out["n_r_tier"] = list(out["n_r_tier"])[: max(out["tiers"], 1)]
+    return out
 
 
 def level_plan(mesh: Mesh, spec: LevelSpec) -> dict:
@@ -122,7 +143,7 @@ def level_plan(mesh: Mesh, spec: LevelSpec) -> dict:
     d = spec.desc()
     info = N.LevelInfo()
     N.check(N.lib().wmc_level_plan(mesh._h, C.byref(d), C.byref(info)))
-    return {k: getattr(info, k) for k, _ in N.LevelInfo._fields_}
+    return _info_dict(info)
 
 
 class Level:
@@ -137,7 +158,7 @@ class Level:
         self._h = h
         info = N.LevelInfo()
         N.check(N.lib().wmc_level_get_info(self._h, C.byref(info)))
-        self.info = {k: getattr(info, k) for k, _ in N.LevelInfo._fields_}
+        self.info = _info_dict(info)
 
     @property
     def stream(self) -> int:
