@@ -41,9 +41,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of N_l (1.0 = the BASELINE counts)")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 3, 4],
-                    help="BASELINE config: 1 (default, MLMC), 0 (single-level MC), 3 (large single level), "
-                         "4 (adaptive MLMC to an RMSE target, log-normal KL coefficient)")
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4],
+                    help="BASELINE config: 1 (default, MLMC), 0 (single-level MC), 2 (graded L-shape MLMC, "
+                         "nested 3-tier LTS), 3 (large single level), 4 (adaptive MLMC to an RMSE target, "
+                         "log-normal KL coefficient)")
     ap.add_argument("--eps", type=float, default=None, help="config 4: RMSE target (default BASELINE 1e-3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -115,6 +116,11 @@ def workload(config: int):
     from paper_2106_11117_b200 import configs
     if config == 0:
         return [configs.config0()], [configs.CONFIG0_COUNT], "BASELINE config 0: single-level MC, h=1/32 refined x4, p=4", None
+    if config == 2:
+        defs = configs.config2()
+        # the CPU sample keeps every level but shortens the horizon to T/8
+        return defs, list(configs.CONFIG2_COUNTS), (
+            "BASELINE config 2: graded L-shape MLMC, nested LTS 3 tiers x p=2, 5 levels h=1/16..1/256, T=2"), 0.25
     if config == 3:
         d = configs.config3()
         # the CPU sample keeps the mesh and the per-step work but shortens the
@@ -124,12 +130,27 @@ def workload(config: int):
         "BASELINE config 1: fixed-N MLMC, LF-LTS, 5 levels h=1/16..1/256, p=32..2"), None
 
 
-def ref_sample_counts(threads: int):
+def oracle_problem(d, final_time=None):
+    """The C restatement's problem for a level definition (test-side mirror of
+    configs.level_spec)."""
+    import oracle_py
+    from paper_2106_11117_b200 import configs
+    T = d.final_time if final_time is None else final_time
+    if d.shape == "lshape":
+        c = configs.CONFIG2_PROBLEM
+        return oracle_py.problem(d.dt, d.substeps, final_time=T, cells=c["cells"], ic=c["ic"], box=c["qoi_box"],
+                                 domain=c["domain"], qoi_mean=True, tiers=d.tiers)
+    return oracle_py.problem(d.dt, d.substeps, final_time=T)
+
+
+def ref_sample_counts(threads: int, defs=None):
     """Bounded sample of config 1 for the CPU, in the proportions of N_l
     (65536 : 16384 : 4096 : 1024 : 256 = 256 : 64 : 16 : 4 : 1), sized for
     ~10-15 s of wall time on `threads` cores (measured: 2.8 s for a quarter of
     this sample on 16 cores)."""
     t = max(1, threads)
+    if defs is not None and defs[0].shape == "lshape":  # config 2: N_l halving, horizon T/8
+        return [8 * t, 4 * t, 2 * t, t, max(1, t // 2)]
     return [64 * t, 16 * t, 4 * t, t, max(1, t // 4)]
 
 
@@ -138,19 +159,41 @@ def run_reference_cpu(defs, threads: int, final_time=None):
     its own run_jobs-style pool of `threads` workers.  Returns dict."""
     import oracle_py
     from paper_2106_11117_b200 import configs
-    counts = ref_sample_counts(threads) if len(defs) > 1 else [4 * threads if final_time is None else threads]
+    counts = ref_sample_counts(threads, defs) if len(defs) > 1 else [4 * threads if final_time is None else threads]
     tmp = tempfile.mkdtemp(prefix="wmc_bench_")
     specs = []
+    nested = any(d.tiers > 1 for d in defs)
     for l, d in enumerate(defs):
         p = os.path.join(tmp, f"l{l}.mesh")
         configs.build_mesh(d).dump(p)
-        specs.append((p, d.dt, d.substeps))
+        # config 2: the reference has no nested tiers; its own LF-LTS on the
+        # same mesh needs P = P_1 and p = 2^tiers (stable at the finest tier)
+        specs.append((p, d.dt, d.substeps ** d.tiers if nested else d.substeps))
     drv = oracle_py.RefDriver()
     extra = {"T": repr(final_time)} if final_time is not None else {}
+    if nested:
+        c = configs.CONFIG2_PROBLEM
+        extra.update({"T": repr(final_time if final_time is not None else defs[0].final_time),
+                      "cells-x": c["cells"][0], "cells-y": c["cells"][1], "ic": ",".join(map(repr, c["ic"])),
+                      "box": ",".join(map(repr, c["qoi_box"])), "domain": ",".join(map(repr, c["domain"])),
+                      "qoi-mean": 1})
     res = drv.mlmc(specs, counts, threads=threads, **extra)
     shutil.rmtree(tmp, ignore_errors=True)
-    return {"value": res["dof_updates"] / res["seconds"], "seconds": res["seconds"],
-            "dof_updates": res["dof_updates"], "counts": counts, "kind": "reference", "cores": res["threads"]}
+    work = res["dof_updates"]
+    if nested:  # the same samples counted in the config-2 (nested) units
+        from paper_2106_11117_b200 import wavemc
+        upd = []
+        for d in defs:
+            spec = configs.level_spec(d)
+            if final_time is not None:
+                spec.final_time = final_time
+            upd.append(wavemc.level_plan(configs.build_mesh(d), spec)["dof_updates_per_solve"])
+        work = sum(n * (upd[l] + (upd[l - 1] if l else 0.0)) for l, n in enumerate(counts))
+    return {"value": work / res["seconds"], "seconds": res["seconds"], "dof_updates": work, "counts": counts,
+            "kind": "reference", "cores": res["threads"],
+            "note": ("reference single-tier LF-LTS (P = P_1, p = 8) on the config-2 meshes and samples (it has no "
+                     "nested tiers); value = nested-scheme DOF-updates of the same samples / reference time"
+                     if nested else None)}
 
 
 def run_port_cpu(defs, threads: int, final_time=None):
@@ -161,11 +204,11 @@ def run_port_cpu(defs, threads: int, final_time=None):
     from paper_2106_11117_b200 import configs
     oracle_py.build()
     orc = oracle_py.COracle()
-    counts = ref_sample_counts(threads) if len(defs) > 1 else [4 * threads if final_time is None else threads]
+    counts = ref_sample_counts(threads, defs) if len(defs) > 1 else [4 * threads if final_time is None else threads]
     from paper_2106_11117_b200 import wavemc
     meshes = [oracle_py.MeshArrays(*configs.build_mesh(d).arrays()) for d in defs]
     T = [final_time if final_time is not None else d.final_time for d in defs]
-    probs = [oracle_py.problem(d.dt, d.substeps, final_time=t) for d, t in zip(defs, T)]
+    probs = [oracle_problem(d, t) for d, t in zip(defs, T)]
     upd = []
     for d, t in zip(defs, T):
         spec = configs.level_spec(d)
@@ -236,7 +279,8 @@ def reference_arm(args, world, rank):
     r0 = timed[0]
     sample = (f"config {args.config} bounded sample N_l={r0['counts']} (of {counts_total}) per step"
               + (f", horizon shortened to T={cpu_T!r}" if cpu_T is not None else "")
-              + f", {r0['cores']} threads, {r0['kind']}")
+              + f", {r0['cores']} threads, {r0['kind']}"
+              + (f"; {r0['note']}" if r0.get("note") else ""))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(r["seconds"] for r in timed) / len(timed),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -412,7 +456,8 @@ def b200_arm(args, world, rank, local):
             line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
                                     "sample": f"config {args.config} bounded sample N_l={cb['counts']}"
                                               + (f", T={cpu_T!r}" if cpu_T is not None else "")
-                                              + f", {cb['seconds']:.1f} s"}
+                                              + f", {cb['seconds']:.1f} s"
+                                              + (f"; {cb['note']}" if cb.get("note") else "")}
         except Exception as exc:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                                     "sample": f"failed: {exc}"}
@@ -436,13 +481,25 @@ def roofline_from_profile(levels, counts, prof, step_ms):
     sub_ms = sum(p["sub_ms"] for p in prof)
     upd_ms = sum(p["upd_ms"] for p in prof)
     sweep_bytes = sub_bytes = sub_flops = sub_updates = 0.0
-    global_path = any(lv.info["substep_path"] == 3 for lv in levels)
+    global_path = any(lv.info["substep_path"] in (3, 4) for lv in levels)
     for l, lv in enumerate(levels):
         for lvl in ([l] + ([l - 1] if l else [])):
             info = levels[lvl].info
             n, nr, steps, p = info["n"], info["n_r"], info["n_steps"], info["p"]
             c = counts[l]
             sweep_bytes += 8.0 * c * (steps - 1) * (2 * n + (n - nr))
+            if info["substep_path"] == 4:
+                # nested tiers: p^k stages of tier k per step, each reading
+                # r_k, E_m, E_{m-1} and writing E_{m+1} (or r_k+1) on R_k,
+                # plus z_n, z_{n-1} in and z_{n+1} out on R_1
+                pk, b, u = 1, 3.0 * nr, 0.0
+                for k, nrk in enumerate(info["n_r_tier"]):
+                    pk *= p
+                    b += 4.0 * pk * nrk
+                    u += (pk - pk // p) * nrk
+                sub_bytes += 8.0 * c * (steps - 1) * b
+                sub_updates += c * (steps - 1) * u
+                continue
             if info["substep_path"] == 3:
                 sub_bytes += 8.0 * c * (steps - 1) * (4 * nr * (p - 1) + 2 * nr)
             elif info["substep_path"] in (1, 2):
@@ -454,15 +511,18 @@ def roofline_from_profile(levels, counts, prof, step_ms):
                          "share_of_step": sweep_ms / step_ms if step_ms else None,
                          "achieved_GBps": gbps(sweep_bytes, sweep_ms)},
                "substep": {"ms": sub_ms, "launches": sum(p["sub_launches"] for p in prof),
-                           "path": "hbm-resident" if global_path else "on-chip",
+                           "path": ("hbm-resident nested tiers" if any(lv.info["substep_path"] == 4 for lv in levels)
+                                    else "hbm-resident" if global_path else "on-chip"),
                            "share_of_step": sub_ms / step_ms if step_ms else None,
-                           "fp64_TFLOPs": sub_flops / (sub_ms * 1e-3) / 1e12 if sub_ms else None,
+                           "fp64_TFLOPs": sub_flops / (sub_ms * 1e-3) / 1e12 if sub_ms and sub_flops else None,
                            "substep_dof_updates_per_s": sub_updates / (sub_ms * 1e-3) if sub_ms else None,
                            "achieved_GBps": gbps(sub_bytes, sub_ms)},
                "r_update": {"ms": upd_ms, "launches": sum(p["upd_launches"] for p in prof),
                             "share_of_step": upd_ms / step_ms if step_ms else None}}
     if global_path and sub_ms >= sweep_ms:
-        roof = {"bound": "hbm", "kernel": "global_substep", "achieved": kernels["substep"]["achieved_GBps"],
+        tiers = any(lv.info["substep_path"] == 4 for lv in levels)
+        roof = {"bound": "hbm", "kernel": "tier_stage" if tiers else "global_substep",
+                "achieved": kernels["substep"]["achieved_GBps"],
                 "unit": "GB/s", "traffic": None, "note": "dominant kernel, HBM-resident substeps (algorithmic bytes)"}
     else:
         roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",
