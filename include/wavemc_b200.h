@@ -132,6 +132,7 @@ typedef struct {
                                  4 HBM-resident nested tiers; -1 plan only */
     int tiers;                /* nested LTS tiers in use */
     int n_r_tier[8];          /* |R_k| for tiers k = 1..tiers (n_r_tier[0] == n_r), rows [0, |R_k|) */
+    long n_structured;        /* sweep rows taking the structured 5-point path (0 before device setup) */
 } wmc_level_info;
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwavemc_b200.so")
+LIB_PATH = os.environ.get("WMC_LIB_PATH") or os.path.join(_HERE, "libwavemc_b200.so")  # override: tuning builds
 
 WMC_OK = 0
 WMC_CONFIG_ERROR = 2
@@ -44,7 +44,8 @@ class LevelInfo(C.Structure):
     _fields_ = [("n", C.c_int), ("n_r", C.c_int), ("n_p", C.c_int), ("p", C.c_int), ("n_steps", C.c_long),
                 ("dt", C.c_double), ("nnz", C.c_long), ("ap_nnz", C.c_long), ("n_recipes", C.c_long),
                 ("batch", C.c_int), ("dof_updates_per_solve", C.c_double), ("lattice", C.c_int),
-                ("substep_path", C.c_int), ("tiers", C.c_int), ("n_r_tier", C.c_int * 8)]
+                ("substep_path", C.c_int), ("tiers", C.c_int), ("n_r_tier", C.c_int * 8),
+                ("n_structured", C.c_long)]
 
 
 class Cost(C.Structure):

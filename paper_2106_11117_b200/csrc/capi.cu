@@ -104,7 +104,10 @@ struct wmc_level {
 
     // sweep operator
     int* d_row_ptr = nullptr;
-    short* d_row_cell = nullptr;
+    int4* d_row_desc = nullptr;
+    double2 row_types[wmc::kMaxRowTypes] = {};
+    int n_row_types = 0;
+    long n_structured = 0;
     int* d_ent = nullptr;
     double* d_a0 = nullptr;
     double* d_z0 = nullptr;
@@ -175,7 +178,7 @@ struct wmc_level {
 
     ~wmc_level() {
         cudaSetDevice(device);
-        for (void* p : {(void*)d_row_ptr, (void*)d_row_cell, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
+        for (void* p : {(void*)d_row_ptr, (void*)d_row_desc, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
                         (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
                         (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
@@ -219,14 +222,40 @@ void build_device_level(wmc_level& L) {
     for (std::size_t k = 0; k < ent.size(); ++k) ent[k] = t.col[k] | (t.cell[k] << wmc::kColBits);
     L.d_row_ptr = upload(t.row_ptr);
     {
-        std::vector<short> rc(t.n, -1);
+        // sweep row descriptors: single-cell rows, and among them the
+        // structured 5-point rows {i - dS, i - 1, i, i + 1, i + dN} whose
+        // (off-diagonal, diagonal) a0 pair is one of <= kMaxRowTypes values
+        std::vector<int4> desc(t.n);
+        std::vector<std::pair<double, double>> types;
         for (int i = 0; i < t.n; ++i) {
-            int c = t.cell[t.row_ptr[i]];
-            for (int k = t.row_ptr[i]; k < t.row_ptr[i + 1]; ++k)
+            const int b = t.row_ptr[i], e = t.row_ptr[i + 1];
+            int c = t.cell[b];
+            for (int k = b; k < e; ++k)
                 if (t.cell[k] != c) c = -1;
-            rc[i] = static_cast<short>(c);
+            desc[i] = make_int4(c, b, 0, 0);
+            if (c < 0 || e - b != 5 || std::getenv("WMC_SWEEP_GENERIC")) continue;
+            const int* col = t.col.data() + b;
+            const double* w = t.a0.data() + b;
+            if (col[1] != i - 1 || col[2] != i || col[3] != i + 1 || !(col[0] < i - 1) || !(col[4] > i + 1)) continue;
+            if (w[0] != w[1] || w[0] != w[3] || w[0] != w[4]) continue;
+            int type = -1;
+            for (std::size_t q = 0; q < types.size(); ++q)
+                if (types[q].first == w[0] && types[q].second == w[2]) type = static_cast<int>(q);
+            if (type < 0) {
+                if (static_cast<int>(types.size()) == wmc::kMaxRowTypes) continue;
+                type = static_cast<int>(types.size());
+                types.emplace_back(w[0], w[2]);
+            }
+            // deepest tier whose P holds all five columns: the substep
+            // kernels of tiers <= pfull take the structured gather too
+            int pfull = 255;
+            for (int q = 0; q < 5; ++q) pfull = std::min<int>(pfull, t.dof_tier[col[q]]);
+            desc[i] = make_int4(c | ((type + 1) << 16) | (pfull << 24), b, i - col[0], col[4] - i);
         }
-        L.d_row_cell = upload(rc);
+        L.n_row_types = static_cast<int>(types.size());
+        for (std::size_t q = 0; q < types.size(); ++q) L.row_types[q] = make_double2(types[q].first, types[q].second);
+        for (const auto& d : desc) L.n_structured += d.x >= 0 && ((d.x >> 16) & 0xff) > 0;
+        L.d_row_desc = upload(desc);
     }
     L.d_ent = upload(ent);
     L.d_a0 = upload(t.a0);
@@ -502,6 +531,8 @@ void run_tiers(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
     }
     a.beta = L.d_beta;
     a.cm = L.d_tier_cm;
+    a.row_desc = L.d_row_desc;
+    for (int q = 0; q < wmc::kMaxRowTypes; ++q) a.wtype[q] = L.row_types[q];
     a.zc = zc;
     a.zp = zp;
     a.step = step;
@@ -543,7 +574,8 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     sw.S = S;
     sw.count = count;
     sw.row_ptr = L.d_row_ptr;
-    sw.row_cell = L.d_row_cell;
+    sw.row_desc = L.d_row_desc;
+    for (int q = 0; q < wmc::kMaxRowTypes; ++q) sw.wtype[q] = L.row_types[q];
     sw.ent = L.d_ent;
     sw.a0 = L.d_a0;
     sw.cells = cells;
@@ -649,6 +681,8 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
             ga.cells = cells;
             ga.g = ws.g;
             ga.c0 = t.c0;
+            ga.row_desc = L.d_row_desc;
+            for (int q = 0; q < wmc::kMaxRowTypes; ++q) ga.wtype[q] = L.row_types[q];
             ga.zc = cur;
             ga.zp = prev;
             ga.step = static_cast<int>(s + 1);
@@ -1035,6 +1069,7 @@ void fill_info(const wmc::LevelTables& t, int batch, bool lattice, wmc_level_inf
     info->batch = batch;
     info->dof_updates_per_solve = wmc::dof_updates_per_solve(t);
     info->tiers = t.tiers;
+    info->n_structured = 0;
     for (int k = 0; k < 8; ++k) info->n_r_tier[k] = k < static_cast<int>(t.n_r_tier.size()) ? t.n_r_tier[k] : 0;
 }
 }  // namespace
@@ -1217,6 +1252,7 @@ int wmc_level_get_info(const wmc_level* L, wmc_level_info* info) {
     return guarded([&] {
         if (!L || !info) throw ConfigError("wmc_level_get_info: NULL argument");
         fill_info(L->tab, L->batch, L->lattice, info, static_cast<int>(L->path));
+        info->n_structured = L->n_structured;
     });
 }
 

@@ -279,9 +279,11 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
     L.n = static_cast<int>(L.dof_vertex.size());
     if (L.n == 0) throw std::invalid_argument("level: mesh has no interior vertices");
     L.in_p.assign(L.n, 0);
+    L.dof_tier.assign(L.n, 0);
     L.mass.resize(L.n);
     for (int i = 0; i < L.n; ++i) {
         L.in_p[i] = sel[L.dof_vertex[i]];
+        L.dof_tier[i] = tiers > 1 ? vt[L.dof_vertex[i]] : sel[L.dof_vertex[i]];
         L.n_p += L.in_p[i];
         L.mass[i] = mass[L.dof_vertex[i]];
     }

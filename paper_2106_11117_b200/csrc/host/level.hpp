@@ -74,6 +74,7 @@ struct LevelTables {
     int n_cells = 0;
     std::vector<int> dof_vertex;        // dof -> mesh vertex
     std::vector<std::uint8_t> in_p;     // per dof
+    std::vector<std::uint8_t> dof_tier; // per dof: deepest P_k holding it (0: none; single tier: in_p)
 
     // full operator, row-wise "parts": A_ij(omega) = sum over the row's
     // entries e with col[e] == j of c[cell[e]] * a0[e]; exact zeros dropped

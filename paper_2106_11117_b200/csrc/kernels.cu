@@ -115,7 +115,13 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
     const int s0 = grid_chunk(a.n) * kSweepChunk + 2 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
     if (row < a.n) {
-        const int b = __ldg(a.row_ptr + row), e = __ldg(a.row_ptr + row + 1);
+        const int4 d = a.row_desc ? __ldg(a.row_desc + row) : make_int4(-1, 0, 0, 0);
+        const bool structured = !kInit && !kParts && d.x >= 0 && ((d.x >> 16) & 0xff) > 0;
+        int b = 0, e = 0;
+        if (!structured) {
+            b = __ldg(a.row_ptr + row);
+            e = __ldg(a.row_ptr + row + 1);
+        }
         double acc0 = 0.0, acc1 = 0.0;
         double2 zself = make_double2(0.0, 0.0);
         // z_{n-1} of a leap-frog row issued before the gather (latency overlap)
@@ -152,10 +158,32 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             }
             acc0 += c.x * p0;
             acc1 += c.y * p1;
-        } else if (a.row_cell && __ldg(a.row_cell + row) >= 0) {
+        } else if (structured) {
+            // structured 5-point row: descriptor only
+            const double2 w = a.wtype[((d.x >> 16) & 0xff) - 1];
+            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + (d.x & 0xffff) * S + s0));
+            const double2 zs = __ldg(reinterpret_cast<const double2*>(a.zc + (row - d.z) * S + s0));
+            const double2 zw = __ldg(reinterpret_cast<const double2*>(a.zc + (row - 1) * S + s0));
+            zself = __ldg(reinterpret_cast<const double2*>(a.zc + row * S + s0));
+            const double2 ze = __ldg(reinterpret_cast<const double2*>(a.zc + (row + 1) * S + s0));
+            const double2 zn = __ldg(reinterpret_cast<const double2*>(a.zc + (row + d.w) * S + s0));
+            double p0 = 0.0, p1 = 0.0;
+            p0 += w.x * zs.x;
+            p1 += w.x * zs.y;
+            p0 += w.x * zw.x;
+            p1 += w.x * zw.y;
+            p0 += w.y * zself.x;
+            p1 += w.y * zself.y;
+            p0 += w.x * ze.x;
+            p1 += w.x * ze.y;
+            p0 += w.x * zn.x;
+            p1 += w.x * zn.y;
+            acc0 = c.x * p0;
+            acc1 = c.y * p1;
+        } else if (d.x >= 0) {
             // the row's elements all lie in one coefficient cell: one
             // coefficient load, A(omega)_ij = c * a0_ij
-            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + __ldg(a.row_cell + row) * S + s0));
+            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + (d.x & 0xffff) * S + s0));
             double p0 = 0.0, p1 = 0.0;
 #pragma unroll 4
             for (int k = b; k < e; ++k) {
@@ -237,6 +265,32 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
         dst[0] = g0;
 }
 
+// A(omega) P v on a structured row (descriptor d, all five columns in P):
+// c (w_off (v_S + v_W) + w_diag v_i + w_off (v_E + v_N)) summed in column order
+__device__ __forceinline__ double2 gather5(const int4 d, const double2* __restrict__ wtype,
+                                           const double* __restrict__ cells, const double* src, std::size_t S,
+                                           int row, int s0) {
+    const double2 w = wtype[((d.x >> 16) & 0xff) - 1];
+    const double2 c = __ldg(reinterpret_cast<const double2*>(cells + (d.x & 0xffff) * S + s0));
+    const double2 vs = *reinterpret_cast<const double2*>(src + (row - d.z) * S + s0);
+    const double2 vw = *reinterpret_cast<const double2*>(src + (row - 1) * S + s0);
+    const double2 vi = *reinterpret_cast<const double2*>(src + row * S + s0);
+    const double2 ve = *reinterpret_cast<const double2*>(src + (row + 1) * S + s0);
+    const double2 vn = *reinterpret_cast<const double2*>(src + (row + d.w) * S + s0);
+    double p0 = 0.0, p1 = 0.0;
+    p0 += w.x * vs.x;
+    p1 += w.x * vs.y;
+    p0 += w.x * vw.x;
+    p1 += w.x * vw.y;
+    p0 += w.y * vi.x;
+    p1 += w.y * vi.y;
+    p0 += w.x * ve.x;
+    p1 += w.x * ve.y;
+    p0 += w.x * vn.x;
+    p1 += w.x * vn.y;
+    return make_double2(c.x * p0, c.y * p1);
+}
+
 // K2 (HBM-resident): one substep over the R rows, warp per (row, 64
 // samples) as in the sweep; A(omega) P d gathered node-centrically from the
 // current d buffer, d_{m+1} written over d_{m-1} (own row only), the last
@@ -260,17 +314,24 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
         zm = *reinterpret_cast<const double2*>(a.zp + idx);
     }
     double acc0 = 0.0, acc1 = 0.0;
-    const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
+    const int4 d = a.row_desc ? __ldg(a.row_desc + row) : make_int4(-1, 0, 0, 0);
+    if (d.x >= 0 && (d.x >> 24) >= 1) {
+        const double2 acc = gather5(d, a.wtype, a.cells, src, S, row, s0);
+        acc0 = acc.x;
+        acc1 = acc.y;
+    } else {
+        const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
 #pragma unroll 4
-    for (int k = b; k < e; ++k) {
-        const int pk = __ldg(a.ent + k);
-        const double w = __ldg(a.a0 + k);
-        const int j = pk & kColMask;
-        const int cell = static_cast<unsigned>(pk) >> kColBits;
-        const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
-        const double2 v = *reinterpret_cast<const double2*>(src + j * S + s0);
-        acc0 += (c.x * w) * v.x;
-        acc1 += (c.y * w) * v.y;
+        for (int k = b; k < e; ++k) {
+            const int pk = __ldg(a.ent + k);
+            const double w = __ldg(a.a0 + k);
+            const int j = pk & kColMask;
+            const int cell = static_cast<unsigned>(pk) >> kColBits;
+            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+            const double2 v = *reinterpret_cast<const double2*>(src + j * S + s0);
+            acc0 += (c.x * w) * v.x;
+            acc1 += (c.y * w) * v.y;
+        }
     }
     acc0 *= scale;
     acc1 *= scale;
@@ -306,17 +367,24 @@ __global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(const __gr
     if (a.m > 0) {
         const double* src = a.e[a.k - 1][a.m & 1];
         double acc0 = 0.0, acc1 = 0.0;
-        const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
+        const int4 d = a.row_desc ? __ldg(a.row_desc + row) : make_int4(-1, 0, 0, 0);
+        if (d.x >= 0 && (d.x >> 24) >= a.k) {
+            const double2 acc = gather5(d, a.wtype, a.cells, src, S, row, s0);
+            acc0 = acc.x;
+            acc1 = acc.y;
+        } else {
+            const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
 #pragma unroll 4
-        for (int q = b; q < e; ++q) {
-            const int pk = __ldg(a.ent + q);
-            const double w = __ldg(a.a0 + q);
-            const int j = pk & kColMask;
-            const int cell = static_cast<unsigned>(pk) >> kColBits;
-            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
-            const double2 x = *reinterpret_cast<const double2*>(src + j * S + s0);
-            acc0 += (c.x * w) * x.x;
-            acc1 += (c.y * w) * x.y;
+            for (int q = b; q < e; ++q) {
+                const int pk = __ldg(a.ent + q);
+                const double w = __ldg(a.a0 + q);
+                const int j = pk & kColMask;
+                const int cell = static_cast<unsigned>(pk) >> kColBits;
+                const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+                const double2 x = *reinterpret_cast<const double2*>(src + j * S + s0);
+                acc0 += (c.x * w) * x.x;
+                acc1 += (c.y * w) * x.y;
+            }
         }
         v.x += acc0;
         v.y += acc1;

@@ -14,6 +14,8 @@
 
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 namespace wmc {
 
 // operator entries pack the column (23 bits) and the coefficient cell (9 bits)
@@ -28,6 +30,14 @@ constexpr int kSweepWarps = 8;   // rows per sweep block
 constexpr int kSubThreads = 1024;
 constexpr int kSubMaxRpt = 8;    // rows per thread in the substep kernel
 
+// Structured sweep rows: a row whose stored entries are exactly the 5-point
+// pattern {i - dS, i - 1, i, i + 1, i + dN} (column order), all in one
+// coefficient cell, with off-diagonal a0 == w.x and diagonal a0 == w.y of a
+// small per-level table, is swept from its descriptor alone (no per-entry
+// index or weight loads).  Same products in the same order as the generic
+// single-cell path: bit-identical results.
+constexpr int kMaxRowTypes = 8;
+
 struct SweepArgs {
     int n;           // rows
     int split;       // rows < split stash g (LTS); 0 for leapfrog
@@ -36,7 +46,12 @@ struct SweepArgs {
     const int* row_ptr;
     const int* ent;      // col | cell << kColBits
     const double* a0;
-    const short* row_cell;  // cell of a single-cell row, -1 otherwise (may be NULL)
+    // per row {info, row_ptr begin, dS, dN}; info = cell | type << 16 |
+    // pfull << 24 for a structured row (type >= 1; pfull = deepest tier whose
+    // P holds all five columns), cell for another single-cell row, -1 for a
+    // row spanning several cells (may be NULL: generic gather everywhere)
+    const int4* row_desc;
+    double2 wtype[kMaxRowTypes];  // (off-diagonal a0, diagonal a0) of type t + 1
     const double* cells;
     const double* z0;    // init only
     const double* zc;    // z_n
@@ -128,6 +143,8 @@ struct GSubArgs {
     int prev_mode;        // 0 buffer, 1 = -c0 g, 2 = zero
     double c0, beta, cm;
     int last;             // fuse z_{n+1} = 2 z_n - z_{n-1} + 2 d_p
+    const int4* row_desc;  // sweep descriptors: rows with pfull >= 1 gather structured
+    double2 wtype[kMaxRowTypes];
     const double* zc;
     double* zp;
     int step;
@@ -158,6 +175,8 @@ struct TierArgs {
     double c0[kMaxTiers], back[kMaxTiers];
     const double* beta;          // p - 1
     const double* cm;            // [tier][p - 1]
+    const int4* row_desc;        // sweep descriptors: rows with pfull >= k gather structured
+    double2 wtype[kMaxRowTypes];
     const double* zc;
     double* zp;
     int step;

@@ -22,13 +22,15 @@ def main():
     ap.add_argument("--nocheck", action="store_true", help="device-resident results, no instability check")
     ap.add_argument("--profile", action="store_true", help="per-kernel CUDA-event times of the last repeat")
     ap.add_argument("--p", type=int, default=0, help="override the number of substeps (timing studies)")
+    ap.add_argument("--config2", action="store_true", help="config-2 level (graded L-shape, nested tiers)")
     a = ap.parse_args()
-    d = configs.config1()[a.level]
+    d = (configs.config2() if a.config2 else configs.config1())[a.level]
     if a.square:
         nc, r = a.square
         d = configs.LevelDef(nc, r, 0.2 / nc, r, d.integrator)
     if a.steps:
-        d = configs.LevelDef(d.n_coarse, d.ratio, d.dt, d.substeps, d.integrator, final_time=a.steps * d.dt)
+        d = configs.LevelDef(d.n_coarse, d.ratio, d.dt, d.substeps, d.integrator, final_time=a.steps * d.dt,
+                             shape=d.shape, tiers=d.tiers)
     if a.p:
         d = configs.LevelDef(d.n_coarse, d.ratio, d.dt, a.p, d.integrator, final_time=d.final_time)
     m = configs.build_mesh(d)
