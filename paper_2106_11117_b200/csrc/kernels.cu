@@ -291,6 +291,129 @@ __device__ __forceinline__ double2 gather5(const int4 d, const double2* __restri
     return make_double2(c.x * p0, c.y * p1);
 }
 
+// K1 (step sweep, default): each warp sweeps R consecutive rows for its 64
+// samples, keeping the window z_{i-1}, z_i, z_{i+1} in registers, so a
+// structured row loads only z_{i+1}, z_{i-dS} and z_{i+dN} (3 of its 5
+// values) and reuses the coefficient of the previous row when the cell is
+// the same.  Generic rows gather as in sweep_kernel.  Products and sums in
+// the same order as sweep_kernel: bit-identical results.
+constexpr int kSweepRows = 4;
+
+template <int R>
+__global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs a) {
+    __shared__ double2 tile[kSweepWarps * R][32];  // g of the block's R rows: [row][lane]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int groups = (a.n + kSweepWarps * R - 1) / (kSweepWarps * R);
+    const int row0 = (blockIdx.x % groups) * kSweepWarps * R;
+    const int chunk = blockIdx.x / groups;
+    const int s0 = chunk * kSweepChunk + 2 * lane;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const int first = row0 + warp * R;
+    auto zrow = [&](int r) {
+        return __ldg(reinterpret_cast<const double2*>(a.zc + static_cast<std::size_t>(r) * S + s0));
+    };
+    double2 zprev = make_double2(0.0, 0.0), zcur = zprev;
+    if (first < a.n) {
+        if (first > 0) zprev = zrow(first - 1);
+        zcur = zrow(first);
+    }
+    int ccell = -1;
+    double2 c = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int k = 0; k < R; ++k) {
+        const int row = first + k;
+        if (row >= a.n) break;
+        const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
+        double2 zm = make_double2(0.0, 0.0);
+        if (row >= a.split) zm = *reinterpret_cast<const double2*>(a.zp + idx);
+        const double2 znext = row + 1 < a.n ? zrow(row + 1) : make_double2(0.0, 0.0);
+        const int4 d = __ldg(a.row_desc + row);
+        double acc0 = 0.0, acc1 = 0.0;
+        if (d.x >= 0 && ((d.x >> 16) & 0xff) > 0) {
+            const double2 w = a.wtype[((d.x >> 16) & 0xff) - 1];
+            if ((d.x & 0xffff) != ccell) {
+                ccell = d.x & 0xffff;
+                c = __ldg(reinterpret_cast<const double2*>(a.cells + ccell * S + s0));
+            }
+            const double2 zs = zrow(row - d.z);
+            const double2 zn = zrow(row + d.w);
+            double p0 = 0.0, p1 = 0.0;
+            p0 += w.x * zs.x;
+            p1 += w.x * zs.y;
+            p0 += w.x * zprev.x;
+            p1 += w.x * zprev.y;
+            p0 += w.y * zcur.x;
+            p1 += w.y * zcur.y;
+            p0 += w.x * znext.x;
+            p1 += w.x * znext.y;
+            p0 += w.x * zn.x;
+            p1 += w.x * zn.y;
+            acc0 = c.x * p0;
+            acc1 = c.y * p1;
+        } else {
+            const int b = d.y, e = __ldg(a.row_ptr + row + 1);
+            if (d.x >= 0) {
+                const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + (d.x & 0xffff) * S + s0));
+                double p0 = 0.0, p1 = 0.0;
+#pragma unroll 4
+                for (int q = b; q < e; ++q) {
+                    const int j = __ldg(a.ent + q) & kColMask;
+                    const double w = __ldg(a.a0 + q);
+                    const double2 z = zrow(j);
+                    p0 += w * z.x;
+                    p1 += w * z.y;
+                }
+                acc0 = cc.x * p0;
+                acc1 = cc.y * p1;
+            } else {
+#pragma unroll 4
+                for (int q = b; q < e; ++q) {
+                    const int pk = __ldg(a.ent + q);
+                    const double w = __ldg(a.a0 + q);
+                    const int j = pk & kColMask;
+                    const int cell = static_cast<unsigned>(pk) >> kColBits;
+                    const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+                    const double2 z = zrow(j);
+                    acc0 += (cc.x * w) * z.x;
+                    acc1 += (cc.y * w) * z.y;
+                }
+            }
+        }
+        if (row < a.split) {
+            if (a.g_node_major)
+                *reinterpret_cast<double2*>(a.g + idx) = make_double2(acc0, acc1);
+            else
+                tile[warp * R + k][lane] = make_double2(acc0, acc1);
+        } else {
+            double2 out;
+            out.x = 2.0 * zcur.x - zm.x - a.factor * acc0;
+            out.y = 2.0 * zcur.y - zm.y - a.factor * acc1;
+            *reinterpret_cast<double2*>(a.zp + idx) = out;
+            if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
+            if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+        }
+        zprev = zcur;
+        zcur = znext;
+    }
+    if (row0 >= a.split || a.g_node_major) return;  // block-uniform
+    // the block's g rows sample-major: thread -> sample tid / 4, 8 rows each
+    __syncthreads();
+    constexpr int kRowsPerThread = kSweepWarps * R * kSweepChunk / (kSweepWarps * 32);
+    const int sl = threadIdx.x / (kSweepWarps * R / kRowsPerThread);
+    const int r0 = (threadIdx.x % (kSweepWarps * R / kRowsPerThread)) * kRowsPerThread;
+    const int s = chunk * kSweepChunk + sl;
+    double* dst = a.g + static_cast<std::size_t>(s) * a.g_stride + row0 + r0;
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; q += 2) {
+        const double2 t0 = tile[r0 + q][sl >> 1], t1 = tile[r0 + q + 1][sl >> 1];
+        const double g0 = (sl & 1) ? t0.y : t0.x, g1 = (sl & 1) ? t1.y : t1.x;
+        if (row0 + r0 + q + 1 < a.split)
+            *reinterpret_cast<double2*>(dst + q) = make_double2(g0, g1);
+        else if (row0 + r0 + q < a.split)
+            dst[q] = g0;
+    }
+}
+
 // K2 (HBM-resident): one substep over the R rows, warp per (row, 64
 // samples) as in the sweep; A(omega) P d gathered node-centrically from the
 // current d buffer, d_{m+1} written over d_{m-1} (own row only), the last
@@ -959,10 +1082,19 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
         const char* v = std::getenv("WMC_SWEEP_PARTS");  // tuning knob
         return v ? std::atoi(v) : 0;
     }();
-    if (parts)
+    static const int one_row = [] {
+        const char* v = std::getenv("WMC_SWEEP_ONE_ROW");  // tuning knob: one row per warp
+        return v ? std::atoi(v) : 0;
+    }();
+    if (parts) {
         sweep_kernel<false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
-    else
+    } else if (one_row || !a.row_desc) {
         sweep_kernel<false, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    } else {
+        const int rows = kSweepWarps * kSweepRows;
+        const unsigned g2 = ((a.n + rows - 1) / rows) * (a.S / kSweepChunk);
+        sweep_rows_kernel<kSweepRows><<<g2, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    }
 }
 
 int substep_smem_bytes(const SubArgs& a) { return static_cast<int>(sub_layout(a, nullptr, nullptr)); }
