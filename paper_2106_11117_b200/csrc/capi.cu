@@ -105,6 +105,7 @@ struct wmc_level {
     // sweep operator
     int* d_row_ptr = nullptr;
     int4* d_row_desc = nullptr;
+    double2* d_wtype = nullptr;
     double2 row_types[wmc::kMaxRowTypes] = {};
     int n_row_types = 0;
     long n_structured = 0;
@@ -178,7 +179,7 @@ struct wmc_level {
 
     ~wmc_level() {
         cudaSetDevice(device);
-        for (void* p : {(void*)d_row_ptr, (void*)d_row_desc, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
+        for (void* p : {(void*)d_row_ptr, (void*)d_row_desc, (void*)d_wtype, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
                         (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
                         (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
@@ -256,6 +257,7 @@ void build_device_level(wmc_level& L) {
         for (std::size_t q = 0; q < types.size(); ++q) L.row_types[q] = make_double2(types[q].first, types[q].second);
         for (const auto& d : desc) L.n_structured += d.x >= 0 && ((d.x >> 16) & 0xff) > 0;
         L.d_row_desc = upload(desc);
+        L.d_wtype = upload(std::vector<double2>(L.row_types, L.row_types + wmc::kMaxRowTypes));
     }
     L.d_ent = upload(ent);
     L.d_a0 = upload(t.a0);
@@ -523,38 +525,62 @@ void run_tiers(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
     a.S = S;
     a.count = count;
     a.cells = cells;
-    for (int k = 0; k < K; ++k) {
-        a.e[k][0] = ws.tier_e[2 * k];
-        a.e[k][1] = ws.tier_e[2 * k + 1];
-        a.c0[k] = t.tier_c0[k];
-        a.back[k] = t.tier_back[k];
-    }
-    a.beta = L.d_beta;
-    a.cm = L.d_tier_cm;
     a.row_desc = L.d_row_desc;
-    for (int q = 0; q < wmc::kMaxRowTypes; ++q) a.wtype[q] = L.row_types[q];
+    a.wtype = L.d_wtype;
     a.zc = zc;
     a.zp = zp;
     a.step = step;
     a.fail = ws.fail;
+    std::vector<int> stage(K + 1, 0);
+    auto buf = [&](int j, int m) { return ws.tier_e[2 * (j - 1) + (m & 1)]; };
     auto run = [&](auto&& self, int k, const double* rhs) -> void {
         const int n_rk = t.n_r_tier[k - 1];
         const int split = k < K ? t.n_r_tier[k] : 0;
         for (int m = 0; m < p; ++m) {
+            stage[k] = m;
             a.k = k;
             a.m = m;
-            a.stage[k - 1] = m;
             a.rhs = rhs;
             a.rhs_next = k < K ? ws.tier_rhs[k] : nullptr;
+            a.src = m > 0 ? buf(k, m) : nullptr;
             a.ptr = L.d_tier_ptr[k - 1];
             a.ent = L.d_tier_ent[k - 1];
             a.a0 = L.d_tier_a0[k - 1];
             a.row_begin = m == 0 ? split : 0;
             a.row_end = n_rk;
             a.split = split;
+            // the update chain of a row finishing at tier k stage m
+            a.depth = 0;
+            for (int j = k; j >= 1; --j) {
+                const int mj = stage[j];
+                auto& ln = a.link[a.depth++];
+                ln = {};
+                if (mj == 0) {
+                    ln.C = t.tier_c0[j - 1];
+                } else {
+                    ln.A = 1.0 + t.beta[mj - 1];
+                    ln.B = t.beta[mj - 1];
+                    ln.C = t.tier_cm[j - 1][mj - 1];
+                    ln.em = buf(j, mj);
+                    ln.emm = mj >= 2 ? buf(j, mj + 1) : nullptr;
+                }
+                if (mj + 1 < p) {
+                    ln.out = buf(j, mj + 1);
+                    break;
+                }
+                if (j == 1) break;  // out == NULL: z_{n+1}
+                ln.back = t.tier_back[j - 1];
+            }
             if (a.row_end > a.row_begin) {
                 wmc::launch_tier_stage(a, stream);
                 ++g_launches;
+                static const bool sync_debug = std::getenv("WMC_SYNC_DEBUG") != nullptr;  // debugging aid
+                if (sync_debug) {
+                    const cudaError_t e = cudaStreamSynchronize(stream);
+                    if (e != cudaSuccess)
+                        throw DeviceError(std::string("tier stage k=") + std::to_string(k) + " m=" + std::to_string(m) +
+                                          ": " + cudaGetErrorString(e));
+                }
             }
             if (split > 0) self(self, k + 1, m == 0 ? rhs : ws.tier_rhs[k]);
         }
@@ -575,7 +601,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     sw.count = count;
     sw.row_ptr = L.d_row_ptr;
     sw.row_desc = L.d_row_desc;
-    for (int q = 0; q < wmc::kMaxRowTypes; ++q) sw.wtype[q] = L.row_types[q];
+    sw.wtype = L.d_wtype;
     sw.ent = L.d_ent;
     sw.a0 = L.d_a0;
     sw.cells = cells;
@@ -663,6 +689,10 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         sw.step = static_cast<int>(s + 1);
         if (L.profile) mark(L, L.ev_sweep, stream);
         wmc::launch_sweep_step(sw, stream);
+        if (std::getenv("WMC_SYNC_DEBUG")) {
+            const cudaError_t e = cudaStreamSynchronize(stream);
+            if (e != cudaSuccess) throw DeviceError(std::string("sweep: ") + cudaGetErrorString(e));
+        }
         if (L.profile) mark(L, L.ev_sweep, stream);
         ++g_launches;
         if (tiers) {
@@ -682,7 +712,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
             ga.g = ws.g;
             ga.c0 = t.c0;
             ga.row_desc = L.d_row_desc;
-            for (int q = 0; q < wmc::kMaxRowTypes; ++q) ga.wtype[q] = L.row_types[q];
+            ga.wtype = L.d_wtype;
             ga.zc = cur;
             ga.zp = prev;
             ga.step = static_cast<int>(s + 1);

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             acc1 += c.y * p1;
         } else if (structured) {
             // structured 5-point row: descriptor only
-            const double2 w = a.wtype[((d.x >> 16) & 0xff) - 1];
+            const double2 w = __ldg(a.wtype + ((d.x >> 16) & 0xff) - 1);
             const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + (d.x & 0xffff) * S + s0));
             const double2 zs = __ldg(reinterpret_cast<const double2*>(a.zc + (row - d.z) * S + s0));
             const double2 zw = __ldg(reinterpret_cast<const double2*>(a.zc + (row - 1) * S + s0));
@@ -265,32 +265,6 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
         dst[0] = g0;
 }
 
-// A(omega) P v on a structured row (descriptor d, all five columns in P):
-// c (w_off (v_S + v_W) + w_diag v_i + w_off (v_E + v_N)) summed in column order
-__device__ __forceinline__ double2 gather5(const int4 d, const double2* __restrict__ wtype,
-                                           const double* __restrict__ cells, const double* src, std::size_t S,
-                                           int row, int s0) {
-    const double2 w = wtype[((d.x >> 16) & 0xff) - 1];
-    const double2 c = __ldg(reinterpret_cast<const double2*>(cells + (d.x & 0xffff) * S + s0));
-    const double2 vs = *reinterpret_cast<const double2*>(src + (row - d.z) * S + s0);
-    const double2 vw = *reinterpret_cast<const double2*>(src + (row - 1) * S + s0);
-    const double2 vi = *reinterpret_cast<const double2*>(src + row * S + s0);
-    const double2 ve = *reinterpret_cast<const double2*>(src + (row + 1) * S + s0);
-    const double2 vn = *reinterpret_cast<const double2*>(src + (row + d.w) * S + s0);
-    double p0 = 0.0, p1 = 0.0;
-    p0 += w.x * vs.x;
-    p1 += w.x * vs.y;
-    p0 += w.x * vw.x;
-    p1 += w.x * vw.y;
-    p0 += w.y * vi.x;
-    p1 += w.y * vi.y;
-    p0 += w.x * ve.x;
-    p1 += w.x * ve.y;
-    p0 += w.x * vn.x;
-    p1 += w.x * vn.y;
-    return make_double2(c.x * p0, c.y * p1);
-}
-
 // K1 (step sweep, default): each warp sweeps R consecutive rows for its 64
 // samples, keeping the window z_{i-1}, z_i, z_{i+1} in registers, so a
 // structured row loads only z_{i+1}, z_{i-dS} and z_{i+dN} (3 of its 5
@@ -298,6 +272,10 @@ __device__ __forceinline__ double2 gather5(const int4 d, const double2* __restri
 // the same.  Generic rows gather as in sweep_kernel.  Products and sums in
 // the same order as sweep_kernel: bit-identical results.
 constexpr int kSweepRows = 4;
+#ifndef WMC_TIER_ROWS
+#define WMC_TIER_ROWS 1
+#endif
+constexpr int kTierRows = WMC_TIER_ROWS;
 
 template <int R>
 __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs a) {
@@ -319,7 +297,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
     }
     int ccell = -1;
     double2 c = make_double2(0.0, 0.0);
-#pragma unroll 1
+#pragma unroll
     for (int k = 0; k < R; ++k) {
         const int row = first + k;
         if (row >= a.n) break;
@@ -330,7 +308,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
         const int4 d = __ldg(a.row_desc + row);
         double acc0 = 0.0, acc1 = 0.0;
         if (d.x >= 0 && ((d.x >> 16) & 0xff) > 0) {
-            const double2 w = a.wtype[((d.x >> 16) & 0xff) - 1];
+            const double2 w = __ldg(a.wtype + ((d.x >> 16) & 0xff) - 1);
             if ((d.x & 0xffff) != ccell) {
                 ccell = d.x & 0xffff;
                 c = __ldg(reinterpret_cast<const double2*>(a.cells + ccell * S + s0));
@@ -418,83 +396,60 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
 // samples) as in the sweep; A(omega) P d gathered node-centrically from the
 // current d buffer, d_{m+1} written over d_{m-1} (own row only), the last
 // substep forms z_{n+1} directly (reference src/integrators.cpp:137-153).
+template <int R>
 __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int row = grid_rowgroup(a.n_r) * kSweepWarps + (threadIdx.x >> 5);
-    if (row >= a.n_r) return;
-    const int s0 = grid_chunk(a.n_r) * kSweepChunk + 2 * lane;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int groups = (a.n_r + kSweepWarps * R - 1) / (kSweepWarps * R);
+    const int first = (blockIdx.x % groups) * kSweepWarps * R + warp * R;
+    if (first >= a.n_r) return;
+    const int s0 = (blockIdx.x / groups) * kSweepChunk + 2 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
     const double* src = a.cur_mode == 0 ? a.dcur : a.g;
     const double scale = a.cur_mode == 0 ? 1.0 : -a.c0;
-    // the row's own values first, so their latency overlaps the gather
-    const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
-    const double2 g = __ldg(reinterpret_cast<const double2*>(a.g + idx));
-    double2 dm = make_double2(0.0, 0.0), dmm = make_double2(0.0, 0.0), zn = dm, zm = dm;
-    if (a.cur_mode == 0) dm = *reinterpret_cast<const double2*>(a.dcur + idx);
-    if (a.prev_mode == 0) dmm = *reinterpret_cast<const double2*>(a.dprev + idx);
-    if (a.last) {
-        zn = *reinterpret_cast<const double2*>(a.zc + idx);
-        zm = *reinterpret_cast<const double2*>(a.zp + idx);
-    }
-    double acc0 = 0.0, acc1 = 0.0;
-    const int4 d = a.row_desc ? __ldg(a.row_desc + row) : make_int4(-1, 0, 0, 0);
-    if (d.x >= 0 && (d.x >> 24) >= 1) {
-        const double2 acc = gather5(d, a.wtype, a.cells, src, S, row, s0);
-        acc0 = acc.x;
-        acc1 = acc.y;
-    } else {
-        const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
-#pragma unroll 4
-        for (int k = b; k < e; ++k) {
-            const int pk = __ldg(a.ent + k);
-            const double w = __ldg(a.a0 + k);
-            const int j = pk & kColMask;
-            const int cell = static_cast<unsigned>(pk) >> kColBits;
-            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
-            const double2 v = *reinterpret_cast<const double2*>(src + j * S + s0);
-            acc0 += (c.x * w) * v.x;
-            acc1 += (c.y * w) * v.y;
+    auto ld = [&](const double* p, int r) {
+        return *reinterpret_cast<const double2*>(p + static_cast<std::size_t>(r) * S + s0);
+    };
+    // window src[i-1], src[i], src[i+1] over the warp's consecutive rows
+    double2 vprev = first > 0 ? ld(src, first - 1) : make_double2(0.0, 0.0);
+    double2 vcur = ld(src, first);
+    int ccell = -1;
+    double2 c = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int row = first + k;
+        if (row >= a.n_r) break;
+        const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
+        const double2 g = __ldg(reinterpret_cast<const double2*>(a.g + idx));
+        double2 dm = make_double2(0.0, 0.0), dmm = make_double2(0.0, 0.0), zn = dm, zm = dm;
+        if (a.cur_mode == 0) dm = vcur;
+        if (a.prev_mode == 0) dmm = *reinterpret_cast<const double2*>(a.dprev + idx);
+        if (a.last) {
+            zn = *reinterpret_cast<const double2*>(a.zc + idx);
+            zm = *reinterpret_cast<const double2*>(a.zp + idx);
         }
-    }
-    acc0 *= scale;
-    acc1 *= scale;
-    if (a.cur_mode != 0) dm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
-    if (a.prev_mode == 1) dmm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
-    double2 next;
-    next.x = (1.0 + a.beta) * dm.x - a.beta * dmm.x - a.cm * (g.x + acc0);
-    next.y = (1.0 + a.beta) * dm.y - a.beta * dmm.y - a.cm * (g.y + acc1);
-    if (!a.last) {
-        *reinterpret_cast<double2*>(a.dprev + idx) = next;
-        return;
-    }
-    double2 out;
-    out.x = 2.0 * zn.x - zm.x + 2.0 * next.x;
-    out.y = 2.0 * zn.y - zm.y + 2.0 * next.y;
-    *reinterpret_cast<double2*>(a.zp + idx) = out;
-    if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
-    if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
-}
-
-// Nested-tier stage (see TierArgs): the single-tier recursion of reference
-// src/integrators.cpp:117-157 applied per tier, with the stage's right-hand
-// side on R_k+1 replaced by the tier-(k+1) solve over the stage interval.
-__global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(const __grid_constant__ TierArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int nrows = a.row_end - a.row_begin;
-    const int row = a.row_begin + grid_rowgroup(nrows) * kSweepWarps + (threadIdx.x >> 5);
-    if (row >= a.row_end) return;
-    const int s0 = grid_chunk(nrows) * kSweepChunk + 2 * lane;
-    const std::size_t S = static_cast<std::size_t>(a.S);
-    const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
-    double2 v = __ldg(reinterpret_cast<const double2*>(a.rhs + idx));
-    if (a.m > 0) {
-        const double* src = a.e[a.k - 1][a.m & 1];
+        const double2 vnext = row + 1 < a.n_r ? ld(src, row + 1) : make_double2(0.0, 0.0);
         double acc0 = 0.0, acc1 = 0.0;
-        const int4 d = a.row_desc ? __ldg(a.row_desc + row) : make_int4(-1, 0, 0, 0);
-        if (d.x >= 0 && (d.x >> 24) >= a.k) {
-            const double2 acc = gather5(d, a.wtype, a.cells, src, S, row, s0);
-            acc0 = acc.x;
-            acc1 = acc.y;
+        const int4 d = __ldg(a.row_desc + row);
+        if (d.x >= 0 && (d.x >> 24) >= 1) {
+            const double2 w = __ldg(a.wtype + ((d.x >> 16) & 0xff) - 1);
+            if ((d.x & 0xffff) != ccell) {
+                ccell = d.x & 0xffff;
+                c = __ldg(reinterpret_cast<const double2*>(a.cells + ccell * S + s0));
+            }
+            const double2 vs = ld(src, row - d.z), vn = ld(src, row + d.w);
+            double p0 = 0.0, p1 = 0.0;
+            p0 += w.x * vs.x;
+            p1 += w.x * vs.y;
+            p0 += w.x * vprev.x;
+            p1 += w.x * vprev.y;
+            p0 += w.y * vcur.x;
+            p1 += w.y * vcur.y;
+            p0 += w.x * vnext.x;
+            p1 += w.x * vnext.y;
+            p0 += w.x * vn.x;
+            p1 += w.x * vn.y;
+            acc0 = c.x * p0;
+            acc1 = c.y * p1;
         } else {
             const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
 #pragma unroll 4
@@ -503,49 +458,145 @@ __global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(const __gr
                 const double w = __ldg(a.a0 + q);
                 const int j = pk & kColMask;
                 const int cell = static_cast<unsigned>(pk) >> kColBits;
-                const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
-                const double2 x = *reinterpret_cast<const double2*>(src + j * S + s0);
-                acc0 += (c.x * w) * x.x;
-                acc1 += (c.y * w) * x.y;
+                const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+                const double2 v = ld(src, j);
+                acc0 += (cc.x * w) * v.x;
+                acc1 += (cc.y * w) * v.y;
             }
         }
-        v.x += acc0;
-        v.y += acc1;
-    }
-    if (row < a.split) {
-        *reinterpret_cast<double2*>(a.rhs_next + idx) = v;
-        return;
-    }
-    // the tier's update, then up through the ancestors whose stage ends here
-    for (int j = a.k;; --j) {
-        const int mj = a.stage[j - 1];
-        double2 en;
-        if (mj == 0) {
-            en = make_double2(-a.c0[j - 1] * v.x, -a.c0[j - 1] * v.y);
+        acc0 *= scale;
+        acc1 *= scale;
+        if (a.cur_mode != 0) dm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
+        if (a.prev_mode == 1) dmm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
+        double2 next;
+        next.x = (1.0 + a.beta) * dm.x - a.beta * dmm.x - a.cm * (g.x + acc0);
+        next.y = (1.0 + a.beta) * dm.y - a.beta * dmm.y - a.cm * (g.y + acc1);
+        if (!a.last) {
+            *reinterpret_cast<double2*>(a.dprev + idx) = next;
         } else {
-            const double beta = a.beta[mj - 1], cm = a.cm[(j - 1) * (a.p - 1) + mj - 1];
-            const double2 em = *reinterpret_cast<const double2*>(a.e[j - 1][mj & 1] + idx);
-            double2 emm = make_double2(0.0, 0.0);
-            if (mj >= 2) emm = *reinterpret_cast<const double2*>(a.e[j - 1][(mj + 1) & 1] + idx);
-            en.x = (1.0 + beta) * em.x - beta * emm.x - cm * v.x;
-            en.y = (1.0 + beta) * em.y - beta * emm.y - cm * v.y;
-        }
-        if (mj + 1 < a.p) {
-            *reinterpret_cast<double2*>(a.e[j - 1][(mj + 1) & 1] + idx) = en;
-            return;
-        }
-        if (j == 1) {
-            const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
-            const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
             double2 out;
-            out.x = 2.0 * zn.x - zm.x + 2.0 * en.x;
-            out.y = 2.0 * zn.y - zm.y + 2.0 * en.y;
+            out.x = 2.0 * zn.x - zm.x + 2.0 * next.x;
+            out.y = 2.0 * zn.y - zm.y + 2.0 * next.y;
             *reinterpret_cast<double2*>(a.zp + idx) = out;
             if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
             if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
-            return;
         }
-        v = make_double2(a.back[j - 1] * en.x, a.back[j - 1] * en.y);
+        vprev = vcur;
+        vcur = vnext;
+    }
+}
+
+// Nested-tier stage (see TierArgs): the single-tier recursion of reference
+// src/integrators.cpp:117-157 applied per tier, with the stage's right-hand
+// side on R_k+1 replaced by the tier-(k+1) solve over the stage interval.
+template <int R>
+__global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(TierArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nrows = a.row_end - a.row_begin;
+    const int groups = (nrows + kSweepWarps * R - 1) / (kSweepWarps * R);
+    const int first = a.row_begin + (blockIdx.x % groups) * kSweepWarps * R + warp * R;
+    if (first >= a.row_end) return;
+    const int s0 = (blockIdx.x / groups) * kSweepChunk + 2 * lane;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const double* src = a.src;
+    auto ld = [&](const double* p, int r) {
+        return *reinterpret_cast<const double2*>(p + static_cast<std::size_t>(r) * S + s0);
+    };
+    // window E_m[i-1], E_m[i], E_m[i+1] over the warp's consecutive rows
+    double2 vprev = make_double2(0.0, 0.0), vcur = vprev;
+    if (a.m > 0) {
+        if (first > 0) vprev = ld(src, first - 1);
+        vcur = ld(src, first);
+    }
+    int ccell = -1;
+    double2 c = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const int row = first + q;
+        if (row >= a.row_end) break;
+        const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
+        double2 v = __ldg(reinterpret_cast<const double2*>(a.rhs + idx));
+        double2 vnext = make_double2(0.0, 0.0);
+        if (a.m > 0) {
+            if (row + 1 < a.row_end) vnext = ld(src, row + 1);
+            double acc0 = 0.0, acc1 = 0.0;
+            const int4 d = __ldg(a.row_desc + row);
+            if (d.x >= 0 && (d.x >> 24) >= a.k) {
+                const double2 w = __ldg(a.wtype + ((d.x >> 16) & 0xff) - 1);
+                if ((d.x & 0xffff) != ccell) {
+                    ccell = d.x & 0xffff;
+                    c = __ldg(reinterpret_cast<const double2*>(a.cells + ccell * S + s0));
+                }
+                const double2 vs = ld(src, row - d.z), vn = ld(src, row + d.w);
+                double p0 = 0.0, p1 = 0.0;
+                p0 += w.x * vs.x;
+                p1 += w.x * vs.y;
+                p0 += w.x * vprev.x;
+                p1 += w.x * vprev.y;
+                p0 += w.y * vcur.x;
+                p1 += w.y * vcur.y;
+                p0 += w.x * vnext.x;
+                p1 += w.x * vnext.y;
+                p0 += w.x * vn.x;
+                p1 += w.x * vn.y;
+                acc0 = c.x * p0;
+                acc1 = c.y * p1;
+            } else {
+                const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
+#pragma unroll 4
+                for (int t = b; t < e; ++t) {
+                    const int pk = __ldg(a.ent + t);
+                    const double w = __ldg(a.a0 + t);
+                    const int j = pk & kColMask;
+                    const int cell = static_cast<unsigned>(pk) >> kColBits;
+                    const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+                    const double2 x = ld(src, j);
+                    acc0 += (cc.x * w) * x.x;
+                    acc1 += (cc.y * w) * x.y;
+                }
+            }
+            v.x += acc0;
+            v.y += acc1;
+        }
+        const double2 em_row = vcur;  // E^k_m of this row (m > 0)
+        vprev = vcur;
+        vcur = vnext;
+        if (row < a.split) {
+            *reinterpret_cast<double2*>(a.rhs_next + idx) = v;
+            continue;
+        }
+        // the tier's update, then up through the ancestors whose stage ends here
+#pragma unroll
+        for (int t = 0; t < kMaxTiers; ++t) {
+            if (t >= a.depth) break;
+            const auto& L = a.link[t];
+            double2 em = make_double2(0.0, 0.0), emm = em;
+            if (t == 0) {
+                em = em_row;
+            } else if (L.em) {
+                em = *reinterpret_cast<const double2*>(L.em + idx);
+            }
+            if (L.emm) emm = *reinterpret_cast<const double2*>(L.emm + idx);
+            double2 en;
+            en.x = L.A * em.x - L.B * emm.x - L.C * v.x;
+            en.y = L.A * em.y - L.B * emm.y - L.C * v.y;
+            if (t + 1 < a.depth) {
+                v = make_double2(L.back * en.x, L.back * en.y);
+                continue;
+            }
+            if (L.out) {
+                *reinterpret_cast<double2*>(L.out + idx) = en;
+            } else {
+                const double2 zn = *reinterpret_cast<const double2*>(a.zc + idx);
+                const double2 zm = *reinterpret_cast<const double2*>(a.zp + idx);
+                double2 out;
+                out.x = 2.0 * zn.x - zm.x + 2.0 * en.x;
+                out.y = 2.0 * zn.y - zm.y + 2.0 * en.y;
+                *reinterpret_cast<double2*>(a.zp + idx) = out;
+                if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
+                if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+            }
+        }
     }
 }
 
@@ -1091,9 +1142,19 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
     } else if (one_row || !a.row_desc) {
         sweep_kernel<false, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     } else {
-        const int rows = kSweepWarps * kSweepRows;
+        static const int r = [] {
+            const char* v = std::getenv("WMC_SWEEP_ROWS");  // tuning knob: rows per warp (2, 4, 8)
+            return v ? std::atoi(v) : kSweepRows;
+        }();
+        const int rows = kSweepWarps * r;
         const unsigned g2 = ((a.n + rows - 1) / rows) * (a.S / kSweepChunk);
-        sweep_rows_kernel<kSweepRows><<<g2, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (r == 2)
+            sweep_rows_kernel<2><<<g2, kSweepWarps * 32, 0, st>>>(a);
+        else if (r == 8)
+            sweep_rows_kernel<8><<<g2, kSweepWarps * 32, 0, st>>>(a);
+        else
+            sweep_rows_kernel<4><<<g2, kSweepWarps * 32, 0, st>>>(a);
     }
 }
 
@@ -1158,15 +1219,17 @@ int substep_max_grid(int device, int smem_bytes) {
 }
 
 void launch_global_substep(const GSubArgs& a, void* stream) {
-    const unsigned grid = ((a.n_r + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
-    global_substep_kernel<<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    const int rows = kSweepWarps * kSweepRows;
+    const unsigned grid = ((a.n_r + rows - 1) / rows) * (a.S / kSweepChunk);
+    global_substep_kernel<kSweepRows><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_tier_stage(const TierArgs& a, void* stream) {
     const int rows = a.row_end - a.row_begin;
     if (rows <= 0) return;
-    const unsigned grid = ((rows + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
-    tier_stage_kernel<<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    const int per = kSweepWarps * kTierRows;
+    const unsigned grid = ((rows + per - 1) / per) * (a.S / kSweepChunk);
+    tier_stage_kernel<kTierRows><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_r_update(const RUpdateArgs& a, void* stream) {

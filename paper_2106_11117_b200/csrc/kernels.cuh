@@ -51,7 +51,7 @@ struct SweepArgs {
     // P holds all five columns), cell for another single-cell row, -1 for a
     // row spanning several cells (may be NULL: generic gather everywhere)
     const int4* row_desc;
-    double2 wtype[kMaxRowTypes];  // (off-diagonal a0, diagonal a0) of type t + 1
+    const double2* wtype;  // [kMaxRowTypes]: (off-diagonal a0, diagonal a0) of type t + 1 (device table)
     const double* cells;
     const double* z0;    // init only
     const double* zc;    // z_n
@@ -144,7 +144,7 @@ struct GSubArgs {
     double c0, beta, cm;
     int last;             // fuse z_{n+1} = 2 z_n - z_{n-1} + 2 d_p
     const int4* row_desc;  // sweep descriptors: rows with pfull >= 1 gather structured
-    double2 wtype[kMaxRowTypes];
+    const double2* wtype;  // device table, see SweepArgs
     const double* zc;
     double* zp;
     int step;
@@ -170,13 +170,21 @@ struct TierArgs {
     const double* cells;
     const double* rhs;           // r_k [row][S]
     double* rhs_next;            // r_k+1 [row][S] (rows < split)
-    double* e[kMaxTiers][2];
-    int stage[kMaxTiers];        // current stage of tiers 1..k
-    double c0[kMaxTiers], back[kMaxTiers];
-    const double* beta;          // p - 1
-    const double* cm;            // [tier][p - 1]
+    const double* src;           // E^k_m (gathered, m >= 1)
+    // the row update and its carry through the ancestors whose stage ends
+    // with this one, fixed per launch: link t (tier k - t) forms
+    // en = A E_m - B E_{m-1} - C v (E_m of link 0 from the gather window),
+    // then either stores en to out, or (out == NULL, tier 1 ending) forms
+    // z_{n+1}, or passes v = back en to link t + 1
+    int depth;
+    struct Link {
+        const double* em;        // NULL: E_m == 0 (stage 0)
+        const double* emm;       // NULL: E_{m-1} == 0 (stages 0, 1)
+        double* out;
+        double A, B, C, back;
+    } link[kMaxTiers];
     const int4* row_desc;        // sweep descriptors: rows with pfull >= k gather structured
-    double2 wtype[kMaxRowTypes];
+    const double2* wtype;  // device table, see SweepArgs
     const double* zc;
     double* zp;
     int step;
