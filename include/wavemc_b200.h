@@ -111,6 +111,9 @@ typedef struct {
                                     p per tier on P_k = vertices of triangles with flag >= k */
     double domain[4];            /* x0, x1, y0, y1 of the coefficient grid (all 0: unit square) */
     int qoi_mean;                /* 1: Q = mean of u(T) over the box (weights / their sum) */
+    double cfl_safety;           /* > 0: per-sample dt = the reference's stable_dt recipe (src/experiments.cpp:30-43:
+                                    power iteration tol 1e-4 from the level's c = 1 warm starts, margin 1.05,
+                                    safety factor cfl_safety), snapped to T / n_steps per sample; dt is ignored */
 } wmc_level_desc;
 
 void wmc_level_desc_default(wmc_level_desc* desc);

@@ -1,6 +1,6 @@
 """Generate tests/golden/*.json from the UNMODIFIED reference library
 (oracle/_ref/wavemc_ref_driver) -- run in the build container, where
-/root/reference exists:  python oracle/make_golden.py [--only-config2]
+/root/reference exists:  python oracle/make_golden.py [--only-config2 | --only-cfl]
 
 The meshes come from the shared problem definition (the product's host mesh
 builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
@@ -69,12 +69,36 @@ def config2_reductions(ref, tmp):
     dump("config2_reductions.json", out)
 
 
+def cfl_samples(ref, tmp):
+    """Per-sample CFL step: the reference's
+    stable_dt recipe (src/experiments.cpp:30-43: power iteration at tol 1e-4
+    from the level's c = 1 warm starts, margin 1.05, safety 0.9) replacing the
+    fixed dt, on config 0 (LF-LTS and leap-frog) and config-1 pairs."""
+    d0 = configs.config0()
+    p0 = os.path.join(tmp, "cfl_config0.mesh")
+    configs.build_mesh(d0).dump(p0)
+    hdr, q = ref.solve(p0, d0.dt, d0.substeps, "lts", 0, 0, 8, cfl=0.9)
+    hdr_lf, q_lf = ref.solve(p0, d0.dt, 1, "lf", 0, 0, 4, cfl=0.9)
+    c1 = configs.config1()
+    specs = []
+    for l, d in enumerate(c1[:3]):
+        p = os.path.join(tmp, f"cfl_config1_l{l}.mesh")
+        configs.build_mesh(d).dump(p)
+        specs.append((p, d.dt, d.substeps))
+    pairs = ref.mlmc(specs, [4, 3, 2], per_sample=True, cfl=0.9)
+    dump("cfl_samples.json", {"safety": 0.9, "config0_lts": {"q": q.tolist(), "header": hdr},
+                              "config0_lf": {"q": q_lf.tolist(), "header": hdr_lf}, "config1_pairs": pairs})
+
+
 def main():
     build()
     ref = RefDriver()
     tmp = tempfile.mkdtemp(prefix="wmc_golden_")
     if "--only-config2" in sys.argv:
         config2_reductions(ref, tmp)
+        return
+    if "--only-cfl" in sys.argv:
+        cfl_samples(ref, tmp)
         return
 
     # RNG words and uniform draws (rng.hpp:14-19, rng.cpp:14-32)
@@ -163,6 +187,7 @@ def main():
     kl_adaptive["model_cost"] = adaptive["model_cost"]
     dump("config4_adaptive.json", kl_adaptive)
     config2_reductions(ref, tmp)
+    cfl_samples(ref, tmp)
     print("golden fixtures written to", GOLDEN)
 
 

@@ -32,7 +32,9 @@ class OProblem(C.Structure):
                 ("final_time", C.c_double), ("dt", C.c_double), ("substeps", C.c_int), ("nu", C.c_double),
                 ("kind", C.c_int), ("ic_x", C.c_double), ("ic_y", C.c_double), ("ic_w2", C.c_double),
                 ("box", C.c_double * 4), ("kl_table", C.POINTER(C.c_double)), ("kl_modes", C.c_int),
-                ("tiers", C.c_int), ("domain", C.c_double * 4), ("qoi_mean", C.c_int)]
+                ("tiers", C.c_int), ("domain", C.c_double * 4), ("qoi_mean", C.c_int),
+                ("cfl_safety", C.c_double), ("warm_full", C.POINTER(C.c_double)),
+                ("warm_coarse", C.POINTER(C.c_double))]
 
 
 def build(force: bool = False) -> None:
@@ -60,7 +62,7 @@ class MeshArrays:
 
 def problem(dt, substeps=1, kind=1, final_time=1.0, nu=0.01, cells=(4, 4), coef=(0.5, 1.5),
             ic=(0.3, 0.5, 0.01), box=(0.7, 0.9, 0.4, 0.6), kl_table=None, tiers=1, domain=None,
-            qoi_mean=False) -> OProblem:
+            qoi_mean=False, cfl_safety=0.0) -> OProblem:
     """kl_table: None (uniform cells) or a contiguous float64 array [cell][mode]
     (kept alive by the returned struct)."""
     p = OProblem()
@@ -80,6 +82,7 @@ def problem(dt, substeps=1, kind=1, final_time=1.0, nu=0.01, cells=(4, 4), coef=
         for i, v in enumerate(domain):
             p.domain[i] = v
     p.qoi_mean = 1 if qoi_mean else 0
+    p.cfl_safety = cfl_safety
     return p
 
 
@@ -106,6 +109,10 @@ class COracle:
                                             C.POINTER(C.c_long)]
         L.wmc_oracle_steps.argtypes = [C.POINTER(OMesh), C.POINTER(OProblem), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_long]
+        L.wmc_oracle_stable_dt.argtypes = [C.POINTER(OMesh), C.POINTER(OProblem), C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double), C.POINTER(C.c_int)]
+        L.wmc_oracle_warm_starts.argtypes = [C.POINTER(OMesh), C.POINTER(OProblem), C.POINTER(C.c_double),
+                                             C.POINTER(C.c_double)]
         L.wmc_oracle_moments.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_long,
                                          C.POINTER(C.c_double)]
         L.wmc_oracle_level_data.argtypes = [C.POINTER(OMesh), C.POINTER(OProblem), C.POINTER(C.c_double),
@@ -145,6 +152,22 @@ class COracle:
         rc = self.lib.wmc_oracle_solve(C.byref(mesh.c), C.byref(pb), cells.ctypes.data_as(C.POINTER(C.c_double)),
                                        C.byref(q), C.byref(step), cnt)
         return rc, q.value, step.value, list(cnt)
+
+    def stable_dt(self, mesh: MeshArrays, pb: OProblem, cells):
+        """Reference stable_dt of one sample: (status, dt, [full iters, coarse iters])."""
+        cells = np.ascontiguousarray(cells, np.float64)
+        dt = C.c_double()
+        it = (C.c_int * 2)()
+        rc = self.lib.wmc_oracle_stable_dt(C.byref(mesh.c), C.byref(pb), cells.ctypes.data_as(C.POINTER(C.c_double)),
+                                           C.byref(dt), it)
+        return rc, dt.value, list(it)
+
+    def warm_starts(self, mesh: MeshArrays, pb: OProblem):
+        n = int((mesh.boundary == 0).sum())
+        wf, wc = np.empty(n), np.empty(n)
+        rc = self.lib.wmc_oracle_warm_starts(C.byref(mesh.c), C.byref(pb), wf.ctypes.data_as(C.POINTER(C.c_double)),
+                                             wc.ctypes.data_as(C.POINTER(C.c_double)))
+        return rc, wf, wc
 
     def steps(self, mesh: MeshArrays, pb: OProblem, cells, z_prev, z_curr, n_steps):
         """Advance a consistent pair (z_prev, z_curr) by n_steps (no start-up step)."""

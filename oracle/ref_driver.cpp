@@ -92,6 +92,7 @@ struct ProblemDef {
     int kl_modes = 0;
     double dom_x0 = 0.0, dom_x1 = 1.0, dom_y0 = 0.0, dom_y1 = 1.0;  // coefficient grid extent
     bool qoi_mean = false;   // Q = mean over the box
+    double cfl = 0.0;        // > 0: per-sample dt = cfl-scaled stable step (experiments.cpp:30-43)
 };
 
 std::vector<double> num_list(const std::string& s) {
@@ -127,6 +128,7 @@ ProblemDef problem_from(const Args& a) {
         d.dom_x0 = v[0], d.dom_x1 = v[1], d.dom_y0 = v[2], d.dom_y1 = v[3];
     }
     d.qoi_mean = a.integer("qoi-mean", 0) != 0;
+    d.cfl = a.num("cfl", 0.0);
     const std::string kl = a.get("kl-table");
     if (!kl.empty()) {  // "<cells> <modes>" then cells*modes values (written by the shared problem definition)
         std::ifstream in(kl);
@@ -151,6 +153,7 @@ struct Level {
     int substeps = 1;
     long n_r = 0;                     // rows of A P with entries (for DOF-update counts)
     long n_steps = 0;
+    std::vector<double> warm_full, warm_coarse;  // per-sample CFL: c = 1 eigenvectors (experiments.cpp:132-148)
 };
 
 TriMesh load_mesh(const std::string& path) {
@@ -245,6 +248,10 @@ Level make_level(const ProblemDef& d, const std::string& mesh_path, double dt, i
                 break;
             }
     lv.n_steps = static_cast<long>(std::ceil(d.final_time / dt - 1e-12));
+    if (d.cfl > 0.0) {  // the reference's per-level warm starts (experiments.cpp:141-145)
+        lv.warm_full = max_eigenvalue(op.normalized, 1e-4, 20000).eigenvector;
+        if (op.n_fine > 0) lv.warm_coarse = coarse_max_eigenvalue(op, 1e-4, 20000).eigenvector;
+    }
     return lv;
 }
 
@@ -280,6 +287,22 @@ double solve_level(const ProblemDef& d, const Level& lv, const std::vector<doubl
     options.kind = d.kind;
     options.final_time = d.final_time;
     options.dt = lv.dt;
+    if (d.cfl > 0.0) {
+        // stable_dt (src/experiments.cpp:30-43; file-local there, restated
+        // over the public max_eigenvalue / coarse_max_eigenvalue)
+        const double margin = 1.05, tol = 1e-4;
+        const auto fullv = max_eigenvalue(op.normalized, tol, 20000, &lv.warm_full);
+        if (cost) cost->weighted_work += static_cast<long>(fullv.iterations) * op.normalized.nnz();
+        if (d.kind == Integrator::LocalTimeStepping && op.n_fine > 0) {
+            const auto coarse = coarse_max_eigenvalue(op, tol, 20000, &lv.warm_coarse);
+            if (cost) cost->weighted_work += static_cast<long>(coarse.iterations) * op.a_coarse.nnz();
+            const double dt_coarse = 2.0 / std::sqrt(margin * coarse.lambda);
+            const double dt_fine = lv.substeps * 2.0 / std::sqrt(margin * fullv.lambda);
+            options.dt = d.cfl * std::min(dt_coarse, dt_fine);
+        } else {
+            options.dt = d.cfl * 2.0 / std::sqrt(margin * fullv.lambda);
+        }
+    }
     options.substeps = lv.substeps;
     options.nu = d.nu;
     const RunResult run = run_wave(op, lv.init, options);

@@ -351,6 +351,147 @@ int wmc_oracle_level_data(const wmc_oracle_mesh* mesh, const wmc_oracle_problem*
     return n;
 }
 
+/* ---- power iteration: src/fem.cpp:132-175 (max_eigenvalue), :177-189
+ *      (coarse_max_eigenvalue); stable_dt: src/experiments.cpp:30-43 ---- */
+
+/* apply = A (coarse == 0) or the coarse part: x masked on P, A (I-P), rows in P zeroed */
+static void eig_apply(const oper* op, int coarse, const double* x, double* y, double* scratch) {
+    if (!coarse) {
+        csr_mul(&op->a, x, y);
+        return;
+    }
+    for (int i = 0; i < op->n; ++i) scratch[i] = op->sel[i] ? 0.0 : x[i];
+    csr_mul(&op->a_coarse, scratch, y);
+    for (int i = 0; i < op->n; ++i)
+        if (op->sel[i]) y[i] = 0.0;
+}
+
+static int power_iteration(const oper* op, int coarse, double tol, int max_iter, const double* warm, double* lambda,
+                           double* vec_out, int* iters) {
+    const int n = op->n;
+    double* v = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+    double* av = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+    double* sc = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+    if (warm) {
+        memcpy(v, warm, sizeof(double) * (size_t)n);
+    } else {
+        for (int i = 0; i < n; ++i) v[i] = (double)(wmc_oracle_mix64((uint64_t)i + 1) >> 11) * 0x1.0p-53 - 0.5;
+    }
+    double norm = 0.0;
+    for (int i = 0; i < n; ++i) norm += v[i] * v[i];
+    norm = sqrt(norm);
+    if (norm == 0.0) {
+        v[0] = 1.0;
+        norm = 1.0;
+    }
+    for (int i = 0; i < n; ++i) v[i] /= norm;
+    double lambda_prev = 0.0;
+    int settled = 0, status = 3;
+    for (int it = 1; it <= max_iter; ++it) {
+        eig_apply(op, coarse, v, av, sc);
+        double rayleigh = 0.0, av2 = 0.0;
+        for (int i = 0; i < n; ++i) rayleigh += v[i] * av[i];
+        for (int i = 0; i < n; ++i) av2 += av[i] * av[i];
+        const double av_norm = sqrt(av2);
+        if (iters) *iters = it;
+        if (av_norm == 0.0) {
+            *lambda = 0.0;
+            status = 0;
+            break;
+        }
+        for (int i = 0; i < n; ++i) v[i] = av[i] / av_norm;
+        if (fabs(rayleigh - lambda_prev) <= tol * fabs(rayleigh)) {
+            if (++settled >= 3) {
+                *lambda = rayleigh;
+                status = 0;
+                break;
+            }
+        } else {
+            settled = 0;
+        }
+        lambda_prev = rayleigh;
+    }
+    if (vec_out) memcpy(vec_out, v, sizeof(double) * (size_t)n);
+    free(v);
+    free(av);
+    free(sc);
+    return status;
+}
+
+static int n_selected(const oper* op) {
+    int c = 0;
+    for (int i = 0; i < op->n; ++i) c += op->sel[i] != 0;
+    return c;
+}
+
+static int stable_dt_op(const oper* op, const wmc_oracle_problem* pb, const double* warm_full,
+                        const double* warm_coarse, double* dt, int* iters) {
+    const double margin = 1.05, tol = 1e-4;
+    double lf = 0.0, lc = 0.0;
+    int it_f = 0, it_c = 0;
+    if (power_iteration(op, 0, tol, 20000, warm_full, &lf, NULL, &it_f) != 0) return 3;
+    if (pb->kind == 1 && n_selected(op) > 0) {
+        if (power_iteration(op, 1, tol, 20000, warm_coarse, &lc, NULL, &it_c) != 0) return 3;
+        int p_fine = pb->substeps;
+        for (int k = 1; k < pb->tiers; ++k) p_fine *= pb->substeps;
+        const double dt_coarse = 2.0 / sqrt(margin * lc);
+        const double dt_fine = p_fine * 2.0 / sqrt(margin * lf);
+        *dt = pb->cfl_safety * (dt_coarse < dt_fine ? dt_coarse : dt_fine);
+    } else {
+        *dt = pb->cfl_safety * 2.0 / sqrt(margin * lf);
+    }
+    if (iters) {
+        iters[0] = it_f;
+        iters[1] = it_c;
+    }
+    return 0;
+}
+
+int wmc_oracle_warm_starts(const wmc_oracle_mesh* mesh, const wmc_oracle_problem* pb, double* warm_full,
+                           double* warm_coarse) {
+    double* ones = (double*)malloc(sizeof(double) * (size_t)(pb->cells_x * pb->cells_y));
+    for (int k = 0; k < pb->cells_x * pb->cells_y; ++k) ones[k] = 1.0;
+    oper op;
+    if (build_operator(mesh, pb, ones, &op) != 0) {
+        free(ones);
+        return 3;
+    }
+    double lam;
+    int status = power_iteration(&op, 0, 1e-4, 20000, NULL, &lam, warm_full, NULL);
+    if (status == 0 && warm_coarse) {
+        if (n_selected(&op) > 0)
+            status = power_iteration(&op, 1, 1e-4, 20000, NULL, &lam, warm_coarse, NULL);
+        else
+            memset(warm_coarse, 0, sizeof(double) * (size_t)op.n);
+    }
+    oper_free(&op);
+    free(ones);
+    return status;
+}
+
+int wmc_oracle_stable_dt(const wmc_oracle_mesh* mesh, const wmc_oracle_problem* pb, const double* cells, double* dt,
+                         int* iters) {
+    oper op;
+    if (build_operator(mesh, pb, cells, &op) != 0) return 3;
+    double *wf = NULL, *wc = NULL;
+    if (!pb->warm_full) {
+        wf = (double*)malloc(sizeof(double) * (size_t)(op.n ? op.n : 1));
+        wc = (double*)malloc(sizeof(double) * (size_t)(op.n ? op.n : 1));
+        if (wmc_oracle_warm_starts(mesh, pb, wf, wc) != 0) {
+            free(wf);
+            free(wc);
+            oper_free(&op);
+            return 3;
+        }
+    }
+    const int status = stable_dt_op(&op, pb, pb->warm_full ? pb->warm_full : wf,
+                                    pb->warm_full ? pb->warm_coarse : wc, dt, iters);
+    free(wf);
+    free(wc);
+    oper_free(&op);
+    return status;
+}
+
 /* ---- time integration: src/integrators.cpp:12-18 (check_finite), :68-87
  *      (leapfrog_init), :89-115 (leapfrog_step), :117-157 (lts_step),
  *      :176-210 (run_wave) ---- */
@@ -372,12 +513,12 @@ typedef struct {
     long cnt[3];
 } integ;
 
-static void integ_init(integ* g, const oper* op, const wmc_oracle_problem* pb) {
+static void integ_init(integ* g, const oper* op, const wmc_oracle_problem* pb, double dt_req) {
     memset(g, 0, sizeof(*g));
     g->op = op;
     g->n = op->n;
     g->kind = pb->kind;
-    const long n_steps = (long)ceil(pb->final_time / pb->dt - 1e-12);
+    const long n_steps = (long)ceil(pb->final_time / dt_req - 1e-12);
     g->dt = pb->final_time / (double)n_steps;
     g->p = pb->kind == 1 ? pb->substeps : 1;
     g->tiers = pb->kind == 1 && pb->tiers > 1 ? pb->tiers : 1;
@@ -528,9 +669,33 @@ int wmc_oracle_solve(const wmc_oracle_mesh* mesh, const wmc_oracle_problem* pb, 
     int status = 0;
     project_z0(mesh, pb, &op, z0);
     qoi_weights(mesh, pb, &op, qw);
+    /* requested step: fixed, or the sample's stable_dt (run_wave snaps it) */
+    double dt_req = pb->dt;
+    if (pb->cfl_safety > 0.0) {
+        double *wf = NULL, *wc = NULL;
+        if (!pb->warm_full) {
+            wf = (double*)malloc(bytes);
+            wc = (double*)malloc(bytes);
+            wmc_oracle_warm_starts(mesh, pb, wf, wc);
+        }
+        status = stable_dt_op(&op, pb, pb->warm_full ? pb->warm_full : wf, pb->warm_full ? pb->warm_coarse : wc,
+                              &dt_req, NULL);
+        free(wf);
+        free(wc);
+        if (status != 0) {
+            if (fail_step) *fail_step = 0;
+            free(z0);
+            free(zp);
+            free(zc);
+            free(scratch);
+            free(qw);
+            oper_free(&op);
+            return status;
+        }
+    }
     integ g;
-    integ_init(&g, &op, pb);
-    const long n_steps = (long)ceil(pb->final_time / pb->dt - 1e-12);
+    integ_init(&g, &op, pb, dt_req);
+    const long n_steps = (long)ceil(pb->final_time / dt_req - 1e-12);
     const double dt = g.dt;
 
     /* leapfrog_init: z1 = z0 + dt M^{1/2} v0 + dt^2/2 (F0 - A z0), v0 = F = 0 */
@@ -576,7 +741,7 @@ int wmc_oracle_steps(const wmc_oracle_mesh* mesh, const wmc_oracle_problem* pb, 
     if (build_operator(mesh, pb, cells, &op) != 0) return 3;
     double* scratch = (double*)malloc(sizeof(double) * (size_t)(op.n ? op.n : 1) * 5);
     integ g;
-    integ_init(&g, &op, pb);
+    integ_init(&g, &op, pb, pb->dt);
     int status = 0;
     for (long s = 0; s < n_steps && status == 0; ++s) {
         integ_step(&g, z_prev, z_curr, scratch);
@@ -596,6 +761,32 @@ int wmc_oracle_eval_pairs(const wmc_oracle_mesh* fine, const wmc_oracle_problem*
     const int ncell = pf->cells_x * pf->cells_y;
     double* cells = (double*)malloc(sizeof(double) * (size_t)ncell);
     int status = 0;
+    /* per-level warm starts, once per call (the reference's level contexts) */
+    wmc_oracle_problem fpb = *pf, cpb;
+    double *wbuf[4] = {NULL, NULL, NULL, NULL};
+    if (pf->cfl_safety > 0.0 && !pf->warm_full) {
+        int nf = 0;
+        for (int v = 0; v < fine->n_vertices; ++v) nf += !fine->boundary[v];
+        wbuf[0] = (double*)malloc(sizeof(double) * (size_t)(nf ? nf : 1));
+        wbuf[1] = (double*)malloc(sizeof(double) * (size_t)(nf ? nf : 1));
+        wmc_oracle_warm_starts(fine, pf, wbuf[0], wbuf[1]);
+        fpb.warm_full = wbuf[0];
+        fpb.warm_coarse = wbuf[1];
+    }
+    if (coarse) {
+        cpb = *pc;
+        if (pc->cfl_safety > 0.0 && !pc->warm_full) {
+            int nc = 0;
+            for (int v = 0; v < coarse->n_vertices; ++v) nc += !coarse->boundary[v];
+            wbuf[2] = (double*)malloc(sizeof(double) * (size_t)(nc ? nc : 1));
+            wbuf[3] = (double*)malloc(sizeof(double) * (size_t)(nc ? nc : 1));
+            wmc_oracle_warm_starts(coarse, pc, wbuf[2], wbuf[3]);
+            cpb.warm_full = wbuf[2];
+            cpb.warm_coarse = wbuf[3];
+        }
+        pc = &cpb;
+    }
+    pf = &fpb;
     for (long i = 0; i < count && status == 0; ++i) {
         if (pf->kl_table)
             wmc_oracle_draw_kl(seed, level, first + (uint64_t)i, pf->kl_table, ncell, pf->kl_modes, cells);
@@ -613,6 +804,7 @@ int wmc_oracle_eval_pairs(const wmc_oracle_mesh* fine, const wmc_oracle_problem*
         q_fine[i] = qf;
         dq[i] = coarse ? qf - qc : qf;
     }
+    for (int k = 0; k < 4; ++k) free(wbuf[k]);
     free(cells);
     return status;
 }

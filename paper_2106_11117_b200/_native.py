@@ -33,7 +33,8 @@ class LevelDesc(C.Structure):
                 ("integrator", C.c_int), ("ic_x", C.c_double), ("ic_y", C.c_double), ("ic_width2", C.c_double),
                 ("qoi_box", C.c_double * 4), ("device", C.c_int), ("batch", C.c_int), ("field", C.c_int),
                 ("kl_sigma", C.c_double), ("kl_corr_len", C.c_double), ("kl_modes", C.c_int),
-                ("tiers", C.c_int), ("domain", C.c_double * 4), ("qoi_mean", C.c_int)]
+                ("tiers", C.c_int), ("domain", C.c_double * 4), ("qoi_mean", C.c_int),
+                ("cfl_safety", C.c_double)]
 
 
 class LShapeMeshSpec(C.Structure):

@@ -91,7 +91,16 @@ struct Workspace {
     double* db = nullptr;
     std::vector<double*> tier_e;    // nested tiers: E^k buffers, 2 per tier, [row][S] over R_k
     std::vector<double*> tier_rhs;  // r_k for k >= 2, [row][S] over R_k
+    // per-sample CFL: (dt_s / dt)^2 and step counts, power-iteration state
+    double* rel = nullptr;
+    int* nsteps = nullptr;
+    double* eig = nullptr;     // part [2][nb][S] | norm | lam | lam_prev | lf | lc  (S each)
+    int* eig_i = nullptr;      // settled | iters | done (S each) | active count
+    int* h_active = nullptr;   // pinned
+    int* h_nsteps = nullptr;   // pinned, S
 };
+
+constexpr int kEigBlocks = 64;  // row blocks of the power-iteration dot products
 
 enum class SubPath { None, Lattice, OnChip, Global, Tiers };
 
@@ -132,6 +141,11 @@ struct wmc_level {
     std::vector<int*> d_tier_ptr, d_tier_ent;
     std::vector<double*> d_tier_a0;
     double* d_tier_cm = nullptr;
+    // per-sample CFL: warm starts and per-dof P membership
+    double* d_warm_full = nullptr;
+    double* d_warm_coarse = nullptr;
+    double warm_full_norm = 0.0, warm_coarse_norm = 0.0;
+    unsigned char* d_in_p = nullptr;
     // QoI
     int* d_qdof = nullptr;
     double* d_qw = nullptr;
@@ -191,9 +205,15 @@ struct wmc_level {
         for (auto* p : d_tier_ent) cudaFree(p);
         for (auto* p : d_tier_a0) cudaFree(p);
         if (d_tier_cm) cudaFree(d_tier_cm);
+        for (void* p : {(void*)d_warm_full, (void*)d_warm_coarse, (void*)d_in_p})
+            if (p) cudaFree(p);
         for (auto& w : ws) {
             for (void* p : {(void*)w.za, (void*)w.zb, (void*)w.g, (void*)w.q, (void*)w.fail, (void*)w.da, (void*)w.db})
                 if (p) cudaFree(p);
+            for (void* p : {(void*)w.rel, (void*)w.nsteps, (void*)w.eig, (void*)w.eig_i})
+                if (p) cudaFree(p);
+            if (w.h_active) cudaFreeHost(w.h_active);
+            if (w.h_nsteps) cudaFreeHost(w.h_nsteps);
             for (auto* p : w.tier_e) cudaFree(p);
             for (auto* p : w.tier_rhs) cudaFree(p);
         }
@@ -336,6 +356,22 @@ void build_device_level(wmc_level& L) {
         const wmc::KLTable kl =
             wmc::kl_cell_table(L.spec.cells_x, L.spec.cells_y, L.spec.kl_sigma, L.spec.kl_corr_len, L.spec.kl_modes);
         L.d_kl = upload(kl.t);
+    }
+    if (t.cfl_safety > 0.0) {
+        // the reference normalises the warm start before iterating (fem.cpp:137-146)
+        auto norm = [](const std::vector<double>& v) {
+            double acc = 0.0;
+            for (double x : v) acc += x * x;
+            const double n = std::sqrt(acc);
+            return n == 0.0 ? 1.0 : n;
+        };
+        L.d_warm_full = upload(t.warm_full);
+        L.warm_full_norm = norm(t.warm_full);
+        if (!t.warm_coarse.empty()) {
+            L.d_warm_coarse = upload(t.warm_coarse);
+            L.warm_coarse_norm = norm(t.warm_coarse);
+        }
+        L.d_in_p = upload(t.in_p);
     }
     L.d_qdof = upload(t.qoi_dof);
     L.d_qw = upload(t.qoi_w);
@@ -487,6 +523,14 @@ Workspace& workspace(wmc_level& L, int role) {
             alloc(&w.da, S * t.n_r);
             alloc(&w.db, S * t.n_r);
         }
+        if (t.cfl_safety > 0.0) {
+            alloc(&w.rel, S);
+            alloc(&w.nsteps, S);
+            alloc(&w.eig, S * (2 * kEigBlocks + 5));
+            alloc(&w.eig_i, S * 3 + 1);
+            check(cudaMallocHost(&w.h_active, sizeof(int)), "cudaMallocHost");
+            check(cudaMallocHost(&w.h_nsteps, sizeof(int) * S), "cudaMallocHost");
+        }
         if (L.path == SubPath::Tiers) {
             w.tier_e.assign(2 * t.tiers, nullptr);
             w.tier_rhs.assign(t.tiers, nullptr);
@@ -517,7 +561,7 @@ cudaEvent_t mark(wmc_level& L, std::vector<cudaEvent_t>& v, cudaStream_t st) {
 // replaces the stage's right-hand side on R_k+1.  At stage 0 the right-hand
 // side of tier k+1 is r_k itself (no product yet), so tier k+1 reads r_k.
 void run_tiers(wmc_level& L, Workspace& ws, const double* cells, int S, int count, const double* zc, double* zp,
-               int step, cudaStream_t stream) {
+               int step, const double* rel, const int* nsteps, cudaStream_t stream) {
     const wmc::LevelTables& t = L.tab;
     const int K = t.tiers, p = t.p;
     wmc::TierArgs a{};
@@ -531,6 +575,8 @@ void run_tiers(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
     a.zp = zp;
     a.step = step;
     a.fail = ws.fail;
+    a.rel = rel;
+    a.nsteps = nsteps;
     std::vector<int> stage(K + 1, 0);
     auto buf = [&](int j, int m) { return ws.tier_e[2 * (j - 1) + (m & 1)]; };
     auto run = [&](auto&& self, int k, const double* rhs) -> void {
@@ -588,11 +634,84 @@ void run_tiers(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
     run(run, 1, ws.g);
 }
 
+// Per-sample CFL (reference stable_dt, src/experiments.cpp:30-43): power
+// iterations for the whole batch from the level's warm starts, then per
+// sample dt, steps and the dt^2 scale of every constant.  Returns the largest
+// step count of the live samples (the batch's horizon).
+long cfl_phase(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
+    const wmc::LevelTables& t = L.tab;
+    const std::size_t SS = static_cast<std::size_t>(S);
+    double* part = ws.eig;
+    double* norm = part + 2 * kEigBlocks * SS;
+    double* lam = norm + SS;
+    double* lam_prev = lam + SS;
+    double* lf = lam_prev + SS;
+    double* lc = lf + SS;
+    int* settled = ws.eig_i;
+    int* iters = settled + SS;
+    int* done = iters + SS;
+    int* active = done + SS;
+    auto power = [&](bool coarse, double* out) {
+        wmc::EigArgs e{};
+        e.n = t.n;
+        e.S = S;
+        e.count = count;
+        e.row_ptr = L.d_row_ptr;
+        e.ent = L.d_ent;
+        e.a0 = L.d_a0;
+        e.cells = cells;
+        e.in_p = L.d_in_p;
+        e.coarse = coarse ? 1 : 0;
+        e.v = ws.za;
+        e.av = ws.zb;
+        e.n_blocks = kEigBlocks;
+        e.part = part;
+        e.norm = norm;
+        e.lam = lam;
+        e.lam_prev = lam_prev;
+        e.settled = settled;
+        e.iters = iters;
+        e.done = done;
+        e.active_count = active;
+        e.tol = 1e-4;
+        check(cudaMemsetAsync(lam_prev, 0, sizeof(double) * SS, stream), "memset");
+        check(cudaMemsetAsync(settled, 0, sizeof(int) * 3 * SS, stream), "memset");
+        wmc::launch_eig_init(coarse ? L.d_warm_coarse : L.d_warm_full, coarse ? L.warm_coarse_norm : L.warm_full_norm,
+                             t.n, S, ws.za, stream);
+        ++g_launches;
+        for (int it = 1;; ++it) {
+            check(cudaMemsetAsync(active, 0, sizeof(int), stream), "memset");
+            wmc::launch_eig_iteration(e, stream);
+            g_launches += 4;
+            check(cudaMemcpyAsync(ws.h_active, active, sizeof(int), cudaMemcpyDeviceToHost, stream), "copy");
+            check(cudaStreamSynchronize(stream), "power iteration");
+            if (*ws.h_active == 0) break;
+            if (it >= 20000) throw NumericalError("max_eigenvalue: power iteration did not converge");
+        }
+        check(cudaMemcpyAsync(out, lam, sizeof(double) * SS, cudaMemcpyDeviceToDevice, stream), "copy");
+    };
+    power(false, lf);
+    const bool use_coarse = t.kind == wmc::Integrator::LocalTimeStepping && t.n_p > 0 && L.d_warm_coarse;
+    if (use_coarse) power(true, lc);
+    wmc::launch_cfl_finalize(lf, lc, use_coarse ? 1 : 0, t.p_fine, t.cfl_safety, L.spec.final_time, t.dt, count, S,
+                             ws.rel, ws.nsteps, stream);
+    ++g_launches;
+    check(cudaMemcpyAsync(ws.h_nsteps, ws.nsteps, sizeof(int) * S, cudaMemcpyDeviceToHost, stream), "copy");
+    check(cudaStreamSynchronize(stream), "cfl");
+    long n_max = 1;
+    for (int s = 0; s < count; ++s) n_max = std::max<long>(n_max, ws.h_nsteps[s]);
+    return n_max;
+}
+
 void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
     const wmc::LevelTables& t = L.tab;
     const bool lts = L.path != SubPath::None;
     const bool global = L.path == SubPath::Global;
     const bool tiers = L.path == SubPath::Tiers;
+    const bool cfl = t.cfl_safety > 0.0;
+    const long n_steps = cfl ? cfl_phase(L, ws, cells, S, count, stream) : t.n_steps;
+    const double* rel = cfl ? ws.rel : nullptr;
+    const int* nsteps = cfl ? ws.nsteps : nullptr;
     wmc::launch_fill_int(ws.fail, INT_MAX, S, stream);
 
     wmc::SweepArgs sw{};
@@ -611,6 +730,8 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     sw.factor = t.init_factor;
     sw.step = 1;
     sw.fail = ws.fail;
+    sw.rel = rel;
+    sw.nsteps = nsteps;
     wmc::launch_sweep_init(sw, stream);
     g_launches += 2;
 
@@ -677,7 +798,13 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         sb.c0 = t.c0;
     }
     const int sub_grid = std::max(1, std::min(L.lattice ? L.lat_grid : L.sub_grid, count));
-    for (long s = 1; s < t.n_steps; ++s) {
+    la.rel = rel;
+    la.nsteps = nsteps;
+    sb.rel = rel;
+    sb.nsteps = nsteps;
+    for (long s = 1; s < n_steps; ++s) {
+        la.step = static_cast<int>(s + 1);
+        sb.step = static_cast<int>(s + 1);
         sw.zc = cur;
         sw.zp = prev;
         sw.zc_out = nullptr;
@@ -697,7 +824,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
         ++g_launches;
         if (tiers) {
             if (L.profile) mark(L, L.ev_sub, stream);
-            run_tiers(L, ws, cells, S, count, cur, prev, static_cast<int>(s + 1), stream);
+            run_tiers(L, ws, cells, S, count, cur, prev, static_cast<int>(s + 1), rel, nsteps, stream);
             if (L.profile) mark(L, L.ev_sub, stream);
         } else if (global) {
             if (L.profile) mark(L, L.ev_sub, stream);
@@ -716,6 +843,8 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
             ga.zc = cur;
             ga.zp = prev;
             ga.step = static_cast<int>(s + 1);
+            ga.rel = rel;
+            ga.nsteps = nsteps;
             ga.fail = ws.fail;
             for (int m = 1; m <= t.p - 1; ++m) {
                 // d_m / d_{m-1}: m = 1 -> (-c0 g, 0); m = 2 -> (A, -c0 g); then A/B alternate
@@ -746,6 +875,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
             ru.zp = prev;
             ru.step = static_cast<int>(s + 1);
             ru.fail = ws.fail;
+            ru.nsteps = nsteps;
             if (L.profile) mark(L, L.ev_upd, stream);
             wmc::launch_r_update(ru, stream);
             if (L.profile) mark(L, L.ev_upd, stream);
@@ -763,6 +893,9 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     qa.z = cur;
     qa.fail = ws.fail;
     qa.q = ws.q;
+    qa.z_alt = prev;
+    qa.nsteps = nsteps;
+    qa.n_max = static_cast<int>(n_steps);
     wmc::launch_qoi(qa, stream);
     ++g_launches;
     check(cudaGetLastError(), "kernel launch");
@@ -1078,6 +1211,8 @@ wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
         s.dom_y1 = desc->domain[3];
     }
     s.qoi_mean = desc->qoi_mean != 0;
+    if (desc->cfl_safety < 0.0 || desc->cfl_safety > 1.0) throw ConfigError("wmc_level_create: cfl_safety in [0, 1]");
+    s.cfl_safety = desc->cfl_safety;
     if (s.field == wmc::Field::LognormalKL &&
         (s.kl_modes < 1 || s.kl_modes > wmc::kMaxKLModes || !(s.kl_corr_len > 0.0) || !(s.kl_sigma >= 0.0)))
         throw ConfigError("wmc_level_create: KL field needs 1..64 modes, corr_len > 0, sigma >= 0");

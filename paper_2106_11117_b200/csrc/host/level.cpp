@@ -9,6 +9,15 @@
 
 namespace wmc {
 
+namespace {
+std::uint64_t mix64_host(std::uint64_t z) {  // reference rng.hpp:14-19
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+}  // namespace
+
 // Chebyshev stabilisation constants, restating reference
 // src/integrators.cpp:34-66: delta = 1 + nu/p^2, T_k(delta) by the three-term
 // recurrence, omega = 2 p U_{p-1}(delta) / T_p(delta),
@@ -491,6 +500,65 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
                 dt_k /= p;
             }
         }
+    }
+    L.p_fine = 1;
+    for (int k = 0; k < L.tiers; ++k) L.p_fine *= L.p;
+    L.cfl_safety = spec.cfl_safety;
+    if (spec.cfl_safety > 0.0) {
+        // power iteration as reference max_eigenvalue (src/fem.cpp:132-175):
+        // mix64 start vector, tol 1e-4, three settled Rayleigh quotients
+        std::vector<double> a1;  // c = 1 operator, one value per stored (row, col)
+        std::vector<int> c1, p1{0};
+        for (int i = 0; i < L.n; ++i) {
+            for (int e = L.row_ptr[i]; e < L.row_ptr[i + 1];) {
+                const int j = L.col[e];
+                double v = 0.0;
+                for (; e < L.row_ptr[i + 1] && L.col[e] == j; ++e) v += L.a0[e];
+                c1.push_back(j);
+                a1.push_back(v);
+            }
+            p1.push_back(static_cast<int>(c1.size()));
+        }
+        auto power = [&](bool coarse) {
+            const int n = L.n;
+            std::vector<double> v(n), av(n);
+            for (int i = 0; i < n; ++i)
+                v[i] = static_cast<double>(mix64_host(static_cast<std::uint64_t>(i) + 1) >> 11) * 0x1.0p-53 - 0.5;
+            double norm = 0.0;
+            for (double x : v) norm += x * x;
+            norm = std::sqrt(norm);
+            if (norm == 0.0) {
+                v[0] = 1.0;
+                norm = 1.0;
+            }
+            for (double& x : v) x /= norm;
+            double prev = 0.0;
+            int settled = 0;
+            for (int it = 1; it <= 20000; ++it) {
+                for (int i = 0; i < n; ++i) {
+                    double acc = 0.0;
+                    if (!(coarse && L.in_p[i]))
+                        for (int e = p1[i]; e < p1[i + 1]; ++e)
+                            if (!(coarse && L.in_p[c1[e]])) acc += a1[e] * v[c1[e]];
+                    av[i] = acc;
+                }
+                double ray = 0.0, nn = 0.0;
+                for (int i = 0; i < n; ++i) ray += v[i] * av[i];
+                for (int i = 0; i < n; ++i) nn += av[i] * av[i];
+                const double avn = std::sqrt(nn);
+                if (avn == 0.0) return v;
+                for (int i = 0; i < n; ++i) v[i] = av[i] / avn;
+                if (std::abs(ray - prev) <= 1e-4 * std::abs(ray)) {
+                    if (++settled >= 3) return v;
+                } else {
+                    settled = 0;
+                }
+                prev = ray;
+            }
+            throw std::runtime_error("level: warm-start power iteration did not converge");
+        };
+        L.warm_full = power(false);
+        if (spec.kind == Integrator::LocalTimeStepping && L.n_p > 0) L.warm_coarse = power(true);
     }
     return L;
 }

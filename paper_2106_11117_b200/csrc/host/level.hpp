@@ -51,6 +51,7 @@ struct LevelSpec {
     QoIBox qoi;
     bool qoi_mean = false;  // Q = mean over the box (weights normalised by their sum)
     int tiers = 1;          // nested LTS tiers (config 2); 1 = the reference's single-tier LF-LTS
+    double cfl_safety = 0.0;  // > 0: per-sample dt from the reference's stable_dt recipe (experiments.cpp:30-43)
     double dom_x0 = 0.0, dom_x1 = 1.0, dom_y0 = 0.0, dom_y1 = 1.0;  // coefficient grid extent
 
     // cell k = iy * cells_x + ix of the coefficient grid, ix = floor((x - x0) / (x1 - x0) * cells_x)
@@ -138,6 +139,13 @@ struct LevelTables {
     std::vector<std::vector<double>> tier_a0;
     std::vector<double> tier_c0, tier_back;
     std::vector<std::vector<double>> tier_cm;
+
+    // per-sample CFL (cfl_safety > 0): warm starts of the power iterations,
+    // the dominant eigenvectors of the c = 1 operator (full, and A (I-P) on
+    // rows outside P), as the reference's level contexts (experiments.cpp:132-148)
+    double cfl_safety = 0.0;
+    std::vector<double> warm_full, warm_coarse;
+    int p_fine = 1;                  // substeps of the finest tier (p^tiers)
 
     // time stepping
     long n_steps = 0;

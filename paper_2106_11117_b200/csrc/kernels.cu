@@ -97,6 +97,28 @@ __device__ __forceinline__ void flag_fail(int* fail, int s, int count, int step)
     if (s < count) atomicMin(fail + s, step);
 }
 
+// per-sample CFL: the lane's two samples' dt^2 scale and whether `step` is
+// still inside their horizons
+__device__ __forceinline__ double2 lane_rel(const double* rel, int s0) {
+    return rel ? __ldg(reinterpret_cast<const double2*>(rel + s0)) : make_double2(1.0, 1.0);
+}
+__device__ __forceinline__ int2 lane_live(const int* nsteps, int s0, int step) {
+    if (!nsteps) return make_int2(1, 1);
+    const int2 n = __ldg(reinterpret_cast<const int2*>(nsteps + s0));
+    return make_int2(step <= n.x, step <= n.y);
+}
+// z_{n+1} store + check_finite for the live samples of the lane
+__device__ __forceinline__ void store_z(double* p, double2 out, int2 live, int* fail, int s0, int count, int step) {
+    if (live.x && live.y) {
+        *reinterpret_cast<double2*>(p) = out;
+    } else {
+        if (live.x) p[0] = out.x;
+        if (live.y) p[1] = out.y;
+    }
+    if (live.x && !(fabs(out.x) <= 1e100)) flag_fail(fail, s0, count, step);
+    if (live.y && !(fabs(out.y) <= 1e100)) flag_fail(fail, s0 + 1, count, step);
+}
+
 // ---------------------------------------------------------------------------
 // K1: the full sweep g = A(omega) z over every row, one warp per (row, 64
 // samples), 16-byte loads per lane.  A(omega)_ij = sum_k c_k a0_ijk
@@ -226,9 +248,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
         if (kInit) {
             // z1 = z0 + dt M^{1/2} v0 + dt^2/2 (F0 - A z0), v0 = F = 0 (integrators.cpp:68-87)
             const double z0 = __ldg(a.z0 + row);
+            const double2 r = lane_rel(a.rel, s0);
             double2 out;
-            out.x = z0 + a.factor * (0.0 - acc0);
-            out.y = z0 + a.factor * (0.0 - acc1);
+            out.x = z0 + (a.factor * r.x) * (0.0 - acc0);
+            out.y = z0 + (a.factor * r.y) * (0.0 - acc1);
             *reinterpret_cast<double2*>(a.zp + idx) = make_double2(z0, z0);
             *reinterpret_cast<double2*>(a.zc_out + idx) = out;
             if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
@@ -241,13 +264,12 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
         } else {
             const double2 zn = zself;  // every row holds its diagonal entry
             const double2 zm = zm_early;
+            const double2 r = lane_rel(a.rel, s0);
             double2 out;
-            out.x = 2.0 * zn.x - zm.x - a.factor * acc0;
-            out.y = 2.0 * zn.y - zm.y - a.factor * acc1;
-            *reinterpret_cast<double2*>(a.zp + idx) = out;
+            out.x = 2.0 * zn.x - zm.x - (a.factor * r.x) * acc0;
+            out.y = 2.0 * zn.y - zm.y - (a.factor * r.y) * acc1;
             // check_finite (integrators.cpp:12-18): non-finite or |z| > 1e100
-            if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
-            if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+            store_z(a.zp + idx, out, lane_live(a.nsteps, s0, a.step), a.fail, s0, a.count, a.step);
         }
     }
     if (kInit || row0 >= a.split || a.g_node_major) return;  // block-uniform
@@ -297,6 +319,9 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
     }
     int ccell = -1;
     double2 c = make_double2(0.0, 0.0);
+    const double2 fac = a.rel ? lane_rel(a.rel, s0) : make_double2(1.0, 1.0);
+    const double2 factor = make_double2(a.factor * fac.x, a.factor * fac.y);
+    const int2 live = lane_live(a.nsteps, s0, a.step);
 #pragma unroll
     for (int k = 0; k < R; ++k) {
         const int row = first + k;
@@ -364,11 +389,9 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
                 tile[warp * R + k][lane] = make_double2(acc0, acc1);
         } else {
             double2 out;
-            out.x = 2.0 * zcur.x - zm.x - a.factor * acc0;
-            out.y = 2.0 * zcur.y - zm.y - a.factor * acc1;
-            *reinterpret_cast<double2*>(a.zp + idx) = out;
-            if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
-            if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+            out.x = 2.0 * zcur.x - zm.x - factor.x * acc0;
+            out.y = 2.0 * zcur.y - zm.y - factor.y * acc1;
+            store_z(a.zp + idx, out, live, a.fail, s0, a.count, a.step);
         }
         zprev = zcur;
         zcur = znext;
@@ -405,7 +428,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
     const int s0 = (blockIdx.x / groups) * kSweepChunk + 2 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
     const double* src = a.cur_mode == 0 ? a.dcur : a.g;
-    const double scale = a.cur_mode == 0 ? 1.0 : -a.c0;
+    const double2 r = lane_rel(a.rel, s0);
+    const double2 c0 = make_double2(a.c0 * r.x, a.c0 * r.y), cm = make_double2(a.cm * r.x, a.cm * r.y);
+    const double2 scale = a.cur_mode == 0 ? make_double2(1.0, 1.0) : make_double2(-c0.x, -c0.y);
+    const int2 live = lane_live(a.nsteps, s0, a.step);
     auto ld = [&](const double* p, int r) {
         return *reinterpret_cast<const double2*>(p + static_cast<std::size_t>(r) * S + s0);
     };
@@ -464,22 +490,20 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
                 acc1 += (cc.y * w) * v.y;
             }
         }
-        acc0 *= scale;
-        acc1 *= scale;
-        if (a.cur_mode != 0) dm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
-        if (a.prev_mode == 1) dmm = make_double2(-a.c0 * g.x, -a.c0 * g.y);
+        acc0 *= scale.x;
+        acc1 *= scale.y;
+        if (a.cur_mode != 0) dm = make_double2(-c0.x * g.x, -c0.y * g.y);
+        if (a.prev_mode == 1) dmm = make_double2(-c0.x * g.x, -c0.y * g.y);
         double2 next;
-        next.x = (1.0 + a.beta) * dm.x - a.beta * dmm.x - a.cm * (g.x + acc0);
-        next.y = (1.0 + a.beta) * dm.y - a.beta * dmm.y - a.cm * (g.y + acc1);
+        next.x = (1.0 + a.beta) * dm.x - a.beta * dmm.x - cm.x * (g.x + acc0);
+        next.y = (1.0 + a.beta) * dm.y - a.beta * dmm.y - cm.y * (g.y + acc1);
         if (!a.last) {
             *reinterpret_cast<double2*>(a.dprev + idx) = next;
         } else {
             double2 out;
             out.x = 2.0 * zn.x - zm.x + 2.0 * next.x;
             out.y = 2.0 * zn.y - zm.y + 2.0 * next.y;
-            *reinterpret_cast<double2*>(a.zp + idx) = out;
-            if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
-            if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+            store_z(a.zp + idx, out, live, a.fail, s0, a.count, a.step);
         }
         vprev = vcur;
         vcur = vnext;
@@ -499,6 +523,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(TierArgs a
     const int s0 = (blockIdx.x / groups) * kSweepChunk + 2 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
     const double* src = a.src;
+    const double2 rr = lane_rel(a.rel, s0);
     auto ld = [&](const double* p, int r) {
         return *reinterpret_cast<const double2*>(p + static_cast<std::size_t>(r) * S + s0);
     };
@@ -578,10 +603,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(TierArgs a
             }
             if (L.emm) emm = *reinterpret_cast<const double2*>(L.emm + idx);
             double2 en;
-            en.x = L.A * em.x - L.B * emm.x - L.C * v.x;
-            en.y = L.A * em.y - L.B * emm.y - L.C * v.y;
+            en.x = L.A * em.x - L.B * emm.x - (L.C * rr.x) * v.x;
+            en.y = L.A * em.y - L.B * emm.y - (L.C * rr.y) * v.y;
             if (t + 1 < a.depth) {
-                v = make_double2(L.back * en.x, L.back * en.y);
+                v = make_double2((L.back / rr.x) * en.x, (L.back / rr.y) * en.y);
                 continue;
             }
             if (L.out) {
@@ -592,9 +617,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(TierArgs a
                 double2 out;
                 out.x = 2.0 * zn.x - zm.x + 2.0 * en.x;
                 out.y = 2.0 * zn.y - zm.y + 2.0 * en.y;
-                *reinterpret_cast<double2*>(a.zp + idx) = out;
-                if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
-                if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+                store_z(a.zp + idx, out, lane_live(a.nsteps, s0, a.step), a.fail, s0, a.count, a.step);
             }
         }
     }
@@ -634,9 +657,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) r_update_kernel(RUpdateArgs 
     double2 out;
     out.x = 2.0 * zn.x - zm.x + 2.0 * d.x;
     out.y = 2.0 * zn.y - zm.y + 2.0 * d.y;
-    *reinterpret_cast<double2*>(a.zp + idx) = out;
-    if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
-    if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+    store_z(a.zp + idx, out, lane_live(a.nsteps, s0, a.step), a.fail, s0, a.count, a.step);
 }
 
 // ---------------------------------------------------------------------------
@@ -712,6 +733,9 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
     if (tid == 0) sm.W[a.n_wid] = 0.0;  // padding entries
 
     for (int s = blockIdx.x; s < a.count; s += gridDim.x) {
+        // per-sample CFL: finished samples are left alone, dt^2 constants scale
+        if (a.nsteps && a.step > __ldg(a.nsteps + s)) continue;
+        const double rs = a.rel ? __ldg(a.rel + s) : 1.0;
         __syncthreads();  // previous sample done with cl / W / d buffers
         for (int k = tid; k < a.n_cells; k += kSubThreads) sm.cl[k] = __ldg(a.cells + k * S + s);
         __syncthreads();
@@ -731,7 +755,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
             dp[k] = 0.0;
             if (r < a.n_r) {
                 g[k] = a.gd[static_cast<std::size_t>(s) * a.g_stride + r];
-                dc[k] = -a.c0 * g[k];
+                dc[k] = -(a.c0 * rs) * g[k];
                 sm.d0[r] = dc[k];
             }
         }
@@ -741,7 +765,7 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
             const double* cur = (m & 1) ? sm.d0 : sm.d1;
             double* nxt = (m & 1) ? sm.d1 : sm.d0;
             const double beta = sm.beta[m - 1];
-            const double cm = sm.cm[m - 1];
+            const double cm = sm.cm[m - 1] * rs;
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
                 const int r = tid + k * kSubThreads;
@@ -907,6 +931,9 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
     const int base = lat_on ? ci * W + j0 : W + 1;
 
     for (int s = blockIdx.x; s < a.count; s += gridDim.x) {
+        // per-sample CFL: finished samples are left alone, dt^2 constants scale
+        if (a.nsteps && a.step > __ldg(a.nsteps + s)) continue;
+        const double rs = a.rel ? __ldg(a.rel + s) : 1.0;
         // ---- per-sample set-up: g staged coalesced into v1, coefficients,
         // generic weights
         double* gdrow = a.gd + static_cast<std::size_t>(s) * a.g_stride;
@@ -948,14 +975,14 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
         double d[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            d[k] = -a.c0 * gg[k];
+            d[k] = -(a.c0 * rs) * gg[k];
             if (k < len) sd[o.v0 + base + k] = d[k] * inv_h;
         }
         double gd[G], gdp[G];
 #pragma unroll
         for (int u = 0; u < G; ++u) {
             gdp[u] = 0.0;
-            gd[u] = -a.c0 * ggg[u];
+            gd[u] = -(a.c0 * rs) * ggg[u];
             if (grow[u] >= 0) sd[o.v0 + grow[u]] = gd[u] * grs[u];
         }
         __syncthreads();
@@ -966,7 +993,7 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
             const int cur = (m & 1) ? o.v0 : o.v1;
             const int nxt = (m & 1) ? o.v1 : o.v0;
             const double beta = sd[o.beta + m - 1];
-            const double cmm = sd[o.cm + m - 1];
+            const double cmm = sd[o.cm + m - 1] * rs;
             const double onepb = 1.0 + beta;
             double gaq[G];
 #pragma unroll
@@ -1031,6 +1058,143 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// K4: per-sample CFL step.  Power iteration of reference max_eigenvalue
+// (src/fem.cpp:132-175) for every sample of the batch at once: av = A(omega) v
+// (coarse: v masked on P, rows in P zeroed, :177-189), per-sample Rayleigh
+// quotient and |av| from fixed-order partial sums, the stopping rule
+// |r - r_prev| <= tol |r| three times in a row, v = av / |av|.
+
+__global__ void eig_init_kernel(const double* __restrict__ warm, double warm_norm, int n, int S, double* v) {
+    const std::size_t total = static_cast<std::size_t>(n) * S;
+    for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < total;
+         q += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+        v[q] = __ldg(warm + q / S) / warm_norm;
+}
+
+__global__ void __launch_bounds__(kSweepWarps * 32) eig_matvec_kernel(EigArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int row = grid_rowgroup(a.n) * kSweepWarps + (threadIdx.x >> 5);
+    if (row >= a.n) return;
+    const int s0 = grid_chunk(a.n) * kSweepChunk + 2 * lane;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    double acc0 = 0.0, acc1 = 0.0;
+    if (!(a.coarse && __ldg(a.in_p + row))) {
+        const int b = __ldg(a.row_ptr + row), e = __ldg(a.row_ptr + row + 1);
+        for (int k = b; k < e; ++k) {
+            const int pk = __ldg(a.ent + k);
+            const int j = pk & kColMask;
+            if (a.coarse && __ldg(a.in_p + j)) continue;
+            const double w = __ldg(a.a0 + k);
+            const int cell = static_cast<unsigned>(pk) >> kColBits;
+            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+            const double2 x = __ldg(reinterpret_cast<const double2*>(a.v + j * S + s0));
+            acc0 += (c.x * w) * x.x;
+            acc1 += (c.y * w) * x.y;
+        }
+    }
+    *reinterpret_cast<double2*>(a.av + static_cast<std::size_t>(row) * S + s0) = make_double2(acc0, acc1);
+}
+
+// partial sums of v.av and av.av over row block blockIdx.y, 64 samples per
+// block (2 per lane), rows of the block strided over its 8 warps
+__global__ void __launch_bounds__(kSweepWarps * 32) eig_dot_kernel(EigArgs a) {
+    __shared__ double2 red[2][kSweepWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int s0 = blockIdx.x * kSweepChunk + 2 * lane;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const int rows_per = (a.n + a.n_blocks - 1) / a.n_blocks;
+    const int r0 = blockIdx.y * rows_per, r1 = min(a.n, r0 + rows_per);
+    double2 va = make_double2(0.0, 0.0), aa = va;
+    for (int r = r0 + warp; r < r1; r += kSweepWarps) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(a.v + r * S + s0));
+        const double2 x = __ldg(reinterpret_cast<const double2*>(a.av + r * S + s0));
+        va.x += v.x * x.x;
+        va.y += v.y * x.y;
+        aa.x += x.x * x.x;
+        aa.y += x.y * x.y;
+    }
+    red[0][warp][lane] = va;
+    red[1][warp][lane] = aa;
+    __syncthreads();
+    if (warp == 0) {
+        for (int w = 1; w < kSweepWarps; ++w) {
+            va.x += red[0][w][lane].x;
+            va.y += red[0][w][lane].y;
+            aa.x += red[1][w][lane].x;
+            aa.y += red[1][w][lane].y;
+        }
+        double* p0 = a.part + static_cast<std::size_t>(blockIdx.y) * S + s0;
+        double* p1 = a.part + (static_cast<std::size_t>(a.n_blocks) + blockIdx.y) * S + s0;
+        *reinterpret_cast<double2*>(p0) = va;
+        *reinterpret_cast<double2*>(p1) = aa;
+    }
+}
+
+__global__ void eig_update_kernel(EigArgs a) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= a.S || a.done[s]) return;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    double ray = 0.0, nn = 0.0;
+    for (int b = 0; b < a.n_blocks; ++b) {
+        ray += a.part[static_cast<std::size_t>(b) * S + s];
+        nn += a.part[(static_cast<std::size_t>(a.n_blocks) + b) * S + s];
+    }
+    const double av_norm = sqrt(nn);
+    a.iters[s] += 1;
+    if (av_norm == 0.0) {  // zero operator
+        a.lam[s] = 0.0;
+        a.done[s] = 2;
+        return;
+    }
+    a.norm[s] = av_norm;
+    if (fabs(ray - a.lam_prev[s]) <= a.tol * fabs(ray)) {
+        if (++a.settled[s] >= 3) {
+            a.lam[s] = ray;
+            a.done[s] = 1;
+            return;
+        }
+    } else {
+        a.settled[s] = 0;
+    }
+    a.lam_prev[s] = ray;
+    atomicAdd(a.active_count, 1);
+}
+
+__global__ void eig_normalize_kernel(EigArgs a) {
+    const std::size_t total = static_cast<std::size_t>(a.n) * a.S;
+    double* v = const_cast<double*>(a.v);
+    for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < total;
+         q += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+        const int s = static_cast<int>(q % a.S);
+        if (!a.done[s]) v[q] = a.av[q] / a.norm[s];
+    }
+}
+
+__global__ void cfl_finalize_kernel(const double* lf, const double* lc, int use_coarse, int p_fine, double safety,
+                                    double T, double dt_ref, int count, int S, double* rel, int* nsteps) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    if (s >= count) {  // padding lanes: one step, unit scale (never read)
+        rel[s] = 1.0;
+        nsteps[s] = 1;
+        return;
+    }
+    const double margin = 1.05;
+    double dt;
+    if (use_coarse) {
+        const double dt_coarse = 2.0 / sqrt(margin * lc[s]);
+        const double dt_fine = p_fine * 2.0 / sqrt(margin * lf[s]);
+        dt = safety * fmin(dt_coarse, dt_fine);
+    } else {
+        dt = safety * 2.0 / sqrt(margin * lf[s]);
+    }
+    const double steps = ceil(T / dt - 1e-12);  // run_wave snapping (integrators.cpp:188-189)
+    const double dts = T / steps;
+    nsteps[s] = static_cast<int>(steps);
+    rel[s] = (dts / dt_ref) * (dts / dt_ref);
+}
+
+// ---------------------------------------------------------------------------
 // K3: QoI per sample, Q = sum_t w_t (z_t / sqrt(M_t)) over the box nodes in a
 // fixed order (deterministic); failed samples report NaN.
 
@@ -1039,9 +1203,10 @@ __global__ void qoi_kernel(QoIArgs a) {
     if (s >= a.count) return;
     const std::size_t S = static_cast<std::size_t>(a.S);
     double acc = 0.0;
+    const double* z = (a.nsteps && ((a.n_max - __ldg(a.nsteps + s)) & 1)) ? a.z_alt : a.z;
     for (int t = 0; t < a.nq; ++t) {
         const int i = __ldg(a.dof + t);
-        acc += __ldg(a.w + t) * (a.z[i * S + s] / __ldg(a.sqrt_mass + t));
+        acc += __ldg(a.w + t) * (z[i * S + s] / __ldg(a.sqrt_mass + t));
     }
     a.q[s] = a.fail[s] == INT_MAX ? acc : __longlong_as_double(0x7ff8000000000000LL);
 }
@@ -1239,6 +1404,25 @@ void launch_r_update(const RUpdateArgs& a, void* stream) {
 
 void launch_qoi(const QoIArgs& a, void* stream) {
     qoi_kernel<<<(a.count + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+}
+
+void launch_eig_init(const double* warm, double warm_norm, int n, int S, double* v, void* stream) {
+    eig_init_kernel<<<2 * 148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(warm, warm_norm, n, S, v);
+}
+
+void launch_eig_iteration(const EigArgs& a, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = ((a.n + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
+    eig_matvec_kernel<<<grid, kSweepWarps * 32, 0, st>>>(a);
+    eig_dot_kernel<<<dim3(a.S / kSweepChunk, a.n_blocks), kSweepWarps * 32, 0, st>>>(a);
+    eig_update_kernel<<<(a.S + 127) / 128, 128, 0, st>>>(a);
+    eig_normalize_kernel<<<2 * 148 * 8, 256, 0, st>>>(a);
+}
+
+void launch_cfl_finalize(const double* lf, const double* lc, int use_coarse, int p_fine, double safety, double T,
+                         double dt_ref, int count, int S, double* rel, int* nsteps, void* stream) {
+    cfl_finalize_kernel<<<(S + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        lf, lc, use_coarse, p_fine, safety, T, dt_ref, count, S, rel, nsteps);
 }
 
 void launch_fill_int(int* p, int value, int n, void* stream) {

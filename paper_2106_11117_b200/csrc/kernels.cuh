@@ -63,6 +63,8 @@ struct SweepArgs {
     double factor;       // init_factor or coarse_factor
     int step;
     int* fail;
+    const double* rel;   // per-sample CFL: (dt_s / dt)^2 scales every dt^2 constant (NULL: 1)
+    const int* nsteps;   // per-sample CFL: steps of sample s; later steps leave it untouched (NULL: all)
 };
 
 struct SubArgs {
@@ -79,6 +81,9 @@ struct SubArgs {
     const double* beta;   // p-1
     const double* cm;     // p-1
     double c0;
+    int step;             // global step being formed (per-sample CFL: skip finished samples)
+    const double* rel;
+    const int* nsteps;
 };
 
 // lattice substep kernel variants (threads, rows per thread, generic rows per
@@ -114,6 +119,9 @@ struct LatArgs {
     int g_stride;
     const double* beta;
     const double* cm;
+    int step;
+    const double* rel;
+    const int* nsteps;
 };
 
 // z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on the R rows (reference
@@ -125,6 +133,7 @@ struct RUpdateArgs {
     double* zp;
     int step;
     int* fail;
+    const int* nsteps;
 };
 
 // One LTS substep of the HBM-resident path (|R| too large for one SM): warp
@@ -149,6 +158,8 @@ struct GSubArgs {
     double* zp;
     int step;
     int* fail;
+    const double* rel;
+    const int* nsteps;
 };
 
 // Nested tiers (BASELINE config 2, no reference counterpart; DESIGN.md
@@ -189,6 +200,8 @@ struct TierArgs {
     double* zp;
     int step;
     int* fail;
+    const double* rel;
+    const int* nsteps;
 };
 
 struct QoIArgs {
@@ -199,6 +212,35 @@ struct QoIArgs {
     const double* z;
     const int* fail;
     double* q;
+    const double* z_alt;  // per-sample CFL: a sample that ended (n_max - nsteps[s]) odd steps early
+    const int* nsteps;    // holds its state in the other buffer
+    int n_max;
+};
+
+// Per-sample CFL step (reference stable_dt, src/experiments.cpp:30-43): batched
+// power iteration on A(omega) (full, and A (I-P) on rows outside P) from the
+// level's warm starts, per-sample Rayleigh quotients and stopping rule of
+// max_eigenvalue (src/fem.cpp:132-175).
+struct EigArgs {
+    int n, S, count;
+    const int* row_ptr;
+    const int* ent;
+    const double* a0;
+    const double* cells;
+    const unsigned char* in_p;
+    int coarse;           // 1: masked columns in P, zero rows in P
+    const double* v;      // [i][S]
+    double* av;
+    int n_blocks;         // row blocks of the dot-product partials
+    double* part;         // [2][n_blocks][S]: v.av, av.av
+    double* norm;         // per sample: |A v| of this iteration
+    double* lam;          // per sample: result
+    double* lam_prev;
+    int* settled;
+    int* iters;
+    int* done;            // 0 running, 1 settled, 2 zero operator
+    int* active_count;    // samples still running after this iteration
+    double tol;
 };
 
 // log-normal KL field on the cell grid: xi_m ~ N(0,1) by Box-Muller over
@@ -217,6 +259,12 @@ void launch_r_update(const RUpdateArgs& a, void* stream);
 void launch_global_substep(const GSubArgs& a, void* stream);
 void launch_tier_stage(const TierArgs& a, void* stream);
 void launch_fill_int(int* p, int value, int n, void* stream);
+void launch_eig_init(const double* warm, double warm_norm, int n, int S, double* v, void* stream);
+void launch_eig_iteration(const EigArgs& a, void* stream);
+// per sample: dt = safety min(2 / sqrt(1.05 lc), p_fine 2 / sqrt(1.05 lf)) (or the LF form), snapped to
+// T / ceil(T / dt - 1e-12); rel = (dt / dt_ref)^2, nsteps; padding lanes get rel 1 and 1 step
+void launch_cfl_finalize(const double* lf, const double* lc, int use_coarse, int p_fine, double safety, double T,
+                         double dt_ref, int count, int S, double* rel, int* nsteps, void* stream);
 void launch_pair_diff(const double* qf, const double* qc, double* dq, int count, void* stream);
 int substep_max_grid(int device, int smem_bytes);
 int lattice_smem_bytes(const LatArgs& a);

@@ -112,6 +112,7 @@ class LevelSpec:
     tiers: int = 1
     domain: tuple = (0.0, 1.0, 0.0, 1.0)
     qoi_mean: bool = False
+    cfl_safety: float = 0.0  # > 0: per-sample dt (reference stable_dt recipe)
 
     def desc(self) -> N.LevelDesc:
         d = N.LevelDesc()
@@ -129,6 +130,7 @@ class LevelSpec:
         for i, v in enumerate(self.domain):
             d.domain[i] = v
         d.qoi_mean = 1 if self.qoi_mean else 0
+        d.cfl_safety = self.cfl_safety
         return d
 
 

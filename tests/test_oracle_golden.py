@@ -138,3 +138,35 @@ def test_config4_kl_pairs_match_reference(golden, coracle):
     assert rc == 0
     assert _rel(qf, g[1]["q"][:2]) < 1e-12
     assert np.max(np.abs(dq - g[1]["dq"][:2])) < 1e-12 * np.max(np.abs(qf))
+
+
+def test_cfl_per_sample_dt_matches_reference(golden, coracle, config0_mesh):
+    """Per-sample CFL step (reference stable_dt, src/experiments.cpp:30-43, over
+    max_eigenvalue / coarse_max_eigenvalue, src/fem.cpp:132-189)."""
+    g = golden("cfl_samples.json")
+    d = configs.config0()
+    pb = problem(d.dt, d.substeps, 1, cfl_safety=g["safety"])
+    rc, _, qf, _, _ = coracle.eval_pairs(config0_mesh, pb, None, None, 0, 0, 0, len(g["config0_lts"]["q"]))
+    assert rc == 0 and _rel(qf, g["config0_lts"]["q"]) < 1e-12
+    pb = problem(d.dt, 1, 0, cfl_safety=g["safety"])
+    rc, _, qf, _, _ = coracle.eval_pairs(config0_mesh, pb, None, None, 0, 0, 0, len(g["config0_lf"]["q"]))
+    assert rc == 0 and _rel(qf, g["config0_lf"]["q"]) < 1e-12
+    # the step really is per sample and near the stability bound
+    rc, dt0, it0 = coracle.stable_dt(config0_mesh, problem(d.dt, d.substeps, 1, cfl_safety=0.9),
+                                     coracle.draw_cells(0, 0, 0))
+    rc, dt1, it1 = coracle.stable_dt(config0_mesh, problem(d.dt, d.substeps, 1, cfl_safety=0.9),
+                                     coracle.draw_cells(0, 0, 1))
+    assert rc == 0 and dt0 != dt1 and 2 * d.dt < dt0 < 4 * d.dt and min(it0) >= 3
+
+
+def test_cfl_pairs_match_reference(golden, coracle):
+    g = golden("cfl_samples.json")
+    c1 = configs.config1()
+    fine = MeshArrays(*configs.build_mesh(c1[1]).arrays())
+    coarse = MeshArrays(*configs.build_mesh(c1[0]).arrays())
+    lv = g["config1_pairs"]["levels"][1]
+    rc, dq, qf, _, _ = coracle.eval_pairs(fine, problem(c1[1].dt, c1[1].substeps, cfl_safety=g["safety"]), coarse,
+                                          problem(c1[0].dt, c1[0].substeps, cfl_safety=g["safety"]), 0, 1, 0, lv["N"])
+    assert rc == 0
+    assert _rel(qf, lv["q"]) < 1e-12
+    assert np.max(np.abs(dq - lv["dq"])) < 1e-12 * np.max(np.abs(qf))
