@@ -184,6 +184,13 @@ int wmc_kl_table(int cells_x, int cells_y, double sigma, double corr_len, int mo
 int wmc_level_draw(wmc_level* level, uint64_t seed, uint32_t level_index, uint64_t first, uint64_t count,
                    double* out);
 
+/* Per-sample CFL step (level created with cfl_safety > 0): the device power
+ * iterations for indices first..first+count-1 of MLMC level `level_index`,
+ * per sample the snapped step dt[i] = T / steps[i] (reference stable_dt,
+ * src/experiments.cpp:30-43, then run_wave's snapping). */
+int wmc_level_cfl(wmc_level* level, uint64_t seed, uint32_t level_index, uint64_t first, uint64_t count, double* dt,
+                  long* steps);
+
 /* Per-sample coefficients exactly as the device draws them (RNG parity). */
 int wmc_draw_cells(uint64_t seed, uint32_t level, uint64_t first, uint64_t count, int n_cells, double lo, double hi,
                    int device, double* out);

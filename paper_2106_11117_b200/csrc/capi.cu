@@ -1144,6 +1144,86 @@ void run_levels(wmc_level** levels, const std::vector<LevelJob>& jobs, std::uint
     }
 }
 
+// Per-level cache of evaluated pairs for the adaptive driver: results for
+// indices [0, computed) in index order.  A sample's (dQ, Q) depends only on
+// (seed, level, index) -- bitwise, whatever the batch it ran in -- so the
+// driver may evaluate ahead of its targets (batches are padded to 64 lanes
+// anyway, and the next level's warm-up can run beside the current wave) and
+// fold exactly the samples the reference's run_mlmc would (src/mlmc.cpp:165-233).
+struct PairCache {
+    std::vector<double> dq, qf;
+    std::vector<int> ff, fc;  // fail steps (INT_MAX: fine)
+    long computed = 0;
+};
+
+// One wave: evaluate, on every level that needs more than its cache holds,
+// the missing indices rounded up to the 64-lane batch granule (plus `spec`:
+// the first 64 pairs of a level not yet in use), levels concurrently on their
+// streams; then fold into acc up to the targets in (level, index) order.
+void cached_wave(wmc_level** levels, int n_levels, const std::vector<long>& targets, int spec, std::uint64_t seed,
+                 std::vector<Acc>& acc, std::vector<PairCache>& cache, wmc_error* err) {
+    struct Issue {
+        int level;
+        long first, count;
+    };
+    std::vector<Issue> issues;
+    for (int l = 0; l < static_cast<int>(targets.size()); ++l)
+        if (targets[l] > cache[l].computed) {
+            const long need = targets[l] - cache[l].computed;
+            issues.push_back({l, cache[l].computed, (need + 63) / 64 * 64});
+        }
+    if (spec >= 0 && spec < n_levels && cache[spec].computed == 0) issues.push_back({spec, 0, 64});
+    for (const auto& j : issues) {
+        ensure_results(*levels[j.level], static_cast<std::size_t>(j.count));
+        issue_pairs(levels[j.level], j.level > 0 ? levels[j.level - 1] : nullptr, seed,
+                    static_cast<std::uint32_t>(j.level), static_cast<std::uint64_t>(j.first),
+                    static_cast<std::uint64_t>(j.count), nullptr, nullptr);
+    }
+    for (const auto& j : issues) {
+        wmc_level* fine = levels[j.level];
+        check(cudaSetDevice(fine->device), "cudaSetDevice");
+        check(cudaStreamSynchronize(fine->stream), "synchronize");
+        PairCache& c = cache[j.level];
+        c.dq.insert(c.dq.end(), fine->h_dq, fine->h_dq + j.count);
+        c.qf.insert(c.qf.end(), fine->h_qf, fine->h_qf + j.count);
+        c.ff.insert(c.ff.end(), fine->h_ff, fine->h_ff + j.count);
+        if (j.level > 0)
+            c.fc.insert(c.fc.end(), fine->h_fc, fine->h_fc + j.count);
+        else
+            c.fc.insert(c.fc.end(), j.count, INT_MAX);
+        c.computed += j.count;
+    }
+    if (err) err->sample = -1;
+    for (int l = 0; l < static_cast<int>(targets.size()); ++l) {
+        Acc& a = acc[l];
+        const PairCache& c = cache[l];
+        const long from = a.n;
+        for (long i = from; i < targets[l]; ++i) {
+            const bool bad_f = c.ff[i] != INT_MAX, bad_c = c.fc[i] != INT_MAX;
+            if (bad_f || bad_c) {
+                if (err) {
+                    err->sample = i;
+                    err->step = bad_f ? c.ff[i] : c.fc[i];
+                    err->level = bad_f ? l : l - 1;
+                }
+                g_last_error = "level " + std::to_string(l) + ", sample " + std::to_string(i) +
+                               ": time integration unstable";
+                throw NumericalError(g_last_error);
+            }
+            a.add(c.dq[i], c.qf[i]);
+        }
+        if (targets[l] > from) {
+            wmc_cost cc{};
+            pair_cost(levels[l], l > 0 ? levels[l - 1] : nullptr, static_cast<std::uint64_t>(targets[l] - from), &cc);
+            a.cost.matvec_full += cc.matvec_full;
+            a.cost.matvec_fine += cc.matvec_fine;
+            a.cost.matvec_coarse += cc.matvec_coarse;
+            a.cost.weighted_work += cc.weighted_work;
+            a.cost.dof_updates += cc.dof_updates;
+        }
+    }
+}
+
 }  // namespace
 
 namespace {
@@ -1477,6 +1557,26 @@ int wmc_level_draw(wmc_level* L, uint64_t seed, uint32_t level_index, uint64_t f
     });
 }
 
+int wmc_level_cfl(wmc_level* L, uint64_t seed, uint32_t level_index, uint64_t first, uint64_t count, double* dt,
+                  long* steps) {
+    return guarded([&] {
+        if (!L || !dt || !steps) throw ConfigError("wmc_level_cfl: NULL argument");
+        if (!(L->tab.cfl_safety > 0.0)) throw ConfigError("wmc_level_cfl: level has no per-sample CFL");
+        check(cudaSetDevice(L->device), "cudaSetDevice");
+        Workspace& w = workspace(*L, 0);
+        for (std::uint64_t off = 0; off < count; off += L->batch) {
+            const int c = static_cast<int>(std::min<std::uint64_t>(L->batch, count - off));
+            const int S = round64(c);
+            launch_draw(*L, seed, level_index, first + off, c, S, L->d_cells, L->stream);
+            cfl_phase(*L, w, L->d_cells, S, c, L->stream);
+            for (int i = 0; i < c; ++i) {
+                steps[off + i] = w.h_nsteps[i];
+                dt[off + i] = L->spec.final_time / static_cast<double>(w.h_nsteps[i]);
+            }
+        }
+    });
+}
+
 int wmc_draw_cells(uint64_t seed, uint32_t level, uint64_t first, uint64_t count, int n_cells, double lo, double hi,
                    int device, double* out) {
     return guarded([&] {
@@ -1542,12 +1642,19 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
             return worst;
         };
         bool converged = false;
+        std::vector<PairCache> cache(n_levels);
+        const bool no_ahead = std::getenv("WMC_MLMC_NO_AHEAD") != nullptr;  // A/B knob: plain waves
         {
             while (true) {
-                std::vector<LevelJob> jobs;
-                for (int l = 0; l <= top; ++l)
-                    if (acc[l].n < targets[l]) jobs.push_back({l, acc[l].n, targets[l] - acc[l].n});
-                run_levels(levels, jobs, cfg->master_seed, acc, err);
+                if (no_ahead) {
+                    std::vector<LevelJob> jobs;
+                    for (int l = 0; l <= top; ++l)
+                        if (acc[l].n < targets[l]) jobs.push_back({l, acc[l].n, targets[l] - acc[l].n});
+                    run_levels(levels, jobs, cfg->master_seed, acc, err);
+                } else {
+                    cached_wave(levels, n_levels, targets, top + 1 <= cap ? top + 1 : -1, cfg->master_seed, acc,
+                                cache, err);
+                }
                 std::vector<double> v(top + 1);
                 for (int l = 0; l <= top; ++l) v[l] = acc[l].variance();
                 const std::vector<long> wanted = optimal_samples_impl(v.data(), model_cost, top + 1, cfg->eps, 2);

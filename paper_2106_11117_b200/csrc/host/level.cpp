@@ -519,11 +519,19 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
             }
             p1.push_back(static_cast<int>(c1.size()));
         }
+        // the start vector is keyed by the reference's DOF index (interior
+        // vertices in vertex order), not by this level's DOF permutation
+        std::vector<int> ref_index(nv, -1);
+        for (int v = 0, k = 0; v < nv; ++v)
+            if (!mesh.boundary_vertex[v]) ref_index[v] = k++;
         auto power = [&](bool coarse) {
             const int n = L.n;
             std::vector<double> v(n), av(n);
             for (int i = 0; i < n; ++i)
-                v[i] = static_cast<double>(mix64_host(static_cast<std::uint64_t>(i) + 1) >> 11) * 0x1.0p-53 - 0.5;
+                v[i] = static_cast<double>(
+                           mix64_host(static_cast<std::uint64_t>(ref_index[L.dof_vertex[i]]) + 1) >> 11) *
+                           0x1.0p-53 -
+                       0.5;
             double norm = 0.0;
             for (double x : v) norm += x * x;
             norm = std::sqrt(norm);

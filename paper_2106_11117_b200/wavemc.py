@@ -213,6 +213,15 @@ def level_draw(level: "Level", seed: int, level_index: int, first: int, count: i
     return out
 
 
+def level_cfl(level: Level, seed: int, level_index: int, first: int, count: int):
+    """Per-sample snapped CFL step and step count as the device computes them."""
+    dt = np.zeros(count, np.float64)
+    steps = np.zeros(count, np.int64)
+    N.check(N.lib().wmc_level_cfl(level._h, seed, level_index, first, count, _dptr(dt),
+                                  steps.ctypes.data_as(C.POINTER(C.c_long))))
+    return dt, steps
+
+
 def draw_cells(seed: int, level: int, first: int, count: int, n_cells: int = 16, lo: float = 0.5,
                hi: float = 1.5, device: int = 0) -> np.ndarray:
     out = np.empty((count, n_cells), np.float64)

@@ -96,3 +96,18 @@ def test_cfl_nested_tiers_match_c_oracle(coracle):
     rc, _, oq, _, _ = coracle.eval_pairs(MeshArrays(*configs.build_mesh(d).arrays()), pb, None, None, 0, 0, 0, 6)
     assert rc == 0
     assert per_sample_rel(qf, oq) < QOI_RTOL
+
+
+@pytest.mark.parametrize("kind", ["lts", "lf"])
+def test_cfl_per_sample_steps_match_c_oracle(coracle, kind):
+    """The device's per-sample (snapped) dt and step count against the C
+    restatement of stable_dt (itself pinned to the reference above)."""
+    d = configs.config0() if kind == "lts" else configs.config0_leapfrog()
+    lv = _level(d, 0.9)
+    dt, steps = wavemc.level_cfl(lv, 0, 0, 0, 70)
+    ma = MeshArrays(*configs.build_mesh(d).arrays())
+    pb = problem(d.dt, d.substeps, 1 if kind == "lts" else 0, cfl_safety=0.9)
+    for i in (0, 1, 2, 33, 69):
+        rc, odt, _ = coracle.stable_dt(ma, pb, coracle.draw_cells(0, 0, i))
+        n = int(np.ceil(1.0 / odt - 1e-12))
+        assert rc == 0 and steps[i] == n and abs(dt[i] - 1.0 / n) <= 1e-15, (i, steps[i], n)

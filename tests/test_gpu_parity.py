@@ -299,3 +299,19 @@ def test_config4_adaptive_mlmc_matches_reference(golden):
     assert res.estimate == pytest.approx(g["estimate"], rel=MOMENT_RTOL)
     for got, want in zip(res.levels, g["levels"]):
         assert got["variance"] == pytest.approx(want["variance"], rel=MOMENT_RTOL)
+
+
+def test_adaptive_driver_evaluate_ahead_is_invisible(monkeypatch):
+    """The driver's evaluate-ahead cache (64-lane granules, next level's
+    warm-up beside the current wave) folds exactly the reference's samples:
+    same N_l, bitwise the same estimate and sums as plain waves."""
+    levels = [configs.build_level(d) for d in configs.config1()[:4]]
+    costs = [lv.info["dof_updates_per_solve"] for lv in levels]
+    cfg = wavemc.MlmcConfig(eps=3e-4)
+    a = wavemc.run_mlmc(levels, costs, cfg)
+    monkeypatch.setenv("WMC_MLMC_NO_AHEAD", "1")
+    b = wavemc.run_mlmc(levels, costs, cfg)
+    assert [s["n_samples"] for s in a.levels] == [s["n_samples"] for s in b.levels]
+    assert a.estimate == b.estimate and a.rmse == b.rmse
+    for x, y in zip(a.levels, b.levels):
+        assert x["sum_dq"] == y["sum_dq"] and x["sum_q2"] == y["sum_q2"]
