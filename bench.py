@@ -525,14 +525,33 @@ def roofline_from_profile(levels, counts, prof, step_ms):
                            "achieved_GBps": gbps(sub_bytes, sub_ms)},
                "r_update": {"ms": upd_ms, "launches": sum(p["upd_launches"] for p in prof),
                             "share_of_step": upd_ms / step_ms if step_ms else None}}
+    # DRAM traffic per launch: the measured/algorithmic ratio of the committed
+    # ncu capture (profiles/traffic.json) times this run's algorithmic bytes
+    # per launch
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            cap = json.load(f)
+    except OSError:
+        cap = {}
+
+    def traffic(key, alg_bytes, launches):
+        c = cap.get(key) or {}
+        if not launches or not c.get("algorithmic_bytes"):
+            return None, None
+        return c["dram_bytes"] / c["algorithmic_bytes"] * alg_bytes / launches, c.get("launch")
+
     if global_path and sub_ms >= sweep_ms:
         tiers = any(lv.info["substep_path"] == 4 for lv in levels)
-        roof = {"bound": "hbm", "kernel": "tier_stage" if tiers else "global_substep",
-                "achieved": kernels["substep"]["achieved_GBps"],
-                "unit": "GB/s", "traffic": None, "note": "dominant kernel, HBM-resident substeps (algorithmic bytes)"}
+        key = "tier_stage" if tiers else "global_substep"
+        t, src = traffic(key, sub_bytes, kernels["substep"]["launches"])
+        roof = {"bound": "hbm", "kernel": key, "achieved": kernels["substep"]["achieved_GBps"],
+                "unit": "GB/s", "traffic": t, "traffic_capture": src,
+                "note": ("dominant kernel, HBM-resident substeps (algorithmic bytes); traffic per global step's "
+                         "group of substep launches")}
     else:
+        t, src = traffic("sweep", sweep_bytes, kernels["sweep"]["launches"])
         roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",
-                "traffic": None,
+                "traffic": t, "traffic_capture": src,
                 "note": ("HBM roofline of the sweep kernel (algorithmic bytes); the dominant substep kernel is "
                          "on-chip (shared-memory) bound, see kernels.substep")}
     return roof, kernels
