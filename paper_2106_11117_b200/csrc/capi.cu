@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <exception>
 #include <memory>
 #include <stdexcept>
@@ -189,6 +191,13 @@ struct wmc_level {
     int* h_fc = nullptr;
     // optional per-kernel event timing (profiling pass only)
     bool profile = false;
+    // captured batch launch sequences, keyed by (workspace, S, count, cells)
+    struct BatchGraph {
+        bool seen = false;
+        cudaGraphExec_t exec = nullptr;
+        long nodes = 0;
+    };
+    std::map<std::tuple<const void*, int, int, const void*>, BatchGraph> graphs;
     std::vector<cudaEvent_t> ev_sweep, ev_sub, ev_upd;  // start/stop pairs
 
     ~wmc_level() {
@@ -221,6 +230,8 @@ struct wmc_level {
             if (p) cudaFree(p);
         for (void* p : {(void*)h_dq, (void*)h_qf, (void*)h_ff, (void*)h_fc})
             if (p) cudaFreeHost(p);
+        for (auto& kv : graphs)
+            if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
         for (auto e : ev_sweep) cudaEventDestroy(e);
         for (auto e : ev_sub) cudaEventDestroy(e);
         for (auto e : ev_upd) cudaEventDestroy(e);
@@ -703,15 +714,12 @@ long cfl_phase(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
     return n_max;
 }
 
-void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
+void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream,
+                          long n_steps, const double* rel, const int* nsteps) {
     const wmc::LevelTables& t = L.tab;
     const bool lts = L.path != SubPath::None;
     const bool global = L.path == SubPath::Global;
     const bool tiers = L.path == SubPath::Tiers;
-    const bool cfl = t.cfl_safety > 0.0;
-    const long n_steps = cfl ? cfl_phase(L, ws, cells, S, count, stream) : t.n_steps;
-    const double* rel = cfl ? ws.rel : nullptr;
-    const int* nsteps = cfl ? ws.nsteps : nullptr;
     wmc::launch_fill_int(ws.fail, INT_MAX, S, stream);
 
     wmc::SweepArgs sw{};
@@ -899,6 +907,47 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     wmc::launch_qoi(qa, stream);
     ++g_launches;
     check(cudaGetLastError(), "kernel launch");
+}
+
+// One batch of solves.  The whole launch sequence of a batch (start-up
+// sweep, n_steps x {sweep, substeps, update}, QoI) depends only on the
+// level, the workspace, the batch shape and the coefficient buffer, so from
+// its second use it is replayed as a CUDA graph captured once: one launch
+// per batch instead of ~3 n_steps (small batches of the adaptive driver are
+// launch-bound).  Per-sample CFL batches (host-synchronised power
+// iterations) and profiled runs take the plain path; WMC_NO_GRAPH=1 forces it.
+void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
+    const wmc::LevelTables& t = L.tab;
+    if (t.cfl_safety > 0.0) {
+        const long n_steps = cfl_phase(L, ws, cells, S, count, stream);
+        solve_batch_launches(L, ws, cells, S, count, stream, n_steps, ws.rel, ws.nsteps);
+        return;
+    }
+    static const bool no_graph = std::getenv("WMC_NO_GRAPH") != nullptr || std::getenv("WMC_SYNC_DEBUG") != nullptr;
+    if (no_graph || L.profile) {
+        solve_batch_launches(L, ws, cells, S, count, stream, t.n_steps, nullptr, nullptr);
+        return;
+    }
+    auto& g = L.graphs[std::make_tuple(static_cast<const void*>(&ws), S, count, static_cast<const void*>(cells))];
+    if (!g.seen) {  // first use: plain launches (one-time attribute setup, allocations)
+        g.seen = true;
+        solve_batch_launches(L, ws, cells, S, count, stream, t.n_steps, nullptr, nullptr);
+        return;
+    }
+    if (!g.exec) {
+        cudaGraph_t graph = nullptr;
+        const long before = g_launches.load();
+        check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "graph capture");
+        solve_batch_launches(L, ws, cells, S, count, stream, t.n_steps, nullptr, nullptr);
+        check(cudaStreamEndCapture(stream, &graph), "graph capture");
+        g.nodes = g_launches.load() - before;
+        g_launches -= g.nodes;  // counted when replayed
+        const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        check(e, "graph instantiate");
+    }
+    check(cudaGraphLaunch(g.exec, stream), "graph launch");
+    g_launches += g.nodes;
 }
 
 void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S,
