@@ -136,6 +136,7 @@ typedef struct {
     int tiers;                /* nested LTS tiers in use */
     int n_r_tier[8];          /* |R_k| for tiers k = 1..tiers (n_r_tier[0] == n_r), rows [0, |R_k|) */
     long n_structured;        /* sweep rows taking the structured 5-point path (0 before device setup) */
+    int nq;                   /* QoI outputs per sample (1: scalar; the experiments' output grid) */
 } wmc_level_info;
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);
@@ -238,6 +239,12 @@ typedef struct {
  * model_cost[l] per level; stats must hold n_levels entries. */
 int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
                  wmc_mlmc_result* result, wmc_level_stats* stats, wmc_error* err);
+
+/* Same driver for QoI vectors (the reference experiments' grid QoIs): also
+ * writes the estimate vector (nq outputs, wmc_level_info.nq) to `estimate`;
+ * result->estimate then holds its norm. */
+int wmc_run_mlmc_vec(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
+                     wmc_mlmc_result* result, wmc_level_stats* stats, double* estimate, wmc_error* err);
 
 /* Host-only helpers of the adaptive driver, as the reference's
  * optimal_samples (src/mlmc.cpp:75-92) and bias_proxy_sq (:94-98). */

@@ -46,7 +46,7 @@ class LevelInfo(C.Structure):
                 ("dt", C.c_double), ("nnz", C.c_long), ("ap_nnz", C.c_long), ("n_recipes", C.c_long),
                 ("batch", C.c_int), ("dof_updates_per_solve", C.c_double), ("lattice", C.c_int),
                 ("substep_path", C.c_int), ("tiers", C.c_int), ("n_r_tier", C.c_int * 8),
-                ("n_structured", C.c_long)]
+                ("n_structured", C.c_long), ("nq", C.c_int)]
 
 
 class Cost(C.Structure):
@@ -109,6 +109,8 @@ SIGNATURES = [
                                      P(Error)]),
     ("wmc_mlmc_config_default", None, [P(MlmcConfig)]),
     ("wmc_run_mlmc", C.c_int, [P(_VP), C.c_int, _DP, P(MlmcConfig), P(MlmcResult), P(LevelStats), P(Error)]),
+    ("wmc_run_mlmc_vec", C.c_int, [P(_VP), C.c_int, _DP, P(MlmcConfig), P(MlmcResult), P(LevelStats), _DP,
+                                   P(Error)]),
     ("wmc_optimal_samples", C.c_int, [_DP, _DP, C.c_int, C.c_double, C.c_long, P(C.c_long)]),
     ("wmc_bias_proxy_sq", C.c_double, [C.c_double, C.c_double]),
     ("wmc_moments_device", C.c_int, [_VP, _VP, _VP, C.c_uint64, _VP]),

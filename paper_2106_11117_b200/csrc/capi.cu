@@ -149,6 +149,7 @@ struct wmc_level {
     double warm_full_norm = 0.0, warm_coarse_norm = 0.0;
     unsigned char* d_in_p = nullptr;
     // QoI
+    int* d_qptr = nullptr;
     int* d_qdof = nullptr;
     double* d_qw = nullptr;
     double* d_qsm = nullptr;
@@ -204,7 +205,7 @@ struct wmc_level {
         cudaSetDevice(device);
         for (void* p : {(void*)d_row_ptr, (void*)d_row_desc, (void*)d_wtype, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
                         (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
-                        (void*)d_cm, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
+                        (void*)d_cm, (void*)d_qptr, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
@@ -384,6 +385,7 @@ void build_device_level(wmc_level& L) {
         }
         L.d_in_p = upload(t.in_p);
     }
+    L.d_qptr = upload(t.qoi_ptr);
     L.d_qdof = upload(t.qoi_dof);
     L.d_qw = upload(t.qoi_w);
     L.d_qsm = upload(t.sqrt_mass_qoi);
@@ -529,7 +531,7 @@ Workspace& workspace(wmc_level& L, int role) {
         alloc(&w.zb, S * t.n);
         alloc(&w.g, S * static_cast<std::size_t>(g_stride(t)));
         alloc(&w.fail, S);
-        alloc(&w.q, S);
+        alloc(&w.q, S * t.nq);
         if (L.path == SubPath::Global) {
             alloc(&w.da, S * t.n_r);
             alloc(&w.db, S * t.n_r);
@@ -892,7 +894,8 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
         std::swap(cur, prev);
     }
     wmc::QoIArgs qa{};
-    qa.nq = static_cast<int>(t.qoi_dof.size());
+    qa.nq = t.nq;
+    qa.ptr = L.d_qptr;
     qa.S = S;
     qa.count = count;
     qa.dof = L.d_qdof;
@@ -960,6 +963,7 @@ void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, st
 }
 
 void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
+    if (coarse && coarse->tab.nq != fine->tab.nq) throw ConfigError("wmc_eval_pairs: QoI sizes differ");
     if (!fine) throw ConfigError("eval_pairs: fine level is NULL");
     if (!coarse) return;
     if (fine->device != coarse->device) throw ConfigError("eval_pairs: levels on different devices");
@@ -1010,12 +1014,13 @@ void ensure_results(wmc_level& L, std::size_t count) {
     for (void* p : {(void*)L.h_dq, (void*)L.h_qf, (void*)L.h_ff, (void*)L.h_fc})
         if (p) cudaFreeHost(p);
     const std::size_t cap = std::max<std::size_t>(count, 256);
-    check(cudaMalloc(&L.r_dq, sizeof(double) * cap), "cudaMalloc results");
-    check(cudaMalloc(&L.r_qf, sizeof(double) * cap), "cudaMalloc results");
+    const std::size_t nq = static_cast<std::size_t>(L.tab.nq);
+    check(cudaMalloc(&L.r_dq, sizeof(double) * cap * nq), "cudaMalloc results");
+    check(cudaMalloc(&L.r_qf, sizeof(double) * cap * nq), "cudaMalloc results");
     check(cudaMalloc(&L.r_ff, sizeof(int) * cap), "cudaMalloc results");
     check(cudaMalloc(&L.r_fc, sizeof(int) * cap), "cudaMalloc results");
-    check(cudaMallocHost(&L.h_dq, sizeof(double) * cap), "cudaMallocHost");
-    check(cudaMallocHost(&L.h_qf, sizeof(double) * cap), "cudaMallocHost");
+    check(cudaMallocHost(&L.h_dq, sizeof(double) * cap * nq), "cudaMallocHost");
+    check(cudaMallocHost(&L.h_qf, sizeof(double) * cap * nq), "cudaMallocHost");
     check(cudaMallocHost(&L.h_ff, sizeof(int) * cap), "cudaMallocHost");
     check(cudaMallocHost(&L.h_fc, sizeof(int) * cap), "cudaMallocHost");
     L.r_cap = cap;
@@ -1045,13 +1050,10 @@ void issue_pairs(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::ui
             wc = &workspace(*coarse, 1);
             solve_batch(*coarse, *wc, fine->d_cells, S, c, st);
         }
-        double* dq_dst = to_host ? fine->r_dq + off : dev_dq + off;
-        double* qf_dst = to_host ? fine->r_qf + off : dev_qf;
-        wmc::launch_pair_diff(wf.q, wc ? wc->q : nullptr, dq_dst, c, st);
-        if (qf_dst)
-            check(cudaMemcpyAsync(to_host ? qf_dst : qf_dst + off, wf.q, sizeof(double) * c, cudaMemcpyDeviceToDevice,
-                                  st),
-                  "copy q");
+        const int nq = fine->tab.nq;
+        double* dq_dst = (to_host ? fine->r_dq : dev_dq) + off * nq;
+        double* qf_dst = to_host ? fine->r_qf + off * nq : (dev_qf ? dev_qf + off * nq : nullptr);
+        wmc::launch_pair_diff(wf.q, wc ? wc->q : nullptr, dq_dst, qf_dst, c, S, nq, st);
         if (to_host) {
             check(cudaMemcpyAsync(fine->r_ff + off, wf.fail, sizeof(int) * c, cudaMemcpyDeviceToDevice, st), "fail");
             if (wc)
@@ -1060,8 +1062,9 @@ void issue_pairs(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::ui
         }
     }
     if (to_host) {
-        check(cudaMemcpyAsync(fine->h_dq, fine->r_dq, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "dq");
-        check(cudaMemcpyAsync(fine->h_qf, fine->r_qf, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "q");
+        const std::size_t nq = static_cast<std::size_t>(fine->tab.nq);
+        check(cudaMemcpyAsync(fine->h_dq, fine->r_dq, sizeof(double) * count * nq, cudaMemcpyDeviceToHost, st), "dq");
+        check(cudaMemcpyAsync(fine->h_qf, fine->r_qf, sizeof(double) * count * nq, cudaMemcpyDeviceToHost, st), "q");
         check(cudaMemcpyAsync(fine->h_ff, fine->r_ff, sizeof(int) * count, cudaMemcpyDeviceToHost, st), "fail");
         if (coarse)
             check(cudaMemcpyAsync(fine->h_fc, fine->r_fc, sizeof(int) * count, cudaMemcpyDeviceToHost, st), "fail");
@@ -1110,50 +1113,73 @@ void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std
     } else {
         issue_pairs(fine, coarse, seed, level, first, count, nullptr, nullptr);
         finish_pairs(fine, coarse != nullptr, level, first, count, err);
-        if (host_dq) std::memcpy(host_dq, fine->h_dq, sizeof(double) * count);
-        if (host_qf) std::memcpy(host_qf, fine->h_qf, sizeof(double) * count);
+        const std::size_t nq = static_cast<std::size_t>(fine->tab.nq);
+        if (host_dq) std::memcpy(host_dq, fine->h_dq, sizeof(double) * count * nq);
+        if (host_qf) std::memcpy(host_qf, fine->h_qf, sizeof(double) * count * nq);
     }
     if (cost) pair_cost(fine, coarse, count, cost);
 }
 
+// LevelAccumulator (reference src/mlmc.cpp:39-73) on QoI vectors of nq
+// outputs with the norm weights w (QoIVector::norm, fem.cpp:15-19: sqrt of
+// sum_k w_k v_k^2); the BASELINE scalar QoI is nq = 1, w = 1.
 struct Acc {
     long n = 0;
-    double s_dq = 0.0, s_dq2 = 0.0, s_q = 0.0, s_q2 = 0.0;
+    std::vector<double> s_dq, s_q, w;
+    double s_dq2 = 0.0, s_q2 = 0.0;
     wmc_cost cost{};
-    // LevelAccumulator::add (reference src/mlmc.cpp:44-53) on the scalar
-    // QoI; QoIVector::norm() of the 2-point encoding is sqrt(1*v*v)
-    void add(double dq, double q) {
+    void init(const std::vector<double>& weights) {
+        if (!w.empty()) return;
+        w = weights;
+        s_dq.assign(w.size(), 0.0);
+        s_q.assign(w.size(), 0.0);
+    }
+    double norm(const double* v) const {
+        double acc = 0.0;
+        for (std::size_t k = 0; k < w.size(); ++k) acc += w[k] * v[k] * v[k];
+        return std::sqrt(acc);
+    }
+    void add(const double* dq, const double* q) {
         ++n;
-        const double a = std::sqrt(dq * dq), b = std::sqrt(q * q);
+        const double a = norm(dq), b = norm(q);
         s_dq2 += a * a;
         s_q2 += b * b;
-        s_dq += dq;
-        s_q += q;
+        for (std::size_t k = 0; k < w.size(); ++k) {
+            s_dq[k] += dq[k];
+            s_q[k] += q[k];
+        }
     }
     // estimate_variance / estimate_mc_variance (src/mlmc.cpp:61-73)
     double variance() const {
         if (n < 2) throw NumericalError("estimate_variance: need at least two samples");
-        const double nn = static_cast<double>(n), sn = std::sqrt(s_dq * s_dq);
+        const double nn = static_cast<double>(n), sn = norm(s_dq.data());
         return std::max(0.0, (s_dq2 - sn * sn / nn) / (nn - 1.0));
     }
     double mc_variance() const {
         if (n < 2) throw NumericalError("estimate_mc_variance: need at least two samples");
-        const double nn = static_cast<double>(n), sn = std::sqrt(s_q * s_q);
+        const double nn = static_cast<double>(n), sn = norm(s_q.data());
         return std::max(0.0, (s_q2 - sn * sn / nn) / nn);
     }
-    double mean_dq() const { return n > 0 ? s_dq * (1.0 / static_cast<double>(n)) : 0.0; }
+    std::vector<double> mean_dq() const {
+        std::vector<double> m(s_dq);
+        const double f = n > 0 ? 1.0 / static_cast<double>(n) : 0.0;
+        for (double& x : m) x *= f;
+        return m;
+    }
+    double mean_dq_norm() const { return w.empty() ? 0.0 : norm(mean_dq().data()); }
 };
 
 void fill_stats(int level, const Acc& a, double model_cost, wmc_level_stats& s) {
     s.level = level;
     s.n_samples = a.n;
-    s.sum_dq = a.s_dq;
+    // scalar QoI: the sums themselves; QoI vectors: their norms
+    s.sum_dq = a.w.size() == 1 ? a.s_dq[0] : (a.w.empty() ? 0.0 : a.norm(a.s_dq.data()));
     s.sum_dq2 = a.s_dq2;
-    s.sum_q = a.s_q;
+    s.sum_q = a.w.size() == 1 ? a.s_q[0] : (a.w.empty() ? 0.0 : a.norm(a.s_q.data()));
     s.sum_q2 = a.s_q2;
     s.variance = a.n >= 2 ? a.variance() : 0.0;
     s.mc_variance = a.n >= 2 ? a.mc_variance() : 0.0;
-    s.mean_dq = a.mean_dq();
+    s.mean_dq = a.w.size() == 1 ? a.mean_dq()[0] : a.mean_dq_norm();
     s.model_cost = model_cost;
     s.cost = a.cost;
 }
@@ -1182,7 +1208,9 @@ void run_levels(wmc_level** levels, const std::vector<LevelJob>& jobs, std::uint
         finish_pairs(fine, j.level > 0, static_cast<std::uint32_t>(j.level), static_cast<std::uint64_t>(j.first),
                      static_cast<std::uint64_t>(j.count), err);
         Acc& a = acc[j.level];
-        for (long i = 0; i < j.count; ++i) a.add(fine->h_dq[i], fine->h_qf[i]);
+        a.init(fine->tab.qoi_norm_w);
+        const int nq = fine->tab.nq;
+        for (long i = 0; i < j.count; ++i) a.add(fine->h_dq + i * nq, fine->h_qf + i * nq);
         wmc_cost c{};
         pair_cost(fine, j.level > 0 ? levels[j.level - 1] : nullptr, static_cast<std::uint64_t>(j.count), &c);
         a.cost.matvec_full += c.matvec_full;
@@ -1233,8 +1261,9 @@ void cached_wave(wmc_level** levels, int n_levels, const std::vector<long>& targ
         check(cudaSetDevice(fine->device), "cudaSetDevice");
         check(cudaStreamSynchronize(fine->stream), "synchronize");
         PairCache& c = cache[j.level];
-        c.dq.insert(c.dq.end(), fine->h_dq, fine->h_dq + j.count);
-        c.qf.insert(c.qf.end(), fine->h_qf, fine->h_qf + j.count);
+        const long nq = fine->tab.nq;
+        c.dq.insert(c.dq.end(), fine->h_dq, fine->h_dq + j.count * nq);
+        c.qf.insert(c.qf.end(), fine->h_qf, fine->h_qf + j.count * nq);
         c.ff.insert(c.ff.end(), fine->h_ff, fine->h_ff + j.count);
         if (j.level > 0)
             c.fc.insert(c.fc.end(), fine->h_fc, fine->h_fc + j.count);
@@ -1245,7 +1274,9 @@ void cached_wave(wmc_level** levels, int n_levels, const std::vector<long>& targ
     if (err) err->sample = -1;
     for (int l = 0; l < static_cast<int>(targets.size()); ++l) {
         Acc& a = acc[l];
+        a.init(levels[l]->tab.qoi_norm_w);
         const PairCache& c = cache[l];
+        const long nq = levels[l]->tab.nq;
         const long from = a.n;
         for (long i = from; i < targets[l]; ++i) {
             const bool bad_f = c.ff[i] != INT_MAX, bad_c = c.fc[i] != INT_MAX;
@@ -1259,7 +1290,7 @@ void cached_wave(wmc_level** levels, int n_levels, const std::vector<long>& targ
                                ": time integration unstable";
                 throw NumericalError(g_last_error);
             }
-            a.add(c.dq[i], c.qf[i]);
+            a.add(c.dq.data() + i * nq, c.qf.data() + i * nq);
         }
         if (targets[l] > from) {
             wmc_cost cc{};
@@ -1294,11 +1325,12 @@ std::vector<long> optimal_samples_impl(const double* v, const double* c, int n, 
 }
 
 // reference bias_proxy_sq (src/mlmc.cpp:94-98) on the scalar QoI
-double bias_proxy_impl(double mean_dq, double alpha) {
+double bias_proxy_norm(double mean_dq_norm, double alpha) {
     const double denom = std::pow(2.0, alpha) - 1.0;
-    const double norm = std::sqrt(mean_dq * mean_dq) / denom;
+    const double norm = mean_dq_norm / denom;
     return norm * norm;
 }
+double bias_proxy_impl(double mean_dq, double alpha) { return bias_proxy_norm(std::sqrt(mean_dq * mean_dq), alpha); }
 
 wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     if (desc->integrator != WMC_LEAPFROG && desc->integrator != WMC_LOCAL_TIME_STEPPING)
@@ -1364,6 +1396,7 @@ void fill_info(const wmc::LevelTables& t, int batch, bool lattice, wmc_level_inf
     info->dof_updates_per_solve = wmc::dof_updates_per_solve(t);
     info->tiers = t.tiers;
     info->n_structured = 0;
+    info->nq = t.nq;
     for (int k = 0; k < 8; ++k) info->n_r_tier[k] = k < static_cast<int>(t.n_r_tier.size()) ? t.n_r_tier[k] : 0;
 }
 }  // namespace
@@ -1672,6 +1705,11 @@ void wmc_mlmc_config_default(wmc_mlmc_config* c) {
 // (:151-161); jobs of one level run as one batched index range.
 int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
                  wmc_mlmc_result* result, wmc_level_stats* stats, wmc_error* err) {
+    return wmc_run_mlmc_vec(levels, n_levels, model_cost, cfg, result, stats, nullptr, err);
+}
+
+int wmc_run_mlmc_vec(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
+                     wmc_mlmc_result* result, wmc_level_stats* stats, double* estimate, wmc_error* err) {
     return guarded([&] {
         if (!levels || n_levels < 1 || !model_cost || !cfg || !result || !stats)
             throw ConfigError("wmc_run_mlmc: bad arguments");
@@ -1681,12 +1719,12 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
         int top = std::min(cfg->initial_levels, cap);
         std::vector<Acc> acc(top + 1);
         std::vector<long> targets(top + 1, cfg->initial_samples);
-        auto bias_proxy = [&](double mean) { return bias_proxy_impl(mean, cfg->alpha); };
+        auto bias_proxy = [&](double mean_norm) { return bias_proxy_norm(mean_norm, cfg->alpha); };
         auto bias_window = [&]() {
             double worst = 0.0;
             for (int j = 0; j < cfg->bias_window && top - j >= 1; ++j) {
                 const int l = top - j;
-                worst = std::max(worst, bias_proxy(acc[l].mean_dq()) * std::pow(2.0, -2.0 * cfg->alpha * (top - l)));
+                worst = std::max(worst, bias_proxy(acc[l].mean_dq_norm()) * std::pow(2.0, -2.0 * cfg->alpha * (top - l)));
             }
             return worst;
         };
@@ -1728,14 +1766,27 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
         std::memset(result, 0, sizeof(*result));
         result->converged = converged ? 1 : 0;
         result->levels_used = top;
+        const int nq = levels[0]->tab.nq;
+        std::vector<double> est(nq, 0.0);
         for (int l = 0; l <= top; ++l) {
             fill_stats(l, acc[l], model_cost[l], stats[l]);
-            result->estimate += acc[l].mean_dq();
+            const std::vector<double> m = acc[l].mean_dq();
+            for (int k = 0; k < nq && k < static_cast<int>(m.size()); ++k) est[k] += m[k];
             result->total_variance += stats[l].variance / static_cast<double>(stats[l].n_samples);
             result->total_model_cost += model_cost[l] * static_cast<double>(stats[l].n_samples);
         }
         result->bias = bias_window();
         result->rmse = std::sqrt(result->total_variance + result->bias);
+        // the MLMC estimate: sum of the levels' mean dQ (reference MlmcResult::estimate);
+        // the scalar field holds it for one output, its norm for QoI vectors
+        if (estimate) std::copy(est.begin(), est.end(), estimate);
+        if (nq == 1) {
+            result->estimate = est[0];
+        } else {
+            Acc norm_of;
+            norm_of.init(levels[0]->tab.qoi_norm_w);
+            result->estimate = norm_of.norm(est.data());
+        }
     });
 }
 

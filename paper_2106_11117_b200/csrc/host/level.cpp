@@ -460,6 +460,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
             L.sqrt_mass_qoi.push_back(std::sqrt(mass[v]));
         }
     }
+    L.qoi_ptr = {0, static_cast<int>(L.qoi_dof.size())};
 
     // time stepping (integrators.cpp:176-210, :117-157)
     L.kind = spec.kind;

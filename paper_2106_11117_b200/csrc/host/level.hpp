@@ -100,9 +100,16 @@ struct LevelTables {
 
     std::vector<double> mass;       // lumped mass per dof
     std::vector<double> z0;         // sqrt(M) * projected u0, per dof
-    std::vector<int> qoi_dof;       // dofs with a nonzero QoI weight
-    std::vector<double> qoi_w;      // Q = sum w_i * (z_i / sqrt(M_i))
-    std::vector<double> sqrt_mass_qoi;  // sqrt(M_i) for qoi_dof
+    // QoI: nq outputs, output k = sum over entries t in [qoi_ptr[k], qoi_ptr[k+1])
+    // of qoi_w[t] * (z[qoi_dof[t]] / sqrt_mass_qoi[t]); the QoI norm is
+    // sqrt(sum_k qoi_norm_w[k] Q_k^2) (reference QoIVector::norm, fem.cpp:15-19).
+    // BASELINE configs: one output (the box integral), weight 1.
+    int nq = 1;
+    std::vector<int> qoi_ptr{0, 0};
+    std::vector<int> qoi_dof;
+    std::vector<double> qoi_w;
+    std::vector<double> sqrt_mass_qoi;
+    std::vector<double> qoi_norm_w{1.0};
 
     std::vector<int> elem_cell;     // per triangle (diagnostics)
 

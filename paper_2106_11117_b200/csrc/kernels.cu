@@ -1200,15 +1200,16 @@ __global__ void cfl_finalize_kernel(const double* lf, const double* lc, int use_
 
 __global__ void qoi_kernel(QoIArgs a) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
     if (s >= a.count) return;
     const std::size_t S = static_cast<std::size_t>(a.S);
     double acc = 0.0;
     const double* z = (a.nsteps && ((a.n_max - __ldg(a.nsteps + s)) & 1)) ? a.z_alt : a.z;
-    for (int t = 0; t < a.nq; ++t) {
+    for (int t = __ldg(a.ptr + k); t < __ldg(a.ptr + k + 1); ++t) {
         const int i = __ldg(a.dof + t);
         acc += __ldg(a.w + t) * (z[i * S + s] / __ldg(a.sqrt_mass + t));
     }
-    a.q[s] = a.fail[s] == INT_MAX ? acc : __longlong_as_double(0x7ff8000000000000LL);
+    a.q[k * S + s] = a.fail[s] == INT_MAX ? acc : __longlong_as_double(0x7ff8000000000000LL);
 }
 
 __global__ void fill_int_kernel(int* p, int value, int n) {
@@ -1216,9 +1217,14 @@ __global__ void fill_int_kernel(int* p, int value, int n) {
     if (i < n) p[i] = value;
 }
 
-__global__ void pair_diff_kernel(const double* qf, const double* qc, double* dq, int count) {
+__global__ void pair_diff_kernel(const double* qf, const double* qc, double* dq, double* q_out, int count, int S,
+                                 int nq) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < count) dq[i] = qc ? qf[i] - qc[i] : qf[i];
+    const int k = blockIdx.y;
+    if (i >= count) return;
+    const std::size_t src = static_cast<std::size_t>(k) * S + i, dst = static_cast<std::size_t>(i) * nq + k;
+    dq[dst] = qc ? qf[src] - qc[src] : qf[src];
+    if (q_out) q_out[dst] = qf[src];
 }
 
 // K3b: per-level moment sums, one block, fixed-order tree: deterministic for
@@ -1403,7 +1409,7 @@ void launch_r_update(const RUpdateArgs& a, void* stream) {
 }
 
 void launch_qoi(const QoIArgs& a, void* stream) {
-    qoi_kernel<<<(a.count + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    qoi_kernel<<<dim3((a.count + 127) / 128, a.nq), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_eig_init(const double* warm, double warm_norm, int n, int S, double* v, void* stream) {
@@ -1429,8 +1435,10 @@ void launch_fill_int(int* p, int value, int n, void* stream) {
     fill_int_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, value, n);
 }
 
-void launch_pair_diff(const double* qf, const double* qc, double* dq, int count, void* stream) {
-    pair_diff_kernel<<<(count + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(qf, qc, dq, count);
+void launch_pair_diff(const double* qf, const double* qc, double* dq, double* q_out, int count, int S, int nq,
+                      void* stream) {
+    pair_diff_kernel<<<dim3((count + 255) / 256, nq), 256, 0, static_cast<cudaStream_t>(stream)>>>(qf, qc, dq, q_out,
+                                                                                                  count, S, nq);
 }
 
 }  // namespace wmc

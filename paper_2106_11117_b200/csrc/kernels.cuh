@@ -205,7 +205,8 @@ struct TierArgs {
 };
 
 struct QoIArgs {
-    int nq, S, count;
+    int nq, S, count;     // nq outputs; output k sums entries ptr[k] .. ptr[k+1]
+    const int* ptr;
     const int* dof;
     const double* w;
     const double* sqrt_mass;
@@ -265,7 +266,10 @@ void launch_eig_iteration(const EigArgs& a, void* stream);
 // T / ceil(T / dt - 1e-12); rel = (dt / dt_ref)^2, nsteps; padding lanes get rel 1 and 1 step
 void launch_cfl_finalize(const double* lf, const double* lc, int use_coarse, int p_fine, double safety, double T,
                          double dt_ref, int count, int S, double* rel, int* nsteps, void* stream);
-void launch_pair_diff(const double* qf, const double* qc, double* dq, int count, void* stream);
+// per-sample results, sample-major: dq[i*nq + k] = qf[k*S + i] - qc[k*S + i]
+// (qc NULL: level 0), q_out[i*nq + k] = qf[k*S + i] (q_out may be NULL)
+void launch_pair_diff(const double* qf, const double* qc, double* dq, double* q_out, int count, int S, int nq,
+                      void* stream);
 int substep_max_grid(int device, int smem_bytes);
 int lattice_smem_bytes(const LatArgs& a);
 int launch_lattice_substeps(const LatArgs& a, int grid, void* stream);  // returns cudaError_t

@@ -271,6 +271,7 @@ class MlmcResult:
     total_model_cost: float
     rmse: float
     levels: list = field(default_factory=list)
+    estimate_vector: object = None  # QoI vectors: the estimate per output (numpy array)
 
 
 def run_mlmc(levels: list[Level], model_cost: list[float], config: MlmcConfig | None = None) -> MlmcResult:
@@ -284,9 +285,10 @@ def run_mlmc(levels: list[Level], model_cost: list[float], config: MlmcConfig | 
     res = N.MlmcResult()
     stats = (N.LevelStats * n)()
     err = N.Error()
-    N.check(N.lib().wmc_run_mlmc(arr, n, cost, C.byref(cfg), C.byref(res), stats, C.byref(err)), err)
+    est = np.zeros(max(1, levels[0].info.get("nq", 1)), np.float64)
+    N.check(N.lib().wmc_run_mlmc_vec(arr, n, cost, C.byref(cfg), C.byref(res), stats, _dptr(est), C.byref(err)), err)
     return MlmcResult(res.estimate, bool(res.converged), res.levels_used, res.total_variance, res.bias,
-                      res.total_model_cost, res.rmse, [_stats(stats[i]) for i in range(res.levels_used + 1)])
+                      res.total_model_cost, res.rmse, [_stats(stats[i]) for i in range(res.levels_used + 1)], est)
 
 
 def optimal_samples(variances, costs, eps: float, min_samples: int = 2) -> list[int]:
