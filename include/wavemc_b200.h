@@ -140,6 +140,35 @@ typedef struct {
 } wmc_level_info;
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);
+/* The reference's own 1D sampling experiments (
+ * reference make_problem, src/experiments.cpp:56-106, 194-237): level `level`
+ * of the hierarchy build_hierarchy([0,6], h0, fine region, fine_h, max_level)
+ * (src/mesh1d.cpp:79-125), fine region [5 - h0, 5] (smooth) or [4 - h0, 4]
+ * (jump), Neumann, u0 = exp(-(x-3)^2/0.09), per-sample CFL step (stable_dt
+ * with the given safety), p = the level's ratio (LTS) or 1 (LF); field
+ * sample_kl (smooth: c^2 = 1 + KL, 100 cos + 100 sin terms) or sample_jump
+ * (c^2 = 1 left of J ~ U[4 - h0, 4), 4 right of it); QoI = u(T) on grid_n
+ * points of [0, 6] (restrict_to_grid), norm with trapezoid weights. */
+#define WMC_EXP_SMOOTH1D 1
+#define WMC_EXP_JUMP1D 2
+typedef struct {
+    int experiment;
+    int integrator;
+    double h0, fine_h, final_time, nu, safety;
+    int grid_n, max_level;
+    int device, batch;
+} wmc_experiment_desc;
+
+/* the reference's default_config (src/config_io.cpp:49-73) for the experiment */
+void wmc_experiment_desc_default(wmc_experiment_desc* desc, int experiment);
+int wmc_level_create_experiment(const wmc_experiment_desc* desc, int level, wmc_level** out);
+/* Host-only plan of an experiment level (sizes, no device work). */
+int wmc_experiment_plan(const wmc_experiment_desc* desc, int level, wmc_level_info* info);
+/* The experiment's model cost per level, the reference's closed-form cost
+ * model (model_params, src/experiments.cpp:177-192; cost_lts_level /
+ * cost_lf_level, src/cost_model.cpp:40-58): the run_mlmc weights. */
+double wmc_experiment_model_cost(const wmc_experiment_desc* desc, int level);
+
 /* Host-only: build the level tables and report their sizes, no device work. */
 int wmc_level_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level_info* info);
 int wmc_level_get_info(const wmc_level* level, wmc_level_info* info);

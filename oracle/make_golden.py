@@ -1,6 +1,6 @@
 """Generate tests/golden/*.json from the UNMODIFIED reference library
 (oracle/_ref/wavemc_ref_driver) -- run in the build container, where
-/root/reference exists:  python oracle/make_golden.py [--only-config2 | --only-cfl]
+/root/reference exists:  python oracle/make_golden.py [--only-config2 | --only-cfl | --only-experiments]
 
 The meshes come from the shared problem definition (the product's host mesh
 builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
@@ -90,6 +90,36 @@ def cfl_samples(ref, tmp):
                               "config0_lf": {"q": q_lf.tolist(), "header": hdr_lf}, "config1_pairs": pairs})
 
 
+def experiments(ref):
+    """The reference's own 1D sampling experiments (SURVEY.md section 8(f)
+    row 2) through its make_problem: per-sample QoI vectors of coupled pairs
+    (every 4th of the 512 grid values plus the norms, to keep the fixture
+    small) and run_mlmc at eps = 4e-3, for smooth1d / jump1d, LF-LTS / LF."""
+    out = {}
+    for name in ("smooth1d", "jump1d"):
+        for kind in ("lts", "lf"):
+            case = {"levels": []}
+            for level, first in ((0, 0), (1, 5), (2, 11)):
+                r = ref.experiment(name, kind, level=level, first=first, count=3)
+                case["model_cost"] = r["model_cost"]
+                samples = []
+                for smp in r["samples"]:
+                    dq, q = np.array(smp["dq"]), np.array(smp["q"])
+                    w = np.full(len(q), 6.0 / (len(q) - 1))
+                    w[0] = w[-1] = 0.5 * 6.0 / (len(q) - 1)
+                    samples.append({"dq_every4": dq[::4].tolist(), "q_every4": q[::4].tolist(),
+                                    "dq_norm": float(np.sqrt(np.sum(w * dq * dq))),
+                                    "q_norm": float(np.sqrt(np.sum(w * q * q)))})
+                case["levels"].append({"level": level, "first": first, "samples": samples})
+            a = ref.experiment(name, kind, eps=4e-3)
+            case["adaptive"] = {"eps": a["eps"], "converged": a["converged"], "total_variance": a["total_variance"],
+                                "bias": a["bias"], "estimate_norm": a["estimate_norm"],
+                                "estimate_every4": a["estimate"][::4], "levels": a["levels"],
+                                "seconds": a["seconds"]}
+            out[f"{name}_{kind}"] = case
+    dump("experiments.json", out)
+
+
 def main():
     build()
     ref = RefDriver()
@@ -99,6 +129,9 @@ def main():
         return
     if "--only-cfl" in sys.argv:
         cfl_samples(ref, tmp)
+        return
+    if "--only-experiments" in sys.argv:
+        experiments(ref)
         return
 
     # RNG words and uniform draws (rng.hpp:14-19, rng.cpp:14-32)
@@ -188,6 +221,7 @@ def main():
     dump("config4_adaptive.json", kl_adaptive)
     config2_reductions(ref, tmp)
     cfl_samples(ref, tmp)
+    experiments(ref)
     print("golden fixtures written to", GOLDEN)
 
 

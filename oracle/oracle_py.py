@@ -266,5 +266,16 @@ class RefDriver:
         rows = [list(map(float, l.split())) for l in self.run("consts", "--p", p, "--nu", repr(nu)).strip().splitlines()]
         return rows[0][0], rows[0][1], [r[0] for r in rows[1:]], [r[1] for r in rows[1:]]
 
+    def experiment(self, name, kind="lts", level=None, first=0, count=1, eps=None, threads=0, **kw):
+        """The reference's own sampling experiment via make_problem (src/experiments.cpp:194-237)."""
+        args = ["experiment", "--name", name, "--kind", kind, "--threads", threads]
+        if level is not None:
+            args += ["--level", level, "--first", first, "--count", count]
+        if eps is not None:
+            args += ["--eps", repr(eps)]
+        for k, v in kw.items():
+            args += [f"--{k}", v]
+        return json.loads(self.run(*args))
+
     def meshcheck(self, mesh_path):
         return json.loads(self.run("meshcheck", "--mesh", mesh_path))

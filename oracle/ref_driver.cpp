@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "wavemc/errors.hpp"
+#include "wavemc/experiments.hpp"
 #include "wavemc/fem.hpp"
 #include "wavemc/integrators.hpp"
 #include "wavemc/mesh.hpp"
@@ -529,6 +530,73 @@ int cmd_adaptive(const Args& a) {
     return 0;
 }
 
+// The reference's own sampling experiments through its public make_problem
+// (src/experiments.cpp:194-237): per-sample QoI vectors of coupled pairs
+// (sample_delta_q) and, with --eps, run_mlmc at the reference's config.
+//   experiment --name smooth1d|jump1d --kind lts|lf --level L --first I --count N [--eps E]
+int cmd_experiment(const Args& a) {
+    const std::string name = a.get("name", "smooth1d");
+    const auto kind = experiment_from_string(name);
+    if (!kind) throw ConfigError("experiment: unknown --name " + name);
+    ExperimentConfig cfg = default_config(*kind);
+    cfg.max_level = static_cast<int>(a.integer("max-level", cfg.max_level));
+    cfg.grid_n = static_cast<int>(a.integer("grid-n", cfg.grid_n));
+    cfg.workers = default_threads(a);
+    const Integrator integ = a.get("kind", "lts") == "lf" ? Integrator::Leapfrog : Integrator::LocalTimeStepping;
+    const MlmcProblem problem = make_problem(cfg, integ);
+    std::printf("{\"experiment\": \"%s\", \"kind\": \"%s\", \"max_level\": %d, \"grid_n\": %d, \"model_cost\": [",
+                name.c_str(), a.get("kind", "lts").c_str(), cfg.max_level, cfg.grid_n);
+    for (int l = 0; l <= problem.max_levels_available; ++l) std::printf("%s%.17g", l ? ", " : "", problem.model_cost(l));
+    std::printf("]");
+    if (!a.get("eps").empty()) {
+        MlmcConfig m;
+        m.eps = a.num("eps", 4e-3);
+        m.alpha = cfg.alpha;
+        m.initial_samples = cfg.initial_samples;
+        m.max_level = cfg.max_level;
+        m.master_seed = a.u64("seed", cfg.seed);
+        m.workers = cfg.workers;
+        m.bias_window = cfg.bias_window;
+        const double t0 = now_s();
+        const MlmcResult r = run_mlmc(problem, m);
+        const double t1 = now_s();
+        std::printf(", \"eps\": %.17g, \"seconds\": %.6f, \"converged\": %s, \"total_variance\": %.17g, \"bias\": %.17g, "
+                    "\"estimate_norm\": %.17g, \"estimate\": [",
+                    m.eps, t1 - t0, r.converged ? "true" : "false", r.total_variance, r.bias, r.estimate.norm());
+        for (std::size_t i = 0; i < r.estimate.values.size(); ++i)
+            std::printf("%s%.17g", i ? ", " : "", r.estimate.values[i]);
+        std::printf("], \"levels\": [");
+        for (std::size_t l = 0; l < r.levels.size(); ++l)
+            std::printf("%s{\"level\": %d, \"N\": %ld, \"variance\": %.17g, \"mean_dq_norm\": %.17g}", l ? ", " : "",
+                        r.levels[l].level, r.levels[l].n_samples, r.levels[l].variance, r.levels[l].mean_dq_norm);
+        std::printf("]");
+    }
+    if (!a.get("level").empty()) {
+        const int level = static_cast<int>(a.integer("level", 0));
+        const long first = static_cast<long>(a.u64("first", 0)), count = a.integer("count", 1);
+        const std::uint64_t seed = a.u64("seed", 0);
+        std::vector<SampleResult> res(count);
+        parallel_for(count, default_threads(a), [&](long i) {
+            res[i] = sample_delta_q(problem, level,
+                                    derive_stream(seed, static_cast<std::uint32_t>(level),
+                                                  static_cast<std::uint64_t>(first + i)));
+        });
+        std::printf(", \"level\": %d, \"first\": %ld, \"samples\": [", level, first);
+        for (long i = 0; i < count; ++i) {
+            std::printf("%s{\"dq\": [", i ? ", " : "");
+            for (std::size_t k = 0; k < res[i].delta_q.values.size(); ++k)
+                std::printf("%s%.17g", k ? ", " : "", res[i].delta_q.values[k]);
+            std::printf("], \"q\": [");
+            for (std::size_t k = 0; k < res[i].q_fine.values.size(); ++k)
+                std::printf("%s%.17g", k ? ", " : "", res[i].q_fine.values[k]);
+            std::printf("]}");
+        }
+        std::printf("]");
+    }
+    std::printf("}\n");
+    return 0;
+}
+
 int cmd_rng(const Args& a) {
     RngStream s = derive_stream(a.u64("seed", 0),
                                 static_cast<std::uint32_t>(a.integer("level", 0)),
@@ -581,7 +649,7 @@ int cmd_level(const Args& a) {
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::fprintf(stderr, "usage: wavemc_ref_driver solve|mlmc|adaptive|rng|consts|meshcheck|level --key value...\n");
+        std::fprintf(stderr, "usage: wavemc_ref_driver solve|mlmc|adaptive|experiment|rng|consts|meshcheck|level --key value...\n");
         return 2;
     }
     try {
@@ -594,6 +662,7 @@ int main(int argc, char** argv) {
         if (cmd == "consts") return cmd_consts(a);
         if (cmd == "meshcheck") return cmd_meshcheck(a);
         if (cmd == "level") return cmd_level(a);
+        if (cmd == "experiment") return cmd_experiment(a);
         throw ConfigError("unknown command " + cmd);
     } catch (const InstabilityError& e) {
         std::fprintf(stderr, "instability at step %ld: %s\n", e.step, e.what());

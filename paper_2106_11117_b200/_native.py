@@ -37,6 +37,16 @@ class LevelDesc(C.Structure):
                 ("cfl_safety", C.c_double)]
 
 
+WMC_EXP_SMOOTH1D = 1
+WMC_EXP_JUMP1D = 2
+
+
+class ExperimentDesc(C.Structure):
+    _fields_ = [("experiment", C.c_int), ("integrator", C.c_int), ("h0", C.c_double), ("fine_h", C.c_double),
+                ("final_time", C.c_double), ("nu", C.c_double), ("safety", C.c_double), ("grid_n", C.c_int),
+                ("max_level", C.c_int), ("device", C.c_int), ("batch", C.c_int)]
+
+
 class LShapeMeshSpec(C.Structure):
     _fields_ = [("n_per_unit", C.c_int), ("tiers", C.c_int), ("grade_radius", C.c_double)]
 
@@ -92,6 +102,10 @@ SIGNATURES = [
     ("wmc_mesh_destroy", None, [_VP]),
     ("wmc_level_desc_default", None, [P(LevelDesc)]),
     ("wmc_level_create", C.c_int, [_VP, P(LevelDesc), P(_VP)]),
+    ("wmc_experiment_desc_default", None, [P(ExperimentDesc), C.c_int]),
+    ("wmc_level_create_experiment", C.c_int, [P(ExperimentDesc), C.c_int, P(_VP)]),
+    ("wmc_experiment_plan", C.c_int, [P(ExperimentDesc), C.c_int, P(LevelInfo)]),
+    ("wmc_experiment_model_cost", C.c_double, [P(ExperimentDesc), C.c_int]),
     ("wmc_level_plan", C.c_int, [_VP, P(LevelDesc), P(LevelInfo)]),
     ("wmc_level_get_info", C.c_int, [_VP, P(LevelInfo)]),
     ("wmc_level_destroy", None, [_VP]),

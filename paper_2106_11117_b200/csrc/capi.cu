@@ -115,6 +115,7 @@ struct wmc_level {
 
     // sweep operator
     int* d_row_ptr = nullptr;
+    int col_bits = 23;
     int4* d_row_desc = nullptr;
     double2* d_wtype = nullptr;
     double2 row_types[wmc::kMaxRowTypes] = {};
@@ -179,6 +180,8 @@ struct wmc_level {
     double* d_cells = nullptr;
     double* d_dq = nullptr;
     double* d_kl = nullptr;  // log-normal KL table [cell][mode]
+    double* d_field_x = nullptr;      // 1D experiments: element midpoints
+    double* d_field_table = nullptr;  // Kl1D table [element][term]
     // per-call results of the pairs whose fine level this is: device and
     // pinned host mirrors, grown on demand (so levels can run concurrently)
     std::size_t r_cap = 0;
@@ -209,7 +212,7 @@ struct wmc_level {
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
-                        (void*)d_grc_a0, (void*)d_kl, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
+                        (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
             if (p) cudaFree(p);
         for (auto* p : d_tier_ptr) cudaFree(p);
         for (auto* p : d_tier_ent) cudaFree(p);
@@ -249,10 +252,19 @@ void build_device_level(wmc_level& L) {
     check(cudaSetDevice(L.device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking), "cudaStreamCreate");
 
-    if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
-    if (t.n_cells > wmc::kMaxCells) throw ConfigError("level: more than 511 coefficient cells");
+    // sweep entries pack col | cell << col_bits: 23/9 bits, or 16/16 when a
+    // level has more than 511 coefficient cells (1D experiments: one per element)
+    if (t.n_cells <= wmc::kMaxCells) {
+        L.col_bits = wmc::kColBits;
+        if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
+    } else {
+        L.col_bits = 16;
+        if (t.n >= 65536 || t.n_cells >= 65536)
+            throw ConfigError("level: more than 511 coefficient cells needs fewer than 65536 DOFs and cells");
+    }
     std::vector<int> ent(t.col.size());
-    for (std::size_t k = 0; k < ent.size(); ++k) ent[k] = t.col[k] | (t.cell[k] << wmc::kColBits);
+    for (std::size_t k = 0; k < ent.size(); ++k)
+        ent[k] = static_cast<int>(static_cast<unsigned>(t.col[k]) | (static_cast<unsigned>(t.cell[k]) << L.col_bits));
     L.d_row_ptr = upload(t.row_ptr);
     {
         // sweep row descriptors: single-cell rows, and among them the
@@ -303,6 +315,8 @@ void build_device_level(wmc_level& L) {
     const std::string fp = force_path ? force_path : "";
     L.n_wid = static_cast<int>(t.rc_ptr.size()) - 1;
     const bool onchip_fits = t.n_r <= wmc::kSubThreads * wmc::kSubMaxRpt && t.n_r < 65536 && L.n_wid < 65535;
+    if (lts && t.n_cells > wmc::kMaxCells && (t.tiers > 1 || fp == "global" || !onchip_fits))
+        throw ConfigError("level: the HBM-resident substep paths support at most 511 coefficient cells");
     if (lts && t.tiers > 1) {
         // nested tiers: HBM-resident stage kernels
         if (t.tiers > wmc::kMaxTiers) throw ConfigError("level: too many tiers");
@@ -364,6 +378,8 @@ void build_device_level(wmc_level& L) {
         L.sub_smem = wmc::substep_smem_bytes(probe);
         L.sub_grid = wmc::substep_max_grid(L.device, L.sub_smem);
     }
+    if (!t.field_x.empty()) L.d_field_x = upload(t.field_x);
+    if (!t.field_table.empty()) L.d_field_table = upload(t.field_table);
     if (L.spec.field == wmc::Field::LognormalKL) {
         const wmc::KLTable kl =
             wmc::kl_cell_table(L.spec.cells_x, L.spec.cells_y, L.spec.kl_sigma, L.spec.kl_corr_len, L.spec.kl_modes);
@@ -671,6 +687,8 @@ long cfl_phase(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
         e.count = count;
         e.row_ptr = L.d_row_ptr;
         e.ent = L.d_ent;
+        e.col_bits = L.col_bits;
+        e.col_mask = (1 << L.col_bits) - 1;
         e.a0 = L.d_a0;
         e.cells = cells;
         e.in_p = L.d_in_p;
@@ -729,6 +747,8 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
     sw.S = S;
     sw.count = count;
     sw.row_ptr = L.d_row_ptr;
+    sw.col_bits = L.col_bits;
+    sw.col_mask = (1 << L.col_bits) - 1;
     sw.row_desc = L.d_row_desc;
     sw.wtype = L.d_wtype;
     sw.ent = L.d_ent;
@@ -957,6 +977,11 @@ void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, st
                  double* cells, cudaStream_t st) {
     if (L.spec.field == wmc::Field::LognormalKL)
         wmc::launch_draw_kl(seed, level, first, count, S, L.tab.n_cells, L.spec.kl_modes, L.d_kl, cells, st);
+    else if (L.spec.field == wmc::Field::Kl1D)
+        wmc::launch_draw_kl1d(seed, level, first, count, S, L.tab.n_cells, L.tab.field_terms, L.d_field_table, cells,
+                              st);
+    else if (L.spec.field == wmc::Field::Jump1D)
+        wmc::launch_draw_jump1d(seed, level, first, count, S, L.tab.n_cells, L.spec.jump_h0, L.d_field_x, cells, st);
     else
         wmc::launch_draw_cells(seed, level, first, count, S, L.tab.n_cells, L.spec.coef_lo, L.spec.coef_hi, cells,
                                st);
@@ -1332,6 +1357,60 @@ double bias_proxy_norm(double mean_dq_norm, double alpha) {
 }
 double bias_proxy_impl(double mean_dq, double alpha) { return bias_proxy_norm(std::sqrt(mean_dq * mean_dq), alpha); }
 
+// batch capacity: the requested one (rounded to 64) or automatic: at most
+// 4096 samples, both workspaces of the level within 15 % of device memory
+void set_batch(wmc_level& L, int requested) {
+    if (requested > 0) {
+        L.batch = round64(requested);
+        return;
+    }
+    check(cudaSetDevice(L.device), "cudaSetDevice");
+    std::size_t free_b = 0, total_b = 0;
+    check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const auto& t = L.tab;
+    double tier_rows = 0.0;
+    if (t.tiers > 1)
+        for (int k = 0; k < t.tiers; ++k) tier_rows += (k > 0 ? 3.0 : 2.0) * t.n_r_tier[k];
+    const double per_sample =
+        2.0 * 8.0 * (2.0 * t.n + g_stride(t) + t.n_cells + 4.0 * t.nq + 2.0 * t.n_r + tier_rows);
+    const long cap = static_cast<long>(0.15 * static_cast<double>(total_b) / per_sample) / 64 * 64;
+    L.batch = static_cast<int>(std::max(64L, std::min(4096L, cap)));
+}
+
+// one level of the reference's 1D experiments: hierarchy, spec and tables
+// (make_problem / build_state_1d, src/experiments.cpp:56-106)
+void experiment_tables(const wmc_experiment_desc* desc, int level, wmc::LevelSpec& s, wmc::LevelTables& t) {
+    if (desc->experiment != WMC_EXP_SMOOTH1D && desc->experiment != WMC_EXP_JUMP1D)
+        throw ConfigError("experiment: unknown experiment");
+    if (desc->integrator != WMC_LEAPFROG && desc->integrator != WMC_LOCAL_TIME_STEPPING)
+        throw ConfigError("experiment: unknown integrator");
+    if (!(desc->safety > 0.0 && desc->safety <= 1.0)) throw ConfigError("experiment: safety in (0, 1]");
+    if (desc->nu < 0.0 || desc->nu > 1.0) throw ConfigError("experiment: nu in [0, 1]");
+    const bool jump = desc->experiment == WMC_EXP_JUMP1D;
+    const double anchor = jump ? 4.0 : 5.0;  // experiments.cpp:68-70
+    const wmc::Hierarchy1D H =
+        wmc::build_hierarchy_1d(0.0, 6.0, desc->h0, anchor - desc->h0, anchor, desc->fine_h, desc->max_level);
+    const wmc::Mesh1D& mesh = H.levels[level];
+    s = wmc::LevelSpec{};
+    s.kind = desc->integrator == WMC_LEAPFROG ? wmc::Integrator::Leapfrog : wmc::Integrator::LocalTimeStepping;
+    s.substeps = s.kind == wmc::Integrator::Leapfrog ? 1 : H.ratios[level];
+    s.nu = desc->nu;
+    s.final_time = desc->final_time;
+    s.dt = mesh.coarse_h;  // nominal: every sample takes its own CFL step
+    s.cfl_safety = desc->safety;
+    s.field = jump ? wmc::Field::Jump1D : wmc::Field::Kl1D;
+    s.jump_h0 = desc->h0;
+    s.ic.x0 = 3.0;  // experiments.cpp:64: u0 = exp(-(x - 3)^2 / 0.09)
+    s.ic.y0 = 0.0;
+    s.ic.width2 = 0.09;
+    s.grid_lo = 0.0;
+    s.grid_hi = 6.0;  // kDomain1dLength
+    s.grid_n = desc->grid_n;
+    s.cells_x = mesh.n_elements();
+    s.cells_y = 1;
+    t = wmc::build_level_tables_1d(mesh, s);
+}
+
 wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     if (desc->integrator != WMC_LEAPFROG && desc->integrator != WMC_LOCAL_TIME_STEPPING)
         throw ConfigError("wmc_level_create: unknown integrator");
@@ -1544,28 +1623,71 @@ int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level
         int ndev = 0;
         check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
         if (L->device < 0 || L->device >= ndev) throw ConfigError("wmc_level_create: no such device");
-        if (desc->batch > 0) {
-            L->batch = round64(desc->batch);
-        } else {
-            // automatic batch: at most 4096 samples, both workspaces of the
-            // level within 15 % of the device memory
-            check(cudaSetDevice(L->device), "cudaSetDevice");
-            std::size_t free_b = 0, total_b = 0;
-            check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-            const auto& t = L->tab;
-            double tier_rows = 0.0;
-            if (t.tiers > 1)
-                for (int k = 0; k < t.tiers; ++k) tier_rows += (k > 0 ? 3.0 : 2.0) * t.n_r_tier[k];
-            const double per_sample =
-                2.0 * 8.0 * (2.0 * t.n + g_stride(t) + t.n_cells + 4.0 + 2.0 * t.n_r + tier_rows);
-            const long cap = static_cast<long>(0.15 * static_cast<double>(total_b) / per_sample) / 64 * 64;
-            L->batch = static_cast<int>(std::max(64L, std::min(4096L, cap)));
-        }
+        set_batch(*L, desc->batch);
         build_device_level(*L);
         *out = L.release();
     });
 }
 
+int wmc_level_create_experiment(const wmc_experiment_desc* desc, int level, wmc_level** out) {
+    return guarded([&] {
+        if (!desc || !out) throw ConfigError("wmc_level_create_experiment: NULL argument");
+        if (level < 0 || level > desc->max_level) throw ConfigError("wmc_level_create_experiment: level out of range");
+        auto L = std::make_unique<wmc_level>();
+        L->device = desc->device;
+        experiment_tables(desc, level, L->spec, L->tab);
+        int ndev = 0;
+        check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (L->device < 0 || L->device >= ndev) throw ConfigError("wmc_level_create_experiment: no such device");
+        set_batch(*L, desc->batch);
+        build_device_level(*L);
+        *out = L.release();
+    });
+}
+
+int wmc_experiment_plan(const wmc_experiment_desc* desc, int level, wmc_level_info* info) {
+    return guarded([&] {
+        if (!desc || !info) throw ConfigError("wmc_experiment_plan: NULL argument");
+        if (level < 0 || level > desc->max_level) throw ConfigError("wmc_experiment_plan: level out of range");
+        wmc::LevelSpec s;
+        wmc::LevelTables t;
+        experiment_tables(desc, level, s, t);
+        fill_info(t, 0, false, info);
+    });
+}
+
+double wmc_experiment_model_cost(const wmc_experiment_desc* d, int level) {
+    if (!d || level < 0) return 0.0;
+    // model_params (experiments.cpp:177-192), 1D: r = h0 / 6, p0 = max(1, ceil(h0 / fine_h - 1e-9))
+    const double r = d->h0 / 6.0, p0 = std::max(1.0, std::ceil(d->h0 / d->fine_h - 1e-9));
+    const int dim = 1;
+    const double pre = d->final_time * std::pow(1.0, 2 * (dim + 1)) / std::pow(d->h0, dim + 1);  // degree 1
+    if (d->integrator == WMC_LEAPFROG) {  // cost_lf_level (cost_model.cpp:40-48)
+        if (level == 0) return pre * ((1.0 - r) * p0 + r * std::pow(p0, dim + 1));
+        const double coarse =
+            (1.0 - r) * (std::pow(2.0, dim) + 1.0) / std::pow(2.0, dim) * std::pow(2.0, dim * level) * p0;
+        return pre * (coarse + 2.0 * r * std::pow(p0, dim + 1));
+    }
+    // cost_lts_level (cost_model.cpp:50-58)
+    if (level == 0) return pre * ((1.0 - r) + r * std::pow(p0, dim + 1));
+    const double coarse = (1.0 - r) * (std::pow(2.0, dim + 1) + 1.0) / std::pow(2.0, dim + 1) *
+                          std::pow(2.0, (dim + 1) * level);
+    return pre * (coarse + 2.0 * r * std::pow(p0, dim + 1));
+}
+
+void wmc_experiment_desc_default(wmc_experiment_desc* d, int experiment) {
+    if (!d) return;
+    std::memset(d, 0, sizeof(*d));
+    d->experiment = experiment;
+    d->integrator = WMC_LOCAL_TIME_STEPPING;
+    d->h0 = 1.0 / 16.0;
+    d->fine_h = experiment == WMC_EXP_JUMP1D ? 1.0 / 512.0 : 1.0 / 256.0;
+    d->final_time = experiment == WMC_EXP_JUMP1D ? 6.0 : 11.0;
+    d->nu = 0.01;
+    d->safety = 0.9;
+    d->grid_n = 512;
+    d->max_level = 4;
+}
 
 int wmc_level_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level_info* info) {
     return guarded([&] {

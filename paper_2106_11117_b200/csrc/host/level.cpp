@@ -66,6 +66,21 @@ constexpr int kLatticeVariants[3][2] = {{512, 8}, {768, 6}, {1024, 4}};
 
 using StiffMap = std::map<std::tuple<int, int, int>, double>;
 
+// Geometry of one level before DOF numbering: what a mesh (2D triangles or
+// 1D elements) contributes to the tables
+struct Geometry {
+    int nv = 0;
+    std::vector<std::uint8_t> boundary;   // Dirichlet vertices (eliminated)
+    std::vector<double> mass;             // lumped mass per vertex
+    StiffMap stiff;                       // (vi, vj, cell) -> geometric stiffness
+    std::vector<std::uint8_t> sel, vt;    // P_1 and the vertex tier
+    std::vector<double> coef0;            // projected u0 coefficients (load / mass)
+    bool qoi_dof_order = false;           // one output, vertex weights qoi_vertex_w[0], DOF order
+    std::vector<std::vector<double>> qoi_vertex_w;
+    std::vector<std::vector<std::pair<int, double>>> qoi_entries;  // else: per output (vertex, weight)
+    std::vector<double> qoi_norm_w;
+};
+
 // Finds the structured block of the refined square and checks, numerically
 // against the assembled element stiffness, that every lattice node
 // (i, j) in [1, m-1]^2 has the 5-point stencil with edge conductances
@@ -190,20 +205,23 @@ std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const
 
 }  // namespace
 
-LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
+static Geometry geometry_2d(const TriMesh& mesh, const LevelSpec& spec, LevelTables& L) {
     if (spec.cells_x < 1 || spec.cells_y < 1) throw std::invalid_argument("level: coefficient grid");
     if (spec.final_time <= 0.0 || spec.dt <= 0.0) throw std::invalid_argument("level: T and dt must be positive");
     if (spec.substeps < 1) throw std::invalid_argument("level: substeps >= 1");
     if (spec.cells_x * spec.cells_y > 511) throw std::invalid_argument("level: at most 511 coefficient cells");
 
-    LevelTables L;
     const int nv = mesh.n_vertices();
     const int nt = mesh.n_triangles();
     L.n_cells = spec.cells_x * spec.cells_y;
 
+    Geometry g;
+    g.nv = nv;
+    g.boundary = mesh.boundary_vertex;
     // lumped mass and element stiffness by cell (fem.cpp:91-116)
-    std::vector<double> mass(nv, 0.0);
-    StiffMap stiff;  // (vi, vj, cell) -> sum area*grad.grad
+    std::vector<double>& mass = g.mass;
+    mass.assign(nv, 0.0);
+    StiffMap& stiff = g.stiff;  // (vi, vj, cell) -> sum area*grad.grad
     L.elem_cell.resize(nt);
     for (int t = 0; t < nt; ++t) {
         const auto& tri = mesh.triangles[t];
@@ -235,7 +253,10 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
     if (spec.tiers < 1 || spec.tiers > 8) throw std::invalid_argument("level: tiers in [1, 8]");
     if (spec.tiers > 1 && (spec.kind != Integrator::LocalTimeStepping || spec.substeps < 2))
         throw std::invalid_argument("level: nested tiers need local time stepping with p >= 2");
-    std::vector<std::uint8_t> sel(nv, 0), vt(nv, 0);
+    std::vector<std::uint8_t>& sel = g.sel;
+    std::vector<std::uint8_t>& vt = g.vt;
+    sel.assign(nv, 0);
+    vt.assign(nv, 0);
     for (int t = 0; t < nt; ++t)
         if (mesh.fine_flags[t])
             for (int v : mesh.triangles[t])
@@ -244,6 +265,56 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
                     vt[v] = std::max<std::uint8_t>(vt[v], std::min<int>(mesh.fine_flags[t], spec.tiers));
                 }
 
+    // initial data: lumped L2 projection with the edge-midpoint rule, then
+    // z0 = sqrt(M) coef (fem.cpp:223-241, :243-255); v0 = 0
+    std::vector<double> load(nv, 0.0);
+    auto u0 = [&](double x, double y) {
+        const double dx = x - spec.ic.x0, dy = y - spec.ic.y0;
+        return std::exp(-(dx * dx + dy * dy) / spec.ic.width2);
+    };
+    for (int t = 0; t < nt; ++t) {
+        const auto& tri = mesh.triangles[t];
+        const double area = mesh.signed_area(t);
+        for (int e = 0; e < 3; ++e) {
+            const auto& a = mesh.vertices[tri[e]];
+            const auto& b = mesh.vertices[tri[(e + 1) % 3]];
+            const double value = u0(0.5 * (a[0] + b[0]), 0.5 * (a[1] + b[1]));
+            load[tri[e]] += area / 3.0 * value * 0.5;
+            load[tri[(e + 1) % 3]] += area / 3.0 * value * 0.5;
+        }
+    }
+    g.coef0.resize(nv);
+    for (int v = 0; v < nv; ++v) g.coef0[v] = load[v] / mass[v];
+
+    // QoI: lumped quadrature of u(T) over the triangles whose centroid lies
+    // in the box, Q = sum_i w_i u_i with u = z / sqrt(M) (fem.cpp:271-275)
+    std::vector<double> qw(nv, 0.0);
+    for (int t = 0; t < nt; ++t) {
+        const auto cc = mesh.centroid(t);
+        if (cc[0] < spec.qoi.x0 || cc[0] > spec.qoi.x1 || cc[1] < spec.qoi.y0 || cc[1] > spec.qoi.y1) continue;
+        const double area = mesh.signed_area(t);
+        for (int v : mesh.triangles[t]) qw[v] += area / 3.0;
+    }
+    if (spec.qoi_mean) {  // mean over the box: divide by the area of its triangles
+        double total = 0.0;
+        for (int v = 0; v < nv; ++v) total += qw[v];
+        if (!(total > 0.0)) throw std::invalid_argument("level: QoI box contains no triangle");
+        for (int v = 0; v < nv; ++v) qw[v] /= total;
+    }
+    // one output: the box functional, entries in DOF order (finish_tables)
+    g.qoi_vertex_w = {qw};
+    g.qoi_norm_w = {1.0};
+    g.qoi_dof_order = true;
+    return g;
+}
+
+
+static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables& L, const TriMesh* mesh) {
+    const int nv = g.nv;
+    const std::vector<double>& mass = g.mass;
+    const StiffMap& stiff = g.stiff;
+    const std::vector<std::uint8_t>& sel = g.sel;
+    const std::vector<std::uint8_t>& vt = g.vt;
     // rows of A P with a nonzero: R; row tier rt = deepest P_k it couples to
     std::vector<std::uint8_t> in_r(nv, 0), rt(nv, 0);
     for (const auto& [key, s] : stiff) {
@@ -262,7 +333,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
     // structured lattice block (substep fast path), decided in vertex space
     std::vector<int> box_vertex;  // (m+1)^2 box nodes in (j, i) order, or empty
     if (spec.kind == Integrator::LocalTimeStepping && tiers == 1)
-        box_vertex = lattice_block(mesh, spec, mass, stiff, in_r, L);
+        if (mesh) box_vertex = lattice_block(*mesh, spec, mass, stiff, in_r, L);
 
     // dof order: the lattice box (row-major), the other R rows (deepest tier
     // first), then the rest, each in mesh vertex order
@@ -274,7 +345,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
     }
     for (int pass = tiers; pass >= 0; --pass)
         for (int v = 0; v < nv; ++v) {
-            if (mesh.boundary_vertex[v] || vdof[v] >= 0) continue;
+            if (g.boundary[v] || vdof[v] >= 0) continue;
             if (pass > 0 ? (!in_r[v] || (tiers > 1 && rt[v] != pass) || (tiers == 1 && pass != 1)) : in_r[v])
                 continue;
             vdof[v] = static_cast<int>(L.dof_vertex.size());
@@ -284,7 +355,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
     L.n_r_tier.assign(tiers, 0);
     for (int k = 1; k <= tiers; ++k)
         for (int v = 0; v < nv; ++v)
-            if (!mesh.boundary_vertex[v] && in_r[v] && (tiers == 1 || rt[v] >= k)) ++L.n_r_tier[k - 1];
+            if (!g.boundary[v] && in_r[v] && (tiers == 1 || rt[v] >= k)) ++L.n_r_tier[k - 1];
     L.n = static_cast<int>(L.dof_vertex.size());
     if (L.n == 0) throw std::invalid_argument("level: mesh has no interior vertices");
     L.in_p.assign(L.n, 0);
@@ -413,54 +484,41 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         L.rc_ptr[w + 1] = static_cast<int>(L.rc_cell.size());
     }
 
-    // initial data: lumped L2 projection with the edge-midpoint rule, then
-    // z0 = sqrt(M) coef (fem.cpp:223-241, :243-255); v0 = 0
-    std::vector<double> load(nv, 0.0);
-    auto u0 = [&](double x, double y) {
-        const double dx = x - spec.ic.x0, dy = y - spec.ic.y0;
-        return std::exp(-(dx * dx + dy * dy) / spec.ic.width2);
-    };
-    for (int t = 0; t < nt; ++t) {
-        const auto& tri = mesh.triangles[t];
-        const double area = mesh.signed_area(t);
-        for (int e = 0; e < 3; ++e) {
-            const auto& a = mesh.vertices[tri[e]];
-            const auto& b = mesh.vertices[tri[(e + 1) % 3]];
-            const double value = u0(0.5 * (a[0] + b[0]), 0.5 * (a[1] + b[1]));
-            load[tri[e]] += area / 3.0 * value * 0.5;
-            load[tri[(e + 1) % 3]] += area / 3.0 * value * 0.5;
-        }
-    }
+    // initial data z0 = sqrt(M) coef (fem.cpp:243-255); v0 = 0
     L.z0.resize(L.n);
     for (int i = 0; i < L.n; ++i) {
         const int v = L.dof_vertex[i];
-        L.z0[i] = std::sqrt(mass[v]) * (load[v] / mass[v]);
+        L.z0[i] = std::sqrt(mass[v]) * g.coef0[v];
     }
-
-    // QoI: lumped quadrature of u(T) over the triangles whose centroid lies
-    // in the box, Q = sum_i w_i u_i with u = z / sqrt(M) (fem.cpp:271-275)
-    std::vector<double> qw(nv, 0.0);
-    for (int t = 0; t < nt; ++t) {
-        const auto cc = mesh.centroid(t);
-        if (cc[0] < spec.qoi.x0 || cc[0] > spec.qoi.x1 || cc[1] < spec.qoi.y0 || cc[1] > spec.qoi.y1) continue;
-        const double area = mesh.signed_area(t);
-        for (int v : mesh.triangles[t]) qw[v] += area / 3.0;
-    }
-    if (spec.qoi_mean) {  // mean over the box: divide by the area of its triangles
-        double total = 0.0;
-        for (int v = 0; v < nv; ++v) total += qw[v];
-        if (!(total > 0.0)) throw std::invalid_argument("level: QoI box contains no triangle");
-        for (int v = 0; v < nv; ++v) qw[v] /= total;
-    }
-    for (int i = 0; i < L.n; ++i) {
-        const int v = L.dof_vertex[i];
-        if (qw[v] != 0.0) {
-            L.qoi_dof.push_back(i);
-            L.qoi_w.push_back(qw[v]);
-            L.sqrt_mass_qoi.push_back(std::sqrt(mass[v]));
+    // QoI tables: output k's entries (DOF order for the box functional, the
+    // given order for explicit entry lists)
+    L.nq = g.qoi_dof_order ? 1 : static_cast<int>(g.qoi_entries.size());
+    L.qoi_norm_w = g.qoi_norm_w;
+    L.qoi_ptr.assign(1, 0);
+    std::vector<int> vdof_of(nv, -1);
+    for (int i = 0; i < L.n; ++i) vdof_of[L.dof_vertex[i]] = i;
+    if (g.qoi_dof_order) {
+        const auto& qw = g.qoi_vertex_w[0];
+        for (int i = 0; i < L.n; ++i) {
+            const int v = L.dof_vertex[i];
+            if (qw[v] != 0.0) {
+                L.qoi_dof.push_back(i);
+                L.qoi_w.push_back(qw[v]);
+                L.sqrt_mass_qoi.push_back(std::sqrt(mass[v]));
+            }
+        }
+        L.qoi_ptr.push_back(static_cast<int>(L.qoi_dof.size()));
+    } else {
+        for (const auto& out : g.qoi_entries) {
+            for (const auto& [v, w] : out) {
+                if (vdof_of[v] < 0) continue;  // a Dirichlet vertex: u = 0
+                L.qoi_dof.push_back(vdof_of[v]);
+                L.qoi_w.push_back(w);
+                L.sqrt_mass_qoi.push_back(std::sqrt(mass[v]));
+            }
+            L.qoi_ptr.push_back(static_cast<int>(L.qoi_dof.size()));
         }
     }
-    L.qoi_ptr = {0, static_cast<int>(L.qoi_dof.size())};
 
     // time stepping (integrators.cpp:176-210, :117-157)
     L.kind = spec.kind;
@@ -524,7 +582,7 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         // vertices in vertex order), not by this level's DOF permutation
         std::vector<int> ref_index(nv, -1);
         for (int v = 0, k = 0; v < nv; ++v)
-            if (!mesh.boundary_vertex[v]) ref_index[v] = k++;
+            if (!g.boundary[v]) ref_index[v] = k++;
         auto power = [&](bool coarse) {
             const int n = L.n;
             std::vector<double> v(n), av(n);
@@ -570,6 +628,87 @@ LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
         if (spec.kind == Integrator::LocalTimeStepping && L.n_p > 0) L.warm_coarse = power(true);
     }
     return L;
+}
+
+
+LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec) {
+    LevelTables L;
+    Geometry g = geometry_2d(mesh, spec, L);
+    return finish_tables(g, spec, L, &mesh);
+}
+
+LevelTables build_level_tables_1d(const Mesh1D& mesh, const LevelSpec& spec) {
+    if (spec.final_time <= 0.0 || spec.dt <= 0.0) throw std::invalid_argument("level: T and dt must be positive");
+    if (spec.grid_n < 2 || !(spec.grid_hi > spec.grid_lo)) throw std::invalid_argument("level: bad output grid");
+    const int ne = mesh.n_elements(), nv = mesh.n_vertices();
+    if (ne < 1) throw std::invalid_argument("level: empty 1D mesh");
+    LevelTables L;
+    L.n_cells = ne;
+    Geometry g;
+    g.nv = nv;
+    g.boundary.assign(nv, 0);  // the reference's experiments are Neumann
+    g.mass.assign(nv, 0.0);
+    g.sel.assign(nv, 0);
+    for (int e = 0; e < ne; ++e) {
+        const double h = mesh.element_size(e);
+        const double k = 1.0 / h;  // times c_e^2 per sample
+        g.stiff[{e, e, e}] += k;
+        g.stiff[{e + 1, e + 1, e}] += k;
+        g.stiff[{e, e + 1, e}] += -k;
+        g.stiff[{e + 1, e, e}] += -k;
+        g.mass[e] += 0.5 * h;
+        g.mass[e + 1] += 0.5 * h;
+        if (mesh.fine_flags[e]) g.sel[e] = g.sel[e + 1] = 1;
+        L.field_x.push_back(mesh.midpoint(e));
+    }
+    g.vt = g.sel;
+    // u0 = exp(-(x - x0)^2 / width2) by two-point Gauss on every element
+    std::vector<double> load(nv, 0.0);
+    for (int e = 0; e < ne; ++e) {
+        const double lo = mesh.vertices[e], hi = mesh.vertices[e + 1];
+        const double h = hi - lo;
+        const double mid = 0.5 * (lo + hi), off = 0.5 * (hi - lo) / std::sqrt(3.0);
+        for (double x : {mid - off, mid + off}) {
+            const double f = std::exp(-(x - spec.ic.x0) * (x - spec.ic.x0) / spec.ic.width2);
+            const double phi_right = (x - lo) / h;
+            load[e] += 0.5 * h * f * (1.0 - phi_right);
+            load[e + 1] += 0.5 * h * f * phi_right;
+        }
+    }
+    g.coef0.resize(nv);
+    for (int v = 0; v < nv; ++v) g.coef0[v] = load[v] / g.mass[v];
+    // restrict_to_grid: linear interpolation at the grid points, trapezoid norm weights
+    const double glo = spec.grid_lo, ghi = spec.grid_hi;
+    const int gn = spec.grid_n;
+    const double spacing = (ghi - glo) / (gn - 1);
+    const double lo = mesh.vertices.front(), hi = mesh.vertices.back();
+    for (int i = 0; i < gn; ++i) {
+        double x = i == gn - 1 ? ghi : glo + spacing * i;
+        if (x < lo - 1e-9 || x > hi + 1e-9) throw std::invalid_argument("level: output grid outside the mesh");
+        x = std::clamp(x, lo, hi);
+        const auto it = std::upper_bound(mesh.vertices.begin(), mesh.vertices.end(), x);
+        int e = static_cast<int>(it - mesh.vertices.begin()) - 1;
+        e = std::clamp(e, 0, ne - 1);
+        const double t = (x - mesh.vertices[e]) / mesh.element_size(e);
+        g.qoi_entries.push_back({{e, 1.0 - t}, {e + 1, t}});
+        g.qoi_norm_w.push_back((i == 0 || i == gn - 1) ? 0.5 * spacing : spacing);
+    }
+    // the reference's KL field (rng.cpp:64-77): amp_k = 1 / (4 pi^2 k^2),
+    // arg = k pi x / 6, c^2 = 1 + sum_k amp (cos arg xi_k + sin arg eta_k)
+    if (spec.field == Field::Kl1D) {
+        const int K = 100;  // kKlTerms (rng.hpp:50)
+        const double pi = 3.14159265358979323846;
+        L.field_terms = 2 * K;
+        L.field_table.resize(static_cast<std::size_t>(ne) * 2 * K);
+        for (int e = 0; e < ne; ++e)
+            for (int k = 1; k <= K; ++k) {
+                const double arg = k * pi * L.field_x[e] / 6.0;
+                const double amp = 1.0 / (4.0 * pi * pi * k * k);
+                L.field_table[static_cast<std::size_t>(e) * 2 * K + (k - 1)] = amp * std::cos(arg);
+                L.field_table[static_cast<std::size_t>(e) * 2 * K + K + (k - 1)] = amp * std::sin(arg);
+            }
+    }
+    return finish_tables(g, spec, L, nullptr);
 }
 
 double dof_updates_per_solve(const LevelTables& t) {

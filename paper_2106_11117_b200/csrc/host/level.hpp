@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "mesh.hpp"
+#include "mesh1d.hpp"
 
 namespace wmc {
 
@@ -34,7 +35,10 @@ struct QoIBox {
     double x0 = 0.7, x1 = 0.9, y0 = 0.4, y1 = 0.6;
 };
 
-enum class Field : int { Uniform = 0, LognormalKL = 1 };
+// Uniform / LognormalKL: per-cell coefficients on a cells_x x cells_y grid
+// (BASELINE); Kl1D / Jump1D: the reference's 1D experiment fields
+// (rng.cpp:42-89), one coefficient per element
+enum class Field : int { Uniform = 0, LognormalKL = 1, Kl1D = 2, Jump1D = 3 };
 
 struct LevelSpec {
     int cells_x = 4, cells_y = 4;  // coefficient grid on the domain box, cell k = iy*cells_x + ix
@@ -52,6 +56,9 @@ struct LevelSpec {
     bool qoi_mean = false;  // Q = mean over the box (weights normalised by their sum)
     int tiers = 1;          // nested LTS tiers (config 2); 1 = the reference's single-tier LF-LTS
     double cfl_safety = 0.0;  // > 0: per-sample dt from the reference's stable_dt recipe (experiments.cpp:30-43)
+    double jump_h0 = 0.0;     // Jump1D: jump position ~ U[4 - h0, 4) (rng.cpp:53-58)
+    double grid_lo = 0.0, grid_hi = 1.0;  // 1D experiments: QoI output grid (reference OutputGrid)
+    int grid_n = 0;
     double dom_x0 = 0.0, dom_x1 = 1.0, dom_y0 = 0.0, dom_y1 = 1.0;  // coefficient grid extent
 
     // cell k = iy * cells_x + ix of the coefficient grid, ix = floor((x - x0) / (x1 - x0) * cells_x)
@@ -147,6 +154,12 @@ struct LevelTables {
     std::vector<double> tier_c0, tier_back;
     std::vector<std::vector<double>> tier_cm;
 
+    // 1D experiment fields: element midpoints, and for Kl1D the table
+    // field_table[e * field_terms + m] with c_e = 1 + sum_m table xi_m over
+    // xi = (kl_cos_1..K, kl_sin_1..K), xi ~ next_symmetric()
+    std::vector<double> field_x, field_table;
+    int field_terms = 0;
+
     // per-sample CFL (cfl_safety > 0): warm starts of the power iterations,
     // the dominant eigenvectors of the c = 1 operator (full, and A (I-P) on
     // rows outside P), as the reference's level contexts (experiments.cpp:132-148)
@@ -167,6 +180,13 @@ struct LevelTables {
 };
 
 LevelTables build_level_tables(const TriMesh& mesh, const LevelSpec& spec);
+
+/// One level of the reference's 1D sampling experiments (smooth1d / jump1d,
+/// experiments.cpp:56-106): Neumann (every vertex a DOF), P1 with c^2 per
+/// element at its midpoint (fem.cpp:66-89), u0 projected with two-point Gauss
+/// (fem.cpp:206-220), QoI = the solution on spec.grid_n points of
+/// [grid_lo, grid_hi] (restrict_to_grid, fem.cpp:277-293).
+LevelTables build_level_tables_1d(const Mesh1D& mesh, const LevelSpec& spec);
 
 /// DOF-updates per solve: steps * (n + (p-1)|R|) for LTS, steps * n for LF
 /// (SURVEY.md section 8(d)); the start-up step counts as one sweep.  Nested

@@ -93,6 +93,53 @@ __global__ void __launch_bounds__(kKLThreads) draw_kl_kernel(std::uint64_t seed,
     }
 }
 
+__device__ __forceinline__ std::uint64_t stream_key(std::uint64_t seed, std::uint32_t level, std::uint64_t index) {
+    std::uint64_t key = mix64(seed);
+    key = mix64(key ^ (0xa511e9b3cc1f25d1ULL + static_cast<std::uint64_t>(level)));
+    return mix64(key ^ (0x63d1c71ad3e29f0bULL + index));
+}
+
+// one block per sample: the stream's symmetric words in shared memory, the
+// element coefficients from the table (rows of `terms` entries)
+constexpr int kKl1dMaxTerms = 256;
+__global__ void __launch_bounds__(128) draw_kl1d_kernel(std::uint64_t seed, std::uint32_t level, std::uint64_t first,
+                                                       int count, int S, int n_cells, int terms,
+                                                       const double* __restrict__ table, double* __restrict__ cells) {
+    __shared__ double xi[kKl1dMaxTerms];
+    const int s = blockIdx.x;
+    if (s >= count) {  // padding lanes: unit coefficient
+        for (int e = threadIdx.x; e < n_cells; e += blockDim.x) cells[static_cast<std::size_t>(e) * S + s] = 1.0;
+        return;
+    }
+    const std::uint64_t key = stream_key(seed, level, first + static_cast<std::uint64_t>(s));
+    for (int m = threadIdx.x; m < terms; m += blockDim.x) {
+        const std::uint64_t w = mix64(key + static_cast<std::uint64_t>(m) * 0x9e3779b97f4a7c15ULL);
+        const double unit = __dmul_rn(static_cast<double>(w >> 11), 0x1.0p-53);
+        xi[m] = __dsub_rn(__dmul_rn(2.0, unit), 1.0);  // next_symmetric (rng.cpp:34-36)
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n_cells; e += blockDim.x) {
+        const double* row = table + static_cast<std::size_t>(e) * terms;
+        double acc = 0.0;
+        for (int m = 0; m < terms; ++m) acc += __ldg(row + m) * xi[m];
+        cells[static_cast<std::size_t>(e) * S + s] = 1.0 + acc;
+    }
+}
+
+__global__ void draw_jump1d_kernel(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S,
+                                   int n_cells, double h0, const double* __restrict__ x, double* __restrict__ cells) {
+    const int s = blockIdx.x;
+    double jump = 10.0;  // padding lanes: unit coefficient everywhere on [0, 6]
+    if (s < count) {
+        const std::uint64_t w = mix64(stream_key(seed, level, first + static_cast<std::uint64_t>(s)));
+        const double unit = __dmul_rn(static_cast<double>(w >> 11), 0x1.0p-53);
+        const double lo = __dsub_rn(4.0, h0);
+        jump = __dadd_rn(lo, __dmul_rn(__dsub_rn(4.0, lo), unit));  // next_uniform(4 - h0, 4)
+    }
+    for (int e = threadIdx.x; e < n_cells; e += blockDim.x)
+        cells[static_cast<std::size_t>(e) * S + s] = __ldg(x + e) < jump ? 1.0 : 4.0;
+}
+
 __device__ __forceinline__ void flag_fail(int* fail, int s, int count, int step) {
     if (s < count) atomicMin(fail + s, step);
 }
@@ -153,13 +200,13 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             // entries grouped by cell: sum a0 z_j within a part, then scale by
             // the part's coefficient (one coefficient load per part)
             double p0 = 0.0, p1 = 0.0;
-            int pcell = static_cast<unsigned>(__ldg(a.ent + b)) >> kColBits;
+            int pcell = static_cast<unsigned>(__ldg(a.ent + b)) >> a.col_bits;
             double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + pcell * S + s0));
             for (int k = b; k < e; ++k) {
                 const int pk = __ldg(a.ent + k);
                 const double w = __ldg(a.a0 + k);
-                const int j = pk & kColMask;
-                const int cell = static_cast<unsigned>(pk) >> kColBits;
+                const int j = pk & a.col_mask;
+                const int cell = static_cast<unsigned>(pk) >> a.col_bits;
                 if (cell != pcell) {  // warp-uniform
                     acc0 += c.x * p0;
                     acc1 += c.y * p1;
@@ -209,7 +256,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             double p0 = 0.0, p1 = 0.0;
 #pragma unroll 4
             for (int k = b; k < e; ++k) {
-                const int j = __ldg(a.ent + k) & kColMask;
+                const int j = __ldg(a.ent + k) & a.col_mask;
                 const double w = __ldg(a.a0 + k);
                 if (kInit) {
                     const double zj = __ldg(a.z0 + j);
@@ -229,8 +276,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             for (int k = b; k < e; ++k) {
                 const int pk = __ldg(a.ent + k);
                 const double w = __ldg(a.a0 + k);
-                const int j = pk & kColMask;
-                const int cell = static_cast<unsigned>(pk) >> kColBits;
+                const int j = pk & a.col_mask;
+                const int cell = static_cast<unsigned>(pk) >> a.col_bits;
                 const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
                 if (kInit) {
                     const double zj = __ldg(a.z0 + j);
@@ -360,7 +407,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
                 double p0 = 0.0, p1 = 0.0;
 #pragma unroll 4
                 for (int q = b; q < e; ++q) {
-                    const int j = __ldg(a.ent + q) & kColMask;
+                    const int j = __ldg(a.ent + q) & a.col_mask;
                     const double w = __ldg(a.a0 + q);
                     const double2 z = zrow(j);
                     p0 += w * z.x;
@@ -373,8 +420,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
                 for (int q = b; q < e; ++q) {
                     const int pk = __ldg(a.ent + q);
                     const double w = __ldg(a.a0 + q);
-                    const int j = pk & kColMask;
-                    const int cell = static_cast<unsigned>(pk) >> kColBits;
+                    const int j = pk & a.col_mask;
+                    const int cell = static_cast<unsigned>(pk) >> a.col_bits;
                     const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
                     const double2 z = zrow(j);
                     acc0 += (cc.x * w) * z.x;
@@ -1082,10 +1129,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32) eig_matvec_kernel(EigArgs a)
         const int b = __ldg(a.row_ptr + row), e = __ldg(a.row_ptr + row + 1);
         for (int k = b; k < e; ++k) {
             const int pk = __ldg(a.ent + k);
-            const int j = pk & kColMask;
+            const int j = pk & a.col_mask;
             if (a.coarse && __ldg(a.in_p + j)) continue;
             const double w = __ldg(a.a0 + k);
-            const int cell = static_cast<unsigned>(pk) >> kColBits;
+            const int cell = static_cast<unsigned>(pk) >> a.col_bits;
             const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
             const double2 x = __ldg(reinterpret_cast<const double2*>(a.v + j * S + s0));
             acc0 += (c.x * w) * x.x;
@@ -1285,6 +1332,18 @@ void launch_draw_kl(std::uint64_t seed, std::uint32_t level, std::uint64_t first
                     int modes, const double* table, double* cells, void* stream) {
     draw_kl_kernel<<<(S + kKLThreads - 1) / kKLThreads, kKLThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         seed, level, first, count, S, n_cells, modes, table, cells);
+}
+
+void launch_draw_kl1d(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
+                      int terms, const double* table, double* cells, void* stream) {
+    draw_kl1d_kernel<<<S, 128, 0, static_cast<cudaStream_t>(stream)>>>(seed, level, first, count, S, n_cells, terms,
+                                                                       table, cells);
+}
+
+void launch_draw_jump1d(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
+                        double h0, const double* x, double* cells, void* stream) {
+    draw_jump1d_kernel<<<S, 128, 0, static_cast<cudaStream_t>(stream)>>>(seed, level, first, count, S, n_cells, h0, x,
+                                                                         cells);
 }
 
 void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,

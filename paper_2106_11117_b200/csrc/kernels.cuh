@@ -44,7 +44,8 @@ struct SweepArgs {
     int S;           // batch stride
     int count;       // live samples
     const int* row_ptr;
-    const int* ent;      // col | cell << kColBits
+    const int* ent;      // col | cell << col_bits (23, or 16 when there are more than 511 cells)
+    int col_bits, col_mask;
     const double* a0;
     // per row {info, row_ptr begin, dS, dN}; info = cell | type << 16 |
     // pfull << 24 for a structured row (type >= 1; pfull = deepest tier whose
@@ -226,6 +227,7 @@ struct EigArgs {
     int n, S, count;
     const int* row_ptr;
     const int* ent;
+    int col_bits, col_mask;
     const double* a0;
     const double* cells;
     const unsigned char* in_p;
@@ -251,6 +253,14 @@ void launch_draw_kl(std::uint64_t seed, std::uint32_t level, std::uint64_t first
                     int modes, const double* table, double* cells, void* stream);
 void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
                        double lo, double hi, double* cells, void* stream);
+// the reference's 1D experiment fields, one coefficient per element
+// (rng.cpp:42-89): Kl1D: c_e = 1 + sum_m table[e][m] xi_m, xi_m = 2 unit - 1
+// (next_symmetric) from words 0..terms-1; Jump1D: J = next_uniform(4 - h0, 4)
+// from word 0, c_e = x_e < J ? 1 : 4
+void launch_draw_kl1d(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
+                      int terms, const double* table, double* cells, void* stream);
+void launch_draw_jump1d(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
+                        double h0, const double* x, double* cells, void* stream);
 void launch_sweep_init(const SweepArgs& a, void* stream);
 void launch_sweep_step(const SweepArgs& a, void* stream);
 int substep_smem_bytes(const SubArgs& a);

@@ -140,6 +140,31 @@ def _info_dict(info: N.LevelInfo) -> dict:
     return out
 
 
+def experiment_desc(experiment: str, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides) -> N.ExperimentDesc:
+    """The reference's default_config for a 1D experiment (src/config_io.cpp:49-73) with overrides."""
+    kind = {"smooth1d": N.WMC_EXP_SMOOTH1D, "jump1d": N.WMC_EXP_JUMP1D}[experiment]
+    d = N.ExperimentDesc()
+    N.lib().wmc_experiment_desc_default(C.byref(d), kind)
+    d.integrator = integrator
+    for k, v in overrides.items():
+        setattr(d, k, v)
+    return d
+
+
+def experiment_plan(experiment: str, level: int, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides) -> dict:
+    """Host-only sizes of one experiment level."""
+    info = N.LevelInfo()
+    N.check(N.lib().wmc_experiment_plan(C.byref(experiment_desc(experiment, integrator, **overrides)), level,
+                                        C.byref(info)))
+    return _info_dict(info)
+
+
+def experiment_model_cost(experiment: str, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides) -> list[float]:
+    """The reference's closed-form model cost of every level (run_mlmc weights)."""
+    d = experiment_desc(experiment, integrator, **overrides)
+    return [N.lib().wmc_experiment_model_cost(C.byref(d), l) for l in range(d.max_level + 1)]
+
+
 def level_plan(mesh: Mesh, spec: LevelSpec) -> dict:
     """Host-only level tables: sizes and DOF-update counts (no device)."""
     d = spec.desc()
@@ -162,6 +187,25 @@ class Level:
         N.check(N.lib().wmc_level_get_info(self._h, C.byref(info)))
         self.info = _info_dict(info)
 
+    @classmethod
+    def experiment(cls, experiment: str, level: int, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides):
+        """Level `level` of the reference's own 1D sampling experiment
+        ("smooth1d" or "jump1d"; reference make_problem, src/experiments.cpp:56-106),
+        reference default_config unless overridden (h0, fine_h, final_time, nu,
+        safety, grid_n, max_level, device, batch)."""
+        d = experiment_desc(experiment, integrator, **overrides)
+        self = cls.__new__(cls)
+        self.mesh = None
+        self.spec = None
+        self.experiment_desc = d
+        h = C.c_void_p()
+        N.check(N.lib().wmc_level_create_experiment(C.byref(d), level, C.byref(h)))
+        self._h = h
+        info = N.LevelInfo()
+        N.check(N.lib().wmc_level_get_info(self._h, C.byref(info)))
+        self.info = _info_dict(info)
+        return self
+
     @property
     def stream(self) -> int:
         return N.lib().wmc_level_stream(self._h) or 0
@@ -174,9 +218,12 @@ class Level:
 
 def eval_pairs(fine: Level, coarse: Level | None, seed: int, level: int, first: int, count: int):
     """Batched sample_delta_q (reference src/mlmc.cpp:21-37) over indices
-    first..first+count-1: returns (dq, q_fine, cost dict)."""
-    dq = np.empty(count, np.float64)
-    qf = np.empty(count, np.float64)
+    first..first+count-1: returns (dq, q_fine, cost dict); QoI vectors
+    (info["nq"] > 1) come back with shape (count, nq)."""
+    nq = fine.info.get("nq", 1)
+    shape = (count,) if nq == 1 else (count, nq)
+    dq = np.empty(shape, np.float64)
+    qf = np.empty(shape, np.float64)
     cost = N.Cost()
     err = N.Error()
     rc = N.lib().wmc_eval_pairs(fine._h, coarse._h if coarse is not None else None, seed, level, first, count,
