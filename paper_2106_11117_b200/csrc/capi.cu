@@ -178,6 +178,7 @@ struct wmc_level {
     // batch state: ws[0] as the fine level of a pair, ws[1] as the coarse one
     Workspace ws[2];
     double* d_cells = nullptr;
+    double* d_cells_coarse = nullptr;  // per-element fields: this level's coefficients as the coarse of a pair
     double* d_dq = nullptr;
     double* d_kl = nullptr;  // log-normal KL table [cell][mode]
     double* d_field_x = nullptr;      // 1D experiments: element midpoints
@@ -208,7 +209,7 @@ struct wmc_level {
         cudaSetDevice(device);
         for (void* p : {(void*)d_row_ptr, (void*)d_row_desc, (void*)d_wtype, (void*)d_ent, (void*)d_a0, (void*)d_z0, (void*)d_sub_ent,
                         (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
-                        (void*)d_cm, (void*)d_qptr, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_dq,
+                        (void*)d_cm, (void*)d_qptr, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_cells_coarse, (void*)d_dq,
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
@@ -987,6 +988,12 @@ void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, st
                                st);
 }
 
+// the 1D experiments' fields are evaluated per element: the coarse level of a
+// pair draws its own coefficients from the same stream (rng.cpp:42-89)
+bool per_element_field(const wmc_level& L) {
+    return L.spec.field == wmc::Field::Kl1D || L.spec.field == wmc::Field::Jump1D;
+}
+
 void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
     if (coarse && coarse->tab.nq != fine->tab.nq) throw ConfigError("wmc_eval_pairs: QoI sizes differ");
     if (!fine) throw ConfigError("eval_pairs: fine level is NULL");
@@ -994,8 +1001,15 @@ void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
     if (fine->device != coarse->device) throw ConfigError("eval_pairs: levels on different devices");
     const auto& a = fine->spec;
     const auto& b = coarse->spec;
+    if (a.field != b.field) throw ConfigError("eval_pairs: coefficient fields of the pair differ");
+    if (per_element_field(*fine)) {
+        // one draw per pair, evaluated on each level's own elements
+        if (a.jump_h0 != b.jump_h0 || fine->tab.field_terms != coarse->tab.field_terms)
+            throw ConfigError("eval_pairs: coefficient fields of the pair differ");
+        return;
+    }
     if (fine->tab.n_cells != coarse->tab.n_cells || a.coef_lo != b.coef_lo || a.coef_hi != b.coef_hi ||
-        a.field != b.field || a.kl_sigma != b.kl_sigma || a.kl_corr_len != b.kl_corr_len || a.kl_modes != b.kl_modes)
+        a.kl_sigma != b.kl_sigma || a.kl_corr_len != b.kl_corr_len || a.kl_modes != b.kl_modes)
         throw ConfigError("eval_pairs: coefficient fields of the pair differ");
 }
 
@@ -1073,7 +1087,19 @@ void issue_pairs(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::ui
         Workspace* wc = nullptr;
         if (coarse) {
             wc = &workspace(*coarse, 1);
-            solve_batch(*coarse, *wc, fine->d_cells, S, c, st);
+            const double* coarse_cells = fine->d_cells;
+            if (per_element_field(*fine)) {
+                // the coarse role has its own buffer: the level may run its own
+                // pair concurrently on its stream
+                if (!coarse->d_cells_coarse)
+                    check(cudaMalloc(&coarse->d_cells_coarse,
+                                     sizeof(double) * static_cast<std::size_t>(coarse->batch) * coarse->tab.n_cells),
+                          "cudaMalloc cells");
+                launch_draw(*coarse, seed, level, first + off, c, S, coarse->d_cells_coarse, st);
+                ++g_launches;
+                coarse_cells = coarse->d_cells_coarse;
+            }
+            solve_batch(*coarse, *wc, coarse_cells, S, c, st);
         }
         const int nq = fine->tab.nq;
         double* dq_dst = (to_host ? fine->r_dq : dev_dq) + off * nq;
