@@ -711,14 +711,20 @@ long cfl_phase(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
         wmc::launch_eig_init(coarse ? L.d_warm_coarse : L.d_warm_full, coarse ? L.warm_coarse_norm : L.warm_full_norm,
                              t.n, S, ws.za, stream);
         ++g_launches;
-        for (int it = 1;; ++it) {
-            check(cudaMemsetAsync(active, 0, sizeof(int), stream), "memset");
-            wmc::launch_eig_iteration(e, stream);
-            g_launches += 4;
+        // iterations are issued in groups between host checks: a settled
+        // sample is frozen (done flag), so extra iterations do not change it
+        int group = 4;
+        for (int it = 0;;) {
+            for (int k = 0; k < group && it < 20000; ++k, ++it) {
+                check(cudaMemsetAsync(active, 0, sizeof(int), stream), "memset");
+                wmc::launch_eig_iteration(e, stream);
+                g_launches += 4;
+            }
             check(cudaMemcpyAsync(ws.h_active, active, sizeof(int), cudaMemcpyDeviceToHost, stream), "copy");
             check(cudaStreamSynchronize(stream), "power iteration");
             if (*ws.h_active == 0) break;
             if (it >= 20000) throw NumericalError("max_eigenvalue: power iteration did not converge");
+            group = std::min(2 * group, 32);
         }
         check(cudaMemcpyAsync(out, lam, sizeof(double) * SS, cudaMemcpyDeviceToDevice, stream), "copy");
     };
