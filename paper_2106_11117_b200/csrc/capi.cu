@@ -164,6 +164,7 @@ struct wmc_level {
     int* d_gen_rows = nullptr;
     double* d_gen_rs = nullptr;
     int* d_gen_soff = nullptr;
+    int* d_gen_warp_slice = nullptr;
     std::uint16_t* d_gen_col = nullptr;
     int* d_slot_rc = nullptr;  // lattice kernel: overflow start offsets
     std::uint16_t* d_ovf_cell = nullptr;
@@ -211,7 +212,7 @@ struct wmc_level {
                         (void*)d_slice_off, (void*)d_rc_ptr, (void*)d_rc_cell, (void*)d_rc_a0, (void*)d_beta,
                         (void*)d_cm, (void*)d_qptr, (void*)d_qdof, (void*)d_qw, (void*)d_qsm, (void*)d_cells, (void*)d_cells_coarse, (void*)d_dq,
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
-                        (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
+                        (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_warp_slice, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
                         (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
             if (p) cudaFree(p);
@@ -498,6 +499,29 @@ void build_device_level(wmc_level& L) {
         L.d_gen_rows = upload(grows);
         L.d_gen_rs = upload(grs);
         L.d_gen_soff = upload(soff);
+        {
+            // balanced warp -> slice assignment (longest slice first onto the
+            // least-loaded warp with a free role), so no warp carries two
+            // wide slices while others idle at the substep barrier
+            const int warps = t.lat_threads / 32, G = t.lat_threads == 1024 ? 1 : 2;
+            std::vector<int> table(static_cast<std::size_t>(warps) * G, -1), load(warps, 0), used(warps, 0);
+            const char* plain = std::getenv("WMC_GEN_PLAIN_ASSIGN");  // A/B knob: slice q of role u to warp q % warps
+            for (int sl = 0; sl < n_slices; ++sl) {
+                const int width = (soff[sl + 1] - soff[sl]) / 32;
+                int best = -1;
+                if (plain) {
+                    best = sl % warps;
+                    if (used[best] >= G) best = -1;
+                } else {
+                    for (int w = 0; w < warps; ++w)
+                        if (used[w] < G && (best < 0 || load[w] < load[best])) best = w;
+                }
+                if (best < 0) throw ConfigError("level: generic rows exceed the lattice kernel's roles");
+                table[static_cast<std::size_t>(best) * G + used[best]++] = sl;
+                load[best] += width;
+            }
+            L.d_gen_warp_slice = upload(table);
+        }
         L.d_gen_col = upload(gcol);
         L.d_slot_rc = upload(ovf_start);
         L.d_slot_a0 = upload(slot_a0);
@@ -799,6 +823,7 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
         la.gen_rows = L.d_gen_rows;
         la.gen_rs = L.d_gen_rs;
         la.gen_soff = L.d_gen_soff;
+        la.gen_warp_slice = L.d_gen_warp_slice;
         la.gen_col = L.d_gen_col;
         la.ovf_start = L.d_slot_rc;
         la.ovf_cell = L.d_ovf_cell;

@@ -955,17 +955,19 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
     const int col = tid % a.cw, strip = tid / a.cw;
     const int ci = 1 + col;
     const bool lat_on = ci <= a.m - 1 && strip < a.n_strips;
-    // generic role: list entries tid + u*T, slots [slice][width][32]
+    // generic role: the warp's u-th 32-row slice from the host's balanced
+    // assignment (widest slices spread over the warps), slots [slice][width][32]
     int grow[G], gslot[G], gwid[G];
     double grs[G];
 #pragma unroll
     for (int u = 0; u < G; ++u) {
-        const int q = tid + u * T;
+        const int wsl = __ldg(a.gen_warp_slice + (tid >> 5) * G + u);
+        const int q = wsl >= 0 ? wsl * 32 + lane : a.n_gen;
         grow[u] = q < a.n_gen ? __ldg(a.gen_rows + q) : -1;
         grs[u] = q < a.n_gen ? __ldg(a.gen_rs + q) : 0.0;
-        const int sl = q < a.n_gen ? q >> 5 : 0;  // idle lanes point at slice 0, width 0
+        const int sl = wsl >= 0 ? wsl : 0;  // idle warps point at slice 0 with width 0
         gslot[u] = __ldg(a.gen_soff + sl) + lane;
-        gwid[u] = q < a.n_gen ? (__ldg(a.gen_soff + sl + 1) - __ldg(a.gen_soff + sl)) >> 5 : 0;
+        gwid[u] = wsl >= 0 ? (__ldg(a.gen_soff + sl + 1) - __ldg(a.gen_soff + sl)) >> 5 : 0;
     }
     __syncthreads();
     int j0 = 1, len = 0;
@@ -1045,24 +1047,24 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
             double gaq[G];
 #pragma unroll
             for (int u = 0; u < G; ++u) {
-                double acc = 0.0;
+                double acc = 0.0, acc2 = 0.0;  // two chains: the gather's loads overlap
                 // warp-uniform jump into a straight-line gather of the
                 // slice's width (Duff's device; widths are <= kLatGenWidth)
                 const int q0 = gslot[u];
-#define WMC_GEN_SLOT(E) acc += sd[o.gw + q0 + 32 * (E)] * sd[cur + gcol[q0 + 32 * (E)]]
+#define WMC_GEN_SLOT(E, A) A += sd[o.gw + q0 + 32 * (E)] * sd[cur + gcol[q0 + 32 * (E)]]
                 switch (gwid[u]) {
-                    case 8: WMC_GEN_SLOT(7); [[fallthrough]];
-                    case 7: WMC_GEN_SLOT(6); [[fallthrough]];
-                    case 6: WMC_GEN_SLOT(5); [[fallthrough]];
-                    case 5: WMC_GEN_SLOT(4); [[fallthrough]];
-                    case 4: WMC_GEN_SLOT(3); [[fallthrough]];
-                    case 3: WMC_GEN_SLOT(2); [[fallthrough]];
-                    case 2: WMC_GEN_SLOT(1); [[fallthrough]];
-                    case 1: WMC_GEN_SLOT(0); [[fallthrough]];
+                    case 8: WMC_GEN_SLOT(7, acc2); [[fallthrough]];
+                    case 7: WMC_GEN_SLOT(6, acc); [[fallthrough]];
+                    case 6: WMC_GEN_SLOT(5, acc2); [[fallthrough]];
+                    case 5: WMC_GEN_SLOT(4, acc); [[fallthrough]];
+                    case 4: WMC_GEN_SLOT(3, acc2); [[fallthrough]];
+                    case 3: WMC_GEN_SLOT(2, acc); [[fallthrough]];
+                    case 2: WMC_GEN_SLOT(1, acc2); [[fallthrough]];
+                    case 1: WMC_GEN_SLOT(0, acc); [[fallthrough]];
                     default: break;
                 }
 #undef WMC_GEN_SLOT
-                gaq[u] = acc;
+                gaq[u] = acc + acc2;
             }
             const int ce = cur + base + W, cw_ = cur + base - W;
             const double vnl = sd[cur + sN];
