@@ -136,6 +136,8 @@ struct wmc_level {
     double* d_cm = nullptr;
     int sub_smem = 0;
     int sub_grid = 0;
+    int small_smem = 0;  // fused small-mesh solve: shared memory per CTA (0: not eligible)
+    int n_sms = 148;
     SubPath path = SubPath::None;
     int* d_apg_ptr = nullptr;
     int* d_apg_ent = nullptr;
@@ -552,6 +554,23 @@ void build_device_level(wmc_level& L) {
             throw ConfigError("level: substep working set exceeds shared memory");
     }
     L.lattice = L.path == SubPath::Lattice;
+    {
+        // fused small-mesh solve: the batched arithmetic is mirrored for the
+        // leap-frog / p = 1 and on-chip generic substep paths
+        int sms = 0, optin = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L.device);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, L.device);
+        L.n_sms = sms > 0 ? sms : 148;
+        if ((L.path == SubPath::None || L.path == SubPath::OnChip) && t.tiers == 1 && t.n_r < 65536) {
+            wmc::SmallArgs probe{};
+            probe.n = t.n;
+            probe.n_r = t.n_r;
+            probe.n_cells = t.n_cells;
+            probe.n_wid = L.path == SubPath::OnChip ? L.n_wid : 0;
+            const int bytes = wmc::small_smem_bytes(probe);
+            if (bytes <= optin) L.small_smem = bytes;
+        }
+    }
     L.d_cells = nullptr;
     check(cudaMalloc(&L.d_cells, sizeof(double) * std::max<std::size_t>(static_cast<std::size_t>(L.batch) * t.n_cells, 1)),
           "cudaMalloc batch");
@@ -971,11 +990,77 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
 // per batch instead of ~3 n_steps (small batches of the adaptive driver are
 // launch-bound).  Per-sample CFL batches (host-synchronised power
 // iterations) and profiled runs take the plain path; WMC_NO_GRAPH=1 forces it.
+// Fused small-mesh solve for small batches (bitwise the same results as the
+// batched kernels; SmallArgs).  WMC_SMALL=0 disables it, WMC_SMALL=N sets the
+// largest batch that takes it (default two samples per SM).
+bool small_path(const wmc_level& L, int count) {
+    if (L.small_smem <= 0) return false;
+    static const int limit = [] {
+        const char* v = std::getenv("WMC_SMALL");
+        return v ? std::atoi(v) : -1;
+    }();
+    const int cap = limit >= 0 ? limit : 2 * L.n_sms;
+    return count <= cap;
+}
+
+void small_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream,
+                 const double* rel, const int* nsteps) {
+    const wmc::LevelTables& t = L.tab;
+    wmc::SmallArgs a{};
+    a.n = t.n;
+    a.n_r = t.n_r;
+    a.p = t.p;
+    a.S = S;
+    a.count = count;
+    a.n_cells = t.n_cells;
+    a.split = L.path == SubPath::OnChip ? t.n_r : 0;
+    a.row_ptr = L.d_row_ptr;
+    a.ent = L.d_ent;
+    a.col_bits = L.col_bits;
+    a.col_mask = (1 << L.col_bits) - 1;
+    a.a0 = L.d_a0;
+    a.row_desc = L.d_row_desc;
+    a.wtype = L.d_wtype;
+    a.sub_ent = L.d_sub_ent;
+    a.slice_off = L.d_slice_off;
+    a.n_wid = L.path == SubPath::OnChip ? L.n_wid : 0;
+    a.rc_ptr = L.d_rc_ptr;
+    a.rc_cell = L.d_rc_cell;
+    a.rc_a0 = L.d_rc_a0;
+    a.cells = cells;
+    a.z0 = L.d_z0;
+    a.init_factor = t.init_factor;
+    a.factor = t.coarse_factor;
+    a.c0 = t.c0;
+    a.beta = L.d_beta;
+    a.cm = L.d_cm;
+    a.n_steps = t.n_steps;
+    a.rel = rel;
+    a.nsteps = nsteps;
+    a.nq = t.nq;
+    a.qptr = L.d_qptr;
+    a.qdof = L.d_qdof;
+    a.qw = L.d_qw;
+    a.qsm = L.d_qsm;
+    a.q = ws.q;
+    a.fail = ws.fail;
+    const int e = wmc::launch_small_solve(a, std::min(count, L.n_sms), stream);
+    ++g_launches;
+    if (e != 0) check(static_cast<cudaError_t>(e), "small solve launch");
+}
+
 void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
     const wmc::LevelTables& t = L.tab;
     if (t.cfl_safety > 0.0) {
         const long n_steps = cfl_phase(L, ws, cells, S, count, stream);
-        solve_batch_launches(L, ws, cells, S, count, stream, n_steps, ws.rel, ws.nsteps);
+        if (small_path(L, count))
+            small_solve(L, ws, cells, S, count, stream, ws.rel, ws.nsteps);
+        else
+            solve_batch_launches(L, ws, cells, S, count, stream, n_steps, ws.rel, ws.nsteps);
+        return;
+    }
+    if (small_path(L, count) && !L.profile) {
+        small_solve(L, ws, cells, S, count, stream, nullptr, nullptr);
         return;
     }
     static const bool no_graph = std::getenv("WMC_NO_GRAPH") != nullptr || std::getenv("WMC_SYNC_DEBUG") != nullptr;

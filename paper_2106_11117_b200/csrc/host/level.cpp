@@ -390,12 +390,17 @@ static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables
         L.row_ptr[i + 1] = static_cast<int>(L.col.size());
     }
 
-    // A P on R rows, parts form (global-memory substep path)
+    // A P on R rows, parts form (HBM-resident and fused small-mesh paths);
+    // col | cell << 23, or << 16 when there are more than 511 cells
+    L.apg_col_bits = L.n_cells <= 511 ? 23 : 16;
+    if (L.apg_col_bits == 16 && (L.n >= 65536 || L.n_cells >= 65536))
+        throw std::invalid_argument("level: more than 511 cells needs fewer than 65536 DOFs and cells");
     L.apg_ptr.assign(L.n_r + 1, 0);
     for (int i = 0; i < L.n_r; ++i) {
         for (const auto& [j, k, a] : rows[i]) {
             if (!L.in_p[j]) continue;
-            L.apg_ent.push_back(j | (k << 23));  // kColBits
+            L.apg_ent.push_back(static_cast<int>(static_cast<unsigned>(j) |
+                                                 (static_cast<unsigned>(k) << L.apg_col_bits)));
             L.apg_a0.push_back(a);
         }
         L.apg_ptr[i + 1] = static_cast<int>(L.apg_ent.size());

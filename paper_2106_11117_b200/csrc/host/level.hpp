@@ -100,10 +100,11 @@ struct LevelTables {
     std::vector<int> rc_cell;
     std::vector<double> rc_a0;
 
-    // A P on R rows as sweep-style parts (col | cell << 24, a0): the
-    // HBM-resident substep path for sets R too large for one SM
+    // A P on R rows as sweep-style parts (col | cell << apg_col_bits, a0):
+    // the HBM-resident substep path for sets R too large for one SM
     std::vector<int> apg_ptr, apg_ent;
     std::vector<double> apg_a0;
+    int apg_col_bits = 23;
 
     std::vector<double> mass;       // lumped mass per dof
     std::vector<double> z0;         // sqrt(M) * projected u0, per dof

@@ -1244,6 +1244,167 @@ __global__ void cfl_finalize_kernel(const double* lf, const double* lc, int use_
 }
 
 // ---------------------------------------------------------------------------
+// K5: fused small-mesh solve (see SmallArgs): the same arithmetic, row by row
+// and in the same order, as the batched path it replaces (sweep_kernel<true>
+// start-up, sweep_rows_kernel's structured / single-cell / multi-cell
+// gathers, substep_kernel's recipe weights and SELL gather, r_update), so a
+// sample's result is bitwise the same whichever path ran it.  Shared
+// memory: cell coefficients | recipe weights W | z_a | z_b | g | d_a | d_b.
+
+__host__ __device__ inline int small_layout(const SmallArgs& a, int* oW, int* za, int* zb, int* g, int* da,
+                                            int* db) {
+    int off = (a.n_cells + 1) & ~1;
+    if (oW) *oW = off;
+    off += (a.n_wid + 2) & ~1;
+    if (za) *za = off;
+    off += (a.n + 1) & ~1;
+    if (zb) *zb = off;
+    off += (a.n + 1) & ~1;
+    const int r = (a.n_r + 1) & ~1;
+    if (g) *g = off;
+    if (da) *da = off + r;
+    if (db) *db = off + 2 * r;
+    return off + 3 * r;
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1) small_solve_kernel(SmallArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    int oW, oza, ozb, og, oda, odb;
+    small_layout(a, &oW, &oza, &ozb, &og, &oda, &odb);
+    double* cl = sm;
+    double* W = sm + oW;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    __shared__ int fail_step;
+    for (int s = blockIdx.x; s < a.count; s += gridDim.x) {
+        const long n_steps = a.nsteps ? __ldg(a.nsteps + s) : a.n_steps;
+        const double rs = a.rel ? __ldg(a.rel + s) : 1.0;
+        for (int k = tid; k < a.n_cells; k += T) cl[k] = __ldg(a.cells + k * S + s);
+        if (tid == 0) fail_step = INT_MAX;
+        __syncthreads();
+        for (int w = tid; w < a.n_wid; w += T) {  // recipe weights (substep_kernel)
+            double acc = 0.0;
+            for (int t = __ldg(a.rc_ptr + w); t < __ldg(a.rc_ptr + w + 1); ++t)
+                acc += cl[__ldg(a.rc_cell + t)] * __ldg(a.rc_a0 + t);
+            W[w] = acc;
+        }
+        if (tid == 0) W[a.n_wid] = 0.0;  // SELL padding weight
+        double* zc = sm + oza;  // z_n
+        double* zp = sm + ozb;  // z_{n-1}, overwritten with z_{n+1}
+        // start-up (sweep_kernel<true>): z1 = z0 + factor (0 - A z0)
+        for (int i = tid; i < a.n; i += T) {
+            const int4 d = __ldg(a.row_desc + i);
+            const int b = __ldg(a.row_ptr + i), e = __ldg(a.row_ptr + i + 1);
+            double acc0 = 0.0;
+            if (d.x >= 0) {
+                const double c = cl[d.x & 0xffff];
+                double p0 = 0.0;
+                for (int q = b; q < e; ++q) {
+                    const double zj = __ldg(a.z0 + (__ldg(a.ent + q) & a.col_mask));
+                    p0 += __ldg(a.a0 + q) * zj;
+                }
+                acc0 = c * p0;
+            } else {
+                for (int q = b; q < e; ++q) {
+                    const unsigned pk = static_cast<unsigned>(__ldg(a.ent + q));
+                    const double zj = __ldg(a.z0 + (pk & a.col_mask));
+                    acc0 += (cl[pk >> a.col_bits] * __ldg(a.a0 + q)) * zj;
+                }
+            }
+            const double z0 = __ldg(a.z0 + i);
+            const double out = z0 + (a.init_factor * rs) * (0.0 - acc0);
+            zp[i] = z0;
+            zc[i] = out;
+            if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, 1);
+        }
+        __syncthreads();
+        const double factor = a.factor * rs;
+        for (long st = 1; st < n_steps; ++st) {
+            const int step = static_cast<int>(st + 1);
+            // sweep (sweep_rows_kernel)
+            for (int i = tid; i < a.n; i += T) {
+                const int4 d = __ldg(a.row_desc + i);
+                double acc0 = 0.0;
+                if (d.x >= 0 && ((d.x >> 16) & 0xff) > 0) {
+                    const double2 w = __ldg(a.wtype + ((d.x >> 16) & 0xff) - 1);
+                    const double c = cl[d.x & 0xffff];
+                    double p0 = 0.0;
+                    p0 += w.x * zc[i - d.z];
+                    p0 += w.x * zc[i - 1];
+                    p0 += w.y * zc[i];
+                    p0 += w.x * zc[i + 1];
+                    p0 += w.x * zc[i + d.w];
+                    acc0 = c * p0;
+                } else if (d.x >= 0) {
+                    const double c = cl[d.x & 0xffff];
+                    double p0 = 0.0;
+                    for (int q = d.y; q < __ldg(a.row_ptr + i + 1); ++q)
+                        p0 += __ldg(a.a0 + q) * zc[__ldg(a.ent + q) & a.col_mask];
+                    acc0 = c * p0;
+                } else {
+                    for (int q = d.y; q < __ldg(a.row_ptr + i + 1); ++q) {
+                        const unsigned pk = static_cast<unsigned>(__ldg(a.ent + q));
+                        acc0 += (cl[pk >> a.col_bits] * __ldg(a.a0 + q)) * zc[pk & a.col_mask];
+                    }
+                }
+                if (i < a.split) {
+                    sm[og + i] = acc0;
+                } else {
+                    const double out = 2.0 * zc[i] - zp[i] - factor * acc0;
+                    zp[i] = out;
+                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                }
+            }
+            __syncthreads();
+            if (a.split > 0) {
+                // substep_kernel: d_1 = -c0 g, then the SELL gather with recipe weights
+                const double c0 = a.c0 * rs;
+                for (int i = tid; i < a.split; i += T) sm[oda + i] = -c0 * sm[og + i];
+                __syncthreads();
+                for (int m = 1; m <= a.p - 1; ++m) {
+                    const double* cur = sm + ((m & 1) ? oda : odb);
+                    double* nxt = sm + ((m & 1) ? odb : oda);
+                    const double beta = __ldg(a.beta + m - 1);
+                    const double cm = __ldg(a.cm + m - 1) * rs;
+                    for (int i = tid; i < a.split; i += T) {
+                        const int slice = i >> 5, lane = i & 31;
+                        const int b = __ldg(a.slice_off + slice), e = __ldg(a.slice_off + slice + 1);
+                        double aq = 0.0;
+                        for (int q = b + lane; q < e; q += 32) {
+                            const std::uint32_t pk = __ldg(a.sub_ent + q);
+                            aq += W[pk >> 16] * cur[pk & 0xffffu];
+                        }
+                        const double dp = m == 1 ? 0.0 : nxt[i];
+                        nxt[i] = (1.0 + beta) * cur[i] - beta * dp - cm * (sm[og + i] + aq);
+                    }
+                    __syncthreads();
+                }
+                // r_update: z_{n+1} = 2 z_n - z_{n-1} + 2 d_p
+                const double* dpv = sm + ((a.p & 1) ? oda : odb);
+                for (int i = tid; i < a.split; i += T) {
+                    const double out = 2.0 * zc[i] - zp[i] + 2.0 * dpv[i];
+                    zp[i] = out;
+                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                }
+            }
+            __syncthreads();
+            double* t = zc;  // z_{n+1} becomes z_n
+            zc = zp;
+            zp = t;
+        }
+        // QoI outputs of the final state (qoi_kernel; NaN for a failed sample)
+        for (int k = tid; k < a.nq; k += T) {
+            double acc = 0.0;
+            for (int q = __ldg(a.qptr + k); q < __ldg(a.qptr + k + 1); ++q)
+                acc += __ldg(a.qw + q) * (zc[__ldg(a.qdof + q)] / __ldg(a.qsm + q));
+            a.q[k * S + s] = fail_step == INT_MAX ? acc : __longlong_as_double(0x7ff8000000000000LL);
+        }
+        if (tid == 0) a.fail[s] = fail_step;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3: QoI per sample, Q = sum_t w_t (z_t / sqrt(M_t)) over the box nodes in a
 // fixed order (deterministic); failed samples report NaN.
 
@@ -1501,5 +1662,20 @@ void launch_pair_diff(const double* qf, const double* qc, double* dq, double* q_
     pair_diff_kernel<<<dim3((count + 255) / 256, nq), 256, 0, static_cast<cudaStream_t>(stream)>>>(qf, qc, dq, q_out,
                                                                                                   count, S, nq);
 }
+
+int small_smem_bytes(const SmallArgs& a) {
+    return small_layout(a, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr) * static_cast<int>(sizeof(double));
+}
+
+int launch_small_solve(const SmallArgs& a, int grid, void* stream) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(small_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        configured = true;
+    }
+    small_solve_kernel<<<grid, kSmallThreads, small_smem_bytes(a), static_cast<cudaStream_t>(stream)>>>(a);
+    return static_cast<int>(cudaGetLastError());
+}
+
 
 }  // namespace wmc

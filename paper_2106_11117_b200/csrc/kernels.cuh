@@ -206,6 +206,52 @@ struct TierArgs {
     const int* nsteps;
 };
 
+// Fused small-mesh solve: one CTA owns one sample at a time (persistent over
+// the batch) and runs the whole solve -- start-up, every global step's sweep,
+// LF-LTS substeps on R and update, check_finite, QoI -- with the state in
+// shared memory.  For levels whose state fits one SM (the 1D experiments,
+// config 0, small MLMC levels) and small batches, where the per-step kernel
+// launches of the batched path dominate.  Same arithmetic as the batched
+// kernels (generic gathers), per-sample CFL scale and horizon included.
+constexpr int kSmallThreads = 512;
+
+struct SmallArgs {
+    int n, n_r, p, S, count, n_cells;
+    int split;                   // rows < split take the substeps (0: leap-frog everywhere)
+    const int* row_ptr;          // full operator (sweep tables, as SweepArgs)
+    const int* ent;
+    int col_bits, col_mask;
+    const double* a0;
+    const int4* row_desc;
+    const double2* wtype;
+    // A P on R rows exactly as the on-chip generic substep kernel holds it:
+    // SELL entries col | wid << 16 per 32-row slice, recipes of the weights
+    const std::uint32_t* sub_ent;
+    const int* slice_off;
+    int n_wid;
+    const int* rc_ptr;
+    const int* rc_cell;
+    const double* rc_a0;
+    const double* cells;         // [k * S + s]
+    const double* z0;
+    double init_factor, factor, c0;  // factor: leap-frog / coarse-row factor
+    const double* beta;          // p - 1
+    const double* cm;            // p - 1
+    long n_steps;                // fixed-dt horizon
+    const double* rel;           // per-sample CFL (NULL: fixed dt)
+    const int* nsteps;
+    int nq;                      // QoI matrix (as QoIArgs)
+    const int* qptr;
+    const int* qdof;
+    const double* qw;
+    const double* qsm;
+    double* q;                   // [k * S + s]
+    int* fail;                   // per sample: first non-finite step (INT_MAX: none)
+};
+
+int small_smem_bytes(const SmallArgs& a);
+int launch_small_solve(const SmallArgs& a, int grid, void* stream);  // returns cudaError_t
+
 struct QoIArgs {
     int nq, S, count;     // nq outputs; output k sums entries ptr[k] .. ptr[k+1]
     const int* ptr;

@@ -59,3 +59,13 @@ def test_experiment_adaptive_mlmc_matches_reference(golden, case):
     for s, lv in zip(res.levels, a["levels"]):
         assert s["variance"] == pytest.approx(lv["variance"], rel=1e-9)
         assert s["mean_dq"] == pytest.approx(lv["mean_dq_norm"], rel=1e-9)
+
+
+@pytest.mark.parametrize("case", ["smooth1d_lts", "jump1d_lf"])
+def test_fused_small_solve_is_bitwise_the_batched_path(case):
+    """Small batches take the fused one-CTA-per-sample solve; it repeats the
+    batched kernels' arithmetic exactly (same bits either way)."""
+    levels, _ = _levels(case, 2)
+    fused = wavemc.eval_pairs(levels[1], levels[0], 3, 1, 10, 40)  # 40 <= 2 x SMs: fused solve
+    big = wavemc.eval_pairs(levels[1], levels[0], 3, 1, 0, 600)  # one batch of 600: batched kernels
+    assert np.array_equal(fused[0], big[0][10:50]) and np.array_equal(fused[1], big[1][10:50])
