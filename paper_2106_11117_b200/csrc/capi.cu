@@ -557,9 +557,8 @@ void build_device_level(wmc_level& L) {
     {
         // fused small-mesh solve: the batched arithmetic is mirrored for the
         // leap-frog / p = 1 and on-chip generic substep paths
-        int sms = 0, optin = 0;
+        int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L.device);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, L.device);
         L.n_sms = sms > 0 ? sms : 148;
         if ((L.path == SubPath::None || L.path == SubPath::OnChip) && t.tiers == 1 && t.n_r < 65536) {
             wmc::SmallArgs probe{};
@@ -568,7 +567,7 @@ void build_device_level(wmc_level& L) {
             probe.n_cells = t.n_cells;
             probe.n_wid = L.path == SubPath::OnChip ? L.n_wid : 0;
             const int bytes = wmc::small_smem_bytes(probe);
-            if (bytes <= optin) L.small_smem = bytes;
+            if (bytes <= wmc::small_max_smem(L.device)) L.small_smem = bytes;
         }
     }
     L.d_cells = nullptr;

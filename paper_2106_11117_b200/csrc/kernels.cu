@@ -1667,12 +1667,23 @@ int small_smem_bytes(const SmallArgs& a) {
     return small_layout(a, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr) * static_cast<int>(sizeof(double));
 }
 
+int small_max_smem(int device) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, small_solve_kernel) != cudaSuccess) return 0;
+    return optin - static_cast<int>(fa.sharedSizeBytes);  // the kernel also holds static shared memory
+}
+
 int launch_small_solve(const SmallArgs& a, int grid, void* stream) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(small_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
+    static int configured = -1;
+    if (configured < 0) {
+        int device = 0;
+        cudaGetDevice(&device);
+        configured = static_cast<int>(
+            cudaFuncSetAttribute(small_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, small_max_smem(device)));
     }
+    if (configured != 0) return configured;
     small_solve_kernel<<<grid, kSmallThreads, small_smem_bytes(a), static_cast<cudaStream_t>(stream)>>>(a);
     return static_cast<int>(cudaGetLastError());
 }

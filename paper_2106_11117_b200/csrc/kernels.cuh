@@ -250,6 +250,7 @@ struct SmallArgs {
 };
 
 int small_smem_bytes(const SmallArgs& a);
+int small_max_smem(int device);  // largest dynamic shared memory the kernel can take
 int launch_small_solve(const SmallArgs& a, int grid, void* stream);  // returns cudaError_t
 
 struct QoIArgs {
