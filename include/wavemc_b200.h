@@ -137,6 +137,8 @@ typedef struct {
     int n_r_tier[8];          /* |R_k| for tiers k = 1..tiers (n_r_tier[0] == n_r), rows [0, |R_k|) */
     long n_structured;        /* sweep rows taking the structured 5-point path (0 before device setup) */
     int nq;                   /* QoI outputs per sample (1: scalar; the experiments' output grid) */
+    int fused;                /* 1: each batch runs as one fused lattice-solve kernel (z_n, z_{n-1} on chip),
+                                 2: the same with z_{n-1} in a per-sample global buffer, 0: per-step kernels */
 } wmc_level_info;
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);

@@ -56,7 +56,7 @@ class LevelInfo(C.Structure):
                 ("dt", C.c_double), ("nnz", C.c_long), ("ap_nnz", C.c_long), ("n_recipes", C.c_long),
                 ("batch", C.c_int), ("dof_updates_per_solve", C.c_double), ("lattice", C.c_int),
                 ("substep_path", C.c_int), ("tiers", C.c_int), ("n_r_tier", C.c_int * 8),
-                ("n_structured", C.c_long), ("nq", C.c_int)]
+                ("n_structured", C.c_long), ("nq", C.c_int), ("fused", C.c_int)]
 
 
 class Cost(C.Structure):

@@ -137,6 +137,8 @@ struct wmc_level {
     int sub_smem = 0;
     int sub_grid = 0;
     int small_smem = 0;  // fused small-mesh solve: shared memory per CTA (0: not eligible)
+    int fused_smem = 0;  // fused lattice solve: shared memory per CTA (0: not eligible)
+    bool fused_zp_global = false;  // fused lattice solve keeps z_{n-1} in a per-sample global buffer
     int n_sms = 148;
     SubPath path = SubPath::None;
     int* d_apg_ptr = nullptr;
@@ -569,6 +571,33 @@ void build_device_level(wmc_level& L) {
             const int bytes = wmc::small_smem_bytes(probe);
             if (bytes <= wmc::small_max_smem(L.device)) L.small_smem = bytes;
         }
+        // fused lattice solve: lattice levels whose z_n (and z_{n-1} when it
+        // fits) stay on chip next to the substep state; WMC_FUSED=0 disables
+        const char* fz = std::getenv("WMC_FUSED");
+        if (L.path == SubPath::Lattice && t.tiers == 1 && t.lat_threads == 512 && t.lat_k == 8 &&
+            !(fz && std::atoi(fz) == 0)) {
+            wmc::LatSolveArgs probe{};
+            probe.lat.n_r = t.n_r;
+            probe.lat.p = t.p;
+            probe.lat.n_cells = t.n_cells;
+            probe.lat.m = t.lat_m;
+            probe.lat.n_strips = static_cast<int>(t.strip_j0.size());
+            probe.lat.n_slots = L.n_slots;
+            probe.n = t.n;
+            // taken when z_{n-1} fits on chip too and the rows outside R
+            // (round-robin, latency-bound gathers) are at most two per
+            // thread: config-1 levels 0 and 1, the bulk of its substep work.
+            // WMC_FUSED_ZP_GLOBAL=1 forces the layout with z_{n-1} in global
+            // memory (tests; it is slower where the rows outside R are many)
+            const int cap = wmc::lattice_solve_max_smem(L.device);
+            const char* zg = std::getenv("WMC_FUSED_ZP_GLOBAL");
+            if (zg && std::atoi(zg) != 0) {
+                probe.zp_global = reinterpret_cast<double*>(16);  // layout without z_{n-1}
+                L.fused_zp_global = true;
+            }
+            const int bytes = wmc::lattice_solve_smem_bytes(probe);
+            if (bytes <= cap && (L.fused_zp_global || t.n - t.n_r <= 2 * t.lat_threads)) L.fused_smem = bytes;
+        }
     }
     L.d_cells = nullptr;
     check(cudaMalloc(&L.d_cells, sizeof(double) * std::max<std::size_t>(static_cast<std::size_t>(L.batch) * t.n_cells, 1)),
@@ -783,6 +812,49 @@ long cfl_phase(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
     return n_max;
 }
 
+wmc::LatArgs lattice_args(const wmc_level& L, Workspace& ws, const double* cells, int S, int count) {
+    const wmc::LevelTables& t = L.tab;
+    wmc::LatArgs la{};
+    la.threads = t.lat_threads;
+    la.strip_k = t.lat_k;
+    la.n_r = t.n_r;
+    la.S = S;
+    la.count = count;
+    la.p = t.p;
+    la.n_cells = t.n_cells;
+    la.cells_x = L.spec.cells_x;
+    la.m = t.lat_m;
+    la.cw = t.lat_cw;
+    la.n_strips = static_cast<int>(t.strip_j0.size());
+    la.n_gen = static_cast<int>(t.gen_rows.size());
+    la.n_slots = L.n_slots;
+    la.inv_h = t.lat_inv_h;
+    la.c0 = t.c0;
+    la.strip_j0 = L.d_strip_j0;
+    la.lat_smask = L.d_lat_smask;
+    la.strip_len = L.d_strip_len;
+    la.cellx = L.d_cellx;
+    la.celly = L.d_celly;
+    la.gen_rows = L.d_gen_rows;
+    la.gen_rs = L.d_gen_rs;
+    la.gen_soff = L.d_gen_soff;
+    la.gen_warp_slice = L.d_gen_warp_slice;
+    la.gen_col = L.d_gen_col;
+    la.ovf_start = L.d_slot_rc;
+    la.ovf_cell = L.d_ovf_cell;
+    la.ovf_a0 = L.d_grc_a0;
+    la.n_ovf = L.n_ovf;
+    la.n_ovf_terms = L.n_ovf_terms;
+    la.slot_a0 = L.d_slot_a0;
+    la.slot_cell = L.d_slot_cell;
+    la.cells = cells;
+    la.gd = ws.g;
+    la.g_stride = g_stride(t);
+    la.beta = L.d_beta;
+    la.cm = L.d_cm;
+    return la;
+}
+
 void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream,
                           long n_steps, const double* rel, const int* nsteps) {
     const wmc::LevelTables& t = L.tab;
@@ -817,45 +889,7 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
     double* cur = ws.za;
     double* prev = ws.zb;
     wmc::LatArgs la{};
-    if (lts && L.lattice) {
-        la.threads = t.lat_threads;
-        la.strip_k = t.lat_k;
-        la.n_r = t.n_r;
-        la.S = S;
-        la.count = count;
-        la.p = t.p;
-        la.n_cells = t.n_cells;
-        la.cells_x = L.spec.cells_x;
-        la.m = t.lat_m;
-        la.cw = t.lat_cw;
-        la.n_strips = static_cast<int>(t.strip_j0.size());
-        la.n_gen = static_cast<int>(t.gen_rows.size());
-        la.n_slots = L.n_slots;
-        la.inv_h = t.lat_inv_h;
-        la.c0 = t.c0;
-        la.strip_j0 = L.d_strip_j0;
-        la.lat_smask = L.d_lat_smask;
-        la.strip_len = L.d_strip_len;
-        la.cellx = L.d_cellx;
-        la.celly = L.d_celly;
-        la.gen_rows = L.d_gen_rows;
-        la.gen_rs = L.d_gen_rs;
-        la.gen_soff = L.d_gen_soff;
-        la.gen_warp_slice = L.d_gen_warp_slice;
-        la.gen_col = L.d_gen_col;
-        la.ovf_start = L.d_slot_rc;
-        la.ovf_cell = L.d_ovf_cell;
-        la.ovf_a0 = L.d_grc_a0;
-        la.n_ovf = L.n_ovf;
-        la.n_ovf_terms = L.n_ovf_terms;
-        la.slot_a0 = L.d_slot_a0;
-        la.slot_cell = L.d_slot_cell;
-        la.cells = cells;
-        la.gd = ws.g;
-        la.g_stride = g_stride(t);
-        la.beta = L.d_beta;
-        la.cm = L.d_cm;
-    }
+    if (lts && L.lattice) la = lattice_args(L, ws, cells, S, count);
     wmc::SubArgs sb{};
     if (lts) {
         sb.n_r = t.n_r;
@@ -1048,8 +1082,52 @@ void small_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     if (e != 0) check(static_cast<cudaError_t>(e), "small solve launch");
 }
 
+// Fused lattice solve of a whole batch (one launch; LatSolveArgs).
+void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream,
+                 const double* rel, const int* nsteps) {
+    const wmc::LevelTables& t = L.tab;
+    wmc::LatSolveArgs a{};
+    a.lat = lattice_args(L, ws, cells, S, count);
+    a.lat.rel = rel;
+    a.lat.nsteps = nsteps;
+    a.n = t.n;
+    a.row_ptr = L.d_row_ptr;
+    a.ent = L.d_ent;
+    a.col_bits = L.col_bits;
+    a.col_mask = (1 << L.col_bits) - 1;
+    a.a0 = L.d_a0;
+    a.row_desc = L.d_row_desc;
+    a.wtype = L.d_wtype;
+    a.z0 = L.d_z0;
+    a.init_factor = t.init_factor;
+    a.factor = t.coarse_factor;
+    a.n_steps = t.n_steps;
+    a.zp_global = L.fused_zp_global ? ws.zb : nullptr;
+    a.nq = t.nq;
+    a.qptr = L.d_qptr;
+    a.qdof = L.d_qdof;
+    a.qw = L.d_qw;
+    a.qsm = L.d_qsm;
+    a.q = ws.q;
+    a.fail = ws.fail;
+    if (L.profile) mark(L, L.ev_sub, stream);
+    const int e = wmc::launch_lattice_solve(a, std::max(1, std::min(count, L.n_sms)), stream);
+    ++g_launches;
+    if (e != 0) check(static_cast<cudaError_t>(e), "fused lattice solve launch");
+    if (L.profile) mark(L, L.ev_sub, stream);
+}
+
 void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int count, cudaStream_t stream) {
     const wmc::LevelTables& t = L.tab;
+    if (L.fused_smem > 0) {
+        if (t.cfl_safety > 0.0) {
+            cfl_phase(L, ws, cells, S, count, stream);
+            fused_solve(L, ws, cells, S, count, stream, ws.rel, ws.nsteps);
+        } else {
+            fused_solve(L, ws, cells, S, count, stream, nullptr, nullptr);
+        }
+        return;
+    }
     if (t.cfl_safety > 0.0) {
         const long n_steps = cfl_phase(L, ws, cells, S, count, stream);
         if (small_path(L, count))
@@ -1616,6 +1694,7 @@ void fill_info(const wmc::LevelTables& t, int batch, bool lattice, wmc_level_inf
     info->dof_updates_per_solve = wmc::dof_updates_per_solve(t);
     info->tiers = t.tiers;
     info->n_structured = 0;
+    info->fused = 0;
     info->nq = t.nq;
     for (int k = 0; k < 8; ++k) info->n_r_tier[k] = k < static_cast<int>(t.n_r_tier.size()) ? t.n_r_tier[k] : 0;
 }
@@ -1843,6 +1922,7 @@ int wmc_level_get_info(const wmc_level* L, wmc_level_info* info) {
         if (!L || !info) throw ConfigError("wmc_level_get_info: NULL argument");
         fill_info(L->tab, L->batch, L->lattice, info, static_cast<int>(L->path));
         info->n_structured = L->n_structured;
+        info->fused = L->fused_smem > 0 ? (L->fused_zp_global ? 2 : 1) : 0;
     });
 }
 

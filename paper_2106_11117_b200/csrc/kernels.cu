@@ -1405,6 +1405,360 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_solve_kernel(SmallArgs
 }
 
 // ---------------------------------------------------------------------------
+// K6: fused lattice solve (see LatSolveArgs).  Thread roles are the lattice
+// kernel's: column ci of strip `strip` (<= K consecutive lattice rows) and G
+// generic rows of R; rows outside R go round-robin.  The substeps, the R
+// update, the leap-frog rows and the QoI are the batched kernels' arithmetic;
+// g = A z_n on the lattice rows comes from the substep stencil (v = z / h)
+// instead of the sweep's per-row descriptors (the same operator, a different
+// rounding: agreement with the per-step path at the 1e-15 level, not
+// bitwise).  A level takes one path for every batch, so results still depend
+// only on (seed, level, index).  Shared memory (doubles): z_n | z_{n-1}
+// (optional) | v0 | v1 | gw | cl | beta | cm | then the integer tables.
+
+struct LatSolveOff {
+    int zn, zp, v0, v1, gw, cl, beta, cm, gcol, sj0, slen, cx, cy, total;
+};
+
+__host__ __device__ inline LatSolveOff lat_solve_offsets(const LatSolveArgs& A) {
+    const LatArgs& a = A.lat;
+    LatSolveOff o;
+    int off = 0;
+    auto take = [&](int doubles) {
+        const int r = off;
+        off += (doubles + 1) & ~1;
+        return r;
+    };
+    const int slots = a.n_slots > 0 ? a.n_slots : 1;
+    o.zn = take(A.n);
+    o.zp = A.zp_global ? -1 : take(A.n);
+    o.v0 = take(a.n_r + 16);  // rows past a short strip read (never write) up to 8 beyond
+    // v1 also holds z_{n+1} of the rows outside R between the sweep and its store
+    o.v1 = take(a.n_r + 16 > A.n - a.n_r ? a.n_r + 16 : A.n - a.n_r);
+    o.gw = take(slots);
+    o.cl = take(a.n_cells);
+    o.beta = take(a.p > 1 ? a.p - 1 : 1);
+    o.cm = take(a.p > 1 ? a.p - 1 : 1);
+    o.gcol = take((slots * 2 + 7) / 8);  // uint16
+    o.sj0 = take((a.n_strips + 1) / 2);  // int
+    o.slen = take((a.n_strips + 1) / 2);
+    o.cx = take((a.m + 1) / 2);
+    o.cy = take((a.m + 1) / 2);
+    o.total = off;
+    return o;
+}
+
+// g_i = (A(omega) z)_i of one row, exactly as sweep_rows_kernel forms it
+// (structured 5-point rows from the descriptor; single-cell and multi-cell
+// rows from the entries), with z and the cell coefficients on chip
+__device__ __forceinline__ double lat_solve_row(const LatSolveArgs& A, int i, const double* zc, const double* cl) {
+    const int4 d = __ldg(A.row_desc + i);
+    double acc0 = 0.0;
+    if (d.x >= 0 && ((d.x >> 16) & 0xff) > 0) {
+        const double2 w = __ldg(A.wtype + ((d.x >> 16) & 0xff) - 1);
+        const double c = cl[d.x & 0xffff];
+        double p0 = 0.0;
+        p0 += w.x * zc[i - d.z];
+        p0 += w.x * zc[i - 1];
+        p0 += w.y * zc[i];
+        p0 += w.x * zc[i + 1];
+        p0 += w.x * zc[i + d.w];
+        acc0 = c * p0;
+    } else if (d.x >= 0) {
+        const double c = cl[d.x & 0xffff];
+        double p0 = 0.0;
+        const int e = __ldg(A.row_ptr + i + 1);
+        for (int q = d.y; q < e; ++q) p0 += __ldg(A.a0 + q) * zc[__ldg(A.ent + q) & A.col_mask];
+        acc0 = c * p0;
+    } else {
+        const int e = __ldg(A.row_ptr + i + 1);
+        for (int q = d.y; q < e; ++q) {
+            const unsigned pk = static_cast<unsigned>(__ldg(A.ent + q));
+            acc0 += (cl[pk >> A.col_bits] * __ldg(A.a0 + q)) * zc[pk & A.col_mask];
+        }
+    }
+    return acc0;
+}
+
+// g = A z_n on the thread's lattice rows by the substep stencil: v = z / sqrt(M)
+// of every R row published to v (owners), one barrier, then the 5-point
+// stencil of lattice_substep_kernel (edge conductances already / h)
+template <int K, int G>
+__device__ __forceinline__ void lat_solve_g(double* sd, int ov, const double* zn, int base, int len, int W, int sS,
+                                            int sN, double inv_h, double kE, double kW, double kNS, double dg,
+                                            const int* grow, const double* grs, double* gg) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (k < len) sd[ov + base + k] = zn[base + k] * inv_h;
+#pragma unroll
+    for (int u = 0; u < G; ++u)
+        if (grow[u] >= 0) sd[ov + grow[u]] = zn[grow[u]] * grs[u];
+    __syncthreads();
+    const int ce = ov + base + W, cw_ = ov + base - W;
+    const double vnl = sd[ov + sN];
+    double vs = sd[ov + sS];
+    double vk = sd[ov + base];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double ve = sd[ce + k], vw = sd[cw_ + k];
+        const double vn = (k + 1 < len) ? sd[ov + base + k + 1] : vnl;
+        gg[k] = k < len ? dg * vk - kE * ve - kW * vw - kNS * (vn + vs) : 0.0;
+        vs = vk;
+        vk = vn;
+    }
+}
+
+template <int T, int K, int G>
+__global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
+    extern __shared__ __align__(16) double sd[];
+    const LatArgs& a = A.lat;
+    const LatSolveOff o = lat_solve_offsets(A);
+    std::uint16_t* gcol = reinterpret_cast<std::uint16_t*>(sd + o.gcol);
+    int* sj0 = reinterpret_cast<int*>(sd + o.sj0);
+    int* slen = reinterpret_cast<int*>(sd + o.slen);
+    int* cx = reinterpret_cast<int*>(sd + o.cx);
+    int* cy = reinterpret_cast<int*>(sd + o.cy);
+    double* zn = sd + o.zn;
+    double* cl = sd + o.cl;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const int W = a.m + 1;
+    const int nr = a.n_r;
+    const double inv_h = a.inv_h;
+    const double hh = 1.0 / inv_h;
+    __shared__ int fail_step;
+
+    // static tables, once per CTA
+    for (int i = tid; i < a.n_slots; i += T) gcol[i] = __ldg(a.gen_col + i);
+    for (int i = tid; i < a.n_strips; i += T) {
+        sj0[i] = __ldg(a.strip_j0 + i);
+        slen[i] = __ldg(a.strip_len + i);
+    }
+    for (int i = tid; i < a.m; i += T) {
+        cx[i] = __ldg(a.cellx + i);
+        cy[i] = __ldg(a.celly + i);
+    }
+    for (int i = tid; i < a.p - 1; i += T) {
+        sd[o.beta + i] = __ldg(a.beta + i);
+        sd[o.cm + i] = __ldg(a.cm + i);
+    }
+    const int col = tid % a.cw, strip = tid / a.cw;
+    const int ci = 1 + col;
+    const bool lat_on = ci <= a.m - 1 && strip < a.n_strips;
+    int grow[G], gslot[G], gwid[G];
+    double grs[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+        const int wsl = __ldg(a.gen_warp_slice + (tid >> 5) * G + u);
+        const int q = wsl >= 0 ? wsl * 32 + lane : a.n_gen;
+        grow[u] = q < a.n_gen ? __ldg(a.gen_rows + q) : -1;
+        grs[u] = q < a.n_gen ? __ldg(a.gen_rs + q) : 0.0;
+        const int sl = wsl >= 0 ? wsl : 0;
+        gslot[u] = __ldg(a.gen_soff + sl) + lane;
+        gwid[u] = wsl >= 0 ? (__ldg(a.gen_soff + sl + 1) - __ldg(a.gen_soff + sl)) >> 5 : 0;
+    }
+    __syncthreads();
+    int j0 = 1, len = 0;
+    if (lat_on) {
+        j0 = sj0[strip];
+        len = slen[strip];
+    }
+    const int base = lat_on ? ci * W + j0 : W + 1;
+    const int sS = lat_on ? base - 1 : 0, sN = lat_on ? base + len : 0;
+
+    for (int s = blockIdx.x; s < a.count; s += gridDim.x) {
+        const long n_steps = a.nsteps ? __ldg(a.nsteps + s) : A.n_steps;
+        const double rs = a.rel ? __ldg(a.rel + s) : 1.0;
+        double* zp = A.zp_global ? A.zp_global + static_cast<std::size_t>(s) * A.n : sd + o.zp;
+        // ---- per-sample set-up: coefficients, z_0, generic weights
+        for (int k = tid; k < a.n_cells; k += T) cl[k] = __ldg(a.cells + k * S + s);
+        for (int i = tid; i < A.n; i += T) {
+            const double z = __ldg(A.z0 + i);
+            zn[i] = z;
+            zp[i] = z;
+        }
+        if (tid == 0) fail_step = INT_MAX;
+        __syncthreads();
+        for (int e = tid; e < a.n_slots; e += T) {
+            const unsigned c = __ldg(a.slot_cell + e);
+            double w;
+            if (!(c & kOvfFlag)) {
+                w = cl[c] * __ldg(a.slot_a0 + e);
+            } else {
+                const int k = c & ~kOvfFlag;
+                w = 0.0;
+                for (int t = __ldg(a.ovf_start + k); t < __ldg(a.ovf_start + k + 1); ++t)
+                    w += cl[__ldg(a.ovf_cell + t)] * __ldg(a.ovf_a0 + t);
+            }
+            sd[o.gw + e] = w;
+        }
+        double kE = 0, kW = 0, kNS = 0, dg = 0;
+        if (lat_on) {
+            const int row = cy[j0] * a.cells_x;
+            const double cR = cl[row + cx[ci]], cL = cl[row + cx[ci - 1]];
+            kE = cR * inv_h;
+            kW = cL * inv_h;
+            kNS = (cL + cR) * (0.5 * inv_h);
+            dg = kE + kW + 2.0 * kNS;
+        }
+        // ---- start-up (sweep_kernel<true>): z_1 = z_0 + f (0 - A z_0)
+        double gg[K], ggg[G];
+        {
+            const double fi = A.init_factor * rs;
+            lat_solve_g<K, G>(sd, o.v0, zn, base, len, W, sS, sN, inv_h, kE, kW, kNS, dg, grow, grs, gg);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (k < len) {
+                    gg[k] = zn[base + k] + fi * (0.0 - gg[k]);
+                    if (!(fabs(gg[k]) <= 1e100)) atomicMin(&fail_step, 1);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                ggg[u] = 0.0;
+                if (grow[u] >= 0) {
+                    ggg[u] = zn[grow[u]] + fi * (0.0 - lat_solve_row(A, grow[u], zn, cl));
+                    if (!(fabs(ggg[u]) <= 1e100)) atomicMin(&fail_step, 1);
+                }
+            }
+            for (int i = nr + tid; i < A.n; i += T) {
+                const double out = zn[i] + fi * (0.0 - lat_solve_row(A, i, zn, cl));
+                sd[o.v1 + i - nr] = out;
+                if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, 1);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (k < len) zn[base + k] = gg[k];
+#pragma unroll
+            for (int u = 0; u < G; ++u)
+                if (grow[u] >= 0) zn[grow[u]] = ggg[u];
+            for (int i = nr + tid; i < A.n; i += T) zn[i] = sd[o.v1 + i - nr];
+            __syncthreads();
+        }
+        const double factor = A.factor * rs;
+        const double c0 = a.c0 * rs;
+        for (long st = 1; st < n_steps; ++st) {
+            const int step = static_cast<int>(st + 1);
+            // ---- sweep: g = A z_n on R rows (lattice rows by the substep
+            // stencil, the others as sweep_rows_kernel), leap-frog update of
+            // the rows outside R (z_{n+1} parked in v1 until every read of
+            // z_n is done)
+            lat_solve_g<K, G>(sd, o.v0, zn, base, len, W, sS, sN, inv_h, kE, kW, kNS, dg, grow, grs, gg);
+#pragma unroll
+            for (int u = 0; u < G; ++u) ggg[u] = grow[u] >= 0 ? lat_solve_row(A, grow[u], zn, cl) : 0.0;
+            for (int i = nr + tid; i < A.n; i += T) {
+                const double zi = zn[i];
+                const double out = 2.0 * zi - zp[i] - factor * lat_solve_row(A, i, zn, cl);
+                sd[o.v1 + i - nr] = out;
+                zp[i] = zi;
+                if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+            }
+            __syncthreads();
+            for (int i = nr + tid; i < A.n; i += T) zn[i] = sd[o.v1 + i - nr];
+            // ---- substeps (lattice_substep_kernel), d_1 = -c0 g
+            double d[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                d[k] = -c0 * gg[k];
+                if (k < len) sd[o.v0 + base + k] = d[k] * inv_h;
+            }
+            double gd[G], gdp[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                gdp[u] = 0.0;
+                gd[u] = -c0 * ggg[u];
+                if (grow[u] >= 0) sd[o.v0 + grow[u]] = gd[u] * grs[u];
+            }
+            __syncthreads();
+            for (int m = 1; m <= a.p - 1; ++m) {
+                const int cur = (m & 1) ? o.v0 : o.v1;
+                const int nxt = (m & 1) ? o.v1 : o.v0;
+                const double beta = sd[o.beta + m - 1];
+                const double cmm = sd[o.cm + m - 1] * rs;
+                const double onepb = 1.0 + beta;
+                double gaq[G];
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    double acc = 0.0, acc2 = 0.0;
+                    const int q0 = gslot[u];
+#define WMC_GEN_SLOT(E, ACC) ACC += sd[o.gw + q0 + 32 * (E)] * sd[cur + gcol[q0 + 32 * (E)]]
+                    switch (gwid[u]) {
+                        case 8: WMC_GEN_SLOT(7, acc2); [[fallthrough]];
+                        case 7: WMC_GEN_SLOT(6, acc); [[fallthrough]];
+                        case 6: WMC_GEN_SLOT(5, acc2); [[fallthrough]];
+                        case 5: WMC_GEN_SLOT(4, acc); [[fallthrough]];
+                        case 4: WMC_GEN_SLOT(3, acc2); [[fallthrough]];
+                        case 3: WMC_GEN_SLOT(2, acc); [[fallthrough]];
+                        case 2: WMC_GEN_SLOT(1, acc2); [[fallthrough]];
+                        case 1: WMC_GEN_SLOT(0, acc); [[fallthrough]];
+                        default: break;
+                    }
+#undef WMC_GEN_SLOT
+                    gaq[u] = acc + acc2;
+                }
+                const int ce = cur + base + W, cw_ = cur + base - W;
+                const double vnl = sd[cur + sN];
+                double vs = sd[cur + sS];
+                double vk = d[0] * inv_h;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const double ve = sd[ce + k], vw = sd[cw_ + k];
+                    const double vn = (k + 1 < len) ? d[k + 1] * inv_h : vnl;
+                    const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
+                    const double dpk = m == 1 ? 0.0 : sd[nxt + base + k] * hh;
+                    const double next = onepb * d[k] - beta * dpk - cmm * (gg[k] + aq);
+                    d[k] = next;
+                    if (k < len) sd[nxt + base + k] = next * inv_h;
+                    vs = vk;
+                    vk = vn;
+                }
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    const double next = onepb * gd[u] - beta * gdp[u] - cmm * (ggg[u] + gaq[u]);
+                    gdp[u] = gd[u];
+                    gd[u] = next;
+                    if (grow[u] >= 0) sd[nxt + grow[u]] = next * grs[u];
+                }
+                __syncthreads();
+            }
+            // ---- R update (r_update_kernel): z_{n+1} = 2 z_n - z_{n-1} + 2 d_p
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (k < len) {
+                    const int i = base + k;
+                    const double zi = zn[i];
+                    const double out = 2.0 * zi - zp[i] + 2.0 * d[k];
+                    zp[i] = zi;
+                    zn[i] = out;
+                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                }
+#pragma unroll
+            for (int u = 0; u < G; ++u)
+                if (grow[u] >= 0) {
+                    const int i = grow[u];
+                    const double zi = zn[i];
+                    const double out = 2.0 * zi - zp[i] + 2.0 * gd[u];
+                    zp[i] = zi;
+                    zn[i] = out;
+                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                }
+            __syncthreads();
+        }
+        // ---- QoI of the final state (qoi_kernel; NaN for a failed sample)
+        for (int k = tid; k < A.nq; k += T) {
+            double acc = 0.0;
+            for (int q = __ldg(A.qptr + k); q < __ldg(A.qptr + k + 1); ++q)
+                acc += __ldg(A.qw + q) * (zn[__ldg(A.qdof + q)] / __ldg(A.qsm + q));
+            A.q[k * S + s] = fail_step == INT_MAX ? acc : __longlong_as_double(0x7ff8000000000000LL);
+        }
+        if (tid == 0) A.fail[s] = fail_step;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3: QoI per sample, Q = sum_t w_t (z_t / sqrt(M_t)) over the box nodes in a
 // fixed order (deterministic); failed samples report NaN.
 
@@ -1688,5 +2042,39 @@ int launch_small_solve(const SmallArgs& a, int grid, void* stream) {
     return static_cast<int>(cudaGetLastError());
 }
 
+
+
+int lattice_solve_smem_bytes(const LatSolveArgs& a) {
+    return lat_solve_offsets(a).total * static_cast<int>(sizeof(double));
+}
+
+int lattice_solve_max_smem(int device) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, lattice_solve_kernel<512, 8, 2>) != cudaSuccess) return 0;
+    return optin - static_cast<int>(fa.sharedSizeBytes);
+}
+
+template <int T, int K, int G>
+static int launch_lat_solve(const LatSolveArgs& a, int grid, cudaStream_t st) {
+    static int configured = -1;
+    if (configured < 0) {
+        int device = 0;
+        cudaGetDevice(&device);
+        configured = static_cast<int>(cudaFuncSetAttribute(lattice_solve_kernel<T, K, G>,
+                                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           lattice_solve_max_smem(device)));
+    }
+    if (configured != 0) return configured;
+    lattice_solve_kernel<T, K, G><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int launch_lattice_solve(const LatSolveArgs& a, int grid, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (a.lat.threads == 512 && a.lat.strip_k == 8) return launch_lat_solve<512, 8, 2>(a, grid, st);
+    return static_cast<int>(cudaErrorInvalidValue);
+}
 
 }  // namespace wmc

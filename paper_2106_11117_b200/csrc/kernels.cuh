@@ -250,6 +250,41 @@ struct SmallArgs {
 };
 
 int small_smem_bytes(const SmallArgs& a);
+
+// Fused lattice solve: the whole solve of one sample per CTA (persistent over
+// the batch) for lattice levels whose state fits one SM -- start-up, every
+// global step's sweep (g = A z_n on all rows from the sweep descriptors,
+// leap-frog update of the rows outside R), the p - 1 substeps of the lattice
+// kernel and the R update, check_finite and the QoI.  z_n lives in shared
+// memory, z_{n-1} too when it fits (else in a per-sample global buffer read
+// and written only by the row's owner).  No HBM traffic per step, and the
+// per-sample set-up (cell coefficients, generic weights) once per solve
+// instead of once per step.  Arithmetic: see kernels.cu (K6).
+struct LatSolveArgs {
+    LatArgs lat;                 // substep tables and constants (gd unused)
+    int n;                       // all rows; rows [n_r, n) are outside R
+    const int* row_ptr;          // sweep tables (as SweepArgs)
+    const int* ent;
+    int col_bits, col_mask;
+    const double* a0;
+    const int4* row_desc;
+    const double2* wtype;
+    const double* z0;
+    double init_factor, factor;  // start-up and coarse-row (leap-frog) factors
+    long n_steps;
+    double* zp_global;           // z_{n-1} at [s * n + i] when it does not fit on chip (NULL: shared)
+    int nq;
+    const int* qptr;
+    const int* qdof;
+    const double* qw;
+    const double* qsm;
+    double* q;                   // [k * S + s]
+    int* fail;                   // per sample: first non-finite step (INT_MAX: none)
+};
+
+int lattice_solve_smem_bytes(const LatSolveArgs& a);
+int lattice_solve_max_smem(int device);
+int launch_lattice_solve(const LatSolveArgs& a, int grid, void* stream);  // returns cudaError_t
 int small_max_smem(int device);  // largest dynamic shared memory the kernel can take
 int launch_small_solve(const SmallArgs& a, int grid, void* stream);  // returns cudaError_t
 

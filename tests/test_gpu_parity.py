@@ -235,6 +235,46 @@ def test_adaptive_mlmc_matches_reference_run_mlmc(golden):
     assert res.bias == pytest.approx(g["bias"], rel=MOMENT_RTOL)
 
 
+@pytest.mark.parametrize("lvl", [0, 1, 2])
+def test_fused_lattice_solve_matches_the_step_kernels(lvl, monkeypatch):
+    """The fused lattice solve (whole solves on chip, one launch per batch)
+    against the per-step sweep / lattice substep / R update kernels on
+    config-1 level meshes (fused on levels 0 and 1; level 2 is forced onto
+    the global-history layout): the same operator, lattice rows' A z_n from
+    the substep stencil instead of the sweep descriptors, so agreement at
+    rounding level."""
+    defs = configs.config1()
+    if lvl == 2:
+        monkeypatch.setenv("WMC_FUSED_ZP_GLOBAL", "1")
+    fused = [configs.build_level(d) for d in defs[max(lvl - 1, 0):lvl + 1]]
+    monkeypatch.delenv("WMC_FUSED_ZP_GLOBAL", raising=False)
+    monkeypatch.setenv("WMC_FUSED", "0")
+    plain = [configs.build_level(d) for d in defs[max(lvl - 1, 0):lvl + 1]]
+    monkeypatch.delenv("WMC_FUSED")
+    assert fused[-1].info["fused"] in (1, 2) and plain[-1].info["fused"] == 0
+    assert fused[-1].info["substep_path"] == plain[-1].info["substep_path"] == 1
+    pair = (lambda lv: (lv[-1], lv[0] if lvl else None))
+    n = 300 if lvl < 2 else 90
+    dq_f, qf_f, _ = wavemc.eval_pairs(*pair(fused), 0, lvl, 5, n)
+    dq_p, qf_p, _ = wavemc.eval_pairs(*pair(plain), 0, lvl, 5, n)
+    assert per_sample_rel(qf_f, qf_p) < 1e-12
+    assert np.max(np.abs(dq_f - dq_p) / np.abs(qf_p)) < 1e-12
+
+
+def test_fused_lattice_solve_with_global_history(monkeypatch):
+    """z_{n-1} in the per-sample global buffer instead of shared memory (the
+    layout levels with larger n take) gives the same bits."""
+    d = configs.config1()[1]
+    a = configs.build_level(d)
+    monkeypatch.setenv("WMC_FUSED_ZP_GLOBAL", "1")
+    b = configs.build_level(d)
+    monkeypatch.delenv("WMC_FUSED_ZP_GLOBAL")
+    assert a.info["fused"] == 1 and b.info["fused"] == 2
+    _, qa, _ = wavemc.eval_pairs(a, None, 0, 1, 0, 200)
+    _, qb, _ = wavemc.eval_pairs(b, None, 0, 1, 0, 200)
+    assert np.array_equal(qa, qb)
+
+
 @pytest.mark.parametrize("path", ["global", "onchip"])
 def test_substep_paths_agree(path, monkeypatch):
     """The HBM-resident and the generic on-chip substep kernels against the

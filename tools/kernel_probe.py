@@ -55,7 +55,7 @@ def main():
         upd = a.count * lv.info["dof_updates_per_solve"]
         if a.profile and r == a.repeat - 1:
             print("profile", wavemc.profile_read(lv))
-        print(f"level {a.level} path={lv.info['substep_path']} n={lv.info['n']} n_r={lv.info['n_r']} "
+        print(f"level {a.level} path={lv.info['substep_path']} fused={lv.info['fused']} n={lv.info['n']} n_r={lv.info['n_r']} "
               f"{a.count} solves {dt:.3f} s "
               f"{upd / dt:.3e} DOF-updates/s q0={q[0]:.12e}")
 
