@@ -7,6 +7,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -253,6 +254,92 @@ namespace {
 
 int round64(long v) { return static_cast<int>((v + 63) / 64 * 64); }
 
+// Generic SELL rows of the lattice kernels: lane placement for shared-memory
+// banks.  A 64-bit shared access is served per half-warp; it costs as many
+// wavefronts as the largest number of distinct addresses that fall into one
+// 8-byte bank (address mod 16 doubles).  The gathers v[col] of each slot and
+// the store of v[row] are the random accesses, so rows are permuted among
+// positions holding the same entry count (slice widths, and every row's
+// arithmetic, unchanged) by a seeded local search that lowers the summed
+// wavefronts.  Rows past a row's count gather column 0 (padding).
+int half_cost(const wmc::LevelTables& t, const std::vector<int>& ord, int h, int width) {
+    const int n_gen = static_cast<int>(ord.size());
+    int cost = 0;
+    int cnt[16];
+    int addr[16][16];
+    for (int e = -1; e < width; ++e) {  // e = -1: the store of v[row]
+        std::fill(cnt, cnt + 16, 0);
+        int worst = 0;
+        for (int l = 0; l < 16; ++l) {
+            const int p = h * 16 + l;
+            if (p >= n_gen) break;
+            const int q = ord[p];
+            int a;
+            if (e < 0)
+                a = t.gen_rows[q];
+            else
+                a = e < t.gen_ptr[q + 1] - t.gen_ptr[q] ? t.gen_col[t.gen_ptr[q] + e] : 0;
+            const int b = a & 15;
+            bool seen = false;
+            for (int k = 0; k < cnt[b]; ++k) seen |= addr[b][k] == a;
+            if (!seen) {
+                addr[b][cnt[b]++] = a;
+                worst = std::max(worst, cnt[b]);
+            }
+        }
+        cost += worst;
+    }
+    return cost;
+}
+
+void optimize_generic_lanes(const wmc::LevelTables& t, std::vector<int>& ord) {
+    const int n_gen = static_cast<int>(ord.size());
+    if (n_gen < 2) return;
+    const int n_half = (n_gen + 15) / 16;
+    std::vector<int> width(n_half, 0), cost(n_half, 0);
+    auto w_of = [&](int p) { return t.gen_ptr[ord[p] + 1] - t.gen_ptr[ord[p]]; };
+    for (int p = 0; p < n_gen; ++p) width[p / 16] = std::max(width[p / 16], w_of(p));
+    for (int h = 0; h + 1 < n_half; h += 2) width[h] = width[h + 1] = std::max(width[h], width[h + 1]);  // slice width
+    for (int h = 0; h < n_half; ++h) cost[h] = half_cost(t, ord, h, width[h]);
+    long before_total = 0;
+    for (int c : cost) before_total += c;
+    // positions grouped by the row's entry count: swaps stay inside a group
+    std::map<int, std::vector<int>> groups;
+    for (int p = 0; p < n_gen; ++p) groups[w_of(p)].push_back(p);
+    std::uint64_t x = 0x9e3779b97f4a7c15ull;
+    auto rnd = [&](std::size_t n) {
+        x ^= x << 13;
+        x ^= x >> 7;
+        x ^= x << 17;
+        return static_cast<std::size_t>(x % n);
+    };
+    for (auto& kv : groups) {
+        const std::vector<int>& pos = kv.second;
+        if (pos.size() < 2) continue;
+        const long iters = 400L * static_cast<long>(pos.size());
+        for (long it = 0; it < iters; ++it) {
+            const int pa = pos[rnd(pos.size())], pb = pos[rnd(pos.size())];
+            const int ha = pa / 16, hb = pb / 16;
+            if (ha == hb) continue;
+            const int before = cost[ha] + cost[hb];
+            std::swap(ord[pa], ord[pb]);
+            const int ca = half_cost(t, ord, ha, width[ha]), cb = half_cost(t, ord, hb, width[hb]);
+            if (ca + cb <= before) {
+                cost[ha] = ca;
+                cost[hb] = cb;
+            } else {
+                std::swap(ord[pa], ord[pb]);
+            }
+        }
+    }
+    if (std::getenv("WMC_BANKS_VERBOSE")) {
+        long after_total = 0;
+        for (int c : cost) after_total += c;
+        std::fprintf(stderr, "generic lanes: %d rows, half-warp wavefronts per substep %ld -> %ld\n", n_gen,
+                     before_total, after_total);
+    }
+}
+
 void build_device_level(wmc_level& L) {
     const wmc::LevelTables& t = L.tab;
     check(cudaSetDevice(L.device), "cudaSetDevice");
@@ -430,6 +517,7 @@ void build_device_level(wmc_level& L) {
             std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
                 return t.gen_ptr[x + 1] - t.gen_ptr[x] > t.gen_ptr[y + 1] - t.gen_ptr[y];
             });
+        if (!fixed_width && !std::getenv("WMC_GEN_NO_BANKS")) optimize_generic_lanes(t, ord);
         std::vector<int> grows(n_gen);
         std::vector<double> grs(n_gen);
         for (int q = 0; q < n_gen; ++q) {

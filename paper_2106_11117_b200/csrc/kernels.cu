@@ -970,14 +970,18 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
         gwid[u] = wsl >= 0 ? (__ldg(a.gen_soff + sl + 1) - __ldg(a.gen_soff + sl)) >> 5 : 0;
     }
     __syncthreads();
-    int j0 = 1, len = 0;
-    if (lat_on) {
+    // column-major box: the strip's nodes are base .. base + len - 1.  Idle
+    // lanes of a strip (columns past m - 1) shadow its last column: their
+    // loads hit the same addresses (a broadcast, not a bank conflict); they
+    // never store (len 0).  Threads past the last strip point at node (1, 1).
+    const bool shadow = !lat_on && strip < a.n_strips;
+    int j0 = 1, len = 0, span = 0;
+    if (lat_on || shadow) {
         j0 = sj0[strip];
-        len = slen[strip];
+        span = slen[strip];
     }
-    // column-major box: the strip's nodes are base .. base + len - 1; idle
-    // threads point at node (1, 1) and never store
-    const int base = lat_on ? ci * W + j0 : W + 1;
+    if (lat_on) len = span;
+    const int base = (lat_on || shadow) ? (lat_on ? ci : a.m - 1) * W + j0 : W + 1;
 
     for (int s = blockIdx.x; s < a.count; s += gridDim.x) {
         // per-sample CFL: finished samples are left alone, dt^2 constants scale
@@ -1037,7 +1041,7 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
         __syncthreads();
 
         // ---- p - 1 substeps, state on chip
-        const int sS = lat_on ? base - 1 : 0, sN = lat_on ? base + len : 0;
+        const int sS = (lat_on || shadow) ? base - 1 : 0, sN = (lat_on || shadow) ? base + span : 0;
         for (int m = 1; m <= a.p - 1; ++m) {
             const int cur = (m & 1) ? o.v0 : o.v1;
             const int nxt = (m & 1) ? o.v1 : o.v0;
@@ -1559,13 +1563,16 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
         gwid[u] = wsl >= 0 ? (__ldg(a.gen_soff + sl + 1) - __ldg(a.gen_soff + sl)) >> 5 : 0;
     }
     __syncthreads();
-    int j0 = 1, len = 0;
-    if (lat_on) {
+    // idle lanes shadow the strip's last column (see lattice_substep_kernel)
+    const bool shadow = !lat_on && strip < a.n_strips;
+    int j0 = 1, len = 0, span = 0;
+    if (lat_on || shadow) {
         j0 = sj0[strip];
-        len = slen[strip];
+        span = slen[strip];
     }
-    const int base = lat_on ? ci * W + j0 : W + 1;
-    const int sS = lat_on ? base - 1 : 0, sN = lat_on ? base + len : 0;
+    if (lat_on) len = span;
+    const int base = (lat_on || shadow) ? (lat_on ? ci : a.m - 1) * W + j0 : W + 1;
+    const int sS = (lat_on || shadow) ? base - 1 : 0, sN = (lat_on || shadow) ? base + span : 0;
 
     for (int s = blockIdx.x; s < a.count; s += gridDim.x) {
         const long n_steps = a.nsteps ? __ldg(a.nsteps + s) : A.n_steps;
