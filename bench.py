@@ -483,16 +483,27 @@ def roofline_from_profile(levels, counts, prof, step_ms):
       HBM-resident substep   8 B x 4 |R| per substep (d_m, d_{m-1}, g in,
                              d_{m+1} out) + 8 B x 2 |R| on the last (z_n, z_{n-1})
       R update               8 B x 4 |R|"""
+    fused_lv = [bool(lv.info.get("fused")) for lv in levels]
     sweep_ms = sum(p["sweep_ms"] for p in prof)
-    sub_ms = sum(p["sub_ms"] for p in prof)
+    sub_ms = sum(p["sub_ms"] for p, f in zip(prof, fused_lv) if not f)
+    fused_ms = sum(p["sub_ms"] for p, f in zip(prof, fused_lv) if f)
     upd_ms = sum(p["upd_ms"] for p in prof)
     sweep_bytes = sub_bytes = sub_flops = sub_updates = 0.0
+    fused_bytes = fused_updates = fused_flops = 0.0
     global_path = any(lv.info["substep_path"] in (3, 4) for lv in levels)
     for l, lv in enumerate(levels):
         for lvl in ([l] + ([l - 1] if l else [])):
             info = levels[lvl].info
             n, nr, steps, p = info["n"], info["n_r"], info["n_steps"], info["p"]
             c = counts[l]
+            if fused_lv[lvl]:
+                # whole solves on chip: HBM sees z_0 and the QoI only; the
+                # SURVEY 8(d) algorithmic figure (24 B per DOF per global step)
+                # is reported as the HBM-equivalent rate of the same work
+                fused_bytes += 24.0 * c * steps * n
+                fused_updates += c * info["dof_updates_per_solve"]
+                fused_flops += c * (steps - 1) * ((p - 1) * (2.0 * info["ap_nnz"] + 7.0 * nr) + 2.0 * info["nnz"])
+                continue
             sweep_bytes += 8.0 * c * (steps - 1) * (2 * n + (n - nr))
             if info["substep_path"] == 4:
                 # nested tiers: p^k stages of tier k per step, each reading
@@ -525,6 +536,16 @@ def roofline_from_profile(levels, counts, prof, step_ms):
                            "achieved_GBps": gbps(sub_bytes, sub_ms)},
                "r_update": {"ms": upd_ms, "launches": sum(p["upd_launches"] for p in prof),
                             "share_of_step": upd_ms / step_ms if step_ms else None}}
+    if fused_ms:
+        kernels["fused_solve"] = {
+            "ms": fused_ms, "levels": [i for i, f in enumerate(fused_lv) if f],
+            "launches": sum(p["sub_launches"] for p, f in zip(prof, fused_lv) if f),
+            "share_of_step": fused_ms / step_ms if step_ms else None,
+            "bound": "on-chip (shared-memory wavefronts + latency; no per-step HBM traffic)",
+            "dof_updates_per_s": fused_updates / (fused_ms * 1e-3),
+            "fp64_TFLOPs": fused_flops / (fused_ms * 1e-3) / 1e12,
+            "hbm_equivalent_GBps": gbps(fused_bytes, fused_ms),
+            "note": "HBM-equivalent = SURVEY 8(d) algorithmic 24 B per DOF per global step over the kernel time"}
     # DRAM traffic per launch: the measured/algorithmic ratio of the committed
     # ncu capture (profiles/traffic.json) times this run's algorithmic bytes
     # per launch
@@ -552,8 +573,9 @@ def roofline_from_profile(levels, counts, prof, step_ms):
         t, src = traffic("sweep", sweep_bytes, kernels["sweep"]["launches"])
         roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",
                 "traffic": t, "traffic_capture": src,
-                "note": ("HBM roofline of the sweep kernel (algorithmic bytes); the dominant substep kernel is "
-                         "on-chip (shared-memory) bound, see kernels.substep")}
+                "note": ("HBM roofline of the sweep kernel (algorithmic bytes, levels without the fused solve); "
+                         "the dominant kernels keep the state on chip and are shared-memory bound, see "
+                         "kernels.fused_solve / kernels.substep")}
     return roof, kernels
 
 

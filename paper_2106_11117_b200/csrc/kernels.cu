@@ -856,6 +856,40 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
 // Generic rows (box ring + transition belt) use a SELL of per-sample
 // weights w_ij = A_ij(omega) sqrt(M_j) acting on v.
 
+// Generic SELL row of the lattice kernels: sum_e w_e v[col_e] over the
+// slice's WD slots, odd slots into a second chain, widest slot first.  One
+// straight-line block per width (selected by a warp-uniform switch) so the
+// slot loads issue back to back instead of one slot per basic block.
+template <int WD>
+__device__ __forceinline__ double gen_gather(const double* __restrict__ sd, int ogw, int cur,
+                                             const std::uint16_t* __restrict__ gcol, int q0) {
+    double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+    for (int e = WD - 1; e >= 0; --e) {
+        const double t = sd[cur + gcol[q0 + 32 * e]];
+        if (e & 1)
+            acc2 += sd[ogw + q0 + 32 * e] * t;
+        else
+            acc += sd[ogw + q0 + 32 * e] * t;
+    }
+    return acc + acc2;
+}
+
+__device__ __forceinline__ double gen_gather_w(int wd, const double* __restrict__ sd, int ogw, int cur,
+                                               const std::uint16_t* __restrict__ gcol, int q0) {
+    switch (wd) {
+        case 8: return gen_gather<8>(sd, ogw, cur, gcol, q0);
+        case 7: return gen_gather<7>(sd, ogw, cur, gcol, q0);
+        case 6: return gen_gather<6>(sd, ogw, cur, gcol, q0);
+        case 5: return gen_gather<5>(sd, ogw, cur, gcol, q0);
+        case 4: return gen_gather<4>(sd, ogw, cur, gcol, q0);
+        case 3: return gen_gather<3>(sd, ogw, cur, gcol, q0);
+        case 2: return gen_gather<2>(sd, ogw, cur, gcol, q0);
+        case 1: return gen_gather<1>(sd, ogw, cur, gcol, q0);
+        default: return 0.0;
+    }
+}
+
 // Shared-memory layout of the lattice kernel, in units of doubles from the
 // dynamic shared base (integer offsets keep every access a 32-bit shared
 // address): v0 | v1 | gw | sa0 | cl | beta | cm | then 8-byte aligned int
@@ -1051,24 +1085,7 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
             double gaq[G];
 #pragma unroll
             for (int u = 0; u < G; ++u) {
-                double acc = 0.0, acc2 = 0.0;  // two chains: the gather's loads overlap
-                // warp-uniform jump into a straight-line gather of the
-                // slice's width (Duff's device; widths are <= kLatGenWidth)
-                const int q0 = gslot[u];
-#define WMC_GEN_SLOT(E, A) A += sd[o.gw + q0 + 32 * (E)] * sd[cur + gcol[q0 + 32 * (E)]]
-                switch (gwid[u]) {
-                    case 8: WMC_GEN_SLOT(7, acc2); [[fallthrough]];
-                    case 7: WMC_GEN_SLOT(6, acc); [[fallthrough]];
-                    case 6: WMC_GEN_SLOT(5, acc2); [[fallthrough]];
-                    case 5: WMC_GEN_SLOT(4, acc); [[fallthrough]];
-                    case 4: WMC_GEN_SLOT(3, acc2); [[fallthrough]];
-                    case 3: WMC_GEN_SLOT(2, acc); [[fallthrough]];
-                    case 2: WMC_GEN_SLOT(1, acc2); [[fallthrough]];
-                    case 1: WMC_GEN_SLOT(0, acc); [[fallthrough]];
-                    default: break;
-                }
-#undef WMC_GEN_SLOT
-                gaq[u] = acc + acc2;
+                gaq[u] = gen_gather_w(gwid[u], sd, o.gw, cur, gcol, gslot[u]);
             }
             const int ce = cur + base + W, cw_ = cur + base - W;
             const double vnl = sd[cur + sN];
@@ -1664,12 +1681,16 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
             }
             __syncthreads();
             for (int i = nr + tid; i < A.n; i += T) zn[i] = sd[o.v1 + i - nr];
-            // ---- substeps (lattice_substep_kernel), d_1 = -c0 g
+            // ---- substeps (lattice_substep_kernel's recursion), d_1 = -c0 g.
+            // Lattice nodes recurse on v = d / h itself (what the stencil and
+            // the neighbours read): v_{m+1} = (1 + beta) v_m - beta v_{m-1}
+            // - (c_m / h)(g + A d_m), three multiplies per node fewer than
+            // carrying d; d_p = h v_p at the update
             double d[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                d[k] = -c0 * gg[k];
-                if (k < len) sd[o.v0 + base + k] = d[k] * inv_h;
+                d[k] = (-c0 * gg[k]) * inv_h;
+                if (k < len) sd[o.v0 + base + k] = d[k];
             }
             double gd[G], gdp[G];
 #pragma unroll
@@ -1685,39 +1706,25 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 const double beta = sd[o.beta + m - 1];
                 const double cmm = sd[o.cm + m - 1] * rs;
                 const double onepb = 1.0 + beta;
+                const double cmh = cmm * inv_h;
                 double gaq[G];
 #pragma unroll
                 for (int u = 0; u < G; ++u) {
-                    double acc = 0.0, acc2 = 0.0;
-                    const int q0 = gslot[u];
-#define WMC_GEN_SLOT(E, ACC) ACC += sd[o.gw + q0 + 32 * (E)] * sd[cur + gcol[q0 + 32 * (E)]]
-                    switch (gwid[u]) {
-                        case 8: WMC_GEN_SLOT(7, acc2); [[fallthrough]];
-                        case 7: WMC_GEN_SLOT(6, acc); [[fallthrough]];
-                        case 6: WMC_GEN_SLOT(5, acc2); [[fallthrough]];
-                        case 5: WMC_GEN_SLOT(4, acc); [[fallthrough]];
-                        case 4: WMC_GEN_SLOT(3, acc2); [[fallthrough]];
-                        case 3: WMC_GEN_SLOT(2, acc); [[fallthrough]];
-                        case 2: WMC_GEN_SLOT(1, acc2); [[fallthrough]];
-                        case 1: WMC_GEN_SLOT(0, acc); [[fallthrough]];
-                        default: break;
-                    }
-#undef WMC_GEN_SLOT
-                    gaq[u] = acc + acc2;
+                    gaq[u] = gen_gather_w(gwid[u], sd, o.gw, cur, gcol, gslot[u]);
                 }
                 const int ce = cur + base + W, cw_ = cur + base - W;
                 const double vnl = sd[cur + sN];
                 double vs = sd[cur + sS];
-                double vk = d[0] * inv_h;
+                double vk = d[0];
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const double ve = sd[ce + k], vw = sd[cw_ + k];
-                    const double vn = (k + 1 < len) ? d[k + 1] * inv_h : vnl;
+                    const double vn = (k + 1 < len) ? d[k + 1] : vnl;
                     const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
-                    const double dpk = m == 1 ? 0.0 : sd[nxt + base + k] * hh;
-                    const double next = onepb * d[k] - beta * dpk - cmm * (gg[k] + aq);
+                    const double vpk = m == 1 ? 0.0 : sd[nxt + base + k];
+                    const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
                     d[k] = next;
-                    if (k < len) sd[nxt + base + k] = next * inv_h;
+                    if (k < len) sd[nxt + base + k] = next;
                     vs = vk;
                     vk = vn;
                 }
@@ -1736,7 +1743,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 if (k < len) {
                     const int i = base + k;
                     const double zi = zn[i];
-                    const double out = 2.0 * zi - zp[i] + 2.0 * d[k];
+                    const double out = 2.0 * zi - zp[i] + 2.0 * (d[k] * hh);
                     zp[i] = zi;
                     zn[i] = out;
                     if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
