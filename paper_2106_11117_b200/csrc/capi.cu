@@ -534,8 +534,12 @@ void build_device_level(wmc_level& L) {
                 const int q = sl * 32 + l;
                 if (q < n_gen) width = std::max(width, t.gen_ptr[ord[q] + 1] - t.gen_ptr[ord[q]]);
             }
-            for (int e = 0; e < width; ++e)
-                for (int l = 0; l < 32; ++l) {
+            // slots go in pairs, [slice][pair][lane][2]: a lane's two weights
+            // are one 16-byte load and its two columns one 32-bit load
+            width = (width + 1) & ~1;
+            for (int pr = 0; pr < width / 2; ++pr)
+                for (int l2 = 0; l2 < 64; ++l2) {
+                    const int l = l2 >> 1, e = 2 * pr + (l2 & 1);
                     const int q = sl * 32 + l;
                     std::uint16_t c = 0;
                     double a1 = 0.0;

@@ -857,20 +857,22 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
 // weights w_ij = A_ij(omega) sqrt(M_j) acting on v.
 
 // Generic SELL row of the lattice kernels: sum_e w_e v[col_e] over the
-// slice's WD slots, odd slots into a second chain, widest slot first.  One
-// straight-line block per width (selected by a warp-uniform switch) so the
-// slot loads issue back to back instead of one slot per basic block.
-template <int WD>
+// slice's 2 NP slots, odd slots into a second chain, widest slot first.
+// Slots are stored in pairs ([slice][pair][lane][2]; q0 = slice offset + 2
+// lane): one 16-byte load brings a pair's weights, one 32-bit load its two
+// columns.  One straight-line block per width (selected by a warp-uniform
+// switch) so the slot loads issue back to back.
+template <int NP>
 __device__ __forceinline__ double gen_gather(const double* __restrict__ sd, int ogw, int cur,
                                              const std::uint16_t* __restrict__ gcol, int q0) {
+    const unsigned* gc2 = reinterpret_cast<const unsigned*>(gcol);
     double acc = 0.0, acc2 = 0.0;
 #pragma unroll
-    for (int e = WD - 1; e >= 0; --e) {
-        const double t = sd[cur + gcol[q0 + 32 * e]];
-        if (e & 1)
-            acc2 += sd[ogw + q0 + 32 * e] * t;
-        else
-            acc += sd[ogw + q0 + 32 * e] * t;
+    for (int p = NP - 1; p >= 0; --p) {
+        const double2 w = *reinterpret_cast<const double2*>(sd + ogw + q0 + 64 * p);
+        const unsigned c = gc2[(q0 + 64 * p) >> 1];
+        acc2 += w.y * sd[cur + (c >> 16)];
+        acc += w.x * sd[cur + (c & 0xffffu)];
     }
     return acc + acc2;
 }
@@ -878,14 +880,10 @@ __device__ __forceinline__ double gen_gather(const double* __restrict__ sd, int 
 __device__ __forceinline__ double gen_gather_w(int wd, const double* __restrict__ sd, int ogw, int cur,
                                                const std::uint16_t* __restrict__ gcol, int q0) {
     switch (wd) {
-        case 8: return gen_gather<8>(sd, ogw, cur, gcol, q0);
-        case 7: return gen_gather<7>(sd, ogw, cur, gcol, q0);
-        case 6: return gen_gather<6>(sd, ogw, cur, gcol, q0);
-        case 5: return gen_gather<5>(sd, ogw, cur, gcol, q0);
-        case 4: return gen_gather<4>(sd, ogw, cur, gcol, q0);
-        case 3: return gen_gather<3>(sd, ogw, cur, gcol, q0);
-        case 2: return gen_gather<2>(sd, ogw, cur, gcol, q0);
-        case 1: return gen_gather<1>(sd, ogw, cur, gcol, q0);
+        case 8: return gen_gather<4>(sd, ogw, cur, gcol, q0);
+        case 6: return gen_gather<3>(sd, ogw, cur, gcol, q0);
+        case 4: return gen_gather<2>(sd, ogw, cur, gcol, q0);
+        case 2: return gen_gather<1>(sd, ogw, cur, gcol, q0);
         default: return 0.0;
     }
 }
@@ -1000,7 +998,7 @@ __global__ void __launch_bounds__(T, 1) lattice_substep_kernel(LatArgs a) {
         grow[u] = q < a.n_gen ? __ldg(a.gen_rows + q) : -1;
         grs[u] = q < a.n_gen ? __ldg(a.gen_rs + q) : 0.0;
         const int sl = wsl >= 0 ? wsl : 0;  // idle warps point at slice 0 with width 0
-        gslot[u] = __ldg(a.gen_soff + sl) + lane;
+        gslot[u] = __ldg(a.gen_soff + sl) + 2 * lane;
         gwid[u] = wsl >= 0 ? (__ldg(a.gen_soff + sl + 1) - __ldg(a.gen_soff + sl)) >> 5 : 0;
     }
     __syncthreads();
@@ -1576,7 +1574,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
         grow[u] = q < a.n_gen ? __ldg(a.gen_rows + q) : -1;
         grs[u] = q < a.n_gen ? __ldg(a.gen_rs + q) : 0.0;
         const int sl = wsl >= 0 ? wsl : 0;
-        gslot[u] = __ldg(a.gen_soff + sl) + lane;
+        gslot[u] = __ldg(a.gen_soff + sl) + 2 * lane;
         gwid[u] = wsl >= 0 ? (__ldg(a.gen_soff + sl + 1) - __ldg(a.gen_soff + sl)) >> 5 : 0;
     }
     __syncthreads();

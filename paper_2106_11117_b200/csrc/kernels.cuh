@@ -109,7 +109,7 @@ struct LatArgs {
     const double* gen_rs;        // 1/sqrt(M)
     const int* gen_soff;         // slot offset of each 32-row slice (rows sorted by length), n_slices + 1
     const int* gen_warp_slice;   // [warp][G]: slice of the warp's u-th generic role (-1: none), balanced by width
-    const std::uint16_t* gen_col;  // per slot: [slice][width][32], padding: col 0, weight 0
+    const std::uint16_t* gen_col;  // per slot: [slice][width / 2][32][2] (slot pairs), padding: col 0, weight 0
     const double* slot_a0;       // per slot: a0 of the single term
     const std::uint16_t* slot_cell;  // per slot: its cell, or kOvfFlag | k: terms ovf_start[k] .. ovf_start[k+1]
     int n_ovf, n_ovf_terms;          // slots whose weight spans several cells (edge on a coefficient line)
