@@ -179,6 +179,10 @@ struct wmc_level {
     int* d_grc_cell = nullptr;
     double* d_grc_a0 = nullptr;
     int n_slots = 0;
+    int* d_rem_ptr = nullptr;  // fused solve: A (I - P) entries of the generic rows
+    int* d_rem_col = nullptr;
+    int* d_rem_cell = nullptr;
+    double* d_rem_a0 = nullptr;
     int lat_smem = 0;
     int lat_grid = 0;
     // batch state: ws[0] as the fine level of a pair, ws[1] as the coarse one
@@ -219,7 +223,8 @@ struct wmc_level {
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_warp_slice, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
-                        (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0})
+                        (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0,
+                        (void*)d_rem_ptr, (void*)d_rem_col, (void*)d_rem_cell, (void*)d_rem_a0})
             if (p) cudaFree(p);
         for (auto* p : d_tier_ptr) cudaFree(p);
         for (auto* p : d_tier_ent) cudaFree(p);
@@ -593,6 +598,26 @@ void build_device_level(wmc_level& L) {
         L.d_cellx = upload(t.lat_cellx);
         L.d_celly = upload(t.lat_celly);
         L.d_gen_rows = upload(grows);
+        {
+            // fused solve: A (I - P) entries of the generic rows (the A P part of
+            // g = A z_n comes from the SELL on v = z / sqrt(M)), sorted order
+            std::vector<int> rp{0}, rcol, rcell;
+            std::vector<double> ra0;
+            for (int q = 0; q < n_gen; ++q) {
+                const int r = grows[q];
+                for (int e = t.row_ptr[r]; e < t.row_ptr[r + 1]; ++e)
+                    if (!t.in_p[t.col[e]]) {
+                        rcol.push_back(t.col[e]);
+                        rcell.push_back(t.cell[e]);
+                        ra0.push_back(t.a0[e]);
+                    }
+                rp.push_back(static_cast<int>(rcol.size()));
+            }
+            L.d_rem_ptr = upload(rp);
+            L.d_rem_col = upload(rcol);
+            L.d_rem_cell = upload(rcell);
+            L.d_rem_a0 = upload(ra0);
+        }
         L.d_gen_rs = upload(grs);
         L.d_gen_soff = upload(soff);
         {
@@ -1195,6 +1220,10 @@ void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     a.factor = t.coarse_factor;
     a.n_steps = t.n_steps;
     a.zp_global = L.fused_zp_global ? ws.zb : nullptr;
+    a.rem_ptr = L.d_rem_ptr;
+    a.rem_col = L.d_rem_col;
+    a.rem_cell = L.d_rem_cell;
+    a.rem_a0 = L.d_rem_a0;
     a.nq = t.nq;
     a.qptr = L.d_qptr;
     a.qdof = L.d_qdof;

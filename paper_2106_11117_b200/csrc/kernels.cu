@@ -1527,6 +1527,18 @@ __device__ __forceinline__ void lat_solve_g(double* sd, int ov, const double* zn
     }
 }
 
+// g = A z_n on a generic R row of the fused solve: the row's A P part is the
+// SELL gather on v = z / sqrt(M) (published to v0 by every R row's owner),
+// the entries with columns outside P come from the small remainder table
+__device__ __forceinline__ double gen_full_row(const LatSolveArgs& A, const double* sd, int ogw, int ov,
+                                               const std::uint16_t* gcol, int gslot, int gwid, int q,
+                                               const double* zn, const double* cl) {
+    double rem = 0.0;
+    for (int t = __ldg(A.rem_ptr + q); t < __ldg(A.rem_ptr + q + 1); ++t)
+        rem += (cl[__ldg(A.rem_cell + t)] * __ldg(A.rem_a0 + t)) * zn[__ldg(A.rem_col + t)];
+    return gen_gather_w(gwid, sd, ogw, ov, gcol, gslot) + rem;
+}
+
 template <int T, int K, int G>
 __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
     extern __shared__ __align__(16) double sd[];
@@ -1565,12 +1577,13 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
     const int col = tid % a.cw, strip = tid / a.cw;
     const int ci = 1 + col;
     const bool lat_on = ci <= a.m - 1 && strip < a.n_strips;
-    int grow[G], gslot[G], gwid[G];
+    int grow[G], gslot[G], gwid[G], gq[G];
     double grs[G];
 #pragma unroll
     for (int u = 0; u < G; ++u) {
         const int wsl = __ldg(a.gen_warp_slice + (tid >> 5) * G + u);
         const int q = wsl >= 0 ? wsl * 32 + lane : a.n_gen;
+        gq[u] = q;
         grow[u] = q < a.n_gen ? __ldg(a.gen_rows + q) : -1;
         grs[u] = q < a.n_gen ? __ldg(a.gen_rs + q) : 0.0;
         const int sl = wsl >= 0 ? wsl : 0;
@@ -1640,7 +1653,8 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
             for (int u = 0; u < G; ++u) {
                 ggg[u] = 0.0;
                 if (grow[u] >= 0) {
-                    ggg[u] = zn[grow[u]] + fi * (0.0 - lat_solve_row(A, grow[u], zn, cl));
+                    ggg[u] = zn[grow[u]] + fi * (0.0 - gen_full_row(A, sd, o.gw, o.v0, gcol, gslot[u], gwid[u], gq[u],
+                                                                     zn, cl));
                     if (!(fabs(ggg[u]) <= 1e100)) atomicMin(&fail_step, 1);
                 }
             }
@@ -1669,7 +1683,8 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
             // z_n is done)
             lat_solve_g<K, G>(sd, o.v0, zn, base, len, W, sS, sN, inv_h, kE, kW, kNS, dg, grow, grs, gg);
 #pragma unroll
-            for (int u = 0; u < G; ++u) ggg[u] = grow[u] >= 0 ? lat_solve_row(A, grow[u], zn, cl) : 0.0;
+            for (int u = 0; u < G; ++u)
+                ggg[u] = grow[u] >= 0 ? gen_full_row(A, sd, o.gw, o.v0, gcol, gslot[u], gwid[u], gq[u], zn, cl) : 0.0;
             for (int i = nr + tid; i < A.n; i += T) {
                 const double zi = zn[i];
                 const double out = 2.0 * zi - zp[i] - factor * lat_solve_row(A, i, zn, cl);

@@ -273,6 +273,13 @@ struct LatSolveArgs {
     double init_factor, factor;  // start-up and coarse-row (leap-frog) factors
     long n_steps;
     double* zp_global;           // z_{n-1} at [s * n + i] when it does not fit on chip (NULL: shared)
+    // A (I - P) entries of the generic rows (sorted SELL order): g = A z_n on
+    // a generic row is the SELL gather on v = z / sqrt(M) (the A P part) plus
+    // these (columns outside P)
+    const int* rem_ptr;
+    const int* rem_col;
+    const int* rem_cell;
+    const double* rem_a0;
     int nq;
     const int* qptr;
     const int* qdof;
