@@ -1,6 +1,6 @@
 """Generate tests/golden/*.json from the UNMODIFIED reference library
 (oracle/_ref/wavemc_ref_driver) -- run in the build container, where
-/root/reference exists:  python oracle/make_golden.py [--only-config2 | --only-cfl | --only-experiments]
+/root/reference exists:  python oracle/make_golden.py [--only-config2 | --only-cfl | --only-experiments | --only-artifacts]
 
 The meshes come from the shared problem definition (the product's host mesh
 builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
@@ -120,6 +120,34 @@ def experiments(ref):
     dump("experiments.json", out)
 
 
+ARTIFACT_CONFIGS = {
+    # small sampling runs of the reference's own experiments: two tolerances,
+    # both integrators, a 64-point output grid, levels 0..3
+    "smooth1d": "experiment = smooth1d\neps = 0.008,0.004\nintegrator = both\ngrid_n = 64\nmax_level = 3\n",
+    "jump1d": "experiment = jump1d\neps = 0.008,0.004\nintegrator = both\ngrid_n = 64\nmax_level = 3\n",
+}
+
+
+def artifacts(ref, tmp):
+    """The reference's artifact files of its sampling experiments
+    (run_experiment -> run_sampling_experiment, src/experiments.cpp:365-409):
+    the config file and every CSV it writes, under tests/golden/artifacts/<exp>/."""
+    import shutil
+    for name, text in ARTIFACT_CONFIGS.items():
+        dst = os.path.join(GOLDEN, "artifacts", name)
+        shutil.rmtree(dst, ignore_errors=True)
+        os.makedirs(dst)
+        with open(os.path.join(dst, "experiment.cfg"), "w") as f:
+            f.write(text)
+        out = os.path.join(tmp, "art_" + name)
+        cfg = os.path.join(tmp, name + ".cfg")
+        with open(cfg, "w") as f:
+            f.write(text + f"workers = {os.cpu_count() or 1}\nout_dir = {out}\n")
+        ref.run("artifacts", "--config", cfg)
+        for fn in sorted(os.listdir(out)):
+            shutil.copy(os.path.join(out, fn), os.path.join(dst, fn))
+
+
 def main():
     build()
     ref = RefDriver()
@@ -132,6 +160,9 @@ def main():
         return
     if "--only-experiments" in sys.argv:
         experiments(ref)
+        return
+    if "--only-artifacts" in sys.argv:
+        artifacts(ref, tmp)
         return
 
     # RNG words and uniform draws (rng.hpp:14-19, rng.cpp:14-32)

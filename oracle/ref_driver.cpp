@@ -27,6 +27,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <optional>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -530,6 +531,18 @@ int cmd_adaptive(const Args& a) {
     return 0;
 }
 
+// The reference's artifact files of a sampling experiment (run_experiment,
+// src/experiments.cpp:365-409, 523-545): the config file is parsed by the
+// reference's own parse_config_file, the CSVs land in its out_dir.
+//   artifacts --config FILE
+int cmd_artifacts(const Args& a) {
+    const ExperimentConfig cfg = parse_config_file(a.get("config"), std::nullopt);
+    std::ostringstream log;
+    const int rc = run_experiment(cfg, log);
+    std::fprintf(stderr, "%s", log.str().c_str());
+    return rc;
+}
+
 // The reference's own sampling experiments through its public make_problem
 // (src/experiments.cpp:194-237): per-sample QoI vectors of coupled pairs
 // (sample_delta_q) and, with --eps, run_mlmc at the reference's config.
@@ -649,7 +662,7 @@ int cmd_level(const Args& a) {
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::fprintf(stderr, "usage: wavemc_ref_driver solve|mlmc|adaptive|experiment|rng|consts|meshcheck|level --key value...\n");
+        std::fprintf(stderr, "usage: wavemc_ref_driver solve|mlmc|adaptive|experiment|artifacts|rng|consts|meshcheck|level --key value...\n");
         return 2;
     }
     try {
@@ -663,6 +676,7 @@ int main(int argc, char** argv) {
         if (cmd == "meshcheck") return cmd_meshcheck(a);
         if (cmd == "level") return cmd_level(a);
         if (cmd == "experiment") return cmd_experiment(a);
+        if (cmd == "artifacts") return cmd_artifacts(a);
         throw ConfigError("unknown command " + cmd);
     } catch (const InstabilityError& e) {
         std::fprintf(stderr, "instability at step %ld: %s\n", e.step, e.what());

@@ -101,6 +101,8 @@ struct Workspace {
     int* eig_i = nullptr;      // settled | iters | done (S each) | active count
     int* h_active = nullptr;   // pinned
     int* h_nsteps = nullptr;   // pinned, S
+    int* it_full = nullptr;    // per sample: power iterations of the full / coarse CFL estimate (cost records)
+    int* it_coarse = nullptr;
 };
 
 constexpr int kEigBlocks = 64;  // row blocks of the power-iteration dot products
@@ -199,6 +201,8 @@ struct wmc_level {
     double* r_dq = nullptr;
     double* r_qf = nullptr;
     int* r_ff = nullptr;
+    int* r_cnt = nullptr;  // per-sample CFL cost counters [6][r_cap]: n_steps, it_full, it_coarse (fine, coarse)
+    int* h_cnt = nullptr;
     int* r_fc = nullptr;
     double* h_dq = nullptr;
     double* h_qf = nullptr;
@@ -235,16 +239,17 @@ struct wmc_level {
         for (auto& w : ws) {
             for (void* p : {(void*)w.za, (void*)w.zb, (void*)w.g, (void*)w.q, (void*)w.fail, (void*)w.da, (void*)w.db})
                 if (p) cudaFree(p);
-            for (void* p : {(void*)w.rel, (void*)w.nsteps, (void*)w.eig, (void*)w.eig_i})
+            for (void* p : {(void*)w.rel, (void*)w.nsteps, (void*)w.eig, (void*)w.eig_i, (void*)w.it_full,
+                            (void*)w.it_coarse})
                 if (p) cudaFree(p);
             if (w.h_active) cudaFreeHost(w.h_active);
             if (w.h_nsteps) cudaFreeHost(w.h_nsteps);
             for (auto* p : w.tier_e) cudaFree(p);
             for (auto* p : w.tier_rhs) cudaFree(p);
         }
-        for (void* p : {(void*)r_dq, (void*)r_qf, (void*)r_ff, (void*)r_fc})
+        for (void* p : {(void*)r_dq, (void*)r_qf, (void*)r_ff, (void*)r_fc, (void*)r_cnt})
             if (p) cudaFree(p);
-        for (void* p : {(void*)h_dq, (void*)h_qf, (void*)h_ff, (void*)h_fc})
+        for (void* p : {(void*)h_dq, (void*)h_qf, (void*)h_ff, (void*)h_fc, (void*)h_cnt})
             if (p) cudaFreeHost(p);
         for (auto& kv : graphs)
             if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -746,6 +751,8 @@ Workspace& workspace(wmc_level& L, int role) {
             alloc(&w.nsteps, S);
             alloc(&w.eig, S * (2 * kEigBlocks + 5));
             alloc(&w.eig_i, S * 3 + 1);
+            alloc(&w.it_full, S);
+            alloc(&w.it_coarse, S);
             check(cudaMallocHost(&w.h_active, sizeof(int)), "cudaMallocHost");
             check(cudaMallocHost(&w.h_nsteps, sizeof(int) * S), "cudaMallocHost");
         }
@@ -917,8 +924,14 @@ long cfl_phase(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
         check(cudaMemcpyAsync(out, lam, sizeof(double) * SS, cudaMemcpyDeviceToDevice, stream), "copy");
     };
     power(false, lf);
+    check(cudaMemcpyAsync(ws.it_full, iters, sizeof(int) * SS, cudaMemcpyDeviceToDevice, stream), "copy");
     const bool use_coarse = t.kind == wmc::Integrator::LocalTimeStepping && t.n_p > 0 && L.d_warm_coarse;
-    if (use_coarse) power(true, lc);
+    if (use_coarse) {
+        power(true, lc);
+        check(cudaMemcpyAsync(ws.it_coarse, iters, sizeof(int) * SS, cudaMemcpyDeviceToDevice, stream), "copy");
+    } else {
+        check(cudaMemsetAsync(ws.it_coarse, 0, sizeof(int) * SS, stream), "memset");
+    }
     wmc::launch_cfl_finalize(lf, lc, use_coarse ? 1 : 0, t.p_fine, t.cfl_safety, L.spec.final_time, t.dt, count, S,
                              ws.rel, ws.nsteps, stream);
     ++g_launches;
@@ -1327,10 +1340,19 @@ void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
         throw ConfigError("eval_pairs: coefficient fields of the pair differ");
 }
 
-void solve_counts(const wmc::LevelTables& t, wmc_cost& c, long solves) {
+// Cost record of `solves` solves of one level, as the reference accumulates
+// it per solve (accumulate_cost + stable_dt's power iterations,
+// src/experiments.cpp:22-43): StepCounters of run_wave -- LF: n_steps full
+// products; LF-LTS: one full (start-up) and per later step one coarse and p
+// fine products (src/integrators.cpp:117-157) -- weighted by the reference's
+// nnz of A, A P and A (I - P), plus the power iterations weighted by the nnz
+// of the operator they apply.
+void solve_counts(const wmc::LevelTables& t, wmc_cost& c, long solves, long n_steps, long it_full = 0,
+                  long it_coarse = 0) {
     const bool lts = t.kind == wmc::Integrator::LocalTimeStepping;
+    const long nnz = t.ref_nnz, nnz_f = t.ref_nnz_fine, nnz_c = t.ref_nnz - t.ref_nnz_fine;
     if (lts && t.tiers > 1) {
-        // nested tiers: p^k stage products A P_k per step on tier k
+        // nested tiers (no reference counterpart): p^k stage products A P_k per step on tier k
         long fine = 0, work = 0, pk = 1;
         for (int k = 0; k < t.tiers; ++k) {
             pk *= t.p;
@@ -1338,22 +1360,31 @@ void solve_counts(const wmc::LevelTables& t, wmc_cost& c, long solves) {
             work += pk * static_cast<long>(t.tier_ent[k].size());
         }
         c.matvec_full += solves;
-        c.matvec_coarse += solves * (t.n_steps - 1);
-        c.matvec_fine += solves * (t.n_steps - 1) * fine;
-        c.weighted_work += solves * (static_cast<long>(t.col.size()) +
-                                     (t.n_steps - 1) * (static_cast<long>(t.col.size()) + work));
+        c.matvec_coarse += solves * (n_steps - 1);
+        c.matvec_fine += solves * (n_steps - 1) * fine;
+        c.weighted_work += solves * (nnz + (n_steps - 1) * (nnz_c + work));
     } else if (lts) {
         c.matvec_full += solves;
-        c.matvec_coarse += solves * (t.n_steps - 1);
-        c.matvec_fine += solves * (t.n_steps - 1) * t.p;
-        c.weighted_work += solves * (static_cast<long>(t.col.size()) +
-                                     (t.n_steps - 1) * (static_cast<long>(t.col.size()) +
-                                                        t.p * static_cast<long>(t.ap_col.size())));
+        c.matvec_coarse += solves * (n_steps - 1);
+        c.matvec_fine += solves * (n_steps - 1) * t.p;
+        c.weighted_work += solves * (nnz + (n_steps - 1) * (nnz_c + t.p * nnz_f));
     } else {
-        c.matvec_full += solves * t.n_steps;
-        c.weighted_work += solves * t.n_steps * static_cast<long>(t.col.size());
+        c.matvec_full += solves * n_steps;
+        c.weighted_work += solves * n_steps * nnz;
     }
+    c.weighted_work += solves * (it_full * nnz + it_coarse * nnz_c);
     c.dof_updates += static_cast<double>(solves) * wmc::dof_updates_per_solve(t);
+}
+
+void solve_counts(const wmc::LevelTables& t, wmc_cost& c, long solves) { solve_counts(t, c, solves, t.n_steps); }
+
+// Cost of pair i of a per-sample CFL level from the counters issue_pairs
+// copied back (fine: fields 0-2, coarse: 3-5 of the fine level's h_cnt).
+void pair_cost_sample(const wmc_level* fine, const wmc_level* coarse, std::size_t i, wmc_cost& c) {
+    const int* h = fine->h_cnt;
+    const std::size_t cap = fine->r_cap;
+    solve_counts(fine->tab, c, 1, h[i], h[cap + i], h[2 * cap + i]);
+    if (coarse) solve_counts(coarse->tab, c, 1, h[3 * cap + i], h[4 * cap + i], h[5 * cap + i]);
 }
 
 // evaluates pairs; host_dq/host_qf may be NULL (device-resident mode: the
@@ -1362,9 +1393,9 @@ void ensure_results(wmc_level& L, std::size_t count) {
     if (count <= L.r_cap) return;
     check(cudaSetDevice(L.device), "cudaSetDevice");
     check(cudaStreamSynchronize(L.stream), "synchronize");
-    for (void* p : {(void*)L.r_dq, (void*)L.r_qf, (void*)L.r_ff, (void*)L.r_fc})
+    for (void* p : {(void*)L.r_dq, (void*)L.r_qf, (void*)L.r_ff, (void*)L.r_fc, (void*)L.r_cnt})
         if (p) cudaFree(p);
-    for (void* p : {(void*)L.h_dq, (void*)L.h_qf, (void*)L.h_ff, (void*)L.h_fc})
+    for (void* p : {(void*)L.h_dq, (void*)L.h_qf, (void*)L.h_ff, (void*)L.h_fc, (void*)L.h_cnt})
         if (p) cudaFreeHost(p);
     const std::size_t cap = std::max<std::size_t>(count, 256);
     const std::size_t nq = static_cast<std::size_t>(L.tab.nq);
@@ -1376,6 +1407,8 @@ void ensure_results(wmc_level& L, std::size_t count) {
     check(cudaMallocHost(&L.h_qf, sizeof(double) * cap * nq), "cudaMallocHost");
     check(cudaMallocHost(&L.h_ff, sizeof(int) * cap), "cudaMallocHost");
     check(cudaMallocHost(&L.h_fc, sizeof(int) * cap), "cudaMallocHost");
+    check(cudaMalloc(&L.r_cnt, sizeof(int) * 6 * cap), "cudaMalloc results");
+    check(cudaMallocHost(&L.h_cnt, sizeof(int) * 6 * cap), "cudaMallocHost");
     L.r_cap = cap;
 }
 
@@ -1419,6 +1452,15 @@ void issue_pairs(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::ui
         double* dq_dst = (to_host ? fine->r_dq : dev_dq) + off * nq;
         double* qf_dst = to_host ? fine->r_qf + off * nq : (dev_qf ? dev_qf + off * nq : nullptr);
         wmc::launch_pair_diff(wf.q, wc ? wc->q : nullptr, dq_dst, qf_dst, c, S, nq, st);
+        if (to_host && fine->tab.cfl_safety > 0.0) {
+            const std::size_t cap_r = fine->r_cap;
+            const int* src[6] = {wf.nsteps, wf.it_full, wf.it_coarse, wc ? wc->nsteps : nullptr,
+                                 wc ? wc->it_full : nullptr, wc ? wc->it_coarse : nullptr};
+            for (int f = 0; f < 6; ++f)
+                if (src[f])
+                    check(cudaMemcpyAsync(fine->r_cnt + f * cap_r + off, src[f], sizeof(int) * c,
+                                          cudaMemcpyDeviceToDevice, st), "counters");
+        }
         if (to_host) {
             check(cudaMemcpyAsync(fine->r_ff + off, wf.fail, sizeof(int) * c, cudaMemcpyDeviceToDevice, st), "fail");
             if (wc)
@@ -1431,6 +1473,10 @@ void issue_pairs(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::ui
         check(cudaMemcpyAsync(fine->h_dq, fine->r_dq, sizeof(double) * count * nq, cudaMemcpyDeviceToHost, st), "dq");
         check(cudaMemcpyAsync(fine->h_qf, fine->r_qf, sizeof(double) * count * nq, cudaMemcpyDeviceToHost, st), "q");
         check(cudaMemcpyAsync(fine->h_ff, fine->r_ff, sizeof(int) * count, cudaMemcpyDeviceToHost, st), "fail");
+        if (fine->tab.cfl_safety > 0.0)
+            for (int f = 0; f < (coarse ? 6 : 3); ++f)
+                check(cudaMemcpyAsync(fine->h_cnt + f * fine->r_cap, fine->r_cnt + f * fine->r_cap,
+                                      sizeof(int) * count, cudaMemcpyDeviceToHost, st), "counters");
         if (coarse)
             check(cudaMemcpyAsync(fine->h_fc, fine->r_fc, sizeof(int) * count, cudaMemcpyDeviceToHost, st), "fail");
     }
@@ -1468,6 +1514,18 @@ void pair_cost(const wmc_level* fine, const wmc_level* coarse, std::uint64_t cou
     if (coarse) solve_counts(coarse->tab, *cost, static_cast<long>(count));
 }
 
+// Cost of pairs [from, from + count) of the fine level's host results: per
+// sample (its own step count and power iterations) on per-sample CFL levels,
+// else the fixed-horizon counts.
+void results_cost(const wmc_level* fine, const wmc_level* coarse, std::size_t from, std::size_t count, wmc_cost* cost) {
+    if (fine->tab.cfl_safety <= 0.0 || !fine->h_cnt) {
+        pair_cost(fine, coarse, count, cost);
+        return;
+    }
+    std::memset(cost, 0, sizeof(*cost));
+    for (std::size_t i = from; i < from + count; ++i) pair_cost_sample(fine, coarse, i, *cost);
+}
+
 // evaluates pairs; host_dq/host_qf may be NULL (device-resident mode: the
 // results for index first+i are written to dev_dq/dev_qf + i when given)
 void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::uint32_t level, std::uint64_t first,
@@ -1481,6 +1539,8 @@ void eval_pairs_impl(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std
         const std::size_t nq = static_cast<std::size_t>(fine->tab.nq);
         if (host_dq) std::memcpy(host_dq, fine->h_dq, sizeof(double) * count * nq);
         if (host_qf) std::memcpy(host_qf, fine->h_qf, sizeof(double) * count * nq);
+        if (cost) results_cost(fine, coarse, 0, count, cost);
+        return;
     }
     if (cost) pair_cost(fine, coarse, count, cost);
 }
@@ -1577,7 +1637,7 @@ void run_levels(wmc_level** levels, const std::vector<LevelJob>& jobs, std::uint
         const int nq = fine->tab.nq;
         for (long i = 0; i < j.count; ++i) a.add(fine->h_dq + i * nq, fine->h_qf + i * nq);
         wmc_cost c{};
-        pair_cost(fine, j.level > 0 ? levels[j.level - 1] : nullptr, static_cast<std::uint64_t>(j.count), &c);
+        results_cost(fine, j.level > 0 ? levels[j.level - 1] : nullptr, 0, static_cast<std::size_t>(j.count), &c);
         a.cost.matvec_full += c.matvec_full;
         a.cost.matvec_fine += c.matvec_fine;
         a.cost.matvec_coarse += c.matvec_coarse;
@@ -1595,6 +1655,7 @@ void run_levels(wmc_level** levels, const std::vector<LevelJob>& jobs, std::uint
 struct PairCache {
     std::vector<double> dq, qf;
     std::vector<int> ff, fc;  // fail steps (INT_MAX: fine)
+    std::vector<wmc_cost> cost;  // per pair (reference CostRecord of sample_delta_q)
     long computed = 0;
 };
 
@@ -1634,6 +1695,11 @@ void cached_wave(wmc_level** levels, int n_levels, const std::vector<long>& targ
             c.fc.insert(c.fc.end(), fine->h_fc, fine->h_fc + j.count);
         else
             c.fc.insert(c.fc.end(), j.count, INT_MAX);
+        for (long i = 0; i < j.count; ++i) {
+            wmc_cost pc{};
+            results_cost(fine, j.level > 0 ? levels[j.level - 1] : nullptr, static_cast<std::size_t>(i), 1, &pc);
+            c.cost.push_back(pc);
+        }
         c.computed += j.count;
     }
     if (err) err->sample = -1;
@@ -1659,7 +1725,14 @@ void cached_wave(wmc_level** levels, int n_levels, const std::vector<long>& targ
         }
         if (targets[l] > from) {
             wmc_cost cc{};
-            pair_cost(levels[l], l > 0 ? levels[l - 1] : nullptr, static_cast<std::uint64_t>(targets[l] - from), &cc);
+            for (long i = from; i < targets[l]; ++i) {
+                const wmc_cost& pc = c.cost[i];
+                cc.matvec_full += pc.matvec_full;
+                cc.matvec_fine += pc.matvec_fine;
+                cc.matvec_coarse += pc.matvec_coarse;
+                cc.weighted_work += pc.weighted_work;
+                cc.dof_updates += pc.dof_updates;
+            }
             a.cost.matvec_full += cc.matvec_full;
             a.cost.matvec_fine += cc.matvec_fine;
             a.cost.matvec_coarse += cc.matvec_coarse;

@@ -358,6 +358,26 @@ static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables
             if (!g.boundary[v] && in_r[v] && (tiers == 1 || rt[v] >= k)) ++L.n_r_tier[k - 1];
     L.n = static_cast<int>(L.dof_vertex.size());
     if (L.n == 0) throw std::invalid_argument("level: mesh has no interior vertices");
+    // the reference's stored entries: from_triplets keeps every (row, col)
+    // pair an element couples, zero sums included (include/wavemc/sparse.hpp:17-40),
+    // restricted to interior rows and columns; a_fine keeps the P columns
+    {
+        long full = 0, fine = 0;
+        int pi = -1, pj = -1;
+        for (const auto& [key, s] : stiff) {  // ordered by (vi, vj, cell)
+            const auto [vi, vj, k] = key;
+            (void)s;
+            (void)k;
+            if (vi == pi && vj == pj) continue;
+            pi = vi;
+            pj = vj;
+            if (g.boundary[vi] || g.boundary[vj]) continue;
+            ++full;
+            if (sel[vj]) ++fine;
+        }
+        L.ref_nnz = full;
+        L.ref_nnz_fine = fine;
+    }
     L.in_p.assign(L.n, 0);
     L.dof_tier.assign(L.n, 0);
     L.mass.resize(L.n);

@@ -90,6 +90,9 @@ struct LevelTables {
     std::vector<int> col;
     std::vector<int> cell;
     std::vector<double> a0;
+    // the reference's nnz of A (normalized) and of A P (a_fine): explicit
+    // zeros kept, as its CSR stores them (cost records' weighted_work)
+    long ref_nnz = 0, ref_nnz_fine = 0;
 
     // A P restricted to R rows, as recipes: entry (row r, col j in P, wid);
     // recipe wid = sum_t c[rc_cell[t]] * rc_a0[t] for t in [rc_ptr[wid], rc_ptr[wid+1])
