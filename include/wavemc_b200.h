@@ -153,6 +153,7 @@ int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level
  * points of [0, 6] (restrict_to_grid), norm with trapezoid weights. */
 #define WMC_EXP_SMOOTH1D 1
 #define WMC_EXP_JUMP1D 2
+#define WMC_EXP_CHANNEL2D 3
 typedef struct {
     int experiment;
     int integrator;
@@ -164,6 +165,20 @@ typedef struct {
 /* the reference's default_config (src/config_io.cpp:49-73) for the experiment */
 void wmc_experiment_desc_default(wmc_experiment_desc* desc, int experiment);
 int wmc_level_create_experiment(const wmc_experiment_desc* desc, int level, wmc_level** out);
+/* The reference's narrow-channel experiment (make_problem Channel2d,
+ * src/experiments.cpp:108-172): level `level` on `mesh`, the reference's
+ * build_channel_mesh(max(h0 / 2^level, fine_h), fine_h) (src/mesh2d.cpp:
+ * 319-359; the adapter passes its TriMesh through wmc_mesh_create).  Per
+ * sample the width b = next_uniform(0.001, 0.007) (sample_width,
+ * src/rng.cpp:59-64) moves the mesh by ChannelGeometry::map; Neumann (every
+ * vertex a DOF), speed 1, bump u0 at (1/2, 0), per-sample CFL step with warm
+ * starts from the reference mesh, p = ceil(h0 2^-level / fine_h) (LF-LTS) or
+ * 1 (LF), QoI = u(T) on grid_n points of the line x = -0.4, y in [-1/2, 1/2]
+ * (extract_line_qoi), trapezoid norm.  desc->experiment = WMC_EXP_CHANNEL2D;
+ * wmc_experiment_desc_default gives the reference's default_config. */
+int wmc_level_create_channel(const wmc_mesh* mesh, const wmc_experiment_desc* desc, int level, wmc_level** out);
+/* Host-only plan of a channel level (sizes, no device work). */
+int wmc_channel_plan(const wmc_mesh* mesh, const wmc_experiment_desc* desc, int level, wmc_level_info* info);
 /* Host-only plan of an experiment level (sizes, no device work). */
 int wmc_experiment_plan(const wmc_experiment_desc* desc, int level, wmc_level_info* info);
 /* The experiment's model cost per level, the reference's closed-form cost

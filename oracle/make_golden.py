@@ -1,6 +1,6 @@
 """Generate tests/golden/*.json from the UNMODIFIED reference library
 (oracle/_ref/wavemc_ref_driver) -- run in the build container, where
-/root/reference exists:  python oracle/make_golden.py [--only-config2 | --only-cfl | --only-experiments | --only-artifacts]
+/root/reference exists:  python oracle/make_golden.py [--only-config2 | --only-cfl | --only-experiments | --only-artifacts | --only-channel]
 
 The meshes come from the shared problem definition (the product's host mesh
 builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
@@ -148,6 +148,42 @@ def artifacts(ref, tmp):
             shutil.copy(os.path.join(out, fn), os.path.join(dst, fn))
 
 
+CHANNEL = {"h0": 0.05, "fine_h": 0.002, "max_level": 2, "grid_n": 64}  # a small narrow-channel hierarchy
+
+
+def channel(ref, tmp):
+    """The reference's narrow-channel experiment (make_problem Channel2d,
+    src/experiments.cpp:108-172) on a small hierarchy: the reference meshes of
+    levels 0..2 (build_channel_mesh, gzip fixtures: the adapter's input),
+    per-sample QoI vectors and cost records of coupled pairs for LF-LTS and
+    LF, and run_mlmc at one tolerance."""
+    import gzip
+    import shutil
+    c = CHANNEL
+    dst = os.path.join(GOLDEN, "channel")
+    os.makedirs(dst, exist_ok=True)
+    for l in range(c["max_level"] + 1):
+        path = os.path.join(tmp, f"channel_l{l}.mesh")
+        ref.run("channel-mesh", "--h0", repr(c["h0"]), "--fine-h", repr(c["fine_h"]), "--level", l, "--out", path)
+        with open(path, "rb") as f, open(os.path.join(dst, f"mesh_l{l}.txt.gz"), "wb") as raw, \
+                gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as g:  # reproducible bytes
+            shutil.copyfileobj(f, g)
+    out = {"config": c}
+    opts = {"h0": repr(c["h0"]), "fine-h": repr(c["fine_h"]), "max-level": c["max_level"], "grid-n": c["grid_n"]}
+    for kind in ("lts", "lf"):
+        case = {"levels": []}
+        for level, first, count in ((0, 0, 6), (1, 3, 4), (2, 7, 3)):
+            r = ref.experiment("channel2d", kind, level=level, first=first, count=count, **opts)
+            case["model_cost"] = r["model_cost"]
+            case["levels"].append({"level": level, "first": first, "samples": r["samples"]})
+        a = ref.experiment("channel2d", kind, eps=2e-4, **opts)
+        case["adaptive"] = {"eps": a["eps"], "converged": a["converged"], "total_variance": a["total_variance"],
+                            "bias": a["bias"], "estimate_norm": a["estimate_norm"], "estimate": a["estimate"],
+                            "levels": a["levels"], "seconds": a["seconds"]}
+        out[kind] = case
+    dump(os.path.join("channel", "channel.json"), out)
+
+
 def main():
     build()
     ref = RefDriver()
@@ -163,6 +199,9 @@ def main():
         return
     if "--only-artifacts" in sys.argv:
         artifacts(ref, tmp)
+        return
+    if "--only-channel" in sys.argv:
+        channel(ref, tmp)
         return
 
     # RNG words and uniform draws (rng.hpp:14-19, rng.cpp:14-32)

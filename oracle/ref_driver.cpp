@@ -543,6 +543,21 @@ int cmd_artifacts(const Args& a) {
     return rc;
 }
 
+// The reference's narrow-channel mesh of one level (build_state_2d,
+// src/experiments.cpp:137-139: build_channel_mesh(max(h0 2^-l, fine_h), fine_h))
+// in its fixture format (dump_mesh, src/mesh_io.cpp:47-55).
+//   channel-mesh --h0 H --fine-h F --level L --out PATH
+int cmd_channel_mesh(const Args& a) {
+    const double h0 = a.num("h0", 1.0 / 60.0), fine_h = a.num("fine-h", 7.6e-4);
+    const int level = static_cast<int>(a.integer("level", 0));
+    const double coarse = h0 / std::pow(2.0, level);
+    const TriMesh m = build_channel_mesh(std::max(coarse, fine_h), fine_h);
+    std::ofstream out(a.get("out"));
+    if (!out) throw ConfigError("channel-mesh: cannot open --out");
+    dump_mesh(m, out);
+    return 0;
+}
+
 // The reference's own sampling experiments through its public make_problem
 // (src/experiments.cpp:194-237): per-sample QoI vectors of coupled pairs
 // (sample_delta_q) and, with --eps, run_mlmc at the reference's config.
@@ -554,6 +569,9 @@ int cmd_experiment(const Args& a) {
     ExperimentConfig cfg = default_config(*kind);
     cfg.max_level = static_cast<int>(a.integer("max-level", cfg.max_level));
     cfg.grid_n = static_cast<int>(a.integer("grid-n", cfg.grid_n));
+    if (!a.get("h0").empty()) cfg.h0 = a.num("h0", cfg.h0);
+    if (!a.get("fine-h").empty()) cfg.fine_h = a.num("fine-h", cfg.fine_h);
+    if (!a.get("final-time").empty()) cfg.final_time = a.num("final-time", cfg.final_time);
     cfg.workers = default_threads(a);
     const Integrator integ = a.get("kind", "lts") == "lf" ? Integrator::Leapfrog : Integrator::LocalTimeStepping;
     const MlmcProblem problem = make_problem(cfg, integ);
@@ -602,7 +620,9 @@ int cmd_experiment(const Args& a) {
             std::printf("], \"q\": [");
             for (std::size_t k = 0; k < res[i].q_fine.values.size(); ++k)
                 std::printf("%s%.17g", k ? ", " : "", res[i].q_fine.values[k]);
-            std::printf("]}");
+            const CostRecord& c = res[i].cost;
+            std::printf("], \"cost\": [%ld, %ld, %ld, %ld]}", c.matvec_full, c.matvec_fine, c.matvec_coarse,
+                        c.weighted_work);
         }
         std::printf("]");
     }
@@ -662,7 +682,7 @@ int cmd_level(const Args& a) {
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::fprintf(stderr, "usage: wavemc_ref_driver solve|mlmc|adaptive|experiment|artifacts|rng|consts|meshcheck|level --key value...\n");
+        std::fprintf(stderr, "usage: wavemc_ref_driver solve|mlmc|adaptive|experiment|artifacts|channel-mesh|rng|consts|meshcheck|level --key value...\n");
         return 2;
     }
     try {
@@ -677,6 +697,7 @@ int main(int argc, char** argv) {
         if (cmd == "level") return cmd_level(a);
         if (cmd == "experiment") return cmd_experiment(a);
         if (cmd == "artifacts") return cmd_artifacts(a);
+        if (cmd == "channel-mesh") return cmd_channel_mesh(a);
         throw ConfigError("unknown command " + cmd);
     } catch (const InstabilityError& e) {
         std::fprintf(stderr, "instability at step %ld: %s\n", e.step, e.what());

@@ -39,6 +39,7 @@ class LevelDesc(C.Structure):
 
 WMC_EXP_SMOOTH1D = 1
 WMC_EXP_JUMP1D = 2
+WMC_EXP_CHANNEL2D = 3
 
 
 class ExperimentDesc(C.Structure):
@@ -105,6 +106,8 @@ SIGNATURES = [
     ("wmc_experiment_desc_default", None, [P(ExperimentDesc), C.c_int]),
     ("wmc_level_create_experiment", C.c_int, [P(ExperimentDesc), C.c_int, P(_VP)]),
     ("wmc_experiment_plan", C.c_int, [P(ExperimentDesc), C.c_int, P(LevelInfo)]),
+    ("wmc_level_create_channel", C.c_int, [_VP, P(ExperimentDesc), C.c_int, P(_VP)]),
+    ("wmc_channel_plan", C.c_int, [_VP, P(ExperimentDesc), C.c_int, P(LevelInfo)]),
     ("wmc_experiment_model_cost", C.c_double, [P(ExperimentDesc), C.c_int]),
     ("wmc_level_plan", C.c_int, [_VP, P(LevelDesc), P(LevelInfo)]),
     ("wmc_level_get_info", C.c_int, [_VP, P(LevelInfo)]),

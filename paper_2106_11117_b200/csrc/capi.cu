@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/wavemc_b200.h"
+#include "host/channel.hpp"
 #include "host/field.hpp"
 #include "host/level.hpp"
 #include "host/mesh.hpp"
@@ -138,6 +139,7 @@ struct wmc_level {
     double* d_beta = nullptr;
     double* d_cm = nullptr;
     int sub_smem = 0;
+    int sub_cl_smem = 1;  // generic substep kernel stages the cell coefficients in shared memory
     int sub_grid = 0;
     int small_smem = 0;  // fused small-mesh solve: shared memory per CTA (0: not eligible)
     int fused_smem = 0;  // fused lattice solve: shared memory per CTA (0: not eligible)
@@ -181,6 +183,10 @@ struct wmc_level {
     int* d_grc_cell = nullptr;
     double* d_grc_a0 = nullptr;
     int n_slots = 0;
+    // narrow-channel experiment: per-sample entry tables
+    wmc::ChannelTables ch;
+    wmc::ChannelArgs ch_args{};
+    std::vector<void*> ch_bufs;
     int* d_rem_ptr = nullptr;  // fused solve: A (I - P) entries of the generic rows
     int* d_rem_col = nullptr;
     int* d_rem_cell = nullptr;
@@ -230,6 +236,7 @@ struct wmc_level {
                         (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0,
                         (void*)d_rem_ptr, (void*)d_rem_col, (void*)d_rem_cell, (void*)d_rem_a0})
             if (p) cudaFree(p);
+        for (void* p : ch_bufs) cudaFree(p);
         for (auto* p : d_tier_ptr) cudaFree(p);
         for (auto* p : d_tier_ent) cudaFree(p);
         for (auto* p : d_tier_a0) cudaFree(p);
@@ -361,14 +368,41 @@ void build_device_level(wmc_level& L) {
         L.col_bits = wmc::kColBits;
         if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
     } else {
+        // as many column bits as the DOFs need (at least 16), the rest for cells
         L.col_bits = 16;
-        if (t.n >= 65536 || t.n_cells >= 65536)
-            throw ConfigError("level: more than 511 coefficient cells needs fewer than 65536 DOFs and cells");
+        while ((1L << L.col_bits) < t.n) ++L.col_bits;
+        if (L.col_bits > 31 || static_cast<long>(t.n_cells) > (1L << (32 - L.col_bits)))
+            throw ConfigError("level: " + std::to_string(t.n) + " DOFs and " + std::to_string(t.n_cells) +
+                              " coefficient cells do not fit a 32-bit entry");
     }
     std::vector<int> ent(t.col.size());
     for (std::size_t k = 0; k < ent.size(); ++k)
         ent[k] = static_cast<int>(static_cast<unsigned>(t.col[k]) | (static_cast<unsigned>(t.cell[k]) << L.col_bits));
     L.d_row_ptr = upload(t.row_ptr);
+    if (L.spec.field == wmc::Field::Channel) {
+        const wmc::ChannelTables& c = L.ch;
+        auto up = [&](const auto& v) {
+            auto* p = upload(v);
+            L.ch_bufs.push_back(static_cast<void*>(p));
+            return p;
+        };
+        wmc::ChannelArgs& a = L.ch_args;
+        a.n_ent = static_cast<int>(c.e_li.size());
+        a.vx = up(c.vx);
+        a.vy = up(c.vy);
+        a.vblend = up(c.vblend);
+        a.tri = up(c.tri);
+        a.ms = up(c.ms);
+        a.m_ptr = up(c.m_ptr);
+        a.m_tri = up(c.m_tri);
+        a.e_li = up(c.e_li);
+        a.e_lj = up(c.e_lj);
+        a.e_mi = up(c.e_mi);
+        a.e_mj = up(c.e_mj);
+        a.e_ks = up(c.e_ks);
+        a.k_ptr = up(c.k_ptr);
+        a.k_tri = up(c.k_tri);
+    }
     {
         // sweep row descriptors: single-cell rows, and among them the
         // structured 5-point rows {i - dS, i - 1, i, i + 1, i + dN} whose
@@ -478,8 +512,15 @@ void build_device_level(wmc_level& L) {
         probe.n_wid = L.n_wid;
         probe.n_cells = t.n_cells;
         probe.n_ent = L.n_sub_ent;
+        probe.cl_smem = 1;
         L.sub_smem = wmc::substep_smem_bytes(probe);
         L.sub_grid = wmc::substep_max_grid(L.device, L.sub_smem);
+        if (L.sub_grid <= 0) {  // many cells (channel): recipes read the coefficients from global memory
+            probe.cl_smem = 0;
+            L.sub_smem = wmc::substep_smem_bytes(probe);
+            L.sub_grid = wmc::substep_max_grid(L.device, L.sub_smem);
+            L.sub_cl_smem = 0;
+        }
     }
     if (!t.field_x.empty()) L.d_field_x = upload(t.field_x);
     if (!t.field_table.empty()) L.d_field_table = upload(t.field_table);
@@ -1028,6 +1069,7 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
         sb.p = t.p;
         sb.n_wid = L.n_wid;
         sb.n_cells = t.n_cells;
+        sb.cl_smem = L.sub_cl_smem;
         sb.n_ent = L.n_sub_ent;
         sb.ent = L.d_sub_ent;
         sb.slice_off = L.d_slice_off;
@@ -1308,6 +1350,8 @@ void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, st
     else if (L.spec.field == wmc::Field::Kl1D)
         wmc::launch_draw_kl1d(seed, level, first, count, S, L.tab.n_cells, L.tab.field_terms, L.d_field_table, cells,
                               st);
+    else if (L.spec.field == wmc::Field::Channel)
+        wmc::launch_draw_channel(seed, level, first, count, S, L.ch_args, cells, st);
     else if (L.spec.field == wmc::Field::Jump1D)
         wmc::launch_draw_jump1d(seed, level, first, count, S, L.tab.n_cells, L.spec.jump_h0, L.d_field_x, cells, st);
     else
@@ -1318,7 +1362,8 @@ void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, st
 // the 1D experiments' fields are evaluated per element: the coarse level of a
 // pair draws its own coefficients from the same stream (rng.cpp:42-89)
 bool per_element_field(const wmc_level& L) {
-    return L.spec.field == wmc::Field::Kl1D || L.spec.field == wmc::Field::Jump1D;
+    return L.spec.field == wmc::Field::Kl1D || L.spec.field == wmc::Field::Jump1D ||
+           L.spec.field == wmc::Field::Channel;
 }
 
 void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
@@ -1824,6 +1869,42 @@ void experiment_tables(const wmc_experiment_desc* desc, int level, wmc::LevelSpe
     t = wmc::build_level_tables_1d(mesh, s);
 }
 
+// One level of the reference's narrow-channel experiment on the reference
+// mesh of that level (make_problem Channel2d / build_state_2d,
+// src/experiments.cpp:132-148): p = ceil(h0 2^-l / fine_h) (LF-LTS) or 1,
+// per-sample CFL step, QoI on grid_n points of [-1/2, 1/2].
+void channel_level_tables(const wmc::TriMesh& mesh, const wmc_experiment_desc* desc, int level, wmc::LevelSpec& s,
+                          wmc::LevelTables& t, wmc::ChannelTables& ch) {
+    if (desc->experiment != WMC_EXP_CHANNEL2D) throw ConfigError("channel: experiment must be WMC_EXP_CHANNEL2D");
+    if (desc->integrator != WMC_LEAPFROG && desc->integrator != WMC_LOCAL_TIME_STEPPING)
+        throw ConfigError("channel: unknown integrator");
+    if (!(desc->safety > 0.0 && desc->safety <= 1.0)) throw ConfigError("channel: safety in (0, 1]");
+    if (desc->nu < 0.0 || desc->nu > 1.0) throw ConfigError("channel: nu in [0, 1]");
+    if (!(desc->h0 > 0.0) || !(desc->fine_h > 0.0)) throw ConfigError("channel: h0 and fine_h must be positive");
+    if (level < 0 || level > desc->max_level) throw ConfigError("channel: level out of range");
+    const double coarse = desc->h0 / std::pow(2.0, level);
+    s = wmc::LevelSpec{};
+    s.kind = desc->integrator == WMC_LEAPFROG ? wmc::Integrator::Leapfrog : wmc::Integrator::LocalTimeStepping;
+    s.substeps = s.kind == wmc::Integrator::Leapfrog
+                     ? 1
+                     : std::max(1, static_cast<int>(std::ceil(coarse / desc->fine_h - 1e-9)));
+    s.nu = desc->nu;
+    s.final_time = desc->final_time;
+    s.dt = coarse;  // nominal: every sample takes its own CFL step
+    s.cfl_safety = desc->safety;
+    s.field = wmc::Field::Channel;
+    s.grid_lo = -wmc::kChannelRectHalfHeight;
+    s.grid_hi = wmc::kChannelRectHalfHeight;
+    s.grid_n = desc->grid_n;
+    try {
+        t = wmc::build_level_tables_channel(mesh, s, ch);
+    } catch (const std::invalid_argument& e) {
+        throw ConfigError(e.what());
+    }
+    s.cells_x = t.n_cells;
+    s.cells_y = 1;
+}
+
 wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     if (desc->integrator != WMC_LEAPFROG && desc->integrator != WMC_LOCAL_TIME_STEPPING)
         throw ConfigError("wmc_level_create: unknown integrator");
@@ -2059,6 +2140,32 @@ int wmc_level_create_experiment(const wmc_experiment_desc* desc, int level, wmc_
     });
 }
 
+int wmc_level_create_channel(const wmc_mesh* mesh, const wmc_experiment_desc* desc, int level, wmc_level** out) {
+    return guarded([&] {
+        if (!mesh || !desc || !out) throw ConfigError("wmc_level_create_channel: NULL argument");
+        auto L = std::make_unique<wmc_level>();
+        L->device = desc->device;
+        channel_level_tables(mesh->mesh, desc, level, L->spec, L->tab, L->ch);
+        int ndev = 0;
+        check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (L->device < 0 || L->device >= ndev) throw ConfigError("wmc_level_create_channel: no such device");
+        set_batch(*L, desc->batch);
+        build_device_level(*L);
+        *out = L.release();
+    });
+}
+
+int wmc_channel_plan(const wmc_mesh* mesh, const wmc_experiment_desc* desc, int level, wmc_level_info* info) {
+    return guarded([&] {
+        if (!mesh || !desc || !info) throw ConfigError("wmc_channel_plan: NULL argument");
+        wmc::LevelSpec s;
+        wmc::LevelTables t;
+        wmc::ChannelTables ch;
+        channel_level_tables(mesh->mesh, desc, level, s, t, ch);
+        fill_info(t, 0, false, info);
+    });
+}
+
 int wmc_experiment_plan(const wmc_experiment_desc* desc, int level, wmc_level_info* info) {
     return guarded([&] {
         if (!desc || !info) throw ConfigError("wmc_experiment_plan: NULL argument");
@@ -2072,9 +2179,15 @@ int wmc_experiment_plan(const wmc_experiment_desc* desc, int level, wmc_level_in
 
 double wmc_experiment_model_cost(const wmc_experiment_desc* d, int level) {
     if (!d || level < 0) return 0.0;
-    // model_params (experiments.cpp:177-192), 1D: r = h0 / 6, p0 = max(1, ceil(h0 / fine_h - 1e-9))
-    const double r = d->h0 / 6.0, p0 = std::max(1.0, std::ceil(d->h0 / d->fine_h - 1e-9));
-    const int dim = 1;
+    // model_params (experiments.cpp:177-192): 1D r = h0 / 6; channel r = channel
+    // area / (two rectangles + channel), dim 2; p0 = max(1, ceil(h0 / fine_h - 1e-9))
+    const bool channel = d->experiment == WMC_EXP_CHANNEL2D;
+    const double channel_area = 2.0 * wmc::kChannelHalfLength * wmc::kChannelRefWidth;
+    const double r = channel ? channel_area / (2.0 * wmc::kChannelRectWidth * 2.0 * wmc::kChannelRectHalfHeight +
+                                               channel_area)
+                             : d->h0 / 6.0;
+    const double p0 = std::max(1.0, std::ceil(d->h0 / d->fine_h - 1e-9));
+    const int dim = channel ? 2 : 1;
     const double pre = d->final_time * std::pow(1.0, 2 * (dim + 1)) / std::pow(d->h0, dim + 1);  // degree 1
     if (d->integrator == WMC_LEAPFROG) {  // cost_lf_level (cost_model.cpp:40-48)
         if (level == 0) return pre * ((1.0 - r) * p0 + r * std::pow(p0, dim + 1));
@@ -2097,6 +2210,11 @@ void wmc_experiment_desc_default(wmc_experiment_desc* d, int experiment) {
     d->h0 = 1.0 / 16.0;
     d->fine_h = experiment == WMC_EXP_JUMP1D ? 1.0 / 512.0 : 1.0 / 256.0;
     d->final_time = experiment == WMC_EXP_JUMP1D ? 6.0 : 11.0;
+    if (experiment == WMC_EXP_CHANNEL2D) {  // src/config_io.cpp:67-73
+        d->h0 = 1.0 / 60.0;
+        d->fine_h = 7.6e-4;
+        d->final_time = 1.0;
+    }
     d->nu = 0.01;
     d->safety = 0.9;
     d->grid_n = 512;

@@ -1,10 +1,13 @@
 #include "level.hpp"
 
+#include "channel.hpp"
+
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
 #include <map>
 #include <stdexcept>
+#include <string>
 #include <tuple>
 
 namespace wmc {
@@ -79,6 +82,8 @@ struct Geometry {
     std::vector<std::vector<double>> qoi_vertex_w;
     std::vector<std::vector<std::pair<int, double>>> qoi_entries;  // else: per output (vertex, weight)
     std::vector<double> qoi_norm_w;
+    bool unit_cells = false;              // channel: cells >= 1 are whole per-sample entries (a0 = 1)
+    std::vector<double> cell_ref;         // channel: reference-geometry value of every cell (warm starts)
 };
 
 // Finds the structured block of the refined square and checks, numerically
@@ -394,7 +399,7 @@ static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables
         const auto [vi, vj, k] = key;
         if (s == 0.0) continue;
         const int i = vdof[vi], j = vdof[vj];
-        rows[i].emplace_back(j, k, s / std::sqrt(mass[vi] * mass[vj]));
+        rows[i].emplace_back(j, k, (g.unit_cells && k > 0) ? 1.0 : s / std::sqrt(mass[vi] * mass[vj]));
     }
     // sweep tables: each row's entries in column order (cell-split entries
     // of one column adjacent)
@@ -412,9 +417,14 @@ static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables
 
     // A P on R rows, parts form (HBM-resident and fused small-mesh paths);
     // col | cell << 23, or << 16 when there are more than 511 cells
-    L.apg_col_bits = L.n_cells <= 511 ? 23 : 16;
-    if (L.apg_col_bits == 16 && (L.n >= 65536 || L.n_cells >= 65536))
-        throw std::invalid_argument("level: more than 511 cells needs fewer than 65536 DOFs and cells");
+    L.apg_col_bits = 23;
+    if (L.n_cells > 511) {  // as many column bits as the DOFs need (at least 16), the rest for cells
+        L.apg_col_bits = 16;
+        while ((1L << L.apg_col_bits) < L.n) ++L.apg_col_bits;
+        if (L.apg_col_bits > 31 || static_cast<long>(L.n_cells) > (1L << (32 - L.apg_col_bits)))
+            throw std::invalid_argument("level: " + std::to_string(L.n) + " DOFs and " +
+                                        std::to_string(L.n_cells) + " coefficient cells do not fit a 32-bit entry");
+    }
     L.apg_ptr.assign(L.n_r + 1, 0);
     for (int i = 0; i < L.n_r; ++i) {
         for (const auto& [j, k, a] : rows[i]) {
@@ -597,7 +607,8 @@ static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables
             for (int e = L.row_ptr[i]; e < L.row_ptr[i + 1];) {
                 const int j = L.col[e];
                 double v = 0.0;
-                for (; e < L.row_ptr[i + 1] && L.col[e] == j; ++e) v += L.a0[e];
+                for (; e < L.row_ptr[i + 1] && L.col[e] == j; ++e)
+                    v += g.cell_ref.empty() ? L.a0[e] : g.cell_ref[L.cell[e]] * L.a0[e];
                 c1.push_back(j);
                 a1.push_back(v);
             }
@@ -748,6 +759,246 @@ double dof_updates_per_solve(const LevelTables& t) {
         return n + static_cast<double>(t.n_steps - 1) * per_step;
     }
     return n + static_cast<double>(t.n_steps - 1) * (n + (t.p - 1) * static_cast<double>(t.n_r));
+}
+
+
+// ---------------------------------------------------------------------------
+// Narrow-channel experiment (see channel.hpp)
+
+double channel_blend(double x) {  // src/mesh2d.cpp:361-367
+    const double a = std::abs(x);
+    if (a <= kChannelHalfLength) return 1.0;
+    if (a >= kChannelBlendOuter) return 0.0;
+    return 0.5 * (1.0 + std::cos(3.14159265358979323846 * (a - kChannelHalfLength) /
+                                 (kChannelBlendOuter - kChannelHalfLength)));
+}
+
+double channel_profile(double y, double width) {  // src/mesh2d.cpp:369-377
+    const double half_ref = 0.5 * kChannelRefWidth;
+    const double peak = 0.5 * (width - kChannelRefWidth);
+    const double a = std::abs(y);
+    double value;
+    if (a <= half_ref)
+        value = peak * (a / half_ref);
+    else
+        value = peak * (kChannelRectHalfHeight - a) / (kChannelRectHalfHeight - half_ref);
+    return y < 0.0 ? -value : value;
+}
+
+LevelTables build_level_tables_channel(const TriMesh& mesh, const LevelSpec& spec, ChannelTables& ch) {
+    if (spec.final_time <= 0.0 || spec.dt <= 0.0) throw std::invalid_argument("level: T and dt must be positive");
+    if (spec.substeps < 1) throw std::invalid_argument("level: substeps >= 1");
+    if (spec.tiers != 1) throw std::invalid_argument("channel: single-tier LTS only");
+    if (spec.grid_n < 2) throw std::invalid_argument("channel: grid_n >= 2");
+    LevelTables L;
+    const int nv = mesh.n_vertices();
+    const int nt = mesh.n_triangles();
+    // moving vertices: blend(x) profile(y) != 0 for a width other than the
+    // reference one (profile vanishes on y = 0 and |y| = 1/2 only)
+    std::vector<std::uint8_t> moving(nv, 0), tri_mov(nt, 0), mass_mov(nv, 0);
+    for (int v = 0; v < nv; ++v)
+        moving[v] = channel_blend(mesh.vertices[v][0]) != 0.0 &&
+                    channel_profile(mesh.vertices[v][1], kChannelWidthLo) != 0.0;
+    for (int t = 0; t < nt; ++t) {
+        for (int v : mesh.triangles[t]) tri_mov[t] |= moving[v];
+        if (tri_mov[t])
+            for (int v : mesh.triangles[t]) mass_mov[v] = 1;
+    }
+
+    Geometry g;
+    g.nv = nv;
+    g.boundary.assign(nv, 0);  // Neumann: assemble(transformed mesh), no restriction (experiments.cpp:158)
+    g.unit_cells = true;
+    g.mass.assign(nv, 0.0);
+    std::vector<double> ms(nv, 0.0);  // mass of fixed triangles only
+    std::map<std::pair<int, int>, double> kref, kfix;  // reference stiffness: all / fixed triangles
+    auto elem = [&](int t, double* gx, double* gy) {  // assemble, fem.cpp:97-116 (speed^2 = 1)
+        const auto& tri = mesh.triangles[t];
+        const auto& p0 = mesh.vertices[tri[0]];
+        const auto& p1 = mesh.vertices[tri[1]];
+        const auto& p2 = mesh.vertices[tri[2]];
+        const double area = mesh.signed_area(t);
+        if (!(area > 0.0)) throw std::runtime_error("channel: nonpositive triangle area");
+        gx[0] = (p1[1] - p2[1]) / (2.0 * area);
+        gx[1] = (p2[1] - p0[1]) / (2.0 * area);
+        gx[2] = (p0[1] - p1[1]) / (2.0 * area);
+        gy[0] = (p2[0] - p1[0]) / (2.0 * area);
+        gy[1] = (p0[0] - p2[0]) / (2.0 * area);
+        gy[2] = (p1[0] - p0[0]) / (2.0 * area);
+        return area;
+    };
+    std::map<std::pair<int, int>, int> cell_of;  // unordered per-sample pair -> cell
+    for (int t = 0; t < nt; ++t) {
+        double gx[3], gy[3];
+        const double area = elem(t, gx, gy);
+        const auto& tri = mesh.triangles[t];
+        for (int i = 0; i < 3; ++i) {
+            g.mass[tri[i]] += area / 3.0;
+            if (!tri_mov[t]) ms[tri[i]] += area / 3.0;
+            for (int j = 0; j < 3; ++j) {
+                const double kij = 1.0 * area * (gx[i] * gx[j] + gy[i] * gy[j]);
+                kref[{tri[i], tri[j]}] += kij;
+                if (!tri_mov[t]) kfix[{tri[i], tri[j]}] += kij;
+                const int a = std::min(tri[i], tri[j]), b = std::max(tri[i], tri[j]);
+                if (tri_mov[t] || mass_mov[a] || mass_mov[b]) cell_of[{a, b}] = 0;
+            }
+        }
+    }
+    int next_cell = 1;
+    for (auto& kv : cell_of) kv.second = next_cell++;
+    L.n_cells = next_cell;
+    // the stiffness map: fixed pairs by element (cell 0), per-sample pairs as
+    // one unit entry of their cell
+    for (int t = 0; t < nt; ++t) {
+        double gx[3], gy[3];
+        const double area = elem(t, gx, gy);
+        const auto& tri = mesh.triangles[t];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                const int a = std::min(tri[i], tri[j]), b = std::max(tri[i], tri[j]);
+                const auto it = cell_of.find({a, b});
+                if (it != cell_of.end())
+                    g.stiff[{tri[i], tri[j], it->second}] = 1.0;
+                else
+                    g.stiff[{tri[i], tri[j], 0}] += 1.0 * area * (gx[i] * gx[j] + gy[i] * gy[j]);
+            }
+    }
+    g.cell_ref.assign(L.n_cells, 1.0);
+    for (const auto& [ab, k] : cell_of)
+        g.cell_ref[k] = kref[ab] / std::sqrt(g.mass[ab.first] * g.mass[ab.second]);
+
+    // selector: vertices of fine-flagged triangles (fem.cpp:119-122)
+    g.sel.assign(nv, 0);
+    g.vt.assign(nv, 0);
+    for (int t = 0; t < nt; ++t)
+        if (mesh.fine_flags[t])
+            for (int v : mesh.triangles[t]) g.sel[v] = g.vt[v] = 1;
+
+    // u0 = bump (experiments.cpp:118-124) by the edge-midpoint lumped
+    // projection (fem.cpp:223-241); its support (|(x - 1/2, y)| < 0.2) lies
+    // where the geometry never moves, so z0 is sample-independent
+    auto u0 = [](double x, double y) {
+        constexpr double radius = 0.2;
+        const double dx = x - 0.5;
+        const double rho2 = dx * dx + y * y;
+        if (rho2 >= radius * radius) return 0.0;
+        return std::exp(1.0 - radius * radius / (radius * radius - rho2));
+    };
+    std::vector<double> load(nv, 0.0);
+    for (int t = 0; t < nt; ++t) {
+        const auto& tri = mesh.triangles[t];
+        const double area = mesh.signed_area(t);
+        for (int e = 0; e < 3; ++e) {
+            const auto& a = mesh.vertices[tri[e]];
+            const auto& b = mesh.vertices[tri[(e + 1) % 3]];
+            const double value = u0(0.5 * (a[0] + b[0]), 0.5 * (a[1] + b[1]));
+            load[tri[e]] += area / 3.0 * value * 0.5;
+            load[tri[(e + 1) % 3]] += area / 3.0 * value * 0.5;
+        }
+    }
+    g.coef0.resize(nv);
+    for (int v = 0; v < nv; ++v) {
+        g.coef0[v] = load[v] / g.mass[v];
+        if (g.coef0[v] != 0.0 && mass_mov[v]) throw std::runtime_error("channel: u0 support meets the moving region");
+    }
+
+    // QoI: u(T) on the line x = -0.4 at the grid points of [-1/2, 1/2]
+    // (extract_line_qoi, fem.cpp:295-340): the first candidate triangle (in
+    // mesh order, x-range containing the line) holding the point, else the
+    // least-missed one; barycentric weights on its corners.  The line lies
+    // where the geometry never moves.
+    std::vector<int> cand;
+    for (int t = 0; t < nt; ++t) {
+        double xmin = 1e30, xmax = -1e30;
+        for (int v : mesh.triangles[t]) {
+            xmin = std::min(xmin, mesh.vertices[v][0]);
+            xmax = std::max(xmax, mesh.vertices[v][0]);
+        }
+        if (xmin - 1e-12 <= kChannelLineX && kChannelLineX <= xmax + 1e-12) cand.push_back(t);
+    }
+    const double lo = -kChannelRectHalfHeight, hi = kChannelRectHalfHeight;
+    const int n_out = spec.grid_n;
+    const double spacing = (hi - lo) / (n_out - 1);
+    g.qoi_entries.resize(n_out);
+    g.qoi_norm_w.resize(n_out);
+    for (int i = 0; i < n_out; ++i) {
+        const double y = i == n_out - 1 ? hi : lo + spacing * i;  // OutputGrid::point
+        g.qoi_norm_w[i] = (i == 0 || i == n_out - 1) ? 0.5 * spacing : spacing;
+        double best_miss = 1e30;
+        std::vector<std::pair<int, double>> best;
+        bool found = false;
+        for (int t : cand) {
+            const auto& tri = mesh.triangles[t];
+            const auto& p0 = mesh.vertices[tri[0]];
+            const auto& p1 = mesh.vertices[tri[1]];
+            const auto& p2 = mesh.vertices[tri[2]];
+            const double x = kChannelLineX;
+            const double area2 = (p1[0] - p0[0]) * (p2[1] - p0[1]) - (p2[0] - p0[0]) * (p1[1] - p0[1]);
+            const double l0 = ((p1[0] - x) * (p2[1] - y) - (p2[0] - x) * (p1[1] - y)) / area2;
+            const double l1 = ((p2[0] - x) * (p0[1] - y) - (p0[0] - x) * (p2[1] - y)) / area2;
+            const double l2 = 1.0 - l0 - l1;
+            const double miss = -std::min({l0, l1, l2});
+            if (miss < best_miss) {
+                best_miss = miss;
+                best = {{tri[0], l0}, {tri[1], l1}, {tri[2], l2}};
+            }
+            if (miss <= 1e-9) {
+                found = true;
+                break;
+            }
+        }
+        if (!found && best_miss > 1e-6) throw std::runtime_error("channel: QoI point outside the mesh");
+        for (const auto& [v, w] : best)
+            if (mass_mov[v]) throw std::runtime_error("channel: QoI line meets the moving region");
+        g.qoi_entries[i] = best;
+    }
+
+    // device tables of the per-sample entries
+    std::vector<int> loc(nv, -1);
+    for (int v = 0; v < nv; ++v)
+        if (mass_mov[v]) {
+            loc[v] = ch.n_local++;
+            ch.vx.push_back(mesh.vertices[v][0]);
+            ch.vy.push_back(mesh.vertices[v][1]);
+            ch.vblend.push_back(channel_blend(mesh.vertices[v][0]));
+            ch.ms.push_back(ms[v]);
+        }
+    std::vector<int> tloc(nt, -1);
+    std::vector<std::vector<int>> vtri(ch.n_local);
+    for (int t = 0; t < nt; ++t)
+        if (tri_mov[t]) {
+            tloc[t] = static_cast<int>(ch.tri.size() / 3);
+            for (int v : mesh.triangles[t]) {
+                ch.tri.push_back(loc[v]);
+                vtri[loc[v]].push_back(tloc[t]);
+            }
+        }
+    ch.m_ptr.assign(1, 0);
+    for (int l = 0; l < ch.n_local; ++l) {
+        ch.m_tri.insert(ch.m_tri.end(), vtri[l].begin(), vtri[l].end());
+        ch.m_ptr.push_back(static_cast<int>(ch.m_tri.size()));
+    }
+    std::vector<std::vector<int>> pair_tri(L.n_cells);
+    for (int t = 0; t < nt; ++t) {
+        if (!tri_mov[t]) continue;
+        const auto& tri = mesh.triangles[t];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                if (tri[a] <= tri[b]) pair_tri[cell_of.at({tri[a], tri[b]})].push_back(tloc[t] * 9 + a * 3 + b);
+    }
+    ch.k_ptr.assign(1, 0);
+    for (const auto& [ab, k] : cell_of) {
+        const auto [a, b] = ab;
+        ch.e_li.push_back(loc[a]);
+        ch.e_lj.push_back(loc[b]);
+        ch.e_mi.push_back(g.mass[a]);
+        ch.e_mj.push_back(g.mass[b]);
+        const auto it = kfix.find(ab);
+        ch.e_ks.push_back(it == kfix.end() ? 0.0 : it->second);
+        ch.k_tri.insert(ch.k_tri.end(), pair_tri[k].begin(), pair_tri[k].end());
+        ch.k_ptr.push_back(static_cast<int>(ch.k_tri.size()));
+    }
+    return finish_tables(g, spec, L, nullptr);
 }
 
 }  // namespace wmc

@@ -37,8 +37,9 @@ struct QoIBox {
 
 // Uniform / LognormalKL: per-cell coefficients on a cells_x x cells_y grid
 // (BASELINE); Kl1D / Jump1D: the reference's 1D experiment fields
-// (rng.cpp:42-89), one coefficient per element
-enum class Field : int { Uniform = 0, LognormalKL = 1, Kl1D = 2, Jump1D = 3 };
+// (rng.cpp:42-89), one coefficient per element; Channel: the narrow-channel
+// experiment's per-sample geometry (channel.hpp), one cell per moving entry
+enum class Field : int { Uniform = 0, LognormalKL = 1, Kl1D = 2, Jump1D = 3, Channel = 4 };
 
 struct LevelSpec {
     int cells_x = 4, cells_y = 4;  // coefficient grid on the domain box, cell k = iy*cells_x + ix

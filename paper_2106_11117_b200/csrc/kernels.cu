@@ -45,6 +45,92 @@ __global__ void draw_cells_kernel(std::uint64_t seed, std::uint32_t level, std::
     }
 }
 
+// Narrow-channel widths (sample_width, src/rng.cpp:59-64: the stream's first
+// word through next_uniform(0.001, 0.007)) and the per-sample entries of the
+// moved mesh, one thread per (entry, sample).  Every vertex position, area,
+// gradient and element product is formed with explicitly rounded operations
+// in the reference's order (ChannelGeometry::map, TriMesh::signed_area,
+// assemble: src/mesh2d.cpp:361-389, include/wavemc/mesh.hpp:65-70,
+// src/fem.cpp:97-116) so that the moved triangles are the reference's to the
+// last bit; only the summation order of a pair's / vertex's triangles differs.
+// Padding lanes take the reference width.
+__device__ __forceinline__ double channel_y(const ChannelArgs& a, int l, double width) {
+    const double y = __ldg(a.vy + l);
+    const double half_ref = __dmul_rn(0.5, 0.004);
+    const double peak = __dmul_rn(0.5, __dsub_rn(width, 0.004));
+    const double ay = fabs(y);
+    double value;
+    if (ay <= half_ref)
+        value = __dmul_rn(peak, __ddiv_rn(ay, half_ref));
+    else
+        value = __ddiv_rn(__dmul_rn(peak, __dsub_rn(0.5, ay)), __dsub_rn(0.5, half_ref));
+    if (y < 0.0) value = -value;
+    return __dadd_rn(y, __dmul_rn(__ldg(a.vblend + l), value));
+}
+
+// area, and gradients of the barycentric basis of moving triangle t
+__device__ __forceinline__ double channel_tri(const ChannelArgs& a, int t, double width, double* gx, double* gy) {
+    const int v0 = __ldg(a.tri + 3 * t), v1 = __ldg(a.tri + 3 * t + 1), v2 = __ldg(a.tri + 3 * t + 2);
+    const double x0 = __ldg(a.vx + v0), x1 = __ldg(a.vx + v1), x2 = __ldg(a.vx + v2);
+    const double y0 = channel_y(a, v0, width), y1 = channel_y(a, v1, width), y2 = channel_y(a, v2, width);
+    const double area = __dmul_rn(0.5, __dsub_rn(__dmul_rn(__dsub_rn(x1, x0), __dsub_rn(y2, y0)),
+                                                 __dmul_rn(__dsub_rn(x2, x0), __dsub_rn(y1, y0))));
+    if (gx) {
+        const double a2 = __dmul_rn(2.0, area);
+        gx[0] = __ddiv_rn(__dsub_rn(y1, y2), a2);
+        gx[1] = __ddiv_rn(__dsub_rn(y2, y0), a2);
+        gx[2] = __ddiv_rn(__dsub_rn(y0, y1), a2);
+        gy[0] = __ddiv_rn(__dsub_rn(x2, x1), a2);
+        gy[1] = __ddiv_rn(__dsub_rn(x0, x2), a2);
+        gy[2] = __ddiv_rn(__dsub_rn(x1, x0), a2);
+    }
+    return area;
+}
+
+__device__ __forceinline__ double channel_mass(const ChannelArgs& a, int l, double width) {
+    double m = __ldg(a.ms + l);
+    for (int q = __ldg(a.m_ptr + l); q < __ldg(a.m_ptr + l + 1); ++q)
+        m = __dadd_rn(m, __ddiv_rn(channel_tri(a, __ldg(a.m_tri + q), width, nullptr, nullptr), 3.0));
+    return m;
+}
+
+__global__ void __launch_bounds__(128) draw_channel_kernel(std::uint64_t seed, std::uint32_t level,
+                                                           std::uint64_t first, int count, int S, ChannelArgs a,
+                                                           double* __restrict__ cells) {
+    const int chunks = (S + 127) / 128;
+    const int k = blockIdx.x / chunks;
+    const int s = (blockIdx.x % chunks) * 128 + threadIdx.x;
+    if (s >= S || k > a.n_ent) return;
+    const std::size_t SS = static_cast<std::size_t>(S);
+    if (k == 0) {
+        cells[s] = 1.0;
+        return;
+    }
+    double width = 0.004;  // padding lanes: the reference geometry
+    if (s < count) {
+        std::uint64_t key = mix64(seed);
+        key = mix64(key ^ (0xa511e9b3cc1f25d1ULL + static_cast<std::uint64_t>(level)));
+        key = mix64(key ^ (0x63d1c71ad3e29f0bULL + (first + static_cast<std::uint64_t>(s))));
+        const std::uint64_t w = mix64(key);
+        const double unit = __dmul_rn(static_cast<double>(w >> 11), 0x1.0p-53);
+        width = __dadd_rn(0.001, __dmul_rn(__dsub_rn(0.007, 0.001), unit));
+    }
+    const int e = k - 1;
+    const int li = __ldg(a.e_li + e), lj = __ldg(a.e_lj + e);
+    const double mi = li >= 0 ? channel_mass(a, li, width) : __ldg(a.e_mi + e);
+    const double mj = lj >= 0 ? channel_mass(a, lj, width) : __ldg(a.e_mj + e);
+    double kij = __ldg(a.e_ks + e);
+    for (int q = __ldg(a.k_ptr + e); q < __ldg(a.k_ptr + e + 1); ++q) {
+        const int code = __ldg(a.k_tri + q);
+        const int t = code / 9, ca = (code / 3) % 3, cb = code % 3;
+        double gx[3], gy[3];
+        const double area = channel_tri(a, t, width, gx, gy);
+        kij = __dadd_rn(kij, __dmul_rn(__dmul_rn(1.0, area),
+                                       __dadd_rn(__dmul_rn(gx[ca], gx[cb]), __dmul_rn(gy[ca], gy[cb]))));
+    }
+    cells[static_cast<std::size_t>(k) * SS + s] = __ddiv_rn(kij, __dsqrt_rn(__dmul_rn(mi, mj)));
+}
+
 // 1D grid over (row group of kSweepWarps rows, 64-sample chunk), row group
 // fastest: concurrently resident blocks cover a contiguous band of rows, so
 // the N/S neighbour rows of a gather are L2 hits (measured faster than
@@ -745,7 +831,7 @@ __host__ __device__ inline std::size_t sub_layout(const SubArgs& a, char* base, 
     const std::size_t o1 = take(sizeof(double) * a.n_r);
     const std::size_t ob = take(sizeof(double) * (a.p > 1 ? a.p - 1 : 1));
     const std::size_t oc = take(sizeof(double) * (a.p > 1 ? a.p - 1 : 1));
-    const std::size_t ol = take(sizeof(double) * a.n_cells);
+    const std::size_t ol = take(sizeof(double) * (a.cl_smem ? a.n_cells : 0));
     const std::size_t os = take(sizeof(int) * (n_slices + 1));
     const std::size_t oe = take(sizeof(std::uint32_t) * a.n_ent);
     if (s) {
@@ -784,12 +870,16 @@ __global__ void __launch_bounds__(kSubThreads, 1) substep_kernel(SubArgs a) {
         if (a.nsteps && a.step > __ldg(a.nsteps + s)) continue;
         const double rs = a.rel ? __ldg(a.rel + s) : 1.0;
         __syncthreads();  // previous sample done with cl / W / d buffers
-        for (int k = tid; k < a.n_cells; k += kSubThreads) sm.cl[k] = __ldg(a.cells + k * S + s);
-        __syncthreads();
+        if (a.cl_smem) {
+            for (int k = tid; k < a.n_cells; k += kSubThreads) sm.cl[k] = __ldg(a.cells + k * S + s);
+            __syncthreads();
+        }
         for (int w = tid; w < a.n_wid; w += kSubThreads) {
             double acc = 0.0;
-            for (int t = __ldg(a.rc_ptr + w); t < __ldg(a.rc_ptr + w + 1); ++t)
-                acc += sm.cl[__ldg(a.rc_cell + t)] * __ldg(a.rc_a0 + t);
+            for (int t = __ldg(a.rc_ptr + w); t < __ldg(a.rc_ptr + w + 1); ++t) {
+                const int k = __ldg(a.rc_cell + t);
+                acc += (a.cl_smem ? sm.cl[k] : __ldg(a.cells + k * S + s)) * __ldg(a.rc_a0 + t);
+            }
             sm.W[w] = acc;
         }
 
@@ -2102,6 +2192,13 @@ int launch_lattice_solve(const LatSolveArgs& a, int grid, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (a.lat.threads == 512 && a.lat.strip_k == 8) return launch_lat_solve<512, 8, 2>(a, grid, st);
     return static_cast<int>(cudaErrorInvalidValue);
+}
+
+
+void launch_draw_channel(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S,
+                         const ChannelArgs& a, double* cells, void* stream) {
+    const unsigned grid = static_cast<unsigned>((S + 127) / 128) * static_cast<unsigned>(a.n_ent + 1);
+    draw_channel_kernel<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(seed, level, first, count, S, a, cells);
 }
 
 }  // namespace wmc

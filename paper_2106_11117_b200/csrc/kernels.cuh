@@ -38,6 +38,27 @@ constexpr int kSubMaxRpt = 8;    // rows per thread in the substep kernel
 // single-cell path: bit-identical results.
 constexpr int kMaxRowTypes = 8;
 
+// Narrow-channel experiment (host/channel.hpp): per-sample operator entries
+// c_k = A_ij(b), k >= 1, from the moved reference mesh; cell 0 is the unit
+// coefficient of the sample-independent entries.
+struct ChannelArgs {
+    int n_ent;                   // per-sample cells 1 .. n_ent
+    const double* vx;            // local vertices: reference position, blend(x)
+    const double* vy;
+    const double* vblend;
+    const int* tri;              // moving triangles, 3 local vertices each
+    const double* ms;            // local vertex: mass of its fixed triangles
+    const int* m_ptr;
+    const int* m_tri;
+    const int* e_li;             // entry endpoints (local vertex, or -1 with the fixed mass)
+    const int* e_lj;
+    const double* e_mi;
+    const double* e_mj;
+    const double* e_ks;          // fixed triangles' stiffness
+    const int* k_ptr;            // moving triangles coupling the pair: t * 9 + a * 3 + b
+    const int* k_tri;
+};
+
 struct SweepArgs {
     int n;           // rows
     int split;       // rows < split stash g (LTS); 0 for leapfrog
@@ -71,6 +92,7 @@ struct SweepArgs {
 struct SubArgs {
     int n_r, S, count, p;
     int n_wid, n_cells, n_ent;
+    int cl_smem;                // 1: cell coefficients staged in shared memory, 0: recipes read them from global
     const std::uint32_t* ent;   // SELL: [slice][width][32], col | wid << 16
     const int* slice_off;       // per slice: entry offset; width = (off[s+1]-off[s]) / 32
     const int* rc_ptr;
@@ -249,6 +271,8 @@ struct SmallArgs {
     int* fail;                   // per sample: first non-finite step (INT_MAX: none)
 };
 
+void launch_draw_channel(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S,
+                         const ChannelArgs& a, double* cells, void* stream);
 int small_smem_bytes(const SmallArgs& a);
 
 // Fused lattice solve: the whole solve of one sample per CTA (persistent over

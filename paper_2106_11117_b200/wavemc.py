@@ -63,6 +63,32 @@ class Mesh:
                                         C.byref(h)))
         return cls(h.value)
 
+    @classmethod
+    def load(cls, path: str) -> "Mesh":
+        """A mesh in the reference's plain-text fixture format (src/mesh_io.cpp:
+        1-9, 47-90: `wavemc-mesh-2d nv nt coarse_h fine_h`, `v x y`, `t a b c flag`),
+        e.g. the reference's build_channel_mesh output; gzip-compressed files
+        (*.gz) too.  No vertex is marked Dirichlet (Neumann problems)."""
+        import gzip
+        opener = gzip.open if str(path).endswith(".gz") else open
+        with opener(path, "rt") as f:
+            head = f.readline().split()
+            if len(head) != 5 or head[0] != "wavemc-mesh-2d":
+                raise ValueError(f"{path}: not a wavemc-mesh-2d fixture")
+            nv, nt = int(head[1]), int(head[2])
+            coarse_h, fine_h = float(head[3]), float(head[4])
+            xy = np.zeros((nv, 2), np.float64)
+            tri = np.zeros((nt, 3), np.int32)
+            fine = np.zeros(nt, np.uint8)
+            for i in range(nv):
+                tag, x, y = f.readline().split()
+                xy[i] = float(x), float(y)
+            for t in range(nt):
+                tag, a, b, c, flag = f.readline().split()
+                tri[t] = int(a), int(b), int(c)
+                fine[t] = int(flag)
+        return cls.from_arrays(xy, tri, fine, np.zeros(nv, np.uint8), coarse_h, fine_h)
+
     def info(self):
         nv, nt = C.c_int(), C.c_int()
         ch, fh = C.c_double(), C.c_double()
@@ -142,7 +168,7 @@ def _info_dict(info: N.LevelInfo) -> dict:
 
 def experiment_desc(experiment: str, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides) -> N.ExperimentDesc:
     """The reference's default_config for a 1D experiment (src/config_io.cpp:49-73) with overrides."""
-    kind = {"smooth1d": N.WMC_EXP_SMOOTH1D, "jump1d": N.WMC_EXP_JUMP1D}[experiment]
+    kind = {"smooth1d": N.WMC_EXP_SMOOTH1D, "jump1d": N.WMC_EXP_JUMP1D, "channel2d": N.WMC_EXP_CHANNEL2D}[experiment]
     d = N.ExperimentDesc()
     N.lib().wmc_experiment_desc_default(C.byref(d), kind)
     d.integrator = integrator
@@ -163,6 +189,14 @@ def experiment_model_cost(experiment: str, integrator: int = N.WMC_LOCAL_TIME_ST
     """The reference's closed-form model cost of every level (run_mlmc weights)."""
     d = experiment_desc(experiment, integrator, **overrides)
     return [N.lib().wmc_experiment_model_cost(C.byref(d), l) for l in range(d.max_level + 1)]
+
+
+def channel_plan(mesh: Mesh, level: int, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides) -> dict:
+    """Host-only sizes of one channel level on `mesh` (no device)."""
+    info = N.LevelInfo()
+    N.check(N.lib().wmc_channel_plan(mesh._h, C.byref(experiment_desc("channel2d", integrator, **overrides)), level,
+                                     C.byref(info)))
+    return _info_dict(info)
 
 
 def level_plan(mesh: Mesh, spec: LevelSpec) -> dict:
@@ -200,6 +234,24 @@ class Level:
         self.experiment_desc = d
         h = C.c_void_p()
         N.check(N.lib().wmc_level_create_experiment(C.byref(d), level, C.byref(h)))
+        self._h = h
+        info = N.LevelInfo()
+        N.check(N.lib().wmc_level_get_info(self._h, C.byref(info)))
+        self.info = _info_dict(info)
+        return self
+
+    @classmethod
+    def channel(cls, mesh: "Mesh", level: int, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides):
+        """Level `level` of the reference's narrow-channel experiment on `mesh`,
+        the reference's build_channel_mesh of that level (make_problem
+        Channel2d, src/experiments.cpp:108-172; wmc_level_create_channel)."""
+        d = experiment_desc("channel2d", integrator, **overrides)
+        self = cls.__new__(cls)
+        self.mesh = mesh
+        self.spec = None
+        self.experiment_desc = d
+        h = C.c_void_p()
+        N.check(N.lib().wmc_level_create_channel(mesh._h, C.byref(d), level, C.byref(h)))
         self._h = h
         info = N.LevelInfo()
         N.check(N.lib().wmc_level_get_info(self._h, C.byref(info)))
