@@ -125,6 +125,9 @@ ARTIFACT_CONFIGS = {
     # both integrators, a 64-point output grid, levels 0..3
     "smooth1d": "experiment = smooth1d\neps = 0.008,0.004\nintegrator = both\ngrid_n = 64\nmax_level = 3\n",
     "jump1d": "experiment = jump1d\neps = 0.008,0.004\nintegrator = both\ngrid_n = 64\nmax_level = 3\n",
+    # the small channel hierarchy of tests/golden/channel (its meshes)
+    "channel2d": ("experiment = channel2d\neps = 0.0004,0.0002\nintegrator = both\nh0 = 0.050000000000000003\n"
+                  "fine_h = 0.002\ngrid_n = 64\nmax_level = 2\n"),
 }
 
 

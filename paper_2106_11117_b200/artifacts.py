@@ -11,7 +11,8 @@ each opened with the reference's header (`# wavemc 0.1.0` and the config echo
 of src/config_io.cpp:227-256 minus `workers` / `out_dir`) and written at 17
 significant digits.  This module writes the same files, same names, header,
 columns and number format, from `wavemc.run_mlmc` on the device levels of the
-1D experiments.  Integer columns (levels, sample counts, convergence) come out
+1D experiments and of the narrow channel (reference meshes given).  Integer
+columns (levels, sample counts, convergence, cost records) come out
 identical to the reference's; floating-point columns agree to the parity
 tolerance of the per-sample QoIs, not to the last digit (different summation
 order on the device), so the files are format-compatible, not byte-identical.
@@ -31,7 +32,7 @@ from ._native import WMC_LEAPFROG, WMC_LOCAL_TIME_STEPPING
 
 VERSION = "wavemc 0.1.0"  # the reference's kVersion (include/wavemc/experiments.hpp:20), first header line
 EXPERIMENTS = ("smooth1d", "jump1d", "channel2d", "cost-sweep", "graded", "convergence")
-SAMPLING = ("smooth1d", "jump1d")  # sampling experiments this framework evaluates on the device
+SAMPLING = ("smooth1d", "jump1d", "channel2d")  # sampling experiments this framework evaluates on the device
 
 
 @dataclass
@@ -208,14 +209,20 @@ def grid_point(lo: float, hi: float, n: int, i: int) -> float:
     return hi if i == n - 1 else lo + ((hi - lo) / (n - 1)) * i
 
 
+def output_grid(experiment: str) -> tuple[float, float]:
+    """The experiment's output grid (experiments.cpp: [0, kDomain1dLength] for
+    the 1D experiments, [-kRectHalfHeight, kRectHalfHeight] for the channel)."""
+    return (-0.5, 0.5) if experiment == "channel2d" else (0.0, 6.0)
+
+
 def write_estimate_csv(c: ExperimentConfig, name: str, result: wavemc.MlmcResult) -> None:
-    """Reference write_estimate_csv (src/experiments.cpp:357-363); the 1D
-    experiments' output grid is [0, 6] (kDomain1dLength)."""
+    """Reference write_estimate_csv (src/experiments.cpp:357-363)."""
     est = result.estimate_vector
+    lo, hi = output_grid(c.experiment)
     with _open(c, name) as f:
         f.write("point,value\n")
         for i in range(len(est)):
-            f.write(f"{_g(grid_point(0.0, 6.0, len(est), i))},{_g(float(est[i]))}\n")
+            f.write(f"{_g(grid_point(lo, hi, len(est), i))},{_g(float(est[i]))}\n")
 
 
 def _overrides(c: ExperimentConfig, device: int) -> dict:
@@ -223,14 +230,19 @@ def _overrides(c: ExperimentConfig, device: int) -> dict:
                 max_level=c.max_level, device=device)
 
 
-def run_sampling_experiment(c: ExperimentConfig, log=sys.stderr, device: int = 0) -> int:
+def run_sampling_experiment(c: ExperimentConfig, log=sys.stderr, device: int = 0, meshes=None) -> int:
     """Reference run_sampling_experiment (src/experiments.cpp:365-409) on the
     device: for each integrator (LF first, then LF-LTS) and each eps, the
     adaptive MLMC driver over the experiment's level hierarchy, then the
-    levels / estimate CSVs and one row of <exp>_work.csv.  Returns the
-    reference's exit status (0 ok, 2 config error, 3 numerical failure)."""
+    levels / estimate CSVs and one row of <exp>_work.csv.  channel2d takes
+    the reference meshes of levels 0..max_level (`meshes`, wavemc.Mesh; the
+    reference's build_channel_mesh output).  Returns the reference's exit
+    status (0 ok, 2 config error, 3 numerical failure)."""
     if c.experiment not in SAMPLING:
         log.write(f"config error: {c.experiment} is not a device sampling experiment here\n")
+        return 2
+    if c.experiment == "channel2d" and (meshes is None or len(meshes) < c.max_level + 1):
+        log.write("config error: channel2d needs the reference mesh of every level\n")
         return 2
     kinds = [k for k in ("lf", "lts") if c.integrator in (k, "both")]
     try:
@@ -240,7 +252,11 @@ def run_sampling_experiment(c: ExperimentConfig, log=sys.stderr, device: int = 0
             for kind in kinds:
                 integ = WMC_LEAPFROG if kind == "lf" else WMC_LOCAL_TIME_STEPPING
                 ov = _overrides(c, device)
-                levels = [wavemc.Level.experiment(c.experiment, l, integ, **ov) for l in range(c.max_level + 1)]
+                if c.experiment == "channel2d":
+                    levels = [wavemc.Level.channel(meshes[l], l, integ, **ov) for l in range(c.max_level + 1)]
+                else:
+                    levels = [wavemc.Level.experiment(c.experiment, l, integ, **ov)
+                              for l in range(c.max_level + 1)]
                 costs = wavemc.experiment_model_cost(c.experiment, integ, **{k: v for k, v in ov.items()
                                                                                 if k != "device"})
                 for k, eps in enumerate(c.eps_list):
