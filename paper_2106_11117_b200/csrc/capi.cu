@@ -120,6 +120,7 @@ struct wmc_level {
     // sweep operator
     int* d_row_ptr = nullptr;
     int col_bits = 23;
+    int* d_cell_ix = nullptr;  // per-entry cells when they do not fit beside the column bits
     int4* d_row_desc = nullptr;
     double2* d_wtype = nullptr;
     double2 row_types[wmc::kMaxRowTypes] = {};
@@ -234,7 +235,8 @@ struct wmc_level {
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_warp_slice, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
                         (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0,
-                        (void*)d_rem_ptr, (void*)d_rem_col, (void*)d_rem_cell, (void*)d_rem_a0})
+                        (void*)d_rem_ptr, (void*)d_rem_col, (void*)d_rem_cell, (void*)d_rem_a0,
+                        (void*)d_cell_ix})
             if (p) cudaFree(p);
         for (void* p : ch_bufs) cudaFree(p);
         for (auto* p : d_tier_ptr) cudaFree(p);
@@ -368,16 +370,22 @@ void build_device_level(wmc_level& L) {
         L.col_bits = wmc::kColBits;
         if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
     } else {
-        // as many column bits as the DOFs need (at least 16), the rest for cells
+        // as many column bits as the DOFs need (at least 16), the rest for
+        // cells; past that (narrow-channel levels with ~1e5 per-sample cells)
+        // the cells go to a separate per-entry array
         L.col_bits = 16;
         while ((1L << L.col_bits) < t.n) ++L.col_bits;
-        if (L.col_bits > 31 || static_cast<long>(t.n_cells) > (1L << (32 - L.col_bits)))
-            throw ConfigError("level: " + std::to_string(t.n) + " DOFs and " + std::to_string(t.n_cells) +
-                              " coefficient cells do not fit a 32-bit entry");
+        if (L.col_bits > 30) throw ConfigError("level: more than 2^30 DOFs");
+        if (static_cast<long>(t.n_cells) > (1L << (32 - L.col_bits))) {
+            L.col_bits = 31;
+            L.d_cell_ix = upload(t.cell);
+        }
     }
     std::vector<int> ent(t.col.size());
     for (std::size_t k = 0; k < ent.size(); ++k)
-        ent[k] = static_cast<int>(static_cast<unsigned>(t.col[k]) | (static_cast<unsigned>(t.cell[k]) << L.col_bits));
+        ent[k] = L.d_cell_ix ? t.col[k]
+                             : static_cast<int>(static_cast<unsigned>(t.col[k]) |
+                                                (static_cast<unsigned>(t.cell[k]) << L.col_bits));
     L.d_row_ptr = upload(t.row_ptr);
     if (L.spec.field == wmc::Field::Channel) {
         const wmc::ChannelTables& c = L.ch;
@@ -414,6 +422,7 @@ void build_device_level(wmc_level& L) {
             int c = t.cell[b];
             for (int k = b; k < e; ++k)
                 if (t.cell[k] != c) c = -1;
+            if (c > 0xffff) c = -1;  // the descriptor holds 16 cell bits
             desc[i] = make_int4(c, b, 0, 0);
             if (c < 0 || e - b != 5 || std::getenv("WMC_SWEEP_GENERIC")) continue;
             const int* col = t.col.data() + b;
@@ -925,7 +934,8 @@ long cfl_phase(wmc_level& L, Workspace& ws, const double* cells, int S, int coun
         e.row_ptr = L.d_row_ptr;
         e.ent = L.d_ent;
         e.col_bits = L.col_bits;
-        e.col_mask = (1 << L.col_bits) - 1;
+        e.cell_ix = L.d_cell_ix;
+        e.col_mask = static_cast<int>((1u << L.col_bits) - 1u);
         e.a0 = L.d_a0;
         e.cells = cells;
         e.in_p = L.d_in_p;
@@ -1040,7 +1050,8 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
     sw.count = count;
     sw.row_ptr = L.d_row_ptr;
     sw.col_bits = L.col_bits;
-    sw.col_mask = (1 << L.col_bits) - 1;
+    sw.cell_ix = L.d_cell_ix;
+    sw.col_mask = static_cast<int>((1u << L.col_bits) - 1u);
     sw.row_desc = L.d_row_desc;
     sw.wtype = L.d_wtype;
     sw.ent = L.d_ent;
@@ -1222,7 +1233,8 @@ void small_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     a.row_ptr = L.d_row_ptr;
     a.ent = L.d_ent;
     a.col_bits = L.col_bits;
-    a.col_mask = (1 << L.col_bits) - 1;
+    a.cell_ix = L.d_cell_ix;
+    a.col_mask = static_cast<int>((1u << L.col_bits) - 1u);
     a.a0 = L.d_a0;
     a.row_desc = L.d_row_desc;
     a.wtype = L.d_wtype;
@@ -1266,7 +1278,8 @@ void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     a.row_ptr = L.d_row_ptr;
     a.ent = L.d_ent;
     a.col_bits = L.col_bits;
-    a.col_mask = (1 << L.col_bits) - 1;
+    a.cell_ix = L.d_cell_ix;
+    a.col_mask = static_cast<int>((1u << L.col_bits) - 1u);
     a.a0 = L.d_a0;
     a.row_desc = L.d_row_desc;
     a.wtype = L.d_wtype;

@@ -422,11 +422,10 @@ static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables
         L.apg_col_bits = 16;
         while ((1L << L.apg_col_bits) < L.n) ++L.apg_col_bits;
         if (L.apg_col_bits > 31 || static_cast<long>(L.n_cells) > (1L << (32 - L.apg_col_bits)))
-            throw std::invalid_argument("level: " + std::to_string(L.n) + " DOFs and " +
-                                        std::to_string(L.n_cells) + " coefficient cells do not fit a 32-bit entry");
+            L.apg_col_bits = 0;  // no packed form (the HBM-resident paths refuse such levels)
     }
     L.apg_ptr.assign(L.n_r + 1, 0);
-    for (int i = 0; i < L.n_r; ++i) {
+    for (int i = 0; i < L.n_r && L.apg_col_bits > 0; ++i) {
         for (const auto& [j, k, a] : rows[i]) {
             if (!L.in_p[j]) continue;
             L.apg_ent.push_back(static_cast<int>(static_cast<unsigned>(j) |

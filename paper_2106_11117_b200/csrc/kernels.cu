@@ -12,6 +12,13 @@ namespace wmc {
 
 namespace {
 
+// The coefficient cell of operator entry q: packed above the column
+// (col | cell << col_bits), or, when the level's cells do not fit beside its
+// columns (narrow-channel levels), from the separate per-entry array.
+__device__ __forceinline__ int ent_cell(const int* __restrict__ cell_ix, int q, int pk, int col_bits) {
+    return cell_ix ? __ldg(cell_ix + q) : static_cast<int>(static_cast<unsigned>(pk) >> col_bits);
+}
+
 // ---------------------------------------------------------------------------
 // K0: per-sample coefficients.  Bit-identical to the reference RngStream
 // (include/wavemc/rng.hpp:14-19, src/rng.cpp:14-32): key from
@@ -261,7 +268,7 @@ __device__ __forceinline__ void store_z(double* p, double2 out, int2 live, int* 
 // (reference src/integrators.cpp:89-115; for LTS rows outside R the
 // recursion collapses to factor = -2 d_p(g = 1), :117-157).
 
-template <bool kInit, bool kParts>
+template <bool kInit, bool kParts, bool kSplit = false>
 __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
     __shared__ double2 tile[kSweepWarps][32];  // g of the block's R rows: [row][lane] = samples 2 lane, 2 lane + 1
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -286,13 +293,13 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
             // entries grouped by cell: sum a0 z_j within a part, then scale by
             // the part's coefficient (one coefficient load per part)
             double p0 = 0.0, p1 = 0.0;
-            int pcell = static_cast<unsigned>(__ldg(a.ent + b)) >> a.col_bits;
+            int pcell = ent_cell(kSplit ? a.cell_ix : nullptr, b, __ldg(a.ent + b), a.col_bits);
             double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + pcell * S + s0));
             for (int k = b; k < e; ++k) {
                 const int pk = __ldg(a.ent + k);
                 const double w = __ldg(a.a0 + k);
                 const int j = pk & a.col_mask;
-                const int cell = static_cast<unsigned>(pk) >> a.col_bits;
+                const int cell = ent_cell(kSplit ? a.cell_ix : nullptr, k, pk, a.col_bits);
                 if (cell != pcell) {  // warp-uniform
                     acc0 += c.x * p0;
                     acc1 += c.y * p1;
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
                 const int pk = __ldg(a.ent + k);
                 const double w = __ldg(a.a0 + k);
                 const int j = pk & a.col_mask;
-                const int cell = static_cast<unsigned>(pk) >> a.col_bits;
+                const int cell = ent_cell(kSplit ? a.cell_ix : nullptr, k, pk, a.col_bits);
                 const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
                 if (kInit) {
                     const double zj = __ldg(a.z0 + j);
@@ -507,7 +514,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
                     const int pk = __ldg(a.ent + q);
                     const double w = __ldg(a.a0 + q);
                     const int j = pk & a.col_mask;
-                    const int cell = static_cast<unsigned>(pk) >> a.col_bits;
+                    const int cell = ent_cell(nullptr, q, pk, a.col_bits)  /* packed: split levels take sweep_kernel */;
                     const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
                     const double2 z = zrow(j);
                     acc0 += (cc.x * w) * z.x;
@@ -1243,7 +1250,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) eig_matvec_kernel(EigArgs a)
             const int j = pk & a.col_mask;
             if (a.coarse && __ldg(a.in_p + j)) continue;
             const double w = __ldg(a.a0 + k);
-            const int cell = static_cast<unsigned>(pk) >> a.col_bits;
+            const int cell = ent_cell(a.cell_ix, k, pk, a.col_bits);
             const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
             const double2 x = __ldg(reinterpret_cast<const double2*>(a.v + j * S + s0));
             acc0 += (c.x * w) * x.x;
@@ -1417,7 +1424,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_solve_kernel(SmallArgs
                 for (int q = b; q < e; ++q) {
                     const unsigned pk = static_cast<unsigned>(__ldg(a.ent + q));
                     const double zj = __ldg(a.z0 + (pk & a.col_mask));
-                    acc0 += (cl[pk >> a.col_bits] * __ldg(a.a0 + q)) * zj;
+                    acc0 += (cl[ent_cell(a.cell_ix, q, static_cast<int>(pk), a.col_bits)] * __ldg(a.a0 + q)) * zj;
                 }
             }
             const double z0 = __ldg(a.z0 + i);
@@ -1453,7 +1460,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_solve_kernel(SmallArgs
                 } else {
                     for (int q = d.y; q < __ldg(a.row_ptr + i + 1); ++q) {
                         const unsigned pk = static_cast<unsigned>(__ldg(a.ent + q));
-                        acc0 += (cl[pk >> a.col_bits] * __ldg(a.a0 + q)) * zc[pk & a.col_mask];
+                        acc0 += (cl[ent_cell(a.cell_ix, q, static_cast<int>(pk), a.col_bits)] * __ldg(a.a0 + q)) *
+                                zc[pk & a.col_mask];
                     }
                 }
                 if (i < a.split) {
@@ -1583,7 +1591,8 @@ __device__ __forceinline__ double lat_solve_row(const LatSolveArgs& A, int i, co
         const int e = __ldg(A.row_ptr + i + 1);
         for (int q = d.y; q < e; ++q) {
             const unsigned pk = static_cast<unsigned>(__ldg(A.ent + q));
-            acc0 += (cl[pk >> A.col_bits] * __ldg(A.a0 + q)) * zc[pk & A.col_mask];
+            acc0 += (cl[ent_cell(A.cell_ix, q, static_cast<int>(pk), A.col_bits)] * __ldg(A.a0 + q)) *
+                    zc[pk & A.col_mask];
         }
     }
     return acc0;
@@ -1988,7 +1997,10 @@ void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t fi
 
 void launch_sweep_init(const SweepArgs& a, void* stream) {
     const unsigned grid = ((a.n + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
-    sweep_kernel<true, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    if (a.cell_ix)
+        sweep_kernel<true, false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    else
+        sweep_kernel<true, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
 void launch_sweep_step(const SweepArgs& a, void* stream) {
@@ -2001,7 +2013,9 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
         const char* v = std::getenv("WMC_SWEEP_ONE_ROW");  // tuning knob: one row per warp
         return v ? std::atoi(v) : 0;
     }();
-    if (parts) {
+    if (a.cell_ix) {  // cells in a separate per-entry array (narrow-channel levels)
+        sweep_kernel<false, false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    } else if (parts) {
         sweep_kernel<false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     } else if (one_row || !a.row_desc) {
         sweep_kernel<false, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);

@@ -67,6 +67,7 @@ struct SweepArgs {
     const int* row_ptr;
     const int* ent;      // col | cell << col_bits (23, or 16 when there are more than 511 cells)
     int col_bits, col_mask;
+    const int* cell_ix;          // per-entry cell when it is not packed above the column (NULL: packed)
     const double* a0;
     // per row {info, row_ptr begin, dS, dN}; info = cell | type << 16 |
     // pfull << 24 for a structured row (type >= 1; pfull = deepest tier whose
@@ -243,6 +244,7 @@ struct SmallArgs {
     const int* row_ptr;          // full operator (sweep tables, as SweepArgs)
     const int* ent;
     int col_bits, col_mask;
+    const int* cell_ix;          // per-entry cell when it is not packed above the column (NULL: packed)
     const double* a0;
     const int4* row_desc;
     const double2* wtype;
@@ -290,6 +292,7 @@ struct LatSolveArgs {
     const int* row_ptr;          // sweep tables (as SweepArgs)
     const int* ent;
     int col_bits, col_mask;
+    const int* cell_ix;          // per-entry cell when it is not packed above the column (NULL: packed)
     const double* a0;
     const int4* row_desc;
     const double2* wtype;
@@ -342,6 +345,7 @@ struct EigArgs {
     const int* row_ptr;
     const int* ent;
     int col_bits, col_mask;
+    const int* cell_ix;          // per-entry cell when it is not packed above the column (NULL: packed)
     const double* a0;
     const double* cells;
     const unsigned char* in_p;
