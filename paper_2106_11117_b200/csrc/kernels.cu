@@ -8,6 +8,16 @@
 
 #include "kernels.cuh"
 
+#ifndef WMC_GSUB_MINB
+#define WMC_GSUB_MINB 4  // 64 registers (measured 1.26x over the unconstrained 120-register build, config 3)
+#endif
+#ifndef WMC_TIER_MINB
+#define WMC_TIER_MINB 6  // 40 registers (measured 1.07x, config 2 level 4)
+#endif
+#ifndef WMC_SWEEP_MINB
+#define WMC_SWEEP_MINB 5  // 48 registers: 5 blocks per SM (measured 1.2x on HBM-bound sweeps over the 64-register build)
+#endif
+
 namespace wmc {
 
 namespace {
@@ -440,7 +450,7 @@ constexpr int kSweepRows = 4;
 constexpr int kTierRows = WMC_TIER_ROWS;
 
 template <int R>
-__global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepWarps * 32, WMC_SWEEP_MINB) sweep_rows_kernel(SweepArgs a) {
     __shared__ double2 tile[kSweepWarps * R][32];  // g of the block's R rows: [row][lane]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int groups = (a.n + kSweepWarps * R - 1) / (kSweepWarps * R);
@@ -560,7 +570,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_rows_kernel(SweepArgs 
 // current d buffer, d_{m+1} written over d_{m-1} (own row only), the last
 // substep forms z_{n+1} directly (reference src/integrators.cpp:137-153).
 template <int R>
-__global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubArgs a) {
+__global__ void __launch_bounds__(kSweepWarps * 32, WMC_GSUB_MINB) global_substep_kernel(GSubArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int groups = (a.n_r + kSweepWarps * R - 1) / (kSweepWarps * R);
     const int first = (blockIdx.x % groups) * kSweepWarps * R + warp * R;
@@ -654,7 +664,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) global_substep_kernel(GSubAr
 // src/integrators.cpp:117-157 applied per tier, with the stage's right-hand
 // side on R_k+1 replaced by the tier-(k+1) solve over the stage interval.
 template <int R>
-__global__ void __launch_bounds__(kSweepWarps * 32) tier_stage_kernel(TierArgs a) {
+__global__ void __launch_bounds__(kSweepWarps * 32, WMC_TIER_MINB) tier_stage_kernel(TierArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nrows = a.row_end - a.row_begin;
     const int groups = (nrows + kSweepWarps * R - 1) / (kSweepWarps * R);
