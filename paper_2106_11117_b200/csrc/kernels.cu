@@ -443,7 +443,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(SweepArgs a) {
 // values) and reuses the coefficient of the previous row when the cell is
 // the same.  Generic rows gather as in sweep_kernel.  Products and sums in
 // the same order as sweep_kernel: bit-identical results.
-constexpr int kSweepRows = 4;
+constexpr int kSweepRows = 4;         // rows per warp of the HBM-resident substep kernel
+constexpr int kSweepRowsDefault = 2;  // rows per warp of the step sweep (measured best with 48 registers)
 #ifndef WMC_TIER_ROWS
 #define WMC_TIER_ROWS 1
 #endif
@@ -2032,7 +2033,7 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
     } else {
         static const int r = [] {
             const char* v = std::getenv("WMC_SWEEP_ROWS");  // tuning knob: rows per warp (2, 4, 8)
-            return v ? std::atoi(v) : kSweepRows;
+            return v ? std::atoi(v) : kSweepRowsDefault;
         }();
         const int rows = kSweepWarps * r;
         const unsigned g2 = ((a.n + rows - 1) / rows) * (a.S / kSweepChunk);
