@@ -27,3 +27,24 @@ def test_experiment_levels_plan():
     assert wavemc.experiment_plan("smooth1d", 4)["p"] == 1
     with pytest.raises(wavemc.ConfigError):
         wavemc.experiment_plan("smooth1d", 9)
+
+
+def test_channel_level_tables_from_reference_meshes():
+    """Host side of the narrow-channel experiment on the reference's own
+    meshes (tests/golden/channel): Neumann DOFs, LF-LTS ratio, per-sample
+    cells and the line QoI, no device needed."""
+    import os
+
+    from paper_2106_11117_b200 import wavemc
+    g = os.path.join(os.path.dirname(__file__), "golden", "channel")
+    ov = dict(h0=0.05, fine_h=0.002, max_level=2, grid_n=64)
+    for l, p in enumerate((25, 13, 7)):
+        m = wavemc.Mesh.load(os.path.join(g, f"mesh_l{l}.txt.gz"))
+        nv, nt, _, _ = m.info()
+        info = wavemc.channel_plan(m, l, **ov)
+        assert info["n"] == nv and info["p"] == p and info["nq"] == 64
+        assert 0 < info["n_r"] < nv and info["n_recipes"] > 0
+        lf = wavemc.channel_plan(m, l, integrator=0, **ov)
+        assert lf["p"] == 1 and lf["n"] == nv
+    cost = wavemc.experiment_model_cost("channel2d", **ov)
+    assert cost == [34308.566617554192, 124605.34624289621, 628499.26331298659]  # the reference's make_problem
