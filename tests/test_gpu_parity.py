@@ -162,6 +162,27 @@ def test_instability_raises_numerical_error_with_step(coracle, mesh0_arrays):
     assert rc == 3 and ei.value.step == step
 
 
+def test_fused_solve_reports_instability_like_the_step_kernels(monkeypatch):
+    """An unstable LF-LTS level (coarse step far above its CFL bound) through
+    the fused lattice solve reports the same first failing sample and step as
+    the per-step kernels (check_finite, src/integrators.cpp:12-18)."""
+    d = configs.config1()[0]
+    spec = configs.level_spec(d)
+    spec.dt = 4.0 * spec.dt
+    m = configs.build_mesh(d)
+    fused = wavemc.Level(m, spec)
+    monkeypatch.setenv("WMC_FUSED", "0")
+    plain = wavemc.Level(m, spec)
+    monkeypatch.delenv("WMC_FUSED")
+    assert fused.info["fused"] == 1 and plain.info["fused"] == 0
+    errs = []
+    for lv in (fused, plain):
+        with pytest.raises(wavemc.NumericalError) as ei:
+            wavemc.eval_pairs(lv, None, 0, 0, 3, 40)
+        errs.append((ei.value.sample, ei.value.step))
+    assert errs[0] == errs[1] and errs[0][0] == 3 and errs[0][1] > 1
+
+
 def test_config_errors_are_reported():
     with pytest.raises(wavemc.ConfigError):
         wavemc.Level(configs.build_mesh(configs.config0()), wavemc.LevelSpec(dt=0.01, nu=2.0))
