@@ -1795,15 +1795,32 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
 #pragma unroll
             for (int u = 0; u < G; ++u)
                 ggg[u] = grow[u] >= 0 ? gen_full_row(A, sd, o.gw, o.v0, gcol, gslot[u], gwid[u], gq[u], zn, cl) : 0.0;
-            for (int i = nr + tid; i < A.n; i += T) {
-                const double zi = zn[i];
-                const double out = 2.0 * zi - zp[i] - factor * lat_solve_row(A, i, zn, cl);
-                sd[o.v1 + i - nr] = out;
-                zp[i] = zi;
-                if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+            // four rows per pass, every load before any store (z_{n-1} may
+            // live in global memory: its latency overlaps instead of chaining)
+            for (int i0 = nr + tid; i0 < A.n; i0 += 4 * T) {
+                double zi[4], zq[4], gr[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * T;
+                    zi[u] = i < A.n ? zn[i] : 0.0;
+                    zq[u] = i < A.n ? zp[i] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) gr[u] = i0 + u * T < A.n ? lat_solve_row(A, i0 + u * T, zn, cl) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * T;
+                    if (i >= A.n) continue;
+                    const double out = 2.0 * zi[u] - zq[u] - factor * gr[u];
+                    sd[o.v1 + i - nr] = out;
+                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                }
             }
             __syncthreads();
-            for (int i = nr + tid; i < A.n; i += T) zn[i] = sd[o.v1 + i - nr];
+            for (int i = nr + tid; i < A.n; i += T) {  // z_{n-1} <- z_n, z_n <- z_{n+1}
+                zp[i] = zn[i];
+                zn[i] = sd[o.v1 + i - nr];
+            }
             // ---- substeps (lattice_substep_kernel's recursion), d_1 = -c0 g.
             // Lattice nodes recurse on v = d / h itself (what the stencil and
             // the neighbours read): v_{m+1} = (1 + beta) v_m - beta v_{m-1}
@@ -1860,13 +1877,19 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 }
                 __syncthreads();
             }
-            // ---- R update (r_update_kernel): z_{n+1} = 2 z_n - z_{n-1} + 2 d_p
+            // ---- R update (r_update_kernel): z_{n+1} = 2 z_n - z_{n-1} + 2 d_p;
+            // z_{n-1} of the thread's rows loaded before any store
+            double zq[K], zgq[G];
+#pragma unroll
+            for (int k = 0; k < K; ++k) zq[k] = k < len ? zp[base + k] : 0.0;
+#pragma unroll
+            for (int u = 0; u < G; ++u) zgq[u] = grow[u] >= 0 ? zp[grow[u]] : 0.0;
 #pragma unroll
             for (int k = 0; k < K; ++k)
                 if (k < len) {
                     const int i = base + k;
                     const double zi = zn[i];
-                    const double out = 2.0 * zi - zp[i] + 2.0 * (d[k] * hh);
+                    const double out = 2.0 * zi - zq[k] + 2.0 * (d[k] * hh);
                     zp[i] = zi;
                     zn[i] = out;
                     if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
@@ -1876,7 +1899,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 if (grow[u] >= 0) {
                     const int i = grow[u];
                     const double zi = zn[i];
-                    const double out = 2.0 * zi - zp[i] + 2.0 * gd[u];
+                    const double out = 2.0 * zi - zgq[u] + 2.0 * gd[u];
                     zp[i] = zi;
                     zn[i] = out;
                     if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
