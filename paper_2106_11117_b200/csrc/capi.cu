@@ -144,7 +144,8 @@ struct wmc_level {
     int sub_grid = 0;
     int small_smem = 0;  // fused small-mesh solve: shared memory per CTA (0: not eligible)
     int fused_smem = 0;  // fused lattice solve: shared memory per CTA (0: not eligible)
-    bool fused_zp_global = false;  // fused lattice solve keeps z_{n-1} in a per-sample global buffer
+    bool fused_zp_global = false;
+    int fused_tmem = 1;            // fused lattice solve: tensor-memory variant (fixed at level creation)  // fused lattice solve keeps z_{n-1} in a per-sample global buffer
     int n_sms = 148;
     SubPath path = SubPath::None;
     int* d_apg_ptr = nullptr;
@@ -272,6 +273,13 @@ struct wmc_level {
 namespace {
 
 int round64(long v) { return static_cast<int>((v + 63) / 64 * 64); }
+
+// fused lattice solve: per-thread generic weights and d_{m-1} in tensor
+// memory (default); WMC_FUSED_TMEM=0 keeps them in shared memory
+int fused_tmem() {
+    const char* e = std::getenv("WMC_FUSED_TMEM");
+    return e ? (std::atoi(e) != 0) : 1;
+}
 
 // Generic SELL rows of the lattice kernels: lane placement for shared-memory
 // banks.  A 64-bit shared access is served per half-warp; it costs as many
@@ -756,9 +764,14 @@ void build_device_level(wmc_level& L) {
             probe.lat.n_strips = static_cast<int>(t.strip_j0.size());
             probe.lat.n_slots = L.n_slots;
             probe.n = t.n;
-            // taken when z_{n-1} fits on chip too and the rows outside R
-            // (round-robin, latency-bound gathers) are at most two per
-            // thread: config-1 levels 0 and 1, the bulk of its substep work.
+            L.fused_tmem = fused_tmem();
+            probe.tmem = L.fused_tmem;
+            // taken when z_{n-1} fits on chip too: config-1 levels 0, 1 and,
+            // with the generic weights in tensor memory (which frees their
+            // shared-memory table), level 2 (n = 8 433; 1.09x over the
+            // per-step kernels although 3 752 rows lie outside R).  Without
+            // tensor memory the rows outside R must be at most two per
+            // thread (round-robin, latency-bound gathers).
             // WMC_FUSED_ZP_GLOBAL=1 forces the layout with z_{n-1} in global
             // memory (tests; it is slower where the rows outside R are many)
             const int cap = wmc::lattice_solve_max_smem(L.device);
@@ -768,7 +781,11 @@ void build_device_level(wmc_level& L) {
                 L.fused_zp_global = true;
             }
             const int bytes = wmc::lattice_solve_smem_bytes(probe);
-            if (bytes <= cap && (L.fused_zp_global || t.n - t.n_r <= 2 * t.lat_threads)) L.fused_smem = bytes;
+            const char* ff = std::getenv("WMC_FUSED_FORCE");  // tuning knob: ignore the rows-outside-R limit
+            const bool force = ff && std::atoi(ff) != 0;
+            if (bytes <= cap &&
+                (force || L.fused_tmem || L.fused_zp_global || t.n - t.n_r <= 2 * t.lat_threads))
+                L.fused_smem = bytes;
         }
     }
     L.d_cells = nullptr;
@@ -1288,6 +1305,7 @@ void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     a.factor = t.coarse_factor;
     a.n_steps = t.n_steps;
     a.zp_global = L.fused_zp_global ? ws.zb : nullptr;
+    a.tmem = L.fused_tmem;
     a.rem_ptr = L.d_rem_ptr;
     a.rem_col = L.d_rem_col;
     a.rem_cell = L.d_rem_cell;

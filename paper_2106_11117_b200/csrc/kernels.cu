@@ -566,6 +566,133 @@ __global__ void __launch_bounds__(kSweepWarps * 32, WMC_SWEEP_MINB) sweep_rows_k
     }
 }
 
+// K1, load-first form: the warp's R row descriptors are loaded together,
+// then every HBM value of its structured rows (z_{i+1}, z_{i-dS}, z_{i+dN},
+// z_{n-1}) before the first product or store, so one warp keeps 4 R x 512 B
+// in flight instead of one row's chain (descriptor -> values -> store) at a
+// time.  Same products and sums in the same order as sweep_rows_kernel:
+// bit-identical results.  MINB trades registers for resident warps.
+template <int R, int MINB>
+__global__ void __launch_bounds__(kSweepWarps * 32, MINB) sweep_ahead_kernel(SweepArgs a) {
+    __shared__ double2 tile[kSweepWarps * R][32];  // g of the block's R rows: [row][lane]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int groups = (a.n + kSweepWarps * R - 1) / (kSweepWarps * R);
+    const int row0 = (blockIdx.x % groups) * kSweepWarps * R;
+    const int chunk = blockIdx.x / groups;
+    const int s0 = chunk * kSweepChunk + 2 * lane;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const int first = row0 + warp * R;
+    auto zrow = [&](int r) {
+        return __ldg(reinterpret_cast<const double2*>(a.zc + static_cast<std::size_t>(r) * S + s0));
+    };
+    const double2 zero = make_double2(0.0, 0.0);
+    int4 d[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+        d[k] = first + k < a.n ? __ldg(a.row_desc + first + k) : make_int4(-1, 0, 0, 0);
+    double2 zprev = zero, zcur = zero;
+    if (first < a.n) {
+        if (first > 0) zprev = zrow(first - 1);
+        zcur = zrow(first);
+    }
+    double2 zx[R], zs[R], zn[R], zm[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int row = first + k;
+        const bool st = row < a.n && d[k].x >= 0 && ((d[k].x >> 16) & 0xff) > 0;
+        zx[k] = row + 1 < a.n ? zrow(row + 1) : zero;
+        zm[k] = row < a.n && row >= a.split
+                    ? *reinterpret_cast<const double2*>(a.zp + static_cast<std::size_t>(row) * S + s0)
+                    : zero;
+        zs[k] = st ? zrow(row - d[k].z) : zero;
+        zn[k] = st ? zrow(row + d[k].w) : zero;
+    }
+    const double2 fac = a.rel ? lane_rel(a.rel, s0) : make_double2(1.0, 1.0);
+    const double2 factor = make_double2(a.factor * fac.x, a.factor * fac.y);
+    const int2 live = lane_live(a.nsteps, s0, a.step);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int row = first + k;
+        if (row >= a.n) break;
+        const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
+        double acc0 = 0.0, acc1 = 0.0;
+        if (d[k].x >= 0 && ((d[k].x >> 16) & 0xff) > 0) {
+            const double2 w = __ldg(a.wtype + ((d[k].x >> 16) & 0xff) - 1);
+            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + (d[k].x & 0xffff) * S + s0));
+            double p0 = 0.0, p1 = 0.0;
+            p0 += w.x * zs[k].x;
+            p1 += w.x * zs[k].y;
+            p0 += w.x * zprev.x;
+            p1 += w.x * zprev.y;
+            p0 += w.y * zcur.x;
+            p1 += w.y * zcur.y;
+            p0 += w.x * zx[k].x;
+            p1 += w.x * zx[k].y;
+            p0 += w.x * zn[k].x;
+            p1 += w.x * zn[k].y;
+            acc0 = c.x * p0;
+            acc1 = c.y * p1;
+        } else {
+            const int b = d[k].y, e = __ldg(a.row_ptr + row + 1);
+            if (d[k].x >= 0) {
+                const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + (d[k].x & 0xffff) * S + s0));
+                double p0 = 0.0, p1 = 0.0;
+#pragma unroll 4
+                for (int q = b; q < e; ++q) {
+                    const int j = __ldg(a.ent + q) & a.col_mask;
+                    const double w = __ldg(a.a0 + q);
+                    const double2 z = zrow(j);
+                    p0 += w * z.x;
+                    p1 += w * z.y;
+                }
+                acc0 = cc.x * p0;
+                acc1 = cc.y * p1;
+            } else {
+#pragma unroll 4
+                for (int q = b; q < e; ++q) {
+                    const int pk = __ldg(a.ent + q);
+                    const double w = __ldg(a.a0 + q);
+                    const int j = pk & a.col_mask;
+                    const int cell = ent_cell(nullptr, q, pk, a.col_bits);
+                    const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
+                    const double2 z = zrow(j);
+                    acc0 += (cc.x * w) * z.x;
+                    acc1 += (cc.y * w) * z.y;
+                }
+            }
+        }
+        if (row < a.split) {
+            if (a.g_node_major)
+                *reinterpret_cast<double2*>(a.g + idx) = make_double2(acc0, acc1);
+            else
+                tile[warp * R + k][lane] = make_double2(acc0, acc1);
+        } else {
+            double2 out;
+            out.x = 2.0 * zcur.x - zm[k].x - factor.x * acc0;
+            out.y = 2.0 * zcur.y - zm[k].y - factor.y * acc1;
+            store_z(a.zp + idx, out, live, a.fail, s0, a.count, a.step);
+        }
+        zprev = zcur;
+        zcur = zx[k];
+    }
+    if (row0 >= a.split || a.g_node_major) return;  // block-uniform
+    __syncthreads();
+    constexpr int kRowsPerThread = kSweepWarps * R * kSweepChunk / (kSweepWarps * 32);
+    const int sl = threadIdx.x / (kSweepWarps * R / kRowsPerThread);
+    const int r0 = (threadIdx.x % (kSweepWarps * R / kRowsPerThread)) * kRowsPerThread;
+    const int s = chunk * kSweepChunk + sl;
+    double* dst = a.g + static_cast<std::size_t>(s) * a.g_stride + row0 + r0;
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; q += 2) {
+        const double2 t0 = tile[r0 + q][sl >> 1], t1 = tile[r0 + q + 1][sl >> 1];
+        const double g0 = (sl & 1) ? t0.y : t0.x, g1 = (sl & 1) ? t1.y : t1.x;
+        if (row0 + r0 + q + 1 < a.split)
+            *reinterpret_cast<double2*>(dst + q) = make_double2(g0, g1);
+        else if (row0 + r0 + q < a.split)
+            dst[q] = g0;
+    }
+}
+
 // K2 (HBM-resident): one substep over the R rows, warp per (row, 64
 // samples) as in the sweep; A(omega) P d gathered node-centrically from the
 // current d buffer, d_{m+1} written over d_{m-1} (own row only), the last
@@ -1563,11 +1690,11 @@ __host__ __device__ inline LatSolveOff lat_solve_offsets(const LatSolveArgs& A) 
     o.v0 = take(a.n_r + 16);  // rows past a short strip read (never write) up to 8 beyond
     // v1 also holds z_{n+1} of the rows outside R between the sweep and its store
     o.v1 = take(a.n_r + 16 > A.n - a.n_r ? a.n_r + 16 : A.n - a.n_r);
-    o.gw = take(slots);
+    o.gw = A.tmem ? -1 : take(slots);  // generic weights and columns live in TMEM when tmem is set
     o.cl = take(a.n_cells);
     o.beta = take(a.p > 1 ? a.p - 1 : 1);
     o.cm = take(a.p > 1 ? a.p - 1 : 1);
-    o.gcol = take((slots * 2 + 7) / 8);  // uint16
+    o.gcol = A.tmem ? -1 : take((slots * 2 + 7) / 8);  // uint16
     o.sj0 = take((a.n_strips + 1) / 2);  // int
     o.slen = take((a.n_strips + 1) / 2);
     o.cx = take((a.m + 1) / 2);
@@ -1637,6 +1764,100 @@ __device__ __forceinline__ void lat_solve_g(double* sd, int ov, const double* zn
     }
 }
 
+// ---- Tensor memory as per-thread private storage (fused lattice solve).
+// TMEM (256 KB per SM, 128 lanes x 512 columns of 32 bits) is read by
+// tcgen05.ld on its own datapath: measured on this B200 at ~390 B/clk/SM
+// beside an unchanged 128 B/clk of shared-memory LDS.128 traffic
+// (tune/tmem_bench.cu), so what a thread alone reads every substep -- its
+// generic rows' SELL weights and columns, and d_{m-1} of its lattice nodes --
+// moves out of the shared-memory pipe the kernel is bound by.  Warp w owns
+// lanes 32 (w % 4) .. + 31 (its sub-partition's lane quarter) and columns
+// 128 (w / 4) .. + 127.  Each tcgen05.ld / st is issued together with its
+// wait in one asm statement, so the compiler cannot read the outputs (or
+// reuse the inputs) early.
+__device__ __forceinline__ void tm_ld16(std::uint32_t addr, std::uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr)
+        : "memory");
+}
+__device__ __forceinline__ void tm_ld16_4(std::uint32_t aw, std::uint32_t (&w)[16], std::uint32_t ac,
+                                          std::uint32_t (&c)[4]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%20];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%16,%17,%18,%19}, [%21];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+          "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15]),
+          "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3])
+        : "r"(aw), "r"(ac)
+        : "memory");
+}
+__device__ __forceinline__ void tm_st16(std::uint32_t addr, const std::uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+        "tcgen05.wait::st.sync.aligned;\n"
+        :
+        : "r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tm_st4(std::uint32_t addr, const std::uint32_t (&r)[4]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n"
+        "tcgen05.wait::st.sync.aligned;\n"
+        :
+        : "r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+        : "memory");
+}
+__device__ __forceinline__ std::uint32_t tm_alloc_512(std::uint32_t* slot) {  // whole warp; one CTA per SM
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
+                 "tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n"
+                 :
+                 : "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(slot)))
+                 : "memory");
+    return 0;
+}
+__device__ __forceinline__ void tm_dealloc_512(std::uint32_t base) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" : : "r"(base) : "memory");
+}
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// generic SELL row from TMEM-held weight pairs (w: [pair][lo x, hi x, lo y,
+// hi y]) and column pairs: gen_gather's products and sums in its order
+template <int NP>
+__device__ __forceinline__ double gen_gather_r(const double* __restrict__ sd, int cur, const std::uint32_t (&w)[16],
+                                               const std::uint32_t (&c)[4]) {
+    double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+    for (int p = NP - 1; p >= 0; --p) {
+        const double wx = __hiloint2double(static_cast<int>(w[4 * p + 1]), static_cast<int>(w[4 * p]));
+        const double wy = __hiloint2double(static_cast<int>(w[4 * p + 3]), static_cast<int>(w[4 * p + 2]));
+        acc2 += wy * sd[cur + (c[p] >> 16)];
+        acc += wx * sd[cur + (c[p] & 0xffffu)];
+    }
+    return acc + acc2;
+}
+
+// warp-uniform width wd; TMEM columns tw (weights) and tc (column pairs)
+__device__ __forceinline__ double gen_gather_tm(int wd, const double* __restrict__ sd, int cur, std::uint32_t tw,
+                                                std::uint32_t tc) {
+    if (wd == 0) return 0.0;
+    std::uint32_t w[16], c[4];
+    tm_ld16_4(tw, w, tc, c);
+    switch (wd) {
+        case 8: return gen_gather_r<4>(sd, cur, w, c);
+        case 6: return gen_gather_r<3>(sd, cur, w, c);
+        case 4: return gen_gather_r<2>(sd, cur, w, c);
+        case 2: return gen_gather_r<1>(sd, cur, w, c);
+        default: return 0.0;
+    }
+}
+
 // g = A z_n on a generic R row of the fused solve: the row's A P part is the
 // SELL gather on v = z / sqrt(M) (published to v0 by every R row's owner),
 // the entries with columns outside P come from the small remainder table
@@ -1648,9 +1869,25 @@ __device__ __forceinline__ double gen_full_row(const LatSolveArgs& A, const doub
         rem += (cl[__ldg(A.rem_cell + t)] * __ldg(A.rem_a0 + t)) * zn[__ldg(A.rem_col + t)];
     return gen_gather_w(gwid, sd, ogw, ov, gcol, gslot) + rem;
 }
+// TMEM form: the gather is warp-collective (tcgen05.ld), so every lane of
+// the warp calls it; the remainder only for lanes holding a row (live)
+__device__ __forceinline__ double gen_full_row_tm(const LatSolveArgs& A, const double* sd, int ov, std::uint32_t tw,
+                                                  std::uint32_t tc, int gwid, int q, bool live, const double* zn,
+                                                  const double* cl) {
+    const double gath = gen_gather_tm(gwid, sd, ov, tw, tc);
+    double rem = 0.0;
+    if (live)
+        for (int t = __ldg(A.rem_ptr + q); t < __ldg(A.rem_ptr + q + 1); ++t)
+            rem += (cl[__ldg(A.rem_cell + t)] * __ldg(A.rem_a0 + t)) * zn[__ldg(A.rem_col + t)];
+    return gath + rem;
+}
 
-template <int T, int K, int G>
+// TM: generic weights / columns and the lattice nodes' d_{m-1} in tensor
+// memory (see tm_ld16); otherwise weights and columns in shared memory and
+// d_{m-1} read back from the buffer the substep overwrites.
+template <int T, int K, int G, bool TM>
 __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
+    static_assert(!TM || (T == 512 && 20 * G + 4 * K <= 128), "TMEM columns per thread");
     extern __shared__ __align__(16) double sd[];
     const LatArgs& a = A.lat;
     const LatSolveOff o = lat_solve_offsets(A);
@@ -1669,9 +1906,26 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
     const double inv_h = a.inv_h;
     const double hh = 1.0 / inv_h;
     __shared__ int fail_step;
+    __shared__ std::uint32_t tm_slot;
+
+    // tensor memory: the whole 512 columns (one CTA per SM); this thread's
+    // columns: weights of generic role u at 16 u, its column pairs at
+    // 20 G + 4 u... see tw_/tc_/tv_ below
+    if (TM) {
+        if ((tid >> 5) == 0) tm_alloc_512(&tm_slot);
+        tm_fence_before();
+        __syncthreads();
+        tm_fence_after();
+    }
+    const std::uint32_t tbase =
+        TM ? tm_slot + (static_cast<std::uint32_t>(32 * ((tid >> 5) & 3)) << 16) + 128u * ((tid >> 5) >> 2) : 0u;
+    auto tw_ = [&](int u) { return tbase + 16u * u; };            // 16 columns: 4 weight pairs
+    auto tc_ = [&](int u) { return tbase + 16u * G + 4u * u; };   // 4 columns: column pairs
+    auto tv_ = [&](int set) { return tbase + 20u * G + 2u * K * set; };  // 2 K columns: v_{m-1}
 
     // static tables, once per CTA
-    for (int i = tid; i < a.n_slots; i += T) gcol[i] = __ldg(a.gen_col + i);
+    if (!TM)
+        for (int i = tid; i < a.n_slots; i += T) gcol[i] = __ldg(a.gen_col + i);
     for (int i = tid; i < a.n_strips; i += T) {
         sj0[i] = __ldg(a.strip_j0 + i);
         slen[i] = __ldg(a.strip_len + i);
@@ -1725,7 +1979,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
         }
         if (tid == 0) fail_step = INT_MAX;
         __syncthreads();
-        for (int e = tid; e < a.n_slots; e += T) {
+        auto slot_weight = [&](int e) {
             const unsigned c = __ldg(a.slot_cell + e);
             double w;
             if (!(c & kOvfFlag)) {
@@ -1736,7 +1990,35 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 for (int t = __ldg(a.ovf_start + k); t < __ldg(a.ovf_start + k + 1); ++t)
                     w += cl[__ldg(a.ovf_cell + t)] * __ldg(a.ovf_a0 + t);
             }
-            sd[o.gw + e] = w;
+            return w;
+        };
+        if (TM) {
+            // each thread forms its own generic rows' weights straight into
+            // its TMEM columns (pairs p < width / 2; the rest zero)
+            __syncthreads();  // cl complete
+            const unsigned* gc2 = reinterpret_cast<const unsigned*>(a.gen_col);
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                std::uint32_t wr[16], cr[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    double w0 = 0.0, w1 = 0.0;
+                    cr[p] = 0u;
+                    if (2 * p < gwid[u]) {
+                        w0 = slot_weight(gslot[u] + 64 * p);
+                        w1 = slot_weight(gslot[u] + 64 * p + 1);
+                        cr[p] = __ldg(gc2 + ((gslot[u] + 64 * p) >> 1));
+                    }
+                    wr[4 * p] = static_cast<std::uint32_t>(__double2loint(w0));
+                    wr[4 * p + 1] = static_cast<std::uint32_t>(__double2hiint(w0));
+                    wr[4 * p + 2] = static_cast<std::uint32_t>(__double2loint(w1));
+                    wr[4 * p + 3] = static_cast<std::uint32_t>(__double2hiint(w1));
+                }
+                tm_st16(tw_(u), wr);
+                tm_st4(tc_(u), cr);
+            }
+        } else {
+            for (int e = tid; e < a.n_slots; e += T) sd[o.gw + e] = slot_weight(e);
         }
         double kE = 0, kW = 0, kNS = 0, dg = 0;
         if (lat_on) {
@@ -1762,9 +2044,13 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 ggg[u] = 0.0;
+                const double gt =
+                    TM ? gen_full_row_tm(A, sd, o.v0, tw_(u), tc_(u), gwid[u], gq[u], grow[u] >= 0, zn, cl) : 0.0;
                 if (grow[u] >= 0) {
-                    ggg[u] = zn[grow[u]] + fi * (0.0 - gen_full_row(A, sd, o.gw, o.v0, gcol, gslot[u], gwid[u], gq[u],
-                                                                     zn, cl));
+                    ggg[u] = zn[grow[u]] +
+                             fi * (0.0 - (TM ? gt
+                                             : gen_full_row(A, sd, o.gw, o.v0, gcol, gslot[u], gwid[u], gq[u], zn,
+                                                            cl)));
                     if (!(fabs(ggg[u]) <= 1e100)) atomicMin(&fail_step, 1);
                 }
             }
@@ -1794,7 +2080,14 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
             lat_solve_g<K, G>(sd, o.v0, zn, base, len, W, sS, sN, inv_h, kE, kW, kNS, dg, grow, grs, gg);
 #pragma unroll
             for (int u = 0; u < G; ++u)
-                ggg[u] = grow[u] >= 0 ? gen_full_row(A, sd, o.gw, o.v0, gcol, gslot[u], gwid[u], gq[u], zn, cl) : 0.0;
+                if (TM) {
+                    const double gt =
+                        gen_full_row_tm(A, sd, o.v0, tw_(u), tc_(u), gwid[u], gq[u], grow[u] >= 0, zn, cl);
+                    ggg[u] = grow[u] >= 0 ? gt : 0.0;
+                } else {
+                    ggg[u] = grow[u] >= 0 ? gen_full_row(A, sd, o.gw, o.v0, gcol, gslot[u], gwid[u], gq[u], zn, cl)
+                                          : 0.0;
+                }
             // four rows per pass, every load before any store (z_{n-1} may
             // live in global memory: its latency overlaps instead of chaining)
             for (int i0 = nr + tid; i0 < A.n; i0 += 4 * T) {
@@ -1850,7 +2143,27 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 double gaq[G];
 #pragma unroll
                 for (int u = 0; u < G; ++u) {
-                    gaq[u] = gen_gather_w(gwid[u], sd, o.gw, cur, gcol, gslot[u]);
+                    gaq[u] = TM ? gen_gather_tm(gwid[u], sd, cur, tw_(u), tc_(u))
+                                : gen_gather_w(gwid[u], sd, o.gw, cur, gcol, gslot[u]);
+                }
+                // TMEM: v_m of the thread's nodes parked for substep m + 1,
+                // v_{m-1} back from the other set
+                std::uint32_t vp[2 * K];
+                if (TM) {
+                    if (m < a.p - 1) {
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            vp[2 * k] = static_cast<std::uint32_t>(__double2loint(d[k]));
+                            vp[2 * k + 1] = static_cast<std::uint32_t>(__double2hiint(d[k]));
+                        }
+                        tm_st16(tv_(m & 1), vp);
+                    }
+                    if (m >= 2) {
+                        tm_ld16(tv_((m - 1) & 1), vp);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 2 * K; ++k) vp[k] = 0u;
+                    }
                 }
                 const int ce = cur + base + W, cw_ = cur + base - W;
                 const double vnl = sd[cur + sN];
@@ -1861,7 +2174,8 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     const double ve = sd[ce + k], vw = sd[cw_ + k];
                     const double vn = (k + 1 < len) ? d[k + 1] : vnl;
                     const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
-                    const double vpk = m == 1 ? 0.0 : sd[nxt + base + k];
+                    const double vpk = TM ? __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]))
+                                          : (m == 1 ? 0.0 : sd[nxt + base + k]);
                     const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
                     d[k] = next;
                     if (k < len) sd[nxt + base + k] = next;
@@ -1915,6 +2229,12 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
         }
         if (tid == 0) A.fail[s] = fail_step;
         __syncthreads();
+    }
+    if (TM) {
+        tm_fence_before();
+        __syncthreads();
+        tm_fence_after();
+        if ((tid >> 5) == 0) tm_dealloc_512(tm_slot);
     }
 }
 
@@ -2047,12 +2367,29 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
         const char* v = std::getenv("WMC_SWEEP_ONE_ROW");  // tuning knob: one row per warp
         return v ? std::atoi(v) : 0;
     }();
+    static const int ahead = [] {
+        const char* v = std::getenv("WMC_SWEEP_AHEAD");  // tuning knob: 10 R + MINB of the load-first sweep (0: off)
+        return v ? std::atoi(v) : 0;
+    }();
     if (a.cell_ix) {  // cells in a separate per-entry array (narrow-channel levels)
         sweep_kernel<false, false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     } else if (parts) {
         sweep_kernel<false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     } else if (one_row || !a.row_desc) {
         sweep_kernel<false, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    } else if (ahead) {
+        // load-first sweep: ahead = 10 R + MINB
+        const int r = ahead / 10;
+        const unsigned g2 = ((a.n + kSweepWarps * r - 1) / (kSweepWarps * r)) * (a.S / kSweepChunk);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        switch (ahead) {
+            case 22: sweep_ahead_kernel<2, 2><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
+            case 23: sweep_ahead_kernel<2, 3><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
+            case 24: sweep_ahead_kernel<2, 4><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
+            case 42: sweep_ahead_kernel<4, 2><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
+            case 43: sweep_ahead_kernel<4, 3><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
+            default: sweep_ahead_kernel<1, 4><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
+        }
     } else {
         static const int r = [] {
             const char* v = std::getenv("WMC_SWEEP_ROWS");  // tuning knob: rows per warp (2, 4, 8)
@@ -2217,28 +2554,32 @@ int lattice_solve_max_smem(int device) {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, lattice_solve_kernel<512, 8, 2>) != cudaSuccess) return 0;
+    if (cudaFuncGetAttributes(&fa, lattice_solve_kernel<512, 8, 2, false>) != cudaSuccess) return 0;
+    cudaFuncAttributes fb{};
+    if (cudaFuncGetAttributes(&fb, lattice_solve_kernel<512, 8, 2, true>) != cudaSuccess) return 0;
+    if (fb.sharedSizeBytes > fa.sharedSizeBytes) fa.sharedSizeBytes = fb.sharedSizeBytes;
     return optin - static_cast<int>(fa.sharedSizeBytes);
 }
 
-template <int T, int K, int G>
+template <int T, int K, int G, bool TM>
 static int launch_lat_solve(const LatSolveArgs& a, int grid, cudaStream_t st) {
     static int configured = -1;
     if (configured < 0) {
         int device = 0;
         cudaGetDevice(&device);
-        configured = static_cast<int>(cudaFuncSetAttribute(lattice_solve_kernel<T, K, G>,
+        configured = static_cast<int>(cudaFuncSetAttribute(lattice_solve_kernel<T, K, G, TM>,
                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            lattice_solve_max_smem(device)));
     }
     if (configured != 0) return configured;
-    lattice_solve_kernel<T, K, G><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
+    lattice_solve_kernel<T, K, G, TM><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
 
 int launch_lattice_solve(const LatSolveArgs& a, int grid, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (a.lat.threads == 512 && a.lat.strip_k == 8) return launch_lat_solve<512, 8, 2>(a, grid, st);
+    if (a.lat.threads == 512 && a.lat.strip_k == 8)
+        return a.tmem ? launch_lat_solve<512, 8, 2, true>(a, grid, st) : launch_lat_solve<512, 8, 2, false>(a, grid, st);
     return static_cast<int>(cudaErrorInvalidValue);
 }
 

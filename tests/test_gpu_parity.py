@@ -282,6 +282,24 @@ def test_fused_lattice_solve_matches_the_step_kernels(lvl, monkeypatch):
     assert np.max(np.abs(dq_f - dq_p) / np.abs(qf_p)) < 1e-12
 
 
+@pytest.mark.parametrize("lvl", [0, 1])
+def test_fused_solve_tensor_memory_is_bitwise_the_shared_memory_form(lvl, monkeypatch):
+    """The fused solve keeps each thread's generic SELL weights / columns and
+    its lattice nodes' d_{m-1} in tensor memory (tcgen05.ld / st) instead of
+    shared memory: the same products in the same order, so the same bits
+    (coupled pairs, level-1 pairs include a level-0 coarse solve)."""
+    defs = configs.config1()
+    a = [configs.build_level(d) for d in defs[max(lvl - 1, 0):lvl + 1]]
+    monkeypatch.setenv("WMC_FUSED_TMEM", "0")
+    b = [configs.build_level(d) for d in defs[max(lvl - 1, 0):lvl + 1]]
+    monkeypatch.delenv("WMC_FUSED_TMEM")
+    assert a[-1].info["fused"] == b[-1].info["fused"] == 1
+    pair = (lambda lv: (lv[-1], lv[0] if lvl else None))
+    dq_a, qa, _ = wavemc.eval_pairs(*pair(a), 0, lvl, 3, 400)
+    dq_b, qb, _ = wavemc.eval_pairs(*pair(b), 0, lvl, 3, 400)
+    assert np.array_equal(qa, qb) and np.array_equal(dq_a, dq_b)
+
+
 def test_fused_lattice_solve_with_global_history(monkeypatch):
     """z_{n-1} in the per-sample global buffer instead of shared memory (the
     layout levels with larger n take) gives the same bits."""
