@@ -1768,7 +1768,7 @@ __device__ __forceinline__ void lat_solve_g(double* sd, int ov, const double* zn
 // TMEM (256 KB per SM, 128 lanes x 512 columns of 32 bits) is read by
 // tcgen05.ld on its own datapath: measured on this B200 at ~390 B/clk/SM
 // beside an unchanged 128 B/clk of shared-memory LDS.128 traffic
-// (tune/tmem_bench.cu), so what a thread alone reads every substep -- its
+// (tools/tmem_bench.cu), so what a thread alone reads every substep -- its
 // generic rows' SELL weights and columns, and d_{m-1} of its lattice nodes --
 // moves out of the shared-memory pipe the kernel is bound by.  Warp w owns
 // lanes 32 (w % 4) .. + 31 (its sub-partition's lane quarter) and columns
