@@ -5,6 +5,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -2165,6 +2166,45 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                         for (int k = 0; k < 2 * K; ++k) vp[k] = 0u;
                     }
                 }
+                if (TM) {
+                    // strip length known at compile time for full (K) and
+                    // one-short (K - 1) strips -- warp-uniform, a strip's
+                    // lanes (its shadow lane included) share one warp -- so
+                    // no per-node length tests; the shared-memory rows as
+                    // pointers (immediate offsets per node)
+                    const double* vc = sd + cur + base;
+                    double* vx = sd + nxt + base;
+                    const double* vE = vc + W;
+                    const double* vW = vc - W;
+                    const double vnl = vc[span];
+                    const double vs0 = vc[-1];
+                    auto nodes = [&](auto nvc) {
+                        constexpr int NV = decltype(nvc)::value;  // 0: runtime length
+                        double vs = vs0;
+                        double vk = d[0];
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            if (NV && k >= NV) break;
+                            const bool has_n = NV ? (k + 1 < NV) : (k + 1 < span);
+                            const double ve = vE[k], vw = vW[k];
+                            const double vn = has_n ? d[k + 1] : vnl;
+                            const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
+                            const double vpk =
+                                __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]));
+                            const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
+                            d[k] = next;
+                            if (lat_on && (NV || k < len)) vx[k] = next;
+                            vs = vk;
+                            vk = vn;
+                        }
+                    };
+                    if (span == K)
+                        nodes(std::integral_constant<int, K>{});
+                    else if (span == K - 1)
+                        nodes(std::integral_constant<int, K - 1>{});
+                    else
+                        nodes(std::integral_constant<int, 0>{});
+                } else {
                 const int ce = cur + base + W, cw_ = cur + base - W;
                 const double vnl = sd[cur + sN];
                 double vs = sd[cur + sS];
@@ -2174,13 +2214,13 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     const double ve = sd[ce + k], vw = sd[cw_ + k];
                     const double vn = (k + 1 < len) ? d[k + 1] : vnl;
                     const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
-                    const double vpk = TM ? __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]))
-                                          : (m == 1 ? 0.0 : sd[nxt + base + k]);
+                    const double vpk = m == 1 ? 0.0 : sd[nxt + base + k];
                     const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
                     d[k] = next;
                     if (k < len) sd[nxt + base + k] = next;
                     vs = vk;
                     vk = vn;
+                }
                 }
 #pragma unroll
                 for (int u = 0; u < G; ++u) {
