@@ -181,11 +181,17 @@ std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const
                 ++j;
                 continue;
             }
+            // a run of lattice rows, cut into the fewest strips of <= K rows,
+            // lengths balanced (31 rows: 8 8 8 7 at K = 8)
             int e = j;
-            while (e <= m - 1 && lat_row[e] && e - j < var[1]) ++e;
-            j0s.push_back(j);
-            lens.push_back(e - j);
-            j = e;
+            while (e <= m - 1 && lat_row[e]) ++e;
+            const int run = e - j, ns = (run + var[1] - 1) / var[1];
+            for (int q = 0; q < ns; ++q) {
+                const int l = run / ns + (q < run % ns ? 1 : 0);
+                j0s.push_back(j);
+                lens.push_back(l);
+                j += l;
+            }
         }
         if (static_cast<int>(j0s.size()) * cw <= var[0]) {
             threads = var[0];

@@ -567,126 +567,154 @@ __global__ void __launch_bounds__(kSweepWarps * 32, WMC_SWEEP_MINB) sweep_rows_k
     }
 }
 
-// K1, load-first form: the warp's R row descriptors are loaded together,
-// then every HBM value of its structured rows (z_{i+1}, z_{i-dS}, z_{i+dN},
-// z_{n-1}) before the first product or store, so one warp keeps 4 R x 512 B
-// in flight instead of one row's chain (descriptor -> values -> store) at a
-// time.  Same products and sums in the same order as sweep_rows_kernel:
-// bit-identical results.  MINB trades registers for resident warps.
+// K1, wide form (fixed dt, S a multiple of 128): four samples per lane with
+// 256-bit loads and stores (LDG/STG.E.ENL2.256), 128 samples per warp, so
+// each load instruction moves 1 KB per warp and a warp's rows keep twice the
+// bytes in flight of sweep_rows_kernel for the same instruction count.  Same
+// per-sample products and sums in the same order: bit-identical.
+struct D4 {
+    double x, y, z, w;
+};
+__device__ __forceinline__ D4 ld4_nc(const double* p) {
+    D4 r;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ D4 ld4(const double* p) {
+    D4 r;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st4(double* p, const D4& v) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+constexpr int kSweepChunkW = 128;  // samples per warp of the wide sweep
+
 template <int R, int MINB>
-__global__ void __launch_bounds__(kSweepWarps * 32, MINB) sweep_ahead_kernel(SweepArgs a) {
-    __shared__ double2 tile[kSweepWarps * R][32];  // g of the block's R rows: [row][lane]
+__global__ void __launch_bounds__(kSweepWarps * 32, MINB) sweep_wide_kernel(SweepArgs a) {
+    __shared__ D4 tile[kSweepWarps * R][32];  // g of the block's R rows: [row][lane] = samples 4 lane .. 4 lane + 3
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int groups = (a.n + kSweepWarps * R - 1) / (kSweepWarps * R);
     const int row0 = (blockIdx.x % groups) * kSweepWarps * R;
     const int chunk = blockIdx.x / groups;
-    const int s0 = chunk * kSweepChunk + 2 * lane;
+    const int s0 = chunk * kSweepChunkW + 4 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
     const int first = row0 + warp * R;
-    auto zrow = [&](int r) {
-        return __ldg(reinterpret_cast<const double2*>(a.zc + static_cast<std::size_t>(r) * S + s0));
-    };
-    const double2 zero = make_double2(0.0, 0.0);
-    int4 d[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-        d[k] = first + k < a.n ? __ldg(a.row_desc + first + k) : make_int4(-1, 0, 0, 0);
-    double2 zprev = zero, zcur = zero;
+    auto zrow = [&](int r) { return ld4_nc(a.zc + static_cast<std::size_t>(r) * S + s0); };
+    const D4 zero{0.0, 0.0, 0.0, 0.0};
+    D4 zprev = zero, zcur = zero;
     if (first < a.n) {
         if (first > 0) zprev = zrow(first - 1);
         zcur = zrow(first);
     }
-    double2 zx[R], zs[R], zn[R], zm[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-        const int row = first + k;
-        const bool st = row < a.n && d[k].x >= 0 && ((d[k].x >> 16) & 0xff) > 0;
-        zx[k] = row + 1 < a.n ? zrow(row + 1) : zero;
-        zm[k] = row < a.n && row >= a.split
-                    ? *reinterpret_cast<const double2*>(a.zp + static_cast<std::size_t>(row) * S + s0)
-                    : zero;
-        zs[k] = st ? zrow(row - d[k].z) : zero;
-        zn[k] = st ? zrow(row + d[k].w) : zero;
-    }
-    const double2 fac = a.rel ? lane_rel(a.rel, s0) : make_double2(1.0, 1.0);
-    const double2 factor = make_double2(a.factor * fac.x, a.factor * fac.y);
-    const int2 live = lane_live(a.nsteps, s0, a.step);
+    int ccell = -1;
+    D4 c = zero;
+    const double f = a.factor;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
         const int row = first + k;
         if (row >= a.n) break;
         const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
-        double acc0 = 0.0, acc1 = 0.0;
-        if (d[k].x >= 0 && ((d[k].x >> 16) & 0xff) > 0) {
-            const double2 w = __ldg(a.wtype + ((d[k].x >> 16) & 0xff) - 1);
-            const double2 c = __ldg(reinterpret_cast<const double2*>(a.cells + (d[k].x & 0xffff) * S + s0));
-            double p0 = 0.0, p1 = 0.0;
-            p0 += w.x * zs[k].x;
-            p1 += w.x * zs[k].y;
-            p0 += w.x * zprev.x;
-            p1 += w.x * zprev.y;
-            p0 += w.y * zcur.x;
-            p1 += w.y * zcur.y;
-            p0 += w.x * zx[k].x;
-            p1 += w.x * zx[k].y;
-            p0 += w.x * zn[k].x;
-            p1 += w.x * zn[k].y;
-            acc0 = c.x * p0;
-            acc1 = c.y * p1;
+        D4 zm = zero;
+        if (row >= a.split) zm = ld4(a.zp + idx);
+        const D4 znext = row + 1 < a.n ? zrow(row + 1) : zero;
+        const int4 d = __ldg(a.row_desc + row);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (d.x >= 0 && ((d.x >> 16) & 0xff) > 0) {
+            const double2 w = __ldg(a.wtype + ((d.x >> 16) & 0xff) - 1);
+            if ((d.x & 0xffff) != ccell) {
+                ccell = d.x & 0xffff;
+                c = ld4_nc(a.cells + ccell * S + s0);
+            }
+            const D4 zs = zrow(row - d.z);
+            const D4 zn = zrow(row + d.w);
+            const double* ps = &zs.x;
+            const double* pw = &zprev.x;
+            const double* pc = &zcur.x;
+            const double* pe = &znext.x;
+            const double* pn = &zn.x;
+            const double* cc = &c.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double p0 = 0.0;
+                p0 += w.x * ps[q];
+                p0 += w.x * pw[q];
+                p0 += w.y * pc[q];
+                p0 += w.x * pe[q];
+                p0 += w.x * pn[q];
+                acc[q] = cc[q] * p0;
+            }
         } else {
-            const int b = d[k].y, e = __ldg(a.row_ptr + row + 1);
-            if (d[k].x >= 0) {
-                const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + (d[k].x & 0xffff) * S + s0));
-                double p0 = 0.0, p1 = 0.0;
-#pragma unroll 4
+            const int b = d.y, e = __ldg(a.row_ptr + row + 1);
+            if (d.x >= 0) {
+                const D4 c1 = ld4_nc(a.cells + (d.x & 0xffff) * S + s0);
+                double p[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
                 for (int q = b; q < e; ++q) {
                     const int j = __ldg(a.ent + q) & a.col_mask;
                     const double w = __ldg(a.a0 + q);
-                    const double2 z = zrow(j);
-                    p0 += w * z.x;
-                    p1 += w * z.y;
+                    const D4 z = zrow(j);
+                    p[0] += w * z.x;
+                    p[1] += w * z.y;
+                    p[2] += w * z.z;
+                    p[3] += w * z.w;
                 }
-                acc0 = cc.x * p0;
-                acc1 = cc.y * p1;
+                acc[0] = c1.x * p[0];
+                acc[1] = c1.y * p[1];
+                acc[2] = c1.z * p[2];
+                acc[3] = c1.w * p[3];
             } else {
-#pragma unroll 4
+#pragma unroll 2
                 for (int q = b; q < e; ++q) {
                     const int pk = __ldg(a.ent + q);
                     const double w = __ldg(a.a0 + q);
                     const int j = pk & a.col_mask;
                     const int cell = ent_cell(nullptr, q, pk, a.col_bits);
-                    const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
-                    const double2 z = zrow(j);
-                    acc0 += (cc.x * w) * z.x;
-                    acc1 += (cc.y * w) * z.y;
+                    const D4 c1 = ld4_nc(a.cells + cell * S + s0);
+                    const D4 z = zrow(j);
+                    acc[0] += (c1.x * w) * z.x;
+                    acc[1] += (c1.y * w) * z.y;
+                    acc[2] += (c1.z * w) * z.z;
+                    acc[3] += (c1.w * w) * z.w;
                 }
             }
         }
         if (row < a.split) {
+            const D4 g{acc[0], acc[1], acc[2], acc[3]};
             if (a.g_node_major)
-                *reinterpret_cast<double2*>(a.g + idx) = make_double2(acc0, acc1);
+                st4(a.g + idx, g);
             else
-                tile[warp * R + k][lane] = make_double2(acc0, acc1);
+                tile[warp * R + k][lane] = g;
         } else {
-            double2 out;
-            out.x = 2.0 * zcur.x - zm[k].x - factor.x * acc0;
-            out.y = 2.0 * zcur.y - zm[k].y - factor.y * acc1;
-            store_z(a.zp + idx, out, live, a.fail, s0, a.count, a.step);
+            D4 out;
+            out.x = 2.0 * zcur.x - zm.x - f * acc[0];
+            out.y = 2.0 * zcur.y - zm.y - f * acc[1];
+            out.z = 2.0 * zcur.z - zm.z - f * acc[2];
+            out.w = 2.0 * zcur.w - zm.w - f * acc[3];
+            st4(a.zp + idx, out);
+            // check_finite (integrators.cpp:12-18)
+            if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
+            if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+            if (!(fabs(out.z) <= 1e100)) flag_fail(a.fail, s0 + 2, a.count, a.step);
+            if (!(fabs(out.w) <= 1e100)) flag_fail(a.fail, s0 + 3, a.count, a.step);
         }
         zprev = zcur;
-        zcur = zx[k];
+        zcur = znext;
     }
     if (row0 >= a.split || a.g_node_major) return;  // block-uniform
+    // the block's g rows sample-major: 128 samples x (kSweepWarps R) rows,
+    // thread -> sample tid / 2, half the rows each
     __syncthreads();
-    constexpr int kRowsPerThread = kSweepWarps * R * kSweepChunk / (kSweepWarps * 32);
-    const int sl = threadIdx.x / (kSweepWarps * R / kRowsPerThread);
-    const int r0 = (threadIdx.x % (kSweepWarps * R / kRowsPerThread)) * kRowsPerThread;
-    const int s = chunk * kSweepChunk + sl;
+    constexpr int kRows = kSweepWarps * R, kTpS = kSweepWarps * 32 / kSweepChunkW, kRpt = kRows / kTpS;
+    const int sl = threadIdx.x / kTpS;
+    const int r0 = (threadIdx.x % kTpS) * kRpt;
+    const int s = chunk * kSweepChunkW + sl;
     double* dst = a.g + static_cast<std::size_t>(s) * a.g_stride + row0 + r0;
 #pragma unroll
-    for (int q = 0; q < kRowsPerThread; q += 2) {
-        const double2 t0 = tile[r0 + q][sl >> 1], t1 = tile[r0 + q + 1][sl >> 1];
-        const double g0 = (sl & 1) ? t0.y : t0.x, g1 = (sl & 1) ? t1.y : t1.x;
+    for (int q = 0; q < kRpt; q += 2) {
+        const double* t0 = &tile[r0 + q][sl >> 2].x;
+        const double* t1 = &tile[r0 + q + 1][sl >> 2].x;
+        const double g0 = t0[sl & 3], g1 = t1[sl & 3];
         if (row0 + r0 + q + 1 < a.split)
             *reinterpret_cast<double2*>(dst + q) = make_double2(g0, g1);
         else if (row0 + r0 + q < a.split)
@@ -1814,6 +1842,55 @@ __device__ __forceinline__ void tm_st4(std::uint32_t addr, const std::uint32_t (
         : "r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
         : "memory");
 }
+// N-column forms (N = 2 K for the d_{m-1} columns): x16 / x4 / x2 chunks,
+// each with its own wait
+__device__ __forceinline__ void tm_ld2(std::uint32_t addr, std::uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(r[0]), "=r"(r[1])
+                 : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld4p(std::uint32_t addr, std::uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_st2(std::uint32_t addr, const std::uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};\n"
+                 "tcgen05.wait::st.sync.aligned;\n"
+                 :
+                 : "r"(addr), "r"(r[0]), "r"(r[1])
+                 : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tm_ldn(std::uint32_t addr, std::uint32_t (&r)[N]) {
+    static_assert(N % 2 == 0, "even column count");
+    int c = 0;
+    if constexpr (N >= 16) {
+        tm_ld16(addr, *reinterpret_cast<std::uint32_t(*)[16]>(r));
+        c = 16;
+    }
+#pragma unroll
+    for (; c + 4 <= N; c += 4) tm_ld4p(addr + c, r + c);
+#pragma unroll
+    for (; c + 2 <= N; c += 2) tm_ld2(addr + c, r + c);
+}
+template <int N>
+__device__ __forceinline__ void tm_stn(std::uint32_t addr, const std::uint32_t (&r)[N]) {
+    static_assert(N % 2 == 0, "even column count");
+    int c = 0;
+    if constexpr (N >= 16) {
+        tm_st16(addr, *reinterpret_cast<const std::uint32_t(*)[16]>(r));
+        c = 16;
+    }
+#pragma unroll
+    for (; c + 4 <= N; c += 4) tm_st4(addr + c, *reinterpret_cast<const std::uint32_t(*)[4]>(r + c));
+#pragma unroll
+    for (; c + 2 <= N; c += 2) tm_st2(addr + c, r + c);
+}
 __device__ __forceinline__ std::uint32_t tm_alloc_512(std::uint32_t* slot) {  // whole warp; one CTA per SM
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
                  "tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n"
@@ -1888,7 +1965,7 @@ __device__ __forceinline__ double gen_full_row_tm(const LatSolveArgs& A, const d
 // d_{m-1} read back from the buffer the substep overwrites.
 template <int T, int K, int G, bool TM>
 __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
-    static_assert(!TM || (T == 512 && 20 * G + 4 * K <= 128), "TMEM columns per thread");
+    static_assert(!TM || (T % 128 == 0 && T <= 512 && 20 * G + 4 * K <= 128), "TMEM columns per thread");
     extern __shared__ __align__(16) double sd[];
     const LatArgs& a = A.lat;
     const LatSolveOff o = lat_solve_offsets(A);
@@ -2157,10 +2234,10 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                             vp[2 * k] = static_cast<std::uint32_t>(__double2loint(d[k]));
                             vp[2 * k + 1] = static_cast<std::uint32_t>(__double2hiint(d[k]));
                         }
-                        tm_st16(tv_(m & 1), vp);
+                        tm_stn<2 * K>(tv_(m & 1), vp);
                     }
                     if (m >= 2) {
-                        tm_ld16(tv_((m - 1) & 1), vp);
+                        tm_ldn<2 * K>(tv_((m - 1) & 1), vp);
                     } else {
 #pragma unroll
                         for (int k = 0; k < 2 * K; ++k) vp[k] = 0u;
@@ -2407,9 +2484,9 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
         const char* v = std::getenv("WMC_SWEEP_ONE_ROW");  // tuning knob: one row per warp
         return v ? std::atoi(v) : 0;
     }();
-    static const int ahead = [] {
-        const char* v = std::getenv("WMC_SWEEP_AHEAD");  // tuning knob: 10 R + MINB of the load-first sweep (0: off)
-        return v ? std::atoi(v) : 0;
+    static const int wide = [] {
+        const char* v = std::getenv("WMC_SWEEP_WIDE");  // 10 R + MINB of the 256-bit sweep (0: off)
+        return v ? std::atoi(v) : 23;
     }();
     if (a.cell_ix) {  // cells in a separate per-entry array (narrow-channel levels)
         sweep_kernel<false, false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
@@ -2417,19 +2494,15 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
         sweep_kernel<false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     } else if (one_row || !a.row_desc) {
         sweep_kernel<false, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
-    } else if (ahead) {
-        // load-first sweep: ahead = 10 R + MINB
-        const int r = ahead / 10;
-        const unsigned g2 = ((a.n + kSweepWarps * r - 1) / (kSweepWarps * r)) * (a.S / kSweepChunk);
+    } else if (wide && !a.rel && !a.nsteps && a.S % kSweepChunkW == 0) {
+        // wide sweep (default for fixed dt): wide = 10 R + MINB
+        const int r = wide / 10;
+        const unsigned g2 = ((a.n + kSweepWarps * r - 1) / (kSweepWarps * r)) * (a.S / kSweepChunkW);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
-        switch (ahead) {
-            case 22: sweep_ahead_kernel<2, 2><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
-            case 23: sweep_ahead_kernel<2, 3><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
-            case 24: sweep_ahead_kernel<2, 4><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
-            case 42: sweep_ahead_kernel<4, 2><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
-            case 43: sweep_ahead_kernel<4, 3><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
-            default: sweep_ahead_kernel<1, 4><<<g2, kSweepWarps * 32, 0, st>>>(a); break;
-        }
+        if (wide == 14)
+            sweep_wide_kernel<1, 4><<<g2, kSweepWarps * 32, 0, st>>>(a);
+        else  // 23 (default; measured: level 4 1.22x, level 3 1.15x over sweep_rows_kernel<2>)
+            sweep_wide_kernel<2, 3><<<g2, kSweepWarps * 32, 0, st>>>(a);
     } else {
         static const int r = [] {
             const char* v = std::getenv("WMC_SWEEP_ROWS");  // tuning knob: rows per warp (2, 4, 8)
