@@ -20,8 +20,9 @@ cap() {  # name regex skip probe-args...
       python tools/kernel_probe.py "$@" > /dev/null 2>&1
 }
 cap fused lattice_solve 0 --level 0 --count 296 --repeat 1
+cap fused2 lattice_solve 0 --level 2 --count 296 --repeat 1
 cap lattice lattice_substep 20 --level 2 --count 1184 --repeat 1
-cap sweep sweep_rows 5 --level 4 --count 1024 --steps 20 --repeat 1
+cap sweep sweep_wide 5 --level 4 --count 1024 --steps 20 --repeat 1
 cap gsub global_substep 10 --square 1024 8 --count 192 --steps 6 --repeat 1
 cap tier tier_stage 30 --config2 --level 4 --count 2048 --steps 10 --repeat 1
 ls -la $out | grep $tag
