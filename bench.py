@@ -572,6 +572,14 @@ def roofline_from_profile(levels, counts, prof, step_ms):
                 "unit": "GB/s", "traffic": t, "traffic_capture": src,
                 "note": ("dominant kernel, HBM-resident substeps (algorithmic bytes); traffic per global step's "
                          "group of substep launches")}
+    elif not sweep_ms and fused_ms:
+        # every level runs the fused on-chip solve (e.g. config 0): no HBM
+        # stream per step; report its SURVEY 8(d) HBM-equivalent rate
+        roof = {"bound": "hbm", "kernel": "fused_solve", "achieved": kernels["fused_solve"]["hbm_equivalent_GBps"],
+                "unit": "GB/s", "traffic": None, "traffic_capture": None,
+                "note": ("HBM-equivalent rate of the fused lattice solve (24 B per DOF per global step over its "
+                         "time); the state never leaves the SM, the kernel is bound on chip "
+                         "(kernels.fused_solve), so this fraction is not its limiter")}
     else:
         t, src = traffic("sweep", sweep_bytes, kernels["sweep"]["launches"])
         roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",

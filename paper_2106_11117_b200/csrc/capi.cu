@@ -277,8 +277,8 @@ int round64(long v) { return static_cast<int>((v + 63) / 64 * 64); }
 // fused lattice solve: per-thread generic weights and d_{m-1} in tensor
 // memory (default); WMC_FUSED_TMEM=0 keeps them in shared memory
 int fused_tmem() {
-    const char* e = std::getenv("WMC_FUSED_TMEM");
-    return e ? (std::atoi(e) != 0) : 1;
+    const char* e = std::getenv("WMC_FUSED_TMEM");  // 0 off, 1 weights + d_{m-1}, 2 weights only
+    return e ? std::atoi(e) : 1;
 }
 
 // Generic SELL rows of the lattice kernels: lane placement for shared-memory

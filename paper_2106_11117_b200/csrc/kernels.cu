@@ -1963,7 +1963,9 @@ __device__ __forceinline__ double gen_full_row_tm(const LatSolveArgs& A, const d
 // TM: generic weights / columns and the lattice nodes' d_{m-1} in tensor
 // memory (see tm_ld16); otherwise weights and columns in shared memory and
 // d_{m-1} read back from the buffer the substep overwrites.
-template <int T, int K, int G, bool TM>
+// VT (with TM): d_{m-1} of the lattice nodes in TMEM too; otherwise read
+// back from the shared-memory buffer the substep overwrites.
+template <int T, int K, int G, bool TM, bool VT = TM>
 __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
     static_assert(!TM || (T % 128 == 0 && T <= 512 && 20 * G + 4 * K <= 128), "TMEM columns per thread");
     extern __shared__ __align__(16) double sd[];
@@ -2227,7 +2229,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 // TMEM: v_m of the thread's nodes parked for substep m + 1,
                 // v_{m-1} back from the other set
                 std::uint32_t vp[2 * K];
-                if (TM) {
+                if (TM && VT) {
                     if (m < a.p - 1) {
 #pragma unroll
                         for (int k = 0; k < K; ++k) {
@@ -2267,7 +2269,8 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                             const double vn = has_n ? d[k + 1] : vnl;
                             const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
                             const double vpk =
-                                __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]));
+                                VT ? __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]))
+                                   : (m == 1 ? 0.0 : vx[k]);
                             const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
                             d[k] = next;
                             if (lat_on && (NV || k < len)) vx[k] = next;
@@ -2674,25 +2677,27 @@ int lattice_solve_max_smem(int device) {
     return optin - static_cast<int>(fa.sharedSizeBytes);
 }
 
-template <int T, int K, int G, bool TM>
+template <int T, int K, int G, bool TM, bool VT>
 static int launch_lat_solve(const LatSolveArgs& a, int grid, cudaStream_t st) {
     static int configured = -1;
     if (configured < 0) {
         int device = 0;
         cudaGetDevice(&device);
-        configured = static_cast<int>(cudaFuncSetAttribute(lattice_solve_kernel<T, K, G, TM>,
+        configured = static_cast<int>(cudaFuncSetAttribute(lattice_solve_kernel<T, K, G, TM, VT>,
                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            lattice_solve_max_smem(device)));
     }
     if (configured != 0) return configured;
-    lattice_solve_kernel<T, K, G, TM><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
+    lattice_solve_kernel<T, K, G, TM, VT><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
 
 int launch_lattice_solve(const LatSolveArgs& a, int grid, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (a.lat.threads == 512 && a.lat.strip_k == 8)
-        return a.tmem ? launch_lat_solve<512, 8, 2, true>(a, grid, st) : launch_lat_solve<512, 8, 2, false>(a, grid, st);
+        return a.tmem == 2 ? launch_lat_solve<512, 8, 2, true, false>(a, grid, st)
+               : a.tmem    ? launch_lat_solve<512, 8, 2, true, true>(a, grid, st)
+                           : launch_lat_solve<512, 8, 2, false, false>(a, grid, st);
     return static_cast<int>(cudaErrorInvalidValue);
 }
 
