@@ -145,7 +145,7 @@ struct wmc_level {
     int small_smem = 0;  // fused small-mesh solve: shared memory per CTA (0: not eligible)
     int fused_smem = 0;  // fused lattice solve: shared memory per CTA (0: not eligible)
     bool fused_zp_global = false;
-    int fused_tmem = 1;            // fused lattice solve: tensor-memory variant (fixed at level creation)  // fused lattice solve keeps z_{n-1} in a per-sample global buffer
+    int fused_tmem = 2;            // fused lattice solve: tensor-memory form (fixed at level creation)  // fused lattice solve keeps z_{n-1} in a per-sample global buffer
     int n_sms = 148;
     SubPath path = SubPath::None;
     int* d_apg_ptr = nullptr;
@@ -274,11 +274,12 @@ namespace {
 
 int round64(long v) { return static_cast<int>((v + 63) / 64 * 64); }
 
-// fused lattice solve: per-thread generic weights and d_{m-1} in tensor
-// memory (default); WMC_FUSED_TMEM=0 keeps them in shared memory
+// fused lattice solve: per-thread generic SELL weights / columns in tensor
+// memory (2, default; measured best), plus the lattice nodes' d_{m-1} (1),
+// or everything in shared memory (0)
 int fused_tmem() {
-    const char* e = std::getenv("WMC_FUSED_TMEM");  // 0 off, 1 weights + d_{m-1}, 2 weights only
-    return e ? std::atoi(e) : 1;
+    const char* e = std::getenv("WMC_FUSED_TMEM");  // 0 off, 1 weights + d_{m-1}, 2 weights only (default)
+    return e ? std::atoi(e) : 2;
 }
 
 // Generic SELL rows of the lattice kernels: lane placement for shared-memory

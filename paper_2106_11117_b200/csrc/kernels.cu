@@ -2246,44 +2246,40 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     }
                 }
                 if (TM) {
-                    // strip length known at compile time for full (K) and
-                    // one-short (K - 1) strips -- warp-uniform, a strip's
-                    // lanes (its shadow lane included) share one warp -- so
-                    // no per-node length tests; the shared-memory rows as
-                    // pointers (immediate offsets per node)
+                    // padded strip: a strip shorter than K treats its nodes
+                    // k >= len as dummies and parks the node above the strip
+                    // (v_N) in d[len] at the substep start, so every node
+                    // reads its north neighbour from d[k + 1] (the last from
+                    // v_N) on one code path; dummies compute and never store.
+                    // Shared-memory rows as pointers (immediate offsets).
                     const double* vc = sd + cur + base;
                     double* vx = sd + nxt + base;
                     const double* vE = vc + W;
                     const double* vW = vc - W;
                     const double vnl = vc[span];
-                    const double vs0 = vc[-1];
-                    auto nodes = [&](auto nvc) {
-                        constexpr int NV = decltype(nvc)::value;  // 0: runtime length
-                        double vs = vs0;
-                        double vk = d[0];
+                    if (span == K - 1) {
+                        d[K - 1] = vnl;
+                    } else if (span < K - 1) {
 #pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            if (NV && k >= NV) break;
-                            const bool has_n = NV ? (k + 1 < NV) : (k + 1 < span);
-                            const double ve = vE[k], vw = vW[k];
-                            const double vn = has_n ? d[k + 1] : vnl;
-                            const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
-                            const double vpk =
-                                VT ? __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]))
-                                   : (m == 1 ? 0.0 : vx[k]);
-                            const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
-                            d[k] = next;
-                            if (lat_on && (NV || k < len)) vx[k] = next;
-                            vs = vk;
-                            vk = vn;
-                        }
-                    };
-                    if (span == K)
-                        nodes(std::integral_constant<int, K>{});
-                    else if (span == K - 1)
-                        nodes(std::integral_constant<int, K - 1>{});
-                    else
-                        nodes(std::integral_constant<int, 0>{});
+                        for (int k = 0; k < K - 1; ++k)
+                            if (k == span) d[k] = vnl;
+                    }
+                    double vs = vc[-1];
+                    double vk = d[0];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const double ve = vE[k], vw = vW[k];
+                        const double vn = k + 1 < K ? d[k + 1] : vnl;
+                        const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
+                        const double vpk =
+                            VT ? __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]))
+                               : (m == 1 ? 0.0 : vx[k]);
+                        const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
+                        d[k] = next;
+                        if (k < len) vx[k] = next;
+                        vs = vk;
+                        vk = vn;
+                    }
                 } else {
                 const int ce = cur + base + W, cw_ = cur + base - W;
                 const double vnl = sd[cur + sN];

@@ -314,7 +314,7 @@ struct LatSolveArgs {
     const double* qsm;
     double* q;                   // [k * S + s]
     int* fail;                   // per sample: first non-finite step (INT_MAX: none)
-    int tmem;                    // 1: generic weights/columns and d_{m-1} in tensor memory (default)
+    int tmem;                    // 0: shared memory; 1: generic weights/columns and d_{m-1} in tensor memory; 2: weights/columns only (default)
 };
 
 int lattice_solve_smem_bytes(const LatSolveArgs& a);

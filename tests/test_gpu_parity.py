@@ -282,13 +282,15 @@ def test_fused_lattice_solve_matches_the_step_kernels(lvl, monkeypatch):
     assert np.max(np.abs(dq_f - dq_p) / np.abs(qf_p)) < 1e-12
 
 
-@pytest.mark.parametrize("lvl", [0, 1])
-def test_fused_solve_tensor_memory_is_bitwise_the_shared_memory_form(lvl, monkeypatch):
-    """The fused solve keeps each thread's generic SELL weights / columns and
-    its lattice nodes' d_{m-1} in tensor memory (tcgen05.ld / st) instead of
-    shared memory: the same products in the same order, so the same bits
-    (coupled pairs, level-1 pairs include a level-0 coarse solve)."""
+@pytest.mark.parametrize("lvl,form", [(0, "2"), (1, "2"), (1, "1")])
+def test_fused_solve_tensor_memory_is_bitwise_the_shared_memory_form(lvl, form, monkeypatch):
+    """The fused solve keeps each thread's generic SELL weights / columns
+    (form 2, default) and optionally its lattice nodes' d_{m-1} (form 1) in
+    tensor memory (tcgen05.ld / st) instead of shared memory: the same
+    products in the same order, so the same bits (coupled pairs, level-1
+    pairs include a level-0 coarse solve)."""
     defs = configs.config1()
+    monkeypatch.setenv("WMC_FUSED_TMEM", form)
     a = [configs.build_level(d) for d in defs[max(lvl - 1, 0):lvl + 1]]
     monkeypatch.setenv("WMC_FUSED_TMEM", "0")
     b = [configs.build_level(d) for d in defs[max(lvl - 1, 0):lvl + 1]]
