@@ -145,7 +145,8 @@ struct wmc_level {
     int small_smem = 0;  // fused small-mesh solve: shared memory per CTA (0: not eligible)
     int fused_smem = 0;  // fused lattice solve: shared memory per CTA (0: not eligible)
     bool fused_zp_global = false;
-    int fused_tmem = 2;            // fused lattice solve: tensor-memory form (fixed at level creation)  // fused lattice solve keeps z_{n-1} in a per-sample global buffer
+    int fused_tmem = 2;            // fused lattice solve: tensor-memory form (fixed at level creation)
+    int sweep_wide = 23;           // 256-bit step sweep: 10 rows-per-warp + blocks-per-SM, 0 off (WMC_SWEEP_WIDE)  // fused lattice solve keeps z_{n-1} in a per-sample global buffer
     int n_sms = 148;
     SubPath path = SubPath::None;
     int* d_apg_ptr = nullptr;
@@ -738,6 +739,10 @@ void build_device_level(wmc_level& L) {
     }
     L.lattice = L.path == SubPath::Lattice;
     {
+        const char* e = std::getenv("WMC_SWEEP_WIDE");  // A/B knob, fixed per level
+        L.sweep_wide = e ? std::atoi(e) : 23;
+    }
+    {
         // fused small-mesh solve: the batched arithmetic is mirrored for the
         // leap-frog / p = 1 and on-chip generic substep paths
         int sms = 0;
@@ -1063,6 +1068,7 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
     wmc::launch_fill_int(ws.fail, INT_MAX, S, stream);
 
     wmc::SweepArgs sw{};
+    sw.wide = L.sweep_wide;
     sw.n = t.n;
     sw.S = S;
     sw.count = count;

@@ -2483,10 +2483,7 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
         const char* v = std::getenv("WMC_SWEEP_ONE_ROW");  // tuning knob: one row per warp
         return v ? std::atoi(v) : 0;
     }();
-    static const int wide = [] {
-        const char* v = std::getenv("WMC_SWEEP_WIDE");  // 10 R + MINB of the 256-bit sweep (0: off)
-        return v ? std::atoi(v) : 23;
-    }();
+    const int wide = a.wide;
     if (a.cell_ix) {  // cells in a separate per-entry array (narrow-channel levels)
         sweep_kernel<false, false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     } else if (parts) {

@@ -88,6 +88,7 @@ struct SweepArgs {
     int* fail;
     const double* rel;   // per-sample CFL: (dt_s / dt)^2 scales every dt^2 constant (NULL: 1)
     const int* nsteps;   // per-sample CFL: steps of sample s; later steps leave it untouched (NULL: all)
+    int wide;            // step sweep form: 10 R + MINB of sweep_wide_kernel (fixed dt, S % 128 == 0), 0: sweep_rows_kernel
 };
 
 struct SubArgs {

@@ -396,3 +396,26 @@ def test_adaptive_driver_evaluate_ahead_is_invisible(monkeypatch):
     assert a.estimate == b.estimate and a.rmse == b.rmse
     for x, y in zip(a.levels, b.levels):
         assert x["sum_dq"] == y["sum_dq"] and x["sum_q2"] == y["sum_q2"]
+
+
+@pytest.mark.parametrize("case", ["lattice", "global", "tiers"])
+def test_wide_sweep_is_bitwise_the_two_sample_sweep(case, monkeypatch):
+    """The 256-bit step sweep (four samples per lane, default for fixed dt
+    and batches of 128k samples) against the 16-byte sweep_rows_kernel: the
+    same per-sample products and sums, so the same bits -- g stashed
+    sample-major (lattice substeps, config-1 level 3), node-major (the
+    HBM-resident substep path) and on the nested-tier path (config 2)."""
+    if case == "tiers":
+        d = configs.config2()[1]
+    else:
+        d = configs.config1()[3 if case == "lattice" else 1]
+    if case == "global":
+        monkeypatch.setenv("WMC_SUBSTEP_PATH", "global")
+        monkeypatch.setenv("WMC_FUSED", "0")
+    a = configs.build_level(d)
+    monkeypatch.setenv("WMC_SWEEP_WIDE", "0")
+    b = configs.build_level(d)
+    _, qa, _ = wavemc.eval_pairs(a, None, 0, 1, 0, 256)
+    _, qb, _ = wavemc.eval_pairs(b, None, 0, 1, 0, 256)
+    assert np.all(np.isfinite(qa))
+    assert np.array_equal(qa, qb)
