@@ -1803,15 +1803,16 @@ __device__ __forceinline__ void lat_solve_g(double* sd, int ov, const double* zn
 // lanes 32 (w % 4) .. + 31 (its sub-partition's lane quarter) and columns
 // 128 (w / 4) .. + 127.  Each tcgen05.ld / st is issued together with its
 // wait in one asm statement, so the compiler cannot read the outputs (or
-// reuse the inputs) early.
+// reuse the inputs) early.  The loads carry no "memory" clobber (TMEM is
+// not memory the compiler tracks; asm volatile keeps them ordered with the
+// tcgen05.st), so shared-memory accesses may be scheduled around them.
 __device__ __forceinline__ void tm_ld16(std::uint32_t addr, std::uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
         "tcgen05.wait::ld.sync.aligned;\n"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(addr)
-        : "memory");
+        : "r"(addr));
 }
 __device__ __forceinline__ void tm_ld16_4(std::uint32_t aw, std::uint32_t (&w)[16], std::uint32_t ac,
                                           std::uint32_t (&c)[4]) {
@@ -1822,8 +1823,7 @@ __device__ __forceinline__ void tm_ld16_4(std::uint32_t aw, std::uint32_t (&w)[1
         : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
           "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15]),
           "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3])
-        : "r"(aw), "r"(ac)
-        : "memory");
+        : "r"(aw), "r"(ac));
 }
 __device__ __forceinline__ void tm_st16(std::uint32_t addr, const std::uint32_t (&r)[16]) {
     asm volatile(
@@ -2270,11 +2270,14 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     for (int k = 0; k < K; ++k) {
                         const double ve = vE[k], vw = vW[k];
                         const double vn = k + 1 < K ? d[k + 1] : vnl;
-                        const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
+                        // g + A d as two shallow chains (FP64 dependency depth 5, was 6):
+                        // (g + dg v_k - kE v_E) - (kW v_W + kNS (v_N + v_S))
+                        const double ga = fma(-kE, ve, fma(dg, vk, gg[k]));
+                        const double gb = fma(kW, vw, kNS * (vn + vs));
                         const double vpk =
                             VT ? __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]))
                                : (m == 1 ? 0.0 : vx[k]);
-                        const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
+                        const double next = fma(-cmh, ga - gb, fma(onepb, d[k], -(beta * vpk)));
                         d[k] = next;
                         if (k < len) vx[k] = next;
                         vs = vk;
@@ -2289,9 +2292,12 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 for (int k = 0; k < K; ++k) {
                     const double ve = sd[ce + k], vw = sd[cw_ + k];
                     const double vn = (k + 1 < len) ? d[k + 1] : vnl;
-                    const double aq = dg * vk - kE * ve - kW * vw - kNS * (vn + vs);
+                    // g + A d as two shallow chains (FP64 dependency depth 5, was 6):
+                    // (g + dg v_k - kE v_E) - (kW v_W + kNS (v_N + v_S))
+                    const double ga = fma(-kE, ve, fma(dg, vk, gg[k]));
+                    const double gb = fma(kW, vw, kNS * (vn + vs));
                     const double vpk = m == 1 ? 0.0 : sd[nxt + base + k];
-                    const double next = onepb * d[k] - beta * vpk - cmh * (gg[k] + aq);
+                    const double next = fma(-cmh, ga - gb, fma(onepb, d[k], -(beta * vpk)));
                     d[k] = next;
                     if (k < len) sd[nxt + base + k] = next;
                     vs = vk;
