@@ -2247,19 +2247,19 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 }
                 if (TM) {
                     // padded strip: a strip shorter than K treats its nodes
-                    // k >= len as dummies and parks the node above the strip
-                    // (v_N) in d[len] at the substep start, so every node
-                    // reads its north neighbour from d[k + 1] (the last from
-                    // v_N) on one code path; dummies compute and never store.
+                    // k >= len as dummies; node len - 1 reads v_N (the node
+                    // above the strip) in place of d[len] -- selected inside
+                    // the loop for the common K - 1 case, parked in d[len]
+                    // before it for shorter strips -- on one code path;
+                    // dummies compute and never store.
                     // Shared-memory rows as pointers (immediate offsets).
                     const double* vc = sd + cur + base;
                     double* vx = sd + nxt + base;
                     const double* vE = vc + W;
                     const double* vW = vc - W;
                     const double vnl = vc[span];
-                    if (span == K - 1) {
-                        d[K - 1] = vnl;
-                    } else if (span < K - 1) {
+                    const bool pad_last = span == K - 1;  // the common short strip: v_N read in the loop
+                    if (span < K - 1) {
 #pragma unroll
                         for (int k = 0; k < K - 1; ++k)
                             if (k == span) d[k] = vnl;
@@ -2269,7 +2269,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         const double ve = vE[k], vw = vW[k];
-                        const double vn = k + 1 < K ? d[k + 1] : vnl;
+                        const double vn = k + 2 < K ? d[k + 1] : k + 2 == K ? (pad_last ? vnl : d[k + 1]) : vnl;
                         // g + A d as two shallow chains (FP64 dependency depth 5, was 6):
                         // (g + dg v_k - kE v_E) - (kW v_W + kNS (v_N + v_S))
                         const double ga = fma(-kE, ve, fma(dg, vk, gg[k]));
