@@ -2213,11 +2213,14 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 if (grow[u] >= 0) sd[o.v0 + grow[u]] = gd[u] * grs[u];
             }
             __syncthreads();
+            // buffer offsets carried through the substeps (swapped each one)
+            // rather than re-derived from the layout; beta / c_m by pointer
+            int cur = o.v0, nxt = o.v1;
+            const double* bp = sd + o.beta;
+            const double* cp = sd + o.cm;
             for (int m = 1; m <= a.p - 1; ++m) {
-                const int cur = (m & 1) ? o.v0 : o.v1;
-                const int nxt = (m & 1) ? o.v1 : o.v0;
-                const double beta = sd[o.beta + m - 1];
-                const double cmm = sd[o.cm + m - 1] * rs;
+                const double beta = bp[m - 1];
+                const double cmm = cp[m - 1] * rs;
                 const double onepb = 1.0 + beta;
                 const double cmh = cmm * inv_h;
                 double gaq[G];
@@ -2312,6 +2315,9 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     if (grow[u] >= 0) sd[nxt + grow[u]] = next * grs[u];
                 }
                 __syncthreads();
+                const int t_ = cur;
+                cur = nxt;
+                nxt = t_;
             }
             // ---- R update (r_update_kernel): z_{n+1} = 2 z_n - z_{n-1} + 2 d_p;
             // z_{n-1} of the thread's rows loaded before any store
