@@ -1313,6 +1313,9 @@ void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     a.n_steps = t.n_steps;
     a.zp_global = L.fused_zp_global ? ws.zb : nullptr;
     a.tmem = L.fused_tmem;
+    a.strips_k_or_k1 = 1;
+    for (int len : t.strip_len)
+        if (len < t.lat_k - 1) a.strips_k_or_k1 = 0;
     a.rem_ptr = L.d_rem_ptr;
     a.rem_col = L.d_rem_col;
     a.rem_cell = L.d_rem_cell;

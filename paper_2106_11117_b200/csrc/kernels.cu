@@ -1965,7 +1965,9 @@ __device__ __forceinline__ double gen_full_row_tm(const LatSolveArgs& A, const d
 // d_{m-1} read back from the buffer the substep overwrites.
 // VT (with TM): d_{m-1} of the lattice nodes in TMEM too; otherwise read
 // back from the shared-memory buffer the substep overwrites.
-template <int T, int K, int G, bool TM, bool VT = TM>
+// PK: every strip holds K or K - 1 rows (host-checked), so the rare path
+// for shorter strips is compiled out.
+template <int T, int K, int G, bool TM, bool VT = TM, bool PK = false>
 __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
     static_assert(!TM || (T % 128 == 0 && T <= 512 && 20 * G + 4 * K <= 128), "TMEM columns per thread");
     extern __shared__ __align__(16) double sd[];
@@ -2262,7 +2264,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     const double* vW = vc - W;
                     const double vnl = vc[span];
                     const bool pad_last = span == K - 1;  // the common short strip: v_N read in the loop
-                    if (span < K - 1) {
+                    if (!PK && span < K - 1) {
 #pragma unroll
                         for (int k = 0; k < K - 1; ++k)
                             if (k == span) d[k] = vnl;
@@ -2682,25 +2684,26 @@ int lattice_solve_max_smem(int device) {
     return optin - static_cast<int>(fa.sharedSizeBytes);
 }
 
-template <int T, int K, int G, bool TM, bool VT>
+template <int T, int K, int G, bool TM, bool VT, bool PK = false>
 static int launch_lat_solve(const LatSolveArgs& a, int grid, cudaStream_t st) {
     static int configured = -1;
     if (configured < 0) {
         int device = 0;
         cudaGetDevice(&device);
-        configured = static_cast<int>(cudaFuncSetAttribute(lattice_solve_kernel<T, K, G, TM, VT>,
+        configured = static_cast<int>(cudaFuncSetAttribute(lattice_solve_kernel<T, K, G, TM, VT, PK>,
                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            lattice_solve_max_smem(device)));
     }
     if (configured != 0) return configured;
-    lattice_solve_kernel<T, K, G, TM, VT><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
+    lattice_solve_kernel<T, K, G, TM, VT, PK><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
 
 int launch_lattice_solve(const LatSolveArgs& a, int grid, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (a.lat.threads == 512 && a.lat.strip_k == 8)
-        return a.tmem == 2 ? launch_lat_solve<512, 8, 2, true, false>(a, grid, st)
+        return a.tmem == 2 ? (a.strips_k_or_k1 ? launch_lat_solve<512, 8, 2, true, false, true>(a, grid, st)
+                                               : launch_lat_solve<512, 8, 2, true, false>(a, grid, st))
                : a.tmem    ? launch_lat_solve<512, 8, 2, true, true>(a, grid, st)
                            : launch_lat_solve<512, 8, 2, false, false>(a, grid, st);
     return static_cast<int>(cudaErrorInvalidValue);

@@ -315,6 +315,7 @@ struct LatSolveArgs {
     const double* qsm;
     double* q;                   // [k * S + s]
     int* fail;                   // per sample: first non-finite step (INT_MAX: none)
+    int strips_k_or_k1;          // every lattice strip holds K or K - 1 rows
     int tmem;                    // 0: shared memory; 1: generic weights/columns and d_{m-1} in tensor memory; 2: weights/columns only (default)
 };
 
