@@ -1768,17 +1768,21 @@ __device__ __forceinline__ double lat_solve_row(const LatSolveArgs& A, int i, co
 // g = A z_n on the thread's lattice rows by the substep stencil: v = z / sqrt(M)
 // of every R row published to v (owners), one barrier, then the 5-point
 // stencil of lattice_substep_kernel (edge conductances already / h)
-template <int K, int G>
+// PUB = false: v is already published (the previous step's R update or the
+// start-up wrote it next to z_n, and a barrier followed)
+template <int K, int G, bool PUB = true>
 __device__ __forceinline__ void lat_solve_g(double* sd, int ov, const double* zn, int base, int len, int W, int sS,
                                             int sN, double inv_h, double kE, double kW, double kNS, double dg,
                                             const int* grow, const double* grs, double* gg) {
+    if (PUB) {
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-        if (k < len) sd[ov + base + k] = zn[base + k] * inv_h;
+        for (int k = 0; k < K; ++k)
+            if (k < len) sd[ov + base + k] = zn[base + k] * inv_h;
 #pragma unroll
-    for (int u = 0; u < G; ++u)
-        if (grow[u] >= 0) sd[ov + grow[u]] = zn[grow[u]] * grs[u];
-    __syncthreads();
+        for (int u = 0; u < G; ++u)
+            if (grow[u] >= 0) sd[ov + grow[u]] = zn[grow[u]] * grs[u];
+        __syncthreads();
+    }
     const int ce = ov + base + W, cw_ = ov + base - W;
     const double vnl = sd[ov + sN];
     double vs = sd[ov + sS];
@@ -2142,12 +2146,19 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, 1);
             }
             __syncthreads();
+            // z_1, and v = z_1 / sqrt(M) published for the first step's sweep
 #pragma unroll
             for (int k = 0; k < K; ++k)
-                if (k < len) zn[base + k] = gg[k];
+                if (k < len) {
+                    zn[base + k] = gg[k];
+                    sd[o.v0 + base + k] = gg[k] * inv_h;
+                }
 #pragma unroll
             for (int u = 0; u < G; ++u)
-                if (grow[u] >= 0) zn[grow[u]] = ggg[u];
+                if (grow[u] >= 0) {
+                    zn[grow[u]] = ggg[u];
+                    sd[o.v0 + grow[u]] = ggg[u] * grs[u];
+                }
             for (int i = nr + tid; i < A.n; i += T) zn[i] = sd[o.v1 + i - nr];
             __syncthreads();
         }
@@ -2159,7 +2170,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
             // stencil, the others as sweep_rows_kernel), leap-frog update of
             // the rows outside R (z_{n+1} parked in v1 until every read of
             // z_n is done)
-            lat_solve_g<K, G>(sd, o.v0, zn, base, len, W, sS, sN, inv_h, kE, kW, kNS, dg, grow, grs, gg);
+            lat_solve_g<K, G, false>(sd, o.v0, zn, base, len, W, sS, sN, inv_h, kE, kW, kNS, dg, grow, grs, gg);
 #pragma unroll
             for (int u = 0; u < G; ++u)
                 if (TM) {
@@ -2336,6 +2347,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     const double out = 2.0 * zi - zq[k] + 2.0 * (d[k] * hh);
                     zp[i] = zi;
                     zn[i] = out;
+                    sd[o.v0 + i] = out * inv_h;  // v for the next step's sweep (the substeps are done with v0)
                     if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
                 }
 #pragma unroll
@@ -2346,6 +2358,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     const double out = 2.0 * zi - zgq[u] + 2.0 * gd[u];
                     zp[i] = zi;
                     zn[i] = out;
+                    sd[o.v0 + i] = out * grs[u];
                     if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
                 }
             __syncthreads();
