@@ -532,7 +532,9 @@ def roofline_from_profile(levels, counts, prof, step_ms):
                          "achieved_GBps": gbps(sweep_bytes, sweep_ms)},
                "substep": {"ms": sub_ms, "launches": sum(p["sub_launches"] for p in prof),
                            "path": ("hbm-resident nested tiers" if any(lv.info["substep_path"] == 4 for lv in levels)
-                                    else "hbm-resident" if global_path else "on-chip"),
+                                    else ("on-chip + hbm-resident" if any(lv.info["substep_path"] in (1, 2) and not f
+                                                                          for lv, f in zip(levels, fused_lv))
+                                          else "hbm-resident") if global_path else "on-chip"),
                            "share_of_step": sub_ms / step_ms if step_ms else None,
                            "fp64_TFLOPs": sub_flops / (sub_ms * 1e-3) / 1e12 if sub_ms and sub_flops else None,
                            "substep_dof_updates_per_s": sub_updates / (sub_ms * 1e-3) if sub_ms else None,

@@ -486,7 +486,13 @@ void build_device_level(wmc_level& L) {
         for (const auto& v : t.tier_cm) cm.insert(cm.end(), v.begin(), v.end());
         L.d_tier_cm = upload(cm);
         L.d_beta = upload(t.beta);
-    } else if (lts && (fp == "global" || !onchip_fits)) {
+    } else if (lts && (fp == "global" || !onchip_fits ||
+                       // p = 2 levels too large for the fused solve: the single
+                       // substep of the HBM/L2-resident kernel also forms z_{n+1}
+                       // (no per-sample weight set-up, no separate R update);
+                       // measured 1.17x on config-1 level 4
+                       (fp.empty() && t.p == 2 && t.n_cells <= wmc::kMaxCells &&
+                        16.0 * t.n + 16.0 * (t.n_r + 16) > 227.0 * 1024.0))) {
         if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
         L.path = SubPath::Global;
         L.d_apg_ptr = upload(t.apg_ptr);
