@@ -419,3 +419,21 @@ def test_wide_sweep_is_bitwise_the_two_sample_sweep(case, monkeypatch):
     _, qb, _ = wavemc.eval_pairs(b, None, 0, 1, 0, 256)
     assert np.all(np.isfinite(qa))
     assert np.array_equal(qa, qb)
+
+
+@pytest.mark.parametrize("n_coarse,ratio", [(16, 4), (32, 8)])
+def test_fused_solve_with_short_strips_matches_the_step_kernels(n_coarse, ratio, monkeypatch):
+    """Refined squares whose lattice runs cut into strips shorter than K - 1
+    (h_min = 1/64: runs of 3 rows) or into K / K - 1 strips (h_min = 1/256:
+    runs of 31) take the fused solve's general and compiled-out short-strip
+    forms; both against the per-step kernels at rounding level."""
+    d = configs.LevelDef(n_coarse, ratio, 0.2 / n_coarse, ratio, configs.config1()[0].integrator, final_time=0.25)
+    fused = configs.build_level(d)
+    monkeypatch.setenv("WMC_FUSED", "0")
+    plain = configs.build_level(d)
+    monkeypatch.delenv("WMC_FUSED")
+    assert fused.info["fused"] == 1 and plain.info["fused"] == 0
+    _, qf, _ = wavemc.eval_pairs(fused, None, 0, 0, 0, 300)
+    _, qp, _ = wavemc.eval_pairs(plain, None, 0, 0, 0, 300)
+    assert np.all(np.isfinite(qf))
+    assert per_sample_rel(qf, qp) < 1e-12
