@@ -190,6 +190,8 @@ struct wmc_level {
     wmc::ChannelTables ch;
     wmc::ChannelArgs ch_args{};
     std::vector<void*> ch_bufs;
+    int* d_ns_rows = nullptr;  // fused solve: non-structured rows outside R held in TMEM
+    int n_ns = 0;
     int* d_rem_ptr = nullptr;  // fused solve: A (I - P) entries of the generic rows
     int* d_rem_col = nullptr;
     int* d_rem_cell = nullptr;
@@ -237,7 +239,7 @@ struct wmc_level {
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_warp_slice, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
                         (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0,
-                        (void*)d_rem_ptr, (void*)d_rem_col, (void*)d_rem_cell, (void*)d_rem_a0,
+                        (void*)d_rem_ptr, (void*)d_rem_col, (void*)d_rem_cell, (void*)d_rem_a0, (void*)d_ns_rows,
                         (void*)d_cell_ix})
             if (p) cudaFree(p);
         for (void* p : ch_bufs) cudaFree(p);
@@ -456,6 +458,40 @@ void build_device_level(wmc_level& L) {
         L.n_row_types = static_cast<int>(types.size());
         for (std::size_t q = 0; q < types.size(); ++q) L.row_types[q] = make_double2(types[q].first, types[q].second);
         for (const auto& d : desc) L.n_structured += d.x >= 0 && ((d.x >> 16) & 0xff) > 0;
+        {
+            // fused solve (TMEM form 2): the rows outside R that are not
+            // structured, at most two per thread of the 512-thread CTA and
+            // kNsMax entries each, keep their CSR entries in TMEM
+            std::vector<int> ns;
+            bool ok = L.d_cell_ix == nullptr;
+            for (int i = t.n_r; i < t.n && ok; ++i) {
+                const int4 d = desc[i];
+                if (d.x >= 0 && ((d.x >> 16) & 0xff) > 0) continue;
+                if (t.row_ptr[i + 1] - t.row_ptr[i] > wmc::kNsMax) ok = false;
+                ns.push_back(i);
+            }
+            const char* e = std::getenv("WMC_FUSED_NS_TMEM");  // A/B knob (0: off)
+            if (ok && !ns.empty() && static_cast<int>(ns.size()) <= 2 * 512 && !(e && std::atoi(e) == 0)) {
+                L.d_ns_rows = upload(ns);
+                L.n_ns = static_cast<int>(ns.size());
+            }
+        }
+        if (std::getenv("WMC_DEBUG_ROWS")) {  // row-class census (tuning)
+            long st = 0, single = 0, multi = 0, len_max = 0, len_sum = 0, long_rows = 0;
+            for (int i = t.n_r; i < t.n; ++i) {
+                const int4 d = desc[i];
+                const int len = t.row_ptr[i + 1] - t.row_ptr[i];
+                if (d.x >= 0 && ((d.x >> 16) & 0xff) > 0) { ++st; continue; }
+                (d.x >= 0 ? single : multi) += 1;
+                len_max = std::max<long>(len_max, len);
+                len_sum += len;
+                long_rows += len > 9;
+            }
+            std::fprintf(stderr, "rows outside R: n=%d n_r=%d structured=%ld single-cell=%ld multi-cell=%ld "
+                         "generic len max=%ld mean=%.2f (>9: %ld) types=%zu\n", t.n, t.n_r, st, single, multi,
+                         len_max, (single + multi) ? double(len_sum) / double(single + multi) : 0.0, long_rows,
+                         types.size());
+        }
         L.d_row_desc = upload(desc);
         L.d_wtype = upload(std::vector<double2>(L.row_types, L.row_types + wmc::kMaxRowTypes));
     }
@@ -1322,6 +1358,8 @@ void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     a.strips_k_or_k1 = 1;
     for (int len : t.strip_len)
         if (len < t.lat_k - 1) a.strips_k_or_k1 = 0;
+    a.ns_rows = L.d_ns_rows;
+    a.n_ns = (L.fused_tmem == 2 && t.lat_threads == 512) ? L.n_ns : 0;
     a.rem_ptr = L.d_rem_ptr;
     a.rem_col = L.d_rem_col;
     a.rem_cell = L.d_rem_cell;

@@ -2008,6 +2008,37 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
     auto tw_ = [&](int u) { return tbase + 16u * u; };            // 16 columns: 4 weight pairs
     auto tc_ = [&](int u) { return tbase + 16u * G + 4u * u; };   // 4 columns: column pairs
     auto tv_ = [&](int set) { return tbase + 20u * G + 2u * K * set; };  // 2 K columns: v_{m-1}
+    // non-structured rows outside R (form 2 only, d_{m-1} not in TMEM):
+    // role j at 20 G + 38 j: kNsMax entry words, 2 kNsMax weight words, row, count | (cell + 1) << 8
+    auto tn_ = [&](int j) { return tbase + 20u * G + 38u * j; };
+    static_assert(!TM || VT || 20 * G + 2 * 38 <= static_cast<int>(128), "TMEM columns for the rows outside R");
+    if (TM && !VT && A.n_ns > 0) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int q = j * T + tid;
+            const int r = q < A.n_ns ? __ldg(A.ns_rows + q) : -1;
+            std::uint32_t ew[kNsMax], ww[2 * kNsMax], mw[2];
+            int b = 0, cnt = 0, cellp = 0;
+            if (r >= 0) {
+                b = __ldg(A.row_ptr + r);
+                cnt = __ldg(A.row_ptr + r + 1) - b;
+                const int4 d = __ldg(A.row_desc + r);
+                cellp = d.x >= 0 ? (d.x & 0xffff) + 1 : 0;
+            }
+#pragma unroll
+            for (int t = 0; t < kNsMax; ++t) {
+                const double w = t < cnt ? __ldg(A.a0 + b + t) : 0.0;
+                ew[t] = t < cnt ? static_cast<std::uint32_t>(__ldg(A.ent + b + t)) : 0u;
+                ww[2 * t] = static_cast<std::uint32_t>(__double2loint(w));
+                ww[2 * t + 1] = static_cast<std::uint32_t>(__double2hiint(w));
+            }
+            mw[0] = static_cast<std::uint32_t>(r);
+            mw[1] = static_cast<std::uint32_t>(cnt) | (static_cast<std::uint32_t>(cellp) << 8);
+            tm_stn<kNsMax>(tn_(j), ew);
+            tm_stn<2 * kNsMax>(tn_(j) + kNsMax, ww);
+            tm_stn<2>(tn_(j) + 3 * kNsMax, mw);
+        }
+    }
 
     // static tables, once per CTA
     if (!TM)
@@ -2191,15 +2222,62 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     zi[u] = i < A.n ? zn[i] : 0.0;
                     zq[u] = i < A.n ? zp[i] : 0.0;
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) gr[u] = i0 + u * T < A.n ? lat_solve_row(A, i0 + u * T, zn, cl) : 0.0;
+                bool mine[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int i = i0 + u * T;
-                    if (i >= A.n) continue;
+                    mine[u] = i < A.n;
+                    if (TM && !VT && A.n_ns > 0 && mine[u]) {  // non-structured rows: the TMEM pass below
+                        const int4 dd = __ldg(A.row_desc + i);
+                        mine[u] = dd.x >= 0 && ((dd.x >> 16) & 0xff) > 0;
+                    }
+                    gr[u] = mine[u] ? lat_solve_row(A, i, zn, cl) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * T;
+                    if (!mine[u]) continue;
                     const double out = 2.0 * zi[u] - zq[u] - factor * gr[u];
                     sd[o.v1 + i - nr] = out;
                     if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                }
+            }
+            if (TM && !VT && A.n_ns > 0) {
+                // the thread's non-structured rows outside R from its TMEM
+                // columns: lat_solve_row's CSR sums in entry order, no global
+                // loads, warp-uniform trip count (predicated on the row length)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (j * T + (tid & ~31) >= A.n_ns) continue;  // warp-uniform
+                    std::uint32_t mw[2], ew[kNsMax];
+                    tm_ldn<2>(tn_(j) + 3 * kNsMax, mw);
+                    tm_ldn<kNsMax>(tn_(j), ew);
+                    std::uint32_t ww[2 * kNsMax];
+                    tm_ldn<2 * kNsMax>(tn_(j) + kNsMax, ww);
+                    const int r = static_cast<int>(mw[0]);
+                    if (r >= 0) {  // per lane (no warp-collective op inside)
+                    const int cnt = static_cast<int>(mw[1] & 0xffu), cellp = static_cast<int>(mw[1] >> 8);
+                    double acc0 = 0.0;
+                    if (cellp) {
+                        double p0 = 0.0;
+#pragma unroll
+                        for (int t = 0; t < kNsMax; ++t)
+                            if (t < cnt)
+                                p0 += __hiloint2double(static_cast<int>(ww[2 * t + 1]), static_cast<int>(ww[2 * t])) *
+                                      zn[ew[t] & static_cast<unsigned>(A.col_mask)];
+                        acc0 = cl[cellp - 1] * p0;
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < kNsMax; ++t)
+                            if (t < cnt)
+                                acc0 += (cl[ew[t] >> A.col_bits] *
+                                         __hiloint2double(static_cast<int>(ww[2 * t + 1]), static_cast<int>(ww[2 * t]))) *
+                                        zn[ew[t] & static_cast<unsigned>(A.col_mask)];
+                    }
+                    const double out = 2.0 * zn[r] - zp[r] - factor * acc0;
+                    sd[o.v1 + r - nr] = out;
+                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                    }
                 }
             }
             __syncthreads();

@@ -27,6 +27,7 @@ constexpr unsigned kOvfFlag = 0x8000u;    // lattice kernel: slot weight in the 
 
 constexpr int kSweepChunk = 64;  // samples per warp in the sweep (2 per lane)
 constexpr int kSweepWarps = 8;   // rows per sweep block
+constexpr int kNsMax = 12;       // fused solve: entries of a TMEM-held row outside R
 constexpr int kSubThreads = 1024;
 constexpr int kSubMaxRpt = 8;    // rows per thread in the substep kernel
 
@@ -304,6 +305,12 @@ struct LatSolveArgs {
     // A (I - P) entries of the generic rows (sorted SELL order): g = A z_n on
     // a generic row is the SELL gather on v = z / sqrt(M) (the A P part) plus
     // these (columns outside P)
+    // rows outside R that are not structured (CSR rows of <= kNsMax entries),
+    // thread t owning ns_rows[t] and ns_rows[t + threads]: their entries live
+    // in the thread's TMEM columns (TMEM form 2; n_ns = 0: gathered from the
+    // CSR arrays in the round-robin sweep like the structured rows)
+    const int* ns_rows;
+    int n_ns;
     const int* rem_ptr;
     const int* rem_col;
     const int* rem_cell;
