@@ -2197,6 +2197,9 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
         const double c0 = a.c0 * rs;
         for (long st = 1; st < n_steps; ++st) {
             const int step = static_cast<int>(st + 1);
+            // check_finite (integrators.cpp:12-18): a per-thread flag over the
+            // step's stores, one atomic per flagged thread at the step end
+            bool bad = false;
             // ---- sweep: g = A z_n on R rows (lattice rows by the substep
             // stencil, the others as sweep_rows_kernel), leap-frog update of
             // the rows outside R (z_{n+1} parked in v1 until every read of
@@ -2239,7 +2242,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     if (!mine[u]) continue;
                     const double out = 2.0 * zi[u] - zq[u] - factor * gr[u];
                     sd[o.v1 + i - nr] = out;
-                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                    bad |= !(fabs(out) <= 1e100);
                 }
             }
             if (TM && !VT && A.n_ns > 0) {
@@ -2276,7 +2279,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     }
                     const double out = 2.0 * zn[r] - zp[r] - factor * acc0;
                     sd[o.v1 + r - nr] = out;
-                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                    bad |= !(fabs(out) <= 1e100);
                     }
                 }
             }
@@ -2426,7 +2429,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     zp[i] = zi;
                     zn[i] = out;
                     sd[o.v0 + i] = out * inv_h;  // v for the next step's sweep (the substeps are done with v0)
-                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                    bad |= !(fabs(out) <= 1e100);
                 }
 #pragma unroll
             for (int u = 0; u < G; ++u)
@@ -2437,8 +2440,9 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     zp[i] = zi;
                     zn[i] = out;
                     sd[o.v0 + i] = out * grs[u];
-                    if (!(fabs(out) <= 1e100)) atomicMin(&fail_step, step);
+                    bad |= !(fabs(out) <= 1e100);
                 }
+            if (bad) atomicMin(&fail_step, step);
             __syncthreads();
         }
         // ---- QoI of the final state (qoi_kernel; NaN for a failed sample)
