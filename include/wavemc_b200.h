@@ -220,6 +220,12 @@ int wmc_eval_pairs_device(wmc_level* fine, wmc_level* coarse, uint64_t seed, uin
 /* The handle's CUDA stream (cudaStream_t) for event timing; all work of a
  * level pair is issued on the fine level's stream. */
 void* wmc_level_stream(wmc_level* level);
+/* Waits for the level's stream.  Every batch of wmc_eval_pairs_device folds
+ * its check_finite flags (reference src/integrators.cpp:12-18) into a record
+ * on the fine level; synchronize reads it: the first failing sample (lowest
+ * index) since the previous call is reported in err (sample, step, level)
+ * with status 3 (NumericalError, as src/mlmc.cpp:31-35), and the record is
+ * cleared. */
 int wmc_synchronize(wmc_level* level, wmc_error* err);
 
 /* KL table of the log-normal field: table[cell * modes + m] =
@@ -299,7 +305,8 @@ int wmc_optimal_samples(const double* variances, const double* costs, int n_leve
 double wmc_bias_proxy_sq(double mean_dq, double alpha);
 
 /* Device-side per-level fold: d_out[0..3] += {sum dq, sum dq^2, sum q, sum q^2}
- * over count device values, one fixed-order block (deterministic). */
+ * over count device values, one fixed-order block (deterministic).  Scalar
+ * QoI levels only (nq == 1; QoI vectors fold on the host): status 2 else. */
 int wmc_moments_device(wmc_level* level, const double* d_dq, const double* d_q, uint64_t count, double* d_out);
 
 /* Kernel-level timing: with profiling on, every sweep, substep and R-update

@@ -1,6 +1,6 @@
 """Generate tests/golden/*.json from the UNMODIFIED reference library
 (oracle/_ref/wavemc_ref_driver) -- run in the build container, where
-/root/reference exists:  python oracle/make_golden.py [--only-config2 | --only-cfl | --only-experiments | --only-artifacts | --only-channel]
+/root/reference exists:  python oracle/make_golden.py [--only-round2 | --only-config1-full | --only-config2 | --only-cfl | --only-experiments | --only-artifacts | --only-channel]
 
 The meshes come from the shared problem definition (the product's host mesh
 builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
@@ -187,6 +187,66 @@ def channel(ref, tmp):
     dump(os.path.join("channel", "channel.json"), out)
 
 
+def config1_full(ref, tmp):
+    """Config-1 per-level sums, means and variances at the BASELINE N_l
+    (65536 / 16384 / 4096 / 1024 / 256 coupled pairs) from the unmodified
+    reference (sample_delta_q + LevelAccumulator + estimate_variance,
+    src/mlmc.cpp:21-73, folded in (level, index) order as run_jobs does,
+    :145-147).  About 75 core-minutes: run in the background."""
+    c1 = configs.config1()
+    specs = []
+    for l, d in enumerate(c1):
+        p = os.path.join(tmp, f"config1_l{l}.mesh")
+        configs.build_mesh(d).dump(p)
+        specs.append((p, d.dt, d.substeps))
+    r = ref.mlmc(specs, configs.CONFIG1_COUNTS, timeout=6 * 3600)
+    dump("config1_full_moments.json", r)
+
+
+def round2(ref, tmp):
+    """Round-2 fixtures: config 0 at its BASELINE 1024 samples (moments and
+    per-sample Q); config-1 global leap-frog pairs at dt = 0.2 h_min on every
+    level (BASELINE config 1's comparison arm; reference leapfrog_step,
+    src/integrators.cpp:89-115); config 3's real mesh (h = 1/1024, square at
+    h/8, p = 8) with T cut to 16 global steps."""
+    d0 = configs.config0()
+    p0 = os.path.join(tmp, "config0.mesh")
+    configs.build_mesh(d0).dump(p0)
+    mo = ref.mlmc([(p0, d0.dt, d0.substeps)], [configs.CONFIG0_COUNT], per_sample=True)
+    dump("config0_moments_1024.json", mo)
+
+    lf = configs.config1("lf")
+    specs = []
+    for l, d in enumerate(lf):
+        p = os.path.join(tmp, f"config1_l{l}.mesh")
+        configs.build_mesh(d).dump(p)
+        specs.append((p, d.dt, d.substeps))
+    pairs = ref.mlmc(specs, [4, 3, 3, 2, 2], kind="lf", per_sample=True)
+    pairs["dt"] = lf[0].dt
+    dump("config1_lf_pairs.json", pairs)
+
+    d3 = configs.config3()
+    p3 = os.path.join(tmp, "config3.mesh")
+    configs.build_mesh(d3).dump(p3)
+    t_cut = 16 * d3.dt
+    hdr, q = ref.solve(p3, d3.dt, d3.substeps, "lts", 0, 0, 3, T=repr(t_cut))
+    hdr2, q2 = ref.solve(p3, d3.dt, d3.substeps, "lts", 0, 4093, 2, T=repr(t_cut))
+    # the BASELINE QoI box [0.7, 0.9] x [0.4, 0.6] is outside the domain of
+    # dependence of the refined square within 16 steps, so the LTS substeps
+    # are pinned through a second QoI over the refined square itself
+    sq = "0.4375,0.5625,0.4375,0.5625"
+    hdr3, q3 = ref.solve(p3, d3.dt, d3.substeps, "lts", 0, 0, 3, T=repr(t_cut), box=sq)
+    t_long = 40 * d3.dt
+    hdr4, q4 = ref.solve(p3, d3.dt, d3.substeps, "lts", 0, 7, 2, T=repr(t_long), box=sq)
+    dump("config3_samples.json", {"dt": d3.dt, "p": d3.substeps, "nu": 0.01, "T": t_cut, "stream_level": 0,
+                                  "header": hdr, "first": [0, 4093], "q": q.tolist() + q2.tolist(),
+                                  "index": [0, 1, 2, 4093, 4094], "meshcheck": ref.meshcheck(p3),
+                                  "square_box": {"box": [0.4375, 0.5625, 0.4375, 0.5625], "T": t_cut, "first": 0,
+                                                 "header": hdr3, "q": q3.tolist()},
+                                  "square_box_long": {"box": [0.4375, 0.5625, 0.4375, 0.5625], "T": t_long,
+                                                      "first": 7, "header": hdr4, "q": q4.tolist()}})
+
+
 def main():
     build()
     ref = RefDriver()
@@ -202,6 +262,12 @@ def main():
         return
     if "--only-artifacts" in sys.argv:
         artifacts(ref, tmp)
+        return
+    if "--only-config1-full" in sys.argv:
+        config1_full(ref, tmp)
+        return
+    if "--only-round2" in sys.argv:
+        round2(ref, tmp)
         return
     if "--only-channel" in sys.argv:
         channel(ref, tmp)

@@ -231,7 +231,7 @@ class RefDriver:
         q = np.array([float(l.split()[1]) for l in lines[1:]])
         return header, q
 
-    def mlmc(self, specs, counts, kind="lts", threads=0, per_sample=False, seed=0, **kw):
+    def mlmc(self, specs, counts, kind="lts", threads=0, per_sample=False, seed=0, timeout=3600, **kw):
         args = ["mlmc", "--kind", kind, "--N", ",".join(map(str, counts)), "--threads", threads, "--seed", seed]
         for mesh_path, dt, p in specs:
             args += ["--level-spec", f"{mesh_path},{dt!r},{p}"]
@@ -239,7 +239,7 @@ class RefDriver:
             args += ["--per-sample", 1]
         for k, v in kw.items():
             args += [f"--{k}", v]
-        return json.loads(self.run(*args))
+        return json.loads(self.run(*args, timeout=timeout))
 
     def adaptive(self, specs, eps, threads=0, seed=0, max_level=6, kind="lts", **kw):
         """Reference run_mlmc (src/mlmc.cpp:165-233) over the given levels."""

@@ -219,6 +219,11 @@ struct wmc_level {
     double* h_qf = nullptr;
     int* h_ff = nullptr;
     int* h_fc = nullptr;
+    // device-resident pairs: first failing (index << 24 | step) of the fine
+    // and coarse solves since the last wmc_synchronize, and the MLMC level
+    // index the pairs were issued with
+    unsigned long long* d_fail_rec = nullptr;
+    int fail_level = 0;
     // optional per-kernel event timing (profiling pass only)
     bool profile = false;
     // captured batch launch sequences, keyed by (workspace, S, count, cells)
@@ -260,7 +265,7 @@ struct wmc_level {
             for (auto* p : w.tier_e) cudaFree(p);
             for (auto* p : w.tier_rhs) cudaFree(p);
         }
-        for (void* p : {(void*)r_dq, (void*)r_qf, (void*)r_ff, (void*)r_fc, (void*)r_cnt})
+        for (void* p : {(void*)r_dq, (void*)r_qf, (void*)r_ff, (void*)r_fc, (void*)r_cnt, (void*)d_fail_rec})
             if (p) cudaFree(p);
         for (void* p : {(void*)h_dq, (void*)h_qf, (void*)h_ff, (void*)h_fc, (void*)h_cnt})
             if (p) cudaFreeHost(p);
@@ -1452,8 +1457,8 @@ bool per_element_field(const wmc_level& L) {
 }
 
 void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
-    if (coarse && coarse->tab.nq != fine->tab.nq) throw ConfigError("wmc_eval_pairs: QoI sizes differ");
     if (!fine) throw ConfigError("eval_pairs: fine level is NULL");
+    if (coarse && coarse->tab.nq != fine->tab.nq) throw ConfigError("wmc_eval_pairs: QoI sizes differ");
     if (!coarse) return;
     if (fine->device != coarse->device) throw ConfigError("eval_pairs: levels on different devices");
     const auto& a = fine->spec;
@@ -1590,6 +1595,15 @@ void issue_pairs(wmc_level* fine, wmc_level* coarse, std::uint64_t seed, std::ui
                 if (src[f])
                     check(cudaMemcpyAsync(fine->r_cnt + f * cap_r + off, src[f], sizeof(int) * c,
                                           cudaMemcpyDeviceToDevice, st), "counters");
+        }
+        if (!to_host) {  // device-resident: fold the batch's failures into the level's record
+            if (!fine->d_fail_rec) {
+                check(cudaMalloc(&fine->d_fail_rec, 2 * sizeof(unsigned long long)), "cudaMalloc fail record");
+                check(cudaMemsetAsync(fine->d_fail_rec, 0xff, 2 * sizeof(unsigned long long), st), "fail record");
+            }
+            fine->fail_level = static_cast<int>(level);
+            wmc::launch_fail_fold(wf.fail, wc ? wc->fail : nullptr, c, first + off, fine->d_fail_rec, st);
+            ++g_launches;
         }
         if (to_host) {
             check(cudaMemcpyAsync(fine->r_ff + off, wf.fail, sizeof(int) * c, cudaMemcpyDeviceToDevice, st), "fail");
@@ -2327,12 +2341,37 @@ void wmc_level_destroy(wmc_level* L) { delete L; }
 
 void* wmc_level_stream(wmc_level* L) { return L ? static_cast<void*>(L->stream) : nullptr; }
 
+// Waits for the level's stream and reports the first failing sample of the
+// device-resident pairs issued since the last call (wmc_eval_pairs_device
+// folds every batch's check_finite flags into the level's record), as
+// finish_pairs does for the host path; the record is cleared.
 int wmc_synchronize(wmc_level* L, wmc_error* err) {
-    (void)err;
     return guarded([&] {
         if (!L) throw ConfigError("wmc_synchronize: NULL level");
         check(cudaSetDevice(L->device), "cudaSetDevice");
         check(cudaStreamSynchronize(L->stream), "synchronize");
+        if (err) {
+            err->sample = -1;
+            err->step = 0;
+            err->level = L->fail_level;
+        }
+        if (!L->d_fail_rec) return;
+        unsigned long long rec[2];
+        check(cudaMemcpy(rec, L->d_fail_rec, sizeof(rec), cudaMemcpyDeviceToHost), "fail record");
+        if (rec[0] == ~0ull && rec[1] == ~0ull) return;
+        check(cudaMemset(L->d_fail_rec, 0xff, sizeof(rec)), "fail record");
+        // the lower sample index first (the fine solve of a pair runs first)
+        const bool fine_first = rec[0] >> 24 <= rec[1] >> 24;
+        const unsigned long long r = fine_first ? rec[0] : rec[1];
+        const long sample = static_cast<long>(r >> 24);
+        if (err) {
+            err->sample = sample;
+            err->step = static_cast<int>(r & 0xffffff);
+            err->level = fine_first ? L->fail_level : L->fail_level - 1;
+        }
+        g_last_error = "level " + std::to_string(L->fail_level) + ", sample " + std::to_string(sample) +
+                       ": time integration unstable";
+        throw NumericalError(g_last_error);
     });
 }
 
@@ -2548,6 +2587,8 @@ int wmc_moments_device(wmc_level* level, const double* d_dq, const double* d_q, 
     return guarded([&] {
         if (!level || !d_dq || !d_q || !d_out) throw ConfigError("wmc_moments_device: NULL argument");
         if (count > static_cast<std::uint64_t>(INT_MAX)) throw ConfigError("wmc_moments_device: count too large");
+        if (level->tab.nq != 1)
+            throw ConfigError("wmc_moments_device: scalar QoI levels only (QoI vectors fold on the host)");
         check(cudaSetDevice(level->device), "cudaSetDevice");
         wmc::launch_moments(d_dq, d_q, static_cast<int>(count), d_out, level->stream);
         ++g_launches;

@@ -5,7 +5,10 @@
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 
 #include "kernels.cuh"
 
@@ -2496,6 +2499,19 @@ __global__ void pair_diff_kernel(const double* qf, const double* qc, double* dq,
     if (q_out) q_out[dst] = qf[src];
 }
 
+// Device-resident results: the first failing sample of a batch (lowest
+// index, then step) folded into a per-level record key = index << 24 | step,
+// read back by wmc_synchronize (reference check_finite -> InstabilityError,
+// src/integrators.cpp:12-18, wrapped per sample as src/mlmc.cpp:31-35)
+__global__ void fail_fold_kernel(const int* __restrict__ ff, const int* __restrict__ fc, int count,
+                                 unsigned long long first, unsigned long long* rec) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int sf = ff[i], sc = fc ? fc[i] : INT_MAX;
+    if (sf != INT_MAX) atomicMin(rec, ((first + i) << 24) | static_cast<unsigned long long>(min(sf, 0xffffff)));
+    if (sc != INT_MAX) atomicMin(rec + 1, ((first + i) << 24) | static_cast<unsigned long long>(min(sc, 0xffffff)));
+}
+
 // K3b: per-level moment sums, one block, fixed-order tree: deterministic for
 // a given count (LevelAccumulator::add, reference src/mlmc.cpp:44-53)
 __global__ void __launch_bounds__(1024) moments_kernel(const double* __restrict__ dq, const double* __restrict__ q,
@@ -2545,6 +2561,11 @@ __global__ void __launch_bounds__(1024) moments_kernel(const double* __restrict_
 }
 
 }  // namespace
+
+void launch_fail_fold(const int* ff, const int* fc, int count, unsigned long long first, unsigned long long* rec,
+                      void* stream) {
+    fail_fold_kernel<<<(count + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(ff, fc, count, first, rec);
+}
 
 void launch_moments(const double* dq, const double* q, int count, double* out, void* stream) {
     moments_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(dq, q, count, out);
@@ -2625,15 +2646,28 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
     }
 }
 
+// cudaFuncSetAttribute applies per device: remember what was set for each
+// (kernel, device) pair, so a process driving several devices configures each
+template <class Kern>
+static int smem_attr_once(Kern kernel, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+    const auto it = done.find(key);
+    if (it != done.end()) return it->second;
+    const int r = static_cast<int>(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done[key] = r;
+    return r;
+}
+
 int substep_smem_bytes(const SubArgs& a) { return static_cast<int>(sub_layout(a, nullptr, nullptr)); }
 
 template <int RPT>
 static int launch_sub_rpt(const SubArgs& a, int grid, int smem, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(substep_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+    smem_attr_once(substep_kernel<RPT>, 227 * 1024);
     substep_kernel<RPT><<<grid, kSubThreads, smem, st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
@@ -2660,11 +2694,7 @@ int lattice_smem_bytes(const LatArgs& a) { return lat_offsets(a).total * static_
 
 template <int T, int K, int G>
 static int launch_lat(const LatArgs& a, int grid, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(lattice_substep_kernel<T, K, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+    smem_attr_once(lattice_substep_kernel<T, K, G>, 227 * 1024);
     lattice_substep_kernel<T, K, G><<<grid, T, lattice_smem_bytes(a), st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
@@ -2750,13 +2780,9 @@ int small_max_smem(int device) {
 }
 
 int launch_small_solve(const SmallArgs& a, int grid, void* stream) {
-    static int configured = -1;
-    if (configured < 0) {
-        int device = 0;
-        cudaGetDevice(&device);
-        configured = static_cast<int>(
-            cudaFuncSetAttribute(small_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, small_max_smem(device)));
-    }
+    int device = 0;
+    cudaGetDevice(&device);
+    const int configured = smem_attr_once(small_solve_kernel, small_max_smem(device));
     if (configured != 0) return configured;
     small_solve_kernel<<<grid, kSmallThreads, small_smem_bytes(a), static_cast<cudaStream_t>(stream)>>>(a);
     return static_cast<int>(cudaGetLastError());
@@ -2781,14 +2807,9 @@ int lattice_solve_max_smem(int device) {
 
 template <int T, int K, int G, bool TM, bool VT, bool PK = false>
 static int launch_lat_solve(const LatSolveArgs& a, int grid, cudaStream_t st) {
-    static int configured = -1;
-    if (configured < 0) {
-        int device = 0;
-        cudaGetDevice(&device);
-        configured = static_cast<int>(cudaFuncSetAttribute(lattice_solve_kernel<T, K, G, TM, VT, PK>,
-                                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           lattice_solve_max_smem(device)));
-    }
+    int device = 0;
+    cudaGetDevice(&device);
+    const int configured = smem_attr_once(lattice_solve_kernel<T, K, G, TM, VT, PK>, lattice_solve_max_smem(device));
     if (configured != 0) return configured;
     lattice_solve_kernel<T, K, G, TM, VT, PK><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
     return static_cast<int>(cudaGetLastError());

@@ -413,5 +413,7 @@ int lattice_smem_bytes(const LatArgs& a);
 int launch_lattice_substeps(const LatArgs& a, int grid, void* stream);  // returns cudaError_t
 // deterministic single-block fold of (dq, q) into out[0..3] += {sum dq, sum dq^2, sum q, sum q^2}
 void launch_moments(const double* dq, const double* q, int count, double* out, void* stream);
+void launch_fail_fold(const int* ff, const int* fc, int count, unsigned long long first, unsigned long long* rec,
+                      void* stream);
 
 }  // namespace wmc
