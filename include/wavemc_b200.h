@@ -132,7 +132,8 @@ typedef struct {
     double dof_updates_per_solve;  /* n + (n_steps-1)(n + sum_k (p^k - p^(k-1))|R_k|) for LTS, n_steps*n for LF */
     int lattice;              /* 1: substeps use the structured refined-square kernel */
     int substep_path;         /* 0 none (LF or p = 1), 1 lattice, 2 generic on-chip, 3 HBM-resident,
-                                 4 HBM-resident nested tiers; -1 plan only */
+                                 4 HBM-resident nested tiers, 5 tiled (R in spatial tiles, every
+                                 substep of a step on chip); -1 plan only */
     int tiers;                /* nested LTS tiers in use */
     int n_r_tier[8];          /* |R_k| for tiers k = 1..tiers (n_r_tier[0] == n_r), rows [0, |R_k|) */
     long n_structured;        /* sweep rows taking the structured 5-point path (0 before device setup) */

@@ -22,6 +22,7 @@
 #include "host/channel.hpp"
 #include "host/field.hpp"
 #include "host/level.hpp"
+#include "host/tiles.hpp"
 #include "host/mesh.hpp"
 #include "kernels.cuh"
 
@@ -108,7 +109,7 @@ struct Workspace {
 
 constexpr int kEigBlocks = 64;  // row blocks of the power-iteration dot products
 
-enum class SubPath { None, Lattice, OnChip, Global, Tiers };
+enum class SubPath { None, Lattice, OnChip, Global, Tiers, Tiled };
 
 struct wmc_level {
     int device = 0;
@@ -152,6 +153,11 @@ struct wmc_level {
     int* d_apg_ptr = nullptr;
     int* d_apg_ent = nullptr;
     double* d_apg_a0 = nullptr;
+    // temporally blocked step on R (SubPath::Tiled, host/tiles.hpp)
+    wmc::TileArgs tile{};          // static part of the kernel arguments
+    std::vector<void*> tile_bufs;
+    int tile_smem = 0;
+    double tile_work = 0.0;        // region positions per box node (diagnostics)
     // nested tiers: A P_k on R_k per tier, substep constants
     std::vector<int*> d_tier_ptr, d_tier_ent;
     std::vector<double*> d_tier_a0;
@@ -248,6 +254,7 @@ struct wmc_level {
                         (void*)d_cell_ix})
             if (p) cudaFree(p);
         for (void* p : ch_bufs) cudaFree(p);
+        for (void* p : tile_bufs) cudaFree(p);
         for (auto* p : d_tier_ptr) cudaFree(p);
         for (auto* p : d_tier_ent) cudaFree(p);
         for (auto* p : d_tier_a0) cudaFree(p);
@@ -527,7 +534,7 @@ void build_device_level(wmc_level& L) {
         for (const auto& v : t.tier_cm) cm.insert(cm.end(), v.begin(), v.end());
         L.d_tier_cm = upload(cm);
         L.d_beta = upload(t.beta);
-    } else if (lts && (fp == "global" || !onchip_fits ||
+    } else if (lts && (fp == "global" || fp == "tiled" || !onchip_fits ||
                        // p = 2 levels too large for the fused solve: the single
                        // substep of the HBM/L2-resident kernel also forms z_{n+1}
                        // (no per-sample weight set-up, no separate R update);
@@ -536,11 +543,78 @@ void build_device_level(wmc_level& L) {
                         16.0 * t.n + 16.0 * (t.n_r + 16) > 227.0 * 1024.0))) {
         if (t.n > wmc::kColMask) throw ConfigError("level: more than 2^23 DOFs");
         L.path = SubPath::Global;
-        L.d_apg_ptr = upload(t.apg_ptr);
-        L.d_apg_ent = upload(t.apg_ent);
-        L.d_apg_a0 = upload(t.apg_a0);
+        // the temporally blocked step when the level has a refined box (R in
+        // tiles, every substep on chip); WMC_TILED=0 keeps the HBM-resident
+        // substeps (A/B), WMC_SUBSTEP_PATH=global as well
+        const char* tiled_env = std::getenv("WMC_TILED");
+        if (fp != "global" && !(tiled_env && std::atoi(tiled_env) == 0) && !L.d_cell_ix) {
+            wmc::TilePlan plan = wmc::plan_tiles(t, wmc::kTileWz, wmc::kTileHz, wmc::kTileK);
+            if (std::getenv("WMC_DEBUG_TILES"))
+                std::fprintf(stderr, "tile plan: ok=%d layout=%s reason=%s tiles=%d max_gen=%d max_app=%d "
+                             "max_ent=%d work=%.3f\n", plan.ok, plan.layout.c_str(), plan.reason.c_str(),
+                             plan.n_tiles, plan.max_gen, plan.max_app, plan.max_ent, plan.work_factor);
+            if (plan.ok) {
+                auto up = [&](const auto& v) {
+                    auto* p = upload(v);
+                    L.tile_bufs.push_back(static_cast<void*>(p));
+                    return p;
+                };
+                wmc::TileArgs& a = L.tile;
+                std::vector<int4> rect(plan.n_tiles), oj(plan.n_tiles);
+                for (int q = 0; q < plan.n_tiles; ++q) {
+                    rect[q] = make_int4(plan.i0[q], plan.j0[q], plan.oi0[q], plan.oi1[q]);
+                    oj[q] = make_int4(plan.oj0[q], plan.oj1[q], plan.tiles_shape[q], 0);
+                }
+                a.p = t.p;
+                a.m = t.lat_m;
+                a.n_cells = t.n_cells;
+                a.cells_x = L.spec.cells_x;
+                a.box_slots = plan.box_slots;
+                a.max_app = plan.max_app;
+                a.max_ent = plan.max_ent;
+                a.max_gen = plan.max_gen;
+                a.n_tiles = plan.n_tiles;
+                a.inv_h = t.lat_inv_h;
+                a.h = 1.0 / t.lat_inv_h;
+                a.inv_h2 = t.lat_inv_h * t.lat_inv_h;
+                a.c0 = t.c0;
+                a.tile_rect = up(rect);
+                a.tile_oj = up(oj);
+                a.gen_off = up(plan.gen_off);
+                a.g_slot = up(plan.g_slot);
+                a.g_dof = up(plan.g_dof);
+                a.g_owned = up(plan.g_owned);
+                a.g_rs = up(plan.g_rs);
+                a.g_ent_off = up(plan.g_ent_off);
+                a.g_rem_off = up(plan.g_rem_off);
+                a.e_slot = up(plan.e_slot);
+                a.e_rc_off = up(plan.e_rc_off);
+                a.rc_cell = up(plan.rc_cell.empty() ? std::vector<int>{0} : plan.rc_cell);
+                a.rc_a0 = up(plan.rc_a0.empty() ? std::vector<double>{0.0} : plan.rc_a0);
+                a.r_dof = up(plan.r_dof.empty() ? std::vector<int>{0} : plan.r_dof);
+                a.r_rc_off = up(plan.r_rc_off);
+                a.rr_cell = up(plan.rr_cell.empty() ? std::vector<int>{0} : plan.rr_cell);
+                a.rr_a0 = up(plan.rr_a0.empty() ? std::vector<double>{0.0} : plan.rr_a0);
+                std::vector<unsigned char> lr(plan.line_row.begin(), plan.line_row.end());
+                a.line_row = up(lr);
+                a.cellx = up(t.lat_cellx);
+                a.celly = up(t.lat_celly);
+                a.beta = up(t.beta);
+                a.cm = up(t.cm);
+                L.tile_smem = wmc::tile_smem_bytes(a);
+                L.tile_work = plan.work_factor;
+                int optin = 0;
+                cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, L.device);
+                if (L.tile_smem + 64 <= optin) L.path = SubPath::Tiled;
+            }
+        }
+        if (L.path == SubPath::Global) {
+            L.d_apg_ptr = upload(t.apg_ptr);
+            L.d_apg_ent = upload(t.apg_ent);
+            L.d_apg_a0 = upload(t.apg_a0);
+        }
     }
-    if (lts && L.path != SubPath::Global && L.path != SubPath::Tiers) {
+    if (lts && L.path != SubPath::Global && L.path != SubPath::Tiers && L.path != SubPath::Tiled) {
         const int n_slices = (t.n_r + 31) / 32;
         std::vector<int> soff(n_slices + 1, 0);
         std::vector<std::uint32_t> sent;
@@ -859,7 +933,7 @@ Workspace& workspace(wmc_level& L, int role) {
         };
         alloc(&w.za, S * t.n);
         alloc(&w.zb, S * t.n);
-        alloc(&w.g, S * static_cast<std::size_t>(g_stride(t)));
+        if (L.path != SubPath::Tiled) alloc(&w.g, S * static_cast<std::size_t>(g_stride(t)));  // tiled: g on chip
         alloc(&w.fail, S);
         alloc(&w.q, S * t.nq);
         if (L.path == SubPath::Global) {
@@ -1112,9 +1186,11 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
     const bool lts = L.path != SubPath::None;
     const bool global = L.path == SubPath::Global;
     const bool tiers = L.path == SubPath::Tiers;
+    const bool tiled = L.path == SubPath::Tiled;
     wmc::launch_fill_int(ws.fail, INT_MAX, S, stream);
 
     wmc::SweepArgs sw{};
+    sw.sample_major = tiled ? 1 : 0;  // the tiled step reads one sample's region contiguously
     sw.wide = L.sweep_wide;
     sw.n = t.n;
     sw.S = S;
@@ -1180,6 +1256,7 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
         sw.g_stride = g_stride(t);
         sw.g_node_major = (global || tiers) ? 1 : 0;
         sw.split = lts ? t.n_r : 0;
+        sw.row_begin = tiled ? t.n_r : 0;  // the tiled step owns R
         sw.factor = t.coarse_factor;
         sw.step = static_cast<int>(s + 1);
         if (L.profile) mark(L, L.ev_sweep, stream);
@@ -1190,7 +1267,23 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
         }
         if (L.profile) mark(L, L.ev_sweep, stream);
         ++g_launches;
-        if (tiers) {
+        if (tiled) {
+            if (L.profile) mark(L, L.ev_sub, stream);
+            wmc::TileArgs ta = L.tile;
+            ta.S = S;
+            ta.count = count;
+            ta.cells = cells;
+            ta.zc = cur;
+            ta.zp = prev;
+            ta.n = t.n;
+            ta.fail = ws.fail;
+            ta.step = static_cast<int>(s + 1);
+            const long items = static_cast<long>(ta.n_tiles) * count;
+            const int e = wmc::launch_tile_step(ta, static_cast<int>(std::min<long>(items, L.n_sms)), stream);
+            if (e != 0) check(static_cast<cudaError_t>(e), "tiled step launch");
+            ++g_launches;
+            if (L.profile) mark(L, L.ev_sub, stream);
+        } else if (tiers) {
             if (L.profile) mark(L, L.ev_sub, stream);
             run_tiers(L, ws, cells, S, count, cur, prev, static_cast<int>(s + 1), rel, nsteps, stream);
             if (L.profile) mark(L, L.ev_sub, stream);
@@ -1265,6 +1358,8 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
     qa.z_alt = prev;
     qa.nsteps = nsteps;
     qa.n_max = static_cast<int>(n_steps);
+    qa.n = t.n;
+    qa.sample_major = tiled ? 1 : 0;
     wmc::launch_qoi(qa, stream);
     ++g_launches;
     check(cudaGetLastError(), "kernel launch");

@@ -199,7 +199,19 @@ std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const
             break;
         }
     }
-    if (!threads) return fail("too many strips for the CTA");
+    // the box geometry holds either way (the tiled step kernel uses it);
+    // the single-CTA lattice kernels need every strip in one CTA
+    L.box = true;
+    L.lat_m = m;
+    L.lat_inv_h = 1.0 / h;
+    L.lat_cellx = cx;
+    L.lat_celly = cy;
+    L.lat_row = lat_row;
+    if (!threads) {
+        L.lattice = false;
+        L.lattice_reason = "too many strips for the CTA";
+        return box;
+    }
     L.lat_threads = threads;
     L.lat_k = kmax;
     L.lattice = true;
@@ -369,6 +381,14 @@ static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables
             if (!g.boundary[v] && in_r[v] && (tiers == 1 || rt[v] >= k)) ++L.n_r_tier[k - 1];
     L.n = static_cast<int>(L.dof_vertex.size());
     if (L.n == 0) throw std::invalid_argument("level: mesh has no interior vertices");
+    if (L.box) {  // box-local lattice coordinates of every dof (tiled step kernel)
+        L.dof_lx.resize(L.n);
+        L.dof_ly.resize(L.n);
+        for (int i = 0; i < L.n; ++i) {
+            L.dof_lx[i] = mesh->lattice[L.dof_vertex[i]][0] - mesh->fine_box_lo;
+            L.dof_ly[i] = mesh->lattice[L.dof_vertex[i]][1] - mesh->fine_box_lo;
+        }
+    }
     // the reference's stored entries: from_triplets keeps every (row, col)
     // pair an element couples, zero sums included (include/wavemc/sparse.hpp:17-40),
     // restricted to interior rows and columns; a_fine keeps the P columns

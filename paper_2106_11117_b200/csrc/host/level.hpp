@@ -133,6 +133,8 @@ struct LevelTables {
     // and kappa = mean coefficient of the two triangles on an edge; every
     // other R row ("generic") keeps explicit per-entry recipes.
     bool lattice = false;
+    bool box = false;                       // box geometry valid (dofs [0, (m+1)^2) = box, column major)
+    std::vector<int> dof_lx, dof_ly;        // box-local lattice coordinates of every dof (when box)
     int lat_m = 0;
     double lat_inv_h = 0.0;
     std::vector<int> lat_cellx, lat_celly;  // coefficient column / row of square column i / row j

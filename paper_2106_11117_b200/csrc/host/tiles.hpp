@@ -1,0 +1,73 @@
+// Spatial tiling of R for the temporally blocked LF-LTS step (config 3 and
+// any box level whose R does not fit one SM).
+//
+// One global step of the reference's lts_step (src/integrators.cpp:117-157)
+// on the rows of R needs, for an owned set O of R rows, d_p on O only; d_p
+// depends on d_{p-1} on the P-neighbours of O, ..., d_1 = -c0 A z_n on the
+// rows within p - 1 hops, and z_n one hop further.  A tile therefore owns a
+// rectangle of the refined-square lattice (plus the R rows outside the box
+// closest to it) and computes all p substeps on the rectangle grown by a
+// halo, keeping every intermediate on chip; values near the halo's outer
+// edge are wrong (their neighbours are missing) but the error travels one
+// hop per substep and never reaches O.  The planner checks exactly that on
+// the level's graph: every "source" of a wrong value (a lattice position
+// whose stencil leaves the rectangle, a generic row with a P-column outside
+// the tile) must be at least p hops from every owned row.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "level.hpp"
+
+namespace wmc {
+
+struct TilePlan {
+    bool ok = false;
+    std::string reason;
+    // region geometry (fixed per plan): Wz x Hz box positions, thread = 2
+    // columns x K rows; local slot of region column c, row r:
+    //   colpos(c) * kTileHs + r + 1, colpos(c) = c even ? c/2 + 1 : Wz/2 + 2 + c/2
+    // (even and odd columns apart, guard columns 0, Wz/2 + 1, Wz + 2; guard
+    // rows 0 and Hz + 1), generic rows outside the box at kTileBoxSlots + k
+    // shapes: 0 wide (wz columns x hz rows), 1 tall (hz columns x wz rows)
+    int wz = 0, hz = 0, k = 0;
+    int hs = 0;          // column stride of the wide shape (odd); the tall one uses (wz + 2) | 1
+    int jres = 0;        // region row origins are = jres (mod k)
+    std::string layout;  // "grid" or "frame"
+    int box_slots = 0;   // slots of the region rectangle incl. guards
+    int max_gen = 0;     // generic rows per tile (<= threads)
+    int max_app = 0;     // appended (outside-rectangle) slots per tile
+    int max_ent = 0;     // generic SELL entries per tile
+    int n_tiles = 0;
+    // per tile
+    std::vector<int> tiles_shape;       // 0 wide, 1 tall
+    std::vector<int> i0, j0;            // region origin (box coordinates, may be < 0)
+    std::vector<int> oi0, oi1, oj0, oj1;  // owned rectangle [oi0, oi1) x [oj0, oj1) (box coordinates)
+    std::vector<int> gen_off;           // generic rows of tile t: [gen_off[t], gen_off[t+1])
+    // per generic row
+    std::vector<int> g_slot, g_dof, g_owned, g_ent_off, g_rem_off;  // ent / rem offsets: [off[r], off[r+1])
+    std::vector<double> g_rs;
+    // per generic SELL entry (P columns): local slot of the column, and the
+    // weight recipe w = sum_t c[cell_t] a0_t (a0 already times sqrt(M_col))
+    std::vector<int> e_slot, e_rc_off;
+    std::vector<int> rc_cell;
+    std::vector<double> rc_a0;
+    // per remainder entry (columns outside P: z_n read from HBM): dof and
+    // recipe A_ij = sum_t c[cell_t] a0_t
+    std::vector<int> r_dof, r_rc_off;
+    std::vector<int> rr_cell;
+    std::vector<double> rr_a0;
+    // line rows: box rows j in [1, m-1] starting a new coefficient row; a
+    // strip starting on one takes separate first-row conductances
+    std::vector<std::uint8_t> line_row;  // per box row
+    double work_factor = 0.0;           // region positions per owned lattice node (diagnostics)
+};
+
+// Plans the tiling for a box level (t.box) with the fixed kernel shape
+// (region wz x hz, K rows per strip).  ok = false (with reason) when the
+// level does not qualify or a tile fails the halo check.
+TilePlan plan_tiles(const LevelTables& t, int wide, int narrow, int k);
+
+}  // namespace wmc

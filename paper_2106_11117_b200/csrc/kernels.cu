@@ -458,8 +458,8 @@ template <int R>
 __global__ void __launch_bounds__(kSweepWarps * 32, WMC_SWEEP_MINB) sweep_rows_kernel(SweepArgs a) {
     __shared__ double2 tile[kSweepWarps * R][32];  // g of the block's R rows: [row][lane]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int groups = (a.n + kSweepWarps * R - 1) / (kSweepWarps * R);
-    const int row0 = (blockIdx.x % groups) * kSweepWarps * R;
+    const int groups = (a.n - a.row_begin + kSweepWarps * R - 1) / (kSweepWarps * R);
+    const int row0 = a.row_begin + (blockIdx.x % groups) * kSweepWarps * R;
     const int chunk = blockIdx.x / groups;
     const int s0 = chunk * kSweepChunk + 2 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
@@ -570,6 +570,82 @@ __global__ void __launch_bounds__(kSweepWarps * 32, WMC_SWEEP_MINB) sweep_rows_k
     }
 }
 
+// K1, sample-major form (tiled levels, z[s * n + i]): thread per (row,
+// sample), consecutive rows in a warp, so a structured row's five loads are
+// coalesced along the rows of one sample.  Rows [row_begin, n) (the tiled
+// step owns R); kInit: every row, the start-up step.  Same products in the
+// same order as sweep_kernel.
+constexpr int kSmSamples = 4;  // samples per thread: the row's descriptor and entries serve four
+template <bool kInit>
+__global__ void __launch_bounds__(256) sweep_sm_kernel(SweepArgs a) {
+    const int row = (kInit ? 0 : a.row_begin) + blockIdx.x * 256 + threadIdx.x;
+    const int s0 = blockIdx.y * kSmSamples;
+    if (row >= a.n) return;
+    const std::size_t n = static_cast<std::size_t>(a.n);
+    const int4 d = __ldg(a.row_desc + row);
+    double acc[kSmSamples], zself[kSmSamples], zm[kSmSamples];
+    auto zat = [&](int u, int i) { return kInit ? __ldg(a.z0 + i) : __ldg(a.zc + (s0 + u) * n + i); };
+#pragma unroll
+    for (int u = 0; u < kSmSamples; ++u) {
+        acc[u] = 0.0;
+        zself[u] = zat(u, row);
+        zm[u] = kInit ? 0.0 : a.zp[(s0 + u) * n + row];
+    }
+    if (d.x >= 0 && ((d.x >> 16) & 0xff) > 0) {
+        const double2 w = __ldg(a.wtype + ((d.x >> 16) & 0xff) - 1);
+        const double* cp = a.cells + static_cast<std::size_t>(d.x & 0xffff) * a.S + s0;
+#pragma unroll
+        for (int u = 0; u < kSmSamples; ++u) {
+            double p0 = 0.0;
+            p0 += w.x * zat(u, row - d.z);
+            p0 += w.x * zat(u, row - 1);
+            p0 += w.y * zself[u];
+            p0 += w.x * zat(u, row + 1);
+            p0 += w.x * zat(u, row + d.w);
+            acc[u] = __ldg(cp + u) * p0;
+        }
+    } else {
+        const int b = d.y, e = __ldg(a.row_ptr + row + 1);
+        if (d.x >= 0) {
+            const double* cp = a.cells + static_cast<std::size_t>(d.x & 0xffff) * a.S + s0;
+            double p0[kSmSamples] = {};
+            for (int q = b; q < e; ++q) {
+                const double w = __ldg(a.a0 + q);
+                const int j = __ldg(a.ent + q) & a.col_mask;
+#pragma unroll
+                for (int u = 0; u < kSmSamples; ++u) p0[u] += w * zat(u, j);
+            }
+#pragma unroll
+            for (int u = 0; u < kSmSamples; ++u) acc[u] = __ldg(cp + u) * p0[u];
+        } else {
+            for (int q = b; q < e; ++q) {
+                const int pk = __ldg(a.ent + q);
+                const double w = __ldg(a.a0 + q);
+                const double* cp =
+                    a.cells + static_cast<std::size_t>(ent_cell(nullptr, q, pk, a.col_bits)) * a.S + s0;
+#pragma unroll
+                for (int u = 0; u < kSmSamples; ++u) acc[u] += (__ldg(cp + u) * w) * zat(u, pk & a.col_mask);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kSmSamples; ++u) {
+        const int s = s0 + u;
+        if (s >= a.count) break;
+        if (kInit) {
+            // z1 = z0 + dt M^{1/2} v0 + dt^2/2 (F0 - A z0), v0 = F = 0 (integrators.cpp:68-87)
+            const double out = zself[u] + a.factor * (0.0 - acc[u]);
+            a.zp[s * n + row] = zself[u];
+            a.zc_out[s * n + row] = out;
+            if (!(fabs(out) <= 1e100)) flag_fail(a.fail, s, a.count, a.step);
+        } else {
+            const double out = 2.0 * zself[u] - zm[u] - a.factor * acc[u];
+            a.zp[s * n + row] = out;
+            if (!(fabs(out) <= 1e100)) flag_fail(a.fail, s, a.count, a.step);  // check_finite (integrators.cpp:12-18)
+        }
+    }
+}
+
 // K1, wide form (fixed dt, S a multiple of 128): four samples per lane with
 // 256-bit loads and stores (LDG/STG.E.ENL2.256), 128 samples per warp, so
 // each load instruction moves 1 KB per warp and a warp's rows keep twice the
@@ -597,8 +673,8 @@ template <int R, int MINB>
 __global__ void __launch_bounds__(kSweepWarps * 32, MINB) sweep_wide_kernel(SweepArgs a) {
     __shared__ D4 tile[kSweepWarps * R][32];  // g of the block's R rows: [row][lane] = samples 4 lane .. 4 lane + 3
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int groups = (a.n + kSweepWarps * R - 1) / (kSweepWarps * R);
-    const int row0 = (blockIdx.x % groups) * kSweepWarps * R;
+    const int groups = (a.n - a.row_begin + kSweepWarps * R - 1) / (kSweepWarps * R);
+    const int row0 = a.row_begin + (blockIdx.x % groups) * kSweepWarps * R;
     const int chunk = blockIdx.x / groups;
     const int s0 = chunk * kSweepChunkW + 4 * lane;
     const std::size_t S = static_cast<std::size_t>(a.S);
@@ -2479,7 +2555,8 @@ __global__ void qoi_kernel(QoIArgs a) {
     const double* z = (a.nsteps && ((a.n_max - __ldg(a.nsteps + s)) & 1)) ? a.z_alt : a.z;
     for (int t = __ldg(a.ptr + k); t < __ldg(a.ptr + k + 1); ++t) {
         const int i = __ldg(a.dof + t);
-        acc += __ldg(a.w + t) * (z[i * S + s] / __ldg(a.sqrt_mass + t));
+        const std::size_t at = a.sample_major ? static_cast<std::size_t>(s) * a.n + i : i * S + s;
+        acc += __ldg(a.w + t) * (z[at] / __ldg(a.sqrt_mass + t));
     }
     a.q[k * S + s] = a.fail[s] == INT_MAX ? acc : __longlong_as_double(0x7ff8000000000000LL);
 }
@@ -2596,6 +2673,11 @@ void launch_draw_cells(std::uint64_t seed, std::uint32_t level, std::uint64_t fi
 }
 
 void launch_sweep_init(const SweepArgs& a, void* stream) {
+    if (a.sample_major) {
+        const dim3 g(static_cast<unsigned>((a.n + 255) / 256), static_cast<unsigned>(a.S / kSmSamples));
+        sweep_sm_kernel<true><<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+        return;
+    }
     const unsigned grid = ((a.n + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
     if (a.cell_ix)
         sweep_kernel<true, false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
@@ -2604,6 +2686,12 @@ void launch_sweep_init(const SweepArgs& a, void* stream) {
 }
 
 void launch_sweep_step(const SweepArgs& a, void* stream) {
+    if (a.sample_major) {
+        const dim3 g(static_cast<unsigned>((a.n - a.row_begin + 255) / 256),
+                     static_cast<unsigned>(a.S / kSmSamples));
+        sweep_sm_kernel<false><<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+        return;
+    }
     const unsigned grid = ((a.n + kSweepWarps - 1) / kSweepWarps) * (a.S / kSweepChunk);
     static const int parts = [] {
         const char* v = std::getenv("WMC_SWEEP_PARTS");  // tuning knob
@@ -2614,16 +2702,21 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
         return v ? std::atoi(v) : 0;
     }();
     const int wide = a.wide;
-    if (a.cell_ix) {  // cells in a separate per-entry array (narrow-channel levels)
+    // a row range (row_begin > 0) takes the descriptor forms below; the host
+    // selects it only for levels with descriptors and packed cells
+    if (a.row_begin > 0) {
+    } else if (a.cell_ix) {  // cells in a separate per-entry array (narrow-channel levels)
         sweep_kernel<false, false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     } else if (parts) {
         sweep_kernel<false, true><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     } else if (one_row || !a.row_desc) {
         sweep_kernel<false, false><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
-    } else if (wide && !a.rel && !a.nsteps && a.S % kSweepChunkW == 0) {
+    }
+    if (a.row_begin == 0 && (a.cell_ix || parts || one_row || !a.row_desc)) return;
+    if (wide && !a.rel && !a.nsteps && a.S % kSweepChunkW == 0) {
         // wide sweep (default for fixed dt): wide = 10 R + MINB
         const int r = wide / 10;
-        const unsigned g2 = ((a.n + kSweepWarps * r - 1) / (kSweepWarps * r)) * (a.S / kSweepChunkW);
+        const unsigned g2 = ((a.n - a.row_begin + kSweepWarps * r - 1) / (kSweepWarps * r)) * (a.S / kSweepChunkW);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         if (wide == 14)
             sweep_wide_kernel<1, 4><<<g2, kSweepWarps * 32, 0, st>>>(a);
@@ -2635,7 +2728,7 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
             return v ? std::atoi(v) : kSweepRowsDefault;
         }();
         const int rows = kSweepWarps * r;
-        const unsigned g2 = ((a.n + rows - 1) / rows) * (a.S / kSweepChunk);
+        const unsigned g2 = ((a.n - a.row_begin + rows - 1) / rows) * (a.S / kSweepChunk);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         if (r == 2)
             sweep_rows_kernel<2><<<g2, kSweepWarps * 32, 0, st>>>(a);
@@ -2648,14 +2741,13 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
 
 // cudaFuncSetAttribute applies per device: remember what was set for each
 // (kernel, device) pair, so a process driving several devices configures each
-template <class Kern>
-static int smem_attr_once(Kern kernel, int bytes) {
+int set_max_dynamic_smem(const void* kernel, int bytes) {
     static std::mutex mu;
     static std::map<std::pair<const void*, int>, int> done;
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
-    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+    const auto key = std::make_pair(kernel, dev);
     const auto it = done.find(key);
     if (it != done.end()) return it->second;
     const int r = static_cast<int>(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -2667,7 +2759,7 @@ int substep_smem_bytes(const SubArgs& a) { return static_cast<int>(sub_layout(a,
 
 template <int RPT>
 static int launch_sub_rpt(const SubArgs& a, int grid, int smem, cudaStream_t st) {
-    smem_attr_once(substep_kernel<RPT>, 227 * 1024);
+    set_max_dynamic_smem(reinterpret_cast<const void*>(substep_kernel<RPT>), 227 * 1024);
     substep_kernel<RPT><<<grid, kSubThreads, smem, st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
@@ -2694,7 +2786,7 @@ int lattice_smem_bytes(const LatArgs& a) { return lat_offsets(a).total * static_
 
 template <int T, int K, int G>
 static int launch_lat(const LatArgs& a, int grid, cudaStream_t st) {
-    smem_attr_once(lattice_substep_kernel<T, K, G>, 227 * 1024);
+    set_max_dynamic_smem(reinterpret_cast<const void*>(lattice_substep_kernel<T, K, G>), 227 * 1024);
     lattice_substep_kernel<T, K, G><<<grid, T, lattice_smem_bytes(a), st>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
@@ -2782,7 +2874,7 @@ int small_max_smem(int device) {
 int launch_small_solve(const SmallArgs& a, int grid, void* stream) {
     int device = 0;
     cudaGetDevice(&device);
-    const int configured = smem_attr_once(small_solve_kernel, small_max_smem(device));
+    const int configured = set_max_dynamic_smem(reinterpret_cast<const void*>(small_solve_kernel), small_max_smem(device));
     if (configured != 0) return configured;
     small_solve_kernel<<<grid, kSmallThreads, small_smem_bytes(a), static_cast<cudaStream_t>(stream)>>>(a);
     return static_cast<int>(cudaGetLastError());
@@ -2809,7 +2901,8 @@ template <int T, int K, int G, bool TM, bool VT, bool PK = false>
 static int launch_lat_solve(const LatSolveArgs& a, int grid, cudaStream_t st) {
     int device = 0;
     cudaGetDevice(&device);
-    const int configured = smem_attr_once(lattice_solve_kernel<T, K, G, TM, VT, PK>, lattice_solve_max_smem(device));
+    const int configured = set_max_dynamic_smem(
+        reinterpret_cast<const void*>(lattice_solve_kernel<T, K, G, TM, VT, PK>), lattice_solve_max_smem(device));
     if (configured != 0) return configured;
     lattice_solve_kernel<T, K, G, TM, VT, PK><<<grid, T, lattice_solve_smem_bytes(a), st>>>(a);
     return static_cast<int>(cudaGetLastError());

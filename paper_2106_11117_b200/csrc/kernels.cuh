@@ -90,6 +90,8 @@ struct SweepArgs {
     const double* rel;   // per-sample CFL: (dt_s / dt)^2 scales every dt^2 constant (NULL: 1)
     const int* nsteps;   // per-sample CFL: steps of sample s; later steps leave it untouched (NULL: all)
     int wide;            // step sweep form: 10 R + MINB of sweep_wide_kernel (fixed dt, S % 128 == 0), 0: sweep_rows_kernel
+    int row_begin;       // step sweeps: rows [row_begin, n) only (the tiled step owns R); 0: all rows
+    int sample_major;    // 1: z[s * n + i] (tiled levels: one sample's rows contiguous), 0: z[i * S + s]
 };
 
 struct SubArgs {
@@ -344,6 +346,8 @@ struct QoIArgs {
     const double* z_alt;  // per-sample CFL: a sample that ended (n_max - nsteps[s]) odd steps early
     const int* nsteps;    // holds its state in the other buffer
     int n_max;
+    int n;                // sample_major: z[s * n + i]
+    int sample_major;
 };
 
 // Per-sample CFL step (reference stable_dt, src/experiments.cpp:30-43): batched
@@ -395,6 +399,54 @@ int substep_smem_bytes(const SubArgs& a);
 int launch_substeps(const SubArgs& a, int grid, void* stream);  // returns cudaError_t
 void launch_qoi(const QoIArgs& a, void* stream);
 void launch_r_update(const RUpdateArgs& a, void* stream);
+
+// Temporally blocked LF-LTS step on R (host/tiles.hpp): one CTA per (tile,
+// sample) work item, persistent over items; the tile's region (kTileWz x
+// kTileHz box positions, or the transposed shape, plus generic rows) stays
+// on chip for the whole step:
+// z_n in, g = A z_n, the p - 1 substeps, z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on
+// the owned rows out.  Rows outside R are left to the sweep.
+constexpr int kTileThreads = 512;
+constexpr int kTileK = 8;     // rows per strip (thread = 2 columns x kTileK rows)
+constexpr int kTileWz = 128;  // region columns
+constexpr int kTileHz = 64;   // region rows
+struct TileArgs {
+    int S, count, p, m, n_cells, cells_x;
+    int box_slots, max_app, max_ent, max_gen, n_tiles;
+    double inv_h, h, inv_h2, c0;
+    const int4* tile_rect;   // per tile: region origin i0, j0; owned columns [oi0, oi1)
+    const int4* tile_oj;     // owned rows [oj0, oj1), shape (0: kTileWz x kTileHz, 1: kTileHz x kTileWz)
+    const int* gen_off;      // per tile: generic rows [gen_off[t], gen_off[t+1])
+    const int* g_slot;
+    const int* g_dof;
+    const int* g_owned;
+    const double* g_rs;      // 1 / sqrt(M)
+    const int* g_ent_off;    // SELL entries [off[r], off[r+1]) (P columns, local slots)
+    const int* g_rem_off;    // remainder entries [off[r], off[r+1]) (other columns, dofs)
+    const int* e_slot;
+    const int* e_rc_off;     // recipe of entry e: [e_rc_off[e], e_rc_off[e+1])
+    const int* rc_cell;
+    const double* rc_a0;     // a0 sqrt(M_col)
+    const int* r_dof;
+    const int* r_rc_off;
+    const int* rr_cell;
+    const double* rr_a0;
+    const unsigned char* line_row;  // per box row: starts a coefficient row
+    const int* cellx;        // per square column / row: coefficient column / row
+    const int* celly;
+    const double* cells;     // [k * S + s]
+    const double* beta;      // p - 1
+    const double* cm;        // p - 1
+    const double* zc;        // z_n, sample-major: z[s * n + i]
+    double* zp;              // z_{n-1} in, z_{n+1} out (owned R rows)
+    int n;
+    int* fail;
+    int step;
+};
+int tile_smem_bytes(const TileArgs& a);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+int set_max_dynamic_smem(const void* kernel, int bytes);
+int launch_tile_step(const TileArgs& a, int grid, void* stream);  // returns cudaError_t
 void launch_global_substep(const GSubArgs& a, void* stream);
 void launch_tier_stage(const TierArgs& a, void* stream);
 void launch_fill_int(int* p, int value, int n, void* stream);

@@ -1,0 +1,572 @@
+// Temporally blocked LF-LTS step on R (sm_100a, FP64): one global step of
+// the reference's lts_step (src/integrators.cpp:117-157) for the rows of R,
+// a spatial tile at a time, with every substep on chip.
+//
+// A work item is (tile, sample).  Its region is kTileWz x kTileHz positions
+// of the refined-square lattice around the tile's owned rectangle plus the
+// tile's generic rows (box ring, R rows outside the box; host/tiles.hpp).
+//   1. z_n of the region in:        v = z / sqrt(M)  (shared memory, buffer 0)
+//   2. g = A z_n:                   lattice 5-point stencil / generic SELL on
+//                                   v plus the non-P columns from HBM
+//   3. d_1 = -c0 g, then p - 1 substeps
+//      d_{m+1} = (1 + beta_m) d_m - beta_m d_{m-1} - c_m (g + A P d_m)
+//      with v double-buffered in shared memory (one barrier per substep)
+//   4. owned rows: z_{n+1} = 2 z_n - z_{n-1} + 2 d_p, check_finite.
+// Values near the region's edge are wrong (missing neighbours) but the
+// planner proved the error cannot travel to an owned row in p substeps.
+//
+// Thread = 2 adjacent columns x kTileK rows of the region (a strip).  A
+// lattice node keeps v = d / h (h = h_min, a power of two: v and d carry the
+// same bits scaled, so the recursion runs on v directly with conductances
+// scaled by 1 / h^2) in registers; g and v_{m-1} live in the thread's
+// tensor-memory columns (tcgen05.ld / st: their own datapath beside the
+// shared-memory pipe the stencil is bound by).  E/W neighbours come from the
+// other threads' columns in shared memory (even and odd columns stored apart,
+// so a warp's 32 loads hit 32 consecutive column positions: conflict-free),
+// N/S neighbours inside the strip from registers.  Generic rows keep d in
+// registers and publish v = d / sqrt(M).
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace wmc {
+namespace {
+
+constexpr int kT = kTileThreads;
+constexpr int kK = kTileK;
+constexpr int kTPC = kTileWz / 2;          // thread columns per strip row
+constexpr int kWarpsPerRow = kTPC / 32;
+static_assert(kTPC % 32 == 0 && kT == kTPC * (kTileHz / kK), "tile shape");
+
+__device__ __forceinline__ void t_ld16(std::uint32_t addr, std::uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+}
+__device__ __forceinline__ void t_st16(std::uint32_t addr, const std::uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+        "tcgen05.wait::st.sync.aligned;\n"
+        :
+        : "r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void t_ld8(std::uint32_t addr, std::uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void t_st8(std::uint32_t addr, const std::uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+                 "tcgen05.wait::st.sync.aligned;\n"
+                 :
+                 : "r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+__device__ __forceinline__ double t_dbl(const std::uint32_t* r) {
+    return __hiloint2double(static_cast<int>(r[1]), static_cast<int>(r[0]));
+}
+__device__ __forceinline__ void t_put(std::uint32_t* r, double d) {
+    r[0] = static_cast<std::uint32_t>(__double2loint(d));
+    r[1] = static_cast<std::uint32_t>(__double2hiint(d));
+}
+
+// conductances (scaled by 1 / h^2) of the thread's two columns: rows 1 ..
+// K-1 of a strip see one coefficient row (squares ia - 1, ia, ib)
+struct ColConst {
+    double kWa, kEa, kNSa, dga;  // column a (kWb = kEa)
+    double kEb, kNSb, dgb;       // column b
+};
+
+// row 0 of a strip starting on a coefficient line: conductances from the
+// coefficient rows above (U) and below (D) the line, recomputed from the
+// shared-memory cell table each time (only such warps take this path)
+struct LineCells {
+    int cu, cd, x0, x1, x2;
+};
+__device__ __forceinline__ void line_row0(const double* cl, const LineCells& lc, double s2, double va, double vb,
+                                          double vWa, double vEb, double vNa, double vSa, double vNb, double vSb,
+                                          double& aqa, double& aqb) {
+    const double U0 = cl[lc.cu + lc.x0], U1 = cl[lc.cu + lc.x1], U2 = cl[lc.cu + lc.x2];
+    const double D0 = cl[lc.cd + lc.x0], D1 = cl[lc.cd + lc.x1], D2 = cl[lc.cd + lc.x2];
+    const double h2 = 0.5 * s2;
+    const double kEa = (U1 + D1) * h2, kWa = (U0 + D0) * h2, kNa = (U0 + U1) * h2, kSa = (D0 + D1) * h2;
+    const double kEb = (U2 + D2) * h2, kNb = (U1 + U2) * h2, kSb = (D1 + D2) * h2;
+    aqa = (kEa + kWa + kNa + kSa) * va - kEa * vb - kWa * vWa - kNa * vNa - kSa * vSa;
+    aqb = (kEb + kEa + kNb + kSb) * vb - kEb * vEb - kEa * va - kNb * vNb - kSb * vSb;
+}
+
+// A v on the thread's two columns, row k (v units): column a's E neighbour is
+// column b and column b's W neighbour column a (registers); the far sides
+// from shared memory; S from the previous row (pa / pb: that row's values
+// before this substep overwrote them), N from the next row or the strip end
+template <int k>
+__device__ __forceinline__ void lattice_row(const double (&va)[kK], const double (&vb)[kK], double pa, double pb,
+                                            double na_end, double nb_end, double vWa, double vEb, const ColConst& c,
+                                            bool line, const double* cl, const LineCells& lc, double s2,
+                                            double& aqa, double& aqb) {
+    const double vNa = k + 1 < kK ? va[k + 1 < kK ? k + 1 : 0] : na_end;
+    const double vNb = k + 1 < kK ? vb[k + 1 < kK ? k + 1 : 0] : nb_end;
+    if (k == 0 && line) {
+        line_row0(cl, lc, s2, va[k], vb[k], vWa, vEb, vNa, pa, vNb, pb, aqa, aqb);
+        return;
+    }
+    aqa = c.dga * va[k] - c.kEa * vb[k] - c.kWa * vWa - c.kNSa * (vNa + pa);
+    aqb = c.dgb * vb[k] - c.kEb * vEb - c.kEa * va[k] - c.kNSb * (vNb + pb);
+}
+
+// TMEM layout per thread (128 columns): row pair q at 16 q: g of rows 2q,
+// 2q+1 of column a, of column b (8 columns), then v_{m-1} likewise (8);
+// then z_n of the next item's positions (64: column a, 80: column b; 16
+// columns each) and w = 2 z_n - z_{n-1} of this item's (96, 112)
+constexpr unsigned kTmZn = 64, kTmW = 96;
+
+// the thread's view of one work item
+struct ItemGeo {
+    int tile, s;
+    int wz, hz, HS;
+    int sa, sb, sWa, sEb;
+    int ia, ib, jr0;
+    unsigned lat, own;  // bit k: column a row k, bit 8 + k: column b
+};
+
+__device__ __forceinline__ ItemGeo item_geo(const TileArgs& a, int item, int warp, int lane) {
+    ItemGeo g;
+    g.tile = item / a.count;
+    g.s = item % a.count;
+    const int4 tr = __ldg(a.tile_rect + g.tile);
+    const int4 toj = __ldg(a.tile_oj + g.tile);
+    // region shape: wide (kTileWz columns, two warps per strip row) or tall
+    // (kTileHz columns, one warp per strip row); the same slot count
+    g.wz = toj.z ? kTileHz : kTileWz;
+    g.hz = toj.z ? kTileWz : kTileHz;
+    g.HS = g.hz + 3;
+    const int wpr = g.wz / 64;
+    const int strip = warp / wpr, tc = (warp % wpr) * 32 + lane;
+    const int pa = tc + 1, pb = g.wz / 2 + 2 + tc;  // column positions of the own columns
+    g.sa = pa * g.HS + strip * kK + 1;
+    g.sb = pb * g.HS + strip * kK + 1;
+    g.sWa = g.sb - g.HS;  // far neighbours: W of column a, E of column b
+    g.sEb = g.sa + g.HS;
+    g.ia = tr.x + 2 * tc;
+    g.ib = g.ia + 1;
+    g.jr0 = tr.y + strip * kK;
+    const int m = a.m;
+    const bool ca_in = g.ia >= 1 && g.ia <= m - 1, cb_in = g.ib >= 1 && g.ib <= m - 1;
+    const int klo = max(0, 1 - g.jr0), khi = min(kK, m - g.jr0);
+    g.lat = 0;
+    g.own = 0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const bool row_in = k >= klo && k < khi;
+        const int j = g.jr0 + k;
+        const bool row_own = j >= toj.x && j < toj.y;
+        if (row_in && ca_in) g.lat |= 1u << k;
+        if (row_in && cb_in) g.lat |= 1u << (8 + k);
+        if (row_in && ca_in && row_own && g.ia >= tr.z && g.ia < tr.w) g.own |= 1u << k;
+        if (row_in && cb_in && row_own && g.ib >= tr.z && g.ib < tr.w) g.own |= 1u << (8 + k);
+    }
+    return g;
+}
+
+// 8 z values of one column of an item's lattice positions (0 elsewhere)
+// (sample-major state: the column's 8 rows are 64 contiguous bytes)
+__device__ __forceinline__ void load_col(const double* __restrict__ z, const ItemGeo& g, int col, int W, int n,
+                                         double (&out)[kK]) {
+    const double* zs = z + static_cast<std::size_t>(g.s) * n + (col ? g.ib : g.ia) * W + g.jr0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) out[k] = (g.lat >> (8 * col + k)) & 1u ? __ldg(zs + k) : 0.0;
+}
+__device__ __forceinline__ void tm_put8(std::uint32_t addr, const double (&d)[kK]) {
+    std::uint32_t r[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) t_put(r + 2 * k, d[4 * h + k]);
+        t_st8(addr + 8 * h, r);
+    }
+}
+__device__ __forceinline__ void tm_get8(std::uint32_t addr, double (&d)[kK]) {
+    std::uint32_t r[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        t_ld8(addr + 8 * h, r);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d[4 * h + k] = t_dbl(r + 2 * k);
+    }
+}
+
+__global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
+    extern __shared__ __align__(16) double sd[];
+    __shared__ std::uint32_t tm_slot;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = a.m + 1, m = a.m;
+    const int buf = a.box_slots + a.max_app;
+    double* B0 = sd;
+    double* B1 = sd + buf;
+    double* wbuf = sd + 2 * buf;
+    double* gst = wbuf + a.max_ent;  // generic rows: d | d_{m-1} | g  (max_gen each)
+    double* cl = gst + 3 * a.max_gen;
+    double* kbeta = cl + a.n_cells;  // substep constants beta_m, c_m
+    double* kcm = kbeta + a.p;
+    for (int q = tid; q < a.p - 1; q += kT) {
+        kbeta[q] = __ldg(a.beta + q);
+        kcm[q] = __ldg(a.cm + q);
+    }
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const double s2 = a.inv_h2;
+    const double* __restrict__ zc = a.zc;
+    double* __restrict__ zp = a.zp;
+
+    // tensor memory: 512 columns (one CTA per SM); warp w: lanes 32 (w % 4)..,
+    // columns 128 (w / 4)..
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
+                     "tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n"
+                     :
+                     : "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&tm_slot)))
+                     : "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const std::uint32_t tb = tm_slot + (static_cast<std::uint32_t>(32 * (warp & 3)) << 16) + 128u * (warp >> 2);
+
+    const int items = a.n_tiles * a.count;
+    // software pipeline: an item's z_n and cell coefficients are loaded
+    // during the previous item's substeps (prologue: the first item here)
+    double cl_next = 0.0;
+    if (blockIdx.x < items) {
+        const ItemGeo g0 = item_geo(a, blockIdx.x, warp, lane);
+        double z[kK];
+        load_col(zc, g0, 0, W, a.n, z);
+        tm_put8(tb + kTmZn, z);
+        load_col(zc, g0, 1, W, a.n, z);
+        tm_put8(tb + kTmZn + 16, z);
+        if (tid < a.n_cells) cl_next = __ldg(a.cells + static_cast<std::size_t>(tid) * S + g0.s);
+    }
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const ItemGeo g = item_geo(a, item, warp, lane);
+        const int s = g.s;
+        const std::size_t zbase = static_cast<std::size_t>(s) * a.n;  // sample-major state
+        const int next_item = item + gridDim.x;
+        const bool has_next = next_item < items;
+        const int gb = __ldg(a.gen_off + g.tile), ng = __ldg(a.gen_off + g.tile + 1) - gb;
+        const bool partial = __any_sync(0xffffffffu, g.lat != 0xffffu);
+        const int sa = g.sa, sb = g.sb, sWa = g.sWa, sEb = g.sEb, HS = g.HS, wz = g.wz, hz = g.hz;
+        const unsigned lat = g.lat;
+
+        if (tid < a.n_cells) cl[tid] = cl_next;
+        __syncthreads();  // cl; and every reader of the previous item's buffers is done
+        // guards of this shape (zero; the previous item may have had the other
+        // shape): column positions 0, wz/2 + 1, wz + 2 and rows 0, hz + 1, hz + 2
+        for (int q = tid; q < 3 * HS; q += kT) {
+            const int pos = q / HS, r = q % HS;
+            const int col = pos == 0 ? 0 : (pos == 1 ? wz / 2 + 1 : wz + 2);
+            B0[col * HS + r] = 0.0;
+            B1[col * HS + r] = 0.0;
+        }
+        for (int q = tid; q < 3 * (wz + 3); q += kT) {
+            const int pos = q / 3, r = q % 3 == 0 ? 0 : hz + q % 3;
+            B0[pos * HS + r] = 0.0;
+            B1[pos * HS + r] = 0.0;
+        }
+
+        ColConst cc;
+        LineCells lc;
+        const bool line = g.jr0 >= 1 && g.jr0 <= m - 1 && __ldg(a.line_row + g.jr0);
+        {
+            const int q0 = min(max(g.ia - 1, 0), m - 1), q1 = min(max(g.ia, 0), m - 1),
+                      q2 = min(max(g.ib, 0), m - 1);
+            const int ru = min(max(g.jr0, 0), m - 1), rd = min(max(g.jr0 - 1, 0), m - 1);
+            lc.cu = __ldg(a.celly + ru) * a.cells_x;
+            lc.cd = __ldg(a.celly + rd) * a.cells_x;
+            lc.x0 = __ldg(a.cellx + q0);
+            lc.x1 = __ldg(a.cellx + q1);
+            lc.x2 = __ldg(a.cellx + q2);
+            const double U0 = cl[lc.cu + lc.x0], U1 = cl[lc.cu + lc.x1], U2 = cl[lc.cu + lc.x2];
+            cc.kWa = U0 * s2;
+            cc.kEa = U1 * s2;
+            cc.kNSa = (U0 + U1) * (0.5 * s2);
+            cc.dga = cc.kEa + cc.kWa + 2.0 * cc.kNSa;
+            cc.kEb = U2 * s2;
+            cc.kNSb = (U1 + U2) * (0.5 * s2);
+            cc.dgb = cc.kEb + cc.kEa + 2.0 * cc.kNSb;
+        }
+
+        // 1. z_n in (prefetched into TMEM): lattice positions v = z / h;
+        // positions outside the box 0 (both buffers); box ring positions
+        // belong to the generic rows
+        double va[kK], vb[kK];
+        tm_get8(tb + kTmZn, va);
+        tm_get8(tb + kTmZn + 16, vb);
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            const int j = g.jr0 + k;
+            const bool jin = j >= 0 && j <= m;
+            va[k] *= a.inv_h;
+            vb[k] *= a.inv_h;
+            if (lat & (1u << k)) {
+                B0[sa + k] = va[k];
+            } else if (!(jin && g.ia >= 0 && g.ia <= m)) {
+                B0[sa + k] = 0.0;
+                B1[sa + k] = 0.0;
+            }
+            if (lat & (1u << (8 + k))) {
+                B0[sb + k] = vb[k];
+            } else if (!(jin && g.ib >= 0 && g.ib <= m)) {
+                B0[sb + k] = 0.0;
+                B1[sb + k] = 0.0;
+            }
+        }
+        // generic rows (tid, tid + T, ...): z_n in, per-sample SELL weights
+        const int eb = __ldg(a.g_ent_off + gb);
+        for (int u = tid; u < ng; u += kT) {
+            const int r = gb + u;
+            B0[__ldg(a.g_slot + r)] = __ldg(zc + zbase + __ldg(a.g_dof + r)) * __ldg(a.g_rs + r);
+            for (int e = __ldg(a.g_ent_off + r); e < __ldg(a.g_ent_off + r + 1); ++e) {
+                double w = 0.0;
+                for (int t = __ldg(a.e_rc_off + e); t < __ldg(a.e_rc_off + e + 1); ++t)
+                    w += cl[__ldg(a.rc_cell + t)] * __ldg(a.rc_a0 + t);
+                wbuf[e - eb] = w;
+            }
+        }
+        __syncthreads();
+
+        // 2. g = A z_n (v units on the lattice), d_1 = -c0 g; TMEM: g, v_0 = 0
+        const double c0 = a.c0;
+        {
+            if (partial) {  // rows / columns outside the lattice read their ring or zero values
+#pragma unroll
+                for (int k = 0; k < kK; ++k) {
+                    if (!(lat & (1u << k))) va[k] = B0[sa + k];
+                    if (!(lat & (1u << (8 + k)))) vb[k] = B0[sb + k];
+                }
+            }
+            const double na_end = B0[sa + kK], nb_end = B0[sb + kK];
+            double pa_ = B0[sa - 1], pb_ = B0[sb - 1];
+#pragma unroll
+            for (int q = 0; q < kK / 2; ++q) {
+                std::uint32_t t[8], z[8];
+                double g2[2][2];
+#define WMC_TILE_G_ROW(K_, R_)                                                                              \
+                {                                                                                           \
+                    double ga, gbb;                                                                         \
+                    lattice_row<K_>(va, vb, pa_, pb_, na_end, nb_end, B0[sWa + K_], B0[sEb + K_], cc, line, \
+                                    cl, lc, s2, ga, gbb);                                                   \
+                    g2[R_][0] = ga;                                                                         \
+                    g2[R_][1] = gbb;                                                                        \
+                    pa_ = va[K_];                                                                           \
+                    pb_ = vb[K_];                                                                           \
+                }
+                if (q == 0) { WMC_TILE_G_ROW(0, 0) WMC_TILE_G_ROW(1, 1) }
+                if (q == 1) { WMC_TILE_G_ROW(2, 0) WMC_TILE_G_ROW(3, 1) }
+                if (q == 2) { WMC_TILE_G_ROW(4, 0) WMC_TILE_G_ROW(5, 1) }
+                if (q == 3) { WMC_TILE_G_ROW(6, 0) WMC_TILE_G_ROW(7, 1) }
+#undef WMC_TILE_G_ROW
+                t_put(t + 0, g2[0][0]);
+                t_put(t + 2, g2[1][0]);
+                t_put(t + 4, g2[0][1]);
+                t_put(t + 6, g2[1][1]);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) z[u] = 0u;
+                t_st8(tb + 16 * q, t);
+                t_st8(tb + 16 * q + 8, z);
+                va[2 * q] = -c0 * g2[0][0];
+                va[2 * q + 1] = -c0 * g2[1][0];
+                vb[2 * q] = -c0 * g2[0][1];
+                vb[2 * q + 1] = -c0 * g2[1][1];
+            }
+#pragma unroll
+            for (int k = 0; k < kK; ++k) {
+                if (lat & (1u << k)) B1[sa + k] = va[k];
+                if (lat & (1u << (8 + k))) B1[sb + k] = vb[k];
+            }
+        }
+        for (int u = tid; u < ng; u += kT) {
+            const int r = gb + u;
+            double acc = 0.0;
+            for (int e = __ldg(a.g_ent_off + r); e < __ldg(a.g_ent_off + r + 1); ++e)
+                acc += wbuf[e - eb] * B0[__ldg(a.e_slot + e)];
+            double rem = 0.0;
+            for (int e = __ldg(a.g_rem_off + r); e < __ldg(a.g_rem_off + r + 1); ++e) {
+                double w = 0.0;
+                for (int t = __ldg(a.r_rc_off + e); t < __ldg(a.r_rc_off + e + 1); ++t)
+                    w += cl[__ldg(a.rr_cell + t)] * __ldg(a.rr_a0 + t);
+                rem += w * __ldg(zc + zbase + __ldg(a.r_dof + e));
+            }
+            const double gg = acc + rem, d1 = -c0 * gg;
+            gst[u] = d1;
+            gst[a.max_gen + u] = 0.0;
+            gst[2 * a.max_gen + u] = gg;
+            B1[__ldg(a.g_slot + r)] = d1 * __ldg(a.g_rs + r);
+        }
+        __syncthreads();
+
+        // prefetch stages, overlapped with the substeps: 0 / 1: z_{n-1} of
+        // this item's columns a / b -> w = 2 z_n - z_{n-1} (TMEM); 2 / 3: z_n
+        // of the next item's columns (TMEM) and its cell coefficients
+        auto issue = [&](int stage, double (&z)[kK]) {
+            if (stage < 2) {
+                load_col(zp, g, stage, W, a.n, z);
+            } else if (has_next) {
+                const ItemGeo gn = item_geo(a, next_item, warp, lane);
+                load_col(zc, gn, stage - 2, W, a.n, z);
+                if (stage == 2 && tid < a.n_cells)
+                    cl_next = __ldg(a.cells + static_cast<std::size_t>(tid) * S + gn.s);
+            }
+        };
+        auto commit = [&](int stage, const double (&z)[kK]) {
+            if (stage < 2) {
+                double zn[kK], w[kK];
+                tm_get8(tb + kTmZn + 16 * stage, zn);
+#pragma unroll
+                for (int k = 0; k < kK; ++k) w[k] = 2.0 * zn[k] - z[k];
+                tm_put8(tb + kTmW + 16 * stage, w);
+            } else if (has_next) {
+                tm_put8(tb + kTmZn + 16 * (stage - 2), z);
+            }
+        };
+
+        // 3. substeps m = 1 .. p-1 (v_m in buffer m & 1)
+        for (int mm = 1; mm <= a.p - 1; ++mm) {
+            const double* cur = (mm & 1) ? B1 : B0;
+            double* nxt = (mm & 1) ? B0 : B1;
+            const double beta = kbeta[mm - 1], cmm = kcm[mm - 1];
+            const double onepb = 1.0 + beta;
+            double pre[kK];
+            if (mm <= 4) issue(mm - 1, pre);
+            if (partial) {
+#pragma unroll
+                for (int k = 0; k < kK; ++k) {
+                    if (!(lat & (1u << k))) va[k] = cur[sa + k];
+                    if (!(lat & (1u << (8 + k)))) vb[k] = cur[sb + k];
+                }
+            }
+            const double na_end = cur[sa + kK], nb_end = cur[sb + kK];
+            double pa_ = cur[sa - 1], pb_ = cur[sb - 1];
+#pragma unroll
+            for (int q = 0; q < kK / 2; ++q) {
+                std::uint32_t tg[8], tv[8];
+                t_ld8(tb + 16 * q, tg);
+                t_ld8(tb + 16 * q + 8, tv);
+                double nx[2][2];
+#define WMC_TILE_S_ROW(K_, R_)                                                                               \
+                {                                                                                            \
+                    double aqa, aqb;                                                                         \
+                    lattice_row<K_>(va, vb, pa_, pb_, na_end, nb_end, cur[sWa + K_], cur[sEb + K_], cc, line, \
+                                    cl, lc, s2, aqa, aqb);                                                   \
+                    nx[R_][0] = onepb * va[K_] - beta * t_dbl(tv + 2 * R_) - cmm * (t_dbl(tg + 2 * R_) + aqa); \
+                    nx[R_][1] = onepb * vb[K_] - beta * t_dbl(tv + 4 + 2 * R_) -                              \
+                                cmm * (t_dbl(tg + 4 + 2 * R_) + aqb);                                         \
+                    pa_ = va[K_];                                                                            \
+                    pb_ = vb[K_];                                                                            \
+                }
+                if (q == 0) { WMC_TILE_S_ROW(0, 0) WMC_TILE_S_ROW(1, 1) }
+                if (q == 1) { WMC_TILE_S_ROW(2, 0) WMC_TILE_S_ROW(3, 1) }
+                if (q == 2) { WMC_TILE_S_ROW(4, 0) WMC_TILE_S_ROW(5, 1) }
+                if (q == 3) { WMC_TILE_S_ROW(6, 0) WMC_TILE_S_ROW(7, 1) }
+#undef WMC_TILE_S_ROW
+                // v_{m-1} <- v_m of rows 2q, 2q+1
+                t_put(tv + 0, va[2 * q]);
+                t_put(tv + 2, va[2 * q + 1]);
+                t_put(tv + 4, vb[2 * q]);
+                t_put(tv + 6, vb[2 * q + 1]);
+                t_st8(tb + 16 * q + 8, tv);
+                va[2 * q] = nx[0][0];
+                va[2 * q + 1] = nx[1][0];
+                vb[2 * q] = nx[0][1];
+                vb[2 * q + 1] = nx[1][1];
+            }
+#pragma unroll
+            for (int k = 0; k < kK; ++k) {
+                if (lat & (1u << k)) nxt[sa + k] = va[k];
+                if (lat & (1u << (8 + k))) nxt[sb + k] = vb[k];
+            }
+            for (int u = tid; u < ng; u += kT) {
+                const int r = gb + u;
+                double acc = 0.0;
+                for (int e = __ldg(a.g_ent_off + r); e < __ldg(a.g_ent_off + r + 1); ++e)
+                    acc += wbuf[e - eb] * cur[__ldg(a.e_slot + e)];
+                const double d = gst[u], dp = gst[a.max_gen + u];
+                const double next = onepb * d - beta * dp - cmm * (gst[2 * a.max_gen + u] + acc);
+                gst[a.max_gen + u] = d;
+                gst[u] = next;
+                nxt[__ldg(a.g_slot + r)] = next * __ldg(a.g_rs + r);
+            }
+            if (mm <= 4) commit(mm - 1, pre);
+            __syncthreads();
+        }
+        for (int stage = a.p - 1; stage < 4; ++stage) {  // short step sequences (p < 5)
+            double pre[kK];
+            issue(stage, pre);
+            commit(stage, pre);
+        }
+
+        // 4. owned rows: z_{n+1} = w + 2 d_p (d = v h), check_finite
+        bool bad = false;
+        {
+            double w[kK];
+            tm_get8(tb + kTmW, w);
+#pragma unroll
+            for (int k = 0; k < kK; ++k)
+                if (g.own & (1u << k)) {
+                    const double out = w[k] + 2.0 * (va[k] * a.h);
+                    zp[zbase + g.ia * W + g.jr0 + k] = out;
+                    bad |= !(fabs(out) <= 1e100);
+                }
+            tm_get8(tb + kTmW + 16, w);
+#pragma unroll
+            for (int k = 0; k < kK; ++k)
+                if (g.own & (1u << (8 + k))) {
+                    const double out = w[k] + 2.0 * (vb[k] * a.h);
+                    zp[zbase + g.ib * W + g.jr0 + k] = out;
+                    bad |= !(fabs(out) <= 1e100);
+                }
+        }
+        for (int u = tid; u < ng; u += kT) {
+            const int r = gb + u;
+            if (!__ldg(a.g_owned + r)) continue;
+            const std::size_t idx = zbase + __ldg(a.g_dof + r);
+            const double out = 2.0 * __ldg(zc + idx) - zp[idx] + 2.0 * gst[u];
+            zp[idx] = out;
+            bad |= !(fabs(out) <= 1e100);
+        }
+        if (bad && s < a.count) atomicMin(a.fail + s, a.step);
+    }
+
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" : : "r"(tm_slot) : "memory");
+}
+
+}  // namespace
+
+int tile_smem_bytes(const TileArgs& a) {
+    return static_cast<int>(sizeof(double)) *
+           (2 * (a.box_slots + a.max_app) + a.max_ent + 3 * a.max_gen + a.n_cells + 2 * a.p + 1);
+}
+
+int launch_tile_step(const TileArgs& a, int grid, void* stream) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, tile_step_kernel);  // static shared memory (the TMEM address slot)
+    const int e = set_max_dynamic_smem(reinterpret_cast<const void*>(tile_step_kernel),
+                                       optin - static_cast<int>(fa.sharedSizeBytes));
+    if (e != 0) return e;
+    tile_step_kernel<<<grid, kT, tile_smem_bytes(a), static_cast<cudaStream_t>(stream)>>>(a);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace wmc

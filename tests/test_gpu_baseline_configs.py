@@ -98,6 +98,7 @@ def test_config3_samples_match_reference(golden, config3_mesh, case):
     lv = wavemc.Level(config3_mesh, spec)
     assert lv.info["n"] == int(hdr["n"]) and lv.info["n_r"] == int(hdr["n_r"])
     assert lv.info["n_steps"] == int(hdr["n_steps"])
+    assert lv.info["substep_path"] == 5  # the temporally blocked tiled step
     got = []
     for i in idx:  # contiguous runs
         _, q, _ = wavemc.eval_pairs(lv, None, 0, 0, i, 1)
@@ -153,3 +154,38 @@ def test_device_resident_path_reports_instability():
     d_q = torch.empty(64, dtype=torch.float64, device="cuda")
     wavemc.eval_pairs_device(ok, None, 0, 0, 0, 64, d_dq.data_ptr(), d_q.data_ptr())
     wavemc.synchronize(ok)
+
+
+def test_config3_tiled_step_matches_hbm_resident_substeps(config3_mesh, monkeypatch):
+    """The tiled step (R in spatial tiles, substeps on chip) against the
+    HBM-resident substep kernels on the config-3 mesh, a batch of 64 samples
+    at 12 global steps (every tile, both region shapes, every sample)."""
+    d = configs.config3()
+    spec = wavemc.LevelSpec(dt=d.dt, substeps=d.substeps, final_time=12 * d.dt,
+                            qoi_box=(0.4375, 0.5625, 0.4375, 0.5625), batch=64)
+    tiled = wavemc.Level(config3_mesh, spec)
+    monkeypatch.setenv("WMC_TILED", "0")
+    glob = wavemc.Level(config3_mesh, spec)
+    monkeypatch.delenv("WMC_TILED")
+    assert tiled.info["substep_path"] == 5 and glob.info["substep_path"] == 3
+    _, a, _ = wavemc.eval_pairs(tiled, None, 0, 0, 100, 64)
+    _, b, _ = wavemc.eval_pairs(glob, None, 0, 0, 100, 64)
+    assert per_sample_rel(a, b) < QOI_RTOL
+
+
+@pytest.mark.parametrize("lvl", [3, 4])
+def test_tiled_step_on_config1_levels(lvl, monkeypatch):
+    """Config-1 levels 3 (p = 4) and 4 (p = 2): the tiled step against the
+    lattice / HBM-resident paths and, for pairs, the reference goldens."""
+    d = configs.config1()[lvl]
+    monkeypatch.setenv("WMC_SUBSTEP_PATH", "tiled")
+    tiled = configs.build_level(d)
+    monkeypatch.setenv("WMC_SUBSTEP_PATH", "global")
+    monkeypatch.setenv("WMC_TILED", "0")
+    other = configs.build_level(d)
+    monkeypatch.delenv("WMC_SUBSTEP_PATH")
+    monkeypatch.delenv("WMC_TILED")
+    assert tiled.info["substep_path"] == 5 and other.info["substep_path"] == 3
+    _, a, _ = wavemc.eval_pairs(tiled, None, 0, lvl, 0, 96)
+    _, b, _ = wavemc.eval_pairs(other, None, 0, lvl, 0, 96)
+    assert per_sample_rel(a, b) < QOI_RTOL
