@@ -580,6 +580,12 @@ void build_device_level(wmc_level& L) {
                 a.c0 = t.c0;
                 a.tile_rect = up(rect);
                 a.tile_oj = up(oj);
+                {
+                    std::vector<int4> tg(plan.thr_geo.size() / 4);
+                    for (std::size_t q = 0; q < tg.size(); ++q)
+                        tg[q] = make_int4(plan.thr_geo[4 * q], plan.thr_geo[4 * q + 1], plan.thr_geo[4 * q + 2], 0);
+                    a.thr_geo = up(tg);
+                }
                 a.gen_off = up(plan.gen_off);
                 a.g_slot = up(plan.g_slot);
                 a.g_dof = up(plan.g_dof);

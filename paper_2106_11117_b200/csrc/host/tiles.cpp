@@ -134,6 +134,7 @@ std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz
 bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, int wide, int narrow, int k, TilePlan& P) {
     const int m = t.lat_m, W = m + 1, p = t.p, n_r = t.n_r, WW = W * W;
     P.tiles_shape.clear();
+    P.thr_geo.clear();
     P.i0.clear(), P.j0.clear(), P.oi0.clear(), P.oi1.clear(), P.oj0.clear(), P.oj1.clear();
     P.gen_off.assign(1, 0);
     P.g_slot.clear(), P.g_dof.clear(), P.g_owned.clear(), P.g_rs.clear();
@@ -343,6 +344,28 @@ bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, int w
                 P.reason = "tile " + std::to_string(q) + ": halo too narrow at generic row " + std::to_string(gens[u]);
                 return false;
             }
+        {
+            // thread geometry (tile_step_kernel's item view): thread = 2
+            // columns x k rows; wz / 64 warps per strip row
+            const int threads = wide / 2 * narrow / k, wpr = wz / 64;
+            for (int tid = 0; tid < threads; ++tid) {
+                const int warp = tid / 32, lane = tid % 32;
+                const int strip = warp / wpr, tc = (warp % wpr) * 32 + lane;
+                const int ia = ri0 + 2 * tc, jr0 = rj0 + strip * k;
+                unsigned lat = 0, own = 0;
+                for (int c = 0; c < 2; ++c)
+                    for (int r = 0; r < k; ++r) {
+                        const int i = ia + c, j = jr0 + r;
+                        if (!interior(i, j)) continue;
+                        lat |= 1u << (k * c + r);
+                        if (i >= d.oi0 && i < d.oi1 && j >= d.oj0 && j < d.oj1) own |= 1u << (k * c + r);
+                    }
+                P.thr_geo.push_back(ia);
+                P.thr_geo.push_back(jr0);
+                P.thr_geo.push_back(static_cast<int>(lat | (own << 16)));
+                P.thr_geo.push_back(0);
+            }
+        }
         P.tiles_shape.push_back(d.shape);
         P.i0.push_back(ri0);
         P.j0.push_back(rj0);

@@ -46,6 +46,10 @@ struct TilePlan {
     std::vector<int> i0, j0;            // region origin (box coordinates, may be < 0)
     std::vector<int> oi0, oi1, oj0, oj1;  // owned rectangle [oi0, oi1) x [oj0, oj1) (box coordinates)
     std::vector<int> gen_off;           // generic rows of tile t: [gen_off[t], gen_off[t+1])
+    // per tile and thread (threads = wide / 2 * narrow / k): the thread's
+    // first column ia, first row jr0, lattice mask | owned mask << 16 (bit
+    // r: column ia row jr0 + r, bit k + r: column ia + 1), see the kernel
+    std::vector<int> thr_geo;           // [tile][thread][4]
     // per generic row
     std::vector<int> g_slot, g_dof, g_owned, g_ent_off, g_rem_off;  // ent / rem offsets: [off[r], off[r+1])
     std::vector<double> g_rs;

@@ -416,6 +416,7 @@ struct TileArgs {
     double inv_h, h, inv_h2, c0;
     const int4* tile_rect;   // per tile: region origin i0, j0; owned columns [oi0, oi1)
     const int4* tile_oj;     // owned rows [oj0, oj1), shape (0: kTileWz x kTileHz, 1: kTileHz x kTileWz)
+    const int4* thr_geo;     // per tile and thread: first column, first row, lattice | owned << 16
     const int* gen_off;      // per tile: generic rows [gen_off[t], gen_off[t+1])
     const int* g_slot;
     const int* g_dof;

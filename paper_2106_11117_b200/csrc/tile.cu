@@ -29,6 +29,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -77,6 +78,27 @@ __device__ __forceinline__ double t_dbl(const std::uint32_t* r) {
 __device__ __forceinline__ void t_put(std::uint32_t* r, double d) {
     r[0] = static_cast<std::uint32_t>(__double2loint(d));
     r[1] = static_cast<std::uint32_t>(__double2hiint(d));
+}
+// 4 doubles <-> 8 TMEM columns, the 32-bit halves packed / unpacked inside
+// the asm so the doubles land in aligned register pairs (no moves)
+__device__ __forceinline__ void t_ld4d(std::uint32_t addr, double (&d)[4]) {
+    asm volatile(
+        "{\n.reg .b32 t<8>;\n"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {t0,t1,t2,t3,t4,t5,t6,t7}, [%4];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        "mov.b64 %0, {t0,t1};\nmov.b64 %1, {t2,t3};\nmov.b64 %2, {t4,t5};\nmov.b64 %3, {t6,t7};\n}\n"
+        : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3])
+        : "r"(addr));
+}
+__device__ __forceinline__ void t_st4d(std::uint32_t addr, double d0, double d1, double d2, double d3) {
+    asm volatile(
+        "{\n.reg .b32 t<8>;\n"
+        "mov.b64 {t0,t1}, %1;\nmov.b64 {t2,t3}, %2;\nmov.b64 {t4,t5}, %3;\nmov.b64 {t6,t7}, %4;\n"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {t0,t1,t2,t3,t4,t5,t6,t7};\n"
+        "tcgen05.wait::st.sync.aligned;\n}\n"
+        :
+        : "r"(addr), "d"(d0), "d"(d1), "d"(d2), "d"(d3)
+        : "memory");
 }
 
 // conductances (scaled by 1 / h^2) of the thread's two columns: rows 1 ..
@@ -141,13 +163,13 @@ struct ItemGeo {
 __device__ __forceinline__ ItemGeo item_geo(const TileArgs& a, int item, int warp, int lane) {
     ItemGeo g;
     g.tile = item / a.count;
-    g.s = item % a.count;
-    const int4 tr = __ldg(a.tile_rect + g.tile);
-    const int4 toj = __ldg(a.tile_oj + g.tile);
+    g.s = item - g.tile * a.count;
+    const int shape = __ldg(&a.tile_oj[g.tile].z);
+    const int4 t = __ldg(a.thr_geo + g.tile * kT + warp * 32 + lane);  // planned per (tile, thread)
     // region shape: wide (kTileWz columns, two warps per strip row) or tall
     // (kTileHz columns, one warp per strip row); the same slot count
-    g.wz = toj.z ? kTileHz : kTileWz;
-    g.hz = toj.z ? kTileWz : kTileHz;
+    g.wz = shape ? kTileHz : kTileWz;
+    g.hz = shape ? kTileWz : kTileHz;
     g.HS = g.hz + 3;
     const int wpr = g.wz / 64;
     const int strip = warp / wpr, tc = (warp % wpr) * 32 + lane;
@@ -156,24 +178,11 @@ __device__ __forceinline__ ItemGeo item_geo(const TileArgs& a, int item, int war
     g.sb = pb * g.HS + strip * kK + 1;
     g.sWa = g.sb - g.HS;  // far neighbours: W of column a, E of column b
     g.sEb = g.sa + g.HS;
-    g.ia = tr.x + 2 * tc;
-    g.ib = g.ia + 1;
-    g.jr0 = tr.y + strip * kK;
-    const int m = a.m;
-    const bool ca_in = g.ia >= 1 && g.ia <= m - 1, cb_in = g.ib >= 1 && g.ib <= m - 1;
-    const int klo = max(0, 1 - g.jr0), khi = min(kK, m - g.jr0);
-    g.lat = 0;
-    g.own = 0;
-#pragma unroll
-    for (int k = 0; k < kK; ++k) {
-        const bool row_in = k >= klo && k < khi;
-        const int j = g.jr0 + k;
-        const bool row_own = j >= toj.x && j < toj.y;
-        if (row_in && ca_in) g.lat |= 1u << k;
-        if (row_in && cb_in) g.lat |= 1u << (8 + k);
-        if (row_in && ca_in && row_own && g.ia >= tr.z && g.ia < tr.w) g.own |= 1u << k;
-        if (row_in && cb_in && row_own && g.ib >= tr.z && g.ib < tr.w) g.own |= 1u << (8 + k);
-    }
+    g.ia = t.x;
+    g.ib = t.x + 1;
+    g.jr0 = t.y;
+    g.lat = static_cast<unsigned>(t.z) & 0xffffu;
+    g.own = static_cast<unsigned>(t.z) >> 16;
     return g;
 }
 
@@ -355,7 +364,6 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
             double pa_ = B0[sa - 1], pb_ = B0[sb - 1];
 #pragma unroll
             for (int q = 0; q < kK / 2; ++q) {
-                std::uint32_t t[8], z[8];
                 double g2[2][2];
 #define WMC_TILE_G_ROW(K_, R_)                                                                              \
                 {                                                                                           \
@@ -372,14 +380,7 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
                 if (q == 2) { WMC_TILE_G_ROW(4, 0) WMC_TILE_G_ROW(5, 1) }
                 if (q == 3) { WMC_TILE_G_ROW(6, 0) WMC_TILE_G_ROW(7, 1) }
 #undef WMC_TILE_G_ROW
-                t_put(t + 0, g2[0][0]);
-                t_put(t + 2, g2[1][0]);
-                t_put(t + 4, g2[0][1]);
-                t_put(t + 6, g2[1][1]);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) z[u] = 0u;
-                t_st8(tb + 16 * q, t);
-                t_st8(tb + 16 * q + 8, z);
+                t_st4d(tb + 16 * q, g2[0][0], g2[1][0], g2[0][1], g2[1][1]);
                 va[2 * q] = -c0 * g2[0][0];
                 va[2 * q + 1] = -c0 * g2[1][0];
                 vb[2 * q] = -c0 * g2[0][1];
@@ -414,36 +415,51 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
         // prefetch stages, overlapped with the substeps: 0 / 1: z_{n-1} of
         // this item's columns a / b -> w = 2 z_n - z_{n-1} (TMEM); 2 / 3: z_n
         // of the next item's columns (TMEM) and its cell coefficients
-        auto issue = [&](int stage, double (&z)[kK]) {
-            if (stage < 2) {
-                load_col(zp, g, stage, W, a.n, z);
+        // stage q (0..7): rows 4 (q & 1) .. + 3 of column (q >> 1) & 1; q < 4:
+        // z_{n-1} of this item -> w, q >= 4: z_n of the next item
+        constexpr int kH = kK / 2;
+        auto issue = [&](int stage, double (&z)[kH]) {
+            const int col = (stage >> 1) & 1, h = stage & 1;
+            if (stage < 4) {
+                const double* zs = zp + zbase + (col ? g.ib : g.ia) * W + g.jr0 + kH * h;
+#pragma unroll
+                for (int k = 0; k < kH; ++k) z[k] = (lat >> (8 * col + kH * h + k)) & 1u ? __ldg(zs + k) : 0.0;
             } else if (has_next) {
-                const ItemGeo gn = item_geo(a, next_item, warp, lane);
-                load_col(zc, gn, stage - 2, W, a.n, z);
-                if (stage == 2 && tid < a.n_cells)
+                const ItemGeo gn = item_geo(a, next_item, warp, lane);  // a table lookup
+                const double* zs = zc + static_cast<std::size_t>(gn.s) * a.n + (col ? gn.ib : gn.ia) * W + gn.jr0 +
+                                   kH * h;
+#pragma unroll
+                for (int k = 0; k < kH; ++k) z[k] = (gn.lat >> (8 * col + kH * h + k)) & 1u ? __ldg(zs + k) : 0.0;
+                if (stage == 4 && tid < a.n_cells)
                     cl_next = __ldg(a.cells + static_cast<std::size_t>(tid) * S + gn.s);
             }
         };
-        auto commit = [&](int stage, const double (&z)[kK]) {
-            if (stage < 2) {
-                double zn[kK], w[kK];
-                tm_get8(tb + kTmZn + 16 * stage, zn);
+        auto commit = [&](int stage, const double (&z)[kH]) {
+            const int col = (stage >> 1) & 1, h = stage & 1;
+            std::uint32_t r[8];
+            if (stage < 4) {
+                t_ld8(tb + kTmZn + 16 * col + 8 * h, r);
 #pragma unroll
-                for (int k = 0; k < kK; ++k) w[k] = 2.0 * zn[k] - z[k];
-                tm_put8(tb + kTmW + 16 * stage, w);
+                for (int k = 0; k < kH; ++k) t_put(r + 2 * k, 2.0 * t_dbl(r + 2 * k) - z[k]);
+                t_st8(tb + kTmW + 16 * col + 8 * h, r);
             } else if (has_next) {
-                tm_put8(tb + kTmZn + 16 * (stage - 2), z);
+#pragma unroll
+                for (int k = 0; k < kH; ++k) t_put(r + 2 * k, z[k]);
+                t_st8(tb + kTmZn + 16 * col + 8 * h, r);
             }
         };
 
-        // 3. substeps m = 1 .. p-1 (v_m in buffer m & 1)
-        for (int mm = 1; mm <= a.p - 1; ++mm) {
-            const double* cur = (mm & 1) ? B1 : B0;
-            double* nxt = (mm & 1) ? B0 : B1;
+        // 3. substeps m = 1 .. p-1 (v_m in buffer m & 1; the parity is a
+        // template argument so the buffer addresses are fixed per body)
+        auto substep = [&](auto odd, auto first, int mm) {
+            constexpr bool kOdd = decltype(odd)::value;
+            constexpr bool kFirst = decltype(first)::value;  // m = 1: v_0 = 0
+            const double* cur = kOdd ? B1 : B0;
+            double* nxt = kOdd ? B0 : B1;
             const double beta = kbeta[mm - 1], cmm = kcm[mm - 1];
             const double onepb = 1.0 + beta;
-            double pre[kK];
-            if (mm <= 4) issue(mm - 1, pre);
+            double pre[kH];
+            if (mm <= 8) issue(mm - 1, pre);
             if (partial) {
 #pragma unroll
                 for (int k = 0; k < kK; ++k) {
@@ -455,18 +471,21 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
             double pa_ = cur[sa - 1], pb_ = cur[sb - 1];
 #pragma unroll
             for (int q = 0; q < kK / 2; ++q) {
-                std::uint32_t tg[8], tv[8];
-                t_ld8(tb + 16 * q, tg);
-                t_ld8(tb + 16 * q + 8, tv);
+                double tg[4], tv[4];
+                t_ld4d(tb + 16 * q, tg);
+                // v_{m-1}: still in the buffer this substep overwrites (own slots)
+                tv[0] = kFirst ? 0.0 : nxt[sa + 2 * q];
+                tv[1] = kFirst ? 0.0 : nxt[sa + 2 * q + 1];
+                tv[2] = kFirst ? 0.0 : nxt[sb + 2 * q];
+                tv[3] = kFirst ? 0.0 : nxt[sb + 2 * q + 1];
                 double nx[2][2];
 #define WMC_TILE_S_ROW(K_, R_)                                                                               \
                 {                                                                                            \
                     double aqa, aqb;                                                                         \
                     lattice_row<K_>(va, vb, pa_, pb_, na_end, nb_end, cur[sWa + K_], cur[sEb + K_], cc, line, \
                                     cl, lc, s2, aqa, aqb);                                                   \
-                    nx[R_][0] = onepb * va[K_] - beta * t_dbl(tv + 2 * R_) - cmm * (t_dbl(tg + 2 * R_) + aqa); \
-                    nx[R_][1] = onepb * vb[K_] - beta * t_dbl(tv + 4 + 2 * R_) -                              \
-                                cmm * (t_dbl(tg + 4 + 2 * R_) + aqb);                                         \
+                    nx[R_][0] = onepb * va[K_] - beta * tv[R_] - cmm * (tg[R_] + aqa);                       \
+                    nx[R_][1] = onepb * vb[K_] - beta * tv[2 + R_] - cmm * (tg[2 + R_] + aqb);               \
                     pa_ = va[K_];                                                                            \
                     pb_ = vb[K_];                                                                            \
                 }
@@ -475,21 +494,23 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
                 if (q == 2) { WMC_TILE_S_ROW(4, 0) WMC_TILE_S_ROW(5, 1) }
                 if (q == 3) { WMC_TILE_S_ROW(6, 0) WMC_TILE_S_ROW(7, 1) }
 #undef WMC_TILE_S_ROW
-                // v_{m-1} <- v_m of rows 2q, 2q+1
-                t_put(tv + 0, va[2 * q]);
-                t_put(tv + 2, va[2 * q + 1]);
-                t_put(tv + 4, vb[2 * q]);
-                t_put(tv + 6, vb[2 * q + 1]);
-                t_st8(tb + 16 * q + 8, tv);
                 va[2 * q] = nx[0][0];
                 va[2 * q + 1] = nx[1][0];
                 vb[2 * q] = nx[0][1];
                 vb[2 * q + 1] = nx[1][1];
             }
+            if (!partial) {  // warp-uniform: every position of the warp is a lattice node
 #pragma unroll
-            for (int k = 0; k < kK; ++k) {
-                if (lat & (1u << k)) nxt[sa + k] = va[k];
-                if (lat & (1u << (8 + k))) nxt[sb + k] = vb[k];
+                for (int k = 0; k < kK; ++k) {
+                    nxt[sa + k] = va[k];
+                    nxt[sb + k] = vb[k];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < kK; ++k) {
+                    if (lat & (1u << k)) nxt[sa + k] = va[k];
+                    if (lat & (1u << (8 + k))) nxt[sb + k] = vb[k];
+                }
             }
             for (int u = tid; u < ng; u += kT) {
                 const int r = gb + u;
@@ -502,11 +523,16 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
                 gst[u] = next;
                 nxt[__ldg(a.g_slot + r)] = next * __ldg(a.g_rs + r);
             }
-            if (mm <= 4) commit(mm - 1, pre);
+            if (mm <= 8) commit(mm - 1, pre);
             __syncthreads();
+        };
+        if (a.p > 1) substep(std::true_type{}, std::true_type{}, 1);
+        for (int mm = 2; mm <= a.p - 1; mm += 2) {
+            substep(std::false_type{}, std::false_type{}, mm);
+            if (mm + 1 <= a.p - 1) substep(std::true_type{}, std::false_type{}, mm + 1);
         }
-        for (int stage = a.p - 1; stage < 4; ++stage) {  // short step sequences (p < 5)
-            double pre[kK];
+        for (int stage = a.p - 1; stage < 8; ++stage) {  // short step sequences (p < 9)
+            double pre[kH];
             issue(stage, pre);
             commit(stage, pre);
         }
