@@ -143,15 +143,26 @@ typedef struct {
 } wmc_level_info;
 
 int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level** out);
+/* A 1D mesh of the reference's sampling experiments: the reference's
+ * Mesh1D (include/wavemc/mesh.hpp:21-33) passed through as arrays -- sorted
+ * vertices (n_vertices), fine flags per element (n_vertices - 1), coarse and
+ * fine sizes.  The adapter feeds it level by level from the reference's own
+ * build_hierarchy (src/mesh1d.cpp:76-125), as build_state_1d does
+ * (src/experiments.cpp:62-85). */
+typedef struct wmc_mesh1d wmc_mesh1d;
+int wmc_mesh1d_create(int n_vertices, const double* vertices, const unsigned char* fine_flags, double coarse_h,
+                      double fine_h, wmc_mesh1d** out);
+void wmc_mesh1d_destroy(wmc_mesh1d* mesh);
+
 /* The reference's own 1D sampling experiments (
  * reference make_problem, src/experiments.cpp:56-106, 194-237): level `level`
- * of the hierarchy build_hierarchy([0,6], h0, fine region, fine_h, max_level)
- * (src/mesh1d.cpp:79-125), fine region [5 - h0, 5] (smooth) or [4 - h0, 4]
- * (jump), Neumann, u0 = exp(-(x-3)^2/0.09), per-sample CFL step (stable_dt
- * with the given safety), p = the level's ratio (LTS) or 1 (LF); field
- * sample_kl (smooth: c^2 = 1 + KL, 100 cos + 100 sin terms) or sample_jump
- * (c^2 = 1 left of J ~ U[4 - h0, 4), 4 right of it); QoI = u(T) on grid_n
- * points of [0, 6] (restrict_to_grid), norm with trapezoid weights. */
+ * on `mesh`, the level's mesh of the reference hierarchy, with `substeps` its
+ * ratio p_l (MeshHierarchy::ratios; LTS) -- LF uses 1; fine region [5 - h0, 5]
+ * (smooth) or [4 - h0, 4] (jump), Neumann, u0 = exp(-(x-3)^2/0.09),
+ * per-sample CFL step (stable_dt with the given safety); field sample_kl
+ * (smooth: c^2 = 1 + KL, 100 cos + 100 sin terms) or sample_jump (c^2 = 1
+ * left of J ~ U[4 - h0, 4), 4 right of it); QoI = u(T) on grid_n points of
+ * [0, 6] (restrict_to_grid), norm with trapezoid weights. */
 #define WMC_EXP_SMOOTH1D 1
 #define WMC_EXP_JUMP1D 2
 #define WMC_EXP_CHANNEL2D 3
@@ -165,7 +176,8 @@ typedef struct {
 
 /* the reference's default_config (src/config_io.cpp:49-73) for the experiment */
 void wmc_experiment_desc_default(wmc_experiment_desc* desc, int experiment);
-int wmc_level_create_experiment(const wmc_experiment_desc* desc, int level, wmc_level** out);
+int wmc_level_create_experiment(const wmc_mesh1d* mesh, int substeps, const wmc_experiment_desc* desc, int level,
+                                wmc_level** out);
 /* The reference's narrow-channel experiment (make_problem Channel2d,
  * src/experiments.cpp:108-172): level `level` on `mesh`, the reference's
  * build_channel_mesh(max(h0 / 2^level, fine_h), fine_h) (src/mesh2d.cpp:
@@ -181,7 +193,8 @@ int wmc_level_create_channel(const wmc_mesh* mesh, const wmc_experiment_desc* de
 /* Host-only plan of a channel level (sizes, no device work). */
 int wmc_channel_plan(const wmc_mesh* mesh, const wmc_experiment_desc* desc, int level, wmc_level_info* info);
 /* Host-only plan of an experiment level (sizes, no device work). */
-int wmc_experiment_plan(const wmc_experiment_desc* desc, int level, wmc_level_info* info);
+int wmc_experiment_plan(const wmc_mesh1d* mesh, int substeps, const wmc_experiment_desc* desc, int level,
+                        wmc_level_info* info);
 /* The experiment's model cost per level, the reference's closed-form cost
  * model (model_params, src/experiments.cpp:177-192; cost_lts_level /
  * cost_lf_level, src/cost_model.cpp:40-58): the run_mlmc weights. */

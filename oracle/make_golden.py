@@ -1,6 +1,6 @@
 """Generate tests/golden/*.json from the UNMODIFIED reference library
 (oracle/_ref/wavemc_ref_driver) -- run in the build container, where
-/root/reference exists:  python oracle/make_golden.py [--only-round2 | --only-config1-full | --only-config2 | --only-cfl | --only-experiments | --only-artifacts | --only-channel]
+/root/reference exists:  python oracle/make_golden.py [--only-round2 | --only-config1-full | --only-mesh1d | --only-config2 | --only-cfl | --only-experiments | --only-artifacts | --only-channel]
 
 The meshes come from the shared problem definition (the product's host mesh
 builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
@@ -187,6 +187,20 @@ def channel(ref, tmp):
     dump(os.path.join("channel", "channel.json"), out)
 
 
+def hierarchies_1d(ref):
+    """The reference's 1D mesh hierarchies of its smooth1d / jump1d
+    experiments (build_state_1d -> build_hierarchy, src/experiments.cpp:62-85):
+    the inputs the product takes through wmc_mesh1d_create, for the default
+    configs (max_level 4; the artifact configs' max_level 3 is its prefix)."""
+    dst = os.path.join(GOLDEN, "mesh1d")
+    os.makedirs(dst, exist_ok=True)
+    for name in ("smooth1d", "jump1d"):  # max_level 4; lower max_level: a prefix (nested bisection)
+        h = json.loads(ref.run("hierarchy1d", "--name", name, "--max-level", 4))
+        with open(os.path.join(dst, f"{name}_L4.json"), "w") as f:
+            json.dump(h, f)
+            f.write("\n")
+
+
 def config1_full(ref, tmp):
     """Config-1 per-level sums, means and variances at the BASELINE N_l
     (65536 / 16384 / 4096 / 1024 / 256 coupled pairs) from the unmodified
@@ -265,6 +279,9 @@ def main():
         return
     if "--only-config1-full" in sys.argv:
         config1_full(ref, tmp)
+        return
+    if "--only-mesh1d" in sys.argv:
+        hierarchies_1d(ref)
         return
     if "--only-round2" in sys.argv:
         round2(ref, tmp)

@@ -558,6 +558,38 @@ int cmd_channel_mesh(const Args& a) {
     return 0;
 }
 
+// The reference's 1D mesh hierarchy of a sampling experiment, exactly as
+// build_state_1d builds it (src/experiments.cpp:62-85: domain [0, 6], fine
+// window [anchor - h0, anchor], build_hierarchy src/mesh1d.cpp:76-125): per
+// level the vertices, fine flags, coarse / fine sizes and the ratio p_l.
+//   hierarchy1d --name smooth1d|jump1d [--h0 H --fine-h F --max-level L]
+int cmd_hierarchy1d(const Args& a) {
+    const std::string name = a.get("name", "smooth1d");
+    const auto kind = experiment_from_string(name);
+    if (!kind || (*kind != ExperimentKind::Smooth1d && *kind != ExperimentKind::Jump1d))
+        throw ConfigError("hierarchy1d: --name smooth1d|jump1d");
+    ExperimentConfig cfg = default_config(*kind);
+    cfg.max_level = static_cast<int>(a.integer("max-level", cfg.max_level));
+    if (!a.get("h0").empty()) cfg.h0 = a.num("h0", cfg.h0);
+    if (!a.get("fine-h").empty()) cfg.fine_h = a.num("fine-h", cfg.fine_h);
+    const double anchor = *kind == ExperimentKind::Jump1d ? 4.0 : 5.0;
+    const MeshHierarchy h = build_hierarchy({0.0, 6.0}, cfg.h0, Interval{anchor - cfg.h0, anchor}, cfg.fine_h,
+                                            cfg.max_level);
+    std::printf("{\"experiment\": \"%s\", \"h0\": %.17g, \"fine_h\": %.17g, \"max_level\": %d, \"levels\": [",
+                name.c_str(), cfg.h0, cfg.fine_h, cfg.max_level);
+    for (int l = 0; l < h.n_levels(); ++l) {
+        const Mesh1D& m = h.levels[l];
+        std::printf("%s{\"ratio\": %d, \"coarse_h\": %.17g, \"fine_h\": %.17g, \"vertices\": [", l ? ", " : "",
+                    h.ratios[l], m.coarse_h, m.fine_h);
+        for (std::size_t i = 0; i < m.vertices.size(); ++i) std::printf("%s%.17g", i ? ", " : "", m.vertices[i]);
+        std::printf("], \"fine_flags\": [");
+        for (std::size_t i = 0; i < m.fine_flags.size(); ++i) std::printf("%s%d", i ? ", " : "", m.fine_flags[i]);
+        std::printf("]}");
+    }
+    std::printf("]}\n");
+    return 0;
+}
+
 // The reference's own sampling experiments through its public make_problem
 // (src/experiments.cpp:194-237): per-sample QoI vectors of coupled pairs
 // (sample_delta_q) and, with --eps, run_mlmc at the reference's config.
@@ -696,6 +728,7 @@ int main(int argc, char** argv) {
         if (cmd == "meshcheck") return cmd_meshcheck(a);
         if (cmd == "level") return cmd_level(a);
         if (cmd == "experiment") return cmd_experiment(a);
+        if (cmd == "hierarchy1d") return cmd_hierarchy1d(a);
         if (cmd == "artifacts") return cmd_artifacts(a);
         if (cmd == "channel-mesh") return cmd_channel_mesh(a);
         throw ConfigError("unknown command " + cmd);

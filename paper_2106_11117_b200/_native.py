@@ -104,8 +104,10 @@ SIGNATURES = [
     ("wmc_level_desc_default", None, [P(LevelDesc)]),
     ("wmc_level_create", C.c_int, [_VP, P(LevelDesc), P(_VP)]),
     ("wmc_experiment_desc_default", None, [P(ExperimentDesc), C.c_int]),
-    ("wmc_level_create_experiment", C.c_int, [P(ExperimentDesc), C.c_int, P(_VP)]),
-    ("wmc_experiment_plan", C.c_int, [P(ExperimentDesc), C.c_int, P(LevelInfo)]),
+    ("wmc_mesh1d_create", C.c_int, [C.c_int, _DP, P(C.c_ubyte), C.c_double, C.c_double, P(_VP)]),
+    ("wmc_mesh1d_destroy", None, [_VP]),
+    ("wmc_level_create_experiment", C.c_int, [_VP, C.c_int, P(ExperimentDesc), C.c_int, P(_VP)]),
+    ("wmc_experiment_plan", C.c_int, [_VP, C.c_int, P(ExperimentDesc), C.c_int, P(LevelInfo)]),
     ("wmc_level_create_channel", C.c_int, [_VP, P(ExperimentDesc), C.c_int, P(_VP)]),
     ("wmc_channel_plan", C.c_int, [_VP, P(ExperimentDesc), C.c_int, P(LevelInfo)]),
     ("wmc_experiment_model_cost", C.c_double, [P(ExperimentDesc), C.c_int]),

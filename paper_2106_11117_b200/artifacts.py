@@ -234,15 +234,17 @@ def run_sampling_experiment(c: ExperimentConfig, log=sys.stderr, device: int = 0
     """Reference run_sampling_experiment (src/experiments.cpp:365-409) on the
     device: for each integrator (LF first, then LF-LTS) and each eps, the
     adaptive MLMC driver over the experiment's level hierarchy, then the
-    levels / estimate CSVs and one row of <exp>_work.csv.  channel2d takes
-    the reference meshes of levels 0..max_level (`meshes`, wavemc.Mesh; the
-    reference's build_channel_mesh output).  Returns the reference's exit
-    status (0 ok, 2 config error, 3 numerical failure)."""
+    levels / estimate CSVs and one row of <exp>_work.csv.  `meshes` holds the
+    reference meshes of levels 0..max_level: wavemc.Mesh (channel2d, the
+    reference's build_channel_mesh output) or wavemc.Mesh1D (smooth1d /
+    jump1d, the reference's build_hierarchy levels with their ratios).
+    Returns the reference's exit status (0 ok, 2 config error, 3 numerical
+    failure)."""
     if c.experiment not in SAMPLING:
         log.write(f"config error: {c.experiment} is not a device sampling experiment here\n")
         return 2
-    if c.experiment == "channel2d" and (meshes is None or len(meshes) < c.max_level + 1):
-        log.write("config error: channel2d needs the reference mesh of every level\n")
+    if meshes is None or len(meshes) < c.max_level + 1:
+        log.write(f"config error: {c.experiment} needs the reference mesh of every level\n")
         return 2
     kinds = [k for k in ("lf", "lts") if c.integrator in (k, "both")]
     try:
@@ -255,7 +257,7 @@ def run_sampling_experiment(c: ExperimentConfig, log=sys.stderr, device: int = 0
                 if c.experiment == "channel2d":
                     levels = [wavemc.Level.channel(meshes[l], l, integ, **ov) for l in range(c.max_level + 1)]
                 else:
-                    levels = [wavemc.Level.experiment(c.experiment, l, integ, **ov)
+                    levels = [wavemc.Level.experiment(c.experiment, l, meshes[l], integ, **ov)
                               for l in range(c.max_level + 1)]
                 costs = wavemc.experiment_model_cost(c.experiment, integ, **{k: v for k, v in ov.items()
                                                                                 if k != "device"})

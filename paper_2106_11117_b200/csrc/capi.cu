@@ -26,6 +26,10 @@
 #include "host/mesh.hpp"
 #include "kernels.cuh"
 
+struct wmc_mesh1d {
+    wmc::Mesh1D mesh;
+};
+
 struct wmc_mesh {
     wmc::TriMesh mesh;
 };
@@ -2037,21 +2041,19 @@ void set_batch(wmc_level& L, int requested) {
 
 // one level of the reference's 1D experiments: hierarchy, spec and tables
 // (make_problem / build_state_1d, src/experiments.cpp:56-106)
-void experiment_tables(const wmc_experiment_desc* desc, int level, wmc::LevelSpec& s, wmc::LevelTables& t) {
+void experiment_tables(const wmc::Mesh1D& mesh, int substeps, const wmc_experiment_desc* desc, wmc::LevelSpec& s,
+                       wmc::LevelTables& t) {
     if (desc->experiment != WMC_EXP_SMOOTH1D && desc->experiment != WMC_EXP_JUMP1D)
         throw ConfigError("experiment: unknown experiment");
+    if (substeps < 1) throw ConfigError("experiment: substeps >= 1");
     if (desc->integrator != WMC_LEAPFROG && desc->integrator != WMC_LOCAL_TIME_STEPPING)
         throw ConfigError("experiment: unknown integrator");
     if (!(desc->safety > 0.0 && desc->safety <= 1.0)) throw ConfigError("experiment: safety in (0, 1]");
     if (desc->nu < 0.0 || desc->nu > 1.0) throw ConfigError("experiment: nu in [0, 1]");
     const bool jump = desc->experiment == WMC_EXP_JUMP1D;
-    const double anchor = jump ? 4.0 : 5.0;  // experiments.cpp:68-70
-    const wmc::Hierarchy1D H =
-        wmc::build_hierarchy_1d(0.0, 6.0, desc->h0, anchor - desc->h0, anchor, desc->fine_h, desc->max_level);
-    const wmc::Mesh1D& mesh = H.levels[level];
     s = wmc::LevelSpec{};
     s.kind = desc->integrator == WMC_LEAPFROG ? wmc::Integrator::Leapfrog : wmc::Integrator::LocalTimeStepping;
-    s.substeps = s.kind == wmc::Integrator::Leapfrog ? 1 : H.ratios[level];
+    s.substeps = s.kind == wmc::Integrator::Leapfrog ? 1 : substeps;
     s.nu = desc->nu;
     s.final_time = desc->final_time;
     s.dt = mesh.coarse_h;  // nominal: every sample takes its own CFL step
@@ -2324,13 +2326,32 @@ int wmc_level_create(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level
     });
 }
 
-int wmc_level_create_experiment(const wmc_experiment_desc* desc, int level, wmc_level** out) {
+int wmc_mesh1d_create(int n_vertices, const double* vertices, const unsigned char* fine_flags, double coarse_h,
+                      double fine_h, wmc_mesh1d** out) {
     return guarded([&] {
-        if (!desc || !out) throw ConfigError("wmc_level_create_experiment: NULL argument");
+        if (!vertices || !fine_flags || !out) throw ConfigError("wmc_mesh1d_create: NULL argument");
+        if (n_vertices < 2) throw ConfigError("wmc_mesh1d_create: at least one element");
+        auto m = std::make_unique<wmc_mesh1d>();
+        m->mesh.vertices.assign(vertices, vertices + n_vertices);
+        m->mesh.fine_flags.assign(fine_flags, fine_flags + n_vertices - 1);
+        for (int i = 0; i + 1 < n_vertices; ++i)
+            if (!(vertices[i + 1] > vertices[i])) throw ConfigError("wmc_mesh1d_create: vertices not increasing");
+        m->mesh.coarse_h = coarse_h;
+        m->mesh.fine_h = fine_h;
+        *out = m.release();
+    });
+}
+
+void wmc_mesh1d_destroy(wmc_mesh1d* mesh) { delete mesh; }
+
+int wmc_level_create_experiment(const wmc_mesh1d* mesh, int substeps, const wmc_experiment_desc* desc, int level,
+                                wmc_level** out) {
+    return guarded([&] {
+        if (!mesh || !desc || !out) throw ConfigError("wmc_level_create_experiment: NULL argument");
         if (level < 0 || level > desc->max_level) throw ConfigError("wmc_level_create_experiment: level out of range");
         auto L = std::make_unique<wmc_level>();
         L->device = desc->device;
-        experiment_tables(desc, level, L->spec, L->tab);
+        experiment_tables(mesh->mesh, substeps, desc, L->spec, L->tab);
         int ndev = 0;
         check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
         if (L->device < 0 || L->device >= ndev) throw ConfigError("wmc_level_create_experiment: no such device");
@@ -2366,13 +2387,14 @@ int wmc_channel_plan(const wmc_mesh* mesh, const wmc_experiment_desc* desc, int 
     });
 }
 
-int wmc_experiment_plan(const wmc_experiment_desc* desc, int level, wmc_level_info* info) {
+int wmc_experiment_plan(const wmc_mesh1d* mesh, int substeps, const wmc_experiment_desc* desc, int level,
+                        wmc_level_info* info) {
     return guarded([&] {
-        if (!desc || !info) throw ConfigError("wmc_experiment_plan: NULL argument");
+        if (!mesh || !desc || !info) throw ConfigError("wmc_experiment_plan: NULL argument");
         if (level < 0 || level > desc->max_level) throw ConfigError("wmc_experiment_plan: level out of range");
         wmc::LevelSpec s;
         wmc::LevelTables t;
-        experiment_tables(desc, level, s, t);
+        experiment_tables(mesh->mesh, substeps, desc, s, t);
         fill_info(t, 0, false, info);
     });
 }

@@ -1,7 +1,7 @@
-// 1D meshes of the reference's own sampling experiments (smooth1d / jump1d):
-// restated from reference proj/src/mesh1d.cpp (build_refined_interval,
-// build_hierarchy) with the same arithmetic, so vertex coordinates agree
-// bit for bit.
+// 1D meshes of the reference's own sampling experiments (smooth1d / jump1d).
+// The product takes them from the caller (wmc_mesh1d_create): the adapter
+// passes the reference's Mesh1D of each level of its build_hierarchy
+// (reference proj/include/wavemc/mesh.hpp:21-33, src/mesh1d.cpp:76-125).
 #pragma once
 
 #include <cstdint>
@@ -19,18 +19,5 @@ struct Mesh1D {
     double element_size(int e) const { return vertices[e + 1] - vertices[e]; }
     double midpoint(int e) const { return 0.5 * (vertices[e] + vertices[e + 1]); }
 };
-
-struct Hierarchy1D {
-    std::vector<Mesh1D> levels;
-    std::vector<int> ratios;  // substeps p_l
-};
-
-/// reference build_refined_interval (mesh1d.cpp:46-77); fine region [fine_lo, fine_hi]
-/// (fine_hi <= fine_lo: uniform mesh)
-Mesh1D build_refined_interval(double lo, double hi, double coarse_h, double fine_lo, double fine_hi, double fine_h);
-
-/// reference build_hierarchy (mesh1d.cpp:79-125)
-Hierarchy1D build_hierarchy_1d(double lo, double hi, double h0, double fine_lo, double fine_hi, double fine_h,
-                               int num_levels);
 
 }  // namespace wmc

@@ -177,11 +177,43 @@ def experiment_desc(experiment: str, integrator: int = N.WMC_LOCAL_TIME_STEPPING
     return d
 
 
-def experiment_plan(experiment: str, level: int, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides) -> dict:
-    """Host-only sizes of one experiment level."""
+class Mesh1D:
+    """A 1D mesh of the reference's sampling experiments (wmc_mesh1d): the
+    reference's Mesh1D (include/wavemc/mesh.hpp:21-33) as arrays, one level of
+    its build_hierarchy (src/mesh1d.cpp:76-125) with that level's ratio p_l."""
+
+    def __init__(self, vertices, fine_flags, coarse_h: float, fine_h: float, ratio: int = 1):
+        v = np.ascontiguousarray(vertices, np.float64)
+        f = np.ascontiguousarray(fine_flags, np.uint8)
+        if f.shape != (len(v) - 1,):
+            raise ValueError("Mesh1D: one fine flag per element")
+        h = C.c_void_p()
+        N.check(N.lib().wmc_mesh1d_create(len(v), _dptr(v), f.ctypes.data_as(C.POINTER(C.c_ubyte)), coarse_h, fine_h,
+                                          C.byref(h)))
+        self._h = h
+        self.ratio = int(ratio)
+        self.n_vertices = len(v)
+
+    @classmethod
+    def hierarchy(cls, levels: list[dict]) -> list["Mesh1D"]:
+        """Meshes from the reference hierarchy's levels, each a dict with
+        vertices, fine_flags, coarse_h, fine_h and ratio (the reference's
+        MeshHierarchy: levels[l] and ratios[l])."""
+        return [cls(lv["vertices"], lv["fine_flags"], lv["coarse_h"], lv["fine_h"], lv["ratio"]) for lv in levels]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib().wmc_mesh1d_destroy(h)
+            self._h = None
+
+
+def experiment_plan(experiment: str, level: int, mesh: Mesh1D, integrator: int = N.WMC_LOCAL_TIME_STEPPING,
+                    **overrides) -> dict:
+    """Host-only sizes of one experiment level on `mesh` (that level's mesh)."""
     info = N.LevelInfo()
-    N.check(N.lib().wmc_experiment_plan(C.byref(experiment_desc(experiment, integrator, **overrides)), level,
-                                        C.byref(info)))
+    N.check(N.lib().wmc_experiment_plan(mesh._h, mesh.ratio, C.byref(experiment_desc(experiment, integrator, **overrides)),
+                                        level, C.byref(info)))
     return _info_dict(info)
 
 
@@ -222,18 +254,20 @@ class Level:
         self.info = _info_dict(info)
 
     @classmethod
-    def experiment(cls, experiment: str, level: int, integrator: int = N.WMC_LOCAL_TIME_STEPPING, **overrides):
+    def experiment(cls, experiment: str, level: int, mesh: Mesh1D, integrator: int = N.WMC_LOCAL_TIME_STEPPING,
+                   **overrides):
         """Level `level` of the reference's own 1D sampling experiment
-        ("smooth1d" or "jump1d"; reference make_problem, src/experiments.cpp:56-106),
+        ("smooth1d" or "jump1d"; reference make_problem, src/experiments.cpp:56-106)
+        on `mesh`, the reference hierarchy's mesh of that level (with its ratio),
         reference default_config unless overridden (h0, fine_h, final_time, nu,
         safety, grid_n, max_level, device, batch)."""
         d = experiment_desc(experiment, integrator, **overrides)
         self = cls.__new__(cls)
-        self.mesh = None
+        self.mesh = mesh
         self.spec = None
         self.experiment_desc = d
         h = C.c_void_p()
-        N.check(N.lib().wmc_level_create_experiment(C.byref(d), level, C.byref(h)))
+        N.check(N.lib().wmc_level_create_experiment(mesh._h, mesh.ratio, C.byref(d), level, C.byref(h)))
         self._h = h
         info = N.LevelInfo()
         N.check(N.lib().wmc_level_get_info(self._h, C.byref(info)))

@@ -45,3 +45,18 @@ def coracle():
     import oracle_py
     oracle_py.build()
     return oracle_py.COracle()
+
+
+@pytest.fixture(scope="session")
+def mesh1d():
+    """The reference's 1D mesh hierarchies (tests/golden/mesh1d, written by
+    oracle/make_golden.py --only-mesh1d from its build_hierarchy) as
+    wavemc.Mesh1D lists: mesh1d(name, max_level=4)."""
+    import json
+
+    def load(name, max_level=4):
+        from paper_2106_11117_b200 import wavemc
+        with open(os.path.join(ROOT, "tests", "golden", "mesh1d", f"{name}_L4.json")) as f:
+            h = json.load(f)
+        return wavemc.Mesh1D.hierarchy(h["levels"][: max_level + 1])
+    return load

@@ -15,18 +15,24 @@ def test_model_cost_matches_reference(golden, case):
     assert wavemc.experiment_model_cost(name, integ) == golden("experiments.json")[case]["model_cost"]
 
 
-def test_experiment_levels_plan():
+def test_experiment_levels_plan(mesh1d):
+    """Levels on the reference's own hierarchy meshes (wmc_mesh1d_create)."""
     prev = 0
+    jm = mesh1d("jump1d")
     for level in range(5):
-        info = wavemc.experiment_plan("jump1d", level)
+        info = wavemc.experiment_plan("jump1d", level, jm[level])
         assert info["nq"] == 512 and info["n"] > prev
+        assert info["n"] == jm[level].n_vertices  # Neumann: every vertex a DOF
         prev = info["n"]
     # jump1d keeps a refined window to the last level (fine h = 1/512 < h0 / 16)
     assert info["p"] == 2 and info["n_r"] > 0
     # smooth1d is uniform on its last level (h0 / 16 = fine h)
-    assert wavemc.experiment_plan("smooth1d", 4)["p"] == 1
+    sm = mesh1d("smooth1d")
+    assert wavemc.experiment_plan("smooth1d", 4, sm[4])["p"] == 1
     with pytest.raises(wavemc.ConfigError):
-        wavemc.experiment_plan("smooth1d", 9)
+        wavemc.experiment_plan("smooth1d", 9, sm[4])
+    with pytest.raises(wavemc.ConfigError):
+        wavemc.Mesh1D([0.0, 1.0, 0.5], [0, 0], 0.5, 0.0)  # vertices not increasing
 
 
 def test_channel_level_tables_from_reference_meshes():

@@ -33,16 +33,17 @@ def _close(a, b, scale=None):
 
 
 @pytest.mark.parametrize("name", sorted(os.listdir(GOLDEN)))
-def test_artifacts_match_reference(name, tmp_path):
+def test_artifacts_match_reference(name, tmp_path, mesh1d):
     with open(os.path.join(GOLDEN, name, "experiment.cfg")) as f:
         c = artifacts.parse_config_text(f.read())
     c.out_dir = str(tmp_path)
     log = io.StringIO()
-    meshes = None
+    from paper_2106_11117_b200 import wavemc
     if c.experiment == "channel2d":  # the reference meshes of the small channel hierarchy
-        from paper_2106_11117_b200 import wavemc
         meshes = [wavemc.Mesh.load(os.path.join(GOLDEN, "..", "channel", f"mesh_l{l}.txt.gz"))
                   for l in range(c.max_level + 1)]
+    else:  # the reference's 1D hierarchy
+        meshes = mesh1d(c.experiment, c.max_level)
     assert artifacts.run_sampling_experiment(c, log, meshes=meshes) == 0, log.getvalue()
     want_files = sorted(fn for fn in os.listdir(os.path.join(GOLDEN, name)) if fn.endswith(".csv"))
     assert sorted(os.listdir(tmp_path)) == want_files

@@ -124,9 +124,9 @@ def test_moments_device_matches_host_fold():
             assert got[k] == pytest.approx(host[key], rel=1e-12, abs=1e-300), (l, key)
 
 
-def test_moments_device_refuses_qoi_vectors():
+def test_moments_device_refuses_qoi_vectors(mesh1d):
     import torch
-    lv = wavemc.Level.experiment("smooth1d", 0)
+    lv = wavemc.Level.experiment("smooth1d", 0, mesh1d("smooth1d")[0])
     assert lv.info["nq"] > 1
     buf = torch.zeros(8, dtype=torch.float64, device="cuda")
     with pytest.raises(wavemc.ConfigError):

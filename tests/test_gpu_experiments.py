@@ -15,10 +15,11 @@ pytestmark = pytest.mark.gpu
 CASES = ["smooth1d_lts", "smooth1d_lf", "jump1d_lts", "jump1d_lf"]
 
 
-def _levels(case, n=5):
+def _levels(case, mesh1d, n=5):
     name, kind = case.split("_")
     integ = WMC_LOCAL_TIME_STEPPING if kind == "lts" else WMC_LEAPFROG
-    return [wavemc.Level.experiment(name, l, integ) for l in range(n)], integ
+    meshes = mesh1d(name)
+    return [wavemc.Level.experiment(name, l, meshes[l], integ) for l in range(n)], integ
 
 
 def _weights(nq):
@@ -28,9 +29,9 @@ def _weights(nq):
 
 
 @pytest.mark.parametrize("case", CASES)
-def test_experiment_pairs_match_reference(golden, case):
+def test_experiment_pairs_match_reference(golden, case, mesh1d):
     g = golden("experiments.json")[case]
-    levels, _ = _levels(case, 3)
+    levels, _ = _levels(case, mesh1d, 3)
     w = _weights(512)
     for lv in g["levels"]:
         l, first, ref = lv["level"], lv["first"], lv["samples"]
@@ -45,9 +46,9 @@ def test_experiment_pairs_match_reference(golden, case):
 
 
 @pytest.mark.parametrize("case", CASES)
-def test_experiment_adaptive_mlmc_matches_reference(golden, case):
+def test_experiment_adaptive_mlmc_matches_reference(golden, case, mesh1d):
     g = golden("experiments.json")[case]
-    levels, integ = _levels(case)
+    levels, integ = _levels(case, mesh1d)
     name = case.split("_")[0]
     cost = wavemc.experiment_model_cost(name, integ)
     a = g["adaptive"]
@@ -62,10 +63,10 @@ def test_experiment_adaptive_mlmc_matches_reference(golden, case):
 
 
 @pytest.mark.parametrize("case", ["smooth1d_lts", "jump1d_lf"])
-def test_fused_small_solve_is_bitwise_the_batched_path(case):
+def test_fused_small_solve_is_bitwise_the_batched_path(case, mesh1d):
     """Small batches take the fused one-CTA-per-sample solve; it repeats the
     batched kernels' arithmetic exactly (same bits either way)."""
-    levels, _ = _levels(case, 2)
+    levels, _ = _levels(case, mesh1d, 2)
     fused = wavemc.eval_pairs(levels[1], levels[0], 3, 1, 10, 40)  # 40 <= 2 x SMs: fused solve
     big = wavemc.eval_pairs(levels[1], levels[0], 3, 1, 0, 600)  # one batch of 600: batched kernels
     assert np.array_equal(fused[0], big[0][10:50]) and np.array_equal(fused[1], big[1][10:50])
