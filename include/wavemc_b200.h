@@ -312,6 +312,21 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
 int wmc_run_mlmc_vec(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
                      wmc_mlmc_result* result, wmc_level_stats* stats, double* estimate, wmc_error* err);
 
+/* Multi-device drivers (the reference's worker pool
+ * run_jobs, src/mlmc.cpp:107-149, one level set per device): levels holds
+ * n_devices groups of n_levels levels, level l of group d at
+ * levels[d * n_levels + l] (each group on its own device, the same level
+ * definitions).  Every wave's index range of a level is split into
+ * contiguous 64-sample granules per device; each device group runs on its
+ * own host thread; the per-sample results are folded on the host in (level,
+ * index) order, so stats, estimate and sample counts are bitwise those of
+ * the one-device drivers, whatever n_devices. */
+int wmc_run_mlmc_fixed_multi(wmc_level** levels, int n_devices, int n_levels, const long* counts, uint64_t seed,
+                             wmc_level_stats* stats, wmc_error* err);
+int wmc_run_mlmc_multi(wmc_level** levels, int n_devices, int n_levels, const double* model_cost,
+                       const wmc_mlmc_config* cfg, wmc_mlmc_result* result, wmc_level_stats* stats, double* estimate,
+                       wmc_error* err);
+
 /* Host-only helpers of the adaptive driver, as the reference's
  * optimal_samples (src/mlmc.cpp:75-92) and bias_proxy_sq (:94-98). */
 int wmc_optimal_samples(const double* variances, const double* costs, int n_levels, double eps, long min_samples,

@@ -130,6 +130,10 @@ SIGNATURES = [
     ("wmc_run_mlmc", C.c_int, [P(_VP), C.c_int, _DP, P(MlmcConfig), P(MlmcResult), P(LevelStats), P(Error)]),
     ("wmc_run_mlmc_vec", C.c_int, [P(_VP), C.c_int, _DP, P(MlmcConfig), P(MlmcResult), P(LevelStats), _DP,
                                    P(Error)]),
+    ("wmc_run_mlmc_fixed_multi", C.c_int, [P(_VP), C.c_int, C.c_int, P(C.c_long), C.c_uint64, P(LevelStats),
+                                           P(Error)]),
+    ("wmc_run_mlmc_multi", C.c_int, [P(_VP), C.c_int, C.c_int, _DP, P(MlmcConfig), P(MlmcResult), P(LevelStats), _DP,
+                                     P(Error)]),
     ("wmc_optimal_samples", C.c_int, [_DP, _DP, C.c_int, C.c_double, C.c_long, P(C.c_long)]),
     ("wmc_bias_proxy_sq", C.c_double, [C.c_double, C.c_double]),
     ("wmc_moments_device", C.c_int, [_VP, _VP, _VP, C.c_uint64, _VP]),

@@ -16,6 +16,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/wavemc_b200.h"
@@ -1908,16 +1909,105 @@ struct PairCache {
     long computed = 0;
 };
 
+// Evaluates index ranges of several levels into the per-level caches (results
+// appended in index order).  With n_dev device groups (levels[d * n_levels +
+// l] is level l on group d) every range is split into contiguous 64-sample
+// granules per group and each group runs on its own host thread (issue,
+// synchronise, copy out); the ranges of one group run concurrently on their
+// level streams.  A sample's results depend only on (seed, level, index), so
+// the caches -- and every fold of them -- are independent of n_dev, bitwise.
+struct Issue {
+    int level;
+    long first, count;
+};
+
+void eval_into_cache(wmc_level** levels, int n_dev, int n_levels, const std::vector<Issue>& issues,
+                     std::uint64_t seed, std::vector<PairCache>& cache) {
+    struct Part {
+        int level;
+        long first, count;
+        PairCache out;
+    };
+    // parts[d]: device group d's sub-ranges, in issue order
+    std::vector<std::vector<Part>> parts(n_dev);
+    for (const auto& j : issues) {
+        const long granules = (j.count + 63) / 64;
+        for (int d = 0; d < n_dev; ++d) {
+            const long g0 = granules * d / n_dev, g1 = granules * (d + 1) / n_dev;
+            const long f = j.first + 64 * g0, c = std::min(j.first + j.count, j.first + 64 * g1) - f;
+            if (c > 0) parts[d].push_back({j.level, f, c, {}});
+        }
+    }
+    auto run_group = [&](int d) {
+        wmc_level** lv = levels + static_cast<std::size_t>(d) * n_levels;
+        for (auto& pt : parts[d]) {
+            ensure_results(*lv[pt.level], static_cast<std::size_t>(pt.count));
+            issue_pairs(lv[pt.level], pt.level > 0 ? lv[pt.level - 1] : nullptr, seed,
+                        static_cast<std::uint32_t>(pt.level), static_cast<std::uint64_t>(pt.first),
+                        static_cast<std::uint64_t>(pt.count), nullptr, nullptr);
+        }
+        for (auto& pt : parts[d]) {
+            wmc_level* fine = lv[pt.level];
+            check(cudaSetDevice(fine->device), "cudaSetDevice");
+            check(cudaStreamSynchronize(fine->stream), "synchronize");
+            PairCache& c = pt.out;
+            const long nq = fine->tab.nq;
+            c.dq.assign(fine->h_dq, fine->h_dq + pt.count * nq);
+            c.qf.assign(fine->h_qf, fine->h_qf + pt.count * nq);
+            c.ff.assign(fine->h_ff, fine->h_ff + pt.count);
+            if (pt.level > 0)
+                c.fc.assign(fine->h_fc, fine->h_fc + pt.count);
+            else
+                c.fc.assign(pt.count, INT_MAX);
+            for (long i = 0; i < pt.count; ++i) {
+                wmc_cost pc{};
+                results_cost(fine, pt.level > 0 ? lv[pt.level - 1] : nullptr, static_cast<std::size_t>(i), 1, &pc);
+                c.cost.push_back(pc);
+            }
+        }
+    };
+    if (n_dev == 1) {
+        run_group(0);
+    } else {
+        std::vector<std::thread> threads;
+        std::vector<std::exception_ptr> errs(n_dev);
+        for (int d = 0; d < n_dev; ++d)
+            threads.emplace_back([&, d] {
+                try {
+                    run_group(d);
+                } catch (...) {
+                    errs[d] = std::current_exception();
+                }
+            });
+        for (auto& t : threads) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+    }
+    // append in index order: issue order, device-group order within an issue
+    for (std::size_t k = 0; k < issues.size(); ++k)
+        for (int d = 0; d < n_dev; ++d)
+            for (auto& pt : parts[d]) {
+                if (pt.level != issues[k].level || pt.first < issues[k].first ||
+                    pt.first >= issues[k].first + issues[k].count)
+                    continue;
+                PairCache& c = cache[pt.level];
+                if (pt.first != c.computed) throw DeviceError("eval_into_cache: results out of order");
+                c.dq.insert(c.dq.end(), pt.out.dq.begin(), pt.out.dq.end());
+                c.qf.insert(c.qf.end(), pt.out.qf.begin(), pt.out.qf.end());
+                c.ff.insert(c.ff.end(), pt.out.ff.begin(), pt.out.ff.end());
+                c.fc.insert(c.fc.end(), pt.out.fc.begin(), pt.out.fc.end());
+                c.cost.insert(c.cost.end(), pt.out.cost.begin(), pt.out.cost.end());
+                c.computed += pt.count;
+            }
+}
+
 // One wave: evaluate, on every level that needs more than its cache holds,
 // the missing indices rounded up to the 64-lane batch granule (plus `spec`:
 // the first 64 pairs of a level not yet in use), levels concurrently on their
-// streams; then fold into acc up to the targets in (level, index) order.
-void cached_wave(wmc_level** levels, int n_levels, const std::vector<long>& targets, int spec, std::uint64_t seed,
-                 std::vector<Acc>& acc, std::vector<PairCache>& cache, wmc_error* err) {
-    struct Issue {
-        int level;
-        long first, count;
-    };
+// streams (device groups on their host threads); then fold into acc up to
+// the targets in (level, index) order.
+void cached_wave(wmc_level** levels, int n_dev, int n_levels, const std::vector<long>& targets, int spec,
+                 std::uint64_t seed, std::vector<Acc>& acc, std::vector<PairCache>& cache, wmc_error* err) {
     std::vector<Issue> issues;
     for (int l = 0; l < static_cast<int>(targets.size()); ++l)
         if (targets[l] > cache[l].computed) {
@@ -1925,32 +2015,7 @@ void cached_wave(wmc_level** levels, int n_levels, const std::vector<long>& targ
             issues.push_back({l, cache[l].computed, (need + 63) / 64 * 64});
         }
     if (spec >= 0 && spec < n_levels && cache[spec].computed == 0) issues.push_back({spec, 0, 64});
-    for (const auto& j : issues) {
-        ensure_results(*levels[j.level], static_cast<std::size_t>(j.count));
-        issue_pairs(levels[j.level], j.level > 0 ? levels[j.level - 1] : nullptr, seed,
-                    static_cast<std::uint32_t>(j.level), static_cast<std::uint64_t>(j.first),
-                    static_cast<std::uint64_t>(j.count), nullptr, nullptr);
-    }
-    for (const auto& j : issues) {
-        wmc_level* fine = levels[j.level];
-        check(cudaSetDevice(fine->device), "cudaSetDevice");
-        check(cudaStreamSynchronize(fine->stream), "synchronize");
-        PairCache& c = cache[j.level];
-        const long nq = fine->tab.nq;
-        c.dq.insert(c.dq.end(), fine->h_dq, fine->h_dq + j.count * nq);
-        c.qf.insert(c.qf.end(), fine->h_qf, fine->h_qf + j.count * nq);
-        c.ff.insert(c.ff.end(), fine->h_ff, fine->h_ff + j.count);
-        if (j.level > 0)
-            c.fc.insert(c.fc.end(), fine->h_fc, fine->h_fc + j.count);
-        else
-            c.fc.insert(c.fc.end(), j.count, INT_MAX);
-        for (long i = 0; i < j.count; ++i) {
-            wmc_cost pc{};
-            results_cost(fine, j.level > 0 ? levels[j.level - 1] : nullptr, static_cast<std::size_t>(i), 1, &pc);
-            c.cost.push_back(pc);
-        }
-        c.computed += j.count;
-    }
+    eval_into_cache(levels, n_dev, n_levels, issues, seed, cache);
     if (err) err->sample = -1;
     for (int l = 0; l < static_cast<int>(targets.size()); ++l) {
         Acc& a = acc[l];
@@ -2610,10 +2675,28 @@ int wmc_run_mlmc(wmc_level** levels, int n_levels, const double* model_cost, con
     return wmc_run_mlmc_vec(levels, n_levels, model_cost, cfg, result, stats, nullptr, err);
 }
 
-int wmc_run_mlmc_vec(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
-                     wmc_mlmc_result* result, wmc_level_stats* stats, double* estimate, wmc_error* err) {
-    return guarded([&] {
-        if (!levels || n_levels < 1 || !model_cost || !cfg || !result || !stats)
+namespace {
+// device groups for the multi-device drivers: level l of group d at
+// levels[d * n_levels + l], one device per group, the same level tables
+void check_device_groups(wmc_level** levels, int n_dev, int n_levels) {
+    if (!levels || n_dev < 1 || n_levels < 1) throw ConfigError("device groups: bad arguments");
+    for (int d = 0; d < n_dev; ++d)
+        for (int l = 0; l < n_levels; ++l) {
+            const wmc_level* a = levels[l];
+            const wmc_level* b = levels[static_cast<std::size_t>(d) * n_levels + l];
+            if (!a || !b) throw ConfigError("device groups: NULL level");
+            if (b->device != levels[static_cast<std::size_t>(d) * n_levels]->device)
+                throw ConfigError("device groups: a group spans several devices");
+            if (a->tab.n != b->tab.n || a->tab.n_r != b->tab.n_r || a->tab.n_steps != b->tab.n_steps ||
+                a->tab.p != b->tab.p || a->tab.nq != b->tab.nq)
+                throw ConfigError("device groups: level " + std::to_string(l) + " differs between groups");
+        }
+}
+
+// the adaptive driver over n_dev device groups (levels[d * n_levels + l])
+void run_mlmc_impl(wmc_level** levels, int n_dev, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
+                   wmc_mlmc_result* result, wmc_level_stats* stats, double* estimate, wmc_error* err) {
+        if (!levels || n_levels < 1 || n_dev < 1 || !model_cost || !cfg || !result || !stats)
             throw ConfigError("wmc_run_mlmc: bad arguments");
         if (!(cfg->eps > 0.0)) throw ConfigError("run_mlmc: eps must be positive");
         if (cfg->alpha < 1.0) throw ConfigError("run_mlmc: alpha >= 1 required");
@@ -2641,8 +2724,8 @@ int wmc_run_mlmc_vec(wmc_level** levels, int n_levels, const double* model_cost,
                         if (acc[l].n < targets[l]) jobs.push_back({l, acc[l].n, targets[l] - acc[l].n});
                     run_levels(levels, jobs, cfg->master_seed, acc, err);
                 } else {
-                    cached_wave(levels, n_levels, targets, top + 1 <= cap ? top + 1 : -1, cfg->master_seed, acc,
-                                cache, err);
+                    cached_wave(levels, n_dev, n_levels, targets, top + 1 <= cap ? top + 1 : -1, cfg->master_seed,
+                                acc, cache, err);
                 }
                 std::vector<double> v(top + 1);
                 for (int l = 0; l <= top; ++l) v[l] = acc[l].variance();
@@ -2689,6 +2772,38 @@ int wmc_run_mlmc_vec(wmc_level** levels, int n_levels, const double* model_cost,
             norm_of.init(levels[0]->tab.qoi_norm_w);
             result->estimate = norm_of.norm(est.data());
         }
+}
+}  // namespace
+
+int wmc_run_mlmc_vec(wmc_level** levels, int n_levels, const double* model_cost, const wmc_mlmc_config* cfg,
+                     wmc_mlmc_result* result, wmc_level_stats* stats, double* estimate, wmc_error* err) {
+    return guarded([&] { run_mlmc_impl(levels, 1, n_levels, model_cost, cfg, result, stats, estimate, err); });
+}
+
+int wmc_run_mlmc_multi(wmc_level** levels, int n_devices, int n_levels, const double* model_cost,
+                       const wmc_mlmc_config* cfg, wmc_mlmc_result* result, wmc_level_stats* stats, double* estimate,
+                       wmc_error* err) {
+    return guarded([&] {
+        check_device_groups(levels, n_devices, n_levels);
+        run_mlmc_impl(levels, n_devices, n_levels, model_cost, cfg, result, stats, estimate, err);
+    });
+}
+
+int wmc_run_mlmc_fixed_multi(wmc_level** levels, int n_devices, int n_levels, const long* counts, uint64_t seed,
+                             wmc_level_stats* stats, wmc_error* err) {
+    return guarded([&] {
+        if (!levels || n_levels < 1 || !counts || !stats) throw ConfigError("wmc_run_mlmc_fixed_multi: bad arguments");
+        check_device_groups(levels, n_devices, n_levels);
+        std::vector<Issue> issues;
+        for (int l = 0; l < n_levels; ++l)
+            if (counts[l] > 0) issues.push_back({l, 0, counts[l]});
+        std::vector<PairCache> cache(n_levels);
+        eval_into_cache(levels, n_devices, n_levels, issues, seed, cache);
+        // fold in (level, index) order (src/mlmc.cpp:145-147): independent of n_devices
+        std::vector<Acc> acc(n_levels);
+        std::vector<long> targets(counts, counts + n_levels);
+        cached_wave(levels, n_devices, n_levels, targets, -1, seed, acc, cache, err);
+        for (int l = 0; l < n_levels; ++l) fill_stats(l, acc[l], 0.0, stats[l]);
     });
 }
 

@@ -14,12 +14,42 @@ import math
 SUM_KEYS = ("n_samples", "sum_dq", "sum_dq2", "sum_q", "sum_q2")
 
 
-def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
-    """(first, count) of rank's contiguous share of n indices."""
+GRANULE = 64  # samples per batch lane group of the device kernels
+
+
+def shard_range(n: int, rank: int, world: int, granule: int = GRANULE) -> tuple[int, int]:
+    """(first, count) of rank's contiguous share of n indices, in whole
+    granules of `granule` samples (the device batch granule: no rank pads a
+    partial batch except the one holding the level's tail)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("shard_range: bad rank/world")
-    a, b = rank * n // world, (rank + 1) * n // world
+    g = (n + granule - 1) // granule
+    g0, g1 = rank * g // world, (rank + 1) * g // world
+    a, b = min(n, granule * g0), min(n, granule * g1)
     return a, b - a
+
+
+def shard_levels(counts: list[int], pair_costs: list[float], world: int,
+                 granule: int = GRANULE) -> list[list[tuple[int, int]]]:
+    """Per rank, per level: (first, count) in whole granules, balanced over
+    all levels: each level's granules split evenly and its remainder granules
+    go to the ranks with the least work so far (cost = pair cost x samples);
+    every rank's indices of a level stay contiguous, ranks in order."""
+    load = [0.0] * world
+    out = [[(0, 0)] * len(counts) for _ in range(world)]
+    for lvl in sorted(range(len(counts)), key=lambda q: -pair_costs[q] * counts[q]):
+        n = counts[lvl]
+        g = (n + granule - 1) // granule
+        per = [g // world] * world
+        for r in sorted(range(world), key=lambda q: (load[q], q))[: g % world]:
+            per[r] += 1
+        first = 0
+        for r in range(world):
+            a, b = min(n, granule * first), min(n, granule * (first + per[r]))
+            out[r][lvl] = (a, b - a)
+            load[r] += (b - a) * pair_costs[lvl]
+            first += per[r]
+    return out
 
 
 def estimators(sums: dict) -> dict:

@@ -424,6 +424,44 @@ def run_mlmc(levels: list[Level], model_cost: list[float], config: MlmcConfig | 
                       res.total_model_cost, res.rmse, [_stats(stats[i]) for i in range(res.levels_used + 1)], est)
 
 
+def _groups(level_groups: list[list[Level]]):
+    n_dev, n = len(level_groups), len(level_groups[0])
+    if any(len(g) != n for g in level_groups):
+        raise ValueError("every device group needs the same number of levels")
+    arr = (C.c_void_p * (n_dev * n))(*[lv._h.value for g in level_groups for lv in g])
+    return arr, n_dev, n
+
+
+def run_mlmc_fixed_multi(level_groups: list[list[Level]], counts: list[int], seed: int = 0) -> list[dict]:
+    """run_mlmc_fixed over several devices (wmc_run_mlmc_fixed_multi): one
+    level list per device, 64-sample granules per device, one host thread per
+    device, host fold in index order -- bitwise the one-device result."""
+    arr, n_dev, n = _groups(level_groups)
+    cnt = (C.c_long * n)(*counts)
+    stats = (N.LevelStats * n)()
+    err = N.Error()
+    N.check(N.lib().wmc_run_mlmc_fixed_multi(arr, n_dev, n, cnt, seed, stats, C.byref(err)), err)
+    return [_stats(stats[i]) for i in range(n)]
+
+
+def run_mlmc_multi(level_groups: list[list[Level]], model_cost: list[float],
+                   config: MlmcConfig | None = None) -> MlmcResult:
+    """The adaptive driver over several devices (wmc_run_mlmc_multi)."""
+    config = config or MlmcConfig()
+    arr, n_dev, n = _groups(level_groups)
+    cost = (C.c_double * n)(*model_cost)
+    cfg = N.MlmcConfig(config.eps, config.alpha, config.initial_samples, config.initial_levels, config.max_level,
+                       config.master_seed, config.bias_window)
+    res = N.MlmcResult()
+    stats = (N.LevelStats * n)()
+    err = N.Error()
+    est = np.zeros(max(1, level_groups[0][0].info.get("nq", 1)), np.float64)
+    N.check(N.lib().wmc_run_mlmc_multi(arr, n_dev, n, cost, C.byref(cfg), C.byref(res), stats, _dptr(est),
+                                       C.byref(err)), err)
+    return MlmcResult(res.estimate, bool(res.converged), res.levels_used, res.total_variance, res.bias,
+                      res.total_model_cost, res.rmse, [_stats(stats[i]) for i in range(res.levels_used + 1)], est)
+
+
 def optimal_samples(variances, costs, eps: float, min_samples: int = 2) -> list[int]:
     """Reference optimal_samples (src/mlmc.cpp:75-92)."""
     n = len(variances)

@@ -58,6 +58,25 @@ def test_shard_ranges_cover_every_index_once():
             assert spans[-1][0] + spans[-1][1] == n
     with pytest.raises(ValueError):
         shard.shard_range(4, 2, 2)
+    # whole 64-sample granules: config-1 level 4 (256 samples) at 8 ranks
+    spans = [shard.shard_range(256, r, 8) for r in range(8)]
+    assert all(c in (0, 64) for _, c in spans) and sum(c for _, c in spans) == 256
+
+
+def test_shard_levels_balance_whole_granules():
+    from paper_2106_11117_b200 import configs
+    counts = configs.CONFIG1_COUNTS
+    costs = [1.0, 2.0, 2.5, 5.0, 12.0]  # pair costs grow with the level
+    for world in (1, 2, 4, 8):
+        plan = shard.shard_levels(counts, costs, world)
+        for lvl, n in enumerate(counts):
+            spans = [plan[r][lvl] for r in range(world)]
+            assert spans[0][0] == 0 and sum(c for _, c in spans) == n
+            for (a, c), (b, _) in zip(spans, spans[1:]):
+                assert a + c == b
+            assert all(c % 64 == 0 or a + c == n for a, c in spans)
+        work = [sum(plan[r][l][1] * costs[l] for l in range(len(counts))) for r in range(world)]
+        assert max(work) / (sum(work) / world) < 1.1
 
 
 def test_two_gloo_ranks_match_single_process(golden):
