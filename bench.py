@@ -8,9 +8,13 @@ levels 0..4 (h_l = 1/16..1/256, p_l = 32..2, N_l = 65536, 16384, 4096, 1024,
 U = n + (p-1)|R| per global step per solve.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--config 0..4] [--integrator lts|lf]
 
-Under torchrun every rank evaluates the index range [r N_l / G, (r+1) N_l / G)
-of every level (weak in samples per GPU? no: total work is fixed -> "strong").
+--gpus N > 1 re-launches itself under torch.distributed.run (N ranks, one
+per GPU, NCCL).  Rank r evaluates whole 64-sample granules of every level
+(balanced over the levels, shard.shard_levels) with streams keyed by the
+global index, so per-sample results do not depend on N; total work is fixed
+("strong" scaling).
 """
 from __future__ import annotations
 
@@ -32,6 +36,9 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 METRIC = "DOF-updates/s (FP64, LTS substeps incl.)"
 TTR_EPS = 1e-4  # RMSE target of the time-to-RMSE run (config-1 hierarchy)
 UNIT = "DOF-updates/s"
+# the paper's per-sample model cost ratio C_l^LF / C_l^LTS of its 2D channel
+# (PAPER.md:1067-1070), context for the measured LTS/LF time ratios
+PAPER_LF_OVER_LTS = [5.89, 7.82, 4.54, 2.51]
 
 
 def parse():
@@ -42,11 +49,14 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--scale", type=float, default=None,
                     help="fraction of N_l (default 1.0 = the BASELINE counts; config 3: 0.03, a 246-sample slice "
-                         "of the 8192 -- per-sample cost is uniform, the full set is ~20 min per step)")
+                         "of the 8192 -- per-sample cost is uniform, the full set is ~10 min per step)")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4],
                     help="BASELINE config: 1 (default, MLMC), 0 (single-level MC), 2 (graded L-shape MLMC, "
                          "nested 3-tier LTS), 3 (large single level), 4 (adaptive MLMC to an RMSE target, "
                          "log-normal KL coefficient)")
+    ap.add_argument("--integrator", default="lts", choices=["lts", "lf"],
+                    help="config 1: lf = the global leap-frog comparison arm (dt = 0.2 h_min on every level); "
+                         "the line then carries the measured LF / LTS time ratios")
     ap.add_argument("--eps", type=float, default=None, help="config 4: RMSE target (default BASELINE 1e-3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -58,6 +68,40 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N without a launcher: re-run this script under
+    torch.distributed.run, N ranks on this node, rendezvous on 127.0.0.1."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def cpu_info() -> dict:
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cores": os.cpu_count() or 1}
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except OSError:
+        return {}
 
 
 # ---------------------------------------------------------------------------
@@ -111,9 +155,9 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baselines (the reference compiled from its own sources, else our port)
+# workloads
 
-def workload(config: int):
+def workload(config: int, integrator: str = "lts"):
     """(level defs, N per level, description, CPU horizon override)."""
     from paper_2106_11117_b200 import configs
     if config == 0:
@@ -128,91 +172,100 @@ def workload(config: int):
         # the CPU sample keeps the mesh and the per-step work but shortens the
         # horizon to 16 global steps (per-step cost is uniform in time)
         return [d], [configs.CONFIG3_COUNT], "BASELINE config 3: single level h=1/1024 refined x8, p=8, T=0.5", 16 * d.dt
+    if integrator == "lf":
+        return configs.config1("lf"), list(configs.CONFIG1_COUNTS), (
+            "BASELINE config 1, global leap-frog arm: fixed-N MLMC, 5 levels h=1/16..1/256, dt=0.2 h_min"), None
     return configs.config1(), list(configs.CONFIG1_COUNTS), (
         "BASELINE config 1: fixed-N MLMC, LF-LTS, 5 levels h=1/16..1/256, p=32..2"), None
 
 
-def oracle_problem(d, final_time=None):
-    """The C restatement's problem for a level definition (test-side mirror of
-    configs.level_spec)."""
-    import oracle_py
-    from paper_2106_11117_b200 import configs
-    T = d.final_time if final_time is None else final_time
-    if d.shape == "lshape":
-        c = configs.CONFIG2_PROBLEM
-        return oracle_py.problem(d.dt, d.substeps, final_time=T, cells=c["cells"], ic=c["ic"], box=c["qoi_box"],
-                                 domain=c["domain"], qoi_mean=True, tiers=d.tiers)
-    return oracle_py.problem(d.dt, d.substeps, final_time=T)
+# ---------------------------------------------------------------------------
+# CPU baselines: the reference compiled from its own sources (oracle/_ref),
+# else our C restatement.  Inputs (meshes, level data) come from a separate
+# process (tools/dump_inputs.py) so the timed reference arm never maps the
+# product library.
+
+def dump_inputs(config: int, final_time=None, lf=False, kl=False) -> dict:
+    tmp = tempfile.mkdtemp(prefix="wmc_inputs_")
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "dump_inputs.py"), "--config", str(config), "--out", tmp]
+    if final_time is not None:
+        cmd += ["--final-time", repr(final_time)]
+    if lf:
+        cmd.append("--lf")
+    if kl:
+        cmd.append("--kl")
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    inp = load_json(os.path.join(tmp, "inputs.json"))
+    inp["dir"] = tmp
+    return inp
 
 
-def ref_sample_counts(threads: int, defs=None):
-    """Bounded sample of config 1 for the CPU, in the proportions of N_l
-    (65536 : 16384 : 4096 : 1024 : 256 = 256 : 64 : 16 : 4 : 1), sized for
-    ~10-15 s of wall time on `threads` cores (measured: 2.8 s for a quarter of
-    this sample on 16 cores)."""
+def ref_sample_counts(threads: int, config: int):
+    """Bounded sample for the CPU, in the proportions of N_l, sized for
+    ~10-20 s of wall time on `threads` cores."""
     t = max(1, threads)
-    if defs is not None and defs[0].shape == "lshape":  # config 2: N_l halving, horizon T/8
+    if config == 2:  # N_l halving, horizon T/8
         return [8 * t, 4 * t, 2 * t, t, max(1, t // 2)]
-    return [64 * t, 16 * t, 4 * t, t, max(1, t // 4)]
+    if config in (1, 4):
+        return [64 * t, 16 * t, 4 * t, t, max(1, t // 4)]
+    return None
 
 
-def run_reference_cpu(defs, threads: int, final_time=None):
-    """A bounded sample through the unmodified reference library (oracle/_ref),
-    its own run_jobs-style pool of `threads` workers.  Returns dict."""
+def config2_extra(final_time):
+    from paper_2106_11117_b200 import configs  # constants only (no library)
+    c = configs.CONFIG2_PROBLEM
+    return {"T": repr(final_time), "cells-x": c["cells"][0], "cells-y": c["cells"][1], "ic": ",".join(map(repr, c["ic"])),
+            "box": ",".join(map(repr, c["qoi_box"])), "domain": ",".join(map(repr, c["domain"])), "qoi-mean": 1}
+
+
+def run_reference_cpu(config: int, threads: int, final_time=None, lf=False, counts=None):
+    """A bounded sample through the unmodified reference library (its own
+    sample_delta_q over a run_jobs-style pool of `threads` workers)."""
     import oracle_py
-    from paper_2106_11117_b200 import configs
-    counts = ref_sample_counts(threads, defs) if len(defs) > 1 else [4 * threads if final_time is None else threads]
-    tmp = tempfile.mkdtemp(prefix="wmc_bench_")
-    specs = []
-    nested = any(d.tiers > 1 for d in defs)
-    for l, d in enumerate(defs):
-        p = os.path.join(tmp, f"l{l}.mesh")
-        configs.build_mesh(d).dump(p)
-        # config 2: the reference has no nested tiers; its own LF-LTS on the
-        # same mesh needs P = P_1 and p = 2^tiers (stable at the finest tier)
-        specs.append((p, d.dt, d.substeps ** d.tiers if nested else d.substeps))
-    drv = oracle_py.RefDriver()
+    inp = dump_inputs(config, final_time, lf)
+    levels = inp["levels"]
+    counts = counts or ref_sample_counts(threads, config) or [4 * threads if final_time is None else threads]
+    nested = any(lv["tiers"] > 1 for lv in levels)
+    # config 2: the reference has no nested tiers; its own LF-LTS on the same
+    # mesh takes P = P_1 and p = 2^tiers (stable at the finest tier)
+    specs = [(lv["mesh"], lv["dt"], lv["p"] ** lv["tiers"] if nested else lv["p"]) for lv in levels]
     extra = {"T": repr(final_time)} if final_time is not None else {}
     if nested:
-        c = configs.CONFIG2_PROBLEM
-        extra.update({"T": repr(final_time if final_time is not None else defs[0].final_time),
-                      "cells-x": c["cells"][0], "cells-y": c["cells"][1], "ic": ",".join(map(repr, c["ic"])),
-                      "box": ",".join(map(repr, c["qoi_box"])), "domain": ",".join(map(repr, c["domain"])),
-                      "qoi-mean": 1})
-    res = drv.mlmc(specs, counts, threads=threads, **extra)
-    shutil.rmtree(tmp, ignore_errors=True)
+        extra = config2_extra(final_time if final_time is not None else 2.0)
+    res = oracle_py.RefDriver().mlmc(specs, counts, kind="lf" if lf else "lts", threads=threads, **extra)
+    shutil.rmtree(inp["dir"], ignore_errors=True)
     work = res["dof_updates"]
     if nested:  # the same samples counted in the config-2 (nested) units
-        from paper_2106_11117_b200 import wavemc
-        upd = []
-        for d in defs:
-            spec = configs.level_spec(d)
-            if final_time is not None:
-                spec.final_time = final_time
-            upd.append(wavemc.level_plan(configs.build_mesh(d), spec)["dof_updates_per_solve"])
+        upd = [lv["dof_updates_per_solve"] for lv in levels]
         work = sum(n * (upd[l] + (upd[l - 1] if l else 0.0)) for l, n in enumerate(counts))
     return {"value": work / res["seconds"], "seconds": res["seconds"], "dof_updates": work, "counts": counts,
-            "kind": "reference", "cores": res["threads"],
+            "kind": "reference", "cores": res["threads"], "levels": res["levels"],
             "note": ("reference single-tier LF-LTS (P = P_1, p = 8) on the config-2 meshes and samples (it has no "
                      "nested tiers); value = nested-scheme DOF-updates of the same samples / reference time"
                      if nested else None)}
 
 
-def run_port_cpu(defs, threads: int, final_time=None):
+def run_port_cpu(config: int, threads: int, final_time=None):
     """Fallback when oracle/_ref is absent: our C restatement, `threads` workers."""
     from concurrent.futures import ThreadPoolExecutor
 
     import oracle_py
-    from paper_2106_11117_b200 import configs
+    from paper_2106_11117_b200 import configs, wavemc
     oracle_py.build()
     orc = oracle_py.COracle()
-    counts = ref_sample_counts(threads, defs) if len(defs) > 1 else [4 * threads if final_time is None else threads]
-    from paper_2106_11117_b200 import wavemc
+    defs = workload(config)[0]
+    counts = ref_sample_counts(threads, config) or [4 * threads if final_time is None else threads]
     meshes = [oracle_py.MeshArrays(*configs.build_mesh(d).arrays()) for d in defs]
     T = [final_time if final_time is not None else d.final_time for d in defs]
-    probs = [oracle_problem(d, t) for d, t in zip(defs, T)]
+    probs = []
     upd = []
     for d, t in zip(defs, T):
+        if d.shape == "lshape":
+            c = configs.CONFIG2_PROBLEM
+            probs.append(oracle_py.problem(d.dt, d.substeps, final_time=t, cells=c["cells"], ic=c["ic"],
+                                           box=c["qoi_box"], domain=c["domain"], qoi_mean=True, tiers=d.tiers))
+        else:
+            probs.append(oracle_py.problem(d.dt, d.substeps, final_time=t))
         spec = configs.level_spec(d)
         spec.final_time = t
         upd.append(wavemc.level_plan(configs.build_mesh(d), spec)["dof_updates_per_solve"])
@@ -220,8 +273,7 @@ def run_port_cpu(defs, threads: int, final_time=None):
 
     def one(job):
         l, i = job
-        rc, _, _, _, _ = orc.eval_pairs(meshes[l], probs[l], meshes[l - 1] if l else None,
-                                        probs[l - 1] if l else None, 0, l, i, 1)
+        orc.eval_pairs(meshes[l], probs[l], meshes[l - 1] if l else None, probs[l - 1] if l else None, 0, l, i, 1)
         return upd[l] + (upd[l - 1] if l else 0.0)
 
     t0 = time.perf_counter()
@@ -232,65 +284,81 @@ def run_port_cpu(defs, threads: int, final_time=None):
             "cores": threads}
 
 
-def reference_time_to_rmse(defs, threads: int):
+def cpu_baseline(config: int, threads: int, final_time=None, lf=False):
+    import oracle_py
+    if os.path.exists(oracle_py.REF_DRIVER):
+        return run_reference_cpu(config, threads, final_time, lf)
+    return run_port_cpu(config, threads, final_time)
+
+
+def reference_time_to_rmse(threads: int):
     """The reference's own run_mlmc (src/mlmc.cpp:165-233) to RMSE TTR_EPS on
     the config-1 hierarchy, wall time measured by the driver."""
     import oracle_py
-    from paper_2106_11117_b200 import configs
-    tmp = tempfile.mkdtemp(prefix="wmc_ttr_")
-    specs = []
-    for l, d in enumerate(defs):
-        p = os.path.join(tmp, f"l{l}.mesh")
-        configs.build_mesh(d).dump(p)
-        specs.append((p, d.dt, d.substeps))
+    inp = dump_inputs(1)
+    specs = [(lv["mesh"], lv["dt"], lv["p"]) for lv in inp["levels"]]
     res = oracle_py.RefDriver().adaptive(specs, TTR_EPS, threads=threads)
-    shutil.rmtree(tmp, ignore_errors=True)
+    shutil.rmtree(inp["dir"], ignore_errors=True)
     return {"eps": TTR_EPS, "seconds": res["seconds"], "rmse": math.sqrt(res["total_variance"] + res["bias"]),
             "converged": res["converged"], "estimate": res["estimate"], "N_l": [lv["N"] for lv in res["levels"]],
             "threads": res["threads"]}
 
 
-def cpu_baseline(defs, threads: int, final_time=None):
+def reference_lf_over_lts(threads: int):
+    """The reference's per-solve time ratio LF / LTS on every config-1 level
+    (leapfrog_step at dt = 0.2 h_min against lts_step at dt = 0.2 h_l), from
+    a bounded sample of single-level solves timed by its own driver."""
     import oracle_py
-    if os.path.exists(oracle_py.REF_DRIVER):
-        return run_reference_cpu(defs, threads, final_time)
-    return run_port_cpu(defs, threads, final_time)
+    drv = oracle_py.RefDriver()
+    out = []
+    lts, lf = dump_inputs(1), dump_inputs(1, lf=True)
+    try:
+        for l, (a, b) in enumerate(zip(lts["levels"], lf["levels"])):
+            n = max(1, threads)
+            ha, _ = drv.solve(a["mesh"], a["dt"], a["p"], "lts", 0, 0, n, threads=threads)
+            hb, _ = drv.solve(b["mesh"], b["dt"], 1, "lf", 0, 0, n, threads=threads)
+            out.append(float(hb["seconds"]) / float(ha["seconds"]))
+    finally:
+        shutil.rmtree(lts["dir"], ignore_errors=True)
+        shutil.rmtree(lf["dir"], ignore_errors=True)
+    return out
 
 
 # ---------------------------------------------------------------------------
 
 def reference_arm(args, world, rank):
-    from paper_2106_11117_b200 import configs
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    defs, counts_total, label, cpu_T = workload(args.config)
+    _, counts_total, label, cpu_T = workload(args.config, args.integrator)
+    lf = args.integrator == "lf"
     try:
-        runs = [cpu_baseline(defs, threads, cpu_T) for _ in range(args.warmup + args.steps)]
+        runs = [cpu_baseline(args.config, threads, cpu_T, lf) for _ in range(args.warmup + args.steps)]
     except Exception as exc:  # the oracle always exists; report loudly
         print(json.dumps({"impl": "reference", "unavailable": f"reference CPU run failed: {exc}"}))
         return 0
     timed = runs[args.warmup:]
     value = sum(r["dof_updates"] for r in timed) / sum(r["seconds"] for r in timed)
     ttr = None
-    if args.config == 1:
+    if args.config == 1 and not lf:
         try:
-            ttr = reference_time_to_rmse(defs, threads)
+            ttr = reference_time_to_rmse(threads)
         except Exception as exc:
             ttr = {"eps": TTR_EPS, "error": str(exc)}
     r0 = timed[0]
+    ci = cpu_info()
     sample = (f"config {args.config} bounded sample N_l={r0['counts']} (of {counts_total}) per step"
               + (f", horizon shortened to T={cpu_T!r}" if cpu_T is not None else "")
-              + f", {r0['cores']} threads, {r0['kind']}"
+              + f", {r0['cores']} threads, {r0['kind']}, {ci['cpu_model']}"
               + (f"; {r0['note']}" if r0.get("note") else ""))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(r["seconds"] for r in timed) / len(timed),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (counter-based RNG draws, seed 0)",
             "config": {"workload": label + " (bounded CPU sample)",
-                       "parallelism": f"{r0['cores']} CPU threads"},
+                       "parallelism": f"{r0['cores']} CPU threads ({ci['cpu_model']})"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": r0["cores"], "kind": r0["kind"],
-                             "sample": sample},
+                             "cpu_model": ci["cpu_model"], "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "time_to_rmse": ttr}
     print(json.dumps(line))
@@ -307,18 +375,19 @@ def b200_arm(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    defs, counts_total, label, cpu_T = workload(args.config)
+    lf = args.integrator == "lf"
+    defs, counts_total, label, cpu_T = workload(args.config, args.integrator)
     if args.scale is None:
         args.scale = 0.03 if args.config == 3 else 1.0
     if args.scale != 1.0:
         label += f" (N_l scaled by {args.scale})"
     counts_total = [max(1, int(round(n * args.scale))) for n in counts_total]
     levels = [configs.build_level(d, device=local) for d in defs]
-    spans = [shard.shard_range(n, rank, world) for n in counts_total]
-    first = [f for f, _ in spans]
-    counts = [c for _, c in spans]
     upd = [lv.info["dof_updates_per_solve"] for lv in levels]
     per_pair = [upd[l] + (upd[l - 1] if l else 0.0) for l in range(len(levels))]
+    spans = shard.shard_levels(counts_total, per_pair, world)[rank]
+    first = [f for f, _ in spans]
+    counts = [c for _, c in spans]
     total_updates = sum(n * per_pair[l] for l, n in enumerate(counts_total))
 
     dev = torch.device("cuda", local)
@@ -328,23 +397,25 @@ def b200_arm(args, world, rank, local):
     streams = [torch.cuda.ExternalStream(lv.stream, device=dev) for lv in levels]
     main = torch.cuda.current_stream(dev)
 
-    def step_device(sequential=False):
+    def step_device(sequential=False, lvls=None, strs=None):
+        lvls = lvls or levels
+        strs = strs or streams
         d_mom.zero_()
         ev0 = torch.cuda.Event()
         ev0.record(main)
-        for l, lv in enumerate(levels):
+        for l, lv in enumerate(lvls):
             if counts[l] == 0:
                 continue
-            streams[l].wait_event(ev0)
-            wavemc.eval_pairs_device(lv, levels[l - 1] if l else None, 0, l, first[l], counts[l],
+            strs[l].wait_event(ev0)
+            wavemc.eval_pairs_device(lv, lvls[l - 1] if l else None, 0, l, first[l], counts[l],
                                      d_dq[l].data_ptr(), d_qf[l].data_ptr())
             wavemc.moments_device(lv, d_dq[l].data_ptr(), d_qf[l].data_ptr(), counts[l],
                                   d_mom.data_ptr() + 8 * 4 * l)
             if sequential:  # profiling: kernels of one level at a time
                 wavemc.synchronize(lv)
-        for l in range(len(levels)):
+        for l in range(len(lvls)):
             e = torch.cuda.Event()
-            e.record(streams[l])
+            e.record(strs[l])
             main.wait_event(e)
         if dist is not None:
             dist.all_reduce(d_mom)
@@ -355,10 +426,15 @@ def b200_arm(args, world, rank, local):
             dist.barrier()
             torch.cuda.synchronize(dev)
 
+    def check_levels():  # device-resident results: the first unstable sample, if any (check_finite)
+        for lv in levels:
+            wavemc.synchronize(lv)
+
     # warm-up, then K timed steps bracketed by barrier + synchronize
     for _ in range(args.warmup):
         step_device()
     barrier()
+    check_levels()
     launches0 = wavemc.launch_count()
     with ClockSampler(local) as clocks:
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -367,6 +443,7 @@ def b200_arm(args, world, rank, local):
             step_device()
         end.record(main)
         barrier()
+    check_levels()
     launches = wavemc.launch_count() - launches0
     ms = start.elapsed_time(end) / args.steps
     if dist is not None:
@@ -377,7 +454,8 @@ def b200_arm(args, world, rank, local):
     mom = d_mom.cpu().tolist()
 
     # e2e: the public host API (per-sample results D2H + host fold in index
-    # order) per step, plus the allreduce of the per-level sums
+    # order) per step, plus the allreduce of the per-level sums; the same K
+    # steps as the device timing
     def step_e2e():
         stats = wavemc.run_mlmc_fixed(levels, counts, 0, first)
         return shard.allreduce_level_sums(stats, device=dev)
@@ -386,13 +464,12 @@ def b200_arm(args, world, rank, local):
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(1, min(args.steps, 2))
     t0.record(main)
-    for _ in range(e2e_steps):
+    for _ in range(args.steps):
         stats = step_e2e()
     t1.record(main)
     barrier()
-    e2e_ms = t0.elapsed_time(t1) / e2e_steps
+    e2e_ms = t0.elapsed_time(t1) / args.steps
     if dist is not None:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -402,7 +479,7 @@ def b200_arm(args, world, rank, local):
     # MLMC time-to-RMSE: the adaptive driver (reference run_mlmc, batched)
     # from scratch to convergence at TTR_EPS, wall time around the public call
     ttr = None
-    if world == 1 and args.config == 1:
+    if world == 1 and args.config == 1 and not lf:
         costs = [lv.info["dof_updates_per_solve"] for lv in levels]
         wavemc.run_mlmc(levels, costs, wavemc.MlmcConfig(eps=TTR_EPS * 4))  # warm-up
         torch.cuda.synchronize(dev)
@@ -414,8 +491,53 @@ def b200_arm(args, world, rank, local):
         ttr = {"eps": TTR_EPS, "seconds": sorted(runs)[1], "runs_s": runs, "rmse": res.rmse,
                "converged": res.converged, "estimate": res.estimate, "N_l": [lv["n_samples"] for lv in res.levels]}
 
+    # config-1 global leap-frog arm: the LTS estimator timed in the same run
+    # and the per-level LF / LTS solve-time ratios (device and reference CPU)
+    lf_vs_lts = None
+    if lf and args.config == 1:
+        lts_levels = [configs.build_level(d, device=local) for d in configs.config1()]
+        lts_streams = [torch.cuda.ExternalStream(lv.stream, device=dev) for lv in lts_levels]
+        for _ in range(max(1, args.warmup)):
+            step_device(lvls=lts_levels, strs=lts_streams)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(main)
+        for _ in range(args.steps):
+            step_device(lvls=lts_levels, strs=lts_streams)
+        b.record(main)
+        barrier()
+        lts_ms = a.elapsed_time(b) / args.steps
+        per_level = []
+        for l in range(len(levels)):  # one 1024-sample batch of single solves per level and integrator
+            ts = []
+            for lv in (levels[l], lts_levels[l]):
+                n = 1024
+                buf = torch.empty(n, dtype=torch.float64, device=dev)
+                wavemc.eval_pairs_device(lv, None, 0, l, 0, n, buf.data_ptr(), buf.data_ptr())
+                wavemc.synchronize(lv)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s = torch.cuda.ExternalStream(lv.stream, device=dev)
+                e0.record(s)
+                wavemc.eval_pairs_device(lv, None, 0, l, 0, n, buf.data_ptr(), buf.data_ptr())
+                e1.record(s)
+                wavemc.synchronize(lv)
+                ts.append(e0.elapsed_time(e1))
+            per_level.append(ts[0] / ts[1])
+        lf_vs_lts = {"estimator_time_ratio_lf_over_lts": ms / lts_ms, "lts_estimator_ms": lts_ms,
+                     "per_level_solve_time_ratio_lf_over_lts": per_level,
+                     "paper_model_cost_ratio_lf_over_lts_channel2d": PAPER_LF_OVER_LTS,
+                     "note": "per-level ratios: one batch of 1024 single solves per integrator on the device"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            try:
+                lf_vs_lts["reference_cpu_per_level_solve_time_ratio_lf_over_lts"] = reference_lf_over_lts(
+                    os.cpu_count() or 1)
+            except Exception as exc:
+                lf_vs_lts["reference_cpu_error"] = str(exc)
+
     # kernel-level profile pass (not timed above): per-kernel device time
-    roofline, kernels = None, None
+    roofline, kernels, step_frac = None, None, None
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    fp64 = load_json(os.path.join(ROOT, "profiles", "fp64_peak.json"))
     if not args.no_profile:
         for lv in levels:
             wavemc.profile_enable(lv, True)
@@ -425,44 +547,46 @@ def b200_arm(args, world, rank, local):
         for lv in levels:
             prof.append(wavemc.profile_read(lv))
             wavemc.profile_enable(lv, False)
-        roofline, kernels = roofline_from_profile(levels, counts, prof, ms)
-
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except OSError:
-        pass
-    if roofline is not None:
-        peak = peaks.get("hbm_gbs", 6650.0)
-        roofline["peak"] = peak
-        roofline["frac"] = roofline["achieved"] / peak
-        roofline["peak_source"] = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback"
+        roofline, kernels, step_bytes = roofline_from_profile(levels, counts, prof, ms, peaks, fp64)
+        step_frac = {"bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (ms * 1e-3) / 1e9,
+                     "peak_GBps": peaks.get("hbm_gbs", 6650.0),
+                     "frac": step_bytes / (ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                     "note": "SURVEY 8(d) algorithmic bytes (24 B per DOF per solve per global step) of the whole "
+                             "step over ms_per_step, against the measured HBM copy peak"}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based RNG draws, seed 0)",
             "config": {"workload": label,
                        "N_l": counts_total, "levels": [{"n": lv.info["n"], "n_r": lv.info["n_r"], "p": lv.info["p"],
-                                                        "n_steps": lv.info["n_steps"]} for lv in levels],
-                       "dof_updates_per_step": total_updates, "parallelism": f"samples sharded over {world} GPU(s)",
+                                                        "n_steps": lv.info["n_steps"],
+                                                        "path": lv.info["substep_path"]} for lv in levels],
+                       "dof_updates_per_step": total_updates,
+                       "parallelism": f"samples sharded over {world} GPU(s) in 64-sample granules",
                        "l2": "inputs (state 2 x n x batch x 8 B per level) exceed L2 at levels 2-4; no flush"},
             "e2e": {"value": total_updates / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": args.steps,
+                    "note": "inputs are seeds (per-sample coefficients drawn on the device); per-sample dQ, Q and "
+                            "fail flags copied D2H and folded on the host every step"},
             "gpu_launches": launches, "clocks": clocks.summary(),
             "moments": [{"level": l, "sum_dq": mom[4 * l], "sum_dq2": mom[4 * l + 1], "sum_q": mom[4 * l + 2],
                          "sum_q2": mom[4 * l + 3]} for l in range(len(levels))],
             "variance": [s["variance"] for s in stats]}
     if ttr is not None:
         line["time_to_rmse"] = ttr
+    if lf_vs_lts is not None:
+        line["lf_vs_lts"] = lf_vs_lts
     if roofline is not None:
         line["roofline"] = roofline
+        line["step_frac"] = step_frac
         line["kernels"] = kernels
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
+        ci = cpu_info()
         try:
-            cb = cpu_baseline(defs, threads, cpu_T)
+            cb = cpu_baseline(args.config, threads, cpu_T, lf)
             line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
+                                    "cpu_model": ci["cpu_model"],
                                     "sample": f"config {args.config} bounded sample N_l={cb['counts']}"
                                               + (f", T={cpu_T!r}" if cpu_T is not None else "")
                                               + f", {cb['seconds']:.1f} s"
@@ -477,130 +601,108 @@ def b200_arm(args, world, rank, local):
     return 0
 
 
-def roofline_from_profile(levels, counts, prof, step_ms):
-    """Per-kernel device time from the profiled pass, and the roofline of the
-    dominant HBM-bound kernel.  Algorithmic bytes per launch (per sample):
-      sweep                  8 B x (n reads of z_n + (n - |R|) reads of z_{n-1}
-                             + n writes of z_{n+1} or g)
-      on-chip substep        8 B x 2 |R| (g in, d_p out) -- on-chip bound
-      HBM-resident substep   8 B x 4 |R| per substep (d_m, d_{m-1}, g in,
-                             d_{m+1} out) + 8 B x 2 |R| on the last (z_n, z_{n-1})
-      R update               8 B x 4 |R|"""
-    fused_lv = [bool(lv.info.get("fused")) for lv in levels]
-    sweep_ms = sum(p["sweep_ms"] for p in prof)
-    sub_ms = sum(p["sub_ms"] for p, f in zip(prof, fused_lv) if not f)
-    fused_ms = sum(p["sub_ms"] for p, f in zip(prof, fused_lv) if f)
-    upd_ms = sum(p["upd_ms"] for p in prof)
-    sweep_bytes = sub_bytes = sub_flops = sub_updates = 0.0
-    fused_bytes = fused_updates = fused_flops = 0.0
-    global_path = any(lv.info["substep_path"] in (3, 4) for lv in levels)
-    for l, lv in enumerate(levels):
-        for lvl in ([l] + ([l - 1] if l else [])):
-            info = levels[lvl].info
-            n, nr, steps, p = info["n"], info["n_r"], info["n_steps"], info["p"]
-            c = counts[l]
-            if fused_lv[lvl]:
-                # whole solves on chip: HBM sees z_0 and the QoI only; the
-                # SURVEY 8(d) algorithmic figure (24 B per DOF per global step)
-                # is reported as the HBM-equivalent rate of the same work
-                fused_bytes += 24.0 * c * steps * n
-                fused_updates += c * info["dof_updates_per_solve"]
-                fused_flops += c * (steps - 1) * ((p - 1) * (2.0 * info["ap_nnz"] + 7.0 * nr) + 2.0 * info["nnz"])
-                continue
-            sweep_bytes += 8.0 * c * (steps - 1) * (2 * n + (n - nr))
-            if info["substep_path"] == 4:
-                # nested tiers: p^k stages of tier k per step, each reading
-                # r_k, E_m, E_{m-1} and writing E_{m+1} (or r_k+1) on R_k,
-                # plus z_n, z_{n-1} in and z_{n+1} out on R_1
-                pk, b, u = 1, 3.0 * nr, 0.0
-                for k, nrk in enumerate(info["n_r_tier"]):
-                    pk *= p
-                    b += 4.0 * pk * nrk
-                    u += (pk - pk // p) * nrk
-                sub_bytes += 8.0 * c * (steps - 1) * b
-                sub_updates += c * (steps - 1) * u
-                continue
-            if info["substep_path"] == 3:
-                sub_bytes += 8.0 * c * (steps - 1) * (4 * nr * (p - 1) + 2 * nr)
-            elif info["substep_path"] in (1, 2):
-                sub_bytes += 8.0 * c * (steps - 1) * 2 * nr
-            sub_flops += c * (steps - 1) * (p - 1) * (2.0 * info["ap_nnz"] + 7.0 * nr)
-            sub_updates += c * (steps - 1) * (p - 1) * nr
-    gbps = lambda b, ms: b / (ms * 1e-3) / 1e9 if ms else None  # noqa: E731
-    kernels = {"sweep": {"ms": sweep_ms, "launches": sum(p["sweep_launches"] for p in prof),
-                         "share_of_step": sweep_ms / step_ms if step_ms else None,
-                         "achieved_GBps": gbps(sweep_bytes, sweep_ms)},
-               "substep": {"ms": sub_ms, "launches": sum(p["sub_launches"] for p in prof),
-                           "path": ("hbm-resident nested tiers" if any(lv.info["substep_path"] == 4 for lv in levels)
-                                    else ("on-chip + hbm-resident" if any(lv.info["substep_path"] in (1, 2) and not f
-                                                                          for lv, f in zip(levels, fused_lv))
-                                          else "hbm-resident") if global_path else "on-chip"),
-                           "share_of_step": sub_ms / step_ms if step_ms else None,
-                           "fp64_TFLOPs": sub_flops / (sub_ms * 1e-3) / 1e12 if sub_ms and sub_flops else None,
-                           "substep_dof_updates_per_s": sub_updates / (sub_ms * 1e-3) if sub_ms else None,
-                           "achieved_GBps": gbps(sub_bytes, sub_ms)},
-               "r_update": {"ms": upd_ms, "launches": sum(p["upd_launches"] for p in prof),
-                            "share_of_step": upd_ms / step_ms if step_ms else None}}
-    if fused_ms:
-        kernels["fused_solve"] = {
-            "ms": fused_ms, "levels": [i for i, f in enumerate(fused_lv) if f],
-            "launches": sum(p["sub_launches"] for p, f in zip(prof, fused_lv) if f),
-            "share_of_step": fused_ms / step_ms if step_ms else None,
-            "bound": "on-chip (shared-memory wavefronts + latency; no per-step HBM traffic)",
-            "dof_updates_per_s": fused_updates / (fused_ms * 1e-3),
-            "fp64_TFLOPs": fused_flops / (fused_ms * 1e-3) / 1e12,
-            "hbm_equivalent_GBps": gbps(fused_bytes, fused_ms),
-            "note": "HBM-equivalent = SURVEY 8(d) algorithmic 24 B per DOF per global step over the kernel time"}
-    # DRAM traffic per launch: the measured/algorithmic ratio of the committed
-    # ncu capture (profiles/traffic.json) times this run's algorithmic bytes
-    # per launch
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            cap = json.load(f)
-    except OSError:
-        cap = {}
+def roofline_from_profile(levels, counts, prof, step_ms, peaks, fp64):
+    """Per-kernel-class device time from the profiled pass (CUDA events on
+    the level streams), the roofline of each class and of the dominant one
+    (largest share of the step).  Algorithmic bytes: 24 B per
+    DOF per solve per global step, split over the kernels that move them:
+      sweep          8 B x (z_n reads + z_{n-1} reads + z_{n+1} / g writes) of its rows
+      tiled step     8 B x 3 |R| (z_n, z_{n-1} in, z_{n+1} out of R)
+      fused solve    24 B x n (the whole step on chip: its HBM-equivalent rate)
+      HBM substeps   8 B x (4 |R| per substep + 2 |R|) (their own bytes, above 8(d))
+    FP64 flops (algorithmic): 2 per operator entry of every product plus 7 per
+    R row and substep (the recursion)."""
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    fp64_peak = fp64.get("fp64_tflops", 37.08)
+    traffic = load_json(os.path.join(ROOT, "profiles", "traffic.json"))
+    cls = {}
 
-    def traffic(key, alg_bytes, launches):
-        c = cap.get(key) or {}
-        if not launches or not c.get("algorithmic_bytes"):
-            return None, None
-        return c["dram_bytes"] / c["algorithmic_bytes"] * alg_bytes / launches, c.get("launch")
+    def add(name, ms, launches, bytes_=0.0, flops=0.0, updates=0.0, alg8d=0.0):
+        c = cls.setdefault(name, {"ms": 0.0, "launches": 0, "bytes": 0.0, "flops": 0.0, "updates": 0.0, "alg8d": 0.0})
+        c["ms"] += ms
+        c["launches"] += launches
+        c["bytes"] += bytes_
+        c["flops"] += flops
+        c["updates"] += updates
+        c["alg8d"] += alg8d
 
-    if global_path and sub_ms >= sweep_ms:
-        tiers = any(lv.info["substep_path"] == 4 for lv in levels)
-        key = "tier_stage" if tiers else "global_substep"
-        t, src = traffic(key, sub_bytes, kernels["substep"]["launches"])
-        roof = {"bound": "hbm", "kernel": key, "achieved": kernels["substep"]["achieved_GBps"],
-                "unit": "GB/s", "traffic": t, "traffic_capture": src,
-                "note": ("dominant kernel, HBM-resident substeps (algorithmic bytes); traffic per global step's "
-                         "group of substep launches")}
-    elif not sweep_ms and fused_ms:
-        # every level runs the fused on-chip solve (e.g. config 0): no HBM
-        # stream per step; report its SURVEY 8(d) HBM-equivalent rate
-        roof = {"bound": "hbm", "kernel": "fused_solve", "achieved": kernels["fused_solve"]["hbm_equivalent_GBps"],
-                "unit": "GB/s", "traffic": None, "traffic_capture": None,
-                "note": ("HBM-equivalent rate of the fused lattice solve (24 B per DOF per global step over its "
-                         "time); the state never leaves the SM, the kernel is bound on chip "
-                         "(kernels.fused_solve), so this fraction is not its limiter")}
+    step_bytes = 0.0
+    # a level's profile covers every solve of that level (the fine role of
+    # its own pairs and the coarse role of the next level's pairs)
+    for lvl, lv in enumerate(levels):
+        c = counts[lvl] + (counts[lvl + 1] if lvl + 1 < len(levels) else 0)
+        info = lv.info
+        n, nr, steps, p = info["n"], info["n_r"], info["n_steps"], info["p"]
+        path = info["substep_path"]
+        p_ = prof[lvl]
+        step_bytes += 24.0 * c * steps * n
+        flops = c * (steps - 1) * ((p - 1) * (2.0 * info["ap_nnz"] + 7.0 * nr) + 2.0 * info["nnz"])
+        if info.get("fused"):
+            add("fused_solve", p_["sub_ms"], p_["sub_launches"], 24.0 * c * steps * n, flops,
+                c * info["dof_updates_per_solve"], 24.0 * c * steps * n)
+            continue
+        if path == 5:  # tiled: the sweep covers the rows outside R, the tile kernel R
+            sweep_b = 24.0 * c * (steps - 1) * (n - nr)
+            sub_b = 24.0 * c * (steps - 1) * nr
+        else:
+            sweep_b = 8.0 * c * (steps - 1) * (2 * n + (n - nr))
+            sub_b = 0.0
+            if path == 3:
+                sub_b = 8.0 * c * (steps - 1) * (4 * nr * (p - 1) + 2 * nr)
+            elif path in (1, 2):
+                sub_b = 8.0 * c * (steps - 1) * 2 * nr
+        sub_u = c * (steps - 1) * (p - 1) * nr
+        if p_["sweep_ms"]:
+            add("sweep", p_["sweep_ms"], p_["sweep_launches"], sweep_b)
+        if path == 5:
+            add("tiled_step", p_["sub_ms"], p_["sub_launches"], sub_b, flops, sub_u, sub_b)
+        elif path == 3:
+            add("global_substep", p_["sub_ms"], p_["sub_launches"], sub_b, flops, sub_u)
+        elif path == 4:
+            add("tier_stage", p_["sub_ms"], p_["sub_launches"], 0.0, flops, sub_u)
+        elif path in (1, 2):
+            add("onchip_substep", p_["sub_ms"], p_["sub_launches"], sub_b, flops, sub_u)
+        if p_["upd_ms"]:
+            add("r_update", p_["upd_ms"], p_["upd_launches"])
+    kernels = {}
+    for name, c in cls.items():
+        k = {"ms": c["ms"], "launches": c["launches"], "share_of_step": c["ms"] / step_ms if step_ms else None}
+        if c["bytes"] and c["ms"]:
+            k["achieved_GBps"] = c["bytes"] / (c["ms"] * 1e-3) / 1e9
+            k["hbm_frac"] = k["achieved_GBps"] / hbm_peak
+        if c["flops"] and c["ms"]:
+            k["fp64_TFLOPs"] = c["flops"] / (c["ms"] * 1e-3) / 1e12
+            k["fp64_frac"] = k["fp64_TFLOPs"] / fp64_peak
+        if c["updates"] and c["ms"]:
+            k["dof_updates_per_s"] = c["updates"] / (c["ms"] * 1e-3)
+        tr = traffic.get(name) or {}
+        if tr.get("algorithmic_bytes") and c["launches"] and c["bytes"]:
+            k["traffic_per_launch"] = tr["dram_bytes"] / tr["algorithmic_bytes"] * c["bytes"] / c["launches"]
+            k["traffic_capture"] = tr.get("launch")
+        kernels[name] = k
+    dom = max(cls, key=lambda q: cls[q]["ms"])
+    k = kernels[dom]
+    if dom in ("fused_solve", "tiled_step", "onchip_substep"):
+        # on-chip kernels: bound by FP64 issue / latency, not HBM; the SURVEY
+        # 8(d) HBM-equivalent rate beside it
+        roof = {"bound": "fp64", "kernel": dom, "achieved": k.get("fp64_TFLOPs"), "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": k.get("fp64_frac"),
+                "peak_source": "measured (profiles/fp64_peak.json, tools/fp64_peak.cu)",
+                "hbm_equivalent": {"achieved": cls[dom]["alg8d"] / (cls[dom]["ms"] * 1e-3) / 1e9
+                                   if cls[dom]["alg8d"] else k.get("achieved_GBps"),
+                                   "peak": hbm_peak, "unit": "GB/s"},
+                "traffic": k.get("traffic_per_launch"), "share_of_step": k["share_of_step"]}
+        he = roof["hbm_equivalent"]
+        he["frac"] = he["achieved"] / hbm_peak if he["achieved"] else None
     else:
-        t, src = traffic("sweep", sweep_bytes, kernels["sweep"]["launches"])
-        roof = {"bound": "hbm", "kernel": "sweep", "achieved": kernels["sweep"]["achieved_GBps"], "unit": "GB/s",
-                "traffic": t, "traffic_capture": src,
-                "note": ("HBM roofline of the sweep kernel (algorithmic bytes, levels without the fused solve); "
-                         "the dominant kernels keep the state on chip and are shared-memory bound, see "
-                         "kernels.fused_solve / kernels.substep")}
-    return roof, kernels
-
-
-def kl_table_file(tmp):
-    from paper_2106_11117_b200 import configs, wavemc
-    kl = configs.KL_FIELD
-    table, _ = wavemc.kl_table(kl["cells"][0], kl["cells"][1], kl["sigma"], kl["corr_len"], kl["modes"])
-    path = os.path.join(tmp, "kl.txt")
-    with open(path, "w") as f:
-        f.write(f"{table.shape[0]} {table.shape[1]}\n")
-        f.write("\n".join(repr(float(v)) for v in table.ravel()) + "\n")
-    return path, {"kl-table": path, "cells-x": kl["cells"][0], "cells-y": kl["cells"][1]}
+        roof = {"bound": "hbm", "kernel": dom, "achieved": k.get("achieved_GBps"), "peak": hbm_peak, "unit": "GB/s",
+                "frac": k.get("hbm_frac"), "traffic": k.get("traffic_per_launch"),
+                "share_of_step": k["share_of_step"]}
+    roof["peak_hbm_source"] = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
+    roof["secondary"] = {name: {q: v for q, v in kk.items() if q in ("share_of_step", "achieved_GBps", "hbm_frac",
+                                                                     "fp64_TFLOPs", "fp64_frac")}
+                         for name, kk in kernels.items() if name != dom}
+    return roof, kernels, step_bytes
 
 
 def adaptive_arm(args, world, rank, local):
@@ -615,23 +717,20 @@ def adaptive_arm(args, world, rank, local):
             return 0
         import oracle_py
         threads = os.cpu_count() or 1
-        tmp = tempfile.mkdtemp(prefix="wmc_c4_")
-        _, klargs = kl_table_file(tmp)
-        specs = []
-        for l, d in enumerate(defs):
-            p = os.path.join(tmp, f"l{l}.mesh")
-            configs.build_mesh(d).dump(p)
-            specs.append((p, d.dt, d.substeps))
-        runs = [oracle_py.RefDriver().adaptive(specs, eps, threads=threads, **klargs)
+        inp = dump_inputs(4, kl=True)
+        specs = [(lv["mesh"], lv["dt"], lv["p"]) for lv in inp["levels"]]
+        runs = [oracle_py.RefDriver().adaptive(specs, eps, threads=threads, **inp["kl"])
                 for _ in range(args.warmup + args.steps)][args.warmup:]
-        shutil.rmtree(tmp, ignore_errors=True)
+        shutil.rmtree(inp["dir"], ignore_errors=True)
         sec = sum(r["seconds"] for r in runs) / len(runs)
+        ci = cpu_info()
         line = {"impl": "reference", "metric": "MLMC time-to-RMSE", "value": sec, "unit": "s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (counter-based RNG, Box-Muller KL weights, seed 0)",
                 "config": {"workload": f"BASELINE config 4: adaptive MLMC to RMSE {eps}, log-normal KL", "eps": eps},
                 "cpu_baseline": {"value": sec, "unit": "s", "cores": threads, "kind": "reference",
+                                 "cpu_model": ci["cpu_model"],
                                  "sample": f"full adaptive run, reference run_mlmc, {threads} threads"},
                 "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 "N_l": [lv["N"] for lv in runs[0]["levels"]], "estimate": runs[0]["estimate"]}
@@ -672,6 +771,8 @@ def adaptive_arm(args, world, rank, local):
 def main():
     args = parse()
     world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.config == 4:
         return adaptive_arm(args, world, rank, local)
     if args.impl == "reference":

@@ -551,8 +551,11 @@ void build_device_level(wmc_level& L) {
         // the temporally blocked step when the level has a refined box (R in
         // tiles, every substep on chip); WMC_TILED=0 keeps the HBM-resident
         // substeps (A/B), WMC_SUBSTEP_PATH=global as well
+        // (automatic only where R does not fit one SM: small boxes take the
+        // HBM/L2-resident substeps, whose halo-free layout wins there)
         const char* tiled_env = std::getenv("WMC_TILED");
-        if (fp != "global" && !(tiled_env && std::atoi(tiled_env) == 0) && !L.d_cell_ix) {
+        if ((fp == "tiled" || (fp.empty() && !onchip_fits)) && !(tiled_env && std::atoi(tiled_env) == 0) &&
+            !L.d_cell_ix) {
             wmc::TilePlan plan = wmc::plan_tiles(t, wmc::kTileWz, wmc::kTileHz, wmc::kTileK);
             if (std::getenv("WMC_DEBUG_TILES"))
                 std::fprintf(stderr, "tile plan: ok=%d layout=%s reason=%s tiles=%d max_gen=%d max_app=%d "

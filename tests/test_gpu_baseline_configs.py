@@ -186,6 +186,7 @@ def test_tiled_step_on_config1_levels(lvl, monkeypatch):
     monkeypatch.delenv("WMC_SUBSTEP_PATH")
     monkeypatch.delenv("WMC_TILED")
     assert tiled.info["substep_path"] == 5 and other.info["substep_path"] == 3
+    assert configs.build_level(d).info["substep_path"] != 5  # small boxes keep the halo-free paths
     _, a, _ = wavemc.eval_pairs(tiled, None, 0, lvl, 0, 96)
     _, b, _ = wavemc.eval_pairs(other, None, 0, lvl, 0, 96)
     assert per_sample_rel(a, b) < QOI_RTOL
