@@ -896,8 +896,8 @@ void build_device_level(wmc_level& L) {
         // fused lattice solve: lattice levels whose z_n (and z_{n-1} when it
         // fits) stay on chip next to the substep state; WMC_FUSED=0 disables
         const char* fz = std::getenv("WMC_FUSED");
-        if (L.path == SubPath::Lattice && t.tiers == 1 && (t.lat_threads == 512 || t.lat_threads == 128) &&
-            t.lat_k == 8 && !(fz && std::atoi(fz) == 0)) {
+        if (L.path == SubPath::Lattice && t.tiers == 1 && t.lat_threads == 512 && t.lat_k == 8 &&
+            !(fz && std::atoi(fz) == 0)) {
             wmc::LatSolveArgs probe{};
             probe.lat.n_r = t.n_r;
             probe.lat.p = t.p;
@@ -926,8 +926,7 @@ void build_device_level(wmc_level& L) {
             const char* ff = std::getenv("WMC_FUSED_FORCE");  // tuning knob: ignore the rows-outside-R limit
             const bool force = ff && std::atoi(ff) != 0;
             if (bytes <= cap &&
-                (force || L.fused_tmem || L.fused_zp_global || t.n - t.n_r <= 2 * t.lat_threads) &&
-                (t.lat_threads == 512 || L.fused_tmem == 2))  // the 128-thread variant: TMEM form 2 only
+                (force || L.fused_tmem || L.fused_zp_global || t.n - t.n_r <= 2 * t.lat_threads))
                 L.fused_smem = bytes;
         }
     }
@@ -1475,7 +1474,7 @@ void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     for (int len : t.strip_len)
         if (len < t.lat_k - 1) a.strips_k_or_k1 = 0;
     a.ns_rows = L.d_ns_rows;
-    a.n_ns = (L.fused_tmem == 2 && (t.lat_threads == 512 || t.lat_threads == 128)) ? L.n_ns : 0;
+    a.n_ns = (L.fused_tmem == 2 && t.lat_threads == 512) ? L.n_ns : 0;
     a.rem_ptr = L.d_rem_ptr;
     a.rem_col = L.d_rem_col;
     a.rem_cell = L.d_rem_cell;
@@ -1488,10 +1487,7 @@ void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     a.q = ws.q;
     a.fail = ws.fail;
     if (L.profile) mark(L, L.ev_sub, stream);
-    // one sample per CTA, as many CTAs as fit the SMs at once (four per SM for
-    // 128-thread small-box variants)
-    const int per_sm = t.lat_threads == 128 ? wmc::lattice_solve_ctas_per_sm(a) : 1;
-    const int e = wmc::launch_lattice_solve(a, std::max(1, std::min(count, L.n_sms * per_sm)), stream);
+    const int e = wmc::launch_lattice_solve(a, std::max(1, std::min(count, L.n_sms)), stream);
     ++g_launches;
     if (e != 0) check(static_cast<cudaError_t>(e), "fused lattice solve launch");
     if (L.profile) mark(L, L.ev_sub, stream);

@@ -65,8 +65,7 @@ int LevelSpec::cell_row(double y) const {
 namespace {
 
 // lattice substep kernel variants: (threads, max rows per thread)
-// (128 x 8 first: small boxes such as config 0's run four CTAs per SM)
-constexpr int kLatticeVariants[4][2] = {{128, 8}, {512, 8}, {768, 6}, {1024, 4}};
+constexpr int kLatticeVariants[3][2] = {{512, 8}, {768, 6}, {1024, 4}};
 
 using StiffMap = std::map<std::tuple<int, int, int>, double>;
 

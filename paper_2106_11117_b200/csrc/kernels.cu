@@ -2055,7 +2055,7 @@ __device__ __forceinline__ double gen_full_row_tm(const LatSolveArgs& A, const d
 // PK: every strip holds K or K - 1 rows (host-checked), so the rare path
 // for shorter strips is compiled out.
 template <int T, int K, int G, bool TM, bool VT = TM, bool PK = false>
-__global__ void __launch_bounds__(T, (T <= 128 ? 4 : 1)) lattice_solve_kernel(LatSolveArgs A) {
+__global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
     static_assert(!TM || (T % 128 == 0 && T <= 512 && 20 * G + 4 * K <= 128), "TMEM columns per thread");
     extern __shared__ __align__(16) double sd[];
     const LatArgs& a = A.lat;
@@ -2800,7 +2800,6 @@ int launch_lattice_substeps(const LatArgs& a, int grid, void* stream) {
     if (a.threads == 1024 && a.strip_k == 4) return launch_lat<1024, 4, 1>(a, grid, st);
     if (a.threads == 768 && a.strip_k == 6) return launch_lat<768, 6, 2>(a, grid, st);
     if (a.threads == 512 && a.strip_k == 8) return launch_lat<512, 8, 2>(a, grid, st);
-    if (a.threads == 128 && a.strip_k == 8) return launch_lat<128, 8, 2>(a, grid, st);
     return static_cast<int>(cudaErrorInvalidValue);
 }
 
@@ -2913,25 +2912,8 @@ static int launch_lat_solve(const LatSolveArgs& a, int grid, cudaStream_t st) {
     return static_cast<int>(cudaGetLastError());
 }
 
-int lattice_solve_ctas_per_sm(const LatSolveArgs& a) {
-    int blocks = 0;
-    const void* k = a.lat.threads == 128
-                        ? reinterpret_cast<const void*>(lattice_solve_kernel<128, 8, 2, true, false, true>)
-                        : reinterpret_cast<const void*>(lattice_solve_kernel<512, 8, 2, true, false, true>);
-    int device = 0;
-    cudaGetDevice(&device);
-    set_max_dynamic_smem(k, lattice_solve_max_smem(device));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, a.lat.threads, lattice_solve_smem_bytes(a)) !=
-        cudaSuccess)
-        return 1;
-    return blocks > 0 ? blocks : 1;
-}
-
 int launch_lattice_solve(const LatSolveArgs& a, int grid, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (a.lat.threads == 128 && a.lat.strip_k == 8 && a.tmem == 2)  // small boxes: four CTAs per SM
-        return a.strips_k_or_k1 ? launch_lat_solve<128, 8, 2, true, false, true>(a, grid, st)
-                                : launch_lat_solve<128, 8, 2, true, false>(a, grid, st);
     if (a.lat.threads == 512 && a.lat.strip_k == 8)
         return a.tmem == 2 ? (a.strips_k_or_k1 ? launch_lat_solve<512, 8, 2, true, false, true>(a, grid, st)
                                                : launch_lat_solve<512, 8, 2, true, false>(a, grid, st))

@@ -331,7 +331,6 @@ struct LatSolveArgs {
 int lattice_solve_smem_bytes(const LatSolveArgs& a);
 int lattice_solve_max_smem(int device);
 int launch_lattice_solve(const LatSolveArgs& a, int grid, void* stream);  // returns cudaError_t
-int lattice_solve_ctas_per_sm(const LatSolveArgs& a);  // resident CTAs per SM of the variant a selects
 int small_max_smem(int device);  // largest dynamic shared memory the kernel can take
 int launch_small_solve(const SmallArgs& a, int grid, void* stream);  // returns cudaError_t
 
