@@ -2565,6 +2565,27 @@ __global__ void qoi_kernel(QoIArgs a) {
     a.q[k * S + s] = a.fail[s] == INT_MAX ? acc : __longlong_as_double(0x7ff8000000000000LL);
 }
 
+// K3, sample-major state (tiled levels): one block per (sample, output), the
+// box entries strided over the threads (coalesced along one sample's rows),
+// a fixed-order tree over the partial sums (deterministic)
+__global__ void __launch_bounds__(256) qoi_sm_kernel(QoIArgs a) {
+    __shared__ double part[256];
+    const int s = blockIdx.x, k = blockIdx.y;
+    const double* z = a.z + static_cast<std::size_t>(s) * a.n;
+    double acc = 0.0;
+    for (int t = __ldg(a.ptr + k) + threadIdx.x; t < __ldg(a.ptr + k + 1); t += 256)
+        acc += __ldg(a.w + t) * (z[__ldg(a.dof + t)] / __ldg(a.sqrt_mass + t));
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        a.q[static_cast<std::size_t>(k) * a.S + s] =
+            a.fail[s] == INT_MAX ? part[0] : __longlong_as_double(0x7ff8000000000000LL);
+}
+
 __global__ void fill_int_kernel(int* p, int value, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = value;
@@ -2831,6 +2852,10 @@ void launch_r_update(const RUpdateArgs& a, void* stream) {
 }
 
 void launch_qoi(const QoIArgs& a, void* stream) {
+    if (a.sample_major && !a.nsteps) {
+        qoi_sm_kernel<<<dim3(a.count, a.nq), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+        return;
+    }
     qoi_kernel<<<dim3((a.count + 127) / 128, a.nq), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
 }
 
