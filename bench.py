@@ -757,7 +757,7 @@ def adaptive_arm(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based RNG, Box-Muller KL weights, seed 0)",
             "config": {"workload": f"BASELINE config 4: adaptive MLMC to RMSE {eps}, log-normal KL (sigma 0.5, "
-                                   "l 0.1, 64 modes, 16x16 cells), config-1 geometry", "eps": eps},
+                                   "l 0.1, 64 modes, 32x32 cells), config-1 geometry", "eps": eps},
             "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 16 * sum(lv["n_samples"] for lv in res.levels)},
             "gpu_launches": (wavemc.launch_count() - launches0) // max(1, args.steps), "clocks": clocks.summary(),

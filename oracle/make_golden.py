@@ -1,6 +1,6 @@
 """Generate tests/golden/*.json from the UNMODIFIED reference library
 (oracle/_ref/wavemc_ref_driver) -- run in the build container, where
-/root/reference exists:  python oracle/make_golden.py [--only-round2 | --only-config1-full | --only-mesh1d | --only-config2 | --only-cfl | --only-experiments | --only-artifacts | --only-channel]
+/root/reference exists:  python oracle/make_golden.py [--only-round2 | --only-config1-full | --only-mesh1d | --only-config4 | --only-config2 | --only-cfl | --only-experiments | --only-artifacts | --only-channel]
 
 The meshes come from the shared problem definition (the product's host mesh
 builder), written in the reference fixture format (src/mesh_io.cpp:1-9) and
@@ -25,6 +25,7 @@ from oracle_py import RefDriver, build  # noqa: E402
 from paper_2106_11117_b200 import configs  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+CONFIG4_TIGHT_EPS = 1.5e-4
 
 
 def dump(name, obj):
@@ -280,6 +281,9 @@ def main():
     if "--only-config1-full" in sys.argv:
         config1_full(ref, tmp)
         return
+    if "--only-config4" in sys.argv:
+        config4(ref, tmp)
+        return
     if "--only-mesh1d" in sys.argv:
         hierarchies_1d(ref)
         return
@@ -356,10 +360,26 @@ def main():
                               for lv, d in zip(pairs["levels"], c1)]
     dump("config1_adaptive.json", adaptive)
 
-    # config 4: log-normal KL coefficient on a 16 x 16 cell grid (new field,
-    # our shared definition), solved by the reference: coupled pairs and the
-    # reference run_mlmc at the BASELINE RMSE target
+    config4(ref, tmp, specs, adaptive["model_cost"])
+    config2_reductions(ref, tmp)
+    cfl_samples(ref, tmp)
+    experiments(ref)
+    print("golden fixtures written to", GOLDEN)
+
+
+def config4(ref, tmp, specs=None, model_cost=None):
+    """Config 4: log-normal KL coefficient on the KL_FIELD cell grid (new
+    field, our shared definition), solved by the reference: coupled pairs and
+    the reference run_mlmc at the BASELINE RMSE target."""
     from paper_2106_11117_b200 import wavemc
+    if specs is None:
+        c1 = configs.config1()
+        specs = []
+        for l, d in enumerate(c1):
+            p = os.path.join(tmp, f"config1_l{l}.mesh")
+            configs.build_mesh(d).dump(p)
+            specs.append((p, d.dt, d.substeps))
+        model_cost = json.load(open(os.path.join(GOLDEN, "config1_adaptive.json")))["model_cost"]
     kl = configs.KL_FIELD
     table, lam = wavemc.kl_table(kl["cells"][0], kl["cells"][1], kl["sigma"], kl["corr_len"], kl["modes"])
     tpath = os.path.join(tmp, "kl.txt")
@@ -373,12 +393,13 @@ def main():
     dump("config4_pairs.json", kl_pairs)
     kl_adaptive = ref.adaptive(specs, configs.CONFIG4_EPS, **klargs)
     kl_adaptive["eps"] = configs.CONFIG4_EPS
-    kl_adaptive["model_cost"] = adaptive["model_cost"]
+    kl_adaptive["model_cost"] = model_cost
+    kl_adaptive["cells"] = list(kl["cells"])
+    # a tighter target, so the driver adds samples and levels beyond the warm-up
+    tight = ref.adaptive(specs, CONFIG4_TIGHT_EPS, **klargs)
+    tight["eps"] = CONFIG4_TIGHT_EPS
+    kl_adaptive["tight"] = tight
     dump("config4_adaptive.json", kl_adaptive)
-    config2_reductions(ref, tmp)
-    cfl_samples(ref, tmp)
-    experiments(ref)
-    print("golden fixtures written to", GOLDEN)
 
 
 if __name__ == "__main__":

@@ -104,8 +104,9 @@ def config4() -> list[LevelDef]:
 
 # config 4 coefficient: c = exp(g), g = 0.5 * truncated KL (64 modes) of the
 # separable exponential covariance exp(-|dx|/0.1 - |dy|/0.1), N(0,1) weights,
-# sampled at the centres of a 16 x 16 cell grid (cell lines on mesh lines)
-KL_FIELD = {"cells": (16, 16), "sigma": 0.5, "corr_len": 0.1, "modes": 64}
+# sampled at the centres of a 32 x 32 cell grid (h = 1/32: a third of the
+# correlation length; cell lines on mesh lines of every level)
+KL_FIELD = {"cells": (32, 32), "sigma": 0.5, "corr_len": 0.1, "modes": 64}
 CONFIG4_EPS = 1e-3
 
 CONFIG0_COUNT = 1024

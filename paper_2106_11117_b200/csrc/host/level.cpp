@@ -232,7 +232,7 @@ static Geometry geometry_2d(const TriMesh& mesh, const LevelSpec& spec, LevelTab
     if (spec.cells_x < 1 || spec.cells_y < 1) throw std::invalid_argument("level: coefficient grid");
     if (spec.final_time <= 0.0 || spec.dt <= 0.0) throw std::invalid_argument("level: T and dt must be positive");
     if (spec.substeps < 1) throw std::invalid_argument("level: substeps >= 1");
-    if (spec.cells_x * spec.cells_y > 511) throw std::invalid_argument("level: at most 511 coefficient cells");
+    if (spec.cells_x * spec.cells_y > 32767) throw std::invalid_argument("level: at most 32767 coefficient cells");
 
     const int nv = mesh.n_vertices();
     const int nt = mesh.n_triangles();
