@@ -370,11 +370,32 @@ def b200_arm(args, world, rank, local):
 
     from paper_2106_11117_b200 import configs, shard, wavemc
 
+    # more ranks than devices (checking the rank path on a one-GPU box): ranks
+    # share devices and the collectives go over gloo on host copies; the line
+    # says so ("ranks_share_devices") -- not a scaling measurement
+    ndev = max(1, torch.cuda.device_count())
+    shared = world > ndev
+    local = local % ndev
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def allreduce(t, op=None):
+        if dist is None:
+            return t
+        kw = {} if op is None else {"op": op}
+        if shared:
+            h = t.cpu()
+            dist.all_reduce(h, **kw)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, **kw)
+        return t
     lf = args.integrator == "lf"
     defs, counts_total, label, cpu_T = workload(args.config, args.integrator)
     if args.scale is None:
@@ -418,7 +439,7 @@ def b200_arm(args, world, rank, local):
             e.record(strs[l])
             main.wait_event(e)
         if dist is not None:
-            dist.all_reduce(d_mom)
+            allreduce(d_mom)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -448,7 +469,7 @@ def b200_arm(args, world, rank, local):
     ms = start.elapsed_time(end) / args.steps
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce(t, dist.ReduceOp.MAX)
         ms = float(t.item())
     value = total_updates / (ms * 1e-3)
     mom = d_mom.cpu().tolist()
@@ -458,7 +479,7 @@ def b200_arm(args, world, rank, local):
     # steps as the device timing
     def step_e2e():
         stats = wavemc.run_mlmc_fixed(levels, counts, 0, first)
-        return shard.allreduce_level_sums(stats, device=dev)
+        return shard.allreduce_level_sums(stats, device=None if shared else dev)
 
     step_e2e()
     barrier()
@@ -472,7 +493,7 @@ def b200_arm(args, world, rank, local):
     e2e_ms = t0.elapsed_time(t1) / args.steps
     if dist is not None:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce(t, dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     d2h = sum(16 * c + 4 * c * (2 if l else 1) for l, c in enumerate(counts))
 
@@ -569,6 +590,7 @@ def b200_arm(args, world, rank, local):
                     "note": "inputs are seeds (per-sample coefficients drawn on the device); per-sample dQ, Q and "
                             "fail flags copied D2H and folded on the host every step"},
             "gpu_launches": launches, "clocks": clocks.summary(),
+            "ranks_share_devices": shared,
             "moments": [{"level": l, "sum_dq": mom[4 * l], "sum_dq2": mom[4 * l + 1], "sum_q": mom[4 * l + 2],
                          "sum_q2": mom[4 * l + 3]} for l in range(len(levels))],
             "variance": [s["variance"] for s in stats]}
