@@ -639,8 +639,10 @@ def roofline_from_profile(levels, counts, prof, step_ms, peaks, fp64):
     traffic = load_json(os.path.join(ROOT, "profiles", "traffic.json"))
     cls = {}
 
-    def add(name, ms, launches, bytes_=0.0, flops=0.0, updates=0.0, alg8d=0.0):
-        c = cls.setdefault(name, {"ms": 0.0, "launches": 0, "bytes": 0.0, "flops": 0.0, "updates": 0.0, "alg8d": 0.0})
+    def add(name, ms, launches, bytes_=0.0, flops=0.0, updates=0.0, alg8d=0.0, solves=0):
+        c = cls.setdefault(name, {"ms": 0.0, "launches": 0, "bytes": 0.0, "flops": 0.0, "updates": 0.0, "alg8d": 0.0,
+                                  "solves": 0})
+        c["solves"] += solves
         c["ms"] += ms
         c["launches"] += launches
         c["bytes"] += bytes_
@@ -661,7 +663,7 @@ def roofline_from_profile(levels, counts, prof, step_ms, peaks, fp64):
         flops = c * (steps - 1) * ((p - 1) * (2.0 * info["ap_nnz"] + 7.0 * nr) + 2.0 * info["nnz"])
         if info.get("fused"):
             add("fused_solve", p_["sub_ms"], p_["sub_launches"], 24.0 * c * steps * n, flops,
-                c * info["dof_updates_per_solve"], 24.0 * c * steps * n)
+                c * info["dof_updates_per_solve"], 24.0 * c * steps * n, solves=c)
             continue
         if path == 5:  # tiled: the sweep covers the rows outside R, the tile kernel R
             sweep_b = 24.0 * c * (steps - 1) * (n - nr)
@@ -698,7 +700,10 @@ def roofline_from_profile(levels, counts, prof, step_ms, peaks, fp64):
         if c["updates"] and c["ms"]:
             k["dof_updates_per_s"] = c["updates"] / (c["ms"] * 1e-3)
         tr = traffic.get(name) or {}
-        if tr.get("algorithmic_bytes") and c["launches"] and c["bytes"]:
+        if tr.get("dram_bytes_per_solve") and c["launches"] and c.get("solves"):
+            k["traffic_per_launch"] = tr["dram_bytes_per_solve"] * c["solves"] / c["launches"]
+            k["traffic_capture"] = tr.get("launch")
+        elif tr.get("algorithmic_bytes") and c["launches"] and c["bytes"]:
             k["traffic_per_launch"] = tr["dram_bytes"] / tr["algorithmic_bytes"] * c["bytes"] / c["launches"]
             k["traffic_capture"] = tr.get("launch")
         kernels[name] = k
