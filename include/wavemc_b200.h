@@ -205,6 +205,20 @@ int wmc_level_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level_i
 int wmc_level_get_info(const wmc_level* level, wmc_level_info* info);
 void wmc_level_destroy(wmc_level* level);
 
+/* Host-only: the temporally blocked step's plan for a box level (spatial
+ * tiles around the box ring, streamed slabs inside), no device work.
+ * ok = 0 with `reason` when the level does not take the tiled step. */
+typedef struct {
+    int ok;
+    int n_tiles, n_slabs;
+    int max_gen;             /* generic rows per tile */
+    double work_factor;      /* region positions per box node */
+    double streamed_frac;    /* box nodes owned by slabs / box nodes */
+    char layout[32];
+    char reason[256];
+} wmc_tile_plan_info;
+int wmc_tile_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, int stream, wmc_tile_plan_info* info);
+
 typedef struct {
     long matvec_full, matvec_fine, matvec_coarse;  /* reference CostRecord, mlmc.hpp:25-32 */
     long weighted_work;

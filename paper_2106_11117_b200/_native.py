@@ -60,6 +60,12 @@ class LevelInfo(C.Structure):
                 ("n_structured", C.c_long), ("nq", C.c_int), ("fused", C.c_int)]
 
 
+class TilePlanInfo(C.Structure):
+    _fields_ = [("ok", C.c_int), ("n_tiles", C.c_int), ("n_slabs", C.c_int), ("max_gen", C.c_int),
+                ("work_factor", C.c_double), ("streamed_frac", C.c_double), ("layout", C.c_char * 32),
+                ("reason", C.c_char * 256)]
+
+
 class Cost(C.Structure):
     _fields_ = [("matvec_full", C.c_long), ("matvec_fine", C.c_long), ("matvec_coarse", C.c_long),
                 ("weighted_work", C.c_long), ("dof_updates", C.c_double)]
@@ -112,6 +118,7 @@ SIGNATURES = [
     ("wmc_channel_plan", C.c_int, [_VP, P(ExperimentDesc), C.c_int, P(LevelInfo)]),
     ("wmc_experiment_model_cost", C.c_double, [P(ExperimentDesc), C.c_int]),
     ("wmc_level_plan", C.c_int, [_VP, P(LevelDesc), P(LevelInfo)]),
+    ("wmc_tile_plan", C.c_int, [_VP, P(LevelDesc), C.c_int, P(TilePlanInfo)]),
     ("wmc_level_get_info", C.c_int, [_VP, P(LevelInfo)]),
     ("wmc_level_destroy", None, [_VP]),
     ("wmc_eval_pairs", C.c_int, [_VP, _VP, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, _DP, _DP, P(Cost),

@@ -163,6 +163,8 @@ struct wmc_level {
     std::vector<void*> tile_bufs;
     int tile_smem = 0;
     double tile_work = 0.0;        // region positions per box node (diagnostics)
+    wmc::StreamArgs slabs{};       // streamed interior of the tiled step (n_slabs = 0: none)
+    int stream_smem = 0;
     // nested tiers: A P_k on R_k per tier, substep constants
     std::vector<int*> d_tier_ptr, d_tier_ent;
     std::vector<double*> d_tier_a0;
@@ -557,11 +559,16 @@ void build_device_level(wmc_level& L) {
         const char* tiled_env = std::getenv("WMC_TILED");
         if ((fp == "tiled" || (fp.empty() && !onchip_fits)) && !(tiled_env && std::atoi(tiled_env) == 0) &&
             !L.d_cell_ix) {
-            wmc::TilePlan plan = wmc::plan_tiles(t, wmc::kTileWz, wmc::kTileHz, wmc::kTileK);
+            // WMC_STREAM=0: tiles only (no streamed interior)
+            const char* stream_env = std::getenv("WMC_STREAM");
+            const bool stream = !(stream_env && std::atoi(stream_env) == 0);
+            wmc::TilePlan plan = wmc::plan_tiles(t, wmc::kTileWz, wmc::kTileHz, wmc::kTileK,
+                                                 stream ? wmc::kStreamThreads : 0, wmc::kStreamMaxP);
             if (std::getenv("WMC_DEBUG_TILES"))
-                std::fprintf(stderr, "tile plan: ok=%d layout=%s reason=%s tiles=%d max_gen=%d max_app=%d "
-                             "max_ent=%d work=%.3f\n", plan.ok, plan.layout.c_str(), plan.reason.c_str(),
-                             plan.n_tiles, plan.max_gen, plan.max_app, plan.max_ent, plan.work_factor);
+                std::fprintf(stderr, "tile plan: ok=%d layout=%s reason=%s tiles=%d slabs=%d max_gen=%d max_app=%d "
+                             "max_ent=%d work=%.3f notes=%s\n", plan.ok, plan.layout.c_str(), plan.reason.c_str(),
+                             plan.n_tiles, plan.n_slabs, plan.max_gen, plan.max_app, plan.max_ent, plan.work_factor,
+                             plan.notes.c_str());
             if (plan.ok) {
                 auto up = [&](const auto& v) {
                     auto* p = upload(v);
@@ -618,6 +625,35 @@ void build_device_level(wmc_level& L) {
                 a.cm = up(t.cm);
                 L.tile_smem = wmc::tile_smem_bytes(a);
                 L.tile_work = plan.work_factor;
+                if (plan.n_slabs > 0) {
+                    wmc::StreamArgs& sa = L.slabs;
+                    std::vector<int4> sg(plan.n_slabs), so(plan.n_slabs);
+                    for (int q = 0; q < plan.n_slabs; ++q) {
+                        sg[q] = make_int4(plan.slab[4 * q], plan.slab[4 * q + 1], plan.slab[4 * q + 2],
+                                          plan.slab[4 * q + 3]);
+                        so[q] = make_int4(plan.slab_own[4 * q], plan.slab_own[4 * q + 1], plan.slab_own[4 * q + 2],
+                                          plan.slab_own[4 * q + 3]);
+                    }
+                    sa.p = t.p;
+                    sa.m = t.lat_m;
+                    sa.cells_x = L.spec.cells_x;
+                    sa.n_slabs = plan.n_slabs;
+                    sa.max_nx = plan.max_nx;
+                    sa.inv_h = a.inv_h;
+                    sa.h = a.h;
+                    sa.inv_h2 = a.inv_h2;
+                    sa.c0 = t.c0;
+                    for (int q = 0; q + 1 < t.p; ++q) {
+                        sa.opb[q] = 1.0 + t.beta[q];
+                        sa.beta[q] = t.beta[q];
+                        sa.cm[q] = t.cm[q];
+                    }
+                    sa.slab = up(sg);
+                    sa.slab_own = up(so);
+                    sa.cellx = a.cellx;
+                    sa.celly = a.celly;
+                    L.stream_smem = wmc::stream_smem_bytes(sa);
+                }
                 int optin = 0;
                 cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, L.device);
                 if (L.tile_smem + 64 <= optin) L.path = SubPath::Tiled;
@@ -1297,6 +1333,22 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
             const int e = wmc::launch_tile_step(ta, static_cast<int>(std::min<long>(items, L.n_sms)), stream);
             if (e != 0) check(static_cast<cudaError_t>(e), "tiled step launch");
             ++g_launches;
+            if (L.slabs.n_slabs > 0) {
+                wmc::StreamArgs sa = L.slabs;
+                sa.S = S;
+                sa.count = count;
+                sa.n = t.n;
+                sa.cells = cells;
+                sa.zc = cur;
+                sa.zp = prev;
+                sa.fail = ws.fail;
+                sa.step = static_cast<int>(s + 1);
+                const long sitems = static_cast<long>(sa.n_slabs) * count;
+                const int es = wmc::launch_stream_step(sa, static_cast<int>(std::min<long>(sitems, 2L * L.n_sms)),
+                                                       stream);
+                if (es != 0) check(static_cast<cudaError_t>(es), "streamed step launch");
+                ++g_launches;
+            }
             if (L.profile) mark(L, L.ev_sub, stream);
         } else if (tiers) {
             if (L.profile) mark(L, L.ev_sub, stream);
@@ -2517,6 +2569,29 @@ int wmc_level_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, wmc_level_i
         if (!mesh || !desc || !info) throw ConfigError("wmc_level_plan: NULL argument");
         const wmc::LevelTables t = wmc::build_level_tables(mesh->mesh, spec_from_desc(desc));
         fill_info(t, 0, t.lattice, info);
+    });
+}
+
+int wmc_tile_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, int stream, wmc_tile_plan_info* info) {
+    return guarded([&] {
+        if (!mesh || !desc || !info) throw ConfigError("wmc_tile_plan: NULL argument");
+        const wmc::LevelTables t = wmc::build_level_tables(mesh->mesh, spec_from_desc(desc));
+        const wmc::TilePlan plan = wmc::plan_tiles(t, wmc::kTileWz, wmc::kTileHz, wmc::kTileK,
+                                                   stream ? wmc::kStreamThreads : 0, wmc::kStreamMaxP);
+        *info = wmc_tile_plan_info{};
+        info->ok = plan.ok ? 1 : 0;
+        info->n_tiles = plan.n_tiles;
+        info->n_slabs = plan.n_slabs;
+        info->max_gen = plan.max_gen;
+        info->work_factor = plan.work_factor;
+        long streamed = 0;
+        for (int q = 0; q < plan.n_slabs; ++q)
+            streamed += static_cast<long>(plan.slab_own[4 * q + 1] - plan.slab_own[4 * q]) *
+                        (plan.slab_own[4 * q + 3] - plan.slab_own[4 * q + 2]);
+        const double box = t.box ? static_cast<double>(t.lat_m + 1) * (t.lat_m + 1) : 1.0;
+        info->streamed_frac = static_cast<double>(streamed) / box;
+        std::snprintf(info->layout, sizeof(info->layout), "%s", plan.layout.c_str());
+        std::snprintf(info->reason, sizeof(info->reason), "%s", plan.ok ? plan.notes.c_str() : plan.reason.c_str());
     });
 }
 

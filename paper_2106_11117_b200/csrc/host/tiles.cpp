@@ -18,6 +18,10 @@ struct TileDesc {
     int oi0, oi1, oj0, oj1;
 };
 
+struct Rect {
+    int i0 = 0, i1 = 0, j0 = 0, j1 = 0;  // [i0, i1) x [j0, j1), empty when i0 == i1
+};
+
 // Regular grid of wide tiles, halo p (columns) / p rounded up to k (rows).
 std::vector<TileDesc> layout_grid(int W, int p, int k, int jres, int wz, int hz) {
     std::vector<TileDesc> out;
@@ -48,7 +52,8 @@ std::vector<TileDesc> layout_grid(int W, int p, int k, int jres, int wz, int hz)
 // right bands (halo 2 p along the edge), wide tiles with halo 2 p in the
 // bottom and top bands, the regular grid inside.  Row origins stay = jres
 // (mod k).
-std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz, int he) {
+// With `inner` the interior grid is left out and its rectangle returned.
+std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz, int he, Rect* inner = nullptr) {
     std::vector<TileDesc> out;
     auto align_down = [&](int j) {  // largest value <= j that is = jres (mod k)
         int r = ((j - jres) % k + k) % k;
@@ -84,16 +89,27 @@ std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz
     // rows a whole number of ih-row bands, each starting = jres (mod k)
     const int band_max = hz - hyi;  // the region must reach hyi rows past the band
     int bb = -1, bt = -1, n_int = 0;
-    for (n_int = (W - 2) / ih; n_int >= 0 && bb < 0; --n_int)
-        for (int b = align_down(band_max); b >= 1; b -= k) {
-            const int t = W - b - n_int * ih;
-            if (b % k == ((jres % k) + k) % k && t >= 1 && t <= band_max) {
-                bb = b;
-                bt = t;
-                break;
+    // band tile regions: below / above the box by hyi rows (the grid case),
+    // or (streamed interior) flush with the box so the bands can be taller
+    int rjb = 0, rjt = 0;
+    if (inner) {  // streamed interior: any height; the bands as tall as their tiles allow
+        rjb = align_down(0);
+        rjt = align_down(W - hz + k - 1);  // the first aligned origin whose region reaches row W - 1
+        bb = rjb + hz - hyi;
+        bt = W - (rjt + hyi);
+        if (bb < p + 1 || bt < p + 1 || W - bb - bt < k) return {};
+    } else {
+        for (n_int = (W - 2) / ih; n_int >= 0 && bb < 0; --n_int)
+            for (int b = align_down(band_max); b >= 1; b -= k) {
+                const int t = W - b - n_int * ih;
+                if (b % k == ((jres % k) + k) % k && t >= 1 && t <= band_max) {
+                    bb = b;
+                    bt = t;
+                    break;
+                }
             }
-        }
-    ++n_int;
+        ++n_int;
+    }
     if (bb < 0) return {};
     auto band = [&](int oj0, int oj1, bool bottom) {
         const int n = ceil_div(cw, bw), w = ceil_div(cw, n);
@@ -105,12 +121,17 @@ std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz
             d.oj0 = oj0;
             d.oj1 = oj1;
             d.ri0 = d.oi0 - (wz - (d.oi1 - d.oi0)) / 2;
-            d.rj0 = bottom ? align_down(oj0 - hyi) : align_down(oj1 + hyi - hz);
+            if (inner)
+                d.rj0 = bottom ? rjb : rjt;
+            else
+                d.rj0 = bottom ? align_down(oj0 - hyi) : align_down(oj1 + hyi - hz);
             out.push_back(d);
         }
     };
     band(0, bb, true);
-    {
+    if (inner) {
+        *inner = Rect{c0, c1, bb, W - bt};
+    } else {
         const int n = ceil_div(cw, iw), w = ceil_div(cw, n);
         for (int r = 0; r < n_int; ++r)
             for (int q = 0; q < n; ++q) {
@@ -129,9 +150,37 @@ std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz
     return out;
 }
 
+// Slabs of the streamed interior: owned row bands of at most slab_rows - 2 p
+// rows (the stream kernel's threads), each region grown by p rows and columns.
+// The region stays inside the box interior [1, m-1]^2 (checked by the
+// caller), so every position is a 5-point lattice row and an owned
+// position's p-hop dependency cone lies in its region.  Returns the region
+// positions.
+long plan_slabs(const Rect& inner, int p, TilePlan& P) {
+    P.slab.clear();
+    P.slab_own.clear();
+    P.n_slabs = P.max_nx = 0;
+    if (inner.i0 == inner.i1) return 0;
+    const int rows = inner.j1 - inner.j0, per = P.slab_rows - 2 * p;
+    const int n = ceil_div(rows, per), each = ceil_div(rows, n);
+    const int nx = inner.i1 - inner.i0 + 2 * p;
+    long positions = 0;
+    for (int q = 0; q < n; ++q) {
+        const int oj0 = inner.j0 + q * each, oj1 = std::min(inner.j1, oj0 + each);
+        const int ny = oj1 - oj0 + 2 * p;
+        P.slab.insert(P.slab.end(), {inner.i0 - p, nx, oj0 - p, ny});
+        P.slab_own.insert(P.slab_own.end(), {p, p + inner.i1 - inner.i0, p, p + oj1 - oj0});
+        positions += static_cast<long>(nx) * ny;
+    }
+    P.n_slabs = n;
+    P.max_nx = nx;
+    return positions;
+}
+
 // Builds the tile tables of P for `tiles` and checks the halos; false with
 // P.reason when a tile fails.
-bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, int wide, int narrow, int k, TilePlan& P) {
+bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, const Rect& inner, int wide, int narrow,
+                 int k, TilePlan& P) {
     const int m = t.lat_m, W = m + 1, p = t.p, n_r = t.n_r, WW = W * W;
     P.tiles_shape.clear();
     P.thr_geo.clear();
@@ -146,6 +195,8 @@ bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, int w
     // owner of every box node, then of every R row outside the box (its
     // lattice position clamped into the box)
     std::vector<int> owner(static_cast<std::size_t>(WW), -1);
+    for (int i = inner.i0; i < inner.i1; ++i)
+        for (int j = inner.j0; j < inner.j1; ++j) owner[i * W + j] = -2;  // streamed
     for (std::size_t q = 0; q < tiles.size(); ++q)
         for (int i = tiles[q].oi0; i < tiles[q].oi1; ++i)
             for (int j = tiles[q].oj0; j < tiles[q].oj1; ++j) {
@@ -156,13 +207,17 @@ bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, int w
                 owner[i * W + j] = static_cast<int>(q);
             }
     for (int x = 0; x < WW; ++x)
-        if (owner[x] < 0) {
+        if (owner[x] == -1) {
             P.reason = "tiles leave a box node unowned";
             return false;
         }
     std::vector<std::vector<int>> belt_owned(tiles.size());
     for (int r = WW; r < n_r; ++r) {
         const int i = std::clamp(t.dof_lx[r], 0, m), j = std::clamp(t.dof_ly[r], 0, m);
+        if (owner[i * W + j] < 0) {
+            P.reason = "an R row outside the box maps into the streamed interior";
+            return false;
+        }
         belt_owned[owner[i * W + j]].push_back(r);
     }
     auto is_box = [&](int r) { return r < WW; };
@@ -383,13 +438,14 @@ bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, int w
     P.e_rc_off.push_back(static_cast<int>(P.rc_cell.size()));
     P.r_rc_off.push_back(static_cast<int>(P.rr_cell.size()));
     P.n_tiles = static_cast<int>(tiles.size());
+    region_positions += plan_slabs(inner, p, P);
     P.work_factor = static_cast<double>(region_positions) / static_cast<double>(WW);
     return true;
 }
 
 }  // namespace
 
-TilePlan plan_tiles(const LevelTables& t, int wide, int narrow, int k) {
+TilePlan plan_tiles(const LevelTables& t, int wide, int narrow, int k, int slab_rows, int stream_max_p) {
     TilePlan P;
     auto fail = [&](const std::string& why) {
         P.ok = false;
@@ -422,18 +478,32 @@ TilePlan plan_tiles(const LevelTables& t, int wide, int narrow, int k) {
     // the regular grid first; the frame layout when an edge halo is too narrow
     // (edge halo 2p, 3p, 4p) when an edge halo is too narrow
     std::string why;
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        const int he = (attempt + 1) * p;
-        const auto tiles = attempt == 0 ? layout_grid(W, p, k, P.jres, wide, narrow)
-                                        : layout_frame(W, p, k, P.jres, wide, narrow, he);
-        const std::string name = attempt == 0 ? "grid" : "frame(" + std::to_string(he) + ")";
+    // with streaming: the frame layouts with a streamed interior first
+    const bool stream = slab_rows > 2 * p && p <= stream_max_p;
+    P.slab_rows = slab_rows;
+    for (int attempt = stream ? -3 : 0; attempt < 4; ++attempt) {
+        Rect inner;
+        const bool streamed = attempt < 0;
+        const int he = streamed ? (attempt + 5) * p : (attempt + 1) * p;
+        std::vector<TileDesc> tiles = streamed       ? layout_frame(W, p, k, P.jres, wide, narrow, he, &inner)
+                                      : attempt == 0 ? layout_grid(W, p, k, P.jres, wide, narrow)
+                                                     : layout_frame(W, p, k, P.jres, wide, narrow, he);
+        std::string name = attempt == 0 ? "grid" : "frame(" + std::to_string(he) + ")";
+        if (streamed) {
+            name += "+stream";
+            if (inner.i0 - p < 1 || inner.i1 + p > m || inner.j0 - p < 1 || inner.j1 + p > m) {
+                why += name + ": interior too close to the ring; ";
+                continue;
+            }
+        }
         if (tiles.empty()) {
             why += name + ": no layout; ";
             continue;
         }
-        if (build_tiles(t, tiles, wide, narrow, k, P)) {
+        if (build_tiles(t, tiles, inner, wide, narrow, k, P)) {
             P.layout = name;
             P.reason.clear();
+            P.notes = why;
             P.ok = true;
             return P;
         }

@@ -35,6 +35,7 @@ struct TilePlan {
     int wz = 0, hz = 0, k = 0;
     int hs = 0;          // column stride of the wide shape (odd); the tall one uses (wz + 2) | 1
     int jres = 0;        // region row origins are = jres (mod k)
+    std::string notes;   // why the layouts tried before this one failed
     std::string layout;  // "grid" or "frame"
     int box_slots = 0;   // slots of the region rectangle incl. guards
     int max_gen = 0;     // generic rows per tile (<= threads)
@@ -67,11 +68,19 @@ struct TilePlan {
     // strip starting on one takes separate first-row conductances
     std::vector<std::uint8_t> line_row;  // per box row
     double work_factor = 0.0;           // region positions per owned lattice node (diagnostics)
+    // streamed interior (stream_step_kernel): slabs of at most `slab_rows`
+    // box rows swept along the columns; region (I0, NX, J0, NY) and owned
+    // region columns [x0, x1), rows [y0, y1); tiles own the rest of the box
+    int slab_rows = 0, n_slabs = 0, max_nx = 0;
+    std::vector<int> slab;      // [slab][4]
+    std::vector<int> slab_own;  // [slab][4]
 };
 
 // Plans the tiling for a box level (t.box) with the fixed kernel shape
 // (region wz x hz, K rows per strip).  ok = false (with reason) when the
 // level does not qualify or a tile fails the halo check.
-TilePlan plan_tiles(const LevelTables& t, int wide, int narrow, int k);
+// slab_rows > 0 (the stream kernel's rows per slab, p <= stream_max_p):
+// frame layouts hand the interior to streamed slabs.
+TilePlan plan_tiles(const LevelTables& t, int wide, int narrow, int k, int slab_rows = 0, int stream_max_p = 0);
 
 }  // namespace wmc

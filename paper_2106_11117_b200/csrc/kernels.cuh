@@ -444,6 +444,30 @@ struct TileArgs {
     int* fail;
     int step;
 };
+// Streamed interior of the tiled step (stream.cu): the box interior away
+// from the ring in horizontal slabs of kStreamThreads rows (one thread per
+// row), each slab swept column by column with all p levels in flight (a
+// wavefront: level m one column behind level m - 1), so a slab's region is
+// unbounded along the sweep and its halo is p columns at the two ends only.
+constexpr int kStreamThreads = 256;
+constexpr int kStreamMaxP = 8;
+struct StreamArgs {
+    int S, count, p, m, n, cells_x, n_slabs, max_nx;
+    double inv_h, h, inv_h2, c0;
+    double opb[kStreamMaxP], beta[kStreamMaxP], cm[kStreamMaxP];  // substep m at [m - 1]: 1 + beta_m, beta_m, c_m
+    const int4* slab;      // region: first column I0, columns NX, first row J0, rows NY (box coordinates)
+    const int4* slab_own;  // owned region columns [x0, x1), rows [y0, y1)
+    const int* cellx;
+    const int* celly;
+    const double* cells;   // [k * S + s]
+    const double* zc;      // z_n, sample-major
+    double* zp;            // z_{n-1} in, z_{n+1} out (owned rows)
+    int* fail;
+    int step;
+};
+int stream_smem_bytes(const StreamArgs& a);
+int launch_stream_step(const StreamArgs& a, int grid, void* stream);  // returns cudaError_t
+
 int tile_smem_bytes(const TileArgs& a);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
 int set_max_dynamic_smem(const void* kernel, int bytes);

@@ -1,0 +1,262 @@
+// Streamed interior of the temporally blocked LF-LTS step (sm_100a, FP64):
+// one global step of the reference's lts_step (src/integrators.cpp:117-157)
+// for the box nodes of R far from the box ring (host/tiles.hpp plans which).
+//
+// A work item is (slab, sample).  A slab is a band of up to kStreamThreads
+// box rows (one thread per row, so a column of the band is one coalesced
+// sample-major load) swept along the box columns.  Iteration t:
+//   level 0  z_n of column t arrives (prefetched one iteration earlier)
+//   level 1  g = A z_n on column t - 1 and d_1 = -c0 g
+//   level m  d_m on column t - m (m = 2 .. p): the recursion
+//            d_m = (1 + beta) d_{m-1} - beta d_{m-2} - c (g + A P d_{m-1})
+//            needs d_{m-1} on columns t - m - 1 .. t - m + 1 of its own row --
+//            the last one produced by level m - 1 earlier in this iteration --
+//            and on the rows above and below (published by the neighbour
+//            threads in the previous iteration)
+//   final    z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on column t - p (owned only).
+// Every level keeps its last three columns in registers (the phase t mod 3 is
+// a template argument, so the window never moves); a level's value for the
+// row neighbours goes through shared memory, double-buffered by the iteration
+// parity: one barrier per iteration for all p levels.  g waits p iterations
+// for its last use in a per-thread ring in tensor memory.
+//
+// The region is the owned band grown by p rows / columns; positions near its
+// edge see zeros for missing neighbours, an error that moves one column or
+// row per level and never reaches the owned positions.  Lattice values are
+// v = d / h (h a power of two) with conductances scaled by 1 / h^2, as in the
+// tile kernel (tile.cu).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "kernels.cuh"
+
+namespace wmc {
+namespace {
+
+constexpr int kT = kStreamThreads;
+constexpr int kPS = kT + 2;  // publish stride (guard rows 0 and kT + 1, always zero)
+constexpr int kRing = 16;    // g ring slots per thread (>= p)
+static_assert(kRing >= kStreamMaxP && (kRing & (kRing - 1)) == 0, "g ring");
+
+struct Cond {
+    double dg, kE, kW, kN, kS;
+};
+
+// conductances (scaled by 1 / h^2) of a node whose W / E squares lie in cell
+// columns key & 0xffff / key >> 16, N / S squares in cell rows cu / cd
+__device__ __forceinline__ Cond cond_of(const StreamArgs& a, int key, int cu, int cd, int s, double half) {
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const int x0 = key & 0xffff, x1 = key >> 16;
+    const double U0 = __ldg(a.cells + static_cast<std::size_t>(cu + x0) * S + s);
+    const double U1 = __ldg(a.cells + static_cast<std::size_t>(cu + x1) * S + s);
+    const double D0 = __ldg(a.cells + static_cast<std::size_t>(cd + x0) * S + s);
+    const double D1 = __ldg(a.cells + static_cast<std::size_t>(cd + x1) * S + s);
+    Cond c;
+    c.kE = (U1 + D1) * half;
+    c.kW = (U0 + D0) * half;
+    c.kN = (U0 + U1) * half;
+    c.kS = (D0 + D1) * half;
+    c.dg = c.kE + c.kW + c.kN + c.kS;
+    return c;
+}
+
+// g ring: slot q at TMEM columns 2q, 2q + 1 of the thread's lane
+__device__ __forceinline__ void ring_put(std::uint32_t tb, int slot, double g) {
+    asm volatile("{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %1;\n"
+                 "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {lo, hi};\n}\n"
+                 :
+                 : "r"(tb + 2u * static_cast<std::uint32_t>(slot)), "d"(g)
+                 : "memory");
+}
+// g of columns t - 2 .. t - 8 (levels 2 .. 8); the previous iteration's
+// store is waited for first
+__device__ __forceinline__ void ring_get7(std::uint32_t tb, int t, double (&g)[7]) {
+    std::uint32_t ad[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) ad[q] = tb + 2u * static_cast<std::uint32_t>((t - 2 - q) & (kRing - 1));
+    asm volatile(
+        "{\n.reg .b32 l<14>;\n"
+        "tcgen05.wait::st.sync.aligned;\n"
+        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l0, l1}, [%7];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l2, l3}, [%8];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l4, l5}, [%9];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l6, l7}, [%10];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l8, l9}, [%11];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l10, l11}, [%12];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l12, l13}, [%13];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        "mov.b64 %0, {l0, l1};\nmov.b64 %1, {l2, l3};\nmov.b64 %2, {l4, l5};\nmov.b64 %3, {l6, l7};\n"
+        "mov.b64 %4, {l8, l9};\nmov.b64 %5, {l10, l11};\nmov.b64 %6, {l12, l13};\n}\n"
+        : "=d"(g[0]), "=d"(g[1]), "=d"(g[2]), "=d"(g[3]), "=d"(g[4]), "=d"(g[5]), "=d"(g[6])
+        : "r"(ad[0]), "r"(ad[1]), "r"(ad[2]), "r"(ad[3]), "r"(ad[4]), "r"(ad[5]), "r"(ad[6])
+        : "memory");
+}
+
+template <int P>
+__global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
+    static_assert(P >= 2 && P <= kStreamMaxP, "levels");
+    extern __shared__ __align__(16) double sd[];
+    __shared__ std::uint32_t tm_slot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    double* pub = sd;  // [level][parity][kPS]
+    int* ckey = reinterpret_cast<int*>(sd + P * 2 * kPS);
+    for (int q = tid; q < P * 2 * kPS; q += kT) pub[q] = 0.0;
+
+    // tensor memory: 64 columns; warps w and w + 4 share lanes 32 (w % 4)..
+    // and take columns 0 / 32 (the g ring, 16 doubles)
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n"
+                     "tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n"
+                     :
+                     : "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&tm_slot)))
+                     : "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const std::uint32_t tb = tm_slot + (static_cast<std::uint32_t>(32 * (warp & 3)) << 16) + 32u * (warp >> 2);
+
+    const int W = a.m + 1, m = a.m;
+    const double half = 0.5 * a.inv_h2, inv_h = a.inv_h, h2 = 2.0 * a.h, c0 = a.c0;
+    const int items = a.n_slabs * a.count;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int s = item / a.n_slabs, sl = item - s * a.n_slabs;  // a sample's slabs on neighbouring CTAs
+        const int4 geo = __ldg(a.slab + sl), own = __ldg(a.slab_own + sl);
+        const int I0 = geo.x, NX = geo.y, J0 = geo.z, NY = geo.w;
+        __syncthreads();  // the previous item's key readers are done
+        for (int x = tid; x < NX; x += kT) {
+            const int i = I0 + x;
+            ckey[x] = __ldg(a.cellx + min(max(i - 1, 0), m - 1)) | (__ldg(a.cellx + min(max(i, 0), m - 1)) << 16);
+        }
+        const int y = tid, j = J0 + y;
+        const bool row_ok = y < NY;
+        const bool own_row = y >= own.z && y < own.w;
+        const int cu = __ldg(a.celly + min(max(j, 0), m - 1)) * a.cells_x;
+        const int cd = __ldg(a.celly + min(max(j - 1, 0), m - 1)) * a.cells_x;
+        const std::size_t base = static_cast<std::size_t>(s) * a.n + (row_ok ? j : J0);
+        const double* __restrict__ zs = a.zc + base;  // + column * W
+        double* __restrict__ zo = a.zp + base;
+        __syncthreads();  // ckey
+
+        auto key = [&](int x) { return ckey[min(max(x, 0), NX - 1)]; };
+        double w[P][3];
+#pragma unroll
+        for (int q = 0; q < P; ++q) w[q][0] = w[q][1] = w[q][2] = 0.0;
+        double znext = row_ok ? __ldg(zs + static_cast<std::size_t>(I0) * W) * inv_h : 0.0;
+        double wv_cur = 0.0, wv_next = 0.0;  // 2 z_n - z_{n-1} of the final column
+        int cur_key = -1;
+        Cond K{0.0, 0.0, 0.0, 0.0, 0.0};
+        bool bad = false;
+        const int NT = NX + P;
+
+        auto body = [&](auto ph, auto slow, int t) {
+            constexpr int PH = decltype(ph)::value;
+            constexpr bool kSlow = decltype(slow)::value;
+            constexpr int C = PH, P1 = (PH + 2) % 3, P2 = (PH + 1) % 3;  // window slots: this, previous, before
+            double gv[7];
+            ring_get7(tb, t, gv);
+            // level 0: z_n of column t; prefetch column t + 1 and the final's
+            // w of column t + 1 - P
+            w[0][C] = znext;
+            wv_cur = wv_next;
+            {
+                const int xn = t + 1, xf = t + 1 - P;
+                znext = row_ok && xn < NX ? __ldg(zs + static_cast<std::size_t>(I0 + xn) * W) * inv_h : 0.0;
+                if (own_row && xf >= own.x && xf < own.y) {
+                    const std::size_t o = static_cast<std::size_t>(I0 + xf) * W;
+                    wv_next = 2.0 * __ldg(zs + o) - zo[o];
+                }
+            }
+            const double* rd = pub + ((t - 1) & 1) * kPS + 1 + y;  // published in the previous iteration
+            double* wr = pub + (t & 1) * kPS + 1 + y;
+            wr[0] = w[0][C];
+            // level 1: g on column t - 1
+            {
+                const Cond k = kSlow ? cond_of(a, key(t - 1), cu, cd, s, half) : K;
+                const double g = k.dg * w[0][P1] - k.kE * w[0][C] - k.kW * w[0][P2] - k.kN * rd[1] - k.kS * rd[-1];
+                ring_put(tb, (t - 1) & (kRing - 1), g);
+                w[1][C] = -c0 * g;
+                if (P > 1) wr[2 * kPS] = w[1][C];
+            }
+#pragma unroll
+            for (int lv = 2; lv <= P; ++lv) {
+                const Cond k = kSlow ? cond_of(a, key(t - lv), cu, cd, s, half) : K;
+                const double* r = rd + (lv - 1) * 2 * kPS;
+                const double vO = w[lv - 1][P1];
+                const double aq = k.dg * vO - k.kE * w[lv - 1][C] - k.kW * w[lv - 1][P2] - k.kN * r[1] - k.kS * r[-1];
+                const double vprev = lv >= 3 ? w[lv >= 3 ? lv - 2 : 0][P2] : 0.0;
+                const double nx = a.opb[lv - 2] * vO - a.beta[lv - 2] * vprev - a.cm[lv - 2] * (gv[lv - 2] + aq);
+                if (lv < P) {
+                    w[lv < P ? lv : 0][C] = nx;
+                    wr[lv * 2 * kPS] = nx;
+                } else {
+                    const int xf = t - P;
+                    if (own_row && xf >= own.x && xf < own.y) {
+                        const double out = wv_cur + h2 * nx;
+                        zo[static_cast<std::size_t>(I0 + xf) * W] = out;
+                        bad |= !(fabs(out) <= 1e100);
+                    }
+                }
+            }
+            __syncthreads();
+        };
+        // fast iterations: every level's column in one run of equal cell
+        // columns (cellx is monotone, so the two ends decide) with the
+        // conductances held in registers; slow ones read them per level
+        auto step = [&](auto ph, int t) {
+            const int k1 = key(t - 1), kp = key(t - P);
+            if (k1 == kp) {
+                if (k1 != cur_key) {
+                    K = cond_of(a, k1, cu, cd, s, half);
+                    cur_key = k1;
+                }
+                body(ph, std::false_type{}, t);
+            } else {
+                body(ph, std::true_type{}, t);
+            }
+        };
+        for (int t0 = 0; t0 < NT; t0 += 3) {
+            step(std::integral_constant<int, 0>{}, t0);
+            if (t0 + 1 < NT) step(std::integral_constant<int, 1>{}, t0 + 1);
+            if (t0 + 2 < NT) step(std::integral_constant<int, 2>{}, t0 + 2);
+        }
+        if (bad && s < a.count) atomicMin(a.fail + s, a.step);
+    }
+
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" : : "r"(tm_slot) : "memory");
+}
+
+template <int P>
+int launch_p(const StreamArgs& a, int grid, void* stream) {
+    const int smem = stream_smem_bytes(a);
+    const int e = set_max_dynamic_smem(reinterpret_cast<const void*>(stream_step_kernel<P>), smem);
+    if (e != 0) return e;
+    stream_step_kernel<P><<<grid, kT, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace
+
+int stream_smem_bytes(const StreamArgs& a) {
+    return static_cast<int>(sizeof(double)) * a.p * 2 * kPS + static_cast<int>(sizeof(int)) * (a.max_nx + 2);
+}
+
+int launch_stream_step(const StreamArgs& a, int grid, void* stream) {
+    switch (a.p) {
+        case 2: return launch_p<2>(a, grid, stream);
+        case 3: return launch_p<3>(a, grid, stream);
+        case 4: return launch_p<4>(a, grid, stream);
+        case 5: return launch_p<5>(a, grid, stream);
+        case 6: return launch_p<6>(a, grid, stream);
+        case 7: return launch_p<7>(a, grid, stream);
+        case 8: return launch_p<8>(a, grid, stream);
+        default: return static_cast<int>(cudaErrorInvalidValue);
+    }
+}
+
+}  // namespace wmc

@@ -239,6 +239,17 @@ def level_plan(mesh: Mesh, spec: LevelSpec) -> dict:
     return _info_dict(info)
 
 
+def tile_plan(mesh: Mesh, spec: LevelSpec, stream: bool = True) -> dict:
+    """Host-only plan of the temporally blocked step (wmc_tile_plan): tiles
+    around the box ring, streamed slabs inside; no device."""
+    d = spec.desc()
+    info = N.TilePlanInfo()
+    N.check(N.lib().wmc_tile_plan(mesh._h, C.byref(d), 1 if stream else 0, C.byref(info)))
+    return {"ok": bool(info.ok), "n_tiles": info.n_tiles, "n_slabs": info.n_slabs, "max_gen": info.max_gen,
+            "work_factor": info.work_factor, "streamed_frac": info.streamed_frac,
+            "layout": info.layout.decode(), "reason": info.reason.decode()}
+
+
 class Level:
     """One MLMC level resident on a device (wmc_level)."""
 
