@@ -1522,6 +1522,10 @@ void fused_solve(wmc_level& L, Workspace& ws, const double* cells, int S, int co
     a.n_steps = t.n_steps;
     a.zp_global = L.fused_zp_global ? ws.zb : nullptr;
     a.tmem = L.fused_tmem;
+    {
+        static const char* e = std::getenv("WMC_FUSED_STAGGER");  // A/B knob (0: off)
+        a.stagger = e ? std::atoi(e) : 1;
+    }
     a.strips_k_or_k1 = 1;
     for (int len : t.strip_len)
         if (len < t.lat_k - 1) a.strips_k_or_k1 = 0;
@@ -2576,8 +2580,16 @@ int wmc_tile_plan(const wmc_mesh* mesh, const wmc_level_desc* desc, int stream, 
     return guarded([&] {
         if (!mesh || !desc || !info) throw ConfigError("wmc_tile_plan: NULL argument");
         const wmc::LevelTables t = wmc::build_level_tables(mesh->mesh, spec_from_desc(desc));
-        const wmc::TilePlan plan = wmc::plan_tiles(t, wmc::kTileWz, wmc::kTileHz, wmc::kTileK,
-                                                   stream ? wmc::kStreamThreads : 0, wmc::kStreamMaxP);
+        // WMC_PLAN_WIDE / WMC_PLAN_NARROW: planning studies of other region shapes (host only)
+        const char* pw = std::getenv("WMC_PLAN_WIDE");
+        const char* pn = std::getenv("WMC_PLAN_NARROW");
+        const wmc::TilePlan plan = wmc::plan_tiles(t, pw ? std::atoi(pw) : wmc::kTileWz, pn ? std::atoi(pn) : wmc::kTileHz,
+                                                   wmc::kTileK, stream ? wmc::kStreamThreads : 0, wmc::kStreamMaxP);
+        if (std::getenv("WMC_DEBUG_TILES"))
+            std::fprintf(stderr, "tile plan: ok=%d layout=%s reason=%s tiles=%d slabs=%d max_gen=%d max_app=%d "
+                         "max_ent=%d work=%.3f notes=%s\n", plan.ok, plan.layout.c_str(), plan.reason.c_str(),
+                         plan.n_tiles, plan.n_slabs, plan.max_gen, plan.max_app, plan.max_ent, plan.work_factor,
+                         plan.notes.c_str());
         *info = wmc_tile_plan_info{};
         info->ok = plan.ok ? 1 : 0;
         info->n_tiles = plan.n_tiles;

@@ -402,10 +402,13 @@ bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, const
         {
             // thread geometry (tile_step_kernel's item view): thread = 2
             // columns x k rows; wz / 64 warps per strip row
-            const int threads = wide / 2 * narrow / k, wpr = wz / 64;
+            // (a strip row narrower than a warp's 32 column pairs -- the tall
+            // shape of a 128 x 32 region -- puts 32 / pairs strips in a warp)
+            const int threads = wide / 2 * narrow / k, pairs = wz / 2;
             for (int tid = 0; tid < threads; ++tid) {
                 const int warp = tid / 32, lane = tid % 32;
-                const int strip = warp / wpr, tc = (warp % wpr) * 32 + lane;
+                const int strip = pairs >= 32 ? warp / (pairs / 32) : warp * (32 / pairs) + lane / pairs;
+                const int tc = pairs >= 32 ? (warp % (pairs / 32)) * 32 + lane : lane % pairs;
                 const int ia = ri0 + 2 * tc, jr0 = rj0 + strip * k;
                 unsigned lat = 0, own = 0;
                 for (int c = 0; c < 2; ++c)

@@ -2395,17 +2395,25 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
             int cur = o.v0, nxt = o.v1;
             const double* bp = sd + o.beta;
             const double* cp = sd + o.cm;
+            const bool lat_first = TM && A.stagger && (((tid >> 5) >> 2) & 1);  // warp-uniform
             for (int m = 1; m <= a.p - 1; ++m) {
                 const double beta = bp[m - 1];
                 const double cmm = cp[m - 1] * rs;
                 const double onepb = 1.0 + beta;
                 const double cmh = cmm * inv_h;
                 double gaq[G];
+                auto gather = [&]() {
 #pragma unroll
-                for (int u = 0; u < G; ++u) {
-                    gaq[u] = TM ? gen_gather_tm(gwid[u], sd, cur, tw_(u), tc_(u))
-                                : gen_gather_w(gwid[u], sd, o.gw, cur, gcol, gslot[u]);
-                }
+                    for (int u = 0; u < G; ++u) {
+                        gaq[u] = TM ? gen_gather_tm(gwid[u], sd, cur, tw_(u), tc_(u))
+                                    : gen_gather_w(gwid[u], sd, o.gw, cur, gcol, gslot[u]);
+                    }
+                };
+                // staggered warps: the generic gather is a latency chain (TMEM
+                // load, shared gather, FP64 sums), the lattice nodes are FP64
+                // work; half of each scheduler's four warps run the two in the
+                // other order so the phases overlap instead of coinciding
+                if (!lat_first) gather();
                 // TMEM: v_m of the thread's nodes parked for substep m + 1,
                 // v_{m-1} back from the other set
                 std::uint32_t vp[2 * K];
@@ -2484,6 +2492,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     vk = vn;
                 }
                 }
+                if (lat_first) gather();
 #pragma unroll
                 for (int u = 0; u < G; ++u) {
                     const double next = onepb * gd[u] - beta * gdp[u] - cmm * (ggg[u] + gaq[u]);

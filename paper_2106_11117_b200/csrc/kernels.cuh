@@ -326,6 +326,7 @@ struct LatSolveArgs {
     int* fail;                   // per sample: first non-finite step (INT_MAX: none)
     int strips_k_or_k1;          // every lattice strip holds K or K - 1 rows
     int tmem;                    // 0: shared memory; 1: generic weights/columns and d_{m-1} in tensor memory; 2: weights/columns only (default)
+    int stagger;                 // substeps: half of each scheduler's warps run their lattice nodes before their generic rows
 };
 
 int lattice_solve_smem_bytes(const LatSolveArgs& a);

@@ -38,7 +38,7 @@ namespace {
 constexpr int kT = kStreamThreads;
 constexpr int kPS = kT + 2;  // publish stride (guard rows 0 and kT + 1, always zero)
 constexpr int kRing = 16;    // g ring slots per thread (>= p)
-static_assert(kRing >= kStreamMaxP && (kRing & (kRing - 1)) == 0, "g ring");
+static_assert(kRing >= 2 * kStreamMaxP && (kRing & (kRing - 1)) == 0, "g ring");
 
 struct Cond {
     double dg, kE, kW, kN, kS;
@@ -62,36 +62,38 @@ __device__ __forceinline__ Cond cond_of(const StreamArgs& a, int key, int cu, in
     return c;
 }
 
-// g ring: slot q at TMEM columns 2q, 2q + 1 of the thread's lane
+// g ring in tensor memory, 16 slots (a slot = 2 columns of the thread's lane)
+// stored twice, at q and q + 16, so the 8 consecutive columns an iteration
+// needs never wrap: one 16-column load with the slot base in a uniform
+// register instead of a load (and its address arithmetic) per level
 __device__ __forceinline__ void ring_put(std::uint32_t tb, int slot, double g) {
     asm volatile("{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %1;\n"
-                 "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {lo, hi};\n}\n"
+                 "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {lo, hi};\n"
+                 "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0 + 32], {lo, hi};\n}\n"
                  :
                  : "r"(tb + 2u * static_cast<std::uint32_t>(slot)), "d"(g)
                  : "memory");
 }
-// g of columns t - 2 .. t - 8 (levels 2 .. 8); the previous iteration's
-// store is waited for first
-__device__ __forceinline__ void ring_get7(std::uint32_t tb, int t, double (&g)[7]) {
-    std::uint32_t ad[7];
-#pragma unroll
-    for (int q = 0; q < 7; ++q) ad[q] = tb + 2u * static_cast<std::uint32_t>((t - 2 - q) & (kRing - 1));
+// g of columns t - 8 .. t - 1 (g[8 - lv] for level lv; the last one is not
+// written yet and unused); the previous iteration's store is waited for first
+__device__ __forceinline__ void ring_get8(std::uint32_t tb, int t, double (&g)[8]) {
+    const std::uint32_t ad = tb + 2u * static_cast<std::uint32_t>((t - 8) & (kRing - 1));
     asm volatile(
-        "{\n.reg .b32 l<14>;\n"
+        "{\n.reg .b32 l<16>;\n"
         "tcgen05.wait::st.sync.aligned;\n"
-        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l0, l1}, [%7];\n"
-        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l2, l3}, [%8];\n"
-        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l4, l5}, [%9];\n"
-        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l6, l7}, [%10];\n"
-        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l8, l9}, [%11];\n"
-        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l10, l11}, [%12];\n"
-        "tcgen05.ld.sync.aligned.32x32b.x2.b32 {l12, l13}, [%13];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {l0, l1, l2, l3, l4, l5, l6, l7, l8, l9, l10, l11, l12, l13, l14, l15}, "
+        "[%8];\n"
         "tcgen05.wait::ld.sync.aligned;\n"
         "mov.b64 %0, {l0, l1};\nmov.b64 %1, {l2, l3};\nmov.b64 %2, {l4, l5};\nmov.b64 %3, {l6, l7};\n"
-        "mov.b64 %4, {l8, l9};\nmov.b64 %5, {l10, l11};\nmov.b64 %6, {l12, l13};\n}\n"
-        : "=d"(g[0]), "=d"(g[1]), "=d"(g[2]), "=d"(g[3]), "=d"(g[4]), "=d"(g[5]), "=d"(g[6])
-        : "r"(ad[0]), "r"(ad[1]), "r"(ad[2]), "r"(ad[3]), "r"(ad[4]), "r"(ad[5]), "r"(ad[6])
+        "mov.b64 %4, {l8, l9};\nmov.b64 %5, {l10, l11};\nmov.b64 %6, {l12, l13};\nmov.b64 %7, {l14, l15};\n}\n"
+        : "=d"(g[0]), "=d"(g[1]), "=d"(g[2]), "=d"(g[3]), "=d"(g[4]), "=d"(g[5]), "=d"(g[6]), "=d"(g[7])
+        : "r"(ad)
         : "memory");
+}
+
+constexpr int kAhead = 6;
+__device__ __forceinline__ void l2_prefetch(const double* p) {
+    asm volatile("prefetch.global.L2 [%0];\n" : : "l"(p));
 }
 
 template <int P>
@@ -104,10 +106,10 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
     int* ckey = reinterpret_cast<int*>(sd + P * 2 * kPS);
     for (int q = tid; q < P * 2 * kPS; q += kT) pub[q] = 0.0;
 
-    // tensor memory: 64 columns; warps w and w + 4 share lanes 32 (w % 4)..
-    // and take columns 0 / 32 (the g ring, 16 doubles)
+    // tensor memory: 128 columns; warps w and w + 4 share lanes 32 (w % 4)..
+    // and take columns 0 / 64 (the doubled g ring, 32 doubles)
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n"
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n"
                      "tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n"
                      :
                      : "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&tm_slot)))
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const std::uint32_t tb = tm_slot + (static_cast<std::uint32_t>(32 * (warp & 3)) << 16) + 32u * (warp >> 2);
+    const std::uint32_t tb = tm_slot + (static_cast<std::uint32_t>(32 * (warp & 3)) << 16) + 64u * (warp >> 2);
 
     const int W = a.m + 1, m = a.m;
     const double half = 0.5 * a.inv_h2, inv_h = a.inv_h, h2 = 2.0 * a.h, c0 = a.c0;
@@ -144,8 +146,11 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
         double w[P][3];
 #pragma unroll
         for (int q = 0; q < P; ++q) w[q][0] = w[q][1] = w[q][2] = 0.0;
-        double znext = row_ok ? __ldg(zs + static_cast<std::size_t>(I0) * W) * inv_h : 0.0;
-        double wv_cur = 0.0, wv_next = 0.0;  // 2 z_n - z_{n-1} of the final column
+        // prefetched one iteration ahead and consumed raw at the start of the
+        // next one (any arithmetic on the loaded value here would wait for it)
+        double znext = row_ok ? __ldg(zs + static_cast<std::size_t>(I0) * W) : 0.0;
+        double fz_next = 0.0, fp_next = 0.0;  // z_n, z_{n-1} of the final column
+        double wv_cur = 0.0;                  // 2 z_n - z_{n-1} of the final column
         int cur_key = -1;
         Cond K{0.0, 0.0, 0.0, 0.0, 0.0};
         bool bad = false;
@@ -155,42 +160,59 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
             constexpr int PH = decltype(ph)::value;
             constexpr bool kSlow = decltype(slow)::value;
             constexpr int C = PH, P1 = (PH + 2) % 3, P2 = (PH + 1) % 3;  // window slots: this, previous, before
-            double gv[7];
-            ring_get7(tb, t, gv);
+            double gv[8];
+            ring_get8(tb, t, gv);
             // level 0: z_n of column t; prefetch column t + 1 and the final's
             // w of column t + 1 - P
-            w[0][C] = znext;
-            wv_cur = wv_next;
+            w[0][C] = znext * inv_h;
+            wv_cur = 2.0 * fz_next - fp_next;
             {
                 const int xn = t + 1, xf = t + 1 - P;
-                znext = row_ok && xn < NX ? __ldg(zs + static_cast<std::size_t>(I0 + xn) * W) * inv_h : 0.0;
+                znext = row_ok && xn < NX ? __ldg(zs + static_cast<std::size_t>(I0 + xn) * W) : 0.0;
                 if (own_row && xf >= own.x && xf < own.y) {
                     const std::size_t o = static_cast<std::size_t>(I0 + xf) * W;
-                    wv_next = 2.0 * __ldg(zs + o) - zo[o];
+                    fz_next = __ldg(zs + o);
+                    fp_next = zo[o];
+                }
+                // the columns kAhead iterations on, into L2 (an iteration is
+                // about as long as a loaded DRAM access)
+                if (row_ok && (tid & 15) == 0) {  // one request per 128-byte line
+                    if (xn + kAhead < NX) l2_prefetch(zs + static_cast<std::size_t>(I0 + xn + kAhead) * W);
+                    if (xf + kAhead >= own.x && xf + kAhead < own.y)
+                        l2_prefetch(zo + static_cast<std::size_t>(I0 + xf + kAhead) * W);
                 }
             }
             const double* rd = pub + ((t - 1) & 1) * kPS + 1 + y;  // published in the previous iteration
             double* wr = pub + (t & 1) * kPS + 1 + y;
-            wr[0] = w[0][C];
+            // (the levels' values are published after the last level: a store
+            // between two levels' neighbour loads would order them -- the
+            // compiler cannot see that the two parity buffers never alias --
+            // and chain load -> FP64 -> store level by level)
             // level 1: g on column t - 1
             {
                 const Cond k = kSlow ? cond_of(a, key(t - 1), cu, cd, s, half) : K;
                 const double g = k.dg * w[0][P1] - k.kE * w[0][C] - k.kW * w[0][P2] - k.kN * rd[1] - k.kS * rd[-1];
                 ring_put(tb, (t - 1) & (kRing - 1), g);
                 w[1][C] = -c0 * g;
-                if (P > 1) wr[2 * kPS] = w[1][C];
             }
 #pragma unroll
             for (int lv = 2; lv <= P; ++lv) {
                 const Cond k = kSlow ? cond_of(a, key(t - lv), cu, cd, s, half) : K;
                 const double* r = rd + (lv - 1) * 2 * kPS;
                 const double vO = w[lv - 1][P1];
-                const double aq = k.dg * vO - k.kE * w[lv - 1][C] - k.kW * w[lv - 1][P2] - k.kN * r[1] - k.kS * r[-1];
                 const double vprev = lv >= 3 ? w[lv >= 3 ? lv - 2 : 0][P2] : 0.0;
-                const double nx = a.opb[lv - 2] * vO - a.beta[lv - 2] * vprev - a.cm[lv - 2] * (gv[lv - 2] + aq);
+                // d_lv = (1 + beta) d - beta d_prev - c (g + A d) in 8 FP64
+                // operations; the E neighbour -- formed a moment ago by level
+                // lv - 1 in this iteration -- enters last, so the levels of
+                // one iteration overlap except for two operations each.
+                // (Writing the levels' independent parts as seven interleaved
+                // chains spilled and ran slower: 3.49 vs 2.84 ms per step.)
+                const double rest =
+                    fma(-k.kS, r[-1], fma(-k.kN, r[1], fma(-k.kW, w[lv - 1][P2], fma(k.dg, vO, gv[8 - lv]))));
+                const double q = fma(a.opb[lv - 2], vO, -(a.beta[lv - 2] * vprev));
+                const double nx = fma(-a.cm[lv - 2], fma(-k.kE, w[lv - 1][C], rest), q);
                 if (lv < P) {
                     w[lv < P ? lv : 0][C] = nx;
-                    wr[lv * 2 * kPS] = nx;
                 } else {
                     const int xf = t - P;
                     if (own_row && xf >= own.x && xf < own.y) {
@@ -200,6 +222,8 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
                     }
                 }
             }
+#pragma unroll
+            for (int lv = 0; lv < P; ++lv) wr[lv * 2 * kPS] = w[lv][C];
             __syncthreads();
         };
         // fast iterations: every level's column in one run of equal cell
@@ -228,7 +252,7 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" : : "r"(tm_slot) : "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" : : "r"(tm_slot) : "memory");
 }
 
 template <int P>
