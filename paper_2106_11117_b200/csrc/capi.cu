@@ -162,6 +162,8 @@ struct wmc_level {
     wmc::TileArgs tile{};          // static part of the kernel arguments
     std::vector<void*> tile_bufs;
     int tile_smem = 0;
+    int tile_ctas_per_sm = 1;
+    int slab_width = 0;            // owned columns of a streamed slab
     double tile_work = 0.0;        // region positions per box node (diagnostics)
     wmc::StreamArgs slabs{};       // streamed interior of the tiled step (n_slabs = 0: none)
     int stream_smem = 0;
@@ -638,6 +640,10 @@ void build_device_level(wmc_level& L) {
                     sa.m = t.lat_m;
                     sa.cells_x = L.spec.cells_x;
                     sa.n_slabs = plan.n_slabs;
+                    sa.threads = plan.slab_threads;
+                    sa.chunks = 1;
+                    sa.chunk_cols = plan.slab_own[1] - plan.slab_own[0];
+                    L.slab_width = sa.chunk_cols;
                     sa.max_nx = plan.max_nx;
                     sa.inv_h = a.inv_h;
                     sa.h = a.h;
@@ -657,6 +663,10 @@ void build_device_level(wmc_level& L) {
                 int optin = 0;
                 cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, L.device);
                 if (L.tile_smem + 64 <= optin) L.path = SubPath::Tiled;
+                // CTAs per SM: registers allow 512 / threads; each takes its shared memory plus 1 KB
+                int smem_per_sm = 0;
+                cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, L.device);
+                L.tile_ctas_per_sm = std::max(1, std::min(512 / wmc::kTileThreads, smem_per_sm / (L.tile_smem + 1024)));
             }
         }
         if (L.path == SubPath::Global) {
@@ -1330,7 +1340,8 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
             ta.fail = ws.fail;
             ta.step = static_cast<int>(s + 1);
             const long items = static_cast<long>(ta.n_tiles) * count;
-            const int e = wmc::launch_tile_step(ta, static_cast<int>(std::min<long>(items, L.n_sms)), stream);
+            const int e = wmc::launch_tile_step(
+                ta, static_cast<int>(std::min<long>(items, static_cast<long>(L.tile_ctas_per_sm) * L.n_sms)), stream);
             if (e != 0) check(static_cast<cudaError_t>(e), "tiled step launch");
             ++g_launches;
             if (L.slabs.n_slabs > 0) {
@@ -1343,9 +1354,26 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
                 sa.zp = prev;
                 sa.fail = ws.fail;
                 sa.step = static_cast<int>(s + 1);
-                const long sitems = static_cast<long>(sa.n_slabs) * count;
-                const int es = wmc::launch_stream_step(sa, static_cast<int>(std::min<long>(sitems, 2L * L.n_sms)),
-                                                       stream);
+                // column chunks: the split of the slabs' owned columns that
+                // needs the fewest column iterations over the grid's rounds
+                // (every chunk leads and trails by p columns and drains p levels)
+                const long grid_max = static_cast<long>(512 / sa.threads) * L.n_sms;  // 128 registers per thread
+                const int width = L.slab_width, lead = 3 * sa.p;
+                long best = -1;
+                static const char* force = std::getenv("WMC_STREAM_CHUNKS");  // A/B knob
+                const int c_lo = force ? std::atoi(force) : 1, c_hi = force ? c_lo : 8;
+                for (int c = c_lo; c <= c_hi && (c == c_lo || width / c >= 4 * lead); ++c) {
+                    const int cols = (width + c - 1) / c;
+                    const long rounds = (static_cast<long>(sa.n_slabs) * c * count + grid_max - 1) / grid_max;
+                    const long cost = rounds * (cols + lead);
+                    if (best < 0 || cost < best) {
+                        best = cost;
+                        sa.chunks = c;
+                        sa.chunk_cols = cols;
+                    }
+                }
+                const long sitems = static_cast<long>(sa.n_slabs) * sa.chunks * count;
+                const int es = wmc::launch_stream_step(sa, static_cast<int>(std::min<long>(sitems, grid_max)), stream);
                 if (es != 0) check(static_cast<cudaError_t>(es), "streamed step launch");
                 ++g_launches;
             }

@@ -53,7 +53,12 @@ std::vector<TileDesc> layout_grid(int W, int p, int k, int jres, int wz, int hz)
 // bottom and top bands, the regular grid inside.  Row origins stay = jres
 // (mod k).
 // With `inner` the interior grid is left out and its rectangle returned.
-std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz, int he, Rect* inner = nullptr) {
+// `thin_sides` (streamed interior only): the bottom and top bands span every
+// column, corners included, and the side bands between them own tw - p
+// columns (their tiles see no corner, so p columns of halo on the inner
+// side are enough -- the halo check has the last word).
+std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz, int he, Rect* inner = nullptr,
+                                   bool thin_sides = false) {
     std::vector<TileDesc> out;
     auto align_down = [&](int j) {  // largest value <= j that is = jres (mod k)
         int r = ((j - jres) % k + k) % k;
@@ -63,23 +68,33 @@ std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz
     const int hye = ceil_div(he, k) * k, hyi = ceil_div(hi, k) * k;
     // side bands: tall tiles (hz columns x wz rows), owned width sb
     const int tw = hz, th = wz;
-    const int sb = tw - he;
+    thin_sides = thin_sides && inner;
+    const int sb = thin_sides ? tw - hi : tw - he;
     if (sb < 8 || 2 * sb >= W) return out;
     const int soh = th - 2 * hye;
     if (soh < k) return out;
+    // rows of the side bands: all of them, or (thin sides) those between the
+    // bottom and top bands, whose heights follow from the wide tiles below
+    int side_j0 = 0, side_j1 = W;
+    if (thin_sides) {
+        const int rjb_ = align_down(0), rjt_ = align_down(W - hz + k - 1);
+        side_j0 = rjb_ + hz - hyi;
+        side_j1 = rjt_ + hyi;
+        if (side_j0 < p + 1 || W - side_j1 < p + 1 || side_j1 - side_j0 < k) return {};
+    }
     for (int side = 0; side < 2; ++side) {
         const int oi0 = side == 0 ? 0 : W - sb, oi1 = side == 0 ? sb : W;
         const int ri0 = side == 0 ? 0 : W - tw;
-        for (int oj0 = 0; oj0 < W;) {
+        for (int oj0 = side_j0; oj0 < side_j1;) {
             const int start = align_down(oj0);
-            const int oj1 = std::min(W, start + soh);
+            const int oj1 = std::min(side_j1, start + soh);
             TileDesc d{1, ri0, start - hye, oi0, oi1, oj0, oj1};
             out.push_back(d);
             oj0 = oj1;
         }
     }
-    // middle columns [sb, W - sb): bottom / top bands (halo he across
-    // columns) and the interior grid (halo hi)
+    // middle columns [sb, W - sb) (thin sides: every column): bottom / top
+    // bands (halo he across columns) and the interior grid (halo hi)
     const int c0 = sb, c1 = W - sb, cw = c1 - c0;
     const int bw = wz - 2 * he;  // band tile owned width
     const int iw = wz - 2 * hi;  // interior owned width
@@ -111,7 +126,20 @@ std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz
         ++n_int;
     }
     if (bb < 0) return {};
+    // thin sides: the corners are square tiles (shape 2, sq x sq positions:
+    // paths along both edges' coarser rows stay inside), owning sq - he columns
+    int sq = 0;
+    while (sq * sq < wz * hz) ++sq;
+    const int cown = sq - he;
+    if (thin_sides && (sq * sq != wz * hz || sq % 64 || cown < sb || 2 * cown >= W)) return {};
     auto band = [&](int oj0, int oj1, bool bottom) {
+        int c0 = thin_sides ? cown : sb, c1 = W - c0;
+        const int cw = c1 - c0;
+        if (thin_sides) {
+            const int rj = bottom ? rjb : align_down(W - sq + k - 1);
+            out.push_back(TileDesc{2, 0, rj, 0, cown, oj0, oj1});
+            out.push_back(TileDesc{2, W - sq, rj, W - cown, W, oj0, oj1});
+        }
         const int n = ceil_div(cw, bw), w = ceil_div(cw, n);
         for (int q = 0; q < n; ++q) {
             TileDesc d;
@@ -130,7 +158,7 @@ std::vector<TileDesc> layout_frame(int W, int p, int k, int jres, int wz, int hz
     };
     band(0, bb, true);
     if (inner) {
-        *inner = Rect{c0, c1, bb, W - bt};
+        *inner = Rect{sb, W - sb, bb, W - bt};
     } else {
         const int n = ceil_div(cw, iw), w = ceil_div(cw, n);
         for (int r = 0; r < n_int; ++r)
@@ -161,7 +189,23 @@ long plan_slabs(const Rect& inner, int p, TilePlan& P) {
     P.slab_own.clear();
     P.n_slabs = P.max_nx = 0;
     if (inner.i0 == inner.i1) return 0;
-    const int rows = inner.j1 - inner.j0, per = P.slab_rows - 2 * p;
+    // CTA size: the multiple of four warps (at most slab_rows, a thread per region
+    // row) that wastes the fewest thread-rows; ties to the larger CTA
+    const int rows = inner.j1 - inner.j0;
+    int best_t = 0;
+    long best_cost = 0;
+    // (multiples of four warps only: the SM's four schedulers take a CTA's
+    // warps round-robin, and an uneven share made 224 threads no faster than 256)
+    for (int T = P.slab_rows; T >= 128 && T > 2 * p + 32; T -= 128) {
+        const long cost = static_cast<long>(ceil_div(rows, T - 2 * p)) * T;
+        if (best_t == 0 || cost < best_cost) {
+            best_t = T;
+            best_cost = cost;
+        }
+    }
+    if (best_t == 0) best_t = P.slab_rows;
+    P.slab_threads = best_t;
+    const int per = best_t - 2 * p;
     const int n = ceil_div(rows, per), each = ceil_div(rows, n);
     const int nx = inner.i1 - inner.i0 + 2 * p;
     long positions = 0;
@@ -225,11 +269,14 @@ bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, const
     long region_positions = 0;
     for (std::size_t q = 0; q < tiles.size(); ++q) {
         const TileDesc& d = tiles[q];
-        const int wz = d.shape == 0 ? wide : narrow, hz = d.shape == 0 ? narrow : wide;
+        int sq = 0;
+        while (sq * sq < wide * narrow) ++sq;
+        const int wz = d.shape == 0 ? wide : d.shape == 1 ? narrow : sq;
+        const int hz = d.shape == 0 ? narrow : d.shape == 1 ? wide : sq;
         const int hs = (hz + 2) | 1;
         const int box_slots = (wz + 3) * hs;
-        if (box_slots != P.box_slots) {
-            P.reason = "shapes with different slot counts";
+        if (box_slots > P.box_slots || wz * hz != wide * narrow) {  // appended slots start at P.box_slots
+            P.reason = "a shape exceeds the plan's slot count";
             return false;
         }
         if (((d.rj0 - P.jres) % k + k) % k != 0) {
@@ -289,7 +336,7 @@ bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, const
                 if (!interior(i, j)) gens.push_back(i * W + j);
         int n_app = 0;
         for (int x : belt_ball) {
-            slot_of[x] = box_slots + n_app++;
+            slot_of[x] = P.box_slots + n_app++;
             gens.push_back(x);
         }
         {
@@ -298,7 +345,7 @@ bool build_tiles(const LevelTables& t, const std::vector<TileDesc>& tiles, const
                 if (is_box(x) && !in_rect(x / W, x % W)) far.push_back(x);
             std::sort(far.begin(), far.end());
             for (int x : far) {
-                slot_of[x] = box_slots + n_app++;
+                slot_of[x] = P.box_slots + n_app++;
                 gens.push_back(x);
             }
         }
@@ -459,7 +506,7 @@ TilePlan plan_tiles(const LevelTables& t, int wide, int narrow, int k, int slab_
     if (t.kind != Integrator::LocalTimeStepping || t.tiers != 1) return fail("single-tier LF-LTS only");
     if (t.p < 2) return fail("p < 2");
     if (t.cfl_safety > 0.0) return fail("per-sample CFL");
-    if (wide % 64 || narrow % k || narrow % 64) return fail("region shape");
+    if (wide % 64 || narrow % k || narrow % 32 || (narrow < 64 && 64 % narrow)) return fail("region shape");
     const int m = t.lat_m, W = m + 1, p = t.p;
     const double h = 1.0 / t.lat_inv_h;
     if (std::exp2(std::round(std::log2(h))) != h) return fail("lattice h not a power of two");
@@ -484,16 +531,18 @@ TilePlan plan_tiles(const LevelTables& t, int wide, int narrow, int k, int slab_
     // with streaming: the frame layouts with a streamed interior first
     const bool stream = slab_rows > 2 * p && p <= stream_max_p;
     P.slab_rows = slab_rows;
-    for (int attempt = stream ? -3 : 0; attempt < 4; ++attempt) {
+    for (int attempt = stream ? -6 : 0; attempt < 4; ++attempt) {
         Rect inner;
         const bool streamed = attempt < 0;
-        const int he = streamed ? (attempt + 5) * p : (attempt + 1) * p;
-        std::vector<TileDesc> tiles = streamed       ? layout_frame(W, p, k, P.jres, wide, narrow, he, &inner)
+        // streamed attempts: halo 2p, 3p, 4p with thin side bands, then the same with full-height ones
+        const bool thin = attempt < -3;
+        const int he = streamed ? ((attempt + 6) % 3 + 2) * p : (attempt + 1) * p;
+        std::vector<TileDesc> tiles = streamed       ? layout_frame(W, p, k, P.jres, wide, narrow, he, &inner, thin)
                                       : attempt == 0 ? layout_grid(W, p, k, P.jres, wide, narrow)
                                                      : layout_frame(W, p, k, P.jres, wide, narrow, he);
         std::string name = attempt == 0 ? "grid" : "frame(" + std::to_string(he) + ")";
         if (streamed) {
-            name += "+stream";
+            name += thin ? "+thin+stream" : "+stream";
             if (inner.i0 - p < 1 || inner.i1 + p > m || inner.j0 - p < 1 || inner.j1 + p > m) {
                 why += name + ": interior too close to the ring; ";
                 continue;

@@ -72,6 +72,7 @@ struct TilePlan {
     // box rows swept along the columns; region (I0, NX, J0, NY) and owned
     // region columns [x0, x1), rows [y0, y1); tiles own the rest of the box
     int slab_rows = 0, n_slabs = 0, max_nx = 0;
+    int slab_threads = 0;       // rows of the tallest slab region rounded up to a warp (the kernel's CTA size)
     std::vector<int> slab;      // [slab][4]
     std::vector<int> slab_own;  // [slab][4]
 };

@@ -2785,6 +2785,9 @@ int set_max_dynamic_smem(const void* kernel, int bytes) {
     const auto it = done.find(key);
     if (it != done.end()) return it->second;
     const int r = static_cast<int>(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    // the largest shared-memory carveout, so kernels that co-reside two CTAs per
+    // SM by their shared memory (tile / stream steps) get the whole array
+    if (r == 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     done[key] = r;
     return r;
 }

@@ -407,16 +407,18 @@ void launch_r_update(const RUpdateArgs& a, void* stream);
 // on chip for the whole step:
 // z_n in, g = A z_n, the p - 1 substeps, z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on
 // the owned rows out.  Rows outside R are left to the sweep.
-constexpr int kTileThreads = 512;
+constexpr int kTileThreads = 256;  // two CTAs per SM: one's barriers and latencies overlap the other's work
 constexpr int kTileK = 8;     // rows per strip (thread = 2 columns x kTileK rows)
 constexpr int kTileWz = 128;  // region columns
-constexpr int kTileHz = 64;   // region rows
+constexpr int kTileHz = 32;   // region rows (shape 1 is the transpose, shape 2 the square of the same area)
+constexpr int kTileSq = 64;
+static_assert(kTileSq * kTileSq == kTileWz * kTileHz, "square shape");
 struct TileArgs {
     int S, count, p, m, n_cells, cells_x;
     int box_slots, max_app, max_ent, max_gen, n_tiles;
     double inv_h, h, inv_h2, c0;
     const int4* tile_rect;   // per tile: region origin i0, j0; owned columns [oi0, oi1)
-    const int4* tile_oj;     // owned rows [oj0, oj1), shape (0: kTileWz x kTileHz, 1: kTileHz x kTileWz)
+    const int4* tile_oj;     // owned rows [oj0, oj1), shape (0: kTileWz x kTileHz, 1: kTileHz x kTileWz, 2: kTileSq x kTileSq)
     const int4* thr_geo;     // per tile and thread: first column, first row, lattice | owned << 16
     const int* gen_off;      // per tile: generic rows [gen_off[t], gen_off[t+1])
     const int* g_slot;
@@ -454,6 +456,8 @@ constexpr int kStreamThreads = 256;
 constexpr int kStreamMaxP = 8;
 struct StreamArgs {
     int S, count, p, m, n, cells_x, n_slabs, max_nx;
+    int threads;             // CTA size: the slabs' rows rounded up to a warp (<= kStreamThreads)
+    int chunks, chunk_cols;  // a slab's owned columns in `chunks` runs of chunk_cols (work items of even length)
     double inv_h, h, inv_h2, c0;
     double opb[kStreamMaxP], beta[kStreamMaxP], cm[kStreamMaxP];  // substep m at [m - 1]: 1 + beta_m, beta_m, c_m
     const int4* slab;      // region: first column I0, columns NX, first row J0, rows NY (box coordinates)

@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5;
     double* pub = sd;  // [level][parity][kPS]
     int* ckey = reinterpret_cast<int*>(sd + P * 2 * kPS);
-    for (int q = tid; q < P * 2 * kPS; q += kT) pub[q] = 0.0;
+    const int nthr = blockDim.x;
+    for (int q = tid; q < P * 2 * kPS; q += nthr) pub[q] = 0.0;
 
     // tensor memory: 128 columns; warps w and w + 4 share lanes 32 (w % 4)..
     // and take columns 0 / 64 (the doubled g ring, 32 doubles)
@@ -122,13 +123,20 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
 
     const int W = a.m + 1, m = a.m;
     const double half = 0.5 * a.inv_h2, inv_h = a.inv_h, h2 = 2.0 * a.h, c0 = a.c0;
-    const int items = a.n_slabs * a.count;
+    const int per_sample = a.n_slabs * a.chunks;
+    const int items = per_sample * a.count;
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int s = item / a.n_slabs, sl = item - s * a.n_slabs;  // a sample's slabs on neighbouring CTAs
-        const int4 geo = __ldg(a.slab + sl), own = __ldg(a.slab_own + sl);
-        const int I0 = geo.x, NX = geo.y, J0 = geo.z, NY = geo.w;
+        // a sample's slabs (and a slab's column chunks) on neighbouring CTAs
+        const int s = item / per_sample, rest = item - s * per_sample;
+        const int sl = rest / a.chunks, ch = rest - sl * a.chunks;
+        const int4 geo = __ldg(a.slab + sl);
+        int4 own = __ldg(a.slab_own + sl);
+        // chunk ch of the owned columns (own.x == p: the region leads by p columns)
+        const int q0 = ch * a.chunk_cols, q1 = min(own.y - own.x, q0 + a.chunk_cols);
+        const int I0 = geo.x + q0, NX = q1 - q0 + 2 * own.x, J0 = geo.z, NY = geo.w;
+        own.y = own.x + q1 - q0;
         __syncthreads();  // the previous item's key readers are done
-        for (int x = tid; x < NX; x += kT) {
+        for (int x = tid; x < NX; x += nthr) {
             const int i = I0 + x;
             ckey[x] = __ldg(a.cellx + min(max(i - 1, 0), m - 1)) | (__ldg(a.cellx + min(max(i, 0), m - 1)) << 16);
         }
@@ -260,7 +268,7 @@ int launch_p(const StreamArgs& a, int grid, void* stream) {
     const int smem = stream_smem_bytes(a);
     const int e = set_max_dynamic_smem(reinterpret_cast<const void*>(stream_step_kernel<P>), smem);
     if (e != 0) return e;
-    stream_step_kernel<P><<<grid, kT, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    stream_step_kernel<P><<<grid, a.threads, smem, static_cast<cudaStream_t>(stream)>>>(a);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -38,9 +38,10 @@ namespace {
 
 constexpr int kT = kTileThreads;
 constexpr int kK = kTileK;
-constexpr int kTPC = kTileWz / 2;          // thread columns per strip row
-constexpr int kWarpsPerRow = kTPC / 32;
-static_assert(kTPC % 32 == 0 && kT == kTPC * (kTileHz / kK), "tile shape");
+constexpr int kTPC = kTileWz / 2;          // thread columns per strip row (wide shape)
+static_assert(kTPC % 32 == 0 && kT == kTPC * (kTileHz / kK) && kT % 128 == 0, "tile shape");
+static_assert(32 % (kTileHz / 2) == 0 || (kTileHz / 2) % 32 == 0, "tall shape: strips per warp");
+constexpr int kTmCols = 128 * (kT / 128);  // tensor-memory columns of a CTA (128 per four warps)
 
 __device__ __forceinline__ void t_ld16(std::uint32_t addr, std::uint32_t (&r)[16]) {
     asm volatile(
@@ -166,13 +167,16 @@ __device__ __forceinline__ ItemGeo item_geo(const TileArgs& a, int item, int war
     g.s = item - g.tile * a.count;
     const int shape = __ldg(&a.tile_oj[g.tile].z);
     const int4 t = __ldg(a.thr_geo + g.tile * kT + warp * 32 + lane);  // planned per (tile, thread)
-    // region shape: wide (kTileWz columns, two warps per strip row) or tall
-    // (kTileHz columns, one warp per strip row); the same slot count
-    g.wz = shape ? kTileHz : kTileWz;
-    g.hz = shape ? kTileWz : kTileHz;
+    // region shape: wide (kTileWz columns), tall (kTileHz columns) or square
+    // (the corners); the same number of positions
+    g.wz = shape == 0 ? kTileWz : shape == 1 ? kTileHz : kTileSq;
+    g.hz = shape == 0 ? kTileHz : shape == 1 ? kTileWz : kTileSq;
     g.HS = g.hz + 3;
-    const int wpr = g.wz / 64;
-    const int strip = warp / wpr, tc = (warp % wpr) * 32 + lane;
+    // a strip row of fewer than 32 column pairs (the tall shape) puts
+    // 32 / pairs strips in a warp (host/tiles.cpp plans the same mapping)
+    const int pairs = g.wz / 2;
+    const int strip = pairs >= 32 ? warp / (pairs / 32) : warp * (32 / pairs) + lane / pairs;
+    const int tc = pairs >= 32 ? (warp % (pairs / 32)) * 32 + lane : lane % pairs;
     const int pa = tc + 1, pb = g.wz / 2 + 2 + tc;  // column positions of the own columns
     g.sa = pa * g.HS + strip * kK + 1;
     g.sb = pb * g.HS + strip * kK + 1;
@@ -213,7 +217,7 @@ __device__ __forceinline__ void tm_get8(std::uint32_t addr, double (&d)[kK]) {
     }
 }
 
-__global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
+__global__ void __launch_bounds__(kT, 512 / kT) tile_step_kernel(TileArgs a) {
     extern __shared__ __align__(16) double sd[];
     __shared__ std::uint32_t tm_slot;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -235,13 +239,13 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
     const double* __restrict__ zc = a.zc;
     double* __restrict__ zp = a.zp;
 
-    // tensor memory: 512 columns (one CTA per SM); warp w: lanes 32 (w % 4)..,
-    // columns 128 (w / 4)..
+    // tensor memory: 128 columns per four warps (the SM's 512 shared by its
+    // CTAs); warp w: lanes 32 (w % 4).., columns 128 (w / 4)..
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
                      "tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n"
                      :
-                     : "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&tm_slot)))
+                     : "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&tm_slot))), "n"(kTmCols)
                      : "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -514,14 +518,31 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
             }
             for (int u = tid; u < ng; u += kT) {
                 const int r = gb + u;
+                // the row's table reads first (independent loads, one latency),
+                // then its entries four at a time: slots and weights of a
+                // group before its gathers (padding: weight 0 on the zero
+                // guard slot 0, so the sum keeps its order and value)
+                const int e0 = __ldg(a.g_ent_off + r), e1 = __ldg(a.g_ent_off + r + 1);
+                const int gs = __ldg(a.g_slot + r);
+                const double rs = __ldg(a.g_rs + r);
+                const double d = gst[u], dp = gst[a.max_gen + u], gg = gst[2 * a.max_gen + u];
                 double acc = 0.0;
-                for (int e = __ldg(a.g_ent_off + r); e < __ldg(a.g_ent_off + r + 1); ++e)
-                    acc += wbuf[e - eb] * cur[__ldg(a.e_slot + e)];
-                const double d = gst[u], dp = gst[a.max_gen + u];
-                const double next = onepb * d - beta * dp - cmm * (gst[2 * a.max_gen + u] + acc);
+                for (int e = e0; e < e1; e += 4) {
+                    int sl[4];
+                    double w[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const bool ok = e + q < e1;
+                        sl[q] = ok ? __ldg(a.e_slot + e + q) : 0;
+                        w[q] = ok ? wbuf[e + q - eb] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc += w[q] * cur[sl[q]];
+                }
+                const double next = onepb * d - beta * dp - cmm * (gg + acc);
                 gst[a.max_gen + u] = d;
                 gst[u] = next;
-                nxt[__ldg(a.g_slot + r)] = next * __ldg(a.g_rs + r);
+                nxt[gs] = next * rs;
             }
             if (mm <= 8) commit(mm - 1, pre);
             __syncthreads();
@@ -572,7 +593,8 @@ __global__ void __launch_bounds__(kT, 1) tile_step_kernel(TileArgs a) {
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" : : "r"(tm_slot) : "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" : : "r"(tm_slot), "n"(kTmCols) : "memory");
 }
 
 }  // namespace
