@@ -51,6 +51,9 @@ extern "C" {
 
 #define WMC_FIELD_UNIFORM 0        /* c_k = next_uniform(lo, hi) per cell */
 #define WMC_FIELD_LOGNORMAL_KL 1   /* c = exp(g), g a truncated KL expansion sampled at cell centres */
+#define WMC_FIELD_LOGNORMAL_KL_ELEMENT 2 /* the same g at every triangle's centroid: one coefficient per element, as
+                                            the reference's assemble evaluates speed2 (src/fem.cpp:103-104); cells_x /
+                                            cells_y unused; the levels of a pair evaluate one draw on their own elements */
 
 typedef struct wmc_mesh wmc_mesh;
 typedef struct wmc_level wmc_level;
@@ -103,7 +106,7 @@ typedef struct {
     double qoi_box[4];           /* x0, x1, y0, y1: Q = lumped integral of u(T) over the box */
     int device;                  /* CUDA device ordinal */
     int batch;                   /* samples per device batch, 0 = automatic */
-    int field;                   /* WMC_FIELD_UNIFORM or WMC_FIELD_LOGNORMAL_KL */
+    int field;                   /* WMC_FIELD_UNIFORM, WMC_FIELD_LOGNORMAL_KL or WMC_FIELD_LOGNORMAL_KL_ELEMENT */
     double kl_sigma;             /* KL: standard deviation of g */
     double kl_corr_len;          /* KL: correlation length of exp(-|dx|/l - |dy|/l) */
     int kl_modes;                /* KL: number of terms, xi_m ~ N(0,1) by Box-Muller over next_unit pairs */

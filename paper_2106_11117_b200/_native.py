@@ -20,6 +20,7 @@ WMC_LEAPFROG = 0
 WMC_LOCAL_TIME_STEPPING = 1
 WMC_FIELD_UNIFORM = 0
 WMC_FIELD_LOGNORMAL_KL = 1
+WMC_FIELD_LOGNORMAL_KL_ELEMENT = 2
 
 
 class SquareMeshSpec(C.Structure):

@@ -723,8 +723,13 @@ void build_device_level(wmc_level& L) {
             L.sub_cl_smem = 0;
         }
     }
-    if (!t.field_x.empty()) L.d_field_x = upload(t.field_x);
+    if (!t.field_x.empty() && L.spec.field != wmc::Field::LognormalKLElem) L.d_field_x = upload(t.field_x);
     if (!t.field_table.empty()) L.d_field_table = upload(t.field_table);
+    if (L.spec.field == wmc::Field::LognormalKLElem) {
+        // one table row per triangle, at its centroid (level.cpp keeps them in field_x)
+        const wmc::KLTable kl = wmc::kl_point_table(t.field_x, L.spec.kl_sigma, L.spec.kl_corr_len, L.spec.kl_modes);
+        L.d_kl = upload(kl.t);
+    }
     if (L.spec.field == wmc::Field::LognormalKL) {
         const wmc::KLTable kl =
             wmc::kl_cell_table(L.spec.cells_x, L.spec.cells_y, L.spec.kl_sigma, L.spec.kl_corr_len, L.spec.kl_modes);
@@ -1629,7 +1634,7 @@ void solve_batch(wmc_level& L, Workspace& ws, const double* cells, int S, int co
 
 void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S,
                  double* cells, cudaStream_t st) {
-    if (L.spec.field == wmc::Field::LognormalKL)
+    if (L.spec.field == wmc::Field::LognormalKL || L.spec.field == wmc::Field::LognormalKLElem)
         wmc::launch_draw_kl(seed, level, first, count, S, L.tab.n_cells, L.spec.kl_modes, L.d_kl, cells, st);
     else if (L.spec.field == wmc::Field::Kl1D)
         wmc::launch_draw_kl1d(seed, level, first, count, S, L.tab.n_cells, L.tab.field_terms, L.d_field_table, cells,
@@ -1647,7 +1652,7 @@ void launch_draw(const wmc_level& L, std::uint64_t seed, std::uint32_t level, st
 // pair draws its own coefficients from the same stream (rng.cpp:42-89)
 bool per_element_field(const wmc_level& L) {
     return L.spec.field == wmc::Field::Kl1D || L.spec.field == wmc::Field::Jump1D ||
-           L.spec.field == wmc::Field::Channel;
+           L.spec.field == wmc::Field::Channel || L.spec.field == wmc::Field::LognormalKLElem;
 }
 
 void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
@@ -1660,7 +1665,9 @@ void check_pair_compat(const wmc_level* fine, const wmc_level* coarse) {
     if (a.field != b.field) throw ConfigError("eval_pairs: coefficient fields of the pair differ");
     if (per_element_field(*fine)) {
         // one draw per pair, evaluated on each level's own elements
-        if (a.jump_h0 != b.jump_h0 || fine->tab.field_terms != coarse->tab.field_terms)
+        if (a.jump_h0 != b.jump_h0 || fine->tab.field_terms != coarse->tab.field_terms ||
+            (a.field == wmc::Field::LognormalKLElem &&
+             (a.kl_sigma != b.kl_sigma || a.kl_corr_len != b.kl_corr_len || a.kl_modes != b.kl_modes)))
             throw ConfigError("eval_pairs: coefficient fields of the pair differ");
         return;
     }
@@ -2283,9 +2290,12 @@ wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     s.qoi.x1 = desc->qoi_box[1];
     s.qoi.y0 = desc->qoi_box[2];
     s.qoi.y1 = desc->qoi_box[3];
-    if (desc->field != WMC_FIELD_UNIFORM && desc->field != WMC_FIELD_LOGNORMAL_KL)
+    if (desc->field != WMC_FIELD_UNIFORM && desc->field != WMC_FIELD_LOGNORMAL_KL &&
+        desc->field != WMC_FIELD_LOGNORMAL_KL_ELEMENT)
         throw ConfigError("wmc_level_create: unknown coefficient field");
-    s.field = desc->field == WMC_FIELD_LOGNORMAL_KL ? wmc::Field::LognormalKL : wmc::Field::Uniform;
+    s.field = desc->field == WMC_FIELD_LOGNORMAL_KL           ? wmc::Field::LognormalKL
+              : desc->field == WMC_FIELD_LOGNORMAL_KL_ELEMENT ? wmc::Field::LognormalKLElem
+                                                              : wmc::Field::Uniform;
     s.kl_sigma = desc->kl_sigma;
     s.kl_corr_len = desc->kl_corr_len;
     s.kl_modes = desc->kl_modes;
@@ -2302,7 +2312,7 @@ wmc::LevelSpec spec_from_desc(const wmc_level_desc* desc) {
     s.qoi_mean = desc->qoi_mean != 0;
     if (desc->cfl_safety < 0.0 || desc->cfl_safety > 1.0) throw ConfigError("wmc_level_create: cfl_safety in [0, 1]");
     s.cfl_safety = desc->cfl_safety;
-    if (s.field == wmc::Field::LognormalKL &&
+    if ((s.field == wmc::Field::LognormalKL || s.field == wmc::Field::LognormalKLElem) &&
         (s.kl_modes < 1 || s.kl_modes > wmc::kMaxKLModes || !(s.kl_corr_len > 0.0) || !(s.kl_sigma >= 0.0)))
         throw ConfigError("wmc_level_create: KL field needs 1..64 modes, corr_len > 0, sigma >= 0");
     return s;

@@ -54,34 +54,54 @@ double phi(const Mode1D& m, double x) {  // x in [-1/2, 1/2], L2-normalised
 
 }  // namespace
 
-KLTable kl_cell_table(int cells_x, int cells_y, double sigma, double corr_len, int modes) {
-    if (cells_x < 1 || cells_y < 1 || modes < 1 || !(sigma >= 0.0) || !(corr_len > 0.0))
-        throw std::invalid_argument("kl_cell_table: bad parameters");
-    const int n1 = modes + 8;  // enough 1D modes for the largest products
-    const std::vector<Mode1D> m1 = modes_1d(corr_len, n1);
-    struct Pair {
-        int i, j;
-        double lambda;
-    };
-    std::vector<Pair> pairs;
+namespace {
+
+struct Pair2D {
+    int i, j;
+    double lambda;
+};
+
+// the `modes` largest products of 1D eigenvalues (stable order)
+std::vector<Pair2D> largest_pairs(const std::vector<Mode1D>& m1, int modes) {
+    const int n1 = static_cast<int>(m1.size());
+    std::vector<Pair2D> pairs;
     for (int i = 0; i < n1; ++i)
         for (int j = 0; j < n1; ++j) pairs.push_back({i, j, m1[i].lambda * m1[j].lambda});
-    std::stable_sort(pairs.begin(), pairs.end(), [](const Pair& x, const Pair& y) { return x.lambda > y.lambda; });
+    std::stable_sort(pairs.begin(), pairs.end(), [](const Pair2D& x, const Pair2D& y) { return x.lambda > y.lambda; });
     pairs.resize(modes);
+    return pairs;
+}
+
+}  // namespace
+
+KLTable kl_point_table(const std::vector<double>& xy, double sigma, double corr_len, int modes) {
+    if (xy.size() % 2 || modes < 1 || !(sigma >= 0.0) || !(corr_len > 0.0))
+        throw std::invalid_argument("kl_point_table: bad parameters");
+    const std::vector<Mode1D> m1 = modes_1d(corr_len, modes + 8);  // enough 1D modes for the largest products
+    const std::vector<Pair2D> pairs = largest_pairs(m1, modes);
     KLTable t;
-    t.cells = cells_x * cells_y;
+    t.cells = static_cast<int>(xy.size() / 2);
     t.modes = modes;
     t.t.resize(static_cast<std::size_t>(t.cells) * modes);
     for (const auto& p : pairs) t.lambda.push_back(p.lambda);
+    for (int c = 0; c < t.cells; ++c) {
+        const double x = xy[2 * c] - 0.5, y = xy[2 * c + 1] - 0.5;
+        for (int m = 0; m < modes; ++m)
+            t.t[static_cast<std::size_t>(c) * modes + m] =
+                sigma * std::sqrt(pairs[m].lambda) * phi(m1[pairs[m].i], x) * phi(m1[pairs[m].j], y);
+    }
+    return t;
+}
+
+KLTable kl_cell_table(int cells_x, int cells_y, double sigma, double corr_len, int modes) {
+    if (cells_x < 1 || cells_y < 1) throw std::invalid_argument("kl_cell_table: bad parameters");
+    std::vector<double> xy;
     for (int iy = 0; iy < cells_y; ++iy)
         for (int ix = 0; ix < cells_x; ++ix) {
-            const double x = (ix + 0.5) / cells_x - 0.5, y = (iy + 0.5) / cells_y - 0.5;
-            const int cell = iy * cells_x + ix;
-            for (int m = 0; m < modes; ++m)
-                t.t[static_cast<std::size_t>(cell) * modes + m] =
-                    sigma * std::sqrt(pairs[m].lambda) * phi(m1[pairs[m].i], x) * phi(m1[pairs[m].j], y);
+            xy.push_back((ix + 0.5) / cells_x);
+            xy.push_back((iy + 0.5) / cells_y);
         }
-    return t;
+    return kl_point_table(xy, sigma, corr_len, modes);
 }
 
 }  // namespace wmc

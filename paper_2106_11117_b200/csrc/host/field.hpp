@@ -25,4 +25,9 @@ struct KLTable {
 
 KLTable kl_cell_table(int cells_x, int cells_y, double sigma, double corr_len, int modes);
 
+// The same expansion at arbitrary points of the unit square (xy interleaved,
+// one table row per point): the per-element field, evaluated at every
+// triangle's centroid as the reference's assemble does (src/fem.cpp:103-104).
+KLTable kl_point_table(const std::vector<double>& xy, double sigma, double corr_len, int modes);
+
 }  // namespace wmc

@@ -101,6 +101,7 @@ std::vector<int> lattice_block(const TriMesh& mesh, const LevelSpec& spec, const
         L.lattice_reason = why;
         return std::vector<int>{};
     };
+    if (spec.field == Field::LognormalKLElem) return fail("per-element coefficient");
     if (mesh.fine_box_lo < 0 || mesh.lattice.size() != mesh.vertices.size()) return fail("no refined box");
     const int qa = mesh.fine_box_lo, m = mesh.fine_box_hi - mesh.fine_box_lo;
     if (m < 4) return fail("refined box too small");
@@ -232,11 +233,13 @@ static Geometry geometry_2d(const TriMesh& mesh, const LevelSpec& spec, LevelTab
     if (spec.cells_x < 1 || spec.cells_y < 1) throw std::invalid_argument("level: coefficient grid");
     if (spec.final_time <= 0.0 || spec.dt <= 0.0) throw std::invalid_argument("level: T and dt must be positive");
     if (spec.substeps < 1) throw std::invalid_argument("level: substeps >= 1");
-    if (spec.cells_x * spec.cells_y > 32767) throw std::invalid_argument("level: at most 32767 coefficient cells");
+    const bool per_elem = spec.field == Field::LognormalKLElem;
+    if (!per_elem && spec.cells_x * spec.cells_y > 32767)
+        throw std::invalid_argument("level: at most 32767 coefficient cells");
 
     const int nv = mesh.n_vertices();
     const int nt = mesh.n_triangles();
-    L.n_cells = spec.cells_x * spec.cells_y;
+    L.n_cells = per_elem ? nt : spec.cells_x * spec.cells_y;
 
     Geometry g;
     g.nv = nv;
@@ -254,8 +257,12 @@ static Geometry geometry_2d(const TriMesh& mesh, const LevelSpec& spec, LevelTab
         const double area = mesh.signed_area(t);
         if (!(area > 0.0)) throw std::runtime_error("level: nonpositive triangle area");
         const auto cc = mesh.centroid(t);
-        const int k = spec.cell_of(cc[0], cc[1]);
+        const int k = per_elem ? t : spec.cell_of(cc[0], cc[1]);
         L.elem_cell[t] = k;
+        if (per_elem) {  // the field's evaluation points (capi: kl_point_table)
+            L.field_x.push_back(cc[0]);
+            L.field_x.push_back(cc[1]);
+        }
         const double gx[3] = {(p1[1] - p2[1]) / (2.0 * area), (p2[1] - p0[1]) / (2.0 * area),
                               (p0[1] - p1[1]) / (2.0 * area)};
         const double gy[3] = {(p2[0] - p1[0]) / (2.0 * area), (p0[0] - p2[0]) / (2.0 * area),

@@ -39,7 +39,9 @@ struct QoIBox {
 // (BASELINE); Kl1D / Jump1D: the reference's 1D experiment fields
 // (rng.cpp:42-89), one coefficient per element; Channel: the narrow-channel
 // experiment's per-sample geometry (channel.hpp), one cell per moving entry
-enum class Field : int { Uniform = 0, LognormalKL = 1, Kl1D = 2, Jump1D = 3, Channel = 4 };
+// LognormalKLElem: the KL field at every triangle's centroid (one coefficient
+// cell per element, as the reference's assemble evaluates it, fem.cpp:103-104)
+enum class Field : int { Uniform = 0, LognormalKL = 1, Kl1D = 2, Jump1D = 3, Channel = 4, LognormalKLElem = 5 };
 
 struct LevelSpec {
     int cells_x = 4, cells_y = 4;  // coefficient grid on the domain box, cell k = iy*cells_x + ix

@@ -175,8 +175,12 @@ __global__ void __launch_bounds__(kKLThreads) draw_kl_kernel(std::uint64_t seed,
     __shared__ double xi_s[kKLMaxModes][kKLThreads];
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= S) return;
+    // blockIdx.y: a chunk of the cells (per-element fields have one cell per
+    // triangle; every chunk's CTA forms the sample's normals again)
+    const int per = (n_cells + gridDim.y - 1) / gridDim.y;
+    const int k_lo = blockIdx.y * per, k_hi = min(n_cells, k_lo + per);
     if (s >= count) {
-        for (int k = 0; k < n_cells; ++k) cells[k * S + s] = 1.0;
+        for (int k = k_lo; k < k_hi; ++k) cells[static_cast<std::size_t>(k) * S + s] = 1.0;
         return;
     }
     std::uint64_t key = mix64(seed);
@@ -193,10 +197,10 @@ __global__ void __launch_bounds__(kKLThreads) draw_kl_kernel(std::uint64_t seed,
         xi_s[2 * i][threadIdx.x] = r * cos(th);
         if (2 * i + 1 < modes) xi_s[2 * i + 1][threadIdx.x] = r * sin(th);
     }
-    for (int k = 0; k < n_cells; ++k) {
+    for (int k = k_lo; k < k_hi; ++k) {
         double g = 0.0;
-        for (int m = 0; m < modes; ++m) g += __ldg(table + k * modes + m) * xi_s[m][threadIdx.x];
-        cells[k * S + s] = exp(g);
+        for (int m = 0; m < modes; ++m) g += __ldg(table + static_cast<std::size_t>(k) * modes + m) * xi_s[m][threadIdx.x];
+        cells[static_cast<std::size_t>(k) * S + s] = exp(g);
     }
 }
 
@@ -2684,7 +2688,9 @@ void launch_moments(const double* dq, const double* q, int count, double* out, v
 
 void launch_draw_kl(std::uint64_t seed, std::uint32_t level, std::uint64_t first, int count, int S, int n_cells,
                     int modes, const double* table, double* cells, void* stream) {
-    draw_kl_kernel<<<(S + kKLThreads - 1) / kKLThreads, kKLThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+    // 256 cells per CTA (the normals cost about as much as 32 cells)
+    const dim3 grid((S + kKLThreads - 1) / kKLThreads, std::max(1, std::min(65535, (n_cells + 255) / 256)));
+    draw_kl_kernel<<<grid, kKLThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         seed, level, first, count, S, n_cells, modes, table, cells);
 }
 

@@ -345,11 +345,26 @@ __global__ void __launch_bounds__(kT, 512 / kT) tile_step_kernel(TileArgs a) {
         for (int u = tid; u < ng; u += kT) {
             const int r = gb + u;
             B0[__ldg(a.g_slot + r)] = __ldg(zc + zbase + __ldg(a.g_dof + r)) * __ldg(a.g_rs + r);
-            for (int e = __ldg(a.g_ent_off + r); e < __ldg(a.g_ent_off + r + 1); ++e) {
-                double w = 0.0;
-                for (int t = __ldg(a.e_rc_off + e); t < __ldg(a.e_rc_off + e + 1); ++t)
-                    w += cl[__ldg(a.rc_cell + t)] * __ldg(a.rc_a0 + t);
+        }
+        // the weights entry by entry (a thread per entry: the index loads of a
+        // warp are consecutive, and two entries' loads are in flight at once)
+        {
+            const int ee = __ldg(a.g_ent_off + gb + ng);
+            for (int e = eb + tid; e < ee; e += 2 * kT) {
+                const int e2 = e + kT;
+                const bool two = e2 < ee;
+                const int t0 = __ldg(a.e_rc_off + e), t1 = __ldg(a.e_rc_off + e + 1);
+                const int u0 = two ? __ldg(a.e_rc_off + e2) : 0, u1 = two ? __ldg(a.e_rc_off + e2 + 1) : 0;
+                double w = 0.0, w2 = 0.0;
+                for (int t = t0, u = u0; t < t1 || u < u1; ++t, ++u) {
+                    const bool pa = t < t1, pb = u < u1;
+                    const int ca = pa ? __ldg(a.rc_cell + t) : 0, cb = pb ? __ldg(a.rc_cell + u) : 0;
+                    const double xa = pa ? __ldg(a.rc_a0 + t) : 0.0, xb = pb ? __ldg(a.rc_a0 + u) : 0.0;
+                    if (pa) w += cl[ca] * xa;
+                    if (pb) w2 += cl[cb] * xb;
+                }
                 wbuf[e - eb] = w;
+                if (two) wbuf[e2 - eb] = w2;
             }
         }
         __syncthreads();
