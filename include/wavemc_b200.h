@@ -262,6 +262,10 @@ int wmc_synchronize(wmc_level* level, wmc_error* err);
 /* KL table of the log-normal field: table[cell * modes + m] =
  * sigma sqrt(lambda_m) phi_m(centre of cell), lambda[m] (unit variance). */
 int wmc_kl_table(int cells_x, int cells_y, double sigma, double corr_len, int modes, double* table, double* lambda);
+/* The expansion's modes for a pointwise evaluator (WMC_FIELD_LOGNORMAL_KL_ELEMENT on the reference side,
+   where speed2(x, y) is a callable, src/fem.cpp:91-104): out[7 m ..] = amp, omega_x, even_x, norm_x, omega_y,
+   even_y, norm_y; mode m is amp * phi_x(x) * phi_y(y), phi(t) = (even ? cos : sin)(omega (t - 1/2)) / norm. */
+int wmc_kl_modes(double sigma, double corr_len, int modes, double* out);
 
 /* The level's per-sample cell coefficients for indices first..first+count-1,
  * out[i * n_cells + k], exactly as the solves use them. */

@@ -400,6 +400,22 @@ def config4(ref, tmp, specs=None, model_cost=None):
     tight["eps"] = CONFIG4_TIGHT_EPS
     kl_adaptive["tight"] = tight
     dump("config4_adaptive.json", kl_adaptive)
+    # the field at every triangle's centroid: the reference's assemble calls
+    # speed2(x, y) = exp(g(x, y)) itself (fem.cpp:103-104), g from the shared mode list
+    modes = wavemc.kl_modes(kl["sigma"], kl["corr_len"], kl["modes"])
+    mpath = os.path.join(tmp, "kl_modes.txt")
+    with open(mpath, "w") as f:
+        f.write(f"{modes.shape[0]}\n")
+        f.write("\n".join(repr(float(v)) for v in modes.ravel()))
+        f.write("\n")
+    elargs = {"kl-modes": mpath}
+    el = {"pairs": ref.mlmc(specs[:3], [4, 3, 2], per_sample=True, **elargs)}
+    el["adaptive"] = ref.adaptive(specs, configs.CONFIG4_EPS, **elargs)
+    el["adaptive"]["eps"] = configs.CONFIG4_EPS
+    el["tight"] = ref.adaptive(specs, CONFIG4_TIGHT_EPS, **elargs)
+    el["tight"]["eps"] = CONFIG4_TIGHT_EPS
+    el["model_cost"] = model_cost
+    dump("config4_element.json", el)
 
 
 if __name__ == "__main__":

@@ -92,6 +92,10 @@ struct ProblemDef {
     double box_x0 = 0.7, box_x1 = 0.9, box_y0 = 0.4, box_y1 = 0.6;
     std::vector<double> kl;  // log-normal KL table [cell * kl_modes + m] (empty: uniform cells)
     int kl_modes = 0;
+    // pointwise log-normal KL (per-element field): mode m is amp * phi_x(x) * phi_y(y) with
+    // phi(t) = (even ? cos : sin)(omega (t - 1/2)) / norm; rows of 7 numbers
+    // (amp, omega_x, even_x, norm_x, omega_y, even_y, norm_y), from wmc_kl_modes
+    std::vector<double> klp;
     double dom_x0 = 0.0, dom_x1 = 1.0, dom_y0 = 0.0, dom_y1 = 1.0;  // coefficient grid extent
     bool qoi_mean = false;   // Q = mean over the box
     double cfl = 0.0;        // > 0: per-sample dt = cfl-scaled stable step (experiments.cpp:30-43)
@@ -141,7 +145,29 @@ ProblemDef problem_from(const Args& a) {
         for (double& v : d.kl) in >> v;
         if (!in) throw ConfigError("kl-table: truncated");
     }
+    const std::string klm = a.get("kl-modes");
+    if (!klm.empty()) {  // "<modes>" then 7 numbers per mode
+        std::ifstream in(klm);
+        in >> d.kl_modes;
+        if (!in || d.kl_modes < 1) throw ConfigError("kl-modes: bad header");
+        d.klp.resize(static_cast<std::size_t>(7) * d.kl_modes);
+        for (double& v : d.klp) in >> v;
+        if (!in) throw ConfigError("kl-modes: truncated");
+    }
     return d;
+}
+
+// g(x, y) of the pointwise KL field for the normals xi
+double kl_point_value(const ProblemDef& d, const std::vector<double>& xi, double x, double y) {
+    auto phi = [](double omega, double even, double norm, double t) {
+        return (even != 0.0 ? std::cos(omega * t) : std::sin(omega * t)) / norm;
+    };
+    double g = 0.0;
+    for (int m = 0; m < d.kl_modes; ++m) {
+        const double* r = d.klp.data() + 7 * m;
+        g += (r[0] * phi(r[1], r[2], r[3], x - 0.5) * phi(r[4], r[5], r[6], y - 0.5)) * xi[m];
+    }
+    return g;
 }
 
 // one level: mesh + interior restriction + sample-independent data
@@ -259,7 +285,7 @@ Level make_level(const ProblemDef& d, const std::string& mesh_path, double dt, i
 
 std::vector<double> draw_cells(const ProblemDef& d, RngStream& stream) {
     std::vector<double> c(d.cells_x * d.cells_y);
-    if (d.kl.empty()) {
+    if (d.kl.empty() && d.klp.empty()) {
         for (double& v : c) v = stream.next_uniform(d.coef_lo, d.coef_hi);
         return c;
     }
@@ -273,6 +299,7 @@ std::vector<double> draw_cells(const ProblemDef& d, RngStream& stream) {
         xi[2 * i] = r * std::cos(th);
         if (2 * i + 1 < d.kl_modes) xi[2 * i + 1] = r * std::sin(th);
     }
+    if (!d.klp.empty()) return xi;  // pointwise field: the sample is its normals (solve_level evaluates g)
     for (std::size_t k = 0; k < c.size(); ++k) {
         double g = 0.0;
         for (int m = 0; m < d.kl_modes; ++m) g += d.kl[k * d.kl_modes + m] * xi[m];
@@ -282,8 +309,10 @@ std::vector<double> draw_cells(const ProblemDef& d, RngStream& stream) {
 }
 
 double solve_level(const ProblemDef& d, const Level& lv, const std::vector<double>& cells, CostRecord* cost) {
+    // the reference evaluates the squared speed at every triangle's centroid (fem.cpp:103-104)
     const DiscreteOperator full =
-        assemble(lv.mesh, [&](double x, double y) { return cells[cell_of(d, x, y)]; });
+        d.klp.empty() ? assemble(lv.mesh, [&](double x, double y) { return cells[cell_of(d, x, y)]; })
+                      : assemble(lv.mesh, [&](double x, double y) { return std::exp(kl_point_value(d, cells, x, y)); });
     const DiscreteOperator op = interior_operator(lv, full);
     RunOptions options;
     options.kind = d.kind;

@@ -128,6 +128,7 @@ SIGNATURES = [
     ("wmc_level_stream", _VP, [_VP]),
     ("wmc_synchronize", C.c_int, [_VP, P(Error)]),
     ("wmc_kl_table", C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _DP, _DP]),
+    ("wmc_kl_modes", C.c_int, [C.c_double, C.c_double, C.c_int, _DP]),
     ("wmc_level_draw", C.c_int, [_VP, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, _DP]),
     ("wmc_level_cfl", C.c_int, [_VP, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, P(C.c_double), P(C.c_long)]),
     ("wmc_draw_cells", C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, C.c_double, C.c_double,

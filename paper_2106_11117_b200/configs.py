@@ -120,14 +120,16 @@ def build_mesh(d: LevelDef):
     return Mesh.build_square(d.n_coarse, d.ratio, FINE_LO, FINE_HI, SNAP)
 
 
-def level_spec(d: LevelDef, device: int = 0, batch: int = 0, kl: bool = False):
+def level_spec(d: LevelDef, device: int = 0, batch: int = 0, kl=False):
+    """kl: False (uniform cells), True (config 4 on the KL cell grid) or
+    "element" (config 4 with the field at every triangle's centroid)."""
     from .wavemc import LevelSpec
     if kl:
-        from ._native import WMC_FIELD_LOGNORMAL_KL
+        from ._native import WMC_FIELD_LOGNORMAL_KL, WMC_FIELD_LOGNORMAL_KL_ELEMENT
         return LevelSpec(dt=d.dt, substeps=d.substeps, integrator=d.integrator, final_time=d.final_time,
                          device=device, batch=batch, cells_x=KL_FIELD["cells"][0], cells_y=KL_FIELD["cells"][1],
-                         field=WMC_FIELD_LOGNORMAL_KL, kl_sigma=KL_FIELD["sigma"], kl_corr_len=KL_FIELD["corr_len"],
-                         kl_modes=KL_FIELD["modes"])
+                         field=WMC_FIELD_LOGNORMAL_KL_ELEMENT if kl == "element" else WMC_FIELD_LOGNORMAL_KL,
+                         kl_sigma=KL_FIELD["sigma"], kl_corr_len=KL_FIELD["corr_len"], kl_modes=KL_FIELD["modes"])
     if d.shape == "lshape":
         c = CONFIG2_PROBLEM
         return LevelSpec(dt=d.dt, substeps=d.substeps, integrator=d.integrator, final_time=d.final_time,
@@ -137,6 +139,6 @@ def level_spec(d: LevelDef, device: int = 0, batch: int = 0, kl: bool = False):
                      batch=batch)
 
 
-def build_level(d: LevelDef, device: int = 0, batch: int = 0, kl: bool = False):
+def build_level(d: LevelDef, device: int = 0, batch: int = 0, kl=False):
     from .wavemc import Level
     return Level(build_mesh(d), level_spec(d, device, batch, kl))

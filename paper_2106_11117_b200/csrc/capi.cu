@@ -157,6 +157,7 @@ struct wmc_level {
     SubPath path = SubPath::None;
     int* d_apg_ptr = nullptr;
     int* d_apg_ent = nullptr;
+    int* d_apg_cell = nullptr;
     double* d_apg_a0 = nullptr;
     // temporally blocked step on R (SubPath::Tiled, host/tiles.hpp)
     wmc::TileArgs tile{};          // static part of the kernel arguments
@@ -258,7 +259,7 @@ struct wmc_level {
                         (void*)d_strip_j0, (void*)d_lat_smask, (void*)d_strip_len, (void*)d_cellx, (void*)d_celly, (void*)d_gen_rows,
                         (void*)d_gen_rs, (void*)d_gen_soff, (void*)d_gen_warp_slice, (void*)d_gen_col, (void*)d_slot_rc, (void*)d_slot_a0,
                         (void*)d_slot_cell, (void*)d_ovf_cell, (void*)d_grc_cell,
-                        (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_a0,
+                        (void*)d_grc_a0, (void*)d_kl, (void*)d_field_x, (void*)d_field_table, (void*)d_apg_ptr, (void*)d_apg_ent, (void*)d_apg_cell, (void*)d_apg_a0,
                         (void*)d_rem_ptr, (void*)d_rem_col, (void*)d_rem_cell, (void*)d_rem_a0, (void*)d_ns_rows,
                         (void*)d_cell_ix})
             if (p) cudaFree(p);
@@ -528,9 +529,23 @@ void build_device_level(wmc_level& L) {
     const char* force_path = std::getenv("WMC_SUBSTEP_PATH");
     const std::string fp = force_path ? force_path : "";
     L.n_wid = static_cast<int>(t.rc_ptr.size()) - 1;
-    const bool onchip_fits = t.n_r <= wmc::kSubThreads * wmc::kSubMaxRpt && t.n_r < 65536 && L.n_wid < 65535;
-    if (lts && t.n_cells > wmc::kMaxCells && (t.tiers > 1 || fp == "global" || !onchip_fits))
-        throw ConfigError("level: the HBM-resident substep paths support at most 511 coefficient cells");
+    const bool onchip_rows = t.n_r <= wmc::kSubThreads * wmc::kSubMaxRpt && t.n_r < 65536 && L.n_wid < 65535;
+    // (one weight per SELL entry and sample on chip: per-element fields on a
+    // large R leave no room for the substep state; they take the HBM-resident
+    // substeps, whose entries then carry their cells in a separate array)
+    const bool onchip_fits = onchip_rows && 8.0 * L.n_wid + 16.0 * t.n_r < 200.0 * 1024.0;
+    if (lts && t.n_cells > wmc::kMaxCells && t.tiers > 1)
+        throw ConfigError("level: nested tiers support at most 511 coefficient cells");
+    auto upload_global = [&] {  // tables of the HBM-resident substeps
+        L.d_apg_ptr = upload(t.apg_ptr);
+        if (t.n_cells > wmc::kMaxCells) {
+            L.d_apg_ent = upload(t.apg_col);
+            L.d_apg_cell = upload(t.apg_cell);
+        } else {
+            L.d_apg_ent = upload(t.apg_ent);
+        }
+        L.d_apg_a0 = upload(t.apg_a0);
+    };
     if (lts && t.tiers > 1) {
         // nested tiers: HBM-resident stage kernels
         if (t.tiers > wmc::kMaxTiers) throw ConfigError("level: too many tiers");
@@ -669,11 +684,7 @@ void build_device_level(wmc_level& L) {
                 L.tile_ctas_per_sm = std::max(1, std::min(512 / wmc::kTileThreads, smem_per_sm / (L.tile_smem + 1024)));
             }
         }
-        if (L.path == SubPath::Global) {
-            L.d_apg_ptr = upload(t.apg_ptr);
-            L.d_apg_ent = upload(t.apg_ent);
-            L.d_apg_a0 = upload(t.apg_a0);
-        }
+        if (L.path == SubPath::Global) upload_global();
     }
     if (lts && L.path != SubPath::Global && L.path != SubPath::Tiers && L.path != SubPath::Tiled) {
         const int n_slices = (t.n_r + 31) / 32;
@@ -921,8 +932,13 @@ void build_device_level(wmc_level& L) {
     }
     if (lts && L.path == SubPath::None) {
         L.path = (L.lattice && fp != "onchip") ? SubPath::Lattice : SubPath::OnChip;
-        if (L.path == SubPath::OnChip && L.sub_grid <= 0)
-            throw ConfigError("level: substep working set exceeds shared memory");
+        if (L.path == SubPath::OnChip && L.sub_grid <= 0) {
+            // the SELL of R does not fit one SM (per-element coefficients: every
+            // entry its own weight): the HBM-resident substeps instead
+            if (t.n > wmc::kColMask) throw ConfigError("level: substep working set exceeds shared memory");
+            L.path = SubPath::Global;
+            upload_global();
+        }
     }
     L.lattice = L.path == SubPath::Lattice;
     {
@@ -1395,6 +1411,7 @@ void solve_batch_launches(wmc_level& L, Workspace& ws, const double* cells, int 
             ga.count = count;
             ga.ptr = L.d_apg_ptr;
             ga.ent = L.d_apg_ent;
+            ga.cell_ix = L.d_apg_cell;
             ga.a0 = L.d_apg_a0;
             ga.cells = cells;
             ga.g = ws.g;
@@ -2713,6 +2730,15 @@ int wmc_kl_table(int cells_x, int cells_y, double sigma, double corr_len, int mo
         const wmc::KLTable kl = wmc::kl_cell_table(cells_x, cells_y, sigma, corr_len, modes);
         if (table) std::copy(kl.t.begin(), kl.t.end(), table);
         if (lambda) std::copy(kl.lambda.begin(), kl.lambda.end(), lambda);
+    });
+}
+
+int wmc_kl_modes(double sigma, double corr_len, int modes, double* out) {
+    return guarded([&] {
+        if (!out) throw ConfigError("wmc_kl_modes: NULL argument");
+        if (modes > wmc::kMaxKLModes) throw ConfigError("wmc_kl_modes: at most 64 modes");
+        const std::vector<double> v = wmc::kl_mode_list(sigma, corr_len, modes);
+        std::copy(v.begin(), v.end(), out);
     });
 }
 

@@ -46,10 +46,12 @@ std::vector<Mode1D> modes_1d(double corr_len, int count) {
     return out;
 }
 
-double phi(const Mode1D& m, double x) {  // x in [-1/2, 1/2], L2-normalised
+double phi_norm(const Mode1D& m) {
     const double a = 0.5, w = m.omega;
-    if (m.even) return std::cos(w * x) / std::sqrt(a + std::sin(2.0 * w * a) / (2.0 * w));
-    return std::sin(w * x) / std::sqrt(a - std::sin(2.0 * w * a) / (2.0 * w));
+    return m.even ? std::sqrt(a + std::sin(2.0 * w * a) / (2.0 * w)) : std::sqrt(a - std::sin(2.0 * w * a) / (2.0 * w));
+}
+double phi(const Mode1D& m, double x) {  // x in [-1/2, 1/2], L2-normalised
+    return (m.even ? std::cos(m.omega * x) : std::sin(m.omega * x)) / phi_norm(m);
 }
 
 }  // namespace
@@ -91,6 +93,19 @@ KLTable kl_point_table(const std::vector<double>& xy, double sigma, double corr_
                 sigma * std::sqrt(pairs[m].lambda) * phi(m1[pairs[m].i], x) * phi(m1[pairs[m].j], y);
     }
     return t;
+}
+
+std::vector<double> kl_mode_list(double sigma, double corr_len, int modes) {
+    if (modes < 1 || !(sigma >= 0.0) || !(corr_len > 0.0)) throw std::invalid_argument("kl_mode_list: bad parameters");
+    const std::vector<Mode1D> m1 = modes_1d(corr_len, modes + 8);
+    const std::vector<Pair2D> pairs = largest_pairs(m1, modes);
+    std::vector<double> out;
+    for (const auto& p : pairs) {
+        const Mode1D &mx = m1[p.i], &my = m1[p.j];
+        out.insert(out.end(), {sigma * std::sqrt(p.lambda), mx.omega, mx.even ? 1.0 : 0.0, phi_norm(mx), my.omega,
+                               my.even ? 1.0 : 0.0, phi_norm(my)});
+    }
+    return out;
 }
 
 KLTable kl_cell_table(int cells_x, int cells_y, double sigma, double corr_len, int modes) {

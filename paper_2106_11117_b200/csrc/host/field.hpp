@@ -30,4 +30,9 @@ KLTable kl_cell_table(int cells_x, int cells_y, double sigma, double corr_len, i
 // triangle's centroid as the reference's assemble does (src/fem.cpp:103-104).
 KLTable kl_point_table(const std::vector<double>& xy, double sigma, double corr_len, int modes);
 
+// The expansion's modes for a pointwise evaluator (the reference-side driver):
+// 7 numbers per mode -- amp = sigma sqrt(lambda_m), then omega, even (1 / 0)
+// and norm of the x and of the y factor, phi(t) = (even ? cos : sin)(omega (t - 1/2)) / norm.
+std::vector<double> kl_mode_list(double sigma, double corr_len, int modes);
+
 }  // namespace wmc

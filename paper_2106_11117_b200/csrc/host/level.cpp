@@ -458,14 +458,20 @@ static LevelTables finish_tables(Geometry& g, const LevelSpec& spec, LevelTables
             L.apg_col_bits = 0;  // no packed form (the HBM-resident paths refuse such levels)
     }
     L.apg_ptr.assign(L.n_r + 1, 0);
-    for (int i = 0; i < L.n_r && L.apg_col_bits > 0; ++i) {
+    const bool apg_unpacked = L.n_cells > 511;  // the HBM-resident substep kernel reads (column, cell) apart
+    for (int i = 0; i < L.n_r && (L.apg_col_bits > 0 || apg_unpacked); ++i) {
         for (const auto& [j, k, a] : rows[i]) {
             if (!L.in_p[j]) continue;
-            L.apg_ent.push_back(static_cast<int>(static_cast<unsigned>(j) |
-                                                 (static_cast<unsigned>(k) << L.apg_col_bits)));
+            if (L.apg_col_bits > 0)
+                L.apg_ent.push_back(static_cast<int>(static_cast<unsigned>(j) |
+                                                     (static_cast<unsigned>(k) << L.apg_col_bits)));
+            if (apg_unpacked) {
+                L.apg_col.push_back(j);
+                L.apg_cell.push_back(k);
+            }
             L.apg_a0.push_back(a);
         }
-        L.apg_ptr[i + 1] = static_cast<int>(L.apg_ent.size());
+        L.apg_ptr[i + 1] = static_cast<int>(L.apg_a0.size());
     }
 
     // nested tiers: A P_k on R_k rows, parts form

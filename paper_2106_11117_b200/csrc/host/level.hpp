@@ -109,6 +109,7 @@ struct LevelTables {
     // A P on R rows as sweep-style parts (col | cell << apg_col_bits, a0):
     // the HBM-resident substep path for sets R too large for one SM
     std::vector<int> apg_ptr, apg_ent;
+    std::vector<int> apg_col, apg_cell;  // the same entries unpacked (levels with more than 511 cells)
     std::vector<double> apg_a0;
     int apg_col_bits = 23;
 

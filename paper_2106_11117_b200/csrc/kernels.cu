@@ -872,8 +872,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32, WMC_GSUB_MINB) global_subste
             for (int q = b; q < e; ++q) {
                 const int pk = __ldg(a.ent + q);
                 const double w = __ldg(a.a0 + q);
-                const int j = pk & kColMask;
-                const int cell = static_cast<unsigned>(pk) >> kColBits;
+                const int j = a.cell_ix ? pk : pk & kColMask;
+                const int cell = a.cell_ix ? __ldg(a.cell_ix + q) : static_cast<int>(static_cast<unsigned>(pk) >> kColBits);
                 const double2 cc = __ldg(reinterpret_cast<const double2*>(a.cells + cell * S + s0));
                 const double2 v = ld(src, j);
                 acc0 += (cc.x * w) * v.x;

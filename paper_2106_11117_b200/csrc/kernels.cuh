@@ -172,6 +172,8 @@ struct GSubArgs {
     int n_r, S, count;
     const int* ptr;
     const int* ent;       // col | cell << kColBits, columns in P
+    const int* cell_ix;   // not NULL: ent holds the column alone and the cell is cell_ix[entry]
+                          // (levels with more than kMaxCells coefficient cells: per-element fields)
     const double* a0;
     const double* cells;
     const double* g;      // [r][S]

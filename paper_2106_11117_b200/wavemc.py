@@ -341,6 +341,13 @@ def synchronize(level: Level) -> None:
     N.check(N.lib().wmc_synchronize(level._h, C.byref(err)), err)
 
 
+def kl_modes(sigma: float, corr_len: float, modes: int):
+    """The KL expansion's modes for a pointwise evaluator (wmc_kl_modes): [modes, 7]."""
+    out = np.empty((modes, 7), np.float64)
+    N.check(N.lib().wmc_kl_modes(sigma, corr_len, modes, _dptr(out)))
+    return out
+
+
 def kl_table(cells_x: int, cells_y: int, sigma: float, corr_len: float, modes: int):
     """(table[cell, mode], lambda[mode]) of the log-normal KL field."""
     table = np.empty((cells_x * cells_y, modes), np.float64)

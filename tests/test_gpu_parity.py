@@ -388,6 +388,36 @@ def test_config4_adaptive_mlmc_matches_reference(golden, target):
         assert got["variance"] == pytest.approx(want["variance"], rel=MOMENT_RTOL)
 
 
+def _kl_element_levels(n=5):
+    return [configs.build_level(d, kl="element") for d in configs.config4()[:n]]
+
+
+def test_config4_element_field_pairs_match_reference(golden):
+    """Config 4 with the KL field at every triangle's centroid -- the rule of
+    the reference's assemble (src/fem.cpp:103-104), which calls
+    speed2(x, y) = exp(g(x, y)) itself on its side: one draw per pair, each
+    level on its own elements."""
+    levels = _kl_element_levels(3)
+    assert all(lv.info["lattice"] == 0 for lv in levels)  # one coefficient per triangle: generic kernels
+    for lv in golden("config4_element.json")["pairs"]["levels"]:
+        l, n = lv["level"], lv["N"]
+        dq, qf, _ = wavemc.eval_pairs(levels[l], levels[l - 1] if l else None, 0, l, 0, n)
+        assert per_sample_rel(qf, lv["q"]) < QOI_RTOL, l
+        assert np.max(np.abs(dq - lv["dq"]) / np.abs(lv["q"])) < 2 * QOI_RTOL, l
+
+
+@pytest.mark.parametrize("target", ["adaptive", "tight"])
+def test_config4_element_field_adaptive_mlmc_matches_reference(golden, target):
+    g0 = golden("config4_element.json")
+    g = g0[target]
+    res = wavemc.run_mlmc(_kl_element_levels(), g0["model_cost"], wavemc.MlmcConfig(eps=g["eps"]))
+    assert res.converged == g["converged"]
+    assert [lv["n_samples"] for lv in res.levels] == [lv["N"] for lv in g["levels"]]
+    assert res.estimate == pytest.approx(g["estimate"], rel=MOMENT_RTOL)
+    for got, want in zip(res.levels, g["levels"]):
+        assert got["variance"] == pytest.approx(want["variance"], rel=MOMENT_RTOL)
+
+
 def test_adaptive_driver_evaluate_ahead_is_invisible(monkeypatch):
     """The driver's evaluate-ahead cache (64-lane granules, next level's
     warm-up beside the current wave) folds exactly the reference's samples:
