@@ -58,6 +58,8 @@ def parse():
                     help="config 1: lf = the global leap-frog comparison arm (dt = 0.2 h_min on every level); "
                          "the line then carries the measured LF / LTS time ratios")
     ap.add_argument("--eps", type=float, default=None, help="config 4: RMSE target (default BASELINE 1e-3)")
+    ap.add_argument("--field", default="cells", choices=["cells", "element"],
+                    help="config 4: KL field on the 32 x 32 cell grid, or at every triangle's centroid")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     return ap.parse_args()
@@ -185,7 +187,7 @@ def workload(config: int, integrator: str = "lts"):
 # process (tools/dump_inputs.py) so the timed reference arm never maps the
 # product library.
 
-def dump_inputs(config: int, final_time=None, lf=False, kl=False) -> dict:
+def dump_inputs(config: int, final_time=None, lf=False, kl=False, kl_element=False) -> dict:
     tmp = tempfile.mkdtemp(prefix="wmc_inputs_")
     cmd = [sys.executable, os.path.join(ROOT, "tools", "dump_inputs.py"), "--config", str(config), "--out", tmp]
     if final_time is not None:
@@ -194,6 +196,8 @@ def dump_inputs(config: int, final_time=None, lf=False, kl=False) -> dict:
         cmd.append("--lf")
     if kl:
         cmd.append("--kl")
+    if kl_element:
+        cmd.append("--kl-element")
     subprocess.run(cmd, check=True, capture_output=True, text=True)
     inp = load_json(os.path.join(tmp, "inputs.json"))
     inp["dir"] = tmp
@@ -744,7 +748,7 @@ def adaptive_arm(args, world, rank, local):
             return 0
         import oracle_py
         threads = os.cpu_count() or 1
-        inp = dump_inputs(4, kl=True)
+        inp = dump_inputs(4, kl=True, kl_element=args.field == "element")
         specs = [(lv["mesh"], lv["dt"], lv["p"]) for lv in inp["levels"]]
         runs = [oracle_py.RefDriver().adaptive(specs, eps, threads=threads, **inp["kl"])
                 for _ in range(args.warmup + args.steps)][args.warmup:]
@@ -755,7 +759,8 @@ def adaptive_arm(args, world, rank, local):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (counter-based RNG, Box-Muller KL weights, seed 0)",
-                "config": {"workload": f"BASELINE config 4: adaptive MLMC to RMSE {eps}, log-normal KL", "eps": eps},
+                "config": {"workload": f"BASELINE config 4: adaptive MLMC to RMSE {eps}, log-normal KL"
+                                       + (" at the element centroids" if args.field == "element" else ""), "eps": eps},
                 "cpu_baseline": {"value": sec, "unit": "s", "cores": threads, "kind": "reference",
                                  "cpu_model": ci["cpu_model"],
                                  "sample": f"full adaptive run, reference run_mlmc, {threads} threads"},
@@ -766,7 +771,7 @@ def adaptive_arm(args, world, rank, local):
     import torch
     from paper_2106_11117_b200 import wavemc
     torch.cuda.set_device(local)
-    levels = [configs.build_level(d, device=local, kl=True) for d in defs]
+    levels = [configs.build_level(d, device=local, kl="element" if args.field == "element" else True) for d in defs]
     costs = [lv.info["dof_updates_per_solve"] for lv in levels]
     for _ in range(args.warmup):
         wavemc.run_mlmc(levels, costs, wavemc.MlmcConfig(eps=eps))
@@ -784,7 +789,8 @@ def adaptive_arm(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-based RNG, Box-Muller KL weights, seed 0)",
             "config": {"workload": f"BASELINE config 4: adaptive MLMC to RMSE {eps}, log-normal KL (sigma 0.5, "
-                                   "l 0.1, 64 modes, 32x32 cells), config-1 geometry", "eps": eps},
+                                   "l 0.1, 64 modes, " + ("per element" if args.field == "element" else "32x32 cells")
+                                   + "), config-1 geometry", "eps": eps},
             "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 16 * sum(lv["n_samples"] for lv in res.levels)},
             "gpu_launches": (wavemc.launch_count() - launches0) // max(1, args.steps), "clocks": clocks.summary(),

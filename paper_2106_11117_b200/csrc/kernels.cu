@@ -2781,7 +2781,7 @@ void launch_sweep_step(const SweepArgs& a, void* stream) {
 
 // cudaFuncSetAttribute applies per device: remember what was set for each
 // (kernel, device) pair, so a process driving several devices configures each
-int set_max_dynamic_smem(const void* kernel, int bytes) {
+int set_max_dynamic_smem(const void* kernel, int bytes, bool max_carveout) {
     static std::mutex mu;
     static std::map<std::pair<const void*, int>, int> done;
     int dev = 0;
@@ -2791,9 +2791,12 @@ int set_max_dynamic_smem(const void* kernel, int bytes) {
     const auto it = done.find(key);
     if (it != done.end()) return it->second;
     const int r = static_cast<int>(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    // the largest shared-memory carveout, so kernels that co-reside two CTAs per
-    // SM by their shared memory (tile / stream steps) get the whole array
-    if (r == 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    // the largest shared-memory carveout for kernels that co-reside several
+    // CTAs per SM by their shared memory (the tiled step).  Not for the others:
+    // an SM configured for them leaves the concurrent levels' sweeps a small
+    // L1 (config-1 estimator 2684 -> 2721 ms when every kernel asked for it)
+    if (r == 0 && max_carveout)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     done[key] = r;
     return r;
 }

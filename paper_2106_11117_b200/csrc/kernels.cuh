@@ -477,7 +477,7 @@ int launch_stream_step(const StreamArgs& a, int grid, void* stream);  // returns
 
 int tile_smem_bytes(const TileArgs& a);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
-int set_max_dynamic_smem(const void* kernel, int bytes);
+int set_max_dynamic_smem(const void* kernel, int bytes, bool max_carveout = false);
 int launch_tile_step(const TileArgs& a, int grid, void* stream);  // returns cudaError_t
 void launch_global_substep(const GSubArgs& a, void* stream);
 void launch_tier_stage(const TierArgs& a, void* stream);

@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
 template <int P>
 int launch_p(const StreamArgs& a, int grid, void* stream) {
     const int smem = stream_smem_bytes(a);
-    const int e = set_max_dynamic_smem(reinterpret_cast<const void*>(stream_step_kernel<P>), smem);
+    const int e = set_max_dynamic_smem(reinterpret_cast<const void*>(stream_step_kernel<P>), smem, true);
     if (e != 0) return e;
     stream_step_kernel<P><<<grid, a.threads, smem, static_cast<cudaStream_t>(stream)>>>(a);
     return static_cast<int>(cudaGetLastError());

@@ -626,7 +626,7 @@ int launch_tile_step(const TileArgs& a, int grid, void* stream) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, tile_step_kernel);  // static shared memory (the TMEM address slot)
     const int e = set_max_dynamic_smem(reinterpret_cast<const void*>(tile_step_kernel),
-                                       optin - static_cast<int>(fa.sharedSizeBytes));
+                                       optin - static_cast<int>(fa.sharedSizeBytes), true);
     if (e != 0) return e;
     tile_step_kernel<<<grid, kT, tile_smem_bytes(a), static_cast<cudaStream_t>(stream)>>>(a);
     return static_cast<int>(cudaGetLastError());

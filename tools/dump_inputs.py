@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--final-time", type=float, default=None)
     ap.add_argument("--lf", action="store_true", help="config 1: the global leap-frog arm (dt = 0.2 h_min)")
     ap.add_argument("--kl", action="store_true", help="config 4: write the log-normal KL table too")
+    ap.add_argument("--kl-element", action="store_true",
+                    help="config 4: the field at the element centroids (the KL mode list instead of the cell table)")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     if a.config == 0:
@@ -56,6 +58,13 @@ def main():
             f.write(f"{table.shape[0]} {table.shape[1]}\n")
             f.write("\n".join(repr(float(v)) for v in table.ravel()) + "\n")
         out["kl"] = {"kl-table": path, "cells-x": kl["cells"][0], "cells-y": kl["cells"][1]}
+        if a.kl_element:
+            modes = wavemc.kl_modes(kl["sigma"], kl["corr_len"], kl["modes"])
+            mpath = os.path.join(a.out, "kl_modes.txt")
+            with open(mpath, "w") as f:
+                f.write(f"{modes.shape[0]}\n")
+                f.write("\n".join(repr(float(v)) for v in modes.ravel()) + "\n")
+            out["kl"] = {"kl-modes": mpath}
     with open(os.path.join(a.out, "inputs.json"), "w") as f:
         json.dump(out, f)
 
