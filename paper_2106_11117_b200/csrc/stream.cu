@@ -266,7 +266,13 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
 template <int P>
 int launch_p(const StreamArgs& a, int grid, void* stream) {
     const int smem = stream_smem_bytes(a);
-    const int e = set_max_dynamic_smem(reinterpret_cast<const void*>(stream_step_kernel<P>), smem, true);
+    // (the device maximum, set once per kernel and device: levels of one
+    // process differ in their column-key array)
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (smem + 64 > optin) return static_cast<int>(cudaErrorInvalidValue);
+    const int e = set_max_dynamic_smem(reinterpret_cast<const void*>(stream_step_kernel<P>), optin - 64, true);
     if (e != 0) return e;
     stream_step_kernel<P><<<grid, a.threads, smem, static_cast<cudaStream_t>(stream)>>>(a);
     return static_cast<int>(cudaGetLastError());

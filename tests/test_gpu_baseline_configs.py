@@ -190,3 +190,27 @@ def test_tiled_step_on_config1_levels(lvl, monkeypatch):
     _, a, _ = wavemc.eval_pairs(tiled, None, 0, lvl, 0, 96)
     _, b, _ = wavemc.eval_pairs(other, None, 0, lvl, 0, 96)
     assert per_sample_rel(a, b) < QOI_RTOL
+
+
+@pytest.mark.parametrize("n_coarse", [128, 256])
+def test_tiled_step_with_streamed_slabs_on_mid_size_boxes(n_coarse, monkeypatch):
+    """Refined boxes of 129^2 / 257^2 nodes at p = 8: thin side bands, square
+    corner tiles and one streamed slab (128- and 256-thread CTAs) against the
+    HBM-resident substeps, with the QoI over the refined square."""
+    d = configs.LevelDef(n_coarse, 8, 0.2 / n_coarse, 8, configs.config1()[0].integrator)
+    mesh = configs.build_mesh(d)
+    spec = wavemc.LevelSpec(dt=d.dt, substeps=d.substeps, final_time=20 * d.dt,
+                            qoi_box=(0.4375, 0.5625, 0.4375, 0.5625), batch=64)
+    plan = wavemc.tile_plan(mesh, spec)
+    assert plan["ok"] and plan["layout"].endswith("+thin+stream") and plan["n_slabs"] >= 1
+    monkeypatch.setenv("WMC_SUBSTEP_PATH", "tiled")
+    tiled = wavemc.Level(mesh, spec)
+    monkeypatch.setenv("WMC_SUBSTEP_PATH", "global")
+    monkeypatch.setenv("WMC_TILED", "0")
+    other = wavemc.Level(mesh, spec)
+    monkeypatch.delenv("WMC_SUBSTEP_PATH")
+    monkeypatch.delenv("WMC_TILED")
+    assert tiled.info["substep_path"] == 5 and other.info["substep_path"] == 3
+    _, a, _ = wavemc.eval_pairs(tiled, None, 0, 0, 7, 70)
+    _, b, _ = wavemc.eval_pairs(other, None, 0, 0, 7, 70)
+    assert per_sample_rel(a, b) < QOI_RTOL

@@ -134,3 +134,48 @@ def test_bias_proxy_known_answers():
     assert wavemc.bias_proxy_sq(0.0, 2.0) == 0.0
     assert wavemc.bias_proxy_sq(3e-5, 2.0) == pytest.approx(1e-10, rel=1e-12)
     assert wavemc.bias_proxy_sq(3e-5, 1.0) == pytest.approx(9.0 * wavemc.bias_proxy_sq(3e-5, 2.0), rel=1e-12)
+
+
+def test_kl_modes_reproduce_the_cell_table():
+    """wmc_kl_modes (the pointwise evaluator's mode list, used on the
+    reference side for the per-element field) against wmc_kl_table."""
+    import numpy as np
+    from paper_2106_11117_b200 import configs, wavemc
+    kl = configs.KL_FIELD
+    table, _ = wavemc.kl_table(8, 8, kl["sigma"], kl["corr_len"], kl["modes"])
+    modes = wavemc.kl_modes(kl["sigma"], kl["corr_len"], kl["modes"])
+
+    def phi(omega, even, norm, t):
+        return (np.cos(omega * t) if even else np.sin(omega * t)) / norm
+
+    for iy in range(8):
+        for ix in range(8):
+            x, y = (ix + 0.5) / 8 - 0.5, (iy + 0.5) / 8 - 0.5
+            row = [m[0] * phi(m[1], m[2], m[3], x) * phi(m[4], m[5], m[6], y) for m in modes]
+            assert np.allclose(row, table[iy * 8 + ix], rtol=1e-13, atol=1e-15)
+
+
+def test_tile_plan_streams_the_interior_of_a_mid_size_box():
+    """Host-only plan of the temporally blocked step on a 257^2-node box at
+    p = 8: thin side bands with corner squares and a streamed interior."""
+    from paper_2106_11117_b200 import configs, wavemc
+    d = configs.LevelDef(256, 8, 0.2 / 256, 8, configs.config1()[0].integrator)
+    mesh = configs.build_mesh(d)
+    spec = wavemc.LevelSpec(dt=d.dt, substeps=d.substeps, final_time=8 * d.dt, batch=64)
+    plan = wavemc.tile_plan(mesh, spec)
+    assert plan["ok"] and plan["layout"] == "frame(24)+thin+stream"
+    assert plan["n_tiles"] == 16 and plan["n_slabs"] == 1 and 0.6 < plan["streamed_frac"] < 0.75
+    no_stream = wavemc.tile_plan(mesh, spec, stream=False)
+    assert no_stream["ok"] and no_stream["n_slabs"] == 0 and no_stream["streamed_frac"] == 0.0
+
+
+def test_per_element_field_level_plan():
+    """One coefficient cell per triangle: no lattice form, same DOF counts."""
+    from paper_2106_11117_b200 import configs, wavemc
+    d = configs.config4()[0]
+    mesh = configs.build_mesh(d)
+    a = wavemc.level_plan(mesh, configs.level_spec(d, kl=True))
+    b = wavemc.level_plan(mesh, configs.level_spec(d, kl="element"))
+    assert a["lattice"] == 1 and b["lattice"] == 0
+    assert (a["n"], a["n_r"], a["n_steps"]) == (b["n"], b["n_r"], b["n_steps"])
+    assert b["nnz"] > a["nnz"]  # an entry per (pair, triangle)
