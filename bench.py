@@ -687,7 +687,17 @@ def roofline_from_profile(levels, counts, prof, step_ms, peaks, fp64):
         elif path == 3:
             add("global_substep", p_["sub_ms"], p_["sub_launches"], sub_b, flops, sub_u)
         elif path == 4:
-            add("tier_stage", p_["sub_ms"], p_["sub_launches"], 0.0, flops, sub_u)
+            # nested tiers: tier k runs p^(k-1) times per step; stage 0 over the rows
+            # outside R_(k+1) (r_k in, E_1 out), stages m >= 1 over all of R_k (r_k and
+            # E_m in, E_(m+1) or r_(k+1) out, E_(m-1) in from m = 2); the last stage of
+            # tier 1 also reads z_n, z_(n-1) and writes z_(n+1) on R_1
+            rk = info["n_r_tier"] + [0]
+            tier_b, runs = 3.0 * rk[0], 1
+            for k in range(info["tiers"]):
+                own = rk[k] - rk[k + 1]
+                tier_b += runs * (2.0 * own + (p - 1) * 3.0 * rk[k] + max(0, p - 2) * own)
+                runs *= p
+            add("tier_stage", p_["sub_ms"], p_["sub_launches"], 8.0 * c * (steps - 1) * tier_b, flops, sub_u)
         elif path in (1, 2):
             add("onchip_substep", p_["sub_ms"], p_["sub_launches"], sub_b, flops, sub_u)
         if p_["upd_ms"]:
