@@ -315,7 +315,10 @@ int fused_tmem() {
 // positions holding the same entry count (slice widths, and every row's
 // arithmetic, unchanged) by a seeded local search that lowers the summed
 // wavefronts.  Rows past a row's count gather column 0 (padding).
-int half_cost(const wmc::LevelTables& t, const std::vector<int>& ord, int h, int width) {
+// perm[q][e]: which entry of generic row q sits in SELL slot e
+using SlotPerm = std::vector<std::vector<int>>;
+
+int half_cost(const wmc::LevelTables& t, const std::vector<int>& ord, int h, int width, const SlotPerm* perm = nullptr) {
     const int n_gen = static_cast<int>(ord.size());
     int cost = 0;
     int cnt[16];
@@ -331,7 +334,12 @@ int half_cost(const wmc::LevelTables& t, const std::vector<int>& ord, int h, int
             if (e < 0)
                 a = t.gen_rows[q];
             else
-                a = e < t.gen_ptr[q + 1] - t.gen_ptr[q] ? t.gen_col[t.gen_ptr[q] + e] : 0;
+                if (perm)  // slot e of the row: an entry, or a hole (weight 0 on column 0)
+                    a = e < static_cast<int>((*perm)[q].size()) && (*perm)[q][e] >= 0
+                            ? t.gen_col[t.gen_ptr[q] + (*perm)[q][e]]
+                            : 0;
+                else
+                    a = e < t.gen_ptr[q + 1] - t.gen_ptr[q] ? t.gen_col[t.gen_ptr[q] + e] : 0;
             const int b = a & 15;
             bool seen = false;
             for (int k = 0; k < cnt[b]; ++k) seen |= addr[b][k] == a;
@@ -345,8 +353,11 @@ int half_cost(const wmc::LevelTables& t, const std::vector<int>& ord, int h, int
     return cost;
 }
 
-void optimize_generic_lanes(const wmc::LevelTables& t, std::vector<int>& ord) {
+void optimize_generic_lanes(const wmc::LevelTables& t, std::vector<int>& ord, SlotPerm& perm) {
     const int n_gen = static_cast<int>(ord.size());
+    perm.assign(n_gen, {});
+    for (int q = 0; q < n_gen; ++q)
+        for (int e = 0; e < t.gen_ptr[q + 1] - t.gen_ptr[q]; ++e) perm[q].push_back(e);
     if (n_gen < 2) return;
     const int n_half = (n_gen + 15) / 16;
     std::vector<int> width(n_half, 0), cost(n_half, 0);
@@ -385,11 +396,41 @@ void optimize_generic_lanes(const wmc::LevelTables& t, std::vector<int>& ord) {
             }
         }
     }
+    long rows_total = 0;
+    for (int c : cost) rows_total += c;
+    // then the order of a row's entries over its slots (a warp gathers slot e
+    // of its 32 rows at once): swaps of two entries of one row that do not
+    // raise the half-warp's wavefront count.  The sum of a row's products is
+    // formed in slot order, so this only changes rounding.
+    for (int p = 0; p < n_gen; ++p) perm[ord[p]].resize(std::max<std::size_t>(perm[ord[p]].size(), width[p / 16]), -1);
+    if (!std::getenv("WMC_GEN_NO_SLOT_PERM")) {
+        for (int h = 0; h < n_half; ++h) {
+            const int rows_h = std::min(16, n_gen - 16 * h);
+            for (long it = 0; it < 6000 && cost[h] > width[h] + 1; ++it) {
+                const int q = ord[16 * h + static_cast<int>(rnd(rows_h))];
+                const int w = static_cast<int>(perm[q].size());  // the slice width: entries and holes
+                if (w < 2) continue;
+                const int e1 = static_cast<int>(rnd(w)), e2 = static_cast<int>(rnd(w));
+                if (e1 == e2) continue;
+                std::swap(perm[q][e1], perm[q][e2]);
+                const int c = half_cost(t, ord, h, width[h], &perm);
+                if (c <= cost[h])
+                    cost[h] = c;
+                else
+                    std::swap(perm[q][e1], perm[q][e2]);
+            }
+        }
+    }
     if (std::getenv("WMC_BANKS_VERBOSE")) {
-        long after_total = 0;
+        long after_total = 0, ideal = 0;
         for (int c : cost) after_total += c;
-        std::fprintf(stderr, "generic lanes: %d rows, half-warp wavefronts per substep %ld -> %ld\n", n_gen,
-                     before_total, after_total);
+        for (int h = 0; h < n_half; ++h) {
+            int w = 0;
+            for (int p = 16 * h; p < std::min(n_gen, 16 * h + 16); ++p) w = std::max(w, w_of(p));
+            ideal += w + 1;
+        }
+        std::fprintf(stderr, "generic lanes: %d rows, half-warp wavefronts per substep %ld -> %ld (rows) -> %ld (slots); "
+                     "conflict-free %ld\n", n_gen, before_total, rows_total, after_total, ideal);
     }
 }
 
@@ -785,7 +826,10 @@ void build_device_level(wmc_level& L) {
             std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
                 return t.gen_ptr[x + 1] - t.gen_ptr[x] > t.gen_ptr[y + 1] - t.gen_ptr[y];
             });
-        if (!fixed_width && !std::getenv("WMC_GEN_NO_BANKS")) optimize_generic_lanes(t, ord);
+        SlotPerm perm(n_gen);
+        for (int q = 0; q < n_gen; ++q)
+            for (int e = 0; e < t.gen_ptr[q + 1] - t.gen_ptr[q]; ++e) perm[q].push_back(e);
+        if (!fixed_width && !std::getenv("WMC_GEN_NO_BANKS")) optimize_generic_lanes(t, ord, perm);
         std::vector<int> grows(n_gen);
         std::vector<double> grs(n_gen);
         for (int q = 0; q < n_gen; ++q) {
@@ -800,7 +844,7 @@ void build_device_level(wmc_level& L) {
             int width = fixed_width ? wmc::kLatGenWidth : 0;
             for (int l = 0; l < 32; ++l) {
                 const int q = sl * 32 + l;
-                if (q < n_gen) width = std::max(width, t.gen_ptr[ord[q] + 1] - t.gen_ptr[ord[q]]);
+                if (q < n_gen) width = std::max(width, static_cast<int>(perm[ord[q]].size()));  // entries and holes
             }
             // slots go in pairs, [slice][pair][lane][2]: a lane's two weights
             // are one 16-byte load and its two columns one 32-bit load
@@ -812,8 +856,8 @@ void build_device_level(wmc_level& L) {
                     std::uint16_t c = 0;
                     double a1 = 0.0;
                     std::uint16_t k1 = 0;
-                    if (q < n_gen && e < t.gen_ptr[ord[q] + 1] - t.gen_ptr[ord[q]]) {
-                        const int ent = t.gen_ptr[ord[q]] + e;
+                    if (q < n_gen && e < static_cast<int>(perm[ord[q]].size()) && perm[ord[q]][e] >= 0) {
+                        const int ent = t.gen_ptr[ord[q]] + perm[ord[q]][e];
                         c = static_cast<std::uint16_t>(t.gen_col[ent]);
                         const int nt = t.gen_rc_ptr[ent + 1] - t.gen_rc_ptr[ent];
                         if (nt == 1) {
