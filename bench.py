@@ -48,8 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--scale", type=float, default=None,
-                    help="fraction of N_l (default 1.0 = the BASELINE counts; config 3: 0.03, a 246-sample slice "
-                         "of the 8192 -- per-sample cost is uniform, the full set is ~10 min per step)")
+                    help="fraction of N_l (default 1.0 = the BASELINE counts; config 3: 1/32, one whole "
+                         "256-sample batch of the 8192 -- the full set is 32 such batches, ~10 min per step)")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4],
                     help="BASELINE config: 1 (default, MLMC), 0 (single-level MC), 2 (graded L-shape MLMC, "
                          "nested 3-tier LTS), 3 (large single level), 4 (adaptive MLMC to an RMSE target, "
@@ -403,7 +403,7 @@ def b200_arm(args, world, rank, local):
     lf = args.integrator == "lf"
     defs, counts_total, label, cpu_T = workload(args.config, args.integrator)
     if args.scale is None:
-        args.scale = 0.03 if args.config == 3 else 1.0
+        args.scale = 0.03125 if args.config == 3 else 1.0
     if args.scale != 1.0:
         label += f" (N_l scaled by {args.scale})"
     counts_total = [max(1, int(round(n * args.scale))) for n in counts_total]
