@@ -92,6 +92,7 @@ struct SweepArgs {
     int wide;            // step sweep form: 10 R + MINB of sweep_wide_kernel (fixed dt, S % 128 == 0), 0: sweep_rows_kernel
     int row_begin;       // step sweeps: rows [row_begin, n) only (the tiled step owns R); 0: all rows
     int sample_major;    // 1: z[s * n + i] (tiled levels: one sample's rows contiguous), 0: z[i * S + s]
+    int sm_groups;       // sample-major sweep: groups of four samples a thread walks through (set by the launch)
 };
 
 struct SubArgs {
