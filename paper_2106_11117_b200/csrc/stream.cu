@@ -157,6 +157,17 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
         // prefetched one iteration ahead and consumed raw at the start of the
         // next one (any arithmetic on the loaded value here would wait for it)
         double znext = row_ok ? __ldg(zs + static_cast<std::size_t>(I0) * W) : 0.0;
+        // running pointers (advanced a column per iteration; recomputing the
+        // addresses from t cost ~35 integer instructions per iteration):
+        // z_n of column t + 1, and z_n / z_{n-1} of the final's column t + 1 - P
+        const std::ptrdiff_t Wd = W;
+        const double* pz = zs + static_cast<std::ptrdiff_t>(I0 + 1) * Wd;
+        const double* pfz = zs + static_cast<std::ptrdiff_t>(I0 + 1 - P) * Wd;
+        double* pzo = zo + static_cast<std::ptrdiff_t>(I0 + 1 - P) * Wd;
+        // L2 prefetch lanes: one request per 128-byte line of the warp's rows,
+        // lanes 0 / 16 for z_n, 8 / 24 for z_{n-1}
+        const bool pf_lane = row_ok && (tid & 7) == 0, pf_zo = (tid & 8) != 0;
+        const std::ptrdiff_t ahead = static_cast<std::ptrdiff_t>(kAhead) * Wd;
         double fz_next = 0.0, fp_next = 0.0;  // z_n, z_{n-1} of the final column
         double wv_cur = 0.0;                  // 2 z_n - z_{n-1} of the final column
         int cur_key = -1;
@@ -176,18 +187,16 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
             wv_cur = 2.0 * fz_next - fp_next;
             {
                 const int xn = t + 1, xf = t + 1 - P;
-                znext = row_ok && xn < NX ? __ldg(zs + static_cast<std::size_t>(I0 + xn) * W) : 0.0;
+                znext = row_ok && xn < NX ? __ldg(pz) : 0.0;
                 if (own_row && xf >= own.x && xf < own.y) {
-                    const std::size_t o = static_cast<std::size_t>(I0 + xf) * W;
-                    fz_next = __ldg(zs + o);
-                    fp_next = zo[o];
+                    fz_next = __ldg(pfz);
+                    fp_next = *pzo;
                 }
                 // the columns kAhead iterations on, into L2 (an iteration is
                 // about as long as a loaded DRAM access)
-                if (row_ok && (tid & 15) == 0) {  // one request per 128-byte line
-                    if (xn + kAhead < NX) l2_prefetch(zs + static_cast<std::size_t>(I0 + xn + kAhead) * W);
-                    if (xf + kAhead >= own.x && xf + kAhead < own.y)
-                        l2_prefetch(zo + static_cast<std::size_t>(I0 + xf + kAhead) * W);
+                if (pf_lane) {
+                    const int xa = (pf_zo ? xf : xn) + kAhead;
+                    if (pf_zo ? (xa >= own.x && xa < own.y) : xa < NX) l2_prefetch((pf_zo ? pzo : pz) + ahead);
                 }
             }
             const double* rd = pub + ((t - 1) & 1) * kPS + 1 + y;  // published in the previous iteration
@@ -225,13 +234,16 @@ __global__ void __launch_bounds__(kT, 2) stream_step_kernel(StreamArgs a) {
                     const int xf = t - P;
                     if (own_row && xf >= own.x && xf < own.y) {
                         const double out = wv_cur + h2 * nx;
-                        zo[static_cast<std::size_t>(I0 + xf) * W] = out;
+                        pzo[-Wd] = out;  // column t - P
                         bad |= !(fabs(out) <= 1e100);
                     }
                 }
             }
 #pragma unroll
             for (int lv = 0; lv < P; ++lv) wr[lv * 2 * kPS] = w[lv][C];
+            pz += Wd;
+            pfz += Wd;
+            pzo += Wd;
             __syncthreads();
         };
         // fast iterations: every level's column in one run of equal cell
