@@ -1028,6 +1028,128 @@ __global__ void __launch_bounds__(kSweepWarps * 32, WMC_TIER_MINB) tier_stage_ke
     }
 }
 
+// Nested-tier stage, wide form (fixed dt, S a multiple of 128): four samples
+// per lane with 256-bit loads and stores like sweep_wide_kernel, the same
+// per-sample products and sums as tier_stage_kernel.
+template <int R, int MINB>
+__global__ void __launch_bounds__(kSweepWarps * 32, MINB) tier_stage_wide_kernel(TierArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nrows = a.row_end - a.row_begin;
+    const int groups = (nrows + kSweepWarps * R - 1) / (kSweepWarps * R);
+    const int first = a.row_begin + (blockIdx.x % groups) * kSweepWarps * R + warp * R;
+    if (first >= a.row_end) return;
+    const int s0 = (blockIdx.x / groups) * kSweepChunkW + 4 * lane;
+    const std::size_t S = static_cast<std::size_t>(a.S);
+    const double* src = a.src;
+    auto at = [&](const double* p, int r) { return p + static_cast<std::size_t>(r) * S + s0; };
+    const D4 zero{0.0, 0.0, 0.0, 0.0};
+    // window E_m[i-1], E_m[i], E_m[i+1] over the warp's consecutive rows
+    D4 vprev = zero, vcur = zero;
+    if (a.m > 0) {
+        if (first > 0) vprev = ld4(at(src, first - 1));
+        vcur = ld4(at(src, first));
+    }
+    int ccell = -1;
+    D4 c = zero;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const int row = first + q;
+        if (row >= a.row_end) break;
+        const std::size_t idx = static_cast<std::size_t>(row) * S + s0;
+        D4 v = ld4_nc(a.rhs + idx);
+        D4 vnext = zero;
+        if (a.m > 0) {
+            if (row + 1 < a.row_end) vnext = ld4(at(src, row + 1));
+            D4 acc = zero;
+            const int4 d = __ldg(a.row_desc + row);
+            if (d.x >= 0 && (d.x >> 24) >= a.k) {
+                const double2 w = __ldg(a.wtype + ((d.x >> 16) & 0xff) - 1);
+                if ((d.x & 0xffff) != ccell) {
+                    ccell = d.x & 0xffff;
+                    c = ld4_nc(a.cells + ccell * S + s0);
+                }
+                const D4 vs = ld4(at(src, row - d.z)), vn = ld4(at(src, row + d.w));
+#define WMC_TIER_STRUCT(F)          \
+    {                               \
+        double p0 = 0.0;            \
+        p0 += w.x * vs.F;           \
+        p0 += w.x * vprev.F;        \
+        p0 += w.y * vcur.F;         \
+        p0 += w.x * vnext.F;        \
+        p0 += w.x * vn.F;           \
+        acc.F = c.F * p0;           \
+    }
+                WMC_TIER_STRUCT(x) WMC_TIER_STRUCT(y) WMC_TIER_STRUCT(z) WMC_TIER_STRUCT(w)
+#undef WMC_TIER_STRUCT
+            } else {
+                const int b = __ldg(a.ptr + row), e = __ldg(a.ptr + row + 1);
+#pragma unroll 2
+                for (int t = b; t < e; ++t) {
+                    const int pk = __ldg(a.ent + t);
+                    const double w = __ldg(a.a0 + t);
+                    const int j = pk & kColMask;
+                    const int cell = static_cast<unsigned>(pk) >> kColBits;
+                    const D4 cc = ld4_nc(a.cells + cell * S + s0);
+                    const D4 x = ld4(at(src, j));
+                    acc.x += (cc.x * w) * x.x;
+                    acc.y += (cc.y * w) * x.y;
+                    acc.z += (cc.z * w) * x.z;
+                    acc.w += (cc.w * w) * x.w;
+                }
+            }
+            v.x += acc.x;
+            v.y += acc.y;
+            v.z += acc.z;
+            v.w += acc.w;
+        }
+        const D4 em_row = vcur;  // E^k_m of this row (m > 0)
+        vprev = vcur;
+        vcur = vnext;
+        if (row < a.split) {
+            st4(a.rhs_next + idx, v);
+            continue;
+        }
+        // the tier's update, then up through the ancestors whose stage ends here
+#pragma unroll
+        for (int t = 0; t < kMaxTiers; ++t) {
+            if (t >= a.depth) break;
+            const auto& L = a.link[t];
+            D4 em = zero, emm = zero;
+            if (t == 0) {
+                em = em_row;
+            } else if (L.em) {
+                em = ld4(L.em + idx);
+            }
+            if (L.emm) emm = ld4(L.emm + idx);
+            D4 en;
+            en.x = L.A * em.x - L.B * emm.x - (L.C * 1.0) * v.x;
+            en.y = L.A * em.y - L.B * emm.y - (L.C * 1.0) * v.y;
+            en.z = L.A * em.z - L.B * emm.z - (L.C * 1.0) * v.z;
+            en.w = L.A * em.w - L.B * emm.w - (L.C * 1.0) * v.w;
+            if (t + 1 < a.depth) {
+                v = D4{L.back * en.x, L.back * en.y, L.back * en.z, L.back * en.w};
+                continue;
+            }
+            if (L.out) {
+                st4(L.out + idx, en);
+            } else {
+                const D4 zn = ld4(a.zc + idx), zm = ld4(a.zp + idx);
+                D4 out;
+                out.x = 2.0 * zn.x - zm.x + 2.0 * en.x;
+                out.y = 2.0 * zn.y - zm.y + 2.0 * en.y;
+                out.z = 2.0 * zn.z - zm.z + 2.0 * en.z;
+                out.w = 2.0 * zn.w - zm.w + 2.0 * en.w;
+                st4(a.zp + idx, out);
+                // check_finite (integrators.cpp:12-18)
+                if (!(fabs(out.x) <= 1e100)) flag_fail(a.fail, s0, a.count, a.step);
+                if (!(fabs(out.y) <= 1e100)) flag_fail(a.fail, s0 + 1, a.count, a.step);
+                if (!(fabs(out.z) <= 1e100)) flag_fail(a.fail, s0 + 2, a.count, a.step);
+                if (!(fabs(out.w) <= 1e100)) flag_fail(a.fail, s0 + 3, a.count, a.step);
+            }
+        }
+    }
+}
+
 // R update: z_{n+1} = 2 z_n - z_{n-1} + 2 d_p on rows < n_r, d_p read
 // sample-major and transposed through shared memory (mirror of the sweep's
 // g store), then one warp per (row, 64 samples) as in the sweep.
@@ -2888,6 +3010,16 @@ void launch_global_substep(const GSubArgs& a, void* stream) {
 void launch_tier_stage(const TierArgs& a, void* stream) {
     const int rows = a.row_end - a.row_begin;
     if (rows <= 0) return;
+    static const bool wide = [] {
+        const char* e = std::getenv("WMC_TIER_WIDE");  // A/B knob (0: the 16-byte form)
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (wide && !a.rel && !a.nsteps && a.S % kSweepChunkW == 0) {
+        constexpr int R = 2;
+        const unsigned grid = ((rows + kSweepWarps * R - 1) / (kSweepWarps * R)) * (a.S / kSweepChunkW);
+        tier_stage_wide_kernel<R, 3><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+        return;
+    }
     const int per = kSweepWarps * kTierRows;
     const unsigned grid = ((rows + per - 1) / per) * (a.S / kSweepChunk);
     tier_stage_kernel<kTierRows><<<grid, kSweepWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
