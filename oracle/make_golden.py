@@ -415,6 +415,9 @@ def config4(ref, tmp, specs=None, model_cost=None):
     el["tight"] = ref.adaptive(specs, CONFIG4_TIGHT_EPS, **elargs)
     el["tight"]["eps"] = CONFIG4_TIGHT_EPS
     el["model_cost"] = model_cost
+    # one coupled pair on each of the five levels (levels 3-4: more than 32 k
+    # triangles, the per-entry cell arrays of the sweep and the substeps)
+    el["pairs_all_levels"] = ref.mlmc(specs, [1, 1, 1, 1, 1], per_sample=True, **elargs)
     dump("config4_element.json", el)
 
 

@@ -406,6 +406,18 @@ def test_config4_element_field_pairs_match_reference(golden):
         assert np.max(np.abs(dq - lv["dq"]) / np.abs(lv["q"])) < 2 * QOI_RTOL, l
 
 
+def test_config4_element_field_pairs_on_all_levels(golden):
+    """One coupled pair per level, levels 3-4 included (41 k / 136 k triangles:
+    cells beside 16-bit columns, and the per-entry cell arrays of the sweep
+    and of the HBM-resident substeps)."""
+    levels = _kl_element_levels(5)
+    for lv in golden("config4_element.json")["pairs_all_levels"]["levels"]:
+        l, n = lv["level"], lv["N"]
+        dq, qf, _ = wavemc.eval_pairs(levels[l], levels[l - 1] if l else None, 0, l, 0, n)
+        assert per_sample_rel(qf, lv["q"]) < QOI_RTOL, l
+        assert np.max(np.abs(dq - lv["dq"]) / np.abs(lv["q"])) < 2 * QOI_RTOL, l
+
+
 @pytest.mark.parametrize("target", ["adaptive", "tight"])
 def test_config4_element_field_adaptive_mlmc_matches_reference(golden, target):
     g0 = golden("config4_element.json")
