@@ -2188,6 +2188,9 @@ __device__ __forceinline__ double gen_full_row_tm(const LatSolveArgs& A, const d
     return gath + rem;
 }
 
+#ifndef WMC_LAT_PIPE
+#define WMC_LAT_PIPE 2
+#endif
 // TM: generic weights / columns and the lattice nodes' d_{m-1} in tensor
 // memory (see tm_ld16); otherwise weights and columns in shared memory and
 // d_{m-1} read back from the buffer the substep overwrites.
@@ -2595,9 +2598,26 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     }
                     double vs = vc[-1];
                     double vk = d[0];
+                    // software-pipelined by kPipe nodes: a node's shared loads are
+                    // issued before the store of the node kPipe before it (the
+                    // compiler cannot see that the two buffers never alias and
+                    // would otherwise chain load -> FP64 -> store node by node)
+                    constexpr int kPipe = WMC_LAT_PIPE;
+                    double ve_[K], vw_[K], vq_[K];
+#pragma unroll
+                    for (int k = 0; k < kPipe && k < K; ++k) {
+                        ve_[k] = vE[k];
+                        vw_[k] = vW[k];
+                        vq_[k] = VT ? 0.0 : (m == 1 ? 0.0 : vx[k]);
+                    }
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
-                        const double ve = vE[k], vw = vW[k];
+                        if (k + kPipe < K) {
+                            ve_[k + kPipe] = vE[k + kPipe];
+                            vw_[k + kPipe] = vW[k + kPipe];
+                            vq_[k + kPipe] = VT ? 0.0 : (m == 1 ? 0.0 : vx[k + kPipe]);
+                        }
+                        const double ve = ve_[k], vw = vw_[k];
                         const double vn = k + 2 < K ? d[k + 1] : k + 2 == K ? (pad_last ? vnl : d[k + 1]) : vnl;
                         // g + A d as two shallow chains (FP64 dependency depth 5, was 6):
                         // (g + dg v_k - kE v_E) - (kW v_W + kNS (v_N + v_S))
@@ -2605,7 +2625,7 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                         const double gb = fma(kW, vw, kNS * (vn + vs));
                         const double vpk =
                             VT ? __hiloint2double(static_cast<int>(vp[2 * k + 1]), static_cast<int>(vp[2 * k]))
-                               : (m == 1 ? 0.0 : vx[k]);
+                               : vq_[k];
                         const double next = fma(-cmh, ga - gb, fma(onepb, d[k], -(beta * vpk)));
                         d[k] = next;
                         if (k < len) vx[k] = next;
