@@ -2557,6 +2557,9 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                 // load, shared gather, FP64 sums), the lattice nodes are FP64
                 // work; half of each scheduler's four warps run the two in the
                 // other order so the phases overlap instead of coinciding
+                // the strip's two end neighbours, loaded ahead of the gather
+                // (level 0: 0.086 -> 0.084 s per 4 096 solves)
+                const double vnl_h = sd[cur + base + span], vs_h = sd[cur + base - 1];
                 if (!lat_first) gather();
                 // TMEM: v_m of the thread's nodes parked for substep m + 1,
                 // v_{m-1} back from the other set
@@ -2589,14 +2592,14 @@ __global__ void __launch_bounds__(T, 1) lattice_solve_kernel(LatSolveArgs A) {
                     double* vx = sd + nxt + base;
                     const double* vE = vc + W;
                     const double* vW = vc - W;
-                    const double vnl = vc[span];
+                    const double vnl = vnl_h;
                     const bool pad_last = span == K - 1;  // the common short strip: v_N read in the loop
                     if (!PK && span < K - 1) {
 #pragma unroll
                         for (int k = 0; k < K - 1; ++k)
                             if (k == span) d[k] = vnl;
                     }
-                    double vs = vc[-1];
+                    double vs = vs_h;
                     double vk = d[0];
                     // software-pipelined by kPipe nodes: a node's shared loads are
                     // issued before the store of the node kPipe before it (the
