@@ -160,3 +160,15 @@ def test_config2_instability_reported(coracle):
                                           0, 4)
     assert rc == 3
     assert e.value.sample == fi and e.value.step == fs
+
+
+def test_config2_wide_tier_stages_match_the_16_byte_form(c2):
+    """Batches that are a multiple of 128 samples take tier_stage_wide_kernel
+    (four samples per lane, 256-bit loads); the same samples in 64-sample
+    batches take the 16-byte form.  Same per-sample products and sums."""
+    defs, meshes, levels, _ = c2
+    d = defs[2]
+    small = wavemc.Level(meshes[2], configs.level_spec(d, batch=64))
+    _, wide, _ = wavemc.eval_pairs(levels[2], None, 3, 2, 0, 256)
+    _, narrow, _ = wavemc.eval_pairs(small, None, 3, 2, 0, 256)
+    assert np.max(np.abs(wide - narrow) / np.abs(narrow)) < 1e-12
