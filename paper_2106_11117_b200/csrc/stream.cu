@@ -18,7 +18,13 @@
 // a template argument, so the window never moves); a level's value for the
 // row neighbours goes through shared memory, double-buffered by the iteration
 // parity: one barrier per iteration for all p levels.  g waits p iterations
-// for its last use in a per-thread ring in tensor memory.
+// for its last use in a per-thread ring in tensor memory (stored twice, so
+// one 16-column load reads an iteration's eight values).  The CTA size is the
+// slabs' row count rounded to four warps (planned per level: 128 threads and
+// four CTAs per SM for config 3); a launch may cut a slab's columns into
+// chunks (work items of even length over the grid's rounds).  Global
+// addresses are running pointers, z_n / z_{n-1} arrive a column ahead in
+// registers (consumed raw an iteration later) and six columns ahead in L2.
 //
 // The region is the owned band grown by p rows / columns; positions near its
 // edge see zeros for missing neighbours, an error that moves one column or
