@@ -31,7 +31,8 @@ struct TilePlan {
     //   colpos(c) * kTileHs + r + 1, colpos(c) = c even ? c/2 + 1 : Wz/2 + 2 + c/2
     // (even and odd columns apart, guard columns 0, Wz/2 + 1, Wz + 2; guard
     // rows 0 and Hz + 1), generic rows outside the box at kTileBoxSlots + k
-    // shapes: 0 wide (wz columns x hz rows), 1 tall (hz columns x wz rows)
+    // shapes: 0 wide (wz columns x hz rows), 1 tall (hz columns x wz rows),
+    // 2 square (sqrt(wz hz) each way: the box corners of the thin-frame layout)
     int wz = 0, hz = 0, k = 0;
     int hs = 0;          // column stride of the wide shape (odd); the tall one uses (wz + 2) | 1
     int jres = 0;        // region row origins are = jres (mod k)
@@ -43,7 +44,7 @@ struct TilePlan {
     int max_ent = 0;     // generic SELL entries per tile
     int n_tiles = 0;
     // per tile
-    std::vector<int> tiles_shape;       // 0 wide, 1 tall
+    std::vector<int> tiles_shape;       // 0 wide, 1 tall, 2 square
     std::vector<int> i0, j0;            // region origin (box coordinates, may be < 0)
     std::vector<int> oi0, oi1, oj0, oj1;  // owned rectangle [oi0, oi1) x [oj0, oj1) (box coordinates)
     std::vector<int> gen_off;           // generic rows of tile t: [gen_off[t], gen_off[t+1])
